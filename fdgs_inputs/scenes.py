@@ -42,7 +42,7 @@ class SceneArrays:
         return int(self.mean.shape[0])
 
     def subset(self, idx) -> "SceneArrays":
-        idx = np.asarray(idx)
+        idx = np.asarray(idx, dtype=np.int64)
         return SceneArrays(*(np.ascontiguousarray(getattr(self, f)[idx]) for f in _FIELDS))
 
     def arrays(self):

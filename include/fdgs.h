@@ -1,0 +1,208 @@
+/*
+ * fdgs.h -- C ABI of libfdgs.so, the B200 (sm_100a) render hot path of
+ * 4DGS-1K (arXiv 2503.16422).
+ *
+ * Citations: P:n = PAPER.md line n (the paper's LaTeX source), with its
+ * section / equation.  DESIGN.md lists every reading taken where the paper is
+ * silent (R1..R20) and the pinned decision path.
+ *
+ * Conventions for every entry point
+ *   - All pointers named d_* / documented "device" are CUDA device pointers;
+ *     "host" pointers are ordinary host memory.  The caller owns every buffer.
+ *     The library never allocates or frees memory; scratch lives in a
+ *     caller-provided workspace whose size the *_workspace_bytes functions
+ *     return (256-byte aligned base required).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     All work is stream-ordered; functions documented "async" never
+ *     synchronise the host.
+ *   - Every function returns fdgs_status.  No C++ exception crosses the ABI;
+ *     nothing aborts.  fdgs_last_error() returns a thread-local message for the
+ *     last non-OK status of the calling thread.
+ *   - Layouts are PyTorch-contiguous float32 / uint32 arrays.
+ *   - Re-entrant: there is no global mutable state besides the thread-local
+ *     error string; concurrent calls on different workspaces are safe.
+ */
+#ifndef FDGS_H
+#define FDGS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FDGS_ABI_VERSION 1
+#define FDGS_TILE 16            /* 16x16-pixel tiles (reading R7) */
+#define FDGS_MAX_TILES 16384    /* tile-grid limit of the binning kernel    */
+
+typedef enum {
+    FDGS_OK = 0,
+    FDGS_ERR_INVALID_ARG = 1,       /* bad pointer / size / camera              */
+    FDGS_ERR_INVALID_SCENE = 2,     /* scene violates the invariants below      */
+    FDGS_ERR_WORKSPACE_TOO_SMALL = 3,
+    FDGS_ERR_OVERFLOW = 4,          /* tile entries exceeded max_entries        */
+    FDGS_ERR_CUDA = 5,              /* a CUDA runtime call failed               */
+    FDGS_ERR_UNSUPPORTED = 6        /* valid request this build does not serve  */
+} fdgs_status;
+
+/* A set of N 4D Gaussians (Sec. 3): mean mu=(x,y,z,t), scales
+ * S_4D, rotation R_4D = L(q_l) R(q_r) from a left and a right quaternion,
+ * opacity sigma, degree-3 SH colour c_i(d).  All DEVICE pointers,
+ * 16-byte aligned, SoA:
+ *   mean, scale, rot_l, rot_r : float[n][4]  (rot in (w,x,y,z) order; scales
+ *                               are linear standard deviations > 0, R12)
+ *   opacity                   : float[n], sigma in (0,1]
+ *   log255_opacity            : float[n], L_i = fp32(ln(255 sigma_i)) computed
+ *                               in binary64 (fdgs_log255_opacity fills it)
+ *   sh                        : float[n][16][3], coefficient k*3+channel
+ * Invariants (checked by fdgs_scene_validate): |‖q‖-1| <= 1e-6, scales > 0,
+ * sigma in (0,1], Sigma_44 > 1e-12. */
+typedef struct {
+    int32_t n;
+    const float *mean;
+    const float *scale;
+    const float *rot_l;
+    const float *rot_r;
+    const float *opacity;
+    const float *log255_opacity;
+    const float *sh;
+} fdgs_scene;
+
+/* Pinhole view "I" of P:126 (HOST struct).  world->camera rotation R
+ * (row-major) and translation T, OpenCV axes (x right, y down, z forward),
+ * pixel (i,j) has centre (i+0.5, j+0.5), u = fx*x/z + cx (reading R13).
+ * Valid iff 1 <= width,height <= 8192, fx,fy > 0, z_near > 0 and
+ * ‖R R^T - I‖_inf <= 1e-5.  bg is the background of the composite (R14). */
+typedef struct {
+    int32_t width, height;
+    float fx, fy, cx, cy;
+    float R[9];
+    float T[3];
+    float z_near;
+    float bg[3];
+} fdgs_camera;
+
+/* Per-frame counters written on the DEVICE by fdgs_render (after the blend). */
+typedef struct {
+    uint32_t n_act;        /* Gaussians in the active set A = M_l | M_r           */
+    uint32_t n_vis;        /* active Gaussians surviving all culls                */
+    uint32_t n_entries;    /* (tile, Gaussian) entries E                          */
+    uint32_t status;       /* fdgs_status of the frame (OVERFLOW when E > cap)    */
+    uint64_t n_evaluated;  /* (pixel, Gaussian) pairs inside the pixel AABB tested
+                              before the pixel terminated (Eq. 2 work)            */
+    uint64_t n_blended;    /* pairs composited (alpha >= 1/255, not terminated)   */
+} fdgs_frame_stats;
+
+const char *fdgs_status_string(fdgs_status s);
+const char *fdgs_last_error(void);
+int32_t fdgs_abi_version(void);
+
+/* Scene checks of SPEC invariants (degenerate Sigma_t guard).
+ * Synchronises `stream`.  *first_bad (host, nullable) receives the lowest
+ * offending index or -1.  Returns FDGS_ERR_INVALID_SCENE if any. */
+fdgs_status fdgs_scene_validate(const fdgs_scene *scene, int64_t *first_bad, void *d_ws, size_t ws_bytes,
+                                void *stream);
+size_t fdgs_scene_validate_workspace_bytes(void);
+
+/* L_i = fp32(ln(255 * sigma_i)) evaluated in binary64 (async). d_out: float[n]. */
+fdgs_status fdgs_log255_opacity(const float *d_opacity, int32_t n, float *d_out, void *stream);
+
+/* Workspace bytes of fdgs_render for n Gaussians, a width x height image and
+ * room for max_entries (tile, Gaussian) entries. */
+size_t fdgs_render_workspace_bytes(int32_t n, int32_t width, int32_t height, int64_t max_entries);
+
+/* Render one frame at timestamp t (Eq. 1-3) under the key-frame
+ * temporal filter (Sec. 4.2.2).  ASYNC, no host synchronisation.
+ *   d_mask_l, d_mask_r : DEVICE uint32[ceil(n/32)] masks M(t_l), M(t_r) of the
+ *                        two bracketing key-frames, bit i of word i/32 is
+ *                        Gaussian i (LSB-first).  The active set is their OR;
+ *                        pass the same pointer twice (or d_mask_r = NULL) at a
+ *                        key-frame; both NULL = every Gaussian active.
+ *   cam                : HOST camera.
+ *   t                  : timestamp (may lie outside [0,1]).
+ *   d_out_rgb          : DEVICE float[3][height][width] (CHW), C + T*bg.
+ *   d_out_T            : DEVICE float[height][width] final transmittance, nullable.
+ *   d_stats            : DEVICE fdgs_frame_stats, nullable.
+ * Steps: mask OR + cull-first slice (Eq. 1/3) + EWA
+ * projection + SH3 colour + order-preserving compaction; stable radix sort of
+ * depth keys; stable tile binning; per-tile front-to-back blend (Eq. 2).
+ * Device-detected errors (E > max_entries) set d_stats->status; the frame is
+ * then undefined and must be re-rendered with a larger workspace.
+ * Errors returned: INVALID_ARG (null scene/output, bad camera, n < 0),
+ * WORKSPACE_TOO_SMALL, UNSUPPORTED (tile grid > FDGS_MAX_TILES), CUDA. */
+fdgs_status fdgs_render(const fdgs_scene *scene, const uint32_t *d_mask_l, const uint32_t *d_mask_r,
+                        const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T, void *d_ws,
+                        size_t ws_bytes, int64_t max_entries, fdgs_frame_stats *d_stats, void *stream);
+
+/* fdgs_render that also records 5 caller-created CUDA events (host array of
+ * cudaEvent_t, passed as void*) on `stream` at the stage boundaries:
+ * [0] start, [1] after preprocess (rows 1-4), [2] after the depth sort
+ * (row 5a), [3] after tile binning (row 5b), [4] after the blend (row 6).
+ * ASYNC; for live per-stage timing (bench.py). */
+fdgs_status fdgs_render_timed(const fdgs_scene *scene, const uint32_t *d_mask_l, const uint32_t *d_mask_r,
+                              const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T, void *d_ws,
+                              size_t ws_bytes, int64_t max_entries, fdgs_frame_stats *d_stats, void *stream,
+                              void *const *stage_events);
+
+/* Same as fdgs_render, then synchronises `stream` and returns the frame status
+ * (FDGS_ERR_OVERFLOW if E > max_entries).  host_stats (nullable) receives the
+ * counters.  For tests and the end-to-end path. */
+fdgs_status fdgs_render_checked(const fdgs_scene *scene, const uint32_t *d_mask_l, const uint32_t *d_mask_r,
+                                const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T, void *d_ws,
+                                size_t ws_bytes, int64_t max_entries, fdgs_frame_stats *host_stats,
+                                void *stream);
+
+/* Device views into a render workspace after fdgs_render (tests/debug only).
+ * Arrays are indexed by the visible slot v < n_vis (ascending Gaussian index):
+ *   rec0 float4 {u, v, A', B'}, rec1 float4 {C', Q2, aabb_x, aabb_y}
+ *   (aabb_x = px0 | px1 << 16 as int bits), rec2 float4 {r, g, b, gid bits},
+ *   depth uint32 (fp32 bits of camera z), order uint32[n_vis] (visible slots
+ *   in canonical (depth, index) order), tile_start uint32[n_tiles + 1],
+ *   entries uint32[E] (visible slots, per tile in canonical order). */
+typedef struct {
+    const void *rec0, *rec1, *rec2;
+    const uint32_t *depth;
+    const uint32_t *order;
+    const uint32_t *tile_start;
+    const uint32_t *entries;
+    const uint32_t *counters; /* [0]=n_act [1]=n_vis [2]=E [3]=status */
+    int32_t n_tiles;
+} fdgs_debug_views;
+fdgs_status fdgs_render_debug_views(void *d_ws, size_t ws_bytes, int32_t n, int32_t width, int32_t height,
+                                    int64_t max_entries, fdgs_debug_views *out);
+
+/* Key-frame visibility mask (Sec. 4.2.2): bit i of d_out_mask is set
+ * iff Gaussian i is visible at t_key from at least one of the n_cams HOST
+ * cameras, "visible" = temporal & support & near & cover culls of the render
+ * decision path (reading R3), so the stored mask is the union over views
+ * {U_j m_{i,j}}.  ASYNC.  d_out_mask: DEVICE uint32[ceil(n/32)]. */
+size_t fdgs_keyframe_workspace_bytes(int32_t n_cams);
+fdgs_status fdgs_keyframe_mask(const fdgs_scene *scene, const fdgs_camera *cams, int32_t n_cams, float t_key,
+                               uint32_t *d_out_mask, void *d_ws, size_t ws_bytes, void *stream);
+
+/* d_out = d_a | d_b over ceil(n/32) words (P:285 active set).  ASYNC. */
+fdgs_status fdgs_mask_or(const uint32_t *d_a, const uint32_t *d_b, int32_t n, uint32_t *d_out, void *stream);
+
+/* Active-set compaction: ascending indices of the set bits
+ * of (d_a | d_b) (d_b nullable) into d_out_idx (DEVICE int32[n]) and their
+ * count into *d_count (DEVICE uint32).  Warp ballot + block scan + decoupled
+ * look-back.  ASYNC. */
+size_t fdgs_mask_compact_workspace_bytes(int32_t n);
+fdgs_status fdgs_mask_compact(const uint32_t *d_a, const uint32_t *d_b, int32_t n, int32_t *d_out_idx,
+                              uint32_t *d_count, void *d_ws, size_t ws_bytes, void *stream);
+
+/* Spatial-temporal variation score (Sec. 4.2.1).  Not built in this
+ * round: returns FDGS_ERR_UNSUPPORTED. */
+typedef struct {
+    float volume_percentile;   /* gamma clip percentile (0.9)          */
+    int32_t combine_mode;      /* 0 = time-aligned sum_t S^T S^S        */
+} fdgs_stv_opts;
+fdgs_status fdgs_stv_score(const fdgs_scene *scene, const fdgs_camera *cams, int32_t n_cams, const float *ts,
+                           int32_t n_ts, const fdgs_stv_opts *opts, float *d_out_score, void *d_ws,
+                           size_t ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDGS_H */

@@ -1,0 +1,244 @@
+"""Python binding of libfdgs.so: same names as include/fdgs.h, marshalling only.
+
+Every step of the render path runs in the CUDA kernels of libfdgs.so;
+PyTorch only provides device memory and streams.  There is no CPU fallback:
+if the library or a CUDA device is missing these functions raise.
+
+Host logic that the paper states and that is not a per-pixel/per-Gaussian
+computation lives here: the key-frame schedule and bracketing of
+Sec. 4.2.2 (readings R4/R5).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import FdgsCamera, FdgsDebugViews, FdgsFrameStats, FdgsScene, check, lib
+
+_FIELDS = ("mean", "scale", "rot_l", "rot_r", "opacity", "log255_opacity", "sh")
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+class Scene:
+    """Device-resident 4D Gaussians (fdgs_scene)."""
+
+    def __init__(self, tensors: dict, device=None):
+        dev = torch.device(device or "cuda")
+        self.t = {}
+        for f in _FIELDS:
+            x = tensors[f]
+            if isinstance(x, np.ndarray):
+                x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+            self.t[f] = x.to(device=dev, dtype=torch.float32).contiguous()
+        self.n = int(self.t["mean"].shape[0])
+        self.device = dev
+        self.struct = FdgsScene(self.n, *[self.t[f].data_ptr() for f in _FIELDS])
+
+    @classmethod
+    def from_arrays(cls, arrays, device=None):
+        return cls({f: getattr(arrays, f) for f in _FIELDS}, device)
+
+    def nbytes(self) -> int:
+        return sum(v.numel() * 4 for v in self.t.values())
+
+
+def camera_struct(cam) -> FdgsCamera:
+    c = FdgsCamera()
+    c.width, c.height = int(cam.width), int(cam.height)
+    c.fx, c.fy, c.cx, c.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
+    c.R[:] = [float(x) for x in np.asarray(cam.R, np.float32).reshape(9)]
+    c.T[:] = [float(x) for x in np.asarray(cam.T, np.float32).reshape(3)]
+    c.z_near = float(cam.z_near)
+    c.bg[:] = [float(b) for b in cam.bg]
+    return c
+
+
+def default_max_entries(n: int) -> int:
+    return int(min(2 ** 32 - 1, max(1 << 20, 64 * max(n, 1))))
+
+
+def mask_words(n: int) -> int:
+    return (n + 31) // 32
+
+
+@dataclass
+class FrameStats:
+    n_act: int
+    n_vis: int
+    n_entries: int
+    status: int
+    n_evaluated: int = 0
+    n_blended: int = 0
+
+
+class Renderer:
+    """fdgs_render with a caller-owned workspace sized for (n, width, height)."""
+
+    def __init__(self, scene: Scene, width: int, height: int, max_entries: int | None = None):
+        self.scene = scene
+        self.width, self.height = int(width), int(height)
+        self.max_entries = int(default_max_entries(scene.n) if max_entries is None else max_entries)
+        self._alloc()
+
+    def _alloc(self):
+        nbytes = lib().fdgs_render_workspace_bytes(self.scene.n, self.width, self.height, self.max_entries)
+        if nbytes == 0:
+            raise ValueError("invalid render size")
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.scene.device)
+        self.ws_bytes = nbytes
+
+    def _masks(self, mask_l, mask_r):
+        for m in (mask_l, mask_r):
+            if m is not None:
+                if m.dtype != torch.int32 or m.numel() != mask_words(self.scene.n) or not m.is_cuda:
+                    raise ValueError(f"mask must be a cuda int32 tensor of {mask_words(self.scene.n)} words")
+        return _ptr(mask_l), _ptr(mask_r)
+
+    def new_output(self):
+        return torch.empty((3, self.height, self.width), dtype=torch.float32, device=self.scene.device)
+
+    def render(self, cam, t, mask_l=None, mask_r=None, out=None, out_T=None, stats=None, stream=None,
+               stage_events=None):
+        """Async render (no host sync).  Returns the CHW float32 output tensor.
+        stage_events: optional 5 torch.cuda.Event recorded at the stage boundaries."""
+        if cam.width != self.width or cam.height != self.height:
+            raise ValueError("camera size differs from the renderer's")
+        out = self.new_output() if out is None else out
+        ml, mr = self._masks(mask_l, mask_r)
+        cs = camera_struct(cam) if not isinstance(cam, FdgsCamera) else cam
+        if stage_events is None:
+            check(lib().fdgs_render(C.byref(self.scene.struct), ml, mr, C.byref(cs), float(t), _ptr(out),
+                                    _ptr(out_T), _ptr(self.ws), self.ws_bytes, self.max_entries, _ptr(stats),
+                                    _stream_ptr(stream)))
+        else:
+            evs = (C.c_void_p * 5)(*[e.cuda_event for e in stage_events])
+            check(lib().fdgs_render_timed(C.byref(self.scene.struct), ml, mr, C.byref(cs), float(t), _ptr(out),
+                                          _ptr(out_T), _ptr(self.ws), self.ws_bytes, self.max_entries, _ptr(stats),
+                                          _stream_ptr(stream), evs))
+        return out
+
+    def render_checked(self, cam, t, mask_l=None, mask_r=None, out=None, out_T=None, stream=None,
+                       grow: bool = True):
+        """Synchronous render; grows the entry capacity and retries on overflow."""
+        out = self.new_output() if out is None else out
+        ml, mr = self._masks(mask_l, mask_r)
+        cs = camera_struct(cam)
+        while True:
+            hs = FdgsFrameStats()
+            st = lib().fdgs_render_checked(C.byref(self.scene.struct), ml, mr, C.byref(cs), float(t), _ptr(out),
+                                           _ptr(out_T), _ptr(self.ws), self.ws_bytes, self.max_entries,
+                                           C.byref(hs), _stream_ptr(stream))
+            if st == _lib.FDGS_ERR_OVERFLOW and grow:
+                self.max_entries = int(min(2 ** 32 - 1, max(2 * self.max_entries, hs.n_entries + 1)))
+                self._alloc()
+                continue
+            check(st)
+            return out, FrameStats(hs.n_act, hs.n_vis, hs.n_entries, hs.status, hs.n_evaluated, hs.n_blended)
+
+    def debug_views(self) -> dict:
+        """Device views (torch tensors into the workspace) after a render."""
+        v = FdgsDebugViews()
+        check(lib().fdgs_render_debug_views(_ptr(self.ws), self.ws_bytes, self.scene.n, self.width, self.height,
+                                            self.max_entries, C.byref(v)))
+        base = self.ws.data_ptr()
+        cnt = self._slice(v.counters, base, 16).view(torch.int32)
+        n_act, n_vis, E, status = [int(x) for x in cnt.cpu()]
+        n = self.scene.n
+
+        def arr(ptr, count, itemsize, dtype):
+            return self._slice(ptr, base, count * itemsize).view(dtype)
+
+        return dict(
+            n_act=n_act, n_vis=n_vis, n_entries=E, status=status,
+            rec0=arr(v.rec0, n, 16, torch.float32).view(n, 4)[:n_vis],
+            rec1=arr(v.rec1, n, 16, torch.float32).view(n, 4)[:n_vis],
+            rec2=arr(v.rec2, n, 16, torch.float32).view(n, 4)[:n_vis],
+            depth=arr(v.depth, n, 4, torch.int32)[:n_vis],
+            order=arr(v.order, n, 4, torch.int32)[:n_vis],
+            tile_start=arr(v.tile_start, v.n_tiles + 1, 4, torch.int32),
+            entries=arr(v.entries, max(E, 1), 4, torch.int32)[:E],
+            n_tiles=v.n_tiles,
+        )
+
+    def _slice(self, ptr, base, nbytes):
+        off = int(ptr) - base
+        return self.ws[off:off + nbytes]
+
+
+# ----------------------------------------------------------- other entries
+def validate(scene: Scene, stream=None):
+    ws = torch.empty(lib().fdgs_scene_validate_workspace_bytes(), dtype=torch.uint8, device=scene.device)
+    bad = C.c_int64(-1)
+    st = lib().fdgs_scene_validate(C.byref(scene.struct), C.byref(bad), _ptr(ws), ws.numel(), _stream_ptr(stream))
+    return st, bad.value
+
+
+def log255_opacity(opacity: torch.Tensor, stream=None) -> torch.Tensor:
+    out = torch.empty_like(opacity)
+    check(lib().fdgs_log255_opacity(_ptr(opacity), opacity.numel(), _ptr(out), _stream_ptr(stream)))
+    return out
+
+
+def keyframe_mask(scene: Scene, cams, t_key: float, out=None, stream=None) -> torch.Tensor:
+    """M(t_key) = OR over cams of the visibility decision."""
+    out = torch.empty(mask_words(scene.n), dtype=torch.int32, device=scene.device) if out is None else out
+    arr = (FdgsCamera * len(cams))(*[camera_struct(c) for c in cams])
+    nb = lib().fdgs_keyframe_workspace_bytes(len(cams))
+    ws = torch.empty(nb, dtype=torch.uint8, device=scene.device)
+    check(lib().fdgs_keyframe_mask(C.byref(scene.struct), arr, len(cams), float(t_key), _ptr(out), _ptr(ws), nb,
+                                   _stream_ptr(stream)))
+    return out  # ws goes back to torch's stream-ordered cache: safe to reuse after the kernel
+
+
+def mask_or(a: torch.Tensor, b: torch.Tensor, n: int, out=None, stream=None) -> torch.Tensor:
+    out = torch.empty_like(a) if out is None else out
+    check(lib().fdgs_mask_or(_ptr(a), _ptr(b), int(n), _ptr(out), _stream_ptr(stream)))
+    return out
+
+
+def mask_compact(a: torch.Tensor, n: int, b: torch.Tensor | None = None, stream=None):
+    """Ascending indices of the set bits of a|b."""
+    idx = torch.empty(max(n, 1), dtype=torch.int32, device=a.device)
+    cnt = torch.zeros(1, dtype=torch.int32, device=a.device)
+    nb = lib().fdgs_mask_compact_workspace_bytes(int(n))
+    ws = torch.empty(nb, dtype=torch.uint8, device=a.device)
+    check(lib().fdgs_mask_compact(_ptr(a), _ptr(b), int(n), _ptr(idx), _ptr(cnt), _ptr(ws), nb, _stream_ptr(stream)))
+    k = int(cnt.item())
+    return idx[:k]
+
+
+def stv_score(*args, **kwargs):
+    check(lib().fdgs_stv_score(None, None, 0, None, 0, None, None, None, 0, None))
+
+
+# ------------------------------------------------ Sec. 4.2.2 host logic
+def keyframes(frames: int, interval: int) -> list:
+    """Key-frame indices at an even interval, last frame appended (R5)."""
+    if not (1 <= interval <= max(frames, 1)):
+        raise ValueError("interval must be in [1, frames]")
+    kf = list(range(0, frames, interval))
+    if kf[-1] != frames - 1:
+        kf.append(frames - 1)
+    return kf
+
+
+def bracket(kf: list, frame: int):
+    """Indices (l, r) of the two bracketing key-frames t_l <= t <= t_r (R4)."""
+    lo = [k for k, f in enumerate(kf) if f <= frame]
+    hi = [k for k, f in enumerate(kf) if f >= frame]
+    left = lo[-1] if lo else 0
+    right = hi[0] if hi else len(kf) - 1
+    return left, right

@@ -1,0 +1,338 @@
+// api.cu -- the extern "C" boundary of libfdgs.so (include/fdgs.h).
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "fdgs_internal.h"
+
+namespace fdgs {
+cudaError_t render_set_smem_attrs();
+
+static thread_local char g_err[512] = "";
+
+static fdgs_status fail(fdgs_status s, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+static fdgs_status cuda_fail(cudaError_t e, const char *where) {
+    return fail(FDGS_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static int sm_count() {
+    static int cached = 0;
+    if (cached == 0) {
+        int dev = 0, c = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && c > 0)
+            cached = c;
+        else
+            cached = 148;
+    }
+    return cached;
+}
+
+RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max_entries) {
+    RenderLayout L{};
+    L.n = n;
+    L.width = width;
+    L.height = height;
+    L.tiles_x = (width + FDGS_TILE - 1) / FDGS_TILE;
+    L.tiles_y = (height + FDGS_TILE - 1) / FDGS_TILE;
+    L.n_tiles = L.tiles_x * L.tiles_y;
+    L.n_parts = (n + kPreBlock - 1) / kPreBlock;
+    L.p_sort = sm_count();
+    // u16 per-warp counters in the binning scatter need <= 65535 ranks per block
+    L.p_bin = std::max(sm_count(), (int)((n + 32767) / 32768));
+    L.bin_warps = L.n_tiles <= 8192 ? 8 : 4;
+    L.max_entries = max_entries;
+    const size_t nn = (size_t)std::max(n, 1);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = align256(off + bytes);
+        return o;
+    };
+    L.counters = take(sizeof(Counters));
+    L.lookback = take(sizeof(uint32_t) * (size_t)std::max(L.n_parts, 1));
+    L.rec0 = take(16 * nn);
+    L.rec1 = take(16 * nn);
+    L.rec2 = take(16 * nn);
+    L.depth = take(4 * nn);
+    L.keys0 = take(4 * nn);
+    L.keys1 = take(4 * nn);
+    L.vals0 = take(4 * nn);
+    L.vals1 = take(4 * nn);
+    L.sort_hist = take(sizeof(uint32_t) * 4 * 256 * (size_t)L.p_sort);
+    L.bin_hist = take(sizeof(uint32_t) * (size_t)L.p_bin * L.n_tiles);
+    L.tile_total = take(sizeof(uint32_t) * (size_t)L.n_tiles);
+    L.tile_start = take(sizeof(uint32_t) * ((size_t)L.n_tiles + 1));
+    L.entries = take(sizeof(uint32_t) * (size_t)std::max<int64_t>(max_entries, 1));
+    L.total = off;
+    return L;
+}
+
+bool make_camdev(const fdgs_camera &c, CamDev &o, const char **why) {
+    if (c.width < 1 || c.height < 1 || c.width > 8192 || c.height > 8192) { *why = "image size outside [1,8192]"; return false; }
+    if (!(c.fx > 0.f) || !(c.fy > 0.f)) { *why = "fx, fy must be > 0"; return false; }
+    if (!(c.z_near > 0.f)) { *why = "z_near must be > 0"; return false; }
+    for (int k = 0; k < 9; ++k)
+        if (!std::isfinite(c.R[k])) { *why = "non-finite R"; return false; }
+    for (int k = 0; k < 3; ++k)
+        if (!std::isfinite(c.T[k]) || !std::isfinite(c.bg[k])) { *why = "non-finite T/bg"; return false; }
+    double worst = 0.0;
+    for (int r = 0; r < 3; ++r)
+        for (int s = 0; s < 3; ++s) {
+            double acc = 0.0;
+            for (int k = 0; k < 3; ++k) acc += (double)c.R[3 * r + k] * (double)c.R[3 * s + k];
+            worst = std::max(worst, std::fabs(acc - (r == s ? 1.0 : 0.0)));
+        }
+    if (worst > 1e-5) { *why = "R is not a rotation (|R R^T - I| > 1e-5)"; return false; }
+    for (int k = 0; k < 9; ++k) o.R[k] = (double)c.R[k];
+    for (int k = 0; k < 3; ++k) o.T[k] = (double)c.T[k];
+    o.fx = c.fx;
+    o.fy = c.fy;
+    o.cx = c.cx;
+    o.cy = c.cy;
+    // pinned: 1.3 * (W / (2 fx)) in binary64 (DESIGN.md decision path)
+    volatile double two_fx = 2.0 * o.fx, two_fy = 2.0 * o.fy;
+    volatile double tx = (double)c.width / two_fx, ty = (double)c.height / two_fy;
+    o.limx = kJClamp * tx;
+    o.limy = kJClamp * ty;
+    o.z_near = (double)c.z_near;
+    for (int k = 0; k < 3; ++k) {
+        // camera centre C = -R^T T (value path only: SH view direction)
+        const double ck = -((double)c.R[k] * c.T[0] + (double)c.R[3 + k] * c.T[1] + (double)c.R[6 + k] * c.T[2]);
+        o.campos[k] = (float)ck;
+        o.bg[k] = c.bg[k];
+    }
+    o.width = c.width;
+    o.height = c.height;
+    return true;
+}
+
+SceneDev make_scenedev(const fdgs_scene &s) {
+    SceneDev d;
+    d.n = s.n;
+    d.mean = reinterpret_cast<const float4 *>(s.mean);
+    d.scale = reinterpret_cast<const float4 *>(s.scale);
+    d.rot_l = reinterpret_cast<const float4 *>(s.rot_l);
+    d.rot_r = reinterpret_cast<const float4 *>(s.rot_r);
+    d.opacity = s.opacity;
+    d.L = s.log255_opacity;
+    d.sh = reinterpret_cast<const float4 *>(s.sh);
+    return d;
+}
+
+static fdgs_status check_scene(const fdgs_scene *s) {
+    if (s == nullptr) return fail(FDGS_ERR_INVALID_ARG, "scene is NULL");
+    if (s->n < 0) return fail(FDGS_ERR_INVALID_ARG, "scene->n < 0");
+    if (s->n == 0) return FDGS_OK;
+    const void *p[] = {s->mean, s->scale, s->rot_l, s->rot_r, s->opacity, s->log255_opacity, s->sh};
+    for (const void *q : p)
+        if (q == nullptr) return fail(FDGS_ERR_INVALID_ARG, "scene array is NULL");
+    const void *a16[] = {s->mean, s->scale, s->rot_l, s->rot_r, s->sh};
+    for (const void *q : a16)
+        if ((uintptr_t)q % 16 != 0) return fail(FDGS_ERR_INVALID_ARG, "scene float4 arrays must be 16-byte aligned");
+    return FDGS_OK;
+}
+
+static std::once_flag g_attr_once;
+static cudaError_t g_attr_err = cudaSuccess;
+
+}  // namespace fdgs
+
+using namespace fdgs;
+
+extern "C" {
+
+const char *fdgs_status_string(fdgs_status s) {
+    switch (s) {
+        case FDGS_OK: return "ok";
+        case FDGS_ERR_INVALID_ARG: return "invalid argument";
+        case FDGS_ERR_INVALID_SCENE: return "invalid scene";
+        case FDGS_ERR_WORKSPACE_TOO_SMALL: return "workspace too small";
+        case FDGS_ERR_OVERFLOW: return "tile-entry capacity exceeded";
+        case FDGS_ERR_CUDA: return "CUDA error";
+        case FDGS_ERR_UNSUPPORTED: return "unsupported";
+    }
+    return "unknown status";
+}
+
+const char *fdgs_last_error(void) { return g_err; }
+int32_t fdgs_abi_version(void) { return FDGS_ABI_VERSION; }
+
+size_t fdgs_scene_validate_workspace_bytes(void) { return 256; }
+
+fdgs_status fdgs_scene_validate(const fdgs_scene *scene, int64_t *first_bad, void *d_ws, size_t ws_bytes,
+                                void *stream) {
+    if (first_bad) *first_bad = -1;
+    fdgs_status s = check_scene(scene);
+    if (s != FDGS_OK) return s;
+    if (d_ws == nullptr || ws_bytes < 256) return fail(FDGS_ERR_WORKSPACE_TOO_SMALL, "validate needs 256 bytes");
+    cudaStream_t st = (cudaStream_t)stream;
+    auto *d_bad = reinterpret_cast<unsigned long long *>(d_ws);
+    cudaError_t e = cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long), st);
+    if (e == cudaSuccess) e = launch_validate(make_scenedev(*scene), d_bad, st);
+    unsigned long long h = ~0ull;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d_bad, sizeof h, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "fdgs_scene_validate");
+    if (h != ~0ull) {
+        if (first_bad) *first_bad = (int64_t)h;
+        return fail(FDGS_ERR_INVALID_SCENE, "Gaussian %llu violates the scene invariants", h);
+    }
+    return FDGS_OK;
+}
+
+fdgs_status fdgs_log255_opacity(const float *d_opacity, int32_t n, float *d_out, void *stream) {
+    if (n < 0 || (n > 0 && (d_opacity == nullptr || d_out == nullptr))) return fail(FDGS_ERR_INVALID_ARG, "bad args");
+    cudaError_t e = launch_log255(d_opacity, n, d_out, (cudaStream_t)stream);
+    return e == cudaSuccess ? FDGS_OK : cuda_fail(e, "fdgs_log255_opacity");
+}
+
+size_t fdgs_render_workspace_bytes(int32_t n, int32_t width, int32_t height, int64_t max_entries) {
+    if (n < 0 || width < 1 || height < 1 || max_entries < 0) return 0;
+    return render_layout(n, width, height, max_entries).total;
+}
+
+fdgs_status fdgs_render_timed(const fdgs_scene *scene, const uint32_t *d_mask_l, const uint32_t *d_mask_r,
+                              const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T, void *d_ws,
+                              size_t ws_bytes, int64_t max_entries, fdgs_frame_stats *d_stats, void *stream,
+                              void *const *stage_events) {
+    fdgs_status s = check_scene(scene);
+    if (s != FDGS_OK) return s;
+    if (cam == nullptr || d_out_rgb == nullptr) return fail(FDGS_ERR_INVALID_ARG, "camera / output is NULL");
+    if (!std::isfinite(t)) return fail(FDGS_ERR_INVALID_ARG, "t is not finite");
+    if (max_entries < 0 || max_entries > 0xffffffffll) return fail(FDGS_ERR_INVALID_ARG, "max_entries out of range");
+    CamDev cd;
+    const char *why = nullptr;
+    if (!make_camdev(*cam, cd, &why)) return fail(FDGS_ERR_INVALID_ARG, "camera: %s", why);
+    const RenderLayout L = render_layout(scene->n, cam->width, cam->height, max_entries);
+    if (L.n_tiles > FDGS_MAX_TILES) return fail(FDGS_ERR_UNSUPPORTED, "tile grid %d > %d", L.n_tiles, FDGS_MAX_TILES);
+    if (d_ws == nullptr || ws_bytes < L.total || (uintptr_t)d_ws % 256 != 0)
+        return fail(FDGS_ERR_WORKSPACE_TOO_SMALL, "workspace needs %zu bytes (256-aligned), got %zu", L.total, ws_bytes);
+    if (d_mask_l == nullptr && d_mask_r != nullptr) d_mask_l = d_mask_r, d_mask_r = nullptr;
+    std::call_once(g_attr_once, [] { g_attr_err = render_set_smem_attrs(); });
+    if (g_attr_err != cudaSuccess) return cuda_fail(g_attr_err, "cudaFuncSetAttribute");
+    cudaError_t e = launch_render(make_scenedev(*scene), d_mask_l, d_mask_r, cd, t, d_out_rgb, d_out_T,
+                                  reinterpret_cast<char *>(d_ws), L, d_stats, (cudaStream_t)stream,
+                                  reinterpret_cast<cudaEvent_t const *>(stage_events));
+    return e == cudaSuccess ? FDGS_OK : cuda_fail(e, "fdgs_render");
+}
+
+fdgs_status fdgs_render(const fdgs_scene *scene, const uint32_t *d_mask_l, const uint32_t *d_mask_r,
+                        const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T, void *d_ws,
+                        size_t ws_bytes, int64_t max_entries, fdgs_frame_stats *d_stats, void *stream) {
+    return fdgs_render_timed(scene, d_mask_l, d_mask_r, cam, t, d_out_rgb, d_out_T, d_ws, ws_bytes, max_entries,
+                             d_stats, stream, nullptr);
+}
+
+fdgs_status fdgs_render_checked(const fdgs_scene *scene, const uint32_t *d_mask_l, const uint32_t *d_mask_r,
+                                const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T, void *d_ws,
+                                size_t ws_bytes, int64_t max_entries, fdgs_frame_stats *host_stats,
+                                void *stream) {
+    fdgs_status s = fdgs_render(scene, d_mask_l, d_mask_r, cam, t, d_out_rgb, d_out_T, d_ws, ws_bytes, max_entries,
+                                nullptr, stream);
+    if (s != FDGS_OK) return s;
+    const RenderLayout L = render_layout(scene->n, cam->width, cam->height, max_entries);
+    Counters c;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemcpyAsync(&c, reinterpret_cast<char *>(d_ws) + L.counters, sizeof c, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "fdgs_render_checked");
+    const uint32_t h[4] = {c.n_act, c.n_vis, c.n_entries, c.status};
+    if (host_stats) {
+        host_stats->n_act = h[0];
+        host_stats->n_vis = h[1];
+        host_stats->n_entries = h[2];
+        host_stats->status = h[3];
+        host_stats->n_evaluated = c.n_eval;
+        host_stats->n_blended = c.n_blend;
+    }
+    if (h[3] != FDGS_OK)
+        return fail((fdgs_status)h[3], "frame status %u: %u entries > capacity %lld", h[3], h[2], (long long)max_entries);
+    return FDGS_OK;
+}
+
+fdgs_status fdgs_render_debug_views(void *d_ws, size_t ws_bytes, int32_t n, int32_t width, int32_t height,
+                                    int64_t max_entries, fdgs_debug_views *out) {
+    if (d_ws == nullptr || out == nullptr) return fail(FDGS_ERR_INVALID_ARG, "NULL");
+    const RenderLayout L = render_layout(n, width, height, max_entries);
+    if (ws_bytes < L.total) return fail(FDGS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
+    char *w = reinterpret_cast<char *>(d_ws);
+    out->rec0 = w + L.rec0;
+    out->rec1 = w + L.rec1;
+    out->rec2 = w + L.rec2;
+    out->depth = reinterpret_cast<const uint32_t *>(w + L.depth);
+    out->order = reinterpret_cast<const uint32_t *>(w + L.vals1);
+    out->tile_start = reinterpret_cast<const uint32_t *>(w + L.tile_start);
+    out->entries = reinterpret_cast<const uint32_t *>(w + L.entries);
+    out->counters = reinterpret_cast<const uint32_t *>(w + L.counters);
+    out->n_tiles = L.n_tiles;
+    return FDGS_OK;
+}
+
+size_t fdgs_keyframe_workspace_bytes(int32_t n_cams) {
+    return n_cams <= 0 ? 256 : align256(sizeof(CamDev) * (size_t)n_cams);
+}
+
+fdgs_status fdgs_keyframe_mask(const fdgs_scene *scene, const fdgs_camera *cams, int32_t n_cams, float t_key,
+                               uint32_t *d_out_mask, void *d_ws, size_t ws_bytes, void *stream) {
+    fdgs_status s = check_scene(scene);
+    if (s != FDGS_OK) return s;
+    if (cams == nullptr || n_cams <= 0 || n_cams > 1024 || d_out_mask == nullptr)
+        return fail(FDGS_ERR_INVALID_ARG, "cameras / output");
+    if (!std::isfinite(t_key)) return fail(FDGS_ERR_INVALID_ARG, "t_key is not finite");
+    if (d_ws == nullptr || ws_bytes < fdgs_keyframe_workspace_bytes(n_cams))
+        return fail(FDGS_ERR_WORKSPACE_TOO_SMALL, "keyframe workspace");
+    std::vector<CamDev> h(n_cams);
+    for (int c = 0; c < n_cams; ++c) {
+        const char *why = nullptr;
+        if (!make_camdev(cams[c], h[c], &why)) return fail(FDGS_ERR_INVALID_ARG, "camera %d: %s", c, why);
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    // pageable source: cudaMemcpyAsync returns once `h` has been staged
+    cudaError_t e = cudaMemcpyAsync(d_ws, h.data(), sizeof(CamDev) * n_cams, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = launch_keyframe(make_scenedev(*scene), reinterpret_cast<CamDev *>(d_ws), n_cams, t_key,
+                                              d_out_mask, st);
+    return e == cudaSuccess ? FDGS_OK : cuda_fail(e, "fdgs_keyframe_mask");
+}
+
+fdgs_status fdgs_mask_or(const uint32_t *d_a, const uint32_t *d_b, int32_t n, uint32_t *d_out, void *stream) {
+    if (n < 0 || (n > 0 && (d_a == nullptr || d_b == nullptr || d_out == nullptr)))
+        return fail(FDGS_ERR_INVALID_ARG, "bad args");
+    cudaError_t e = launch_mask_or(d_a, d_b, n, d_out, (cudaStream_t)stream);
+    return e == cudaSuccess ? FDGS_OK : cuda_fail(e, "fdgs_mask_or");
+}
+
+size_t fdgs_mask_compact_workspace_bytes(int32_t n) {
+    return align256(sizeof(uint32_t) * (32 + (size_t)(std::max(n, 0) + 255) / 256));
+}
+
+fdgs_status fdgs_mask_compact(const uint32_t *d_a, const uint32_t *d_b, int32_t n, int32_t *d_out_idx,
+                              uint32_t *d_count, void *d_ws, size_t ws_bytes, void *stream) {
+    if (n < 0 || (n > 0 && (d_a == nullptr || d_out_idx == nullptr)) || d_count == nullptr)
+        return fail(FDGS_ERR_INVALID_ARG, "bad args");
+    if (d_ws == nullptr || ws_bytes < fdgs_mask_compact_workspace_bytes(n))
+        return fail(FDGS_ERR_WORKSPACE_TOO_SMALL, "compact workspace");
+    cudaError_t e = launch_mask_compact(d_a, d_b, n, d_out_idx, d_count, reinterpret_cast<uint32_t *>(d_ws),
+                                        (cudaStream_t)stream);
+    return e == cudaSuccess ? FDGS_OK : cuda_fail(e, "fdgs_mask_compact");
+}
+
+fdgs_status fdgs_stv_score(const fdgs_scene *, const fdgs_camera *, int32_t, const float *, int32_t,
+                           const fdgs_stv_opts *, float *, void *, size_t, void *) {
+    return fail(FDGS_ERR_UNSUPPORTED, "fdgs_stv_score is not built yet (SURVEY NEXT-f1)");
+}
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+// fdgs_internal.h -- host-side launchers shared by the .cu files of libfdgs.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/fdgs.h"
+#include "fdgs_device.cuh"
+
+namespace fdgs {
+
+constexpr int kPreBlock = 256;         // Gaussians per preprocess partition
+constexpr uint32_t kFlagA = 1u << 30;  // look-back: aggregate available
+constexpr uint32_t kFlagP = 2u << 30;  // look-back: inclusive prefix available
+constexpr uint32_t kValMask = (1u << 30) - 1;
+
+// Counter block at the head of the render workspace (zeroed per frame).
+struct Counters {
+    uint32_t n_act, n_vis, n_entries, status;  // mirrors fdgs_frame_stats
+    uint32_t part_ticket;
+    uint32_t sort_ticket[4];
+    uint32_t bin_ticket;
+    uint32_t blend_ticket;
+    uint32_t pad[5];
+    unsigned long long n_eval;   // (pixel, Gaussian) pairs tested before termination
+    unsigned long long n_blend;  // pairs composited
+    uint32_t pad2[12];
+};
+static_assert(sizeof(Counters) == 128, "Counters layout");
+
+struct SceneDev {
+    int32_t n;
+    const float4 *mean, *scale, *rot_l, *rot_r;
+    const float *opacity, *L;
+    const float4 *sh;  // [n][12] float4 = 48 floats
+};
+
+// Workspace layout of fdgs_render (all offsets 256-byte aligned).
+struct RenderLayout {
+    int32_t n, width, height, tiles_x, tiles_y, n_tiles;
+    int32_t n_parts;   // preprocess partitions
+    int32_t p_sort;    // sort partitions
+    int32_t p_bin;     // binning partitions
+    int32_t bin_warps; // warps per binning block
+    int64_t max_entries;
+    size_t counters, lookback, rec0, rec1, rec2, depth, keys0, keys1, vals0, vals1, sort_hist, bin_hist,
+        tile_total, tile_start, entries, total;
+};
+RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max_entries);
+
+bool make_camdev(const fdgs_camera &c, CamDev &out, const char **why);
+SceneDev make_scenedev(const fdgs_scene &s);
+
+// launchers (return cudaGetLastError())
+cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint32_t *mask_r, const CamDev &cam,
+                          float t, float *out_rgb, float *out_T, char *ws, const RenderLayout &L,
+                          fdgs_frame_stats *stats, cudaStream_t st, cudaEvent_t const *stage_events);
+cudaError_t launch_keyframe(const SceneDev &sc, const CamDev *d_cams, int n_cams, float t, uint32_t *out,
+                            cudaStream_t st);
+cudaError_t launch_mask_or(const uint32_t *a, const uint32_t *b, int n, uint32_t *out, cudaStream_t st);
+cudaError_t launch_mask_compact(const uint32_t *a, const uint32_t *b, int n, int32_t *idx, uint32_t *count,
+                                uint32_t *ws_ticket_and_status, cudaStream_t st);
+cudaError_t launch_validate(const SceneDev &sc, unsigned long long *d_first_bad, cudaStream_t st);
+cudaError_t launch_log255(const float *op, int n, float *out, cudaStream_t st);
+
+}  // namespace fdgs

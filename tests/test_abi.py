@@ -1,0 +1,77 @@
+"""The C-ABI library builds, loads and exports every symbol include/fdgs.h
+declares; argument checks that need no GPU (-m "not gpu")."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "fdgs.h")
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(fdgs_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2503_16422_b200 import build
+    build.build_lib()
+    from paper_2503_16422_b200 import _lib
+    return _lib.lib()
+
+
+def test_every_declared_symbol_is_exported(lib):
+    from paper_2503_16422_b200 import _lib
+    declared = _declared()
+    assert len(declared) >= 15
+    assert sorted(_lib.EXPORTS) == declared
+    so = os.path.join(ROOT, "paper_2503_16422_b200", "libfdgs.so")
+    out = subprocess.run(["nm", "-D", "--defined-only", so], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (fdgs_[a-z0-9_]+)$", out, flags=re.M))
+    assert set(declared) <= exported
+    for name in declared:
+        assert getattr(lib, name) is not None
+
+
+def test_library_is_sm100a(lib):
+    so = os.path.join(ROOT, "paper_2503_16422_b200", "libfdgs.so")
+    out = subprocess.run(["cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_status_strings_and_version(lib):
+    assert lib.fdgs_abi_version() == 1
+    assert lib.fdgs_status_string(0) == b"ok"
+    assert lib.fdgs_status_string(4) == b"tile-entry capacity exceeded"
+
+
+def test_host_side_argument_errors_without_gpu(lib):
+    from paper_2503_16422_b200 import _lib
+    cam = _lib.FdgsCamera()
+    cam.width = cam.height = 64
+    cam.fx = cam.fy = 64.0
+    # NULL scene -> INVALID_ARG before any CUDA call
+    st = lib.fdgs_render(None, None, None, C.byref(cam), 0.0, None, None, None, 0, 0, None, None)
+    assert st == _lib.FDGS_ERR_INVALID_ARG
+    assert b"scene" in lib.fdgs_last_error()
+    sc = _lib.FdgsScene()
+    sc.n = 0
+    # bad camera (R = 0 is not a rotation)
+    out = C.c_float()
+    st = lib.fdgs_render(C.byref(sc), None, None, C.byref(cam), 0.0, C.byref(out), None, None, 0, 0, None, None)
+    assert st == _lib.FDGS_ERR_INVALID_ARG and b"camera" in lib.fdgs_last_error()
+    # stv score is declared but not built this round
+    assert lib.fdgs_stv_score(None, None, 0, None, 0, None, None, None, 0, None) == _lib.FDGS_ERR_UNSUPPORTED
+
+
+def test_workspace_sizes(lib):
+    a = lib.fdgs_render_workspace_bytes(200_000, 1352, 1014, 12_800_000)
+    b = lib.fdgs_render_workspace_bytes(200_000, 1352, 1014, 25_600_000)
+    assert a > 200_000 * 48 and b - a >= 4 * 12_800_000
+    assert lib.fdgs_render_workspace_bytes(-1, 10, 10, 0) == 0
+    assert lib.fdgs_mask_compact_workspace_bytes(1000) >= 4 * (32 + 4)

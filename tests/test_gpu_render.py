@@ -1,0 +1,257 @@
+"""GPU parity of the CUDA render path (through the C-ABI) against the oracle.
+
+Bars (BASELINE.json north_star): masks, decision records and tile lists
+bit-exact; RGB max-abs <= 2e-4 and mean-abs <= 1e-5 against the oracle's
+nearest admissible termination branch.  Sizes span several tiles with ragged
+edges; full-size configs are checked on the launch configuration bench.py
+times (sampled pixels).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import fdgs_inputs as fi
+import oracle
+import paper_2503_16422_b200 as fd
+from paper_2503_16422_b200 import _lib
+
+from parity import assert_records_bit_exact, assert_rgb_parity, assert_tile_lists_bit_exact, mask_bits
+
+pytestmark = pytest.mark.gpu
+
+
+def _np_mask(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def _render(scene_arr, cam, t, mask_l=None, mask_r=None, max_entries=None):
+    sc = fd.Scene.from_arrays(scene_arr)
+    r = fd.Renderer(sc, cam.width, cam.height, max_entries=max_entries)
+    T = torch.empty((cam.height, cam.width), dtype=torch.float32, device="cuda")
+    out, stats = r.render_checked(cam, t, mask_l, mask_r, out_T=T)
+    return out.cpu().numpy(), T.cpu().numpy(), stats, r
+
+
+# ------------------------------------------------------------------ C1 tiny
+@pytest.mark.parametrize("t", [0.0, 1 / 3, 2 / 3, 1.0])
+def test_c1_full_frame_parity(t):
+    scene = fi.make_scene("c1")
+    cam = fi.make_cameras("c1")[0]
+    t = float(np.float32(t))
+    img, T, stats, r = _render(scene, cam, t)
+    views = r.debug_views()
+    assert_records_bit_exact(views, scene, cam, t)
+    assert_tile_lists_bit_exact(views, scene, cam, t)
+    orc = oracle.render(scene, cam, t)
+    assert_rgb_parity(img, orc)
+    assert np.abs(T.reshape(-1) - orc["T"]).max() < 2e-4
+    assert stats.n_act == scene.n and stats.n_vis == orc["stats"]["n_vis"]
+
+
+# ------------------------------------------------------- reduced configs
+SMALL = {
+    # name: (n, width, height, fx, cameras, frames, interval)
+    "c2": (20_000, 200, 200, 1111.0 / 4, 6, 150, 10),
+    "c3": (20_000, 338, 254, 250.0, 5, 300, 20),
+    "c4": (60_000, 338, 254, 250.0, 5, 300, 20),
+}
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_reduced_config_masked_parity(name):
+    n, W, H, f, ncam, F, D = SMALL[name]
+    scene = fi.make_scene(name, n=n)
+    cams = fi.make_cameras(name, width=W, height=H, fx=f, count=ncam)
+    times = fi.frame_times(F)
+    kf = fd.keyframes(F, D)
+    frame = kf[3] + D // 2                      # mid-window
+    l, r = fd.bracket(kf, frame)
+    sc = fd.Scene.from_arrays(scene)
+    ml = fd.keyframe_mask(sc, cams, float(times[kf[l]]))
+    mr = fd.keyframe_mask(sc, cams, float(times[kf[r]]))
+    torch.cuda.synchronize()
+    for m, k in ((ml, kf[l]), (mr, kf[r])):
+        assert np.array_equal(_np_mask(m), oracle.keyframe_mask(scene, cams, times[k]))
+    active = _np_mask(ml) | _np_mask(mr)
+    cam = cams[ncam // 2]
+    t = float(times[frame])
+    img, T, stats, rd = _render(scene, cam, t, ml, mr)
+    views = rd.debug_views()
+    assert stats.n_act == int(mask_bits(active, n).sum())
+    assert_records_bit_exact(views, scene, cam, t, active)
+    assert_tile_lists_bit_exact(views, scene, cam, t, active)
+    orc = oracle.render(scene, cam, t, mask=active)
+    mx, mean, used = assert_rgb_parity(img, orc)
+    assert stats.n_vis == orc["stats"]["n_vis"] > 100
+
+
+# --------------------------------------------------- full-size C3 (bench)
+def test_c3_full_size_sampled_parity():
+    scene = fi.make_scene("c3")
+    cams = fi.make_cameras("c3")
+    times = fi.frame_times(300)
+    kf = fd.keyframes(300, 20)
+    frame = 150
+    l, r = fd.bracket(kf, frame)
+    sc = fd.Scene.from_arrays(scene)
+    ml = fd.keyframe_mask(sc, cams, float(times[kf[l]]))
+    mr = fd.keyframe_mask(sc, cams, float(times[kf[r]]))
+    torch.cuda.synchronize()
+    assert np.array_equal(_np_mask(ml), oracle.keyframe_mask(scene, cams, times[kf[l]]))
+    assert np.array_equal(_np_mask(mr), oracle.keyframe_mask(scene, cams, times[kf[r]]))
+    active = _np_mask(ml) | _np_mask(mr)
+    cam = cams[7]
+    t = float(times[frame])
+    img, T, stats, rd = _render(scene, cam, t, ml, mr)
+    views = rd.debug_views()
+    assert_records_bit_exact(views, scene, cam, t, active)
+    assert_tile_lists_bit_exact(views, scene, cam, t, active)
+    rng = np.random.default_rng(0)
+    pix = np.unique(rng.integers(0, cam.width * cam.height, 4000))
+    orc = oracle.render(scene, cam, t, mask=active, pixels=pix)
+    assert_rgb_parity(img, orc, pixels=pix)
+
+
+def test_c4_full_size_sampled_parity_unmasked():
+    scene = fi.make_scene("c4")
+    cam = fi.make_cameras("c4")[3]
+    t = float(fi.frame_times(300)[77])
+    img, T, stats, rd = _render(scene, cam, t)
+    views = rd.debug_views()
+    assert_records_bit_exact(views, scene, cam, t)
+    assert_tile_lists_bit_exact(views, scene, cam, t)
+    rng = np.random.default_rng(1)
+    pix = np.unique(rng.integers(0, cam.width * cam.height, 1500))
+    orc = oracle.render(scene, cam, t, pixels=pix)
+    assert_rgb_parity(img, orc, pixels=pix)
+
+
+# ------------------------------------------------------------ invariants
+def test_all_ones_mask_equals_unmasked_and_determinism():
+    n, W, H, f = 30_000, 300, 200, 220.0
+    scene = fi.make_scene("c3", n=n)
+    cam = fi.make_cameras("c3", width=W, height=H, fx=f, count=3)[1]
+    ones = torch.full((fd.mask_words(n),), -1, dtype=torch.int32, device="cuda")
+    a, _, _, _ = _render(scene, cam, 0.4)
+    b, _, _, _ = _render(scene, cam, 0.4, ones)
+    c, _, _, _ = _render(scene, cam, 0.4, ones, ones)
+    d, _, _, _ = _render(scene, cam, 0.4)
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+    assert np.array_equal(a, d)                      # bit-identical reruns
+
+
+def test_keyframe_soundness_on_gpu():
+    n, W, H, f = 30_000, 300, 200, 220.0
+    scene = fi.make_scene("c3", n=n)
+    cams = fi.make_cameras("c3", width=W, height=H, fx=f, count=4)
+    sc = fd.Scene.from_arrays(scene)
+    tk = float(np.float32(20 / 299))
+    m = fd.keyframe_mask(sc, cams, tk)
+    for cam in cams:
+        a, _, _, _ = _render(scene, cam, tk)
+        b, _, _, _ = _render(scene, cam, tk, m)
+        assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------ edge cases
+def test_empty_scene_and_all_zero_mask_give_background():
+    cam = fi.make_cameras("c1")[0]
+    cam.bg = (0.1, 0.2, 0.3)
+    empty = fi.make_scene("c1", n=1).subset([])
+    img, T, stats, _ = _render(empty, cam, 0.5)
+    assert np.all(img == np.array(cam.bg, np.float32)[:, None, None]) and np.all(T == 1)
+    scene = fi.make_scene("c1")
+    zero = torch.zeros(fd.mask_words(scene.n), dtype=torch.int32, device="cuda")
+    img, T, stats, _ = _render(scene, cam, 0.5, zero)
+    assert stats.n_act == 0 and stats.n_vis == 0
+    assert np.all(img == np.array(cam.bg, np.float32)[:, None, None])
+
+
+@pytest.mark.parametrize("W,H", [(1, 1), (17, 33), (16, 16), (250, 7)])
+def test_ragged_and_tiny_images(W, H):
+    scene = fi.make_scene("c1", n=800, seed=9)
+    cam = fi.make_cameras("c1", width=W, height=H, fx=64.0 * max(W, H) / 64)[0]
+    img, T, stats, rd = _render(scene, cam, 0.5)
+    views = rd.debug_views()
+    assert_records_bit_exact(views, scene, cam, 0.5)
+    assert_tile_lists_bit_exact(views, scene, cam, 0.5)
+    assert_rgb_parity(img, oracle.render(scene, cam, 0.5))
+
+
+def test_single_gaussian_closed_form_on_gpu():
+    """North-star pin, on the GPU: one on-axis isotropic Gaussian."""
+    cam = fi.scenes._cam(65, 65, 64.0, np.eye(3), np.zeros(3), np.zeros(3), bg=(0.1, 0.2, 0.3))
+    cam.cx = cam.cy = 32.5
+    sc = fi.isotropic_scene([[0, 0, 4.0, 0.5]], [[0.2, 0.2, 0.2, 0.3]], [0.9], colors=[0.8, 0.4, 0.1])
+    img, T, _, _ = _render(sc, cam, 0.5)
+    j, i = np.mgrid[0:65, 0:65]
+    s = float(sc.scale[0, 0])
+    sp2 = (64.0 * s / 4.0) ** 2 + 0.3
+    a_un = float(sc.opacity[0]) * np.exp(-((i + 0.5 - 32.5) ** 2 + (j + 0.5 - 32.5) ** 2) / (2 * sp2))
+    alpha = np.where(a_un >= 1 / 255, np.minimum(0.99, a_un), 0.0)
+    c = 0.28209479177387814 * sc.sh[0, 0].astype(np.float64) + 0.5
+    bg = np.array(cam.bg, np.float32).astype(np.float64)
+    expect = c[:, None, None] * alpha[None] + (1 - alpha[None]) * bg[:, None, None]
+    sure = np.abs(a_un * 255 - 1) > 1e-4
+    assert np.abs(img - expect)[:, sure].max() < 2e-4
+
+
+def test_overflow_is_reported_and_recovered():
+    scene = fi.make_scene("c1")
+    cam = fi.make_cameras("c1")[0]
+    sc = fd.Scene.from_arrays(scene)
+    r = fd.Renderer(sc, cam.width, cam.height, max_entries=8)
+    with pytest.raises(fd.FdgsError) as ei:
+        r.render_checked(cam, 0.5, grow=False)
+    assert ei.value.status == _lib.FDGS_ERR_OVERFLOW
+    out, stats = r.render_checked(cam, 0.5)          # grows and re-renders
+    assert stats.status == 0 and r.max_entries >= stats.n_entries
+    assert_rgb_parity(out.cpu().numpy(), oracle.render(scene, cam, 0.5))
+
+
+def test_validate_and_log255():
+    scene = fi.make_scene("c3", n=50_000)
+    sc = fd.Scene.from_arrays(scene)
+    st, bad = fd.validate(sc)
+    assert st == 0 and bad == -1
+    L = fd.log255_opacity(sc.t["opacity"])
+    assert np.array_equal(L.cpu().numpy().view(np.uint32), scene.log255_opacity.view(np.uint32))
+    broken = fi.make_scene("c3", n=1000)
+    broken.rot_l[17] *= 1.01
+    broken.scale[400, 2] = 0.0
+    st, bad = fd.validate(fd.Scene.from_arrays(broken))
+    assert st == _lib.FDGS_ERR_INVALID_SCENE and bad == 17
+
+
+def test_mask_or_and_compact_bit_exact():
+    rng = np.random.default_rng(3)
+    for n in (1, 31, 32, 33, 1000, 200_003):
+        nw = (n + 31) // 32
+        a = rng.integers(0, 2 ** 32, nw, dtype=np.uint64).astype(np.uint32)
+        b = rng.integers(0, 2 ** 32, nw, dtype=np.uint64).astype(np.uint32)
+        if n % 32:
+            a[-1] &= (1 << (n % 32)) - 1
+            b[-1] &= (1 << (n % 32)) - 1
+        ta = torch.from_numpy(a.view(np.int32)).cuda()
+        tb = torch.from_numpy(b.view(np.int32)).cuda()
+        o = fd.mask_or(ta, tb, n)
+        assert np.array_equal(_np_mask(o), a | b)
+        idx = fd.mask_compact(ta, n, tb).cpu().numpy()
+        want = np.nonzero(mask_bits(a | b, n))[0]
+        assert np.array_equal(idx, want)
+        idx = fd.mask_compact(ta, n).cpu().numpy()
+        assert np.array_equal(idx, np.nonzero(mask_bits(a, n))[0])
+
+
+def test_extrapolated_time_and_bad_camera():
+    scene = fi.make_scene("c1")
+    cam = fi.make_cameras("c1")[0]
+    img, _, stats, _ = _render(scene, cam, 1.7)        # outside [0,1]: allowed
+    assert_rgb_parity(img, oracle.render(scene, cam, float(np.float32(1.7))))
+    bad = fi.make_cameras("c1")[0]
+    bad.R = np.eye(3, dtype=np.float32) * 2
+    sc = fd.Scene.from_arrays(scene)
+    with pytest.raises(fd.FdgsError):
+        fd.Renderer(sc, 64, 64).render(bad, 0.5)
