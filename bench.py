@@ -1,0 +1,441 @@
+#!/usr/bin/env python
+"""Frames/s of the 4DGS-1K render hot path on B200 (BASELINE.json metric).
+
+Workload (configs[2]): the N3V-shaped 200k-Gaussian scene,
+1352x1014, 20 cameras x 300 timestamps = 6000 frames, key-frame interval 20,
+every frame rendered with the union mask of its two bracketing key-frames.
+A step renders the next F (default 60) frames of this rank's share of the
+sequence (frame f -> rank f mod N, weak scaling).  L2 is flushed between
+steps (a 512 MiB write), outside the timed events.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Rank 0 prints one JSON line.  `--impl reference` times the CPU oracle (this
+tier's reference arm) on bounded samples of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frames/sec at 1352x1014 (N3V-shaped 200k-Gaussian masked scene)"
+UNIT = "frames/s"
+CONFIG = "c3"
+N_CAMS = 20
+N_FRAMES_T = 300
+INTERVAL = 20
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--frames-per-step", type=int, default=60)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-stage-events", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+def sequence():
+    """All (frame f, time index, camera) of the sequence, ordered by f."""
+    return [(f, f // N_CAMS, f % N_CAMS) for f in range(N_CAMS * N_FRAMES_T)]
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during timing."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- helpers
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def load_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+def cpu_oracle_run(scene, cams, masks, kf, frames, seconds, row_stride=8):
+    """Time the oracle as it stands on bounded samples: rows j = 0 mod row_stride
+    of consecutive frames until `seconds` elapse.  Returns (frames/s, info)."""
+    import oracle
+    from paper_2503_16422_b200.api import bracket
+    import fdgs_inputs as fi
+
+    times = fi.frame_times(N_FRAMES_T)
+    W, H = cams[0].width, cams[0].height
+    rows = np.arange(0, H, row_stride)
+    pix = (rows[:, None] * W + np.arange(W)[None, :]).ravel()
+    done_px, k, t0 = 0, 0, time.perf_counter()
+    oracle.load()
+    t0 = time.perf_counter()
+    while True:
+        f, ti, ci = frames[k % len(frames)]
+        li, ri = bracket(kf, ti)
+        act = masks[li] | masks[ri]
+        oracle.render(scene, cams[ci], float(times[ti]), mask=act, pixels=pix)
+        done_px += pix.size
+        k += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    fps = done_px / (W * H) / el
+    return fps, dict(cores=oracle.num_threads(), frames=k, seconds=round(el, 2),
+                     sample=f"oracle per-pixel render of rows j%{row_stride}==0 ({pix.size} px) of {k} "
+                            f"consecutive masked C3 frames; fps = sampled pixels/(W*H)/wall")
+
+
+# ----------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import fdgs_inputs as fi
+    import paper_2503_16422_b200 as fd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---- scene: rank 0 draws it, NCCL broadcast to the others
+    cfg = fi.CONFIGS[CONFIG]
+    n = cfg["n"]
+    shapes = {"mean": (n, 4), "scale": (n, 4), "rot_l": (n, 4), "rot_r": (n, 4), "opacity": (n,),
+              "log255_opacity": (n,), "sh": (n, 16, 3)}
+    if rank == 0:
+        arrays = fi.make_scene(CONFIG)
+        tens = {k: torch.from_numpy(v).to(dev) for k, v in arrays.arrays().items()}
+    else:
+        arrays = None
+        tens = {k: torch.empty(s, dtype=torch.float32, device=dev) for k, s in shapes.items()}
+    if world > 1:
+        for k in shapes:
+            dist.broadcast(tens[k], src=0)
+    scene = fd.Scene(tens, device=dev)
+    cams = fi.make_cameras(CONFIG)
+    cam_structs = [fd.camera_struct(c) for c in cams]
+    times = fi.frame_times(N_FRAMES_T)
+    kf = fd.keyframes(N_FRAMES_T, INTERVAL)
+    # ---- key-frame masks: key-frame k built by rank k mod N, all-reduced (disjoint rows)
+    words = fd.mask_words(n)
+    masks = torch.zeros((len(kf), words), dtype=torch.int32, device=dev)
+    t_mask0 = time.perf_counter()
+    for k in range(len(kf)):
+        if k % world == rank:
+            fd.keyframe_mask(scene, cams, float(times[kf[k]]), out=masks[k])
+    if world > 1:
+        dist.all_reduce(masks, op=dist.ReduceOp.SUM)
+    torch.cuda.synchronize()
+    mask_build_s = time.perf_counter() - t_mask0
+
+    seq = sequence()
+    mine = [x for x in seq if x[0] % world == rank]
+    F = args.frames_per_step
+    renderer = fd.Renderer(scene, cams[0].width, cams[0].height)
+    outs = [renderer.new_output() for _ in range(F)]
+    stats = torch.zeros((F, 4), dtype=torch.int64, device=dev)  # fdgs_frame_stats is 32 bytes
+    flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device=dev)  # 512 MiB > L2
+    stream = torch.cuda.current_stream()
+    use_ev = not args.no_stage_events
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(F)]
+    for row in evs:
+        for e in row:
+            e.record(stream)  # materialise the CUDA events
+    torch.cuda.synchronize()
+
+    # grow the entry capacity once if the sequence needs more than the default
+    _, st0 = renderer.render_checked(cams[mine[0][2]], float(times[mine[0][1]]))
+
+    def frame_args(x):
+        f, ti, ci = x
+        li, ri = fd.bracket(kf, ti)
+        return cam_structs[ci], float(times[ti]), masks[li], masks[ri]
+
+    def run_step(step_frames, timed, count=False):
+        flush.zero_()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for k, x in enumerate(step_frames):
+            cs, t, ml, mr = frame_args(x)
+            renderer.render(cs, t, ml, mr, out=outs[k], stats=stats[k] if count else None,
+                            stage_events=evs[k] if (use_ev and timed) else None)
+        end.record(stream)
+        end.synchronize()
+        ms = start.elapsed_time(end)
+        stage = None
+        if use_ev and timed:
+            stage = np.zeros(4)
+            for k in range(len(step_frames)):
+                for s in range(4):
+                    stage[s] += evs[k][s].elapsed_time(evs[k][s + 1])
+        return ms, stage
+
+    ptr = 0
+
+    def next_frames():
+        nonlocal ptr
+        out = [mine[(ptr + k) % len(mine)] for k in range(F)]
+        ptr += F
+        return out
+
+    for _ in range(args.warmup):
+        run_step(next_frames(), False)
+    sampler = ClockSampler(local)
+    sampler.start()
+    step_ms, stage_ms = [], np.zeros(4)
+    n_eval = n_blend = 0
+    n_vis_tot = n_ent_tot = n_act_tot = 0
+    timed_frames = []
+    for _ in range(args.steps):
+        fr = next_frames()
+        timed_frames.append(fr)
+        ms, stg = run_step(fr, True)
+        step_ms.append(ms)
+        if stg is not None:
+            stage_ms += stg
+    clocks = sampler.stop()
+    # work counters of the same frames (counting blend variant, not timed)
+    for fr in timed_frames:
+        run_step(fr, False, count=True)
+        s = stats.cpu().numpy()
+        lo = np.ascontiguousarray(s[:, 0]).view(np.uint32).reshape(F, 2)
+        hi = np.ascontiguousarray(s[:, 1]).view(np.uint32).reshape(F, 2)
+        n_act_tot += int(lo[:, 0].sum())
+        n_vis_tot += int(lo[:, 1].sum())
+        n_ent_tot += int(hi[:, 0].sum())
+        assert np.all(hi[:, 1] == 0), "a frame overflowed its entry capacity"
+        n_eval += int(s[:, 2].sum())
+        n_blend += int(s[:, 3].sum())
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    frames_total = world * args.steps * F
+    value = frames_total / (total_ms / 1e3)
+    frames_rank = args.steps * F
+
+    # ---- roofline of the dominant stage
+    peaks, peak_src = load_peaks()
+    stage_names = ["preprocess", "depth_sort", "binning", "blend"]
+    res = dict(metric=METRIC, value=round(value, 2), unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
+               ms_per_step=round(total_ms / args.steps, 4), higher_is_better=True, scaling="weak", vs_baseline=None,
+               dtype="f32 (decision path f64)", data="synthetic",
+               config={"workload": "c3: N3V-shaped 200k 4D Gaussians, 1352x1014, 20 cams x 300 t, "
+                                   "key-frame interval 20, masked (union of bracketing key-frames)",
+                       "frames_per_step": F, "frames_per_rank": frames_rank, "partition": "frame f -> rank f mod N",
+                       "l2": "flushed between steps (512 MiB write)", "parallelism": f"frames x{world}"},
+               gpu_launches=13 * frames_rank)
+    if use_ev and stage_ms.sum() > 0:
+        per_frame = stage_ms / frames_rank
+        dom = int(np.argmax(stage_ms))
+        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        if dom == 3:
+            flops = 10.0 * n_eval + 12.0 * n_blend
+            achieved = flops / (stage_ms[3] / 1e3) / 1e12
+            peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+            rl = {"kernel": "k_blend", "bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2),
+                  "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                  "peak_src": f"148 SMs x 128 FP32 lanes x 2 (FMA) x {sm_mhz:.0f} MHz (sm_max from {peak_src} peaks)",
+                  "work": "10 flops per evaluated (pixel,Gaussian) pair + 12 per blended pair (DESIGN.md)"}
+        else:
+            hbm = float(peaks.get("hbm_gbs", 6650.0))
+            nb = {0: 68.0 * n_act_tot + 192.0 * n_vis_tot + 68.0 * n_vis_tot,
+                  1: 72.0 * n_vis_tot, 2: 40.0 * n_ent_tot}[dom]
+            achieved = nb / (stage_ms[dom] / 1e3) / 1e9
+            rl = {"kernel": stage_names[dom], "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
+                  "unit": "GB/s", "frac": round(achieved / hbm, 4), "peak_src": peak_src}
+        tr = load_traffic().get(rl["kernel"])
+        rl["traffic"] = tr
+        res["roofline"] = rl
+        res["stages"] = {nm: {"ms_per_frame": round(float(per_frame[i]), 4),
+                              "share": round(float(stage_ms[i] / stage_ms.sum()), 4)} for i, nm in enumerate(stage_names)}
+        res["stages"]["stage_events_sum_vs_step"] = round(float(stage_ms.sum() / sum(step_ms)), 4)
+    res["work_per_frame"] = {"n_act": round(n_act_tot / frames_rank), "n_vis": round(n_vis_tot / frames_rank),
+                             "entries": round(n_ent_tot / frames_rank), "evaluated_pairs": round(n_eval / frames_rank),
+                             "blended_pairs": round(n_blend / frames_rank)}
+    res["clocks"] = clocks
+    res["setup"] = {"keyframe_masks_s": round(mask_build_s, 3), "n_keyframes": len(kf)}
+
+    # ---- e2e through the public API with host buffers
+    if not args.no_e2e:
+        import torch as _t
+        host_masks = masks.cpu().pin_memory()
+        dev_masks = _t.empty_like(masks)
+        host_out = _t.empty((F, 3, cams[0].height, cams[0].width), dtype=_t.float32).pin_memory()
+        e2e_ms = []
+        h2d_bytes = d2h_bytes = 0
+        for it in range(args.warmup + max(1, args.steps // 2)):
+            fr = next_frames()
+            need = sorted({i for x in fr for i in fd.bracket(kf, x[1])})
+            flush.zero_()
+            _t.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            a = _t.cuda.Event(enable_timing=True)
+            b = _t.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for i in need:
+                dev_masks[i].copy_(host_masks[i], non_blocking=True)
+            for k, x in enumerate(fr):
+                f, ti, ci = x
+                li, ri = fd.bracket(kf, ti)
+                renderer.render(cam_structs[ci], float(times[ti]), dev_masks[li], dev_masks[ri], out=outs[k])
+                host_out[k].copy_(outs[k], non_blocking=True)
+            b.record(stream)
+            b.synchronize()
+            if it >= args.warmup:
+                e2e_ms.append(a.elapsed_time(b))
+                h2d_bytes = len(need) * words * 4
+                d2h_bytes = F * 3 * cams[0].height * cams[0].width * 4
+        tot = float(sum(e2e_ms))
+        if world > 1:
+            t = _t.tensor([tot], dtype=_t.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tot = float(t.item())
+        res["e2e"] = {"value": round(world * len(e2e_ms) * F / (tot / 1e3), 2), "unit": UNIT,
+                      "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
+                      "path": "Renderer.render (fdgs_render) with key-frame masks H2D from pinned host and every "
+                              "frame D2H to pinned host inside the timed region"}
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        fps, info = cpu_oracle_run(arrays, cams, masks.cpu().numpy().view(np.uint32), kf, mine, args.cpu_seconds)
+        res["cpu_baseline"] = {"value": round(fps, 5), "unit": UNIT, "cores": info["cores"], "kind": "oracle",
+                               "sample": info["sample"]}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+
+
+# ------------------------------------------------------------- reference
+def run_reference(args):
+    """This tier's reference arm: the CPU oracle as it stands (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import fdgs_inputs as fi
+    import oracle
+
+    scene = fi.make_scene(CONFIG)
+    cams = fi.make_cameras(CONFIG)
+    times = fi.frame_times(N_FRAMES_T)
+    from paper_2503_16422_b200.api import keyframes  # host schedule only (no CUDA)
+    kf = keyframes(N_FRAMES_T, INTERVAL)
+    masks = np.stack([oracle.keyframe_mask(scene, cams, times[k]) for k in kf])
+    seq = sequence()
+    per_step = max(1.0, 60.0 / max(1, args.steps + args.warmup))
+    vals = []
+    info = None
+    for s in range(args.warmup + args.steps):
+        frames = seq[(s * 7) % len(seq):] + seq
+        fps, info = cpu_oracle_run(scene, cams, masks, kf, frames, per_step, row_stride=16)
+        if s >= args.warmup:
+            vals.append(fps)
+    value = float(np.mean(vals))
+    res = dict(metric=METRIC, value=round(value, 5), unit=UNIT, n_gpus=world, steps=args.steps,
+               warmup=args.warmup, ms_per_step=round(per_step * 1e3, 1), higher_is_better=True, scaling="weak",
+               vs_baseline=None, dtype="f64", data="synthetic", impl="reference",
+               config={"workload": "c3: N3V-shaped 200k 4D Gaussians, 1352x1014, masked; each step a bounded "
+                                   "row sample (rows j%16==0) of consecutive frames"},
+               cpu_baseline={"value": round(value, 5), "unit": UNIT, "kind": "oracle", "cores": info["cores"],
+                             "sample": info["sample"]},
+               e2e={"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+    print(json.dumps(res), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -68,6 +68,8 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.rec1 = take(16 * nn);
     L.rec2 = take(16 * nn);
     L.depth = take(4 * nn);
+    L.rect = take(8 * nn);
+    L.rect_sorted = take(8 * nn);
     L.keys0 = take(4 * nn);
     L.keys1 = take(4 * nn);
     L.vals0 = take(4 * nn);

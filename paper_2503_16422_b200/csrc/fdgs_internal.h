@@ -43,7 +43,7 @@ struct RenderLayout {
     int32_t p_bin;     // binning partitions
     int32_t bin_warps; // warps per binning block
     int64_t max_entries;
-    size_t counters, lookback, rec0, rec1, rec2, depth, keys0, keys1, vals0, vals1, sort_hist, bin_hist,
+    size_t counters, lookback, rec0, rec1, rec2, depth, rect, rect_sorted, keys0, keys1, vals0, vals1, sort_hist, bin_hist,
         tile_total, tile_start, entries, total;
 };
 RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max_entries);

@@ -25,25 +25,31 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
-// Decoupled look-back (single thread): publish `total` for partition `part`,
-// return the exclusive prefix.  Status word = flag(2 bits) | value(30 bits).
-__device__ __forceinline__ uint32_t lookback_exclusive(uint32_t *status, uint32_t part, uint32_t total) {
+// Decoupled look-back, one warp: publish `total` for partition `part`, return
+// the exclusive prefix (all lanes).  Status word = flag(2 bits) | value(30
+// bits); the warp inspects 32 predecessors per round trip.
+__device__ __forceinline__ uint32_t lookback_warp(uint32_t *status, uint32_t part, uint32_t total, int lane) {
     if (part == 0) {
-        st_volatile(&status[0], kFlagP | total);
+        if (lane == 0) st_volatile(&status[0], kFlagP | total);
         return 0;
     }
-    st_volatile(&status[part], kFlagA | total);
+    if (lane == 0) st_volatile(&status[part], kFlagA | total);
     uint32_t excl = 0;
-    int j = (int)part - 1;
+    int base = (int)part - 1;
     while (true) {
-        const uint32_t s = ld_volatile(&status[j]);
-        const uint32_t f = s & ~kValMask;
-        if (f == 0) continue;
-        excl += s & kValMask;
-        if (f == kFlagP) break;
-        --j;
+        const int j = base - lane;
+        uint32_t s = j >= 0 ? ld_volatile(&status[j]) : (kFlagP | 0u);
+        if (__any_sync(0xffffffffu, (s & ~kValMask) == 0)) continue;  // a predecessor is not published yet
+        const uint32_t pmask = __ballot_sync(0xffffffffu, (s & ~kValMask) == kFlagP);
+        const int stop = pmask ? __ffs(pmask) - 1 : 31;
+        uint32_t v = lane <= stop ? (s & kValMask) : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (pmask) break;
+        base -= 32;
     }
-    st_volatile(&status[part], kFlagP | (excl + total));
+    if (lane == 0) st_volatile(&status[part], kFlagP | (excl + total));
     return excl;
 }
 
@@ -52,7 +58,7 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess(SceneDev sc, const uin
                                                           const uint32_t *__restrict__ mask_r, CamDev cam, float t,
                                                           Counters *ctr, uint32_t *lb, float4 *__restrict__ rec0,
                                                           float4 *__restrict__ rec1, float4 *__restrict__ rec2,
-                                                          uint32_t *__restrict__ depth) {
+                                                          uint32_t *__restrict__ depth, uint2 *__restrict__ rect) {
     __shared__ uint32_t s_part, s_excl;
     __shared__ uint32_t s_wvis[kPreBlock / 32], s_wact[kPreBlock / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -85,19 +91,23 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess(SceneDev sc, const uin
         s_wact[warp] = __popc(bact);
     }
     __syncthreads();
-    if (tid == 0) {
-        uint32_t tot = 0, act_tot = 0;
+    if (warp == 0) {
+        uint32_t tot = 0, act_tot = 0, mine = 0;
 #pragma unroll
         for (int w = 0; w < kPreBlock / 32; ++w) {
             const uint32_t c = s_wvis[w];
-            s_wvis[w] = tot;
+            if (w == lane) mine = tot;
             tot += c;
             act_tot += s_wact[w];
         }
-        if (act_tot) atomicAdd(&ctr->n_act, act_tot);
-        const uint32_t excl = lookback_exclusive(lb, part, tot);
-        s_excl = excl;
-        if (part == gridDim.x - 1) ctr->n_vis = excl + tot;
+        __syncwarp();
+        if (lane < kPreBlock / 32) s_wvis[lane] = mine;
+        if (lane == 0 && act_tot) atomicAdd(&ctr->n_act, act_tot);
+        const uint32_t excl = lookback_warp(lb, part, tot, lane);
+        if (lane == 0) {
+            s_excl = excl;
+            if (part == gridDim.x - 1) ctr->n_vis = excl + tot;
+        }
     }
     __syncthreads();
     if (vis) {
@@ -110,6 +120,7 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess(SceneDev sc, const uin
                                 __int_as_float(pj.py0 | (pj.py1 << 16)));
         rec2[pos] = make_float4(rgb[0], rgb[1], rgb[2], __int_as_float(i));
         depth[pos] = pj.depth_bits;
+        rect[pos] = make_uint2(pj.px0 | (pj.px1 << 16), pj.py0 | (pj.py1 << 16));
     }
 }
 
@@ -124,13 +135,13 @@ __device__ __forceinline__ void part_range(uint32_t n, int parts, int b, uint32_
 
 // Per-partition digit histogram; the last block to finish turns the [P][256]
 // table into global exclusive offsets (digit-major, partition-minor).
-__global__ void __launch_bounds__(kSortThreads) k_sort_upsweep(const uint32_t *__restrict__ keys,
-                                                               const Counters *ctrc, Counters *ctr, int pass,
-                                                               uint32_t *__restrict__ hist) {
+__global__ void __launch_bounds__(kSortThreads) k_sort_upsweep(const uint32_t *__restrict__ keys, Counters *ctr,
+                                                               int pass, uint32_t *__restrict__ hist) {
     __shared__ uint32_t h[256];
+    __shared__ uint32_t s_scan[256];
     __shared__ bool s_last;
     const int tid = threadIdx.x, P = gridDim.x, b = blockIdx.x;
-    const uint32_t n = ctrc->n_vis;
+    const uint32_t n = ctr->n_vis;
     const int shift = 8 * pass;
     uint32_t lo, hi;
     part_range(n, P, b, lo, hi);
@@ -145,11 +156,18 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_upsweep(const uint32_t *_
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    // digit tid: total over partitions, block-exclusive-scan over digits, then
-    // per-partition running offsets.
+    // digit tid: total over partitions (L2 loads, pipelined), block scan over
+    // digits, then per-partition running offsets.
     uint32_t tot = 0;
-    for (int p = 0; p < P; ++p) tot += ld_volatile(&hist[(size_t)p * 256 + tid]);
-    __shared__ uint32_t s_scan[256];
+    int p = 0;
+    for (; p + 8 <= P; p += 8) {
+        uint32_t c[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) c[k] = __ldcg(&hist[(size_t)(p + k) * 256 + tid]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) tot += c[k];
+    }
+    for (; p < P; ++p) tot += __ldcg(&hist[(size_t)p * 256 + tid]);
     s_scan[tid] = tot;
     __syncthreads();
     for (int off = 1; off < 256; off <<= 1) {
@@ -159,20 +177,33 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_upsweep(const uint32_t *_
         __syncthreads();
     }
     uint32_t run = s_scan[tid] - tot;
-    for (int p = 0; p < P; ++p) {
-        const uint32_t c = ld_volatile(&hist[(size_t)p * 256 + tid]);
+    for (p = 0; p + 8 <= P; p += 8) {
+        uint32_t c[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) c[k] = __ldcg(&hist[(size_t)(p + k) * 256 + tid]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            hist[(size_t)(p + k) * 256 + tid] = run;
+            run += c[k];
+        }
+    }
+    for (; p < P; ++p) {
+        const uint32_t c = __ldcg(&hist[(size_t)p * 256 + tid]);
         hist[(size_t)p * 256 + tid] = run;
         run += c;
     }
 }
 
 // Stable scatter: 256-item tiles, within-warp ranks by match_any, cross-warp
-// prefix per digit in shared memory.
+// prefix per digit in shared memory.  The last pass also gathers the packed
+// pixel AABB of each Gaussian into canonical order (rect_out) for binning.
 __global__ void __launch_bounds__(kSortThreads) k_sort_downsweep(const uint32_t *__restrict__ keys_in,
                                                                  const uint32_t *__restrict__ vals_in,
                                                                  uint32_t *__restrict__ keys_out,
                                                                  uint32_t *__restrict__ vals_out, const Counters *ctrc,
-                                                                 int pass, const uint32_t *__restrict__ hist) {
+                                                                 int pass, const uint32_t *__restrict__ hist,
+                                                                 const uint2 *__restrict__ rect_in,
+                                                                 uint2 *__restrict__ rect_out) {
     constexpr int NW = kSortThreads / 32;
     __shared__ uint32_t s_off[256];
     __shared__ uint32_t s_w[NW][256];
@@ -188,6 +219,8 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_downsweep(const uint32_t 
         const bool valid = i < hi;
         const uint32_t key = valid ? __ldg(keys_in + i) : 0u;
         const uint32_t val = valid ? (vals_in ? __ldg(vals_in + i) : i) : 0u;
+        uint2 rc = make_uint2(0, 0);
+        if (rect_out != nullptr && valid) rc = __ldg(rect_in + val);
         const uint32_t d = valid ? (key >> shift) & 255u : 256u;
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
         const uint32_t rank = __popc(peers & lanemask_lt());
@@ -211,63 +244,89 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_downsweep(const uint32_t 
             const uint32_t pos = s_w[warp][d] + rank;
             if (keys_out) keys_out[pos] = key;
             vals_out[pos] = val;
+            if (rect_out) rect_out[pos] = rc;
         }
         __syncthreads();
     }
 }
 
 // ---------------------------------------------------------------- row 5b
-__device__ __forceinline__ void unpack_rect(float4 r1, int &px0, int &px1, int &py0, int &py1) {
-    const uint32_t ax = __float_as_uint(r1.z), ay = __float_as_uint(r1.w);
-    px0 = ax & 0xffff;
-    px1 = ax >> 16;
-    py0 = ay & 0xffff;
-    py1 = ay >> 16;
+// Tile rectangle of a packed pixel AABB (16x16 tiles).
+struct TileRect {
+    int tx0, ty0, nx, ny;
+};
+__device__ __forceinline__ TileRect tile_rect(uint2 r) {
+    TileRect t;
+    t.tx0 = (r.x & 0xffff) >> 4;
+    t.ty0 = (r.y & 0xffff) >> 4;
+    t.nx = (int)(r.x >> 20) - t.tx0 + 1;
+    t.ny = (int)(r.y >> 20) - t.ty0 + 1;
+    return t;
 }
 
-// Per-partition (canonical-rank range) histogram over tiles -> hist[b][T].
-__global__ void __launch_bounds__(256) k_bin_count(const uint32_t *__restrict__ order, const float4 *__restrict__ rec1,
-                                                   const Counters *ctrc, int tiles_x, int n_tiles,
-                                                   uint32_t *__restrict__ hist) {
-    extern __shared__ uint32_t sh_cnt[];
+// Per-partition tile histogram via a 2D difference array: 4 shared atomics per
+// Gaussian, then row and column prefix sums -> hist[b][T].
+__global__ void __launch_bounds__(256) k_bin_count(const uint2 *__restrict__ rects, const Counters *ctrc, int tiles_x,
+                                                   int tiles_y, uint32_t *__restrict__ hist) {
+    extern __shared__ int sh_diff[];  // (tiles_y + 1) x (tiles_x + 1)
     const int tid = threadIdx.x, P = gridDim.x, b = blockIdx.x;
-    for (int k = tid; k < n_tiles; k += blockDim.x) sh_cnt[k] = 0;
+    const int gx = tiles_x + 1, gy = tiles_y + 1;
+    for (int k = tid; k < gx * gy; k += blockDim.x) sh_diff[k] = 0;
     __syncthreads();
     uint32_t lo, hi;
     part_range(ctrc->n_vis, P, b, lo, hi);
     for (uint32_t r = lo + tid; r < hi; r += blockDim.x) {
-        const uint32_t v = __ldg(order + r);
-        int px0, px1, py0, py1;
-        unpack_rect(__ldg(rec1 + v), px0, px1, py0, py1);
-        for (int ty = py0 >> 4; ty <= (py1 >> 4); ++ty)
-            for (int tx = px0 >> 4; tx <= (px1 >> 4); ++tx) atomicAdd(&sh_cnt[ty * tiles_x + tx], 1u);
+        const TileRect t = tile_rect(__ldg(rects + r));
+        const int x1 = t.tx0 + t.nx, y1 = t.ty0 + t.ny;
+        atomicAdd(&sh_diff[t.ty0 * gx + t.tx0], 1);
+        atomicAdd(&sh_diff[t.ty0 * gx + x1], -1);
+        atomicAdd(&sh_diff[y1 * gx + t.tx0], -1);
+        atomicAdd(&sh_diff[y1 * gx + x1], 1);
     }
     __syncthreads();
-    for (int k = tid; k < n_tiles; k += blockDim.x) hist[(size_t)b * n_tiles + k] = sh_cnt[k];
+    for (int y = tid; y < tiles_y; y += blockDim.x) {  // prefix along x
+        int run = 0;
+        for (int x = 0; x < tiles_x; ++x) {
+            run += sh_diff[y * gx + x];
+            sh_diff[y * gx + x] = run;
+        }
+    }
+    __syncthreads();
+    for (int x = tid; x < tiles_x; x += blockDim.x) {  // prefix along y
+        int run = 0;
+        for (int y = 0; y < tiles_y; ++y) {
+            run += sh_diff[y * gx + x];
+            sh_diff[y * gx + x] = run;
+        }
+    }
+    __syncthreads();
+    const int n_tiles = tiles_x * tiles_y;
+    for (int k = tid; k < n_tiles; k += blockDim.x)
+        hist[(size_t)b * n_tiles + k] = (uint32_t)sh_diff[(k / tiles_x) * gx + (k % tiles_x)];
 }
 
-// Column scan: for 32 consecutive tiles, exclusive prefix over partitions
-// (in place) + per-tile totals; the last block scans the totals into
-// tile_start[0..T] and checks the entry capacity.
-__global__ void __launch_bounds__(256) k_bin_colscan(uint32_t *__restrict__ hist, int P, int n_tiles,
-                                                     uint32_t *__restrict__ tile_total,
-                                                     uint32_t *__restrict__ tile_start, Counters *ctr,
-                                                     int64_t max_entries) {
-    __shared__ uint32_t s_part[8][32];
+// Column scan: tile t's exclusive prefix over partitions (in place) and its
+// total; the last block scans the totals into tile_start[0..T] and checks the
+// entry capacity.  Block = 32 tiles x 32 partition slices.
+__global__ void __launch_bounds__(1024) k_bin_colscan(uint32_t *__restrict__ hist, int P, int n_tiles,
+                                                      uint32_t *__restrict__ tile_total,
+                                                      uint32_t *__restrict__ tile_start, Counters *ctr,
+                                                      int64_t max_entries) {
+    __shared__ uint32_t s_part[32][33];
+    __shared__ uint32_t s_sum[1024];
     __shared__ bool s_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int t = blockIdx.x * 32 + lane;
-    const int per = (P + 7) / 8;
+    const int per = (P + 31) / 32;
     const int b0 = min(warp * per, P), b1 = min(b0 + per, P);
     uint32_t sum = 0;
     if (t < n_tiles)
-        for (int b = b0; b < b1; ++b) sum += hist[(size_t)b * n_tiles + t];
+        for (int b = b0; b < b1; ++b) sum += __ldcg(&hist[(size_t)b * n_tiles + t]);
     s_part[warp][lane] = sum;
     __syncthreads();
     if (warp == 0) {
         uint32_t run = 0;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
+        for (int w = 0; w < 32; ++w) {
             const uint32_t c = s_part[w][lane];
             s_part[w][lane] = run;
             run += c;
@@ -278,7 +337,7 @@ __global__ void __launch_bounds__(256) k_bin_colscan(uint32_t *__restrict__ hist
     if (t < n_tiles) {
         uint32_t run = s_part[warp][lane];
         for (int b = b0; b < b1; ++b) {
-            const uint32_t c = hist[(size_t)b * n_tiles + t];
+            const uint32_t c = __ldcg(&hist[(size_t)b * n_tiles + t]);
             hist[(size_t)b * n_tiles + t] = run;
             run += c;
         }
@@ -289,15 +348,13 @@ __global__ void __launch_bounds__(256) k_bin_colscan(uint32_t *__restrict__ hist
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    // exclusive scan of tile_total -> tile_start (block-wide, chunked)
-    __shared__ uint32_t s_sum[256];
-    const int chunk = (n_tiles + 255) / 256;
+    const int chunk = (n_tiles + 1023) / 1024;
     const int k0 = min(tid * chunk, n_tiles), k1 = min(k0 + chunk, n_tiles);
     uint32_t local = 0;
-    for (int k = k0; k < k1; ++k) local += ld_volatile(&tile_total[k]);
+    for (int k = k0; k < k1; ++k) local += __ldcg(&tile_total[k]);
     s_sum[tid] = local;
     __syncthreads();
-    for (int off = 1; off < 256; off <<= 1) {
+    for (int off = 1; off < 1024; off <<= 1) {
         const uint32_t v = tid >= off ? s_sum[tid - off] : 0;
         __syncthreads();
         s_sum[tid] += v;
@@ -306,19 +363,20 @@ __global__ void __launch_bounds__(256) k_bin_colscan(uint32_t *__restrict__ hist
     uint32_t run = s_sum[tid] - local;
     for (int k = k0; k < k1; ++k) {
         tile_start[k] = run;
-        run += ld_volatile(&tile_total[k]);
+        run += __ldcg(&tile_total[k]);
     }
-    if (tid == 255) {
-        const uint32_t E = s_sum[255];
+    if (tid == 1023) {
+        const uint32_t E = s_sum[1023];
         tile_start[n_tiles] = E;
         ctr->n_entries = E;
         if ((int64_t)E > max_entries) ctr->status = FDGS_ERR_OVERFLOW;
     }
 }
 
-// Stable scatter of entries: warp-private u16 counters per tile; warp w owns a
-// contiguous sub-range of the block's canonical ranks and walks it in order.
-__global__ void k_bin_scatter(const uint32_t *__restrict__ order, const float4 *__restrict__ rec1,
+// Stable scatter of entries.  Warp w owns a contiguous sub-range of the
+// block's canonical ranks and walks it in order with warp-private u16 tile
+// counters; each round loads 32 rects at once and broadcasts them by shuffle.
+__global__ void k_bin_scatter(const uint32_t *__restrict__ order, const uint2 *__restrict__ rects,
                               const Counters *ctrc, int tiles_x, int n_tiles, const uint32_t *__restrict__ hist,
                               const uint32_t *__restrict__ tile_start, uint32_t *__restrict__ entries) {
     extern __shared__ uint32_t sh_base[];  // [n_tiles] u32 global base, then [NW][n_tiles] u16
@@ -334,15 +392,19 @@ __global__ void k_bin_scatter(const uint32_t *__restrict__ order, const float4 *
     const uint32_t per = (hi - lo + NW - 1) / NW;
     const uint32_t w0 = min(lo + warp * per, hi), w1 = min(w0 + per, hi);
     uint16_t *my = cnt + warp * n_tiles;
-    for (uint32_t r = w0; r < w1; ++r) {
-        int px0, px1, py0, py1;
-        unpack_rect(__ldg(rec1 + __ldg(order + r)), px0, px1, py0, py1);
-        const int tx0 = px0 >> 4, ty0 = py0 >> 4, nx = (px1 >> 4) - tx0 + 1, ny = (py1 >> 4) - ty0 + 1;
-        for (int e = lane; e < nx * ny; e += 32) {
-            const int ty = ty0 + e / nx, tx = tx0 + e % nx;
-            my[ty * tiles_x + tx] += 1;
+    for (uint32_t r0 = w0; r0 < w1; r0 += 32) {
+        const uint32_t r = r0 + lane;
+        const uint2 rc = r < w1 ? __ldg(rects + r) : make_uint2(0, 0);
+        const int m = min(32u, w1 - r0);
+        for (int j = 0; j < m; ++j) {
+            const uint2 q = make_uint2(__shfl_sync(0xffffffffu, rc.x, j), __shfl_sync(0xffffffffu, rc.y, j));
+            const TileRect t = tile_rect(q);
+            for (int e = lane; e < t.nx * t.ny; e += 32) {
+                const int ty = t.ty0 + e / t.nx, tx = t.tx0 + e % t.nx;
+                my[ty * tiles_x + tx] += 1;
+            }
+            __syncwarp();
         }
-        __syncwarp();
     }
     __syncthreads();
     for (int k = tid; k < n_tiles; k += blockDim.x) {
@@ -355,18 +417,27 @@ __global__ void k_bin_scatter(const uint32_t *__restrict__ order, const float4 *
         }
     }
     __syncthreads();
-    for (uint32_t r = w0; r < w1; ++r) {
-        const uint32_t v = __ldg(order + r);
-        int px0, px1, py0, py1;
-        unpack_rect(__ldg(rec1 + v), px0, px1, py0, py1);
-        const int tx0 = px0 >> 4, ty0 = py0 >> 4, nx = (px1 >> 4) - tx0 + 1, ny = (py1 >> 4) - ty0 + 1;
-        for (int e = lane; e < nx * ny; e += 32) {
-            const int tile = (ty0 + e / nx) * tiles_x + tx0 + e % nx;
-            const uint32_t pos = sh_base[tile] + my[tile];
-            my[tile] += 1;
-            entries[pos] = v;
+    for (uint32_t r0 = w0; r0 < w1; r0 += 32) {
+        const uint32_t r = r0 + lane;
+        uint2 rc = make_uint2(0, 0);
+        uint32_t v = 0;
+        if (r < w1) {
+            rc = __ldg(rects + r);
+            v = __ldg(order + r);
         }
-        __syncwarp();
+        const int m = min(32u, w1 - r0);
+        for (int j = 0; j < m; ++j) {
+            const uint2 q = make_uint2(__shfl_sync(0xffffffffu, rc.x, j), __shfl_sync(0xffffffffu, rc.y, j));
+            const uint32_t vj = __shfl_sync(0xffffffffu, v, j);
+            const TileRect t = tile_rect(q);
+            for (int e = lane; e < t.nx * t.ny; e += 32) {
+                const int tile = (t.ty0 + e / t.nx) * tiles_x + t.tx0 + e % t.nx;
+                const uint32_t pos = sh_base[tile] + my[tile];
+                my[tile] += 1;
+                entries[pos] = vj;
+            }
+            __syncwarp();
+        }
     }
 }
 
@@ -376,9 +447,59 @@ __device__ __forceinline__ float ex2_approx(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// Packed fp32x2 (Blackwell FADD2/FFMA2), IEEE RN per lane.  Used only where
+// no product feeds an add (no contraction hazard), see DESIGN.md.
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    float2 d;
+    asm("sub.rn.f32x2 %0, %1, %2;"
+        : "=l"(*reinterpret_cast<unsigned long long *>(&d))
+        : "l"(*reinterpret_cast<unsigned long long *>(&a)), "l"(*reinterpret_cast<unsigned long long *>(&b)));
+    return d;
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(*reinterpret_cast<unsigned long long *>(&d))
+        : "l"(*reinterpret_cast<unsigned long long *>(&a)), "l"(*reinterpret_cast<unsigned long long *>(&b)),
+          "l"(*reinterpret_cast<unsigned long long *>(&c)));
+    return d;
+}
 
-constexpr int kBlendThreads = 256;
+constexpr int kBlendThreads = 128;  // one 16x16 tile, 2 horizontally adjacent pixels per thread
 
+// Staged splat record in shared memory (double-buffered batches).
+struct BlendBatch {
+    float4 a[kBlendThreads];  // u, v, A', B'
+    float4 c[kBlendThreads];  // C', Q2, r, g
+    float2 d[kBlendThreads];  // b, tile-local AABB mask (x bits 0-15, y bits 16-31)
+};
+
+__device__ __forceinline__ void stage_load(const uint32_t *__restrict__ entries, const float4 *__restrict__ rec0,
+                                           const float4 *__restrict__ rec1, const float4 *__restrict__ rec2,
+                                           uint32_t k, uint32_t end, float4 &r0, float4 &r1, float4 &r2) {
+    if (k < end) {
+        const uint32_t v = __ldg(entries + k);
+        r0 = __ldg(rec0 + v);
+        r1 = __ldg(rec1 + v);
+        r2 = __ldg(rec2 + v);
+    }
+}
+
+__device__ __forceinline__ void stage_store(BlendBatch &B, int tid, uint32_t k, uint32_t end, int tx, int ty,
+                                            const float4 &r0, const float4 &r1, const float4 &r2) {
+    if (k < end) {
+        const uint32_t ax = __float_as_uint(r1.z), ay = __float_as_uint(r1.w);
+        const int x0 = max((int)(ax & 0xffff) - tx * 16, 0), x1 = min((int)(ax >> 16) - tx * 16, 15);
+        const int y0 = max((int)(ay & 0xffff) - ty * 16, 0), y1 = min((int)(ay >> 16) - ty * 16, 15);
+        const uint32_t xm = ((2u << x1) - 1u) & ~((1u << x0) - 1u);
+        const uint32_t ym = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
+        B.a[tid] = r0;
+        B.c[tid] = make_float4(r1.x, r1.y, r2.x, r2.y);
+        B.d[tid] = make_float2(r2.z, __uint_as_float(xm | (ym << 16)));
+    }
+}
+
+template <bool kCount>
 __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restrict__ tile_start,
                                                          const uint32_t *__restrict__ entries,
                                                          const float4 *__restrict__ rec0,
@@ -387,86 +508,88 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restr
                                                          int tiles_x, int width, int height, float bg0, float bg1,
                                                          float bg2, float *__restrict__ out_rgb,
                                                          float *__restrict__ out_T, fdgs_frame_stats *stats) {
-    __shared__ float4 s0[kBlendThreads];
-    __shared__ float4 s1[kBlendThreads];
-    __shared__ float2 s2[kBlendThreads];
+    __shared__ BlendBatch sb[2];
     __shared__ bool s_last;
     const bool ok = ctr->status == FDGS_OK;
     const int tile = blockIdx.x, tx = tile % tiles_x, ty = tile / tiles_x;
-    const int tid = threadIdx.x, lx = tid & 15, ly = tid >> 4;
-    const int i = tx * 16 + lx, j = ty * 16 + ly;
-    const bool inside = i < width && j < height;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int ly = tid >> 3, lx = (tid & 7) * 2;
+    const int i0 = tx * 16 + lx, j = ty * 16 + ly;
+    const bool in0 = i0 < width && j < height, in1 = i0 + 1 < width && j < height;
     const uint32_t start = __ldg(tile_start + tile), end = __ldg(tile_start + tile + 1);
-    const float pxf = (float)i + 0.5f, pyf = (float)j + 0.5f;
-    const uint32_t pix = (1u << lx) | (1u << (16 + ly));
-    float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
-    bool done = !inside;
+    const float pyf = (float)j + 0.5f;
+    const float2 px = make_float2((float)i0 + 0.5f, (float)(i0 + 1) + 0.5f);
+    const uint32_t pb0 = (1u << lx) | (1u << (16 + ly)), pb1 = (2u << lx) | (1u << (16 + ly));
+    const uint32_t wrows = 0xFu << (16 + 4 * warp);  // this warp's 4 rows in the y-mask
+    float2 T = make_float2(1.0f, 1.0f), Cr = make_float2(0.f, 0.f), Cg = Cr, Cb = Cr;
+    bool done0 = !in0, done1 = !in1;
     uint32_t n_eval = 0, n_blend = 0;
-    for (uint32_t base = ok ? start : end; base < end; base += kBlendThreads) {
-        const uint32_t k = base + tid;
-        if (k < end) {
-            const uint32_t v = __ldg(entries + k);
-            const float4 r0 = __ldg(rec0 + v), r1 = __ldg(rec1 + v), r2 = __ldg(rec2 + v);
-            int px0, px1, py0, py1;
-            unpack_rect(r1, px0, px1, py0, py1);
-            const int x0 = max(px0 - tx * 16, 0), x1 = min(px1 - tx * 16, 15);
-            const int y0 = max(py0 - ty * 16, 0), y1 = min(py1 - ty * 16, 15);
-            const uint32_t xm = ((2u << x1) - 1u) & ~((1u << x0) - 1u);
-            const uint32_t ym = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
-            s0[tid] = r0;
-            s1[tid] = make_float4(r1.x, r1.y, r2.x, r2.y);
-            s2[tid] = make_float2(r2.z, __uint_as_float(xm | (ym << 16)));
-        }
-        __syncthreads();
-        if (!done) {
+    const uint32_t first = ok ? start : end;
+    float4 r0, r1, r2;
+    stage_load(entries, rec0, rec1, rec2, first + tid, end, r0, r1, r2);
+    stage_store(sb[0], tid, first + tid, end, tx, ty, r0, r1, r2);
+    __syncthreads();
+    int buf = 0;
+    for (uint32_t base = first; base < end; base += kBlendThreads) {
+        const uint32_t nxt = base + kBlendThreads;
+        stage_load(entries, rec0, rec1, rec2, nxt + tid, end, r0, r1, r2);  // prefetch the next batch
+        const BlendBatch &B = sb[buf];
+        if (!(done0 && done1)) {
             const int cnt = (int)min((uint32_t)kBlendThreads, end - base);
             for (int q = 0; q < cnt; ++q) {
-                const float2 c2 = s2[q];
-                const uint32_t m = __float_as_uint(c2.y);
-                if ((m & pix) != pix) continue;
-                ++n_eval;
-                const float4 a = s0[q];
-                const float4 c = s1[q];
-                const float dx = __fsub_rn(pxf, a.x);
+                const float2 dq = B.d[q];
+                const uint32_t m = __float_as_uint(dq.y);
+                if ((m & wrows) == 0) continue;  // warp-uniform: no row of this warp in the AABB
+                const float4 a = B.a[q];
+                const float4 c = B.c[q];
+                // pinned e2 chain: dy terms once per row, dx terms per pixel
                 const float dy = __fsub_rn(pyf, a.y);
                 const float t1 = __fmul_rn(a.w, dy);
-                const float t2 = __fmaf_rn(a.z, dx, t1);
                 const float t3 = __fmul_rn(c.x, dy);
                 const float t4 = __fmaf_rn(t3, dy, c.y);
-                const float e2 = __fmaf_rn(dx, t2, t4);
-                if (!(e2 >= 0.0f)) continue;
-                const float alpha = fminf(0.99f, ex2_approx(e2) * (1.0f / 255.0f));
-                const float test = T * (1.0f - alpha);
-                if (test < 1e-4f) {
-                    done = true;
-                    break;
-                }
-                const float w = alpha * T;
-                C0 = fmaf(c.z, w, C0);
-                C1 = fmaf(c.w, w, C1);
-                C2 = fmaf(c2.x, w, C2);
-                T = test;
-                ++n_blend;
+                const float2 dx = sub2(px, make_float2(a.x, a.x));
+                const float2 t2 = fma2(make_float2(a.z, a.z), dx, make_float2(t1, t1));
+                const float2 e2 = fma2(dx, t2, make_float2(t4, t4));
+                const bool box0 = (m & pb0) == pb0 && !done0, box1 = (m & pb1) == pb1 && !done1;
+                const bool v0 = box0 && e2.x >= 0.0f, v1 = box1 && e2.y >= 0.0f;
+                if (kCount) n_eval += (uint32_t)box0 + (uint32_t)box1;
+                if (!(v0 || v1)) continue;
+                const float a0 = v0 ? fminf(0.99f, ex2_approx(e2.x) * (1.0f / 255.0f)) : 0.0f;
+                const float a1 = v1 ? fminf(0.99f, ex2_approx(e2.y) * (1.0f / 255.0f)) : 0.0f;
+                float w0 = a0 * T.x, w1 = a1 * T.y;
+                const bool s0 = v0 && (T.x - w0) < 1e-4f, s1 = v1 && (T.y - w1) < 1e-4f;
+                w0 = s0 ? 0.0f : w0;
+                w1 = s1 ? 0.0f : w1;
+                done0 |= s0;
+                done1 |= s1;
+                if (kCount) n_blend += (uint32_t)(v0 && !s0) + (uint32_t)(v1 && !s1);
+                const float2 w = make_float2(w0, w1);
+                T = sub2(T, w);
+                Cr = fma2(make_float2(c.z, c.z), w, Cr);
+                Cg = fma2(make_float2(c.w, c.w), w, Cg);
+                Cb = fma2(make_float2(dq.x, dq.x), w, Cb);
+                if (done0 && done1) break;
             }
         }
-        if (__syncthreads_count(done) == kBlendThreads) break;
+        stage_store(sb[buf ^ 1], tid, nxt + tid, end, tx, ty, r0, r1, r2);
+        buf ^= 1;
+        if (__syncthreads_count(done0 && done1) == kBlendThreads) break;
     }
-    // Eq. 2 work counters (algorithmic pairs), one atomic per warp
+    if (kCount) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        n_eval += __shfl_xor_sync(0xffffffffu, n_eval, o);
-        n_blend += __shfl_xor_sync(0xffffffffu, n_blend, o);
-    }
-    if ((tid & 31) == 0 && n_eval) {
-        atomicAdd(&ctr->n_eval, (unsigned long long)n_eval);
-        atomicAdd(&ctr->n_blend, (unsigned long long)n_blend);
-    }
-    if (stats) {
+        for (int o = 16; o > 0; o >>= 1) {
+            n_eval += __shfl_xor_sync(0xffffffffu, n_eval, o);
+            n_blend += __shfl_xor_sync(0xffffffffu, n_blend, o);
+        }
+        if ((tid & 31) == 0 && n_eval) {
+            atomicAdd(&ctr->n_eval, (unsigned long long)n_eval);
+            atomicAdd(&ctr->n_blend, (unsigned long long)n_blend);
+        }
         __threadfence();
         __syncthreads();
         if (tid == 0) s_last = atomicAdd(&ctr->blend_ticket, 1u) == gridDim.x - 1;
         __syncthreads();
-        if (s_last && tid == 0) {
+        if (s_last && tid == 0 && stats != nullptr) {
             __threadfence();
             volatile Counters *vc = ctr;
             stats->n_act = vc->n_act;
@@ -478,12 +601,18 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restr
         }
     }
     if (!ok) return;
-    if (inside) {
-        const size_t hw = (size_t)width * height, p = (size_t)j * width + i;
-        out_rgb[p] = fmaf(T, bg0, C0);
-        out_rgb[hw + p] = fmaf(T, bg1, C1);
-        out_rgb[2 * hw + p] = fmaf(T, bg2, C2);
-        if (out_T) out_T[p] = T;
+    const size_t hw = (size_t)width * height, p = (size_t)j * width + i0;
+    if (in0) {
+        out_rgb[p] = fmaf(T.x, bg0, Cr.x);
+        out_rgb[hw + p] = fmaf(T.x, bg1, Cg.x);
+        out_rgb[2 * hw + p] = fmaf(T.x, bg2, Cb.x);
+        if (out_T) out_T[p] = T.x;
+    }
+    if (in1) {
+        out_rgb[p + 1] = fmaf(T.y, bg0, Cr.y);
+        out_rgb[hw + p + 1] = fmaf(T.y, bg1, Cg.y);
+        out_rgb[2 * hw + p + 1] = fmaf(T.y, bg2, Cb.y);
+        if (out_T) out_T[p + 1] = T.y;
     }
 }
 
@@ -497,6 +626,8 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     float4 *rec1 = reinterpret_cast<float4 *>(ws + L.rec1);
     float4 *rec2 = reinterpret_cast<float4 *>(ws + L.rec2);
     uint32_t *depth = reinterpret_cast<uint32_t *>(ws + L.depth);
+    uint2 *rect = reinterpret_cast<uint2 *>(ws + L.rect);
+    uint2 *rect_sorted = reinterpret_cast<uint2 *>(ws + L.rect_sorted);
     uint32_t *keys[2] = {reinterpret_cast<uint32_t *>(ws + L.keys0), reinterpret_cast<uint32_t *>(ws + L.keys1)};
     uint32_t *vals[2] = {reinterpret_cast<uint32_t *>(ws + L.vals0), reinterpret_cast<uint32_t *>(ws + L.vals1)};
     uint32_t *shist = reinterpret_cast<uint32_t *>(ws + L.sort_hist);
@@ -510,26 +641,35 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     e = cudaMemsetAsync(ws + L.counters, 0, L.rec0 - L.counters, st);  // counters + look-back
     if (e != cudaSuccess) return e;
     if (L.n_parts > 0)
-        k_preprocess<<<L.n_parts, kPreBlock, 0, st>>>(sc, mask_l, mask_r, cam, t, ctr, lb, rec0, rec1, rec2, depth);
+        k_preprocess<<<L.n_parts, kPreBlock, 0, st>>>(sc, mask_l, mask_r, cam, t, ctr, lb, rec0, rec1, rec2, depth,
+                                                      rect);
     if (ev && (e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
     for (int pass = 0; pass < 4; ++pass) {
         const uint32_t *kin = pass == 0 ? depth : keys[(pass - 1) & 1];
         const uint32_t *vin = pass == 0 ? nullptr : vals[(pass - 1) & 1];
-        k_sort_upsweep<<<L.p_sort, kSortThreads, 0, st>>>(kin, ctr, ctr, pass, shist + (size_t)pass * L.p_sort * 256);
+        uint32_t *h = shist + (size_t)pass * L.p_sort * 256;
+        k_sort_upsweep<<<L.p_sort, kSortThreads, 0, st>>>(kin, ctr, pass, h);
         k_sort_downsweep<<<L.p_sort, kSortThreads, 0, st>>>(kin, vin, pass == 3 ? nullptr : keys[pass & 1],
-                                                             vals[pass & 1], ctr, pass,
-                                                             shist + (size_t)pass * L.p_sort * 256);
+                                                             vals[pass & 1], ctr, pass, h, rect,
+                                                             pass == 3 ? rect_sorted : nullptr);
     }
     const uint32_t *order = vals[1];
     if (ev && (e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
-    k_bin_count<<<L.p_bin, 256, (size_t)L.n_tiles * 4, st>>>(order, rec1, ctr, L.tiles_x, L.n_tiles, bhist);
-    k_bin_colscan<<<(L.n_tiles + 31) / 32, 256, 0, st>>>(bhist, L.p_bin, L.n_tiles, ttot, tstart, ctr, L.max_entries);
+    const size_t cnt_smem = sizeof(int) * (size_t)(L.tiles_x + 1) * (L.tiles_y + 1);
+    k_bin_count<<<L.p_bin, 256, cnt_smem, st>>>(rect_sorted, ctr, L.tiles_x, L.tiles_y, bhist);
+    k_bin_colscan<<<(L.n_tiles + 31) / 32, 1024, 0, st>>>(bhist, L.p_bin, L.n_tiles, ttot, tstart, ctr, L.max_entries);
     const size_t scat_smem = (size_t)L.n_tiles * 4 + (size_t)L.bin_warps * L.n_tiles * 2;
-    k_bin_scatter<<<L.p_bin, 32 * L.bin_warps, scat_smem, st>>>(order, rec1, ctr, L.tiles_x, L.n_tiles, bhist, tstart,
-                                                                 entries);
+    k_bin_scatter<<<L.p_bin, 32 * L.bin_warps, scat_smem, st>>>(order, rect_sorted, ctr, L.tiles_x, L.n_tiles, bhist,
+                                                                 tstart, entries);
     if (ev && (e = cudaEventRecord(ev[3], st)) != cudaSuccess) return e;
-    k_blend<<<L.n_tiles, kBlendThreads, 0, st>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width, L.height,
-                                                 cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T, stats);
+    if (stats != nullptr)
+        k_blend<true><<<L.n_tiles, kBlendThreads, 0, st>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
+                                                           L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T,
+                                                           stats);
+    else
+        k_blend<false><<<L.n_tiles, kBlendThreads, 0, st>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
+                                                            L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T,
+                                                            nullptr);
     if (ev && (e = cudaEventRecord(ev[4], st)) != cudaSuccess) return e;
     return cudaGetLastError();
 }
