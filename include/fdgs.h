@@ -109,7 +109,10 @@ size_t fdgs_scene_validate_workspace_bytes(void);
 fdgs_status fdgs_log255_opacity(const float *d_opacity, int32_t n, float *d_out, void *stream);
 
 /* Workspace bytes of fdgs_render for n Gaussians, a width x height image and
- * room for max_entries (tile, Gaussian) entries. */
+ * room for max_entries (tile, Gaussian) entries.  A render workspace must be
+ * zero-filled (cudaMemset 0) once before its first fdgs_render; it can then be
+ * reused by any number of frames on one stream (its look-back tables are
+ * epoch-tagged). */
 size_t fdgs_render_workspace_bytes(int32_t n, int32_t width, int32_t height, int64_t max_entries);
 
 /* Render one frame at timestamp t (Eq. 1-3) under the key-frame

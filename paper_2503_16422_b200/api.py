@@ -97,7 +97,8 @@ class Renderer:
         nbytes = lib().fdgs_render_workspace_bytes(self.scene.n, self.width, self.height, self.max_entries)
         if nbytes == 0:
             raise ValueError("invalid render size")
-        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.scene.device)
+        # zero-filled once: the epoch-tagged look-back tables require it (include/fdgs.h)
+        self.ws = torch.zeros(nbytes, dtype=torch.uint8, device=self.scene.device)
         self.ws_bytes = nbytes
 
     def _masks(self, mask_l, mask_r):

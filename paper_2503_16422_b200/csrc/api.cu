@@ -51,19 +51,29 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.n_tiles = L.tiles_x * L.tiles_y;
     L.n_parts = (n + kPreBlock - 1) / kPreBlock;
     L.p_sort = sm_count();
-    // u16 per-warp counters in the binning scatter need <= 65535 ranks per block
-    L.p_bin = std::max(sm_count(), (int)((n + 32767) / 32768));
-    L.bin_warps = L.n_tiles <= 8192 ? 8 : 4;
+    L.sort_parts = std::max(1, (n + kDepthTile - 1) / kDepthTile);
+    L.tile_parts = (int32_t)std::max<int64_t>(1, (max_entries + kTileTile - 1) / kTileTile);
     L.max_entries = max_entries;
     const size_t nn = (size_t)std::max(n, 1);
+    const size_t cap = (size_t)std::max<int64_t>(max_entries, 1);
     size_t off = 0;
     auto take = [&](size_t bytes) {
         const size_t o = off;
         off = align256(off + bytes);
         return o;
     };
+    // cleared per frame
     L.counters = take(sizeof(Counters));
     L.lookback = take(sizeof(uint32_t) * (size_t)std::max(L.n_parts, 1));
+    L.sort_gbase = take(sizeof(uint32_t) * 4 * 256);
+    L.tile_diff = take(sizeof(int) * (size_t)(L.tiles_x + 1) * (L.tiles_y + 1));
+    L.emit_lb = take(sizeof(uint32_t) * ((nn + 1023) / 1024));
+    L.zero_end = off;
+    // persistent (zero-filled once)
+    L.epoch = take(sizeof(uint32_t));
+    L.sort_status = take(sizeof(uint64_t) * 4 * 256 * (size_t)L.sort_parts);
+    L.tile_status = take(sizeof(uint64_t) * 2 * 128 * (size_t)L.tile_parts);
+    // per-frame scratch, fully written before read
     L.rec0 = take(16 * nn);
     L.rec1 = take(16 * nn);
     L.rec2 = take(16 * nn);
@@ -74,11 +84,16 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.keys1 = take(4 * nn);
     L.vals0 = take(4 * nn);
     L.vals1 = take(4 * nn);
-    L.sort_hist = take(sizeof(uint32_t) * 4 * 256 * (size_t)L.p_sort);
-    L.bin_hist = take(sizeof(uint32_t) * (size_t)L.p_bin * L.n_tiles);
-    L.tile_total = take(sizeof(uint32_t) * (size_t)L.n_tiles);
+    L.tile_gbase = take(sizeof(uint32_t) * 256);
     L.tile_start = take(sizeof(uint32_t) * ((size_t)L.n_tiles + 1));
-    L.entries = take(sizeof(uint32_t) * (size_t)std::max<int64_t>(max_entries, 1));
+    L.emit_cnt = take(4 * nn);
+    L.emit_off = take(4 * nn);
+    L.chunk_first = take(4 * ((size_t)L.tile_parts + 1));
+    L.ekey0 = take(4 * cap);
+    L.ekey1 = take(4 * cap);
+    L.eval0 = take(4 * cap);
+    L.eval1 = take(4 * cap);
+    L.entries = take(4 * cap);
     L.total = off;
     return L;
 }

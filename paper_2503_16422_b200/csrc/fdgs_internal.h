@@ -10,6 +10,9 @@
 namespace fdgs {
 
 constexpr int kPreBlock = 256;         // Gaussians per preprocess partition
+constexpr int kDepthTile = 1024;       // keys per depth-sort partition (256 threads x 4)
+constexpr int kTileSortItems = 8;      // entries per thread in the tile passes
+constexpr int kTileTile = 256 * kTileSortItems;
 constexpr uint32_t kFlagA = 1u << 30;  // look-back: aggregate available
 constexpr uint32_t kFlagP = 2u << 30;  // look-back: inclusive prefix available
 constexpr uint32_t kValMask = (1u << 30) - 1;
@@ -18,10 +21,12 @@ constexpr uint32_t kValMask = (1u << 30) - 1;
 struct Counters {
     uint32_t n_act, n_vis, n_entries, status;  // mirrors fdgs_frame_stats
     uint32_t part_ticket;
-    uint32_t sort_ticket[4];
+    uint32_t sort_ticket[5];  // [0] histogram kernel, [1 + pass] onesweep partitions
     uint32_t bin_ticket;
     uint32_t blend_ticket;
-    uint32_t pad[5];
+    uint32_t tile_ticket[2];
+    uint32_t n_sort_entries;     // E when it fits the capacity, else 0
+    uint32_t pad[1];
     unsigned long long n_eval;   // (pixel, Gaussian) pairs tested before termination
     unsigned long long n_blend;  // pairs composited
     uint32_t pad2[12];
@@ -35,16 +40,21 @@ struct SceneDev {
     const float4 *sh;  // [n][12] float4 = 48 floats
 };
 
-// Workspace layout of fdgs_render (all offsets 256-byte aligned).
+// Workspace layout of fdgs_render (all offsets 256-byte aligned).  The
+// region [counters, zero_end) is cleared per frame; the epoch word and the
+// epoch-tagged look-back tables persist (the workspace must be zero-filled
+// once before first use).
 struct RenderLayout {
     int32_t n, width, height, tiles_x, tiles_y, n_tiles;
-    int32_t n_parts;   // preprocess partitions
-    int32_t p_sort;    // sort partitions
-    int32_t p_bin;     // binning partitions
-    int32_t bin_warps; // warps per binning block
+    int32_t n_parts;     // preprocess partitions
+    int32_t p_sort;      // SM count (grid of the histogram kernels)
+    int32_t sort_parts;  // depth-sort partitions (upper bound from n)
+    int32_t tile_parts;  // tile-sort partitions (upper bound from max_entries)
     int64_t max_entries;
-    size_t counters, lookback, rec0, rec1, rec2, depth, rect, rect_sorted, keys0, keys1, vals0, vals1, sort_hist, bin_hist,
-        tile_total, tile_start, entries, total;
+    size_t counters, lookback, sort_gbase, tile_diff, emit_lb, zero_end;
+    size_t epoch, sort_status, tile_status;
+    size_t rec0, rec1, rec2, depth, rect, rect_sorted, keys0, keys1, vals0, vals1;
+    size_t tile_gbase, tile_start, emit_cnt, emit_off, chunk_first, ekey0, ekey1, eval0, eval1, entries, total;
 };
 RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max_entries);
 

@@ -4,13 +4,15 @@
 //                    (Eq. 1) + temporal marginal (Eq. 3)
 //                    + EWA projection + SH3 colour + order-preserving
 //                    compaction (warp ballot, block scan, decoupled look-back)
-//   k_sort_*         row 5a: stable LSD radix sort (4 x 8-bit) of the fp32 depth
-//                    keys -> canonical (depth, index) order ("sorted by
-//                    their depth", reading R8)
-//   k_bin_*          row 5b: stable counting sort of (tile, canonical rank)
-//                    entries: per-block tile histograms, column scan, scatter
+//   k_sort_*         row 5a: stable onesweep LSD radix sort (4 x 8-bit) of the
+//                    fp32 depth keys -> canonical (depth, index) order (P:126
+//                    "sorted by their depth", reading R8)
+//   k_bin_count..    row 5b: per-tile counts (2D difference array), emission of
+//                    (tile, slot) entries in canonical order, then two stable
+//                    7-bit onesweep passes on the tile id
 //   k_blend          row 6: per-tile front-to-back Eq. 2 with warp-uniform
 //                    early exit
+#include <algorithm>
 #include <cstdio>
 
 #include "fdgs_internal.h"
@@ -124,8 +126,17 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess(SceneDev sc, const uin
     }
 }
 
-// ---------------------------------------------------------------- row 5a
+// ---------------------------------------------------------------- rows 5a/5b
+// Both sorts are stable LSD radix passes in onesweep form: partitions taken in
+// ticket order, within-warp ranks by match_any, per-warp digit counters,
+// per-digit decoupled look-back across partitions.  Look-back status words
+// are 64-bit {epoch:32 | flag:2 | count:30}; the epoch (bumped once per frame)
+// retires the previous frame's words, so no per-frame zeroing is needed.
 constexpr int kSortThreads = 256;
+constexpr uint64_t kStA = 1ull << 30, kStP = 2ull << 30;
+
+__device__ __forceinline__ uint64_t ld_volatile64(const uint64_t *p) { return *(const volatile uint64_t *)p; }
+__device__ __forceinline__ void st_volatile64(uint64_t *p, uint64_t v) { *(volatile uint64_t *)p = v; }
 
 __device__ __forceinline__ void part_range(uint32_t n, int parts, int b, uint32_t &lo, uint32_t &hi) {
     const uint32_t chunk = (n + parts - 1) / parts;
@@ -133,124 +144,148 @@ __device__ __forceinline__ void part_range(uint32_t n, int parts, int b, uint32_
     hi = min(lo + chunk, n);
 }
 
-// Per-partition digit histogram; the last block to finish turns the [P][256]
-// table into global exclusive offsets (digit-major, partition-minor).
-__global__ void __launch_bounds__(kSortThreads) k_sort_upsweep(const uint32_t *__restrict__ keys, Counters *ctr,
-                                                               int pass, uint32_t *__restrict__ hist) {
-    __shared__ uint32_t h[256];
+template <int BITS, int ITEMS>
+struct Onesweep {
+    static constexpr int kDigits = 1 << BITS;
+    static constexpr int kTile = kSortThreads * ITEMS;
+};
+
+// One stable pass over n = *n_ptr keys (digit = (key >> shift) & (2^BITS-1)).
+//   gbase  : exclusive global base of every digit
+//   status : [parts][2^BITS] look-back words (epoch-tagged)
+//   vals_in NULL = identity values; keys_out NULL = do not write keys;
+//   rect_in/rect_out: optional payload gathered through the value (row 5b input).
+template <int BITS, int ITEMS>
+__global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint32_t *__restrict__ keys_in,
+                                                           const uint32_t *__restrict__ vals_in,
+                                                           uint32_t *__restrict__ keys_out,
+                                                           uint32_t *__restrict__ vals_out, const uint32_t *n_ptr,
+                                                           const uint32_t *epoch_ptr, uint32_t *ticket, int shift,
+                                                           const uint32_t *__restrict__ gbase, uint64_t *status,
+                                                           const uint2 *__restrict__ rect_in,
+                                                           uint2 *__restrict__ rect_out) {
+    constexpr int NW = kSortThreads / 32;
+    constexpr int D = 1 << BITS;
+    constexpr int TILE = kSortThreads * ITEMS;
+    constexpr uint32_t MASK = D - 1;
+    __shared__ uint32_t s_w[NW][D];
+    __shared__ uint32_t s_part;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t n = *n_ptr;
+    const uint64_t epoch = (uint64_t)*epoch_ptr << 32;
+    const uint32_t parts = (n + TILE - 1) / TILE;
+    while (true) {  // persistent: partitions are taken in ticket order
+    if (tid == 0) s_part = atomicAdd(ticket, 1u);
+    for (int k = lane; k < D; k += 32) s_w[warp][k] = 0;
+    __syncthreads();
+    const uint32_t part = s_part;
+    if (part >= parts) return;
+    uint32_t key[ITEMS], val[ITEMS], dig[ITEMS], rk[ITEMS];
+    const uint32_t base = part * TILE + warp * (32 * ITEMS);
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const uint32_t i = base + k * 32 + lane;
+        const bool valid = i < n;
+        key[k] = valid ? __ldg(keys_in + i) : 0u;
+        val[k] = valid ? (vals_in ? __ldg(vals_in + i) : i) : 0u;
+        dig[k] = valid ? (key[k] >> shift) & MASK : (uint32_t)D;
+    }
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const uint32_t peers = __match_any_sync(0xffffffffu, dig[k]);
+        const bool leader = (__ffs(peers) - 1) == lane;
+        if (dig[k] < (uint32_t)D) rk[k] = s_w[warp][dig[k]] + __popc(peers & lanemask_lt());
+        __syncwarp();
+        if (leader && dig[k] < (uint32_t)D) s_w[warp][dig[k]] += __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int d = tid; d < D; d += kSortThreads) {
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const uint32_t c = s_w[w][d];
+            s_w[w][d] = tot;
+            tot += c;
+        }
+        uint64_t *st = status + (size_t)part * D + d;
+        uint32_t excl = 0;
+        if (part == 0) {
+            st_volatile64(st, epoch | kStP | tot);
+        } else {
+            st_volatile64(st, epoch | kStA | tot);
+            const uint64_t *p = st - D;
+            while (true) {
+                const uint64_t s = ld_volatile64(p);
+                if ((s & 0xffffffff00000000ull) != epoch || (s & (3ull << 30)) == 0) continue;
+                excl += (uint32_t)(s & kValMask);
+                if ((s & (3ull << 30)) == kStP) break;
+                p -= D;
+            }
+            st_volatile64(st, epoch | kStP | (excl + tot));
+        }
+        const uint32_t gb = __ldg(gbase + d) + excl;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) s_w[w][d] += gb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        if (dig[k] < (uint32_t)D) {
+            const uint32_t pos = s_w[warp][dig[k]] + rk[k];
+            if (keys_out) keys_out[pos] = key[k];
+            vals_out[pos] = val[k];
+            if (rect_out) rect_out[pos] = __ldg(rect_in + val[k]);
+        }
+    }
+    __syncthreads();
+    }
+}
+
+// Row 5a prologue: digit histograms of the four 8-bit depth passes in one
+// read of the keys; the last block turns them into exclusive bases.  Block 0
+// also bumps the per-frame look-back epoch.
+__global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint32_t *__restrict__ keys, Counters *ctr,
+                                                            uint32_t *__restrict__ ghist, uint32_t *epoch) {
+    __shared__ uint32_t h[4][256];
     __shared__ uint32_t s_scan[256];
     __shared__ bool s_last;
-    const int tid = threadIdx.x, P = gridDim.x, b = blockIdx.x;
+    const int tid = threadIdx.x;
     const uint32_t n = ctr->n_vis;
-    const int shift = 8 * pass;
-    uint32_t lo, hi;
-    part_range(n, P, b, lo, hi);
-    h[tid] = 0;
+    if (blockIdx.x == 0 && tid == 0) *epoch = *epoch + 1;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) h[p][tid] = 0;
     __syncthreads();
-    for (uint32_t i = lo + tid; i < hi; i += kSortThreads) atomicAdd(&h[(__ldg(keys + i) >> shift) & 255u], 1u);
+    for (uint32_t i = blockIdx.x * blockDim.x + tid; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t k = __ldg(keys + i);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255u], 1u);
+    }
     __syncthreads();
-    hist[(size_t)b * 256 + tid] = h[tid];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+        if (h[p][tid]) atomicAdd(&ghist[p * 256 + tid], h[p][tid]);
     __threadfence();
     __syncthreads();
-    if (tid == 0) s_last = atomicAdd(&ctr->sort_ticket[pass], 1u) == (uint32_t)P - 1;
+    if (tid == 0) s_last = atomicAdd(&ctr->sort_ticket[0], 1u) == gridDim.x - 1;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    // digit tid: total over partitions (L2 loads, pipelined), block scan over
-    // digits, then per-partition running offsets.
-    uint32_t tot = 0;
-    int p = 0;
-    for (; p + 8 <= P; p += 8) {
-        uint32_t c[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) c[k] = __ldcg(&hist[(size_t)(p + k) * 256 + tid]);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) tot += c[k];
-    }
-    for (; p < P; ++p) tot += __ldcg(&hist[(size_t)p * 256 + tid]);
-    s_scan[tid] = tot;
-    __syncthreads();
-    for (int off = 1; off < 256; off <<= 1) {
-        const uint32_t v = tid >= off ? s_scan[tid - off] : 0;
+    for (int p = 0; p < 4; ++p) {
+        const uint32_t c = __ldcg(&ghist[p * 256 + tid]);
+        s_scan[tid] = c;
         __syncthreads();
-        s_scan[tid] += v;
-        __syncthreads();
-    }
-    uint32_t run = s_scan[tid] - tot;
-    for (p = 0; p + 8 <= P; p += 8) {
-        uint32_t c[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) c[k] = __ldcg(&hist[(size_t)(p + k) * 256 + tid]);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            hist[(size_t)(p + k) * 256 + tid] = run;
-            run += c[k];
+        for (int off = 1; off < 256; off <<= 1) {
+            const uint32_t v = tid >= off ? s_scan[tid - off] : 0;
+            __syncthreads();
+            s_scan[tid] += v;
+            __syncthreads();
         }
-    }
-    for (; p < P; ++p) {
-        const uint32_t c = __ldcg(&hist[(size_t)p * 256 + tid]);
-        hist[(size_t)p * 256 + tid] = run;
-        run += c;
-    }
-}
-
-// Stable scatter: 256-item tiles, within-warp ranks by match_any, cross-warp
-// prefix per digit in shared memory.  The last pass also gathers the packed
-// pixel AABB of each Gaussian into canonical order (rect_out) for binning.
-__global__ void __launch_bounds__(kSortThreads) k_sort_downsweep(const uint32_t *__restrict__ keys_in,
-                                                                 const uint32_t *__restrict__ vals_in,
-                                                                 uint32_t *__restrict__ keys_out,
-                                                                 uint32_t *__restrict__ vals_out, const Counters *ctrc,
-                                                                 int pass, const uint32_t *__restrict__ hist,
-                                                                 const uint2 *__restrict__ rect_in,
-                                                                 uint2 *__restrict__ rect_out) {
-    constexpr int NW = kSortThreads / 32;
-    __shared__ uint32_t s_off[256];
-    __shared__ uint32_t s_w[NW][256];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, P = gridDim.x, b = blockIdx.x;
-    const uint32_t n = ctrc->n_vis;
-    const int shift = 8 * pass;
-    uint32_t lo, hi;
-    part_range(n, P, b, lo, hi);
-    if (lo >= hi) return;
-    s_off[tid] = hist[(size_t)b * 256 + tid];
-    for (uint32_t base = lo; base < hi; base += kSortThreads) {
-        const uint32_t i = base + tid;
-        const bool valid = i < hi;
-        const uint32_t key = valid ? __ldg(keys_in + i) : 0u;
-        const uint32_t val = valid ? (vals_in ? __ldg(vals_in + i) : i) : 0u;
-        uint2 rc = make_uint2(0, 0);
-        if (rect_out != nullptr && valid) rc = __ldg(rect_in + val);
-        const uint32_t d = valid ? (key >> shift) & 255u : 256u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t rank = __popc(peers & lanemask_lt());
-#pragma unroll
-        for (int k = 0; k < 8; ++k) s_w[warp][lane + 32 * k] = 0;
-        __syncwarp();
-        if (valid && (__ffs(peers) - 1) == lane) s_w[warp][d] = __popc(peers);
-        __syncthreads();
-        {
-            uint32_t run = s_off[tid];
-#pragma unroll
-            for (int w = 0; w < NW; ++w) {
-                const uint32_t c = s_w[w][tid];
-                s_w[w][tid] = run;
-                run += c;
-            }
-            s_off[tid] = run;
-        }
-        __syncthreads();
-        if (valid) {
-            const uint32_t pos = s_w[warp][d] + rank;
-            if (keys_out) keys_out[pos] = key;
-            vals_out[pos] = val;
-            if (rect_out) rect_out[pos] = rc;
-        }
+        ghist[p * 256 + tid] = s_scan[tid] - c;
         __syncthreads();
     }
 }
 
-// ---------------------------------------------------------------- row 5b
 // Tile rectangle of a packed pixel AABB (16x16 tiles).
 struct TileRect {
     int tx0, ty0, nx, ny;
@@ -264,94 +299,62 @@ __device__ __forceinline__ TileRect tile_rect(uint2 r) {
     return t;
 }
 
-// Per-partition tile histogram via a 2D difference array: 4 shared atomics per
-// Gaussian, then row and column prefix sums -> hist[b][T].
-__global__ void __launch_bounds__(256) k_bin_count(const uint2 *__restrict__ rects, const Counters *ctrc, int tiles_x,
-                                                   int tiles_y, uint32_t *__restrict__ hist) {
-    extern __shared__ int sh_diff[];  // (tiles_y + 1) x (tiles_x + 1)
-    const int tid = threadIdx.x, P = gridDim.x, b = blockIdx.x;
-    const int gx = tiles_x + 1, gy = tiles_y + 1;
-    for (int k = tid; k < gx * gy; k += blockDim.x) sh_diff[k] = 0;
-    __syncthreads();
-    uint32_t lo, hi;
-    part_range(ctrc->n_vis, P, b, lo, hi);
-    for (uint32_t r = lo + tid; r < hi; r += blockDim.x) {
+// Row 5b (1/5): per-tile entry counts through a global 2D difference array
+// (4 reductions per visible Gaussian) and the per-Gaussian entry counts.
+__global__ void k_bin_count(const uint2 *__restrict__ rects, const Counters *ctrc, int tiles_x,
+                            int *__restrict__ diff, uint32_t *__restrict__ cnt) {
+    const uint32_t n = ctrc->n_vis;
+    const int gx = tiles_x + 1;
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
         const TileRect t = tile_rect(__ldg(rects + r));
         const int x1 = t.tx0 + t.nx, y1 = t.ty0 + t.ny;
-        atomicAdd(&sh_diff[t.ty0 * gx + t.tx0], 1);
-        atomicAdd(&sh_diff[t.ty0 * gx + x1], -1);
-        atomicAdd(&sh_diff[y1 * gx + t.tx0], -1);
-        atomicAdd(&sh_diff[y1 * gx + x1], 1);
+        atomicAdd(&diff[t.ty0 * gx + t.tx0], 1);
+        atomicAdd(&diff[t.ty0 * gx + x1], -1);
+        atomicAdd(&diff[y1 * gx + t.tx0], -1);
+        atomicAdd(&diff[y1 * gx + x1], 1);
+        cnt[r] = (uint32_t)(t.nx * t.ny);
     }
-    __syncthreads();
-    for (int y = tid; y < tiles_y; y += blockDim.x) {  // prefix along x
-        int run = 0;
-        for (int x = 0; x < tiles_x; ++x) {
-            run += sh_diff[y * gx + x];
-            sh_diff[y * gx + x] = run;
-        }
-    }
-    __syncthreads();
-    for (int x = tid; x < tiles_x; x += blockDim.x) {  // prefix along y
-        int run = 0;
-        for (int y = 0; y < tiles_y; ++y) {
-            run += sh_diff[y * gx + x];
-            sh_diff[y * gx + x] = run;
-        }
-    }
-    __syncthreads();
-    const int n_tiles = tiles_x * tiles_y;
-    for (int k = tid; k < n_tiles; k += blockDim.x)
-        hist[(size_t)b * n_tiles + k] = (uint32_t)sh_diff[(k / tiles_x) * gx + (k % tiles_x)];
 }
 
-// Column scan: tile t's exclusive prefix over partitions (in place) and its
-// total; the last block scans the totals into tile_start[0..T] and checks the
-// entry capacity.  Block = 32 tiles x 32 partition slices.
-__global__ void __launch_bounds__(1024) k_bin_colscan(uint32_t *__restrict__ hist, int P, int n_tiles,
-                                                      uint32_t *__restrict__ tile_total,
-                                                      uint32_t *__restrict__ tile_start, Counters *ctr,
-                                                      int64_t max_entries) {
-    __shared__ uint32_t s_part[32][33];
+// Row 5b (2/5), one block: 2D prefix of the difference array -> per-tile
+// counts -> tile_start[0..T] and E (capacity check), and the exclusive digit
+// bases of the two tile passes (low 7 bits, then the high bits).
+__global__ void __launch_bounds__(1024) k_tile_scan(const int *__restrict__ diff, int tiles_x, int tiles_y,
+                                                    uint32_t *__restrict__ tile_start, uint32_t *__restrict__ tbase,
+                                                    Counters *ctr, int64_t max_entries) {
+    extern __shared__ int sm[];  // (tiles_y + 1) x (tiles_x + 1)
     __shared__ uint32_t s_sum[1024];
-    __shared__ bool s_last;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int t = blockIdx.x * 32 + lane;
-    const int per = (P + 31) / 32;
-    const int b0 = min(warp * per, P), b1 = min(b0 + per, P);
-    uint32_t sum = 0;
-    if (t < n_tiles)
-        for (int b = b0; b < b1; ++b) sum += __ldcg(&hist[(size_t)b * n_tiles + t]);
-    s_part[warp][lane] = sum;
+    __shared__ uint32_t s_dig[2][128];
+    const int tid = threadIdx.x;
+    const int gx = tiles_x + 1, gy = tiles_y + 1, T = tiles_x * tiles_y;
+    for (int k = tid; k < gx * gy; k += blockDim.x) sm[k] = __ldcg(diff + k);
+    if (tid < 256) s_dig[tid >> 7][tid & 127] = 0;
     __syncthreads();
-    if (warp == 0) {
-        uint32_t run = 0;
-        for (int w = 0; w < 32; ++w) {
-            const uint32_t c = s_part[w][lane];
-            s_part[w][lane] = run;
-            run += c;
-        }
-        if (t < n_tiles) tile_total[t] = run;
-    }
-    __syncthreads();
-    if (t < n_tiles) {
-        uint32_t run = s_part[warp][lane];
-        for (int b = b0; b < b1; ++b) {
-            const uint32_t c = __ldcg(&hist[(size_t)b * n_tiles + t]);
-            hist[(size_t)b * n_tiles + t] = run;
-            run += c;
+    for (int y = tid; y < tiles_y; y += blockDim.x) {
+        int run = 0;
+        for (int x = 0; x < tiles_x; ++x) {
+            run += sm[y * gx + x];
+            sm[y * gx + x] = run;
         }
     }
-    __threadfence();
     __syncthreads();
-    if (tid == 0) s_last = atomicAdd(&ctr->bin_ticket, 1u) == gridDim.x - 1;
+    for (int x = tid; x < tiles_x; x += blockDim.x) {
+        int run = 0;
+        for (int y = 0; y < tiles_y; ++y) {
+            run += sm[y * gx + x];
+            sm[y * gx + x] = run;
+        }
+    }
     __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    const int chunk = (n_tiles + 1023) / 1024;
-    const int k0 = min(tid * chunk, n_tiles), k1 = min(k0 + chunk, n_tiles);
+    const int chunk = (T + 1023) / 1024;
+    const int k0 = min(tid * chunk, T), k1 = min(k0 + chunk, T);
     uint32_t local = 0;
-    for (int k = k0; k < k1; ++k) local += __ldcg(&tile_total[k]);
+    for (int k = k0; k < k1; ++k) {
+        const uint32_t c = (uint32_t)sm[(k / tiles_x) * gx + (k % tiles_x)];
+        local += c;
+        atomicAdd(&s_dig[0][k & 127], c);
+        atomicAdd(&s_dig[1][k >> 7], c);
+    }
     s_sum[tid] = local;
     __syncthreads();
     for (int off = 1; off < 1024; off <<= 1) {
@@ -363,80 +366,114 @@ __global__ void __launch_bounds__(1024) k_bin_colscan(uint32_t *__restrict__ his
     uint32_t run = s_sum[tid] - local;
     for (int k = k0; k < k1; ++k) {
         tile_start[k] = run;
-        run += __ldcg(&tile_total[k]);
+        run += (uint32_t)sm[(k / tiles_x) * gx + (k % tiles_x)];
+    }
+    if (tid < 2) {  // digit bases of the two tile passes
+        uint32_t acc = 0;
+        for (int d = 0; d < 128; ++d) {
+            tbase[tid * 128 + d] = acc;
+            acc += s_dig[tid][d];
+        }
     }
     if (tid == 1023) {
         const uint32_t E = s_sum[1023];
-        tile_start[n_tiles] = E;
+        tile_start[T] = E;
         ctr->n_entries = E;
         if ((int64_t)E > max_entries) ctr->status = FDGS_ERR_OVERFLOW;
+        else ctr->n_sort_entries = E;
     }
 }
 
-// Stable scatter of entries.  Warp w owns a contiguous sub-range of the
-// block's canonical ranks and walks it in order with warp-private u16 tile
-// counters; each round loads 32 rects at once and broadcasts them by shuffle.
-__global__ void k_bin_scatter(const uint32_t *__restrict__ order, const uint2 *__restrict__ rects,
-                              const Counters *ctrc, int tiles_x, int n_tiles, const uint32_t *__restrict__ hist,
-                              const uint32_t *__restrict__ tile_start, uint32_t *__restrict__ entries) {
-    extern __shared__ uint32_t sh_base[];  // [n_tiles] u32 global base, then [NW][n_tiles] u16
-    const int NW = blockDim.x >> 5;
-    uint16_t *cnt = reinterpret_cast<uint16_t *>(sh_base + n_tiles);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, P = gridDim.x, b = blockIdx.x;
+// Row 5b (3/5): exclusive scan of the per-Gaussian entry counts in canonical
+// order (single pass, warp look-back) -> emission offsets.
+__global__ void __launch_bounds__(1024) k_emit_scan(const uint32_t *__restrict__ cnt, const Counters *ctrc,
+                                                    uint32_t *ticket, uint32_t *lb, uint32_t *__restrict__ off,
+                                                    uint32_t *__restrict__ chunk_first) {
+    __shared__ uint32_t s_w[32];
+    __shared__ uint32_t s_part, s_excl;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t n = ctrc->n_vis;
+    if (tid == 0) s_part = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t part = s_part;
+    if (part * 1024 >= n) return;
+    const uint32_t i = part * 1024 + tid;
+    const uint32_t c = i < n ? __ldg(cnt + i) : 0u;
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = s_w[lane], wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        s_w[lane] = wi - w;
+        const uint32_t tot = __shfl_sync(0xffffffffu, wi, 31);
+        const uint32_t excl = lookback_warp(lb, part, tot, lane);
+        if (lane == 0) s_excl = excl;
+    }
+    __syncthreads();
+    if (i < n) {
+        const uint32_t o = s_excl + s_w[warp] + incl - c;
+        off[i] = o;
+        // first Gaussian of every emission chunk that starts inside [o, o + c)
+        for (uint32_t k = (o + kTileTile - 1) / kTileTile; k * kTileTile < o + c; ++k) chunk_first[k] = i;
+    }
+}
+
+// Row 5b (4/5): emission in canonical order: (tile id, visible slot) for every
+// tile of every Gaussian's rectangle, Gaussian-major, tiles row-major.  One
+// block per chunk of kTileTile entries (load-balanced, coalesced stores): the
+// chunk's Gaussians are staged in shared memory and each entry finds its
+// Gaussian by binary search there.
+constexpr int kEmitWin = 1024;  // Gaussians staged per window
+__global__ void __launch_bounds__(256) k_emit(const uint2 *__restrict__ rects, const uint32_t *__restrict__ order,
+                                              const uint32_t *__restrict__ off,
+                                              const uint32_t *__restrict__ chunk_first, const Counters *ctrc,
+                                              int tiles_x, uint32_t *__restrict__ ekey, uint32_t *__restrict__ eval) {
+    __shared__ uint32_t s_off[kEmitWin];
+    __shared__ uint2 s_rect[kEmitWin];
+    __shared__ uint32_t s_v[kEmitWin];
+    const int tid = threadIdx.x;
     if (ctrc->status != FDGS_OK) return;
-    uint32_t lo, hi;
-    part_range(ctrc->n_vis, P, b, lo, hi);
-    if (lo >= hi) return;
-    for (int k = tid; k < n_tiles * NW; k += blockDim.x) cnt[k] = 0;
-    __syncthreads();
-    const uint32_t per = (hi - lo + NW - 1) / NW;
-    const uint32_t w0 = min(lo + warp * per, hi), w1 = min(w0 + per, hi);
-    uint16_t *my = cnt + warp * n_tiles;
-    for (uint32_t r0 = w0; r0 < w1; r0 += 32) {
-        const uint32_t r = r0 + lane;
-        const uint2 rc = r < w1 ? __ldg(rects + r) : make_uint2(0, 0);
-        const int m = min(32u, w1 - r0);
-        for (int j = 0; j < m; ++j) {
-            const uint2 q = make_uint2(__shfl_sync(0xffffffffu, rc.x, j), __shfl_sync(0xffffffffu, rc.y, j));
-            const TileRect t = tile_rect(q);
-            for (int e = lane; e < t.nx * t.ny; e += 32) {
-                const int ty = t.ty0 + e / t.nx, tx = t.tx0 + e % t.nx;
-                my[ty * tiles_x + tx] += 1;
+    const uint32_t n = ctrc->n_vis, E = ctrc->n_sort_entries;
+    const uint32_t chunks = (E + kTileTile - 1) / kTileTile;
+    for (uint32_t k = blockIdx.x; k < chunks; k += gridDim.x) {
+        const uint32_t e0 = k * kTileTile, e1 = min(e0 + kTileTile, E);
+        uint32_t r0 = __ldg(chunk_first + k);
+        uint32_t e = e0;
+        while (e < e1) {  // windows of kEmitWin Gaussians (one window unless Gaussians have 1-2 tiles)
+            const uint32_t m = min((uint32_t)kEmitWin, n - r0);
+            for (uint32_t q = tid; q < m; q += blockDim.x) {
+                s_off[q] = __ldg(off + r0 + q);
+                s_rect[q] = __ldg(rects + r0 + q);
+                s_v[q] = __ldg(order + r0 + q);
             }
-            __syncwarp();
-        }
-    }
-    __syncthreads();
-    for (int k = tid; k < n_tiles; k += blockDim.x) {
-        sh_base[k] = __ldg(tile_start + k) + __ldg(hist + (size_t)b * n_tiles + k);
-        uint16_t run = 0;
-        for (int w = 0; w < NW; ++w) {
-            const uint16_t c = cnt[w * n_tiles + k];
-            cnt[w * n_tiles + k] = run;
-            run = (uint16_t)(run + c);
-        }
-    }
-    __syncthreads();
-    for (uint32_t r0 = w0; r0 < w1; r0 += 32) {
-        const uint32_t r = r0 + lane;
-        uint2 rc = make_uint2(0, 0);
-        uint32_t v = 0;
-        if (r < w1) {
-            rc = __ldg(rects + r);
-            v = __ldg(order + r);
-        }
-        const int m = min(32u, w1 - r0);
-        for (int j = 0; j < m; ++j) {
-            const uint2 q = make_uint2(__shfl_sync(0xffffffffu, rc.x, j), __shfl_sync(0xffffffffu, rc.y, j));
-            const uint32_t vj = __shfl_sync(0xffffffffu, v, j);
-            const TileRect t = tile_rect(q);
-            for (int e = lane; e < t.nx * t.ny; e += 32) {
-                const int tile = (t.ty0 + e / t.nx) * tiles_x + t.tx0 + e % t.nx;
-                const uint32_t pos = sh_base[tile] + my[tile];
-                my[tile] += 1;
-                entries[pos] = vj;
+            __syncthreads();
+            const uint32_t wend = (r0 + m < n) ? min(e1, __ldg(off + r0 + m)) : e1;
+            for (uint32_t i = e + tid; i < wend; i += blockDim.x) {
+                // largest q with s_off[q] <= i
+                int lo = 0, hi = (int)m - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (s_off[mid] <= i) lo = mid; else hi = mid - 1;
+                }
+                const TileRect t = tile_rect(s_rect[lo]);
+                const int kk = (int)(i - s_off[lo]);
+                const int qy = __float2int_rz(((float)kk + 0.5f) / (float)t.nx);
+                ekey[i] = (uint32_t)((t.ty0 + qy) * tiles_x + t.tx0 + (kk - qy * t.nx));
+                eval[i] = s_v[lo];
             }
-            __syncwarp();
+            __syncthreads();
+            e = wend;
+            r0 += m;
         }
     }
 }
@@ -630,37 +667,54 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     uint2 *rect_sorted = reinterpret_cast<uint2 *>(ws + L.rect_sorted);
     uint32_t *keys[2] = {reinterpret_cast<uint32_t *>(ws + L.keys0), reinterpret_cast<uint32_t *>(ws + L.keys1)};
     uint32_t *vals[2] = {reinterpret_cast<uint32_t *>(ws + L.vals0), reinterpret_cast<uint32_t *>(ws + L.vals1)};
-    uint32_t *shist = reinterpret_cast<uint32_t *>(ws + L.sort_hist);
-    uint32_t *bhist = reinterpret_cast<uint32_t *>(ws + L.bin_hist);
-    uint32_t *ttot = reinterpret_cast<uint32_t *>(ws + L.tile_total);
     uint32_t *tstart = reinterpret_cast<uint32_t *>(ws + L.tile_start);
     uint32_t *entries = reinterpret_cast<uint32_t *>(ws + L.entries);
 
     cudaError_t e = cudaSuccess;
     if (ev && (e = cudaEventRecord(ev[0], st)) != cudaSuccess) return e;
-    e = cudaMemsetAsync(ws + L.counters, 0, L.rec0 - L.counters, st);  // counters + look-back
+    e = cudaMemsetAsync(ws + L.counters, 0, L.zero_end - L.counters, st);  // counters, look-back, histograms
     if (e != cudaSuccess) return e;
     if (L.n_parts > 0)
         k_preprocess<<<L.n_parts, kPreBlock, 0, st>>>(sc, mask_l, mask_r, cam, t, ctr, lb, rec0, rec1, rec2, depth,
                                                       rect);
     if (ev && (e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
+    uint32_t *gbase = reinterpret_cast<uint32_t *>(ws + L.sort_gbase);  // [4][256] depth digit bases
+    uint32_t *epoch = reinterpret_cast<uint32_t *>(ws + L.epoch);
+    uint64_t *sstat = reinterpret_cast<uint64_t *>(ws + L.sort_status);
+    k_sort_hist<<<L.p_sort, kSortThreads, 0, st>>>(depth, ctr, gbase, epoch);
+    constexpr int kDItems = 4;
     for (int pass = 0; pass < 4; ++pass) {
         const uint32_t *kin = pass == 0 ? depth : keys[(pass - 1) & 1];
         const uint32_t *vin = pass == 0 ? nullptr : vals[(pass - 1) & 1];
-        uint32_t *h = shist + (size_t)pass * L.p_sort * 256;
-        k_sort_upsweep<<<L.p_sort, kSortThreads, 0, st>>>(kin, ctr, pass, h);
-        k_sort_downsweep<<<L.p_sort, kSortThreads, 0, st>>>(kin, vin, pass == 3 ? nullptr : keys[pass & 1],
-                                                             vals[pass & 1], ctr, pass, h, rect,
-                                                             pass == 3 ? rect_sorted : nullptr);
+        k_onesweep<8, kDItems><<<std::min(L.sort_parts, 4 * L.p_sort), kSortThreads, 0, st>>>(
+            kin, vin, pass == 3 ? nullptr : keys[pass & 1], vals[pass & 1], &ctr->n_vis, epoch,
+            &ctr->sort_ticket[1 + pass], 8 * pass, gbase + 256 * pass,
+            sstat + (size_t)pass * L.sort_parts * 256, rect, pass == 3 ? rect_sorted : nullptr);
     }
     const uint32_t *order = vals[1];
     if (ev && (e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
-    const size_t cnt_smem = sizeof(int) * (size_t)(L.tiles_x + 1) * (L.tiles_y + 1);
-    k_bin_count<<<L.p_bin, 256, cnt_smem, st>>>(rect_sorted, ctr, L.tiles_x, L.tiles_y, bhist);
-    k_bin_colscan<<<(L.n_tiles + 31) / 32, 1024, 0, st>>>(bhist, L.p_bin, L.n_tiles, ttot, tstart, ctr, L.max_entries);
-    const size_t scat_smem = (size_t)L.n_tiles * 4 + (size_t)L.bin_warps * L.n_tiles * 2;
-    k_bin_scatter<<<L.p_bin, 32 * L.bin_warps, scat_smem, st>>>(order, rect_sorted, ctr, L.tiles_x, L.n_tiles, bhist,
-                                                                 tstart, entries);
+    int *diff = reinterpret_cast<int *>(ws + L.tile_diff);
+    uint32_t *tbase = reinterpret_cast<uint32_t *>(ws + L.tile_gbase);
+    uint32_t *ecnt = reinterpret_cast<uint32_t *>(ws + L.emit_cnt);
+    uint32_t *eoff = reinterpret_cast<uint32_t *>(ws + L.emit_off);
+    uint32_t *elb = reinterpret_cast<uint32_t *>(ws + L.emit_lb);
+    uint32_t *ek[2] = {reinterpret_cast<uint32_t *>(ws + L.ekey0), reinterpret_cast<uint32_t *>(ws + L.ekey1)};
+    uint32_t *evl[2] = {reinterpret_cast<uint32_t *>(ws + L.eval0), reinterpret_cast<uint32_t *>(ws + L.eval1)};
+    uint64_t *tstat = reinterpret_cast<uint64_t *>(ws + L.tile_status);
+    const int grid_v = std::max(1, std::min((L.n + 255) / 256, 8 * L.p_sort));
+    constexpr int kTItems = kTileSortItems;
+    k_bin_count<<<grid_v, 256, 0, st>>>(rect_sorted, ctr, L.tiles_x, diff, ecnt);
+    const size_t scan_smem = sizeof(int) * (size_t)(L.tiles_x + 1) * (L.tiles_y + 1);
+    k_tile_scan<<<1, 1024, scan_smem, st>>>(diff, L.tiles_x, L.tiles_y, tstart, tbase, ctr, L.max_entries);
+    uint32_t *cfirst = reinterpret_cast<uint32_t *>(ws + L.chunk_first);
+    k_emit_scan<<<std::max(1, (L.n + 1023) / 1024), 1024, 0, st>>>(ecnt, ctr, &ctr->bin_ticket, elb, eoff, cfirst);
+    const int pgrid = 4 * L.p_sort;  // persistent grids
+    k_emit<<<pgrid, 256, 0, st>>>(rect_sorted, order, eoff, cfirst, ctr, L.tiles_x, ek[0], evl[0]);
+    k_onesweep<7, kTItems><<<pgrid, kSortThreads, 0, st>>>(ek[0], evl[0], ek[1], evl[1], &ctr->n_sort_entries, epoch,
+                                                           &ctr->tile_ticket[0], 0, tbase, tstat, nullptr, nullptr);
+    k_onesweep<7, kTItems><<<pgrid, kSortThreads, 0, st>>>(ek[1], evl[1], nullptr, entries, &ctr->n_sort_entries,
+                                                           epoch, &ctr->tile_ticket[1], 7, tbase + 128,
+                                                           tstat + (size_t)L.tile_parts * 128, nullptr, nullptr);
     if (ev && (e = cudaEventRecord(ev[3], st)) != cudaSuccess) return e;
     if (stats != nullptr)
         k_blend<true><<<L.n_tiles, kBlendThreads, 0, st>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
@@ -676,9 +730,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
 
 // Opt-in to large dynamic shared memory once per process.
 __host__ cudaError_t render_set_smem_attrs() {
-    cudaError_t e = cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    return cudaFuncSetAttribute(k_tile_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
 }
 
 }  // namespace fdgs
