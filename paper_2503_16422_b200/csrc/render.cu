@@ -214,13 +214,25 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint32_t *__res
             st_volatile64(st, epoch | kStP | tot);
         } else {
             st_volatile64(st, epoch | kStA | tot);
-            const uint64_t *p = st - D;
-            while (true) {
-                const uint64_t s = ld_volatile64(p);
-                if ((s & 0xffffffff00000000ull) != epoch || (s & (3ull << 30)) == 0) continue;
-                excl += (uint32_t)(s & kValMask);
-                if ((s & (3ull << 30)) == kStP) break;
-                p -= D;
+            // windowed look-back: 8 predecessors per round trip, nearest first
+            int q = (int)part - 1;
+            bool found = false;
+            while (!found) {
+                uint64_t w[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    w[k] = q - k >= 0 ? ld_volatile64(status + (size_t)(q - k) * D + d) : (epoch | kStP);
+                int k = 0;
+                for (; k < 8; ++k) {
+                    const uint64_t s = w[k];
+                    if ((s & 0xffffffff00000000ull) != epoch || (s & (3ull << 30)) == 0) break;  // not yet published
+                    excl += (uint32_t)(s & kValMask);
+                    if ((s & (3ull << 30)) == kStP) {
+                        found = true;
+                        break;
+                    }
+                }
+                q -= k;  // resume at the first unpublished predecessor
             }
             st_volatile64(st, epoch | kStP | (excl + tot));
         }
@@ -536,6 +548,14 @@ __device__ __forceinline__ void stage_store(BlendBatch &B, int tid, uint32_t k, 
     }
 }
 
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    float2 d;
+    asm("mul.rn.f32x2 %0, %1, %2;"
+        : "=l"(*reinterpret_cast<unsigned long long *>(&d))
+        : "l"(*reinterpret_cast<unsigned long long *>(&a)), "l"(*reinterpret_cast<unsigned long long *>(&b)));
+    return d;
+}
+
 template <bool kCount>
 __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restrict__ tile_start,
                                                          const uint32_t *__restrict__ entries,
@@ -558,8 +578,11 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restr
     const float2 px = make_float2((float)i0 + 0.5f, (float)(i0 + 1) + 0.5f);
     const uint32_t pb0 = (1u << lx) | (1u << (16 + ly)), pb1 = (2u << lx) | (1u << (16 + ly));
     const uint32_t wrows = 0xFu << (16 + 4 * warp);  // this warp's 4 rows in the y-mask
+    const float kInf = __int_as_float(0x7f800000);
+    // eligibility threshold on e2: 0 while the pixel is live, +inf once it is
+    // outside the image or terminated (e2 is finite, so e2 >= +inf is false)
+    float2 thr = make_float2(in0 ? 0.0f : kInf, in1 ? 0.0f : kInf);
     float2 T = make_float2(1.0f, 1.0f), Cr = make_float2(0.f, 0.f), Cg = Cr, Cb = Cr;
-    bool done0 = !in0, done1 = !in1;
     uint32_t n_eval = 0, n_blend = 0;
     const uint32_t first = ok ? start : end;
     float4 r0, r1, r2;
@@ -571,7 +594,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restr
         const uint32_t nxt = base + kBlendThreads;
         stage_load(entries, rec0, rec1, rec2, nxt + tid, end, r0, r1, r2);  // prefetch the next batch
         const BlendBatch &B = sb[buf];
-        if (!(done0 && done1)) {
+        if (!__all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf)) {
             const int cnt = (int)min((uint32_t)kBlendThreads, end - base);
             for (int q = 0; q < cnt; ++q) {
                 const float2 dq = B.d[q];
@@ -587,30 +610,29 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restr
                 const float2 dx = sub2(px, make_float2(a.x, a.x));
                 const float2 t2 = fma2(make_float2(a.z, a.z), dx, make_float2(t1, t1));
                 const float2 e2 = fma2(dx, t2, make_float2(t4, t4));
-                const bool box0 = (m & pb0) == pb0 && !done0, box1 = (m & pb1) == pb1 && !done1;
-                const bool v0 = box0 && e2.x >= 0.0f, v1 = box1 && e2.y >= 0.0f;
-                if (kCount) n_eval += (uint32_t)box0 + (uint32_t)box1;
+                const bool box0 = (m & pb0) == pb0, box1 = (m & pb1) == pb1;
+                const bool v0 = box0 && e2.x >= thr.x, v1 = box1 && e2.y >= thr.y;
+                if (kCount) n_eval += (uint32_t)(box0 && thr.x == 0.0f) + (uint32_t)(box1 && thr.y == 0.0f);
                 if (!(v0 || v1)) continue;
                 const float a0 = v0 ? fminf(0.99f, ex2_approx(e2.x) * (1.0f / 255.0f)) : 0.0f;
                 const float a1 = v1 ? fminf(0.99f, ex2_approx(e2.y) * (1.0f / 255.0f)) : 0.0f;
-                float w0 = a0 * T.x, w1 = a1 * T.y;
-                const bool s0 = v0 && (T.x - w0) < 1e-4f, s1 = v1 && (T.y - w1) < 1e-4f;
-                w0 = s0 ? 0.0f : w0;
-                w1 = s1 ? 0.0f : w1;
-                done0 |= s0;
-                done1 |= s1;
+                float2 w = mul2(make_float2(a0, a1), T);
+                const float2 test = sub2(T, w);
+                const bool s0 = v0 && test.x < 1e-4f, s1 = v1 && test.y < 1e-4f;
+                w.x = s0 ? 0.0f : w.x;
+                w.y = s1 ? 0.0f : w.y;
+                thr.x = s0 ? kInf : thr.x;
+                thr.y = s1 ? kInf : thr.y;
                 if (kCount) n_blend += (uint32_t)(v0 && !s0) + (uint32_t)(v1 && !s1);
-                const float2 w = make_float2(w0, w1);
                 T = sub2(T, w);
                 Cr = fma2(make_float2(c.z, c.z), w, Cr);
                 Cg = fma2(make_float2(c.w, c.w), w, Cg);
                 Cb = fma2(make_float2(dq.x, dq.x), w, Cb);
-                if (done0 && done1) break;
             }
         }
         stage_store(sb[buf ^ 1], tid, nxt + tid, end, tx, ty, r0, r1, r2);
         buf ^= 1;
-        if (__syncthreads_count(done0 && done1) == kBlendThreads) break;
+        if (__syncthreads_count(thr.x == kInf && thr.y == kInf) == kBlendThreads) break;
     }
     if (kCount) {
 #pragma unroll
