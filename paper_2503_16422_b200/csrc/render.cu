@@ -144,17 +144,13 @@ __device__ __forceinline__ void part_range(uint32_t n, int parts, int b, uint32_
     hi = min(lo + chunk, n);
 }
 
-template <int BITS, int ITEMS>
-struct Onesweep {
-    static constexpr int kDigits = 1 << BITS;
-    static constexpr int kTile = kSortThreads * ITEMS;
-};
-
 // One stable pass over n = *n_ptr keys (digit = (key >> shift) & (2^BITS-1)).
 //   gbase  : exclusive global base of every digit
 //   status : [parts][2^BITS] look-back words (epoch-tagged)
 //   vals_in NULL = identity values; keys_out NULL = do not write keys;
 //   rect_in/rect_out: optional payload gathered through the value (row 5b input).
+// The partition is reordered by digit in shared memory first, so the global
+// stores are contiguous runs per digit (coalesced) instead of 4-byte scatters.
 template <int BITS, int ITEMS>
 __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint32_t *__restrict__ keys_in,
                                                            const uint32_t *__restrict__ vals_in,
@@ -169,6 +165,9 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint32_t *__res
     constexpr int TILE = kSortThreads * ITEMS;
     constexpr uint32_t MASK = D - 1;
     __shared__ uint32_t s_w[NW][D];
+    __shared__ uint32_t s_lbase[D];   // block-local exclusive base of each digit
+    __shared__ uint32_t s_gofs[D];    // global position of the digit's first key in this partition
+    __shared__ uint32_t s_key[TILE], s_val[TILE];
     __shared__ uint32_t s_part;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t n = *n_ptr;
@@ -200,14 +199,45 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint32_t *__res
         __syncwarp();
     }
     __syncthreads();
-    for (int d = tid; d < D; d += kSortThreads) {
-        uint32_t tot = 0;
+    // per digit: prefix over warps, block total, block-local base (scan over
+    // digits), then the look-back for the global offset
+    uint32_t tot_d[(D + kSortThreads - 1) / kSortThreads];
 #pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            const uint32_t c = s_w[w][d];
-            s_w[w][d] = tot;
-            tot += c;
+    for (int c = 0; c * kSortThreads < D; ++c) {
+        const int d = c * kSortThreads + tid;
+        uint32_t tot = 0;
+        if (d < D) {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const uint32_t x = s_w[w][d];
+                s_w[w][d] = tot;
+                tot += x;
+            }
+            s_lbase[d] = tot;
         }
+        tot_d[c] = tot;
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the digit totals (D <= 256)
+        uint32_t run = 0;
+        for (int c0 = 0; c0 < D; c0 += 32) {
+            const uint32_t x = c0 + lane < D ? s_lbase[c0 + lane] : 0u;
+            uint32_t inc = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (c0 + lane < D) s_lbase[c0 + lane] = run + inc - x;
+            run += __shfl_sync(0xffffffffu, inc, 31);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c * kSortThreads < D; ++c) {
+        const int d = c * kSortThreads + tid;
+        if (d >= D) continue;
+        const uint32_t tot = tot_d[c];
         uint64_t *st = status + (size_t)part * D + d;
         uint32_t excl = 0;
         if (part == 0) {
@@ -224,10 +254,10 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint32_t *__res
                     w[k] = q - k >= 0 ? ld_volatile64(status + (size_t)(q - k) * D + d) : (epoch | kStP);
                 int k = 0;
                 for (; k < 8; ++k) {
-                    const uint64_t s = w[k];
-                    if ((s & 0xffffffff00000000ull) != epoch || (s & (3ull << 30)) == 0) break;  // not yet published
-                    excl += (uint32_t)(s & kValMask);
-                    if ((s & (3ull << 30)) == kStP) {
+                    const uint64_t sv = w[k];
+                    if ((sv & 0xffffffff00000000ull) != epoch || (sv & (3ull << 30)) == 0) break;
+                    excl += (uint32_t)(sv & kValMask);
+                    if ((sv & (3ull << 30)) == kStP) {
                         found = true;
                         break;
                     }
@@ -236,19 +266,26 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint32_t *__res
             }
             st_volatile64(st, epoch | kStP | (excl + tot));
         }
-        const uint32_t gb = __ldg(gbase + d) + excl;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) s_w[w][d] += gb;
+        s_gofs[d] = __ldg(gbase + d) + excl;
     }
-    __syncthreads();
+    // local reorder by digit (stable), then contiguous global runs
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
         if (dig[k] < (uint32_t)D) {
-            const uint32_t pos = s_w[warp][dig[k]] + rk[k];
-            if (keys_out) keys_out[pos] = key[k];
-            vals_out[pos] = val[k];
-            if (rect_out) rect_out[pos] = __ldg(rect_in + val[k]);
+            const uint32_t li = s_lbase[dig[k]] + s_w[warp][dig[k]] + rk[k];
+            s_key[li] = key[k];
+            s_val[li] = val[k];
         }
+    }
+    __syncthreads();
+    const uint32_t cnt = min((uint32_t)TILE, n - part * TILE);
+    for (uint32_t li = tid; li < cnt; li += kSortThreads) {
+        const uint32_t kk = s_key[li], vv = s_val[li];
+        const uint32_t d = (kk >> shift) & MASK;
+        const uint32_t pos = s_gofs[d] + (li - s_lbase[d]);
+        if (keys_out) keys_out[pos] = kk;
+        vals_out[pos] = vv;
+        if (rect_out) rect_out[pos] = __ldg(rect_in + vv);
     }
     __syncthreads();
     }
@@ -311,24 +348,7 @@ __device__ __forceinline__ TileRect tile_rect(uint2 r) {
     return t;
 }
 
-// Row 5b (1/5): per-tile entry counts through a global 2D difference array
-// (4 reductions per visible Gaussian) and the per-Gaussian entry counts.
-__global__ void k_bin_count(const uint2 *__restrict__ rects, const Counters *ctrc, int tiles_x,
-                            int *__restrict__ diff, uint32_t *__restrict__ cnt) {
-    const uint32_t n = ctrc->n_vis;
-    const int gx = tiles_x + 1;
-    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-        const TileRect t = tile_rect(__ldg(rects + r));
-        const int x1 = t.tx0 + t.nx, y1 = t.ty0 + t.ny;
-        atomicAdd(&diff[t.ty0 * gx + t.tx0], 1);
-        atomicAdd(&diff[t.ty0 * gx + x1], -1);
-        atomicAdd(&diff[y1 * gx + t.tx0], -1);
-        atomicAdd(&diff[y1 * gx + x1], 1);
-        cnt[r] = (uint32_t)(t.nx * t.ny);
-    }
-}
-
-// Row 5b (2/5), one block: 2D prefix of the difference array -> per-tile
+// Row 5b (2/4), one block: 2D prefix of the difference array -> per-tile
 // counts -> tile_start[0..T] and E (capacity check), and the exclusive digit
 // bases of the two tile passes (low 7 bits, then the high bits).
 __global__ void __launch_bounds__(1024) k_tile_scan(const int *__restrict__ diff, int tiles_x, int tiles_y,
@@ -396,11 +416,14 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const int *__restrict__ diff
     }
 }
 
-// Row 5b (3/5): exclusive scan of the per-Gaussian entry counts in canonical
-// order (single pass, warp look-back) -> emission offsets.
-__global__ void __launch_bounds__(1024) k_emit_scan(const uint32_t *__restrict__ cnt, const Counters *ctrc,
-                                                    uint32_t *ticket, uint32_t *lb, uint32_t *__restrict__ off,
-                                                    uint32_t *__restrict__ chunk_first) {
+// Row 5b (1/4): per-Gaussian entry counts nx*ny in canonical order -> their
+// exclusive scan (single pass, warp look-back) = emission offsets, the first
+// Gaussian of every emission chunk, and the per-tile counts through a global
+// 2D difference array (4 reductions per visible Gaussian).
+__global__ void __launch_bounds__(1024) k_bin_scan(const uint2 *__restrict__ rects, const Counters *ctrc,
+                                                   int tiles_x, uint32_t *ticket, uint32_t *lb,
+                                                   int *__restrict__ diff, uint32_t *__restrict__ off,
+                                                   uint32_t *__restrict__ chunk_first, uint32_t max_chunks) {
     __shared__ uint32_t s_w[32];
     __shared__ uint32_t s_part, s_excl;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -410,7 +433,16 @@ __global__ void __launch_bounds__(1024) k_emit_scan(const uint32_t *__restrict__
     const uint32_t part = s_part;
     if (part * 1024 >= n) return;
     const uint32_t i = part * 1024 + tid;
-    const uint32_t c = i < n ? __ldg(cnt + i) : 0u;
+    uint32_t c = 0;
+    if (i < n) {
+        const TileRect t = tile_rect(__ldg(rects + i));
+        const int gx = tiles_x + 1, x1 = t.tx0 + t.nx, y1 = t.ty0 + t.ny;
+        atomicAdd(&diff[t.ty0 * gx + t.tx0], 1);
+        atomicAdd(&diff[t.ty0 * gx + x1], -1);
+        atomicAdd(&diff[y1 * gx + t.tx0], -1);
+        atomicAdd(&diff[y1 * gx + x1], 1);
+        c = (uint32_t)(t.nx * t.ny);
+    }
     uint32_t incl = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -436,11 +468,12 @@ __global__ void __launch_bounds__(1024) k_emit_scan(const uint32_t *__restrict__
         const uint32_t o = s_excl + s_w[warp] + incl - c;
         off[i] = o;
         // first Gaussian of every emission chunk that starts inside [o, o + c)
-        for (uint32_t k = (o + kTileTile - 1) / kTileTile; k * kTileTile < o + c; ++k) chunk_first[k] = i;
+        for (uint32_t k = (o + kTileTile - 1) / kTileTile; k * kTileTile < o + c && k < max_chunks; ++k)
+            chunk_first[k] = i;
     }
 }
 
-// Row 5b (4/5): emission in canonical order: (tile id, visible slot) for every
+// Row 5b (3/4): emission in canonical order: (tile id, visible slot) for every
 // tile of every Gaussian's rectangle, Gaussian-major, tiles row-major.  One
 // block per chunk of kTileTile entries (load-balanced, coalesced stores): the
 // chunk's Gaussians are staged in shared memory and each entry finds its
@@ -520,7 +553,7 @@ constexpr int kBlendThreads = 128;  // one 16x16 tile, 2 horizontally adjacent p
 struct BlendBatch {
     float4 a[kBlendThreads];  // u, v, A', B'
     float4 c[kBlendThreads];  // C', Q2, r, g
-    float2 d[kBlendThreads];  // b, tile-local AABB mask (x bits 0-15, y bits 16-31)
+    float4 d[kBlendThreads];  // b, pixel-AABB mask (x bits 0-15, y bits 16-31), reached rows (bits 16-31), -
 };
 
 __device__ __forceinline__ void stage_load(const uint32_t *__restrict__ entries, const float4 *__restrict__ rec0,
@@ -534,6 +567,13 @@ __device__ __forceinline__ void stage_load(const uint32_t *__restrict__ entries,
     }
 }
 
+// Stage one splat record for the tile.  Besides the pixel-AABB mask (the
+// per-pixel decision), a refined row mask culls whole warps: row r is kept only
+// if the ellipse {e2 >= -margin} reaches the row's segment of pixel centres
+// (the concave quadratic's maximum over the segment, at the clamped argmax).
+// This is pure culling: the margin (1e-3 relative to the quadratic's
+// magnitude, + 1e-3) exceeds the rounding of both this test and the pinned
+// fp32 e2 chain, so no pixel with e2 >= 0 is dropped.
 __device__ __forceinline__ void stage_store(BlendBatch &B, int tid, uint32_t k, uint32_t end, int tx, int ty,
                                             const float4 &r0, const float4 &r1, const float4 &r2) {
     if (k < end) {
@@ -542,9 +582,21 @@ __device__ __forceinline__ void stage_store(BlendBatch &B, int tid, uint32_t k, 
         const int y0 = max((int)(ay & 0xffff) - ty * 16, 0), y1 = min((int)(ay >> 16) - ty * 16, 15);
         const uint32_t xm = ((2u << x1) - 1u) & ~((1u << x0) - 1u);
         const uint32_t ym = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
+        uint32_t yr = 0;
+        const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
+        const float dxl = (float)(tx * 16 + x0) + 0.5f - u, dxr = (float)(tx * 16 + x1) + 0.5f - u;
+        const float dxm = fmaxf(fabsf(dxl), fabsf(dxr));
+        const float hA = -0.5f / Ap;  // A' < 0
+        for (int r = y0; r <= y1; ++r) {
+            const float dy = (float)(ty * 16 + r) + 0.5f - v;
+            const float dx = fminf(fmaxf(Bp * dy * hA, dxl), dxr);
+            const float f = fmaf(dx, fmaf(Ap, dx, Bp * dy), fmaf(Cp * dy, dy, Q2));
+            const float mag = fabsf(Ap) * dxm * dxm + fabsf(Bp) * dxm * fabsf(dy) + fabsf(Cp) * dy * dy;
+            if (f >= -(1e-3f * mag + 1e-3f)) yr |= 1u << r;
+        }
         B.a[tid] = r0;
         B.c[tid] = make_float4(r1.x, r1.y, r2.x, r2.y);
-        B.d[tid] = make_float2(r2.z, __uint_as_float(xm | (ym << 16)));
+        B.d[tid] = make_float4(r2.z, __uint_as_float(xm | (ym << 16)), __uint_as_float(yr << 16), 0.0f);
     }
 }
 
@@ -570,6 +622,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restr
     const bool ok = ctr->status == FDGS_OK;
     const int tile = blockIdx.x, tx = tile % tiles_x, ty = tile / tiles_x;
     const int tid = threadIdx.x, warp = tid >> 5;
+    // warp w owns rows 4w..4w+3; thread: row tid >> 3, columns 2*(tid & 7) + {0,1}
     const int ly = tid >> 3, lx = (tid & 7) * 2;
     const int i0 = tx * 16 + lx, j = ty * 16 + ly;
     const bool in0 = i0 < width && j < height, in1 = i0 + 1 < width && j < height;
@@ -577,7 +630,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restr
     const float pyf = (float)j + 0.5f;
     const float2 px = make_float2((float)i0 + 0.5f, (float)(i0 + 1) + 0.5f);
     const uint32_t pb0 = (1u << lx) | (1u << (16 + ly)), pb1 = (2u << lx) | (1u << (16 + ly));
-    const uint32_t wrows = 0xFu << (16 + 4 * warp);  // this warp's 4 rows in the y-mask
+    const uint32_t wrows = 0xFu << (16 + 4 * warp);  // this warp's 4 rows
     const float kInf = __int_as_float(0x7f800000);
     // eligibility threshold on e2: 0 while the pixel is live, +inf once it is
     // outside the image or terminated (e2 is finite, so e2 >= +inf is false)
@@ -597,9 +650,11 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restr
         if (!__all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf)) {
             const int cnt = (int)min((uint32_t)kBlendThreads, end - base);
             for (int q = 0; q < cnt; ++q) {
-                const float2 dq = B.d[q];
+                const float4 dq = B.d[q];
                 const uint32_t m = __float_as_uint(dq.y);
-                if ((m & wrows) == 0) continue;  // warp-uniform: no row of this warp in the AABB
+                if (kCount)  // algorithmic work: pairs in the pixel AABB of live pixels
+                    n_eval += (uint32_t)((m & pb0) == pb0 && thr.x == 0.0f) + (uint32_t)((m & pb1) == pb1 && thr.y == 0.0f);
+                if ((__float_as_uint(dq.z) & wrows) == 0) continue;  // warp-uniform: ellipse misses these rows
                 const float4 a = B.a[q];
                 const float4 c = B.c[q];
                 // pinned e2 chain: dy terms once per row, dx terms per pixel
@@ -612,7 +667,6 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restr
                 const float2 e2 = fma2(dx, t2, make_float2(t4, t4));
                 const bool box0 = (m & pb0) == pb0, box1 = (m & pb1) == pb1;
                 const bool v0 = box0 && e2.x >= thr.x, v1 = box1 && e2.y >= thr.y;
-                if (kCount) n_eval += (uint32_t)(box0 && thr.x == 0.0f) + (uint32_t)(box1 && thr.y == 0.0f);
                 if (!(v0 || v1)) continue;
                 const float a0 = v0 ? fminf(0.99f, ex2_approx(e2.x) * (1.0f / 255.0f)) : 0.0f;
                 const float a1 = v1 ? fminf(0.99f, ex2_approx(e2.y) * (1.0f / 255.0f)) : 0.0f;
@@ -717,19 +771,17 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     if (ev && (e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
     int *diff = reinterpret_cast<int *>(ws + L.tile_diff);
     uint32_t *tbase = reinterpret_cast<uint32_t *>(ws + L.tile_gbase);
-    uint32_t *ecnt = reinterpret_cast<uint32_t *>(ws + L.emit_cnt);
     uint32_t *eoff = reinterpret_cast<uint32_t *>(ws + L.emit_off);
     uint32_t *elb = reinterpret_cast<uint32_t *>(ws + L.emit_lb);
     uint32_t *ek[2] = {reinterpret_cast<uint32_t *>(ws + L.ekey0), reinterpret_cast<uint32_t *>(ws + L.ekey1)};
     uint32_t *evl[2] = {reinterpret_cast<uint32_t *>(ws + L.eval0), reinterpret_cast<uint32_t *>(ws + L.eval1)};
     uint64_t *tstat = reinterpret_cast<uint64_t *>(ws + L.tile_status);
-    const int grid_v = std::max(1, std::min((L.n + 255) / 256, 8 * L.p_sort));
     constexpr int kTItems = kTileSortItems;
-    k_bin_count<<<grid_v, 256, 0, st>>>(rect_sorted, ctr, L.tiles_x, diff, ecnt);
+    uint32_t *cfirst = reinterpret_cast<uint32_t *>(ws + L.chunk_first);
+    k_bin_scan<<<std::max(1, (L.n + 1023) / 1024), 1024, 0, st>>>(rect_sorted, ctr, L.tiles_x, &ctr->bin_ticket, elb,
+                                                                   diff, eoff, cfirst, (uint32_t)L.tile_parts);
     const size_t scan_smem = sizeof(int) * (size_t)(L.tiles_x + 1) * (L.tiles_y + 1);
     k_tile_scan<<<1, 1024, scan_smem, st>>>(diff, L.tiles_x, L.tiles_y, tstart, tbase, ctr, L.max_entries);
-    uint32_t *cfirst = reinterpret_cast<uint32_t *>(ws + L.chunk_first);
-    k_emit_scan<<<std::max(1, (L.n + 1023) / 1024), 1024, 0, st>>>(ecnt, ctr, &ctr->bin_ticket, elb, eoff, cfirst);
     const int pgrid = 4 * L.p_sort;  // persistent grids
     k_emit<<<pgrid, 256, 0, st>>>(rect_sorted, order, eoff, cfirst, ctr, L.tiles_x, ek[0], evl[0]);
     k_onesweep<7, kTItems><<<pgrid, kSortThreads, 0, st>>>(ek[0], evl[0], ek[1], evl[1], &ctr->n_sort_entries, epoch,

@@ -48,6 +48,17 @@ def test_c1_full_frame_parity(t):
     assert_rgb_parity(img, orc)
     assert np.abs(T.reshape(-1) - orc["T"]).max() < 2e-4
     assert stats.n_act == scene.n and stats.n_vis == orc["stats"]["n_vis"]
+    # Eq. 2 work counters of the counting blend variant = the oracle's counts
+    # (pairs in the pixel AABB before termination / pairs composited), up to
+    # knife-edge pixels
+    sc = fd.Scene.from_arrays(scene)
+    rr = fd.Renderer(sc, cam.width, cam.height)
+    st = torch.zeros(4, dtype=torch.int64, device="cuda")
+    rr.render(cam, t, stats=st)
+    s_np = st.cpu().numpy()
+    knife = orc["stats"]["knife"]
+    assert abs(int(s_np[2]) - orc["stats"]["evaluated"]) <= 64 * knife
+    assert abs(int(s_np[3]) - orc["stats"]["blended"]) <= 64 * knife
 
 
 # ------------------------------------------------------- reduced configs
