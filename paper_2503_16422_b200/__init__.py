@@ -6,6 +6,7 @@ include/fdgs.h, with this thin ctypes binding.  See DESIGN.md.
 """
 from .api import (  # noqa: F401
     FrameStats,
+    RenderPipeline,
     Renderer,
     Scene,
     bracket,

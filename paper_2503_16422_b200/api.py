@@ -179,6 +179,38 @@ class Renderer:
         return self.ws[off:off + nbytes]
 
 
+class RenderPipeline:
+    """Frame-pipelined rendering of a sequence: `depth` independent workspaces on
+    `depth` CUDA streams, frame k on stream k mod depth.  The latency-bound
+    front end of one frame (preprocess, sorts, binning) overlaps the ALU-bound
+    blend of the previous one; each frame is still one fdgs_render call."""
+
+    def __init__(self, scene: Scene, width: int, height: int, depth: int = 2, max_entries: int | None = None):
+        self.renderers = [Renderer(scene, width, height, max_entries) for _ in range(depth)]
+        self.streams = [torch.cuda.Stream(device=scene.device) for _ in range(depth)]
+        self.depth = depth
+
+    def render_many(self, frames, outs, stats=None, stage_events=None, stream=None):
+        """frames: list of (cam, t, mask_l, mask_r); outs: list of output tensors.
+        Ordered after the current work of `stream` (default: current stream), and
+        `stream` waits for every frame before continuing.  Async."""
+        main = stream or torch.cuda.current_stream()
+        start = torch.cuda.Event()
+        start.record(main)
+        for s in self.streams:
+            s.wait_event(start)
+        for k, (cam, t, ml, mr) in enumerate(frames):
+            i = k % self.depth
+            self.renderers[i].render(cam, t, ml, mr, out=outs[k], stats=None if stats is None else stats[k],
+                                     stream=self.streams[i],
+                                     stage_events=None if stage_events is None else stage_events[k])
+        for s in self.streams:
+            e = torch.cuda.Event()
+            e.record(s)
+            main.wait_event(e)
+        return outs
+
+
 # ----------------------------------------------------------- other entries
 def validate(scene: Scene, stream=None):
     ws = torch.empty(lib().fdgs_scene_validate_workspace_bytes(), dtype=torch.uint8, device=scene.device)

@@ -266,3 +266,26 @@ def test_extrapolated_time_and_bad_camera():
     sc = fd.Scene.from_arrays(scene)
     with pytest.raises(fd.FdgsError):
         fd.Renderer(sc, 64, 64).render(bad, 0.5)
+
+
+def test_render_pipeline_matches_sequential():
+    """Frame pipelining over 3 streams/workspaces gives the sequential frames bit for bit."""
+    n, W, H, f = 30_000, 300, 200, 220.0
+    scene = fi.make_scene("c3", n=n)
+    cams = fi.make_cameras("c3", width=W, height=H, fx=f, count=4)
+    sc = fd.Scene.from_arrays(scene)
+    kf = fd.keyframes(300, 20)
+    times = fi.frame_times(300)
+    masks = [fd.keyframe_mask(sc, cams, float(times[k])) for k in kf]
+    frames = []
+    for fr in range(100, 124):
+        l, r = fd.bracket(kf, fr)
+        frames.append((cams[fr % 4], float(times[fr]), masks[l], masks[r]))
+    pipe = fd.RenderPipeline(sc, W, H, depth=3)
+    outs = [pipe.renderers[0].new_output() for _ in frames]
+    pipe.render_many(frames, outs)
+    torch.cuda.synchronize()
+    seq = fd.Renderer(sc, W, H)
+    for (cam, t, ml, mr), o in zip(frames, outs):
+        ref, _ = seq.render_checked(cam, t, ml, mr)
+        assert torch.equal(ref, o)
