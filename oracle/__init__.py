@@ -19,6 +19,7 @@ from .oracle import (  # noqa: F401
     render_image,
     canonical_order,
     tile_lists,
+    band_tiles,
     keyframe_mask,
     keyframes,
     bracket,

@@ -406,9 +406,81 @@ int or_canonical_order(const or_scene *S, const uint32_t *mask, const or_camera 
     return nv;
 }
 
+/* Tile cover of one visible Gaussian in tile row ty.
+ * The pixel columns of row band ty that the m-inflated ellipse
+ * {e2(dx,dy) = A'dx^2 + B'dxdy + C'dy^2 + Q2 >= -m} can reach, computed in
+ * binary64 from the binary32 record fields, intersected with the pixel AABB:
+ * the band is empty iff it misses the ellipse's y-range; else the x-extent over
+ * the band comes from the extreme points (dx = +-sqrt(-4C'Qm/K), K = 4A'C' -
+ * B'^2) when their dy lies in the band, else from the roots at the band edge
+ * nearest to them.  Returns 0 (empty) or 1 with tiles [*txa, *txb].  The margin
+ * m = 2^-12 (|A'|X^2 + |B'|XY + |C'|Y^2) + 2^-10 exceeds the rounding of the
+ * pinned fp32 e2 chain, so every pixel with e2 >= 0 lies in a covered tile. */
+int or_band_tiles(const float *f32, int px0, int px1, int py0, int py1, int ty, int *txa, int *txb)
+{
+    const double u = f32[0], v = f32[1], Ap = f32[2], Bp = f32[3], Cp = f32[4], Q2 = f32[5];
+    int ja = 16 * ty, jb = 16 * ty + 15;
+    if (ja < py0) ja = py0;
+    if (jb > py1) jb = py1;
+    if (ja > jb) return 0;
+    const double dya = ((double)ja + 0.5) - v, dyb = ((double)jb + 0.5) - v;
+    const double X = fmax(fabs(((double)px0 + 0.5) - u), fabs(((double)px1 + 0.5) - u));
+    const double Y = fmax(fabs(dya), fabs(dyb));
+    double mag = fabs(Ap) * X;
+    mag = mag * X;
+    double t = fabs(Bp) * X;
+    mag = fma(t, Y, mag);
+    t = fabs(Cp) * Y;
+    mag = fma(t, Y, mag);
+    const double m = fma(mag, 0x1p-12, 0x1p-10);
+    const double Qm = Q2 + m;
+    double K = 4.0 * Ap;
+    K = K * Cp;
+    K = fma(-Bp, Bp, K);                         /* 4A'C' - B'^2 > 0 */
+    const double dxm = sqrt(((-4.0 * Cp) * Qm) / K);
+    const double dym = sqrt(((-4.0 * Ap) * Qm) / K);
+    if (dyb < -dym || dya > dym) return 0;       /* band misses the y-range */
+    const double dyr = -(Bp * dxm) / (2.0 * Cp);  /* dy of the rightmost point */
+    const double i2a = 0.5 / Ap;
+    double xr, xl;
+    if (dyr >= dya && dyr <= dyb) {
+        xr = dxm;
+    } else {
+        const double dy = dyr < dya ? dya : dyb;
+        const double b = Bp * dy;
+        double c = Cp * dy;
+        c = fma(c, dy, Qm);
+        double D = b * b;
+        D = fma(-4.0 * Ap, c, D);
+        D = D > 0.0 ? D : 0.0;
+        xr = (-b - sqrt(D)) * i2a;
+    }
+    const double dyl = -dyr;                       /* dy of the leftmost point */
+    if (dyl >= dya && dyl <= dyb) {
+        xl = -dxm;
+    } else {
+        const double dy = dyl < dya ? dya : dyb;
+        const double b = Bp * dy;
+        double c = Cp * dy;
+        c = fma(c, dy, Qm);
+        double D = b * b;
+        D = fma(-4.0 * Ap, c, D);
+        D = D > 0.0 ? D : 0.0;
+        xl = (-b + sqrt(D)) * i2a;
+    }
+    double ca = ceil((u + xl) - 0.5), cb = floor((u + xr) - 0.5);
+    if (ca < (double)px0) ca = (double)px0;
+    if (cb > (double)px1) cb = (double)px1;
+    if (ca > cb) return 0;
+    *txa = ((int)ca) >> 4;
+    *txb = ((int)cb) >> 4;
+    return 1;
+}
+
 /* Exported: per-tile lists (16x16 tiles, tile id = ty*ceil(W/16)+tx) in
  * canonical order: each visible Gaussian appended, in canonical order, to
- * every tile its pixel AABB intersects.  ranges[2*tile] = [start, end). */
+ * every tile of its tile cover (or_band_tiles per tile row of its pixel
+ * AABB).  ranges[2*tile] = [start, end). */
 int64_t or_tile_lists(const or_scene *S, const uint32_t *mask, const or_camera *cam, float t,
                       int64_t *ranges, int32_t *ids, int64_t cap)
 {
@@ -417,15 +489,20 @@ int64_t or_tile_lists(const or_scene *S, const uint32_t *mask, const or_camera *
     const int tw = (cam->width + 15) / 16, th = (cam->height + 15) / 16, nt = tw * th;
     int64_t *cnt = (int64_t *)calloc((size_t)nt, sizeof(int64_t));
     for (int j = 0; j < nv; ++j)
-        for (int ty = vis[j].py0 / 16; ty <= vis[j].py1 / 16; ++ty)
-            for (int tx = vis[j].px0 / 16; tx <= vis[j].px1 / 16; ++tx) cnt[ty * tw + tx]++;
+        for (int ty = vis[j].py0 / 16; ty <= vis[j].py1 / 16; ++ty) {
+            int a, b;
+            if (!or_band_tiles(vis[j].f32, vis[j].px0, vis[j].px1, vis[j].py0, vis[j].py1, ty, &a, &b)) continue;
+            for (int tx = a; tx <= b; ++tx) cnt[ty * tw + tx]++;
+        }
     int64_t total = 0;
     for (int k = 0; k < nt; ++k) { ranges[2 * k] = total; total += cnt[k]; ranges[2 * k + 1] = total; cnt[k] = ranges[2 * k]; }
     if (total <= cap)
         for (int j = 0; j < nv; ++j)
-            for (int ty = vis[j].py0 / 16; ty <= vis[j].py1 / 16; ++ty)
-                for (int tx = vis[j].px0 / 16; tx <= vis[j].px1 / 16; ++tx)
-                    ids[cnt[ty * tw + tx]++] = vis[j].stage;
+            for (int ty = vis[j].py0 / 16; ty <= vis[j].py1 / 16; ++ty) {
+                int a, b;
+                if (!or_band_tiles(vis[j].f32, vis[j].px0, vis[j].px1, vis[j].py0, vis[j].py1, ty, &a, &b)) continue;
+                for (int tx = a; tx <= b; ++tx) ids[cnt[ty * tw + tx]++] = vis[j].stage;
+            }
     free(cnt);
     free(vis);
     return total;

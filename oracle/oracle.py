@@ -61,6 +61,8 @@ def load():
             lib.or_mask_or.argtypes = [P, P, C.c_int32, P]
             lib.or_rotor4.argtypes = [P, P, P]
             lib.or_sh_basis.argtypes = [P, P]
+            lib.or_band_tiles.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P]
+            lib.or_band_tiles.restype = C.c_int
             lib.or_num_threads.restype = C.c_int
             _lib = lib
     return _lib
@@ -168,6 +170,16 @@ def tile_lists(scene, cam, t, mask=None, cap=None):
                            ids.ctypes.data, ids.shape[0])
     assert E2 == E
     return ranges, ids[:E].copy()
+
+
+def band_tiles(f32, rect, ty):
+    """Tile cover of one Gaussian in tile row ty: (txa, txb) or None."""
+    lib = load()
+    f = np.ascontiguousarray(f32, np.float32)
+    a, b = C.c_int(), C.c_int()
+    ok = lib.or_band_tiles(f.ctypes.data, int(rect[0]), int(rect[1]), int(rect[2]), int(rect[3]), int(ty),
+                           C.byref(a), C.byref(b))
+    return (a.value, b.value) if ok else None
 
 
 def keyframe_mask(scene, cams, t_key):

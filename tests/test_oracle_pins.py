@@ -455,7 +455,17 @@ def test_active_set_union_dominance():
 
 
 # ------------------------------------------------------------ tile lists
+def _q_exact(f32, i, j):
+    """The e2 quadratic in binary64 at pixel centre (i+.5, j+.5) (exact-ish)."""
+    u, v, A, B, C, Q = (float(x) for x in f32)
+    dx, dy = i + 0.5 - u, j + 0.5 - v
+    return A * dx * dx + B * dx * dy + C * dy * dy + Q
+
+
 def test_tile_lists_brute_force():
+    """Tile lists: canonical order, a subset of the
+    AABB tiles, covering every pixel whose e2 quadratic is >= 0 (brute force
+    over all pixels in binary64), and strictly tighter than the AABB."""
     scene = fi.make_scene("c1", n=500, seed=4)
     cam = fi.make_cameras("c1", width=72, height=56, fx=60.0)[0]
     for t in (0.0, 0.5):
@@ -464,16 +474,54 @@ def test_tile_lists_brute_force():
         order = oracle.canonical_order(scene, cam, t)
         assert np.all(rec["stage"][order] == oracle.ST_VISIBLE)
         tw, th = (cam.width + 15) // 16, (cam.height + 15) // 16
-        E = 0
+        E_aabb = 0
         for ty in range(th):
             for tx in range(tw):
                 x0, x1, y0, y1 = 16 * tx, 16 * tx + 15, 16 * ty, 16 * ty + 15
-                want = [g for g in order if rec["rect"][g, 0] <= x1 and rec["rect"][g, 1] >= x0
+                aabb = [g for g in order if rec["rect"][g, 0] <= x1 and rec["rect"][g, 1] >= x0
                         and rec["rect"][g, 2] <= y1 and rec["rect"][g, 3] >= y0]
+                E_aabb += len(aabb)
                 k = ty * tw + tx
-                assert list(ids[ranges[k, 0]:ranges[k, 1]]) == want
-                E += len(want)
-        assert E == ids.size
+                got = list(ids[ranges[k, 0]:ranges[k, 1]])
+                assert set(got) <= set(aabb)                          # subset of the AABB tiles
+                assert got == [g for g in aabb if g in set(got)]      # canonical order
+                for g in aabb:                                        # coverage of every e2 >= 0 pixel
+                    if g in set(got):
+                        continue
+                    px0, px1, py0, py1 = rec["rect"][g]
+                    for j in range(max(y0, py0), min(y1, py1) + 1):
+                        for i in range(max(x0, px0), min(x1, px1) + 1):
+                            assert _q_exact(rec["f32"][g], i, j) < -1e-6, (g, i, j)
+        assert ids.size < E_aabb                                       # the cover is tighter than the AABB
         # canonical order = ascending (depth bits, index)
         keys = [(int(rec["depth_bits"][g]), int(g)) for g in order]
         assert keys == sorted(keys)
+
+
+def test_band_tiles_closed_form():
+    """An axis-aligned isotropic splat: the cover of each band is the set of
+    tiles the closed-form disc (radius sqrt(-Q2/A')) reaches, inflated by the
+    margin only."""
+    cam = fi.make_cameras("c1", width=129, height=129, fx=64.0)[0]
+    cam.cx = cam.cy = 64.5
+    sc = fi.isotropic_scene([[0, 0, 0.0, 0.5]], [[0.6, 0.6, 0.6, 0.3]], [0.9])
+    rec = oracle.records(sc, cam, 0.5)
+    f32 = rec["f32"][0]
+    u, v, A = float(f32[0]), float(f32[1]), float(f32[2])
+    Q = float(f32[5])
+    r = math.sqrt(-Q / A)                                  # e2 >= 0 disc radius (pixels)
+    px0, px1, py0, py1 = rec["rect"][0]
+    for ty in range(py0 // 16, py1 // 16 + 1):
+        band = oracle.band_tiles(f32, rec["rect"][0], ty)
+        ja, jb = max(16 * ty, py0), min(16 * ty + 15, py1)
+        dy = min(abs(ja + 0.5 - v), abs(jb + 0.5 - v)) if not (ja + 0.5 <= v <= jb + 0.5) else 0.0
+        if dy > r + 0.05:
+            assert band is None
+            continue
+        assert band is not None
+        half = math.sqrt(max(r * r - dy * dy, 0.0))
+        lo, hi = math.ceil(u - half - 0.5), math.floor(u + half - 0.5)
+        lo, hi = max(lo, px0), min(hi, px1)
+        if lo <= hi:
+            assert band[0] <= lo // 16 and band[1] >= hi // 16         # covers the disc's columns
+        assert band[0] >= (lo - 2) // 16 and band[1] <= (hi + 2) // 16  # and not much more
