@@ -406,26 +406,18 @@ int or_canonical_order(const or_scene *S, const uint32_t *mask, const or_camera 
     return nv;
 }
 
-/* Tile cover of one visible Gaussian in tile row ty.
- * The pixel columns of row band ty that the m-inflated ellipse
- * {e2(dx,dy) = A'dx^2 + B'dxdy + C'dy^2 + Q2 >= -m} can reach, computed in
- * binary64 from the binary32 record fields, intersected with the pixel AABB:
- * the band is empty iff it misses the ellipse's y-range; else the x-extent over
- * the band comes from the extreme points (dx = +-sqrt(-4C'Qm/K), K = 4A'C' -
- * B'^2) when their dy lies in the band, else from the roots at the band edge
- * nearest to them.  Returns 0 (empty) or 1 with tiles [*txa, *txb].  The margin
- * m = 2^-12 (|A'|X^2 + |B'|XY + |C'|Y^2) + 2^-10 exceeds the rounding of the
- * pinned fp32 e2 chain, so every pixel with e2 >= 0 lies in a covered tile. */
-int or_band_tiles(const float *f32, int px0, int px1, int py0, int py1, int ty, int *txa, int *txb)
+/* Tile cover of a visible Gaussian.  Per Gaussian,
+ * in binary64 from the binary32 record fields: the margin m = 2^-12 (|A'|X^2 +
+ * |B'|XY + |C'|Y^2) + 2^-10 over its pixel AABB (X, Y the largest |dx|, |dy|),
+ * Qm = Q2 + m, K = 4A'C' - B'^2 > 0, the half extents dxm = sqrt(-4C'Qm/K),
+ * dym = sqrt(-4A'Qm/K) of the m-inflated ellipse e2 >= -m, the dy of its
+ * rightmost point dyr = -B'dxm/(2C') (leftmost: -dyr) and 1/(2A').
+ * c[0..4] = dxm, dym, dyr, i2a, Qm. */
+void or_band_consts(const float *f32, int px0, int px1, int py0, int py1, double *c)
 {
     const double u = f32[0], v = f32[1], Ap = f32[2], Bp = f32[3], Cp = f32[4], Q2 = f32[5];
-    int ja = 16 * ty, jb = 16 * ty + 15;
-    if (ja < py0) ja = py0;
-    if (jb > py1) jb = py1;
-    if (ja > jb) return 0;
-    const double dya = ((double)ja + 0.5) - v, dyb = ((double)jb + 0.5) - v;
     const double X = fmax(fabs(((double)px0 + 0.5) - u), fabs(((double)px1 + 0.5) - u));
-    const double Y = fmax(fabs(dya), fabs(dyb));
+    const double Y = fmax(fabs(((double)py0 + 0.5) - v), fabs(((double)py1 + 0.5) - v));
     double mag = fabs(Ap) * X;
     mag = mag * X;
     double t = fabs(Bp) * X;
@@ -437,37 +429,43 @@ int or_band_tiles(const float *f32, int px0, int px1, int py0, int py1, int ty, 
     double K = 4.0 * Ap;
     K = K * Cp;
     K = fma(-Bp, Bp, K);                         /* 4A'C' - B'^2 > 0 */
-    const double dxm = sqrt(((-4.0 * Cp) * Qm) / K);
-    const double dym = sqrt(((-4.0 * Ap) * Qm) / K);
-    if (dyb < -dym || dya > dym) return 0;       /* band misses the y-range */
-    const double dyr = -(Bp * dxm) / (2.0 * Cp);  /* dy of the rightmost point */
-    const double i2a = 0.5 / Ap;
-    double xr, xl;
-    if (dyr >= dya && dyr <= dyb) {
-        xr = dxm;
-    } else {
-        const double dy = dyr < dya ? dya : dyb;
-        const double b = Bp * dy;
-        double c = Cp * dy;
-        c = fma(c, dy, Qm);
-        double D = b * b;
-        D = fma(-4.0 * Ap, c, D);
-        D = D > 0.0 ? D : 0.0;
-        xr = (-b - sqrt(D)) * i2a;
-    }
-    const double dyl = -dyr;                       /* dy of the leftmost point */
-    if (dyl >= dya && dyl <= dyb) {
-        xl = -dxm;
-    } else {
-        const double dy = dyl < dya ? dya : dyb;
-        const double b = Bp * dy;
-        double c = Cp * dy;
-        c = fma(c, dy, Qm);
-        double D = b * b;
-        D = fma(-4.0 * Ap, c, D);
-        D = D > 0.0 ? D : 0.0;
-        xl = (-b + sqrt(D)) * i2a;
-    }
+    c[0] = sqrt(((-4.0 * Cp) * Qm) / K);
+    c[1] = sqrt(((-4.0 * Ap) * Qm) / K);
+    c[2] = -(Bp * c[0]) / (2.0 * Cp);
+    c[3] = 0.5 / Ap;
+    c[4] = Qm;
+}
+
+/* Tiles [*txa, *txb] of tile row ty reached by the m-inflated ellipse: the
+ * band is empty iff it misses the y-range [-dym, dym]; else the x-extent over
+ * the band is +-dxm where the extreme point's dy lies in the band, else the
+ * root at the band edge nearest to it; pixel columns clamped to the AABB.
+ * Returns 0 if no tile.  The margin exceeds the rounding of the pinned fp32
+ * e2 chain, so every pixel with e2 >= 0 lies in a covered tile. */
+static double or_band_root(const double *c, double Ap, double Bp, double Cp, double dy, double sgn)
+{
+    const double b = Bp * dy;
+    double cc = Cp * dy;
+    cc = fma(cc, dy, c[4]);
+    double D = b * b;
+    D = fma(-4.0 * Ap, cc, D);
+    D = D > 0.0 ? D : 0.0;
+    return sgn > 0.0 ? (-b + sqrt(D)) * c[3] : (-b - sqrt(D)) * c[3];
+}
+
+int or_band_tiles(const float *f32, int px0, int px1, int py0, int py1, const double *c, int ty, int *txa,
+                  int *txb)
+{
+    const double u = f32[0], v = f32[1], Ap = f32[2], Bp = f32[3], Cp = f32[4];
+    int ja = 16 * ty, jb = 16 * ty + 15;
+    if (ja < py0) ja = py0;
+    if (jb > py1) jb = py1;
+    if (ja > jb) return 0;
+    const double dya = ((double)ja + 0.5) - v, dyb = ((double)jb + 0.5) - v;
+    if (dyb < -c[1] || dya > c[1]) return 0;       /* band misses the y-range */
+    const double dyr = c[2], dyl = -c[2];
+    const double xr = (dyr >= dya && dyr <= dyb) ? c[0] : or_band_root(c, Ap, Bp, Cp, dyr < dya ? dya : dyb, -1.0);
+    const double xl = (dyl >= dya && dyl <= dyb) ? -c[0] : or_band_root(c, Ap, Bp, Cp, dyl < dya ? dya : dyb, 1.0);
     double ca = ceil((u + xl) - 0.5), cb = floor((u + xr) - 0.5);
     if (ca < (double)px0) ca = (double)px0;
     if (cb > (double)px1) cb = (double)px1;
@@ -488,10 +486,13 @@ int64_t or_tile_lists(const or_scene *S, const uint32_t *mask, const or_camera *
     or_gauss *vis = or_visible(S, mask, cam, t, &nv, &na);
     const int tw = (cam->width + 15) / 16, th = (cam->height + 15) / 16, nt = tw * th;
     int64_t *cnt = (int64_t *)calloc((size_t)nt, sizeof(int64_t));
+    double *bc = (double *)malloc(sizeof(double) * 5 * (size_t)(nv > 0 ? nv : 1));
+    for (int j = 0; j < nv; ++j) or_band_consts(vis[j].f32, vis[j].px0, vis[j].px1, vis[j].py0, vis[j].py1, bc + 5 * j);
     for (int j = 0; j < nv; ++j)
         for (int ty = vis[j].py0 / 16; ty <= vis[j].py1 / 16; ++ty) {
             int a, b;
-            if (!or_band_tiles(vis[j].f32, vis[j].px0, vis[j].px1, vis[j].py0, vis[j].py1, ty, &a, &b)) continue;
+            if (!or_band_tiles(vis[j].f32, vis[j].px0, vis[j].px1, vis[j].py0, vis[j].py1, bc + 5 * j, ty, &a, &b))
+                continue;
             for (int tx = a; tx <= b; ++tx) cnt[ty * tw + tx]++;
         }
     int64_t total = 0;
@@ -500,9 +501,12 @@ int64_t or_tile_lists(const or_scene *S, const uint32_t *mask, const or_camera *
         for (int j = 0; j < nv; ++j)
             for (int ty = vis[j].py0 / 16; ty <= vis[j].py1 / 16; ++ty) {
                 int a, b;
-                if (!or_band_tiles(vis[j].f32, vis[j].px0, vis[j].px1, vis[j].py0, vis[j].py1, ty, &a, &b)) continue;
+                if (!or_band_tiles(vis[j].f32, vis[j].px0, vis[j].px1, vis[j].py0, vis[j].py1, bc + 5 * j, ty, &a,
+                                   &b))
+                    continue;
                 for (int tx = a; tx <= b; ++tx) ids[cnt[ty * tw + tx]++] = vis[j].stage;
             }
+    free(bc);
     free(cnt);
     free(vis);
     return total;
@@ -511,6 +515,7 @@ int64_t or_tile_lists(const or_scene *S, const uint32_t *mask, const or_camera *
 /* ---------------------------------------------------- per-pixel compositing */
 typedef struct {
     int32_t px0, px1;
+    int32_t txa, txb;      /* tile cover of this row band (-1,-2 if empty) */
     float u, v, Ap, Bp, Cp, Q2;
     double u64, v64, A, B, C, amp, rgb[3];
 } or_cand;
@@ -554,7 +559,7 @@ static void or_composite(const or_cand *cand, int nc, int k0, int i, float pxf, 
     for (int k = k0; k < nc; ++k) {
         const or_cand *c = &cand[k];
         if (i < c->px0 || i > c->px1) continue;
-        if (primary) P->evaluated++;
+        if (primary && (i >> 4) >= c->txa && (i >> 4) <= c->txb) P->evaluated++;  /* work in covered tiles */
         if (!(or_e2(c, pxf, pyf) >= 0.0f)) continue;
         const double dx = px - c->u64, dy = py - c->v64;
         const double power = 0.5 * (c->A * dx * dx + 2.0 * c->B * dx * dy + c->C * dy * dy);
@@ -587,7 +592,8 @@ static void or_composite(const or_cand *cand, int nc, int k0, int i, float pxf, 
  *   rgb[3*k..]   primary branch   C + T*bg
  *   T[k]         primary final transmittance
  *   alt_rgb[OR_MAX_LEAVES*3*k..] alternative admissible results, n_alt[k] of them
- * stats[0]=n_act stats[1]=n_vis stats[2]=evaluated pairs stats[3]=blended
+ * stats[0]=n_act stats[1]=n_vis stats[2]=evaluated pairs (in the pixel AABB and a
+ * covered tile, before termination: the Eq. 2 work) stats[3]=blended
  * stats[4]=knife-edge decisions.  Returns 0. */
 int or_render(const or_scene *S, const uint32_t *mask, const or_camera *cam, float t,
               const int64_t *pix, int64_t n_pix,
@@ -624,6 +630,12 @@ int or_render(const or_scene *S, const uint32_t *mask, const or_camera *cam, flo
                 if (j < g->py0 || j > g->py1) continue;
                 or_cand *c = &cand[nc++];
                 c->px0 = g->px0; c->px1 = g->px1;
+                double bcq[5];
+                or_band_consts(g->f32, g->px0, g->px1, g->py0, g->py1, bcq);
+                if (!or_band_tiles(g->f32, g->px0, g->px1, g->py0, g->py1, bcq, j >> 4, &c->txa, &c->txb)) {
+                    c->txa = -1;
+                    c->txb = -2;
+                }
                 c->u = g->f32[0]; c->v = g->f32[1]; c->Ap = g->f32[2]; c->Bp = g->f32[3]; c->Cp = g->f32[4]; c->Q2 = g->f32[5];
                 c->u64 = g->u; c->v64 = g->v; c->A = g->conic[0]; c->B = g->conic[1]; c->C = g->conic[2];
                 c->amp = g->amp; c->rgb[0] = g->rgb[0]; c->rgb[1] = g->rgb[1]; c->rgb[2] = g->rgb[2];

@@ -61,7 +61,8 @@ def load():
             lib.or_mask_or.argtypes = [P, P, C.c_int32, P]
             lib.or_rotor4.argtypes = [P, P, P]
             lib.or_sh_basis.argtypes = [P, P]
-            lib.or_band_tiles.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P]
+            lib.or_band_consts.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, P]
+            lib.or_band_tiles.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, P, P]
             lib.or_band_tiles.restype = C.c_int
             lib.or_num_threads.restype = C.c_int
             _lib = lib
@@ -177,8 +178,10 @@ def band_tiles(f32, rect, ty):
     lib = load()
     f = np.ascontiguousarray(f32, np.float32)
     a, b = C.c_int(), C.c_int()
-    ok = lib.or_band_tiles(f.ctypes.data, int(rect[0]), int(rect[1]), int(rect[2]), int(rect[3]), int(ty),
-                           C.byref(a), C.byref(b))
+    bc = np.zeros(5, np.float64)
+    r = [int(x) for x in rect]
+    lib.or_band_consts(f.ctypes.data, r[0], r[1], r[2], r[3], bc.ctypes.data)
+    ok = lib.or_band_tiles(f.ctypes.data, r[0], r[1], r[2], r[3], bc.ctypes.data, int(ty), C.byref(a), C.byref(b))
     return (a.value, b.value) if ok else None
 
 

@@ -211,6 +211,69 @@ __device__ __forceinline__ int project_gaussian(const Slice &sl, const CamDev &c
     return kVisible;
 }
 
+// Tile cover of a visible Gaussian, binary64 from
+// the binary32 record fields, pinned op sequence (identical list in the
+// oracle: or_band_consts / or_band_tiles).
+struct BandConsts {
+    double dxm, dym, dyr, i2a, Qm;
+};
+
+__device__ __forceinline__ BandConsts band_consts(float fu, float fv, float fA, float fB, float fC, float fQ,
+                                                  int px0, int px1, int py0, int py1) {
+    const double u = fu, v = fv, Ap = fA, Bp = fB, Cp = fC, Q2 = fQ;
+    const double X = fmax(fabs(dsub(dadd((double)px0, 0.5), u)), fabs(dsub(dadd((double)px1, 0.5), u)));
+    const double Y = fmax(fabs(dsub(dadd((double)py0, 0.5), v)), fabs(dsub(dadd((double)py1, 0.5), v)));
+    double mag = dmul(fabs(Ap), X);
+    mag = dmul(mag, X);
+    double t = dmul(fabs(Bp), X);
+    mag = dfma(t, Y, mag);
+    t = dmul(fabs(Cp), Y);
+    mag = dfma(t, Y, mag);
+    const double m = dfma(mag, 0x1p-12, 0x1p-10);
+    BandConsts c;
+    c.Qm = dadd(Q2, m);
+    double K = dmul(4.0, Ap);
+    K = dmul(K, Cp);
+    K = dfma(-Bp, Bp, K);
+    c.dxm = __dsqrt_rn(ddiv(dmul(dmul(-4.0, Cp), c.Qm), K));
+    c.dym = __dsqrt_rn(ddiv(dmul(dmul(-4.0, Ap), c.Qm), K));
+    c.dyr = -ddiv(dmul(Bp, c.dxm), dmul(2.0, Cp));
+    c.i2a = ddiv(0.5, Ap);
+    return c;
+}
+
+__device__ __forceinline__ double band_root(const BandConsts &c, double Ap, double Bp, double Cp, double dy,
+                                            bool plus) {
+    const double b = dmul(Bp, dy);
+    double cc = dmul(Cp, dy);
+    cc = dfma(cc, dy, c.Qm);
+    double D = dmul(b, b);
+    D = dfma(dmul(-4.0, Ap), cc, D);
+    D = D > 0.0 ? D : 0.0;
+    return plus ? dmul(dadd(-b, __dsqrt_rn(D)), c.i2a) : dmul(dsub(-b, __dsqrt_rn(D)), c.i2a);
+}
+
+__device__ __forceinline__ bool band_tiles(const BandConsts &c, float fu, float fv, float fA, float fB, float fC,
+                                           int px0, int px1, int py0, int py1, int ty, int &txa, int &txb) {
+    const double u = fu, v = fv, Ap = fA, Bp = fB, Cp = fC;
+    int ja = 16 * ty, jb = 16 * ty + 15;
+    ja = max(ja, py0);
+    jb = min(jb, py1);
+    if (ja > jb) return false;
+    const double dya = dsub(dadd((double)ja, 0.5), v), dyb = dsub(dadd((double)jb, 0.5), v);
+    if (dyb < -c.dym || dya > c.dym) return false;
+    const double dyr = c.dyr, dyl = -c.dyr;
+    const double xr = (dyr >= dya && dyr <= dyb) ? c.dxm : band_root(c, Ap, Bp, Cp, dyr < dya ? dya : dyb, false);
+    const double xl = (dyl >= dya && dyl <= dyb) ? -c.dxm : band_root(c, Ap, Bp, Cp, dyl < dya ? dya : dyb, true);
+    double ca = ceil(dsub(dadd(u, xl), 0.5)), cb = floor(dsub(dadd(u, xr), 0.5));
+    if (ca < (double)px0) ca = (double)px0;
+    if (cb > (double)px1) cb = (double)px1;
+    if (ca > cb) return false;
+    txa = ((int)ca) >> 4;
+    txb = ((int)cb) >> 4;
+    return true;
+}
+
 // Degree-3 SH colour c_i(d), value path in fp32: rgb = max(0, sum + 0.5).
 __device__ __forceinline__ void sh_color(const float4 *__restrict__ sh4, float dx, float dy, float dz, float out[3]) {
     const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);

@@ -29,7 +29,9 @@ struct Counters {
     uint32_t pad[1];
     unsigned long long n_eval;   // (pixel, Gaussian) pairs tested before termination
     unsigned long long n_blend;  // pairs composited
-    uint32_t pad2[12];
+    uint32_t row_ticket;         // row-item scan partitions
+    uint32_t n_items;            // (Gaussian, tile row) items
+    uint32_t pad2[10];
 };
 static_assert(sizeof(Counters) == 128, "Counters layout");
 
@@ -51,10 +53,10 @@ struct RenderLayout {
     int32_t sort_parts;  // depth-sort partitions (upper bound from n)
     int32_t tile_parts;  // tile-sort partitions (upper bound from max_entries)
     int64_t max_entries;
-    size_t counters, lookback, sort_gbase, tile_diff, emit_lb, zero_end;
+    size_t counters, lookback, sort_gbase, tile_diff, emit_lb, row_lb, zero_end;
     size_t epoch, sort_status, tile_status;
     size_t rec0, rec1, rec2, depth, rect, rect_sorted, keys0, keys1, vals0, vals1;
-    size_t tile_gbase, tile_start, emit_cnt, emit_off, chunk_first, ekey0, ekey1, eval0, eval1, entries, total;
+    size_t tile_gbase, tile_start, band_consts, roff, rchunk_first, item_pack, item_v, emit_off, chunk_first, ekey0, ekey1, eval0, eval1, entries, total;
 };
 RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max_entries);
 

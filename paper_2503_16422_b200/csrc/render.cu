@@ -7,9 +7,9 @@
 //   k_sort_*         row 5a: stable onesweep LSD radix sort (4 x 8-bit) of the
 //                    fp32 depth keys -> canonical (depth, index) order (P:126
 //                    "sorted by their depth", reading R8)
-//   k_bin_count..    row 5b: per-tile counts (2D difference array), emission of
-//                    (tile, slot) entries in canonical order, then two stable
-//                    7-bit onesweep passes on the tile id
+//   k_bin_scan..     row 5b: tile cover per (Gaussian, tile row) (band_tiles),
+//                    per-tile counts, emission of (tile, slot) entries in
+//                    canonical order, then two stable 7-bit onesweep passes
 //   k_blend          row 6: per-tile front-to-back Eq. 2 with warp-uniform
 //                    early exit
 #include <algorithm>
@@ -348,33 +348,182 @@ __device__ __forceinline__ TileRect tile_rect(uint2 r) {
     return t;
 }
 
-// Row 5b (2/4), one block: 2D prefix of the difference array -> per-tile
+// Row 5b (1/5): tile rows per Gaussian (ny of its pixel AABB) in canonical
+// order -> their exclusive scan = row-item offsets (single pass, warp
+// look-back), and the first Gaussian of every row-item chunk.
+constexpr int kItemTile = 1024;  // row items per chunk / partition
+__global__ void __launch_bounds__(1024) k_bin_scan(const uint2 *__restrict__ rects, const uint32_t *__restrict__ order,
+                                                   const float4 *__restrict__ rec0, const float4 *__restrict__ rec1,
+                                                   const Counters *ctrc, uint32_t *ticket, uint32_t *lb,
+                                                   uint32_t *__restrict__ off, uint32_t *__restrict__ chunk_first,
+                                                   uint32_t max_chunks, uint32_t *n_items,
+                                                   BandConsts *__restrict__ bconst) {
+    __shared__ uint32_t s_w[32];
+    __shared__ uint32_t s_part, s_excl;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t n = ctrc->n_vis;
+    if (tid == 0) s_part = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t part = s_part;
+    if (part * 1024 >= n) return;
+    const uint32_t i = part * 1024 + tid;
+    uint32_t c = 0;
+    if (i < n) {
+        const uint2 rc = __ldg(rects + i);
+        c = (uint32_t)tile_rect(rc).ny;
+        const uint32_t v = __ldg(order + i);
+        const float4 a = __ldg(rec0 + v), b = __ldg(rec1 + v);
+        bconst[i] = band_consts(a.x, a.y, a.z, a.w, b.x, b.y, rc.x & 0xffff, rc.x >> 16, rc.y & 0xffff, rc.y >> 16);
+    }
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = s_w[lane], wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        s_w[lane] = wi - w;
+        const uint32_t tot = __shfl_sync(0xffffffffu, wi, 31);
+        const uint32_t excl = lookback_warp(lb, part, tot, lane);
+        if (lane == 0) {
+            s_excl = excl;
+            if ((part + 1) * 1024 >= n) *n_items = excl + tot;  // last partition
+        }
+    }
+    __syncthreads();
+    if (i < n) {
+        const uint32_t o = s_excl + s_w[warp] + incl - c;
+        off[i] = o;
+        for (uint32_t k = (o + kItemTile - 1) / kItemTile; k * kItemTile < o + c && k < max_chunks; ++k)
+            chunk_first[k] = i;
+    }
+}
+
+// Row 5b (2/5): one thread per row item (Gaussian r, tile row ty): the tile
+// cover [txa, txb] of the row (band_tiles, binary64 pinned), its entry count,
+// the per-row difference array of the tile counts, and the exclusive scan of
+// the counts (look-back) = emission offsets + first item of every entry chunk.
+__global__ void __launch_bounds__(1024) k_row_scan(const uint2 *__restrict__ rects, const uint32_t *__restrict__ order,
+                                                   const float4 *__restrict__ rec0, const float4 *__restrict__ rec1,
+                                                   const BandConsts *__restrict__ bconst,
+                                                   const uint32_t *__restrict__ roff,
+                                                   const uint32_t *__restrict__ rchunk_first,
+                                                   const Counters *ctrc, const uint32_t *n_items_ptr, int tiles_x,
+                                                   uint32_t *ticket, uint32_t *lb, int *__restrict__ diff,
+                                                   uint32_t *__restrict__ item_pack, uint32_t *__restrict__ item_v,
+                                                   uint32_t *__restrict__ eoff, uint32_t *__restrict__ echunk_first,
+                                                   uint32_t max_echunks, uint32_t item_cap) {
+    __shared__ uint32_t s_off[kItemTile + 1];
+    __shared__ uint32_t s_w[32];
+    __shared__ uint32_t s_part, s_excl;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t n = ctrc->n_vis, ni = *n_items_ptr;
+    if (ni > item_cap) {  // more row items than the workspace holds
+        if (blockIdx.x == 0 && tid == 0) const_cast<Counters *>(ctrc)->status = FDGS_ERR_OVERFLOW;
+        return;
+    }
+    while (true) {  // persistent: partitions in ticket order
+    if (tid == 0) s_part = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t part = s_part;
+    if (part * kItemTile >= ni) return;
+    // window of Gaussians owning this chunk's items (each owns >= 1 item)
+    const uint32_t r0 = __ldg(rchunk_first + part);
+    const uint32_t m = min((uint32_t)kItemTile, n - r0);
+    for (uint32_t q = tid; q < m; q += blockDim.x) s_off[q] = __ldg(roff + r0 + q);
+    if (tid == 0) s_off[m] = 0xffffffffu;
+    __syncthreads();
+    const uint32_t i = part * kItemTile + tid;
+    uint32_t c = 0;
+    if (i < ni) {
+        int lo = 0, hi = (int)m - 1;  // largest q with s_off[q] <= i
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_off[mid] <= i) lo = mid; else hi = mid - 1;
+        }
+        const uint32_t r = r0 + lo;
+        const uint2 rc = __ldg(rects + r);
+        const int px0 = rc.x & 0xffff, px1 = rc.x >> 16, py0 = rc.y & 0xffff, py1 = rc.y >> 16;
+        const int ty = (py0 >> 4) + (int)(i - s_off[lo]);
+        const uint32_t v = __ldg(order + r);
+        const float4 a = __ldg(rec0 + v), b = __ldg(rec1 + v);
+        int txa, txb;
+        uint32_t pack = 0xffffffffu;  // empty row
+        const BandConsts bc = bconst[r];
+        if (band_tiles(bc, a.x, a.y, a.z, a.w, b.x, px0, px1, py0, py1, ty, txa, txb)) {
+            c = (uint32_t)(txb - txa + 1);
+            pack = (uint32_t)ty | ((uint32_t)txa << 11) | ((uint32_t)txb << 22);  // tiles_x, tiles_y <= 512
+            atomicAdd(&diff[ty * (tiles_x + 1) + txa], 1);
+            atomicAdd(&diff[ty * (tiles_x + 1) + txb + 1], -1);
+        }
+        item_pack[i] = pack;
+        item_v[i] = v;
+    }
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = s_w[lane], wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        s_w[lane] = wi - w;
+        const uint32_t tot = __shfl_sync(0xffffffffu, wi, 31);
+        const uint32_t excl = lookback_warp(lb, part, tot, lane);
+        if (lane == 0) s_excl = excl;
+    }
+    __syncthreads();
+    if (i < ni) {
+        const uint32_t o = s_excl + s_w[warp] + incl - c;
+        eoff[i] = o;
+        for (uint32_t k = (o + kTileTile - 1) / kTileTile; k * kTileTile < o + c && k < max_echunks; ++k)
+            echunk_first[k] = i;
+    }
+    __syncthreads();
+    }
+}
+
+// Row 5b (3/5), one block: per-row prefix of the difference array -> per-tile
 // counts -> tile_start[0..T] and E (capacity check), and the exclusive digit
 // bases of the two tile passes (low 7 bits, then the high bits).
 __global__ void __launch_bounds__(1024) k_tile_scan(const int *__restrict__ diff, int tiles_x, int tiles_y,
                                                     uint32_t *__restrict__ tile_start, uint32_t *__restrict__ tbase,
                                                     Counters *ctr, int64_t max_entries) {
-    extern __shared__ int sm[];  // (tiles_y + 1) x (tiles_x + 1)
+    extern __shared__ int sm[];  // tiles_y x (tiles_x + 1)
     __shared__ uint32_t s_sum[1024];
     __shared__ uint32_t s_dig[2][128];
-    const int tid = threadIdx.x;
-    const int gx = tiles_x + 1, gy = tiles_y + 1, T = tiles_x * tiles_y;
-    for (int k = tid; k < gx * gy; k += blockDim.x) sm[k] = __ldcg(diff + k);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gx = tiles_x + 1, T = tiles_x * tiles_y;
+    for (int k = tid; k < gx * tiles_y; k += blockDim.x) sm[k] = __ldcg(diff + k);
     if (tid < 256) s_dig[tid >> 7][tid & 127] = 0;
     __syncthreads();
-    for (int y = tid; y < tiles_y; y += blockDim.x) {
+    for (int y = warp; y < tiles_y; y += 32) {  // row prefix, one warp per row
         int run = 0;
-        for (int x = 0; x < tiles_x; ++x) {
-            run += sm[y * gx + x];
-            sm[y * gx + x] = run;
-        }
-    }
-    __syncthreads();
-    for (int x = tid; x < tiles_x; x += blockDim.x) {
-        int run = 0;
-        for (int y = 0; y < tiles_y; ++y) {
-            run += sm[y * gx + x];
-            sm[y * gx + x] = run;
+        for (int x0 = 0; x0 < tiles_x; x0 += 32) {
+            const int x = x0 + lane;
+            int val = x < tiles_x ? sm[y * gx + x] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, val, o);
+                if (lane >= o) val += t;
+            }
+            if (x < tiles_x) sm[y * gx + x] = run + val;
+            run += __shfl_sync(0xffffffffu, val, 31);
         }
     }
     __syncthreads();
@@ -412,108 +561,52 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const int *__restrict__ diff
         tile_start[T] = E;
         ctr->n_entries = E;
         if ((int64_t)E > max_entries) ctr->status = FDGS_ERR_OVERFLOW;
-        else ctr->n_sort_entries = E;
+        else if (ctr->status == FDGS_OK) ctr->n_sort_entries = E;
     }
 }
 
-// Row 5b (1/4): per-Gaussian entry counts nx*ny in canonical order -> their
-// exclusive scan (single pass, warp look-back) = emission offsets, the first
-// Gaussian of every emission chunk, and the per-tile counts through a global
-// 2D difference array (4 reductions per visible Gaussian).
-__global__ void __launch_bounds__(1024) k_bin_scan(const uint2 *__restrict__ rects, const Counters *ctrc,
-                                                   int tiles_x, uint32_t *ticket, uint32_t *lb,
-                                                   int *__restrict__ diff, uint32_t *__restrict__ off,
-                                                   uint32_t *__restrict__ chunk_first, uint32_t max_chunks) {
-    __shared__ uint32_t s_w[32];
-    __shared__ uint32_t s_part, s_excl;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t n = ctrc->n_vis;
-    if (tid == 0) s_part = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const uint32_t part = s_part;
-    if (part * 1024 >= n) return;
-    const uint32_t i = part * 1024 + tid;
-    uint32_t c = 0;
-    if (i < n) {
-        const TileRect t = tile_rect(__ldg(rects + i));
-        const int gx = tiles_x + 1, x1 = t.tx0 + t.nx, y1 = t.ty0 + t.ny;
-        atomicAdd(&diff[t.ty0 * gx + t.tx0], 1);
-        atomicAdd(&diff[t.ty0 * gx + x1], -1);
-        atomicAdd(&diff[y1 * gx + t.tx0], -1);
-        atomicAdd(&diff[y1 * gx + x1], 1);
-        c = (uint32_t)(t.nx * t.ny);
-    }
-    uint32_t incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_w[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t w = s_w[lane], wi = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= o) wi += y;
-        }
-        s_w[lane] = wi - w;
-        const uint32_t tot = __shfl_sync(0xffffffffu, wi, 31);
-        const uint32_t excl = lookback_warp(lb, part, tot, lane);
-        if (lane == 0) s_excl = excl;
-    }
-    __syncthreads();
-    if (i < n) {
-        const uint32_t o = s_excl + s_w[warp] + incl - c;
-        off[i] = o;
-        // first Gaussian of every emission chunk that starts inside [o, o + c)
-        for (uint32_t k = (o + kTileTile - 1) / kTileTile; k * kTileTile < o + c && k < max_chunks; ++k)
-            chunk_first[k] = i;
-    }
-}
-
-// Row 5b (3/4): emission in canonical order: (tile id, visible slot) for every
-// tile of every Gaussian's rectangle, Gaussian-major, tiles row-major.  One
+// Row 5b (4/5): emission in canonical order: (tile id, visible slot) for every
+// covered tile of every row item, Gaussian-major, then row, then column.  One
 // block per chunk of kTileTile entries (load-balanced, coalesced stores): the
-// chunk's Gaussians are staged in shared memory and each entry finds its
-// Gaussian by binary search there.
-constexpr int kEmitWin = 1024;  // Gaussians staged per window
-__global__ void __launch_bounds__(256) k_emit(const uint2 *__restrict__ rects, const uint32_t *__restrict__ order,
-                                              const uint32_t *__restrict__ off,
+// chunk's row items are staged in shared memory and each entry finds its item
+// by binary search there.
+constexpr int kEmitWin = 1024;  // row items staged per window
+__global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ item_pack,
+                                              const uint32_t *__restrict__ item_v, const uint32_t *__restrict__ eoff,
                                               const uint32_t *__restrict__ chunk_first, const Counters *ctrc,
-                                              int tiles_x, uint32_t *__restrict__ ekey, uint32_t *__restrict__ eval) {
+                                              const uint32_t *n_items_ptr, int tiles_x, uint32_t *__restrict__ ekey,
+                                              uint32_t *__restrict__ eval) {
     __shared__ uint32_t s_off[kEmitWin];
-    __shared__ uint2 s_rect[kEmitWin];
+    __shared__ uint32_t s_pack[kEmitWin];
     __shared__ uint32_t s_v[kEmitWin];
     const int tid = threadIdx.x;
     if (ctrc->status != FDGS_OK) return;
-    const uint32_t n = ctrc->n_vis, E = ctrc->n_sort_entries;
+    const uint32_t ni = *n_items_ptr, E = ctrc->n_sort_entries;
     const uint32_t chunks = (E + kTileTile - 1) / kTileTile;
     for (uint32_t k = blockIdx.x; k < chunks; k += gridDim.x) {
         const uint32_t e0 = k * kTileTile, e1 = min(e0 + kTileTile, E);
         uint32_t r0 = __ldg(chunk_first + k);
         uint32_t e = e0;
-        while (e < e1) {  // windows of kEmitWin Gaussians (one window unless Gaussians have 1-2 tiles)
-            const uint32_t m = min((uint32_t)kEmitWin, n - r0);
+        while (e < e1) {  // windows of kEmitWin items
+            const uint32_t m = min((uint32_t)kEmitWin, ni - r0);
             for (uint32_t q = tid; q < m; q += blockDim.x) {
-                s_off[q] = __ldg(off + r0 + q);
-                s_rect[q] = __ldg(rects + r0 + q);
-                s_v[q] = __ldg(order + r0 + q);
+                s_off[q] = __ldg(eoff + r0 + q);
+                s_pack[q] = __ldg(item_pack + r0 + q);
+                s_v[q] = __ldg(item_v + r0 + q);
             }
             __syncthreads();
-            const uint32_t wend = (r0 + m < n) ? min(e1, __ldg(off + r0 + m)) : e1;
+            const uint32_t wend = (r0 + m < ni) ? min(e1, __ldg(eoff + r0 + m)) : e1;
             for (uint32_t i = e + tid; i < wend; i += blockDim.x) {
-                // largest q with s_off[q] <= i
+                // largest q with s_off[q] <= i (empty items share the next item's offset,
+                // the largest such q is the non-empty owner)
                 int lo = 0, hi = (int)m - 1;
                 while (lo < hi) {
                     const int mid = (lo + hi + 1) >> 1;
                     if (s_off[mid] <= i) lo = mid; else hi = mid - 1;
                 }
-                const TileRect t = tile_rect(s_rect[lo]);
-                const int kk = (int)(i - s_off[lo]);
-                const int qy = __float2int_rz(((float)kk + 0.5f) / (float)t.nx);
-                ekey[i] = (uint32_t)((t.ty0 + qy) * tiles_x + t.tx0 + (kk - qy * t.nx));
+                const uint32_t pk = s_pack[lo];
+                const uint32_t ty = pk & 0x7ffu, txa = (pk >> 11) & 0x7ffu;
+                ekey[i] = ty * (uint32_t)tiles_x + txa + (i - s_off[lo]);
                 eval[i] = s_v[lo];
             }
             __syncthreads();
@@ -778,12 +871,24 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     uint64_t *tstat = reinterpret_cast<uint64_t *>(ws + L.tile_status);
     constexpr int kTItems = kTileSortItems;
     uint32_t *cfirst = reinterpret_cast<uint32_t *>(ws + L.chunk_first);
-    k_bin_scan<<<std::max(1, (L.n + 1023) / 1024), 1024, 0, st>>>(rect_sorted, ctr, L.tiles_x, &ctr->bin_ticket, elb,
-                                                                   diff, eoff, cfirst, (uint32_t)L.tile_parts);
+    uint32_t *roff = reinterpret_cast<uint32_t *>(ws + L.roff);
+    uint32_t *rcfirst = reinterpret_cast<uint32_t *>(ws + L.rchunk_first);
+    uint32_t *ipack = reinterpret_cast<uint32_t *>(ws + L.item_pack);
+    uint32_t *iv = reinterpret_cast<uint32_t *>(ws + L.item_v);
+    uint32_t *rlb = reinterpret_cast<uint32_t *>(ws + L.row_lb);
+    const uint32_t item_chunks = (uint32_t)((L.max_entries + 1023) / 1024);
+    BandConsts *bconst = reinterpret_cast<BandConsts *>(ws + L.band_consts);
+    k_bin_scan<<<std::max(1, (L.n + 1023) / 1024), 1024, 0, st>>>(rect_sorted, order, rec0, rec1, ctr,
+                                                                   &ctr->bin_ticket, elb, roff, rcfirst, item_chunks,
+                                                                   &ctr->n_items, bconst);
+    k_row_scan<<<(int)std::min<uint32_t>(item_chunks, 2 * L.p_sort), 1024, 0, st>>>(
+        rect_sorted, order, rec0, rec1, bconst, roff, rcfirst, ctr, &ctr->n_items,
+                                                  L.tiles_x, &ctr->row_ticket, rlb, diff, ipack, iv, eoff, cfirst,
+                                                  (uint32_t)L.tile_parts, (uint32_t)L.max_entries);
     const size_t scan_smem = sizeof(int) * (size_t)(L.tiles_x + 1) * (L.tiles_y + 1);
     k_tile_scan<<<1, 1024, scan_smem, st>>>(diff, L.tiles_x, L.tiles_y, tstart, tbase, ctr, L.max_entries);
     const int pgrid = 4 * L.p_sort;  // persistent grids
-    k_emit<<<pgrid, 256, 0, st>>>(rect_sorted, order, eoff, cfirst, ctr, L.tiles_x, ek[0], evl[0]);
+    k_emit<<<pgrid, 256, 0, st>>>(ipack, iv, eoff, cfirst, ctr, &ctr->n_items, L.tiles_x, ek[0], evl[0]);
     k_onesweep<7, kTItems><<<pgrid, kSortThreads, 0, st>>>(ek[0], evl[0], ek[1], evl[1], &ctr->n_sort_entries, epoch,
                                                            &ctr->tile_ticket[0], 0, tbase, tstat, nullptr, nullptr);
     k_onesweep<7, kTItems><<<pgrid, kSortThreads, 0, st>>>(ek[1], evl[1], nullptr, entries, &ctr->n_sort_entries,
