@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--no-stage-events", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--streams", type=int, default=4, help="frame-pipelining depth (workspaces/streams)")
+    p.add_argument("--no-split", action="store_true", help="blend on the front-end stream (no priority split)")
     return p.parse_args()
 
 
@@ -210,7 +211,7 @@ def run_ours(args):
     seq = sequence()
     mine = [x for x in seq if x[0] % world == rank]
     F = args.frames_per_step
-    pipe = fd.RenderPipeline(scene, cams[0].width, cams[0].height, depth=args.streams)
+    pipe = fd.RenderPipeline(scene, cams[0].width, cams[0].height, depth=args.streams, split=not args.no_split)
     renderer = pipe.renderers[0]
     outs = [renderer.new_output() for _ in range(F)]
     stats = torch.zeros((F, 4), dtype=torch.int64, device=dev)  # fdgs_frame_stats is 32 bytes
@@ -316,7 +317,8 @@ def run_ours(args):
                                    "key-frame interval 20, masked (union of bracketing key-frames)",
                        "frames_per_step": F, "frames_per_rank": frames_rank, "partition": "frame f -> rank f mod N",
                        "l2": "flushed between steps (512 MiB write)", "parallelism": f"frames x{world}",
-                       "streams_per_gpu": args.streams},
+                       "streams_per_gpu": args.streams,
+                       "stream_split": "front end high priority, blend low priority" if not args.no_split else "none"},
                gpu_launches=13 * frames_rank)
     if use_ev and stage_ms.sum() > 0:
         per_frame = stage_ms / frames_rank
@@ -346,6 +348,25 @@ def run_ours(args):
         res["stages"]["note"] = (f"per-stage CUDA events of every timed frame; a stage's time is the union of its "
                                  f"per-frame intervals (busy time); with {args.streams} frame-pipelining streams "
                                  "stages of different frames run concurrently, so shares can sum above 1")
+    # isolated (one stream, nothing overlapping) per-stage times of one extra step
+    # of the same frames, outside the timed region: the blend's own throughput
+    if use_ev and stage_ms.sum() > 0 and "roofline" in res:
+        iso = fd.RenderPipeline(scene, cams[0].width, cams[0].height, depth=1, split=False)
+        iso.renderers[0] = renderer
+        fr = timed_frames[0]
+        flush.zero_()
+        torch.cuda.synchronize()
+        iso.render_many([frame_args(x) for x in fr], outs[:len(fr)], stage_events=evs, stream=stream)
+        torch.cuda.synchronize()
+        iso_ms = np.array([sum(evs[k][s_].elapsed_time(evs[k][s_ + 1]) for k in range(len(fr))) for s_ in range(4)])
+        if res["roofline"]["kernel"] == "k_blend":
+            fl = (10.0 * n_eval + 12.0 * n_blend) / len(timed_frames)
+            ach = fl / (iso_ms[3] / 1e3) / 1e12
+            res["roofline"]["isolated"] = {"achieved": round(ach, 3), "frac": round(ach / res["roofline"]["peak"], 4),
+                                           "ms_per_frame": round(float(iso_ms[3] / len(fr)), 4),
+                                           "note": "same frames on one stream, no overlap (outside the timed region)"}
+        res["stages_isolated_ms_per_frame"] = {nm: round(float(iso_ms[i] / len(fr)), 4)
+                                               for i, nm in enumerate(stage_names)}
     res["work_per_frame"] = {"n_act": round(n_act_tot / frames_rank), "n_vis": round(n_vis_tot / frames_rank),
                              "entries": round(n_ent_tot / frames_rank), "evaluated_pairs": round(n_eval / frames_rank),
                              "blended_pairs": round(n_blend / frames_rank)}

@@ -148,6 +148,20 @@ fdgs_status fdgs_render_timed(const fdgs_scene *scene, const uint32_t *d_mask_l,
                               size_t ws_bytes, int64_t max_entries, fdgs_frame_stats *d_stats, void *stream,
                               void *const *stage_events);
 
+/* fdgs_render with the blend (row 6) on a second stream: the front end
+ * (rows 1-5) runs on `stream`, then `split_event` (a caller-created
+ * cudaEvent_t, passed as void*) is recorded on it and `blend_stream` waits for
+ * it before the blend.  Lets a caller give the latency-bound front end a
+ * higher stream priority than the ALU-bound blend so that consecutive frames
+ * interleave.  The workspace is in use until the blend completes on
+ * `blend_stream`: the caller must order the workspace's next frame after it.
+ * stage_events (nullable) as in fdgs_render_timed ([3], [4] on blend_stream).
+ * ASYNC. */
+fdgs_status fdgs_render_split(const fdgs_scene *scene, const uint32_t *d_mask_l, const uint32_t *d_mask_r,
+                              const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T, void *d_ws,
+                              size_t ws_bytes, int64_t max_entries, fdgs_frame_stats *d_stats, void *stream,
+                              void *blend_stream, void *split_event, void *const *stage_events);
+
 /* Same as fdgs_render, then synchronises `stream` and returns the frame status
  * (FDGS_ERR_OVERFLOW if E > max_entries).  host_stats (nullable) receives the
  * counters.  For tests and the end-to-end path. */

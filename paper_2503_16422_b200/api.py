@@ -131,6 +131,21 @@ class Renderer:
                                           _stream_ptr(stream), evs))
         return out
 
+    def render_split(self, cam, t, mask_l=None, mask_r=None, out=None, out_T=None, stats=None, stream=None,
+                     blend_stream=None, split_event=None, stage_events=None):
+        """fdgs_render_split: front end on `stream`, blend on `blend_stream`."""
+        out = self.new_output() if out is None else out
+        ml, mr = self._masks(mask_l, mask_r)
+        cs = camera_struct(cam) if not isinstance(cam, FdgsCamera) else cam
+        if split_event.cuda_event == 0:
+            split_event.record(stream)  # materialise the CUDA event
+        evs = None if stage_events is None else (C.c_void_p * 5)(*[e.cuda_event for e in stage_events])
+        check(lib().fdgs_render_split(C.byref(self.scene.struct), ml, mr, C.byref(cs), float(t), _ptr(out),
+                                      _ptr(out_T), _ptr(self.ws), self.ws_bytes, self.max_entries, _ptr(stats),
+                                      _stream_ptr(stream), _stream_ptr(blend_stream),
+                                      C.c_void_p(split_event.cuda_event), evs))
+        return out
+
     def render_checked(self, cam, t, mask_l=None, mask_r=None, out=None, out_T=None, stream=None,
                        grow: bool = True):
         """Synchronous render; grows the entry capacity and retries on overflow."""
@@ -180,15 +195,25 @@ class Renderer:
 
 
 class RenderPipeline:
-    """Frame-pipelined rendering of a sequence: `depth` independent workspaces on
-    `depth` CUDA streams, frame k on stream k mod depth.  The latency-bound
-    front end of one frame (preprocess, sorts, binning) overlaps the ALU-bound
-    blend of the previous one; each frame is still one fdgs_render call."""
+    """Frame-pipelined rendering of a sequence: `depth` independent workspaces,
+    frame k on workspace k mod depth.  Each workspace has a high-priority
+    front-end stream (preprocess, sorts, binning) and a low-priority blend
+    stream (fdgs_render_split), so the latency-bound front end of later frames
+    is scheduled ahead of, and overlaps, the ALU-bound blends."""
 
-    def __init__(self, scene: Scene, width: int, height: int, depth: int = 2, max_entries: int | None = None):
+    def __init__(self, scene: Scene, width: int, height: int, depth: int = 4, max_entries: int | None = None,
+                 split: bool = True):
         self.renderers = [Renderer(scene, width, height, max_entries) for _ in range(depth)]
-        self.streams = [torch.cuda.Stream(device=scene.device) for _ in range(depth)]
+        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
+        self.split = split
+        self.front = [torch.cuda.Stream(device=scene.device, priority=-1 if split else 0) for _ in range(depth)]
+        self.blend = [torch.cuda.Stream(device=scene.device, priority=0) for _ in range(depth)] if split else None
+        self.split_ev = [torch.cuda.Event() for _ in range(depth)]
         self.depth = depth
+
+    @property
+    def streams(self):
+        return self.front + (self.blend or [])
 
     def render_many(self, frames, outs, stats=None, stage_events=None, stream=None):
         """frames: list of (cam, t, mask_l, mask_r); outs: list of output tensors.
@@ -201,9 +226,18 @@ class RenderPipeline:
             s.wait_event(start)
         for k, (cam, t, ml, mr) in enumerate(frames):
             i = k % self.depth
-            self.renderers[i].render(cam, t, ml, mr, out=outs[k], stats=None if stats is None else stats[k],
-                                     stream=self.streams[i],
-                                     stage_events=None if stage_events is None else stage_events[k])
+            r = self.renderers[i]
+            if not self.split:
+                r.render(cam, t, ml, mr, out=outs[k], stats=None if stats is None else stats[k], stream=self.front[i],
+                         stage_events=None if stage_events is None else stage_events[k])
+                continue
+            if k >= self.depth:  # the workspace is free once its previous blend is done
+                done = torch.cuda.Event()
+                done.record(self.blend[i])
+                self.front[i].wait_event(done)
+            r.render_split(cam, t, ml, mr, out=outs[k], stats=None if stats is None else stats[k],
+                           stream=self.front[i], blend_stream=self.blend[i], split_event=self.split_ev[i],
+                           stage_events=None if stage_events is None else stage_events[k])
         for s in self.streams:
             e = torch.cuda.Event()
             e.record(s)

@@ -227,10 +227,10 @@ size_t fdgs_render_workspace_bytes(int32_t n, int32_t width, int32_t height, int
     return render_layout(n, width, height, max_entries).total;
 }
 
-fdgs_status fdgs_render_timed(const fdgs_scene *scene, const uint32_t *d_mask_l, const uint32_t *d_mask_r,
-                              const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T, void *d_ws,
-                              size_t ws_bytes, int64_t max_entries, fdgs_frame_stats *d_stats, void *stream,
-                              void *const *stage_events) {
+static fdgs_status render_impl(const fdgs_scene *scene, const uint32_t *d_mask_l, const uint32_t *d_mask_r,
+                               const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T, void *d_ws,
+                               size_t ws_bytes, int64_t max_entries, fdgs_frame_stats *d_stats, void *stream,
+                               void *const *stage_events, void *blend_stream, void *split_event) {
     fdgs_status s = check_scene(scene);
     if (s != FDGS_OK) return s;
     if (cam == nullptr || d_out_rgb == nullptr) return fail(FDGS_ERR_INVALID_ARG, "camera / output is NULL");
@@ -248,8 +248,27 @@ fdgs_status fdgs_render_timed(const fdgs_scene *scene, const uint32_t *d_mask_l,
     if (g_attr_err != cudaSuccess) return cuda_fail(g_attr_err, "cudaFuncSetAttribute");
     cudaError_t e = launch_render(make_scenedev(*scene), d_mask_l, d_mask_r, cd, t, d_out_rgb, d_out_T,
                                   reinterpret_cast<char *>(d_ws), L, d_stats, (cudaStream_t)stream,
-                                  reinterpret_cast<cudaEvent_t const *>(stage_events));
+                                  reinterpret_cast<cudaEvent_t const *>(stage_events), (cudaStream_t)blend_stream,
+                                  (cudaEvent_t)split_event);
     return e == cudaSuccess ? FDGS_OK : cuda_fail(e, "fdgs_render");
+}
+
+fdgs_status fdgs_render_timed(const fdgs_scene *scene, const uint32_t *d_mask_l, const uint32_t *d_mask_r,
+                              const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T, void *d_ws,
+                              size_t ws_bytes, int64_t max_entries, fdgs_frame_stats *d_stats, void *stream,
+                              void *const *stage_events) {
+    return render_impl(scene, d_mask_l, d_mask_r, cam, t, d_out_rgb, d_out_T, d_ws, ws_bytes, max_entries, d_stats,
+                       stream, stage_events, nullptr, nullptr);
+}
+
+fdgs_status fdgs_render_split(const fdgs_scene *scene, const uint32_t *d_mask_l, const uint32_t *d_mask_r,
+                              const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T, void *d_ws,
+                              size_t ws_bytes, int64_t max_entries, fdgs_frame_stats *d_stats, void *stream,
+                              void *blend_stream, void *split_event, void *const *stage_events) {
+    if (blend_stream == nullptr || split_event == nullptr)
+        return fail(FDGS_ERR_INVALID_ARG, "fdgs_render_split needs a blend stream and an event");
+    return render_impl(scene, d_mask_l, d_mask_r, cam, t, d_out_rgb, d_out_T, d_ws, ws_bytes, max_entries, d_stats,
+                       stream, stage_events, blend_stream, split_event);
 }
 
 fdgs_status fdgs_render(const fdgs_scene *scene, const uint32_t *d_mask_l, const uint32_t *d_mask_r,

@@ -66,7 +66,8 @@ SceneDev make_scenedev(const fdgs_scene &s);
 // launchers (return cudaGetLastError())
 cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint32_t *mask_r, const CamDev &cam,
                           float t, float *out_rgb, float *out_T, char *ws, const RenderLayout &L,
-                          fdgs_frame_stats *stats, cudaStream_t st, cudaEvent_t const *stage_events);
+                          fdgs_frame_stats *stats, cudaStream_t st, cudaEvent_t const *stage_events,
+                          cudaStream_t blend_st = nullptr, cudaEvent_t split_ev = nullptr);
 cudaError_t launch_keyframe(const SceneDev &sc, const CamDev *d_cams, int n_cams, float t, uint32_t *out,
                             cudaStream_t st);
 cudaError_t launch_mask_or(const uint32_t *a, const uint32_t *b, int n, uint32_t *out, cudaStream_t st);

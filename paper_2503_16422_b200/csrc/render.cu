@@ -825,7 +825,8 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restr
 // ---------------------------------------------------------------- launcher
 cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint32_t *mask_r, const CamDev &cam,
                           float t, float *out_rgb, float *out_T, char *ws, const RenderLayout &L,
-                          fdgs_frame_stats *stats, cudaStream_t st, cudaEvent_t const *ev) {
+                          fdgs_frame_stats *stats, cudaStream_t st, cudaEvent_t const *ev, cudaStream_t blend_st,
+                          cudaEvent_t split_ev) {
     Counters *ctr = reinterpret_cast<Counters *>(ws + L.counters);
     uint32_t *lb = reinterpret_cast<uint32_t *>(ws + L.lookback);
     float4 *rec0 = reinterpret_cast<float4 *>(ws + L.rec0);
@@ -894,16 +895,23 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     k_onesweep<7, kTItems><<<pgrid, kSortThreads, 0, st>>>(ek[1], evl[1], nullptr, entries, &ctr->n_sort_entries,
                                                            epoch, &ctr->tile_ticket[1], 7, tbase + 128,
                                                            tstat + (size_t)L.tile_parts * 128, nullptr, nullptr);
-    if (ev && (e = cudaEventRecord(ev[3], st)) != cudaSuccess) return e;
+    // the blend may run on its own (lower-priority) stream, ordered after the front end
+    cudaStream_t bst = st;
+    if (blend_st != nullptr) {
+        if ((e = cudaEventRecord(split_ev, st)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(blend_st, split_ev, 0)) != cudaSuccess) return e;
+        bst = blend_st;
+    }
+    if (ev && (e = cudaEventRecord(ev[3], bst)) != cudaSuccess) return e;
     if (stats != nullptr)
-        k_blend<true><<<L.n_tiles, kBlendThreads, 0, st>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
-                                                           L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T,
-                                                           stats);
-    else
-        k_blend<false><<<L.n_tiles, kBlendThreads, 0, st>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
+        k_blend<true><<<L.n_tiles, kBlendThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
                                                             L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T,
-                                                            nullptr);
-    if (ev && (e = cudaEventRecord(ev[4], st)) != cudaSuccess) return e;
+                                                            stats);
+    else
+        k_blend<false><<<L.n_tiles, kBlendThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x,
+                                                             L.width, L.height, cam.bg[0], cam.bg[1], cam.bg[2],
+                                                             out_rgb, out_T, nullptr);
+    if (ev && (e = cudaEventRecord(ev[4], bst)) != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

@@ -281,11 +281,13 @@ def test_render_pipeline_matches_sequential():
     for fr in range(100, 124):
         l, r = fd.bracket(kf, fr)
         frames.append((cams[fr % 4], float(times[fr]), masks[l], masks[r]))
-    pipe = fd.RenderPipeline(sc, W, H, depth=3)
-    outs = [pipe.renderers[0].new_output() for _ in frames]
-    pipe.render_many(frames, outs)
-    torch.cuda.synchronize()
     seq = fd.Renderer(sc, W, H)
-    for (cam, t, ml, mr), o in zip(frames, outs):
-        ref, _ = seq.render_checked(cam, t, ml, mr)
-        assert torch.equal(ref, o)
+    refs = [seq.render_checked(cam, t, ml, mr)[0] for (cam, t, ml, mr) in frames]
+    for split in (False, True):
+        pipe = fd.RenderPipeline(sc, W, H, depth=3, split=split)
+        outs = [pipe.renderers[0].new_output() for _ in frames]
+        pipe.render_many(frames, outs)
+        pipe.render_many(frames[::-1], outs[::-1])   # reuse every workspace again
+        torch.cuda.synchronize()
+        for ref, o in zip(refs, outs):
+            assert torch.equal(ref, o)
