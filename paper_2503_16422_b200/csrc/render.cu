@@ -14,6 +14,7 @@
 //                    early exit
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "fdgs_internal.h"
 
@@ -823,6 +824,20 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restr
 }
 
 // ---------------------------------------------------------------- launcher
+// Persistent-grid sizes (blocks per SM); FDGS_PGRID / FDGS_RGRID override for tuning.
+static int tune_env(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return e ? std::max(1, atoi(e)) : dflt;
+}
+static int tune_pgrid() {
+    static const int v = tune_env("FDGS_PGRID", 1);
+    return v;
+}
+static int tune_rgrid() {
+    static const int v = tune_env("FDGS_RGRID", 1);
+    return v;
+}
+
 cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint32_t *mask_r, const CamDev &cam,
                           float t, float *out_rgb, float *out_T, char *ws, const RenderLayout &L,
                           fdgs_frame_stats *stats, cudaStream_t st, cudaEvent_t const *ev, cudaStream_t blend_st,
@@ -856,7 +871,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     for (int pass = 0; pass < 4; ++pass) {
         const uint32_t *kin = pass == 0 ? depth : keys[(pass - 1) & 1];
         const uint32_t *vin = pass == 0 ? nullptr : vals[(pass - 1) & 1];
-        k_onesweep<8, kDItems><<<std::min(L.sort_parts, 4 * L.p_sort), kSortThreads, 0, st>>>(
+        k_onesweep<8, kDItems><<<std::min(L.sort_parts, tune_pgrid() * L.p_sort), kSortThreads, 0, st>>>(
             kin, vin, pass == 3 ? nullptr : keys[pass & 1], vals[pass & 1], &ctr->n_vis, epoch,
             &ctr->sort_ticket[1 + pass], 8 * pass, gbase + 256 * pass,
             sstat + (size_t)pass * L.sort_parts * 256, rect, pass == 3 ? rect_sorted : nullptr);
@@ -882,13 +897,13 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     k_bin_scan<<<std::max(1, (L.n + 1023) / 1024), 1024, 0, st>>>(rect_sorted, order, rec0, rec1, ctr,
                                                                    &ctr->bin_ticket, elb, roff, rcfirst, item_chunks,
                                                                    &ctr->n_items, bconst);
-    k_row_scan<<<(int)std::min<uint32_t>(item_chunks, 2 * L.p_sort), 1024, 0, st>>>(
+    k_row_scan<<<(int)std::min<uint32_t>(item_chunks, tune_rgrid() * L.p_sort), 1024, 0, st>>>(
         rect_sorted, order, rec0, rec1, bconst, roff, rcfirst, ctr, &ctr->n_items,
                                                   L.tiles_x, &ctr->row_ticket, rlb, diff, ipack, iv, eoff, cfirst,
                                                   (uint32_t)L.tile_parts, (uint32_t)L.max_entries);
     const size_t scan_smem = sizeof(int) * (size_t)(L.tiles_x + 1) * (L.tiles_y + 1);
     k_tile_scan<<<1, 1024, scan_smem, st>>>(diff, L.tiles_x, L.tiles_y, tstart, tbase, ctr, L.max_entries);
-    const int pgrid = 4 * L.p_sort;  // persistent grids
+    const int pgrid = tune_pgrid() * L.p_sort;  // persistent grids
     k_emit<<<pgrid, 256, 0, st>>>(ipack, iv, eoff, cfirst, ctr, &ctr->n_items, L.tiles_x, ek[0], evl[0]);
     k_onesweep<7, kTItems><<<pgrid, kSortThreads, 0, st>>>(ek[0], evl[0], ek[1], evl[1], &ctr->n_sort_entries, epoch,
                                                            &ctr->tile_ticket[0], 0, tbase, tstat, nullptr, nullptr);
