@@ -67,8 +67,8 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.lookback = take(sizeof(uint32_t) * (size_t)std::max(L.n_parts, 1));
     L.sort_gbase = take(sizeof(uint32_t) * 4 * 256);
     L.tile_diff = take(sizeof(int) * (size_t)(L.tiles_x + 1) * (L.tiles_y + 1));
-    L.emit_lb = take(sizeof(uint32_t) * ((nn + 1023) / 1024));
-    L.row_lb = take(sizeof(uint32_t) * ((cap + 1023) / 1024));
+    L.emit_lb = take(sizeof(uint32_t) * ((nn + 255) / 256));
+    L.row_lb = take(sizeof(uint32_t) * ((cap + 255) / 256));
     L.zero_end = off;
     // persistent (zero-filled once)
     L.epoch = take(sizeof(uint32_t));
@@ -89,7 +89,7 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.tile_start = take(sizeof(uint32_t) * ((size_t)L.n_tiles + 1));
     L.band_consts = take(sizeof(BandConsts) * nn);          // tile-cover constants per Gaussian
     L.roff = take(4 * nn);                                  // row-item offset per Gaussian
-    L.rchunk_first = take(4 * ((cap + 1023) / 1024 + 1));    // first Gaussian of each item chunk
+    L.rchunk_first = take(4 * ((cap + 255) / 256 + 1));      // first Gaussian of each item chunk
     L.item_pack = take(4 * cap);                            // (ty, txa, txb) per row item
     L.item_v = take(4 * cap);                               // visible slot per row item
     L.emit_off = take(4 * cap);                             // entry offset per row item

@@ -352,8 +352,9 @@ __device__ __forceinline__ TileRect tile_rect(uint2 r) {
 // Row 5b (1/5): tile rows per Gaussian (ny of its pixel AABB) in canonical
 // order -> their exclusive scan = row-item offsets (single pass, warp
 // look-back), and the first Gaussian of every row-item chunk.
-constexpr int kItemTile = 1024;  // row items per chunk / partition
-__global__ void __launch_bounds__(1024) k_bin_scan(const uint2 *__restrict__ rects, const uint32_t *__restrict__ order,
+constexpr int kScanNT = 256;     // threads (= items) per scan partition
+constexpr int kItemTile = kScanNT;  // row items per chunk / partition
+__global__ void __launch_bounds__(kScanNT) k_bin_scan(const uint2 *__restrict__ rects, const uint32_t *__restrict__ order,
                                                    const float4 *__restrict__ rec0, const float4 *__restrict__ rec1,
                                                    const Counters *ctrc, uint32_t *ticket, uint32_t *lb,
                                                    uint32_t *__restrict__ off, uint32_t *__restrict__ chunk_first,
@@ -366,8 +367,8 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const uint2 *__restrict__ rec
     if (tid == 0) s_part = atomicAdd(ticket, 1u);
     __syncthreads();
     const uint32_t part = s_part;
-    if (part * 1024 >= n) return;
-    const uint32_t i = part * 1024 + tid;
+    if (part * kScanNT >= n) return;
+    const uint32_t i = part * kScanNT + tid;
     uint32_t c = 0;
     if (i < n) {
         const uint2 rc = __ldg(rects + i);
@@ -385,18 +386,18 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const uint2 *__restrict__ rec
     if (lane == 31) s_w[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-        uint32_t w = s_w[lane], wi = w;
+        uint32_t w = lane < kScanNT / 32 ? s_w[lane] : 0u, wi = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
             if (lane >= o) wi += y;
         }
-        s_w[lane] = wi - w;
+        if (lane < kScanNT / 32) s_w[lane] = wi - w;
         const uint32_t tot = __shfl_sync(0xffffffffu, wi, 31);
         const uint32_t excl = lookback_warp(lb, part, tot, lane);
         if (lane == 0) {
             s_excl = excl;
-            if ((part + 1) * 1024 >= n) *n_items = excl + tot;  // last partition
+            if ((part + 1) * kScanNT >= n) *n_items = excl + tot;  // last partition
         }
     }
     __syncthreads();
@@ -412,7 +413,7 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const uint2 *__restrict__ rec
 // cover [txa, txb] of the row (band_tiles, binary64 pinned), its entry count,
 // the per-row difference array of the tile counts, and the exclusive scan of
 // the counts (look-back) = emission offsets + first item of every entry chunk.
-__global__ void __launch_bounds__(1024) k_row_scan(const uint2 *__restrict__ rects, const uint32_t *__restrict__ order,
+__global__ void __launch_bounds__(kScanNT) k_row_scan(const uint2 *__restrict__ rects, const uint32_t *__restrict__ order,
                                                    const float4 *__restrict__ rec0, const float4 *__restrict__ rec1,
                                                    const BandConsts *__restrict__ bconst,
                                                    const uint32_t *__restrict__ roff,
@@ -477,13 +478,13 @@ __global__ void __launch_bounds__(1024) k_row_scan(const uint2 *__restrict__ rec
     if (lane == 31) s_w[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-        uint32_t w = s_w[lane], wi = w;
+        uint32_t w = lane < kScanNT / 32 ? s_w[lane] : 0u, wi = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
             if (lane >= o) wi += y;
         }
-        s_w[lane] = wi - w;
+        if (lane < kScanNT / 32) s_w[lane] = wi - w;
         const uint32_t tot = __shfl_sync(0xffffffffu, wi, 31);
         const uint32_t excl = lookback_warp(lb, part, tot, lane);
         if (lane == 0) s_excl = excl;
@@ -892,12 +893,12 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     uint32_t *ipack = reinterpret_cast<uint32_t *>(ws + L.item_pack);
     uint32_t *iv = reinterpret_cast<uint32_t *>(ws + L.item_v);
     uint32_t *rlb = reinterpret_cast<uint32_t *>(ws + L.row_lb);
-    const uint32_t item_chunks = (uint32_t)((L.max_entries + 1023) / 1024);
+    const uint32_t item_chunks = (uint32_t)((L.max_entries + kItemTile - 1) / kItemTile);
     BandConsts *bconst = reinterpret_cast<BandConsts *>(ws + L.band_consts);
-    k_bin_scan<<<std::max(1, (L.n + 1023) / 1024), 1024, 0, st>>>(rect_sorted, order, rec0, rec1, ctr,
+    k_bin_scan<<<std::max(1, (L.n + kScanNT - 1) / kScanNT), kScanNT, 0, st>>>(rect_sorted, order, rec0, rec1, ctr,
                                                                    &ctr->bin_ticket, elb, roff, rcfirst, item_chunks,
                                                                    &ctr->n_items, bconst);
-    k_row_scan<<<(int)std::min<uint32_t>(item_chunks, tune_rgrid() * L.p_sort), 1024, 0, st>>>(
+    k_row_scan<<<(int)std::min<uint32_t>(item_chunks, tune_rgrid() * L.p_sort), kScanNT, 0, st>>>(
         rect_sorted, order, rec0, rec1, bconst, roff, rcfirst, ctr, &ctr->n_items,
                                                   L.tiles_x, &ctr->row_ticket, rlb, diff, ipack, iv, eoff, cfirst,
                                                   (uint32_t)L.tile_parts, (uint32_t)L.max_entries);
