@@ -669,30 +669,33 @@ __device__ __forceinline__ void stage_load(const uint32_t *__restrict__ entries,
 // This is pure culling: the margin (1e-3 relative to the quadratic's
 // magnitude, + 1e-3) exceeds the rounding of both this test and the pinned
 // fp32 e2 chain, so no pixel with e2 >= 0 is dropped.
+__device__ __forceinline__ void stage_fields(int tx, int ty, const float4 &r0, const float4 &r1, const float4 &r2,
+                                             float4 &oa, float4 &oc, float4 &od) {
+    const uint32_t ax = __float_as_uint(r1.z), ay = __float_as_uint(r1.w);
+    const int x0 = max((int)(ax & 0xffff) - tx * 16, 0), x1 = min((int)(ax >> 16) - tx * 16, 15);
+    const int y0 = max((int)(ay & 0xffff) - ty * 16, 0), y1 = min((int)(ay >> 16) - ty * 16, 15);
+    const uint32_t xm = ((2u << x1) - 1u) & ~((1u << x0) - 1u);
+    const uint32_t ym = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
+    uint32_t yr = 0;
+    const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
+    const float dxl = (float)(tx * 16 + x0) + 0.5f - u, dxr = (float)(tx * 16 + x1) + 0.5f - u;
+    const float dxm = fmaxf(fabsf(dxl), fabsf(dxr));
+    const float hA = -0.5f / Ap;  // A' < 0
+    for (int r = y0; r <= y1; ++r) {
+        const float dy = (float)(ty * 16 + r) + 0.5f - v;
+        const float dx = fminf(fmaxf(Bp * dy * hA, dxl), dxr);
+        const float f = fmaf(dx, fmaf(Ap, dx, Bp * dy), fmaf(Cp * dy, dy, Q2));
+        const float mag = fabsf(Ap) * dxm * dxm + fabsf(Bp) * dxm * fabsf(dy) + fabsf(Cp) * dy * dy;
+        if (f >= -(1e-3f * mag + 1e-3f)) yr |= 1u << r;
+    }
+    oa = r0;
+    oc = make_float4(r1.x, r1.y, r2.x, r2.y);
+    od = make_float4(r2.z, __uint_as_float(xm | (ym << 16)), __uint_as_float(yr << 16), 0.0f);
+}
+
 __device__ __forceinline__ void stage_store(BlendBatch &B, int tid, uint32_t k, uint32_t end, int tx, int ty,
                                             const float4 &r0, const float4 &r1, const float4 &r2) {
-    if (k < end) {
-        const uint32_t ax = __float_as_uint(r1.z), ay = __float_as_uint(r1.w);
-        const int x0 = max((int)(ax & 0xffff) - tx * 16, 0), x1 = min((int)(ax >> 16) - tx * 16, 15);
-        const int y0 = max((int)(ay & 0xffff) - ty * 16, 0), y1 = min((int)(ay >> 16) - ty * 16, 15);
-        const uint32_t xm = ((2u << x1) - 1u) & ~((1u << x0) - 1u);
-        const uint32_t ym = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
-        uint32_t yr = 0;
-        const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
-        const float dxl = (float)(tx * 16 + x0) + 0.5f - u, dxr = (float)(tx * 16 + x1) + 0.5f - u;
-        const float dxm = fmaxf(fabsf(dxl), fabsf(dxr));
-        const float hA = -0.5f / Ap;  // A' < 0
-        for (int r = y0; r <= y1; ++r) {
-            const float dy = (float)(ty * 16 + r) + 0.5f - v;
-            const float dx = fminf(fmaxf(Bp * dy * hA, dxl), dxr);
-            const float f = fmaf(dx, fmaf(Ap, dx, Bp * dy), fmaf(Cp * dy, dy, Q2));
-            const float mag = fabsf(Ap) * dxm * dxm + fabsf(Bp) * dxm * fabsf(dy) + fabsf(Cp) * dy * dy;
-            if (f >= -(1e-3f * mag + 1e-3f)) yr |= 1u << r;
-        }
-        B.a[tid] = r0;
-        B.c[tid] = make_float4(r1.x, r1.y, r2.x, r2.y);
-        B.d[tid] = make_float4(r2.z, __uint_as_float(xm | (ym << 16)), __uint_as_float(yr << 16), 0.0f);
-    }
+    if (k < end) stage_fields(tx, ty, r0, r1, r2, B.a[tid], B.c[tid], B.d[tid]);
 }
 
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
@@ -824,18 +827,200 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restr
     }
 }
 
+// Warp-specialised blend: one producer warp stages records 32 at a time into
+// a ring of kWsBuf shared-memory batches (gathers + the row-culling mask), four
+// consumer warps composite them.  Full/empty mbarriers replace block-wide
+// barriers, so consumer warps drift independently; a consumer whose pixels
+// have all terminated keeps releasing batches without computing, and the
+// producer stops once all four are done.  Pixel mapping and arithmetic are
+// those of k_blend.
+constexpr int kWsBuf = 6;
+constexpr int kWsThreads = 160;
+struct WsBatch {
+    float4 a[32], c[32], d[32];
+};
+
+__device__ __forceinline__ void mb_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mb_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t *bar, uint32_t parity) {
+    const uint32_t addr = (uint32_t)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+
+template <bool kCount>
+__global__ void __launch_bounds__(kWsThreads) k_blend_ws(const uint32_t *__restrict__ tile_start,
+                                                         const uint32_t *__restrict__ entries,
+                                                         const float4 *__restrict__ rec0,
+                                                         const float4 *__restrict__ rec1,
+                                                         const float4 *__restrict__ rec2, Counters *ctr, int tiles_x,
+                                                         int width, int height, float bg0, float bg1, float bg2,
+                                                         float *__restrict__ out_rgb, float *__restrict__ out_T,
+                                                         fdgs_frame_stats *stats) {
+    __shared__ WsBatch sb[kWsBuf];
+    __shared__ uint32_t s_n[kWsBuf];
+    __shared__ __align__(8) uint64_t full[kWsBuf], empty[kWsBuf];
+    __shared__ uint32_t s_done;
+    __shared__ bool s_last;
+    const bool ok = ctr->status == FDGS_OK;
+    const int tile = blockIdx.x, tx = tile % tiles_x, ty = tile / tiles_x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t start = __ldg(tile_start + tile), end = __ldg(tile_start + tile + 1);
+    if (tid == 0) {
+        for (int b = 0; b < kWsBuf; ++b) {
+            mb_init(&full[b], 1);
+            mb_init(&empty[b], 4);
+        }
+        s_done = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t first = ok ? start : end;
+    if (warp == 4) {  // ------------------------------------------------ producer
+        uint32_t k = 0;
+        for (uint32_t base = first;; base += 32, ++k) {
+            const int b = (int)(k % kWsBuf);
+            if (k >= kWsBuf) mb_wait(&empty[b], ((k / kWsBuf) - 1) & 1);
+            const bool stop = base >= end || *(volatile uint32_t *)&s_done == 4;
+            const uint32_t n = stop ? 0u : min(32u, end - base);
+            if (lane < (int)n) {
+                const uint32_t v = __ldg(entries + base + lane);
+                const float4 r0 = __ldg(rec0 + v), r1 = __ldg(rec1 + v), r2 = __ldg(rec2 + v);
+                stage_fields(tx, ty, r0, r1, r2, sb[b].a[lane], sb[b].c[lane], sb[b].d[lane]);
+            }
+            if (lane == 0) s_n[b] = n;
+            __syncwarp();
+            if (lane == 0) mb_arrive(&full[b]);
+            if (n == 0) break;
+        }
+    } else {  // --------------------------------------------------------- consumers
+        const int ly = tid >> 3, lx = (tid & 7) * 2;
+        const int i0 = tx * 16 + lx, j = ty * 16 + ly;
+        const bool in0 = i0 < width && j < height, in1 = i0 + 1 < width && j < height;
+        const float pyf = (float)j + 0.5f;
+        const float2 px = make_float2((float)i0 + 0.5f, (float)(i0 + 1) + 0.5f);
+        const uint32_t pb0 = (1u << lx) | (1u << (16 + ly)), pb1 = (2u << lx) | (1u << (16 + ly));
+        const uint32_t wrows = 0xFu << (16 + 4 * warp);
+        const float kInf = __int_as_float(0x7f800000);
+        float2 thr = make_float2(in0 ? 0.0f : kInf, in1 ? 0.0f : kInf);
+        float2 T = make_float2(1.0f, 1.0f), Cr = make_float2(0.f, 0.f), Cg = Cr, Cb = Cr;
+        uint32_t n_eval = 0, n_blend = 0;
+        bool wdone = false;
+        for (uint32_t k = 0;; ++k) {
+            const int b = (int)(k % kWsBuf);
+            mb_wait(&full[b], (k / kWsBuf) & 1);
+            const int cnt = (int)s_n[b];
+            if (cnt == 0) break;
+            if (!wdone) {
+                const WsBatch &B = sb[b];
+                for (int q = 0; q < cnt; ++q) {
+                    const float4 dq = B.d[q];
+                    const uint32_t m = __float_as_uint(dq.y);
+                    if (kCount)
+                        n_eval += (uint32_t)((m & pb0) == pb0 && thr.x == 0.0f) +
+                                  (uint32_t)((m & pb1) == pb1 && thr.y == 0.0f);
+                    if ((__float_as_uint(dq.z) & wrows) == 0) continue;
+                    const float4 a = B.a[q];
+                    const float4 c = B.c[q];
+                    const float dy = __fsub_rn(pyf, a.y);
+                    const float t1 = __fmul_rn(a.w, dy);
+                    const float t3 = __fmul_rn(c.x, dy);
+                    const float t4 = __fmaf_rn(t3, dy, c.y);
+                    const float2 dx = sub2(px, make_float2(a.x, a.x));
+                    const float2 t2 = fma2(make_float2(a.z, a.z), dx, make_float2(t1, t1));
+                    const float2 e2 = fma2(dx, t2, make_float2(t4, t4));
+                    const bool v0 = (m & pb0) == pb0 && e2.x >= thr.x, v1 = (m & pb1) == pb1 && e2.y >= thr.y;
+                    if (!(v0 || v1)) continue;
+                    const float a0 = v0 ? fminf(0.99f, ex2_approx(e2.x) * (1.0f / 255.0f)) : 0.0f;
+                    const float a1 = v1 ? fminf(0.99f, ex2_approx(e2.y) * (1.0f / 255.0f)) : 0.0f;
+                    float2 w = mul2(make_float2(a0, a1), T);
+                    const float2 test = sub2(T, w);
+                    const bool s0 = v0 && test.x < 1e-4f, s1 = v1 && test.y < 1e-4f;
+                    w.x = s0 ? 0.0f : w.x;
+                    w.y = s1 ? 0.0f : w.y;
+                    thr.x = s0 ? kInf : thr.x;
+                    thr.y = s1 ? kInf : thr.y;
+                    if (kCount) n_blend += (uint32_t)(v0 && !s0) + (uint32_t)(v1 && !s1);
+                    T = sub2(T, w);
+                    Cr = fma2(make_float2(c.z, c.z), w, Cr);
+                    Cg = fma2(make_float2(c.w, c.w), w, Cg);
+                    Cb = fma2(make_float2(dq.x, dq.x), w, Cb);
+                }
+                wdone = __all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf);
+                if (wdone && lane == 0) atomicAdd(&s_done, 1u);
+            }
+            __syncwarp();
+            if (lane == 0) mb_arrive(&empty[b]);
+        }
+        if (kCount) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                n_eval += __shfl_xor_sync(0xffffffffu, n_eval, o);
+                n_blend += __shfl_xor_sync(0xffffffffu, n_blend, o);
+            }
+            if (lane == 0 && n_eval) {
+                atomicAdd(&ctr->n_eval, (unsigned long long)n_eval);
+                atomicAdd(&ctr->n_blend, (unsigned long long)n_blend);
+            }
+        }
+        if (ok) {
+            const size_t hw = (size_t)width * height, p = (size_t)j * width + i0;
+            if (in0) {
+                out_rgb[p] = fmaf(T.x, bg0, Cr.x);
+                out_rgb[hw + p] = fmaf(T.x, bg1, Cg.x);
+                out_rgb[2 * hw + p] = fmaf(T.x, bg2, Cb.x);
+                if (out_T) out_T[p] = T.x;
+            }
+            if (in1) {
+                out_rgb[p + 1] = fmaf(T.y, bg0, Cr.y);
+                out_rgb[hw + p + 1] = fmaf(T.y, bg1, Cg.y);
+                out_rgb[2 * hw + p + 1] = fmaf(T.y, bg2, Cb.y);
+                if (out_T) out_T[p + 1] = T.y;
+            }
+        }
+    }
+    if (kCount) {
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) s_last = atomicAdd(&ctr->blend_ticket, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (s_last && tid == 0 && stats != nullptr) {
+            __threadfence();
+            volatile Counters *vc = ctr;
+            stats->n_act = vc->n_act;
+            stats->n_vis = vc->n_vis;
+            stats->n_entries = vc->n_entries;
+            stats->status = vc->status;
+            stats->n_evaluated = vc->n_eval;
+            stats->n_blended = vc->n_blend;
+        }
+    }
+}
+
 // ---------------------------------------------------------------- launcher
 // Persistent-grid sizes (blocks per SM); FDGS_PGRID / FDGS_RGRID override for tuning.
 static int tune_env(const char *name, int dflt) {
     const char *e = getenv(name);
-    return e ? std::max(1, atoi(e)) : dflt;
+    return e ? std::max(0, atoi(e)) : dflt;
 }
 static int tune_pgrid() {
-    static const int v = tune_env("FDGS_PGRID", 1);
+    static const int v = std::max(1, tune_env("FDGS_PGRID", 1));
     return v;
 }
 static int tune_rgrid() {
-    static const int v = tune_env("FDGS_RGRID", 1);
+    static const int v = std::max(1, tune_env("FDGS_RGRID", 1));
     return v;
 }
 
@@ -919,7 +1104,17 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         bst = blend_st;
     }
     if (ev && (e = cudaEventRecord(ev[3], bst)) != cudaSuccess) return e;
-    if (stats != nullptr)
+    static const bool ws_blend = tune_env("FDGS_BLEND_WS", 1) == 1;  // FDGS_BLEND_WS=0: block-synchronous k_blend
+    if (ws_blend) {
+        if (stats != nullptr)
+            k_blend_ws<true><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x,
+                                                                L.width, L.height, cam.bg[0], cam.bg[1], cam.bg[2],
+                                                                out_rgb, out_T, stats);
+        else
+            k_blend_ws<false><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x,
+                                                                 L.width, L.height, cam.bg[0], cam.bg[1], cam.bg[2],
+                                                                 out_rgb, out_T, nullptr);
+    } else if (stats != nullptr)
         k_blend<true><<<L.n_tiles, kBlendThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
                                                             L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T,
                                                             stats);
