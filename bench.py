@@ -35,6 +35,27 @@ CONFIG = "c3"
 N_CAMS = 20
 N_FRAMES_T = 300
 INTERVAL = 20
+MASKED = True
+WORKLOADS = {
+    "c2": "c2: D-NeRF-shaped 100k 4D Gaussians, 800x800, 50 cams x 150 t, key-frame interval 10",
+    "c3": "c3: N3V-shaped 200k 4D Gaussians, 1352x1014, 20 cams x 300 t, key-frame interval 20",
+    "c4": "c4: N3V-shaped 3M 4D Gaussians (vanilla-4DGS scale), 1352x1014, 20 cams x 300 t, key-frame interval 20",
+}
+
+
+def apply_config(args):
+    """BASELINE configs[1..3]; c3 is the metric's named workload (the default)."""
+    global CONFIG, N_CAMS, N_FRAMES_T, INTERVAL, MASKED, METRIC
+    import fdgs_inputs as fi
+    CONFIG = args.config
+    cfg = fi.CONFIGS[CONFIG]
+    N_CAMS = {"hemisphere50": 50, "arc20": 20}[cfg["rig"]]
+    N_FRAMES_T = cfg["frames"]
+    INTERVAL = cfg["keyframe_interval"]
+    MASKED = not args.unmasked
+    if CONFIG != "c3" or not MASKED:
+        METRIC = (f"frames/sec at {cfg['width']}x{cfg['height']} ({CONFIG}, "
+                  f"{'masked' if MASKED else 'unmasked'})")
 
 
 def parse():
@@ -50,6 +71,8 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--streams", type=int, default=4, help="frame-pipelining depth (workspaces/streams)")
     p.add_argument("--no-split", action="store_true", help="blend on the front-end stream (no priority split)")
+    p.add_argument("--config", choices=["c2", "c3", "c4"], default="c3")
+    p.add_argument("--unmasked", action="store_true", help="render without the key-frame filter")
     return p.parse_args()
 
 
@@ -145,8 +168,10 @@ def cpu_oracle_run(scene, cams, masks, kf, frames, seconds, row_stride=8):
     t0 = time.perf_counter()
     while True:
         f, ti, ci = frames[k % len(frames)]
-        li, ri = bracket(kf, ti)
-        act = masks[li] | masks[ri]
+        act = None
+        if masks is not None:
+            li, ri = bracket(kf, ti)
+            act = masks[li] | masks[ri]
         oracle.render(scene, cams[ci], float(times[ti]), mask=act, pixels=pix)
         done_px += pix.size
         k += 1
@@ -156,7 +181,8 @@ def cpu_oracle_run(scene, cams, masks, kf, frames, seconds, row_stride=8):
     fps = done_px / (W * H) / el
     return fps, dict(cores=oracle.num_threads(), frames=k, seconds=round(el, 2),
                      sample=f"oracle per-pixel render of rows j%{row_stride}==0 ({pix.size} px) of {k} "
-                            f"consecutive masked C3 frames; fps = sampled pixels/(W*H)/wall")
+                            f"consecutive {'masked' if masks is not None else 'unmasked'} {CONFIG} frames; "
+                            f"fps = sampled pixels/(W*H)/wall")
 
 
 # ----------------------------------------------------------------- ours
@@ -227,6 +253,8 @@ def run_ours(args):
 
     def frame_args(x):
         f, ti, ci = x
+        if not MASKED:
+            return cam_structs[ci], float(times[ti]), None, None
         li, ri = fd.bracket(kf, ti)
         return cam_structs[ci], float(times[ti]), masks[li], masks[ri]
 
@@ -313,8 +341,8 @@ def run_ours(args):
     res = dict(metric=METRIC, value=round(value, 2), unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
                ms_per_step=round(total_ms / args.steps, 4), higher_is_better=True, scaling="weak", vs_baseline=None,
                dtype="f32 (decision path f64)", data="synthetic",
-               config={"workload": "c3: N3V-shaped 200k 4D Gaussians, 1352x1014, 20 cams x 300 t, "
-                                   "key-frame interval 20, masked (union of bracketing key-frames)",
+               config={"workload": WORKLOADS[CONFIG] + (", masked (union of bracketing key-frames)" if MASKED
+                                                         else ", unmasked"),
                        "frames_per_step": F, "frames_per_rank": frames_rank, "partition": "frame f -> rank f mod N",
                        "l2": "flushed between steps (512 MiB write)", "parallelism": f"frames x{world}",
                        "streams_per_gpu": args.streams,
@@ -383,7 +411,7 @@ def run_ours(args):
         h2d_bytes = d2h_bytes = 0
         for it in range(args.warmup + max(1, args.steps // 2)):
             fr = next_frames()
-            need = sorted({i for x in fr for i in fd.bracket(kf, x[1])})
+            need = sorted({i for x in fr for i in fd.bracket(kf, x[1])}) if MASKED else []
             flush.zero_()
             _t.cuda.synchronize()
             if world > 1:
@@ -397,7 +425,8 @@ def run_ours(args):
             for k, x in enumerate(fr):
                 f, ti, ci = x
                 li, ri = fd.bracket(kf, ti)
-                jobs.append((cam_structs[ci], float(times[ti]), dev_masks[li], dev_masks[ri]))
+                jobs.append((cam_structs[ci], float(times[ti]), dev_masks[li] if MASKED else None,
+                             dev_masks[ri] if MASKED else None))
             pipe.render_many(jobs, outs[:len(fr)], stream=stream)
             for k in range(len(fr)):
                 host_out[k].copy_(outs[k], non_blocking=True)
@@ -419,7 +448,8 @@ def run_ours(args):
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        fps, info = cpu_oracle_run(arrays, cams, masks.cpu().numpy().view(np.uint32), kf, mine, args.cpu_seconds)
+        fps, info = cpu_oracle_run(arrays, cams, masks.cpu().numpy().view(np.uint32) if MASKED else None, kf, mine,
+                                   args.cpu_seconds)
         res["cpu_baseline"] = {"value": round(fps, 5), "unit": UNIT, "cores": info["cores"], "kind": "oracle",
                                "sample": info["sample"]}
     if world > 1:
@@ -468,6 +498,7 @@ def run_reference(args):
 
 def main():
     args = parse()
+    apply_config(args)
     if args.impl == "reference":
         run_reference(args)
     else:

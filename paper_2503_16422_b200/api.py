@@ -67,7 +67,8 @@ def camera_struct(cam) -> FdgsCamera:
 
 
 def default_max_entries(n: int) -> int:
-    return int(min(2 ** 32 - 1, max(1 << 20, 64 * max(n, 1))))
+    """Entry capacity of a render workspace; render_checked grows it on overflow."""
+    return int(min(2 ** 32 - 1, max(1 << 22, 24 * max(n, 1))))
 
 
 def mask_words(n: int) -> int:
