@@ -49,7 +49,7 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.tiles_x = (width + FDGS_TILE - 1) / FDGS_TILE;
     L.tiles_y = (height + FDGS_TILE - 1) / FDGS_TILE;
     L.n_tiles = L.tiles_x * L.tiles_y;
-    L.n_parts = (n + kPreBlock - 1) / kPreBlock;
+    L.n_parts = (n + 2 * kPreBlock - 1) / (2 * kPreBlock);  // preprocess partitions (kPreItems)
     L.p_sort = sm_count();
     L.sort_parts = std::max(1, (n + kDepthTile - 1) / kDepthTile);
     L.tile_parts = (int32_t)std::max<int64_t>(1, (max_entries + kTileTile - 1) / kTileTile);
@@ -67,13 +67,13 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.lookback = take(sizeof(uint32_t) * (size_t)std::max(L.n_parts, 1));
     L.sort_gbase = take(sizeof(uint32_t) * 4 * 256);
     L.tile_diff = take(sizeof(int) * (size_t)(L.tiles_x + 1) * (L.tiles_y + 1));
+    L.row_diff = take(sizeof(int) * ((size_t)L.tiles_y + 1));
     L.emit_lb = take(sizeof(uint32_t) * ((nn + 255) / 256));
-    L.row_lb = take(sizeof(uint32_t) * ((cap + 255) / 256));
     L.zero_end = off;
     // persistent (zero-filled once)
     L.epoch = take(sizeof(uint32_t));
     L.sort_status = take(sizeof(uint64_t) * 4 * 256 * (size_t)L.sort_parts);
-    L.tile_status = take(sizeof(uint64_t) * 2 * 128 * (size_t)L.tile_parts);
+    L.tile_status = take(sizeof(uint64_t) * 2 * 256 * (size_t)L.tile_parts);
     // per-frame scratch, fully written before read
     L.rec0 = take(16 * nn);
     L.rec1 = take(16 * nn);
@@ -85,15 +85,15 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.keys1 = take(4 * nn);
     L.vals0 = take(4 * nn);
     L.vals1 = take(4 * nn);
-    L.tile_gbase = take(sizeof(uint32_t) * 256);
+    L.tile_gbase = take(sizeof(uint32_t) * 512);
     L.tile_start = take(sizeof(uint32_t) * ((size_t)L.n_tiles + 1));
+    L.row_start = take(sizeof(uint32_t) * ((size_t)L.tiles_y + 1));
+    L.row_hist = take(sizeof(uint32_t) * (size_t)L.tiles_y * kRowSeg * L.tiles_x);  // [tiles_y][kRowSeg][tiles_x]
     L.band_consts = take(sizeof(BandConsts) * nn);          // tile-cover constants per Gaussian
     L.roff = take(4 * nn);                                  // row-item offset per Gaussian
     L.rchunk_first = take(4 * ((cap + 255) / 256 + 1));      // first Gaussian of each item chunk
     L.item_pack = take(4 * cap);                            // (ty, txa, txb) per row item
     L.item_v = take(4 * cap);                               // visible slot per row item
-    L.emit_off = take(4 * cap);                             // entry offset per row item
-    L.chunk_first = take(4 * ((size_t)L.tile_parts + 1));   // first item of each entry chunk
     L.ekey0 = take(4 * cap);
     L.ekey1 = take(4 * cap);
     L.eval0 = take(4 * cap);

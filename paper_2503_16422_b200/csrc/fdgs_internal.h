@@ -11,8 +11,9 @@ namespace fdgs {
 
 constexpr int kPreBlock = 256;         // Gaussians per preprocess partition
 constexpr int kDepthTile = 1024;       // keys per depth-sort partition (256 threads x 4)
-constexpr int kTileSortItems = 8;      // entries per thread in the tile passes
+constexpr int kTileSortItems = 4;      // row items per thread in the row-partition passes
 constexpr int kTileTile = 256 * kTileSortItems;
+constexpr int kRowSeg = 4;             // blocks per tile row in the row scatter
 constexpr uint32_t kFlagA = 1u << 30;  // look-back: aggregate available
 constexpr uint32_t kFlagP = 2u << 30;  // look-back: inclusive prefix available
 constexpr uint32_t kValMask = (1u << 30) - 1;
@@ -51,12 +52,12 @@ struct RenderLayout {
     int32_t n_parts;     // preprocess partitions
     int32_t p_sort;      // SM count (grid of the histogram kernels)
     int32_t sort_parts;  // depth-sort partitions (upper bound from n)
-    int32_t tile_parts;  // tile-sort partitions (upper bound from max_entries)
+    int32_t tile_parts;  // row-partition partitions (upper bound from max_entries)
     int64_t max_entries;
-    size_t counters, lookback, sort_gbase, tile_diff, emit_lb, row_lb, zero_end;
+    size_t counters, lookback, sort_gbase, tile_diff, row_diff, emit_lb, zero_end;
     size_t epoch, sort_status, tile_status;
     size_t rec0, rec1, rec2, depth, rect, rect_sorted, keys0, keys1, vals0, vals1;
-    size_t tile_gbase, tile_start, band_consts, roff, rchunk_first, item_pack, item_v, emit_off, chunk_first, ekey0, ekey1, eval0, eval1, entries, total;
+    size_t tile_gbase, tile_start, row_start, row_hist, band_consts, roff, rchunk_first, item_pack, item_v, ekey0, ekey1, eval0, eval1, entries, total;
 };
 RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max_entries);
 

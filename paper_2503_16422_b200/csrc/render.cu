@@ -57,73 +57,145 @@ __device__ __forceinline__ uint32_t lookback_warp(uint32_t *status, uint32_t par
 }
 
 // ---------------------------------------------------------------- rows 1-4
+// A partition is kPreItems = 2 x 256 Gaussians.  Phase A culls all of them
+// cheaply (mask bit, then the temporal cull); the survivors are compacted in
+// shared memory (ascending index) so phase B runs the binary64 slice and
+// projection on dense survivors only, instead of diverging warps.
+constexpr int kPreItems = 2 * kPreBlock;
+struct PreRes {
+    float u, v, Ap, Bp, Cp, Q2, mx, my, mz;
+    uint32_t ax, ay, depth;
+    int i;
+};
+
 __global__ void __launch_bounds__(kPreBlock) k_preprocess(SceneDev sc, const uint32_t *__restrict__ mask_l,
                                                           const uint32_t *__restrict__ mask_r, CamDev cam, float t,
                                                           Counters *ctr, uint32_t *lb, float4 *__restrict__ rec0,
                                                           float4 *__restrict__ rec1, float4 *__restrict__ rec2,
                                                           uint32_t *__restrict__ depth, uint2 *__restrict__ rect) {
-    __shared__ uint32_t s_part, s_excl;
-    __shared__ uint32_t s_wvis[kPreBlock / 32], s_wact[kPreBlock / 32];
+    constexpr int NW = kPreBlock / 32;
+    __shared__ uint32_t s_part, s_excl, s_nsurv;
+    __shared__ uint32_t s_cnt[2][NW], s_act;
+    __shared__ uint16_t s_idx[kPreItems];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_part = atomicAdd(&ctr->part_ticket, 1u);
+    if (tid == 0) {
+        s_part = atomicAdd(&ctr->part_ticket, 1u);
+        s_act = 0;
+    }
     __syncthreads();
     const uint32_t part = s_part;
-    const int i = (int)part * kPreBlock + tid;
-    bool act = false;
-    if (i < sc.n) {
-        uint32_t w = 0xffffffffu;
-        if (mask_l != nullptr) {
-            w = __ldg(mask_l + (i >> 5));
-            if (mask_r != nullptr) w |= __ldg(mask_r + (i >> 5));
+    // ---- phase A: mask + temporal cull, survivors compacted in index order
+    uint32_t bal[2];
+    uint32_t nact = 0;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int i = (int)part * kPreItems + q * kPreBlock + tid;
+        bool act = false, surv = false;
+        if (i < sc.n) {
+            uint32_t w = 0xffffffffu;
+            if (mask_l != nullptr) {
+                w = __ldg(mask_l + (i >> 5));
+                if (mask_r != nullptr) w |= __ldg(mask_r + (i >> 5));
+            }
+            act = (w >> (i & 31)) & 1u;
+            if (act) surv = temporal_pass(__ldg(sc.mean + i), __ldg(sc.scale + i), __ldg(sc.rot_l + i),
+                                          __ldg(sc.rot_r + i), t);
         }
-        act = (w >> (i & 31)) & 1u;
+        nact += __popc(__ballot_sync(0xffffffffu, act));
+        bal[q] = __ballot_sync(0xffffffffu, surv);
+        if (lane == 0) s_cnt[q][warp] = __popc(bal[q]);
     }
-    Slice sl;
-    Proj pj;
-    int st = -1;
-    if (act) {
-        st = slice_gaussian(__ldg(sc.mean + i), __ldg(sc.scale + i), __ldg(sc.rot_l + i), __ldg(sc.rot_r + i),
-                            __ldg(sc.L + i), t, sl);
-        if (st == kNear) st = project_gaussian(sl, cam, pj);
-    }
-    const bool vis = st == kVisible;
-    const uint32_t bvis = __ballot_sync(0xffffffffu, vis);
-    const uint32_t bact = __ballot_sync(0xffffffffu, act);
-    if (lane == 0) {
-        s_wvis[warp] = __popc(bvis);
-        s_wact[warp] = __popc(bact);
+    if (lane == 0 && nact) atomicAdd(&s_act, nact);
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t run = 0;
+        for (int q = 0; q < 2; ++q)
+            for (int w = 0; w < NW; ++w) {
+                const uint32_t c = s_cnt[q][w];
+                s_cnt[q][w] = run;
+                run += c;
+            }
+        s_nsurv = run;
+        if (s_act) atomicAdd(&ctr->n_act, s_act);
     }
     __syncthreads();
-    if (warp == 0) {
-        uint32_t tot = 0, act_tot = 0, mine = 0;
 #pragma unroll
-        for (int w = 0; w < kPreBlock / 32; ++w) {
-            const uint32_t c = s_wvis[w];
-            if (w == lane) mine = tot;
-            tot += c;
-            act_tot += s_wact[w];
+    for (int q = 0; q < 2; ++q)
+        if ((bal[q] >> lane) & 1u)
+            s_idx[s_cnt[q][warp] + __popc(bal[q] & lanemask_lt())] = (uint16_t)(q * kPreBlock + tid);
+    __syncthreads();
+    // ---- phase B: slice + projection on the dense survivors
+    const uint32_t ns = s_nsurv;
+    PreRes res[2];
+    uint32_t vb[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const uint32_t sidx = r * kPreBlock + tid;
+        bool vis = false;
+        if (sidx < ns) {
+            const int i = (int)part * kPreItems + s_idx[sidx];
+            Slice sl;
+            Proj pj;
+            int st = slice_gaussian(__ldg(sc.mean + i), __ldg(sc.scale + i), __ldg(sc.rot_l + i), __ldg(sc.rot_r + i),
+                                    __ldg(sc.L + i), t, sl);
+            if (st == kNear) st = project_gaussian(sl, cam, pj);
+            vis = st == kVisible;
+            if (vis) {
+                res[r].u = pj.u;
+                res[r].v = pj.v;
+                res[r].Ap = pj.Ap;
+                res[r].Bp = pj.Bp;
+                res[r].Cp = pj.Cp;
+                res[r].Q2 = pj.Q2;
+                res[r].mx = (float)sl.mu3[0];
+                res[r].my = (float)sl.mu3[1];
+                res[r].mz = (float)sl.mu3[2];
+                res[r].ax = pj.px0 | (pj.px1 << 16);
+                res[r].ay = pj.py0 | (pj.py1 << 16);
+                res[r].depth = pj.depth_bits;
+                res[r].i = i;
+            }
         }
+        vb[r] = __ballot_sync(0xffffffffu, vis);
+    }
+    __syncthreads();  // s_cnt reuse
+    if (lane == 0) {
+        s_cnt[0][warp] = __popc(vb[0]);
+        s_cnt[1][warp] = __popc(vb[1]);
+    }
+    __syncthreads();
+    if (warp == 0) {  // survivor order = (round, warp, lane) = ascending Gaussian index
+        uint32_t run = 0, mine0 = 0, mine1 = 0;
+        for (int q = 0; q < 2; ++q)
+            for (int w = 0; w < NW; ++w) {
+                const uint32_t c = s_cnt[q][w];
+                if (w == lane) (q == 0 ? mine0 : mine1) = run;
+                run += c;
+            }
         __syncwarp();
-        if (lane < kPreBlock / 32) s_wvis[lane] = mine;
-        if (lane == 0 && act_tot) atomicAdd(&ctr->n_act, act_tot);
-        const uint32_t excl = lookback_warp(lb, part, tot, lane);
+        if (lane < NW) {
+            s_cnt[0][lane] = mine0;
+            s_cnt[1][lane] = mine1;
+        }
+        const uint32_t excl = lookback_warp(lb, part, run, lane);
         if (lane == 0) {
             s_excl = excl;
-            if (part == gridDim.x - 1) ctr->n_vis = excl + tot;
+            if (part == gridDim.x - 1) ctr->n_vis = excl + run;
         }
     }
     __syncthreads();
-    if (vis) {
-        const uint32_t pos = s_excl + s_wvis[warp] + __popc(bvis & lanemask_lt());
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        if (!((vb[r] >> lane) & 1u)) continue;
+        const PreRes &R = res[r];
+        const uint32_t pos = s_excl + s_cnt[r][warp] + __popc(vb[r] & lanemask_lt());
         float rgb[3];
-        sh_color(sc.sh + (size_t)i * 12, (float)sl.mu3[0] - cam.campos[0], (float)sl.mu3[1] - cam.campos[1],
-                 (float)sl.mu3[2] - cam.campos[2], rgb);
-        rec0[pos] = make_float4(pj.u, pj.v, pj.Ap, pj.Bp);
-        rec1[pos] = make_float4(pj.Cp, pj.Q2, __int_as_float(pj.px0 | (pj.px1 << 16)),
-                                __int_as_float(pj.py0 | (pj.py1 << 16)));
-        rec2[pos] = make_float4(rgb[0], rgb[1], rgb[2], __int_as_float(i));
-        depth[pos] = pj.depth_bits;
-        rect[pos] = make_uint2(pj.px0 | (pj.px1 << 16), pj.py0 | (pj.py1 << 16));
+        sh_color(sc.sh + (size_t)R.i * 12, R.mx - cam.campos[0], R.my - cam.campos[1], R.mz - cam.campos[2], rgb);
+        rec0[pos] = make_float4(R.u, R.v, R.Ap, R.Bp);
+        rec1[pos] = make_float4(R.Cp, R.Q2, __uint_as_float(R.ax), __uint_as_float(R.ay));
+        rec2[pos] = make_float4(rgb[0], rgb[1], rgb[2], __int_as_float(R.i));
+        depth[pos] = R.depth;
+        rect[pos] = make_uint2(R.ax, R.ay);
     }
 }
 
@@ -359,7 +431,7 @@ __global__ void __launch_bounds__(kScanNT) k_bin_scan(const uint2 *__restrict__ 
                                                    const Counters *ctrc, uint32_t *ticket, uint32_t *lb,
                                                    uint32_t *__restrict__ off, uint32_t *__restrict__ chunk_first,
                                                    uint32_t max_chunks, uint32_t *n_items,
-                                                   BandConsts *__restrict__ bconst) {
+                                                   BandConsts *__restrict__ bconst, int *__restrict__ rowdiff) {
     __shared__ uint32_t s_w[32];
     __shared__ uint32_t s_part, s_excl;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -372,7 +444,10 @@ __global__ void __launch_bounds__(kScanNT) k_bin_scan(const uint2 *__restrict__ 
     uint32_t c = 0;
     if (i < n) {
         const uint2 rc = __ldg(rects + i);
-        c = (uint32_t)tile_rect(rc).ny;
+        const TileRect tr = tile_rect(rc);
+        c = (uint32_t)tr.ny;
+        atomicAdd(&rowdiff[tr.ty0], 1);            // row-item counts per tile row (1D diff)
+        atomicAdd(&rowdiff[tr.ty0 + tr.ny], -1);
         const uint32_t v = __ldg(order + i);
         const float4 a = __ldg(rec0 + v), b = __ldg(rec1 + v);
         bconst[i] = band_consts(a.x, a.y, a.z, a.w, b.x, b.y, rc.x & 0xffff, rc.x >> 16, rc.y & 0xffff, rc.y >> 16);
@@ -409,110 +484,77 @@ __global__ void __launch_bounds__(kScanNT) k_bin_scan(const uint2 *__restrict__ 
     }
 }
 
-// Row 5b (2/5): one thread per row item (Gaussian r, tile row ty): the tile
-// cover [txa, txb] of the row (band_tiles, binary64 pinned), its entry count,
-// the per-row difference array of the tile counts, and the exclusive scan of
-// the counts (look-back) = emission offsets + first item of every entry chunk.
-__global__ void __launch_bounds__(kScanNT) k_row_scan(const uint2 *__restrict__ rects, const uint32_t *__restrict__ order,
-                                                   const float4 *__restrict__ rec0, const float4 *__restrict__ rec1,
-                                                   const BandConsts *__restrict__ bconst,
-                                                   const uint32_t *__restrict__ roff,
-                                                   const uint32_t *__restrict__ rchunk_first,
-                                                   const Counters *ctrc, const uint32_t *n_items_ptr, int tiles_x,
-                                                   uint32_t *ticket, uint32_t *lb, int *__restrict__ diff,
-                                                   uint32_t *__restrict__ item_pack, uint32_t *__restrict__ item_v,
-                                                   uint32_t *__restrict__ eoff, uint32_t *__restrict__ echunk_first,
-                                                   uint32_t max_echunks, uint32_t item_cap) {
+// Row 5b (2/6): one thread per row item (Gaussian r, tile row ty): its tile
+// cover [txa, txb] (band_tiles, binary64 pinned), the row key for the stable
+// row partition, and the per-row difference array of the per-tile counts.
+// Items are in canonical order (Gaussian-major, rows ascending).
+__global__ void __launch_bounds__(kScanNT) k_row_items(const uint2 *__restrict__ rects,
+                                                       const uint32_t *__restrict__ order,
+                                                       const float4 *__restrict__ rec0,
+                                                       const float4 *__restrict__ rec1,
+                                                       const BandConsts *__restrict__ bconst,
+                                                       const uint32_t *__restrict__ roff,
+                                                       const uint32_t *__restrict__ rchunk_first,
+                                                       const Counters *ctrc, const uint32_t *n_items_ptr, int tiles_x,
+                                                       int *__restrict__ diff, uint32_t *__restrict__ item_key,
+                                                       uint32_t *__restrict__ item_pack, uint32_t *__restrict__ item_v,
+                                                       uint32_t item_cap) {
     __shared__ uint32_t s_off[kItemTile + 1];
-    __shared__ uint32_t s_w[32];
-    __shared__ uint32_t s_part, s_excl;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     const uint32_t n = ctrc->n_vis, ni = *n_items_ptr;
     if (ni > item_cap) {  // more row items than the workspace holds
         if (blockIdx.x == 0 && tid == 0) const_cast<Counters *>(ctrc)->status = FDGS_ERR_OVERFLOW;
         return;
     }
-    while (true) {  // persistent: partitions in ticket order
-    if (tid == 0) s_part = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const uint32_t part = s_part;
-    if (part * kItemTile >= ni) return;
-    // window of Gaussians owning this chunk's items (each owns >= 1 item)
-    const uint32_t r0 = __ldg(rchunk_first + part);
-    const uint32_t m = min((uint32_t)kItemTile, n - r0);
-    for (uint32_t q = tid; q < m; q += blockDim.x) s_off[q] = __ldg(roff + r0 + q);
-    if (tid == 0) s_off[m] = 0xffffffffu;
-    __syncthreads();
-    const uint32_t i = part * kItemTile + tid;
-    uint32_t c = 0;
-    if (i < ni) {
-        int lo = 0, hi = (int)m - 1;  // largest q with s_off[q] <= i
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_off[mid] <= i) lo = mid; else hi = mid - 1;
+    for (uint32_t part = blockIdx.x; part * kItemTile < ni; part += gridDim.x) {
+        // window of Gaussians owning this chunk's items (each owns >= 1 item)
+        const uint32_t r0 = __ldg(rchunk_first + part);
+        const uint32_t m = min((uint32_t)kItemTile, n - r0);
+        for (uint32_t q = tid; q < m; q += blockDim.x) s_off[q] = __ldg(roff + r0 + q);
+        __syncthreads();
+        const uint32_t i = part * kItemTile + tid;
+        if (i < ni) {
+            int lo = 0, hi = (int)m - 1;  // largest q with s_off[q] <= i
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_off[mid] <= i) lo = mid; else hi = mid - 1;
+            }
+            const uint32_t r = r0 + lo;
+            const uint2 rc = __ldg(rects + r);
+            const int px0 = rc.x & 0xffff, px1 = rc.x >> 16, py0 = rc.y & 0xffff, py1 = rc.y >> 16;
+            const int ty = (py0 >> 4) + (int)(i - s_off[lo]);
+            const uint32_t v = __ldg(order + r);
+            const float4 a = __ldg(rec0 + v), b = __ldg(rec1 + v);
+            int txa, txb;
+            uint32_t pack = 0u;  // empty row: txb + 1 <= txa
+            if (band_tiles(bconst[r], a.x, a.y, a.z, a.w, b.x, px0, px1, py0, py1, ty, txa, txb)) {
+                pack = (uint32_t)txa | ((uint32_t)(txb + 1) << 16);
+                atomicAdd(&diff[ty * (tiles_x + 1) + txa], 1);
+                atomicAdd(&diff[ty * (tiles_x + 1) + txb + 1], -1);
+            }
+            item_key[i] = (uint32_t)ty;
+            item_pack[i] = pack;
+            item_v[i] = v;
         }
-        const uint32_t r = r0 + lo;
-        const uint2 rc = __ldg(rects + r);
-        const int px0 = rc.x & 0xffff, px1 = rc.x >> 16, py0 = rc.y & 0xffff, py1 = rc.y >> 16;
-        const int ty = (py0 >> 4) + (int)(i - s_off[lo]);
-        const uint32_t v = __ldg(order + r);
-        const float4 a = __ldg(rec0 + v), b = __ldg(rec1 + v);
-        int txa, txb;
-        uint32_t pack = 0xffffffffu;  // empty row
-        const BandConsts bc = bconst[r];
-        if (band_tiles(bc, a.x, a.y, a.z, a.w, b.x, px0, px1, py0, py1, ty, txa, txb)) {
-            c = (uint32_t)(txb - txa + 1);
-            pack = (uint32_t)ty | ((uint32_t)txa << 11) | ((uint32_t)txb << 22);  // tiles_x, tiles_y <= 512
-            atomicAdd(&diff[ty * (tiles_x + 1) + txa], 1);
-            atomicAdd(&diff[ty * (tiles_x + 1) + txb + 1], -1);
-        }
-        item_pack[i] = pack;
-        item_v[i] = v;
-    }
-    uint32_t incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_w[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t w = lane < kScanNT / 32 ? s_w[lane] : 0u, wi = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= o) wi += y;
-        }
-        if (lane < kScanNT / 32) s_w[lane] = wi - w;
-        const uint32_t tot = __shfl_sync(0xffffffffu, wi, 31);
-        const uint32_t excl = lookback_warp(lb, part, tot, lane);
-        if (lane == 0) s_excl = excl;
-    }
-    __syncthreads();
-    if (i < ni) {
-        const uint32_t o = s_excl + s_w[warp] + incl - c;
-        eoff[i] = o;
-        for (uint32_t k = (o + kTileTile - 1) / kTileTile; k * kTileTile < o + c && k < max_echunks; ++k)
-            echunk_first[k] = i;
-    }
-    __syncthreads();
+        __syncthreads();
     }
 }
 
-// Row 5b (3/5), one block: per-row prefix of the difference array -> per-tile
-// counts -> tile_start[0..T] and E (capacity check), and the exclusive digit
-// bases of the two tile passes (low 7 bits, then the high bits).
-__global__ void __launch_bounds__(1024) k_tile_scan(const int *__restrict__ diff, int tiles_x, int tiles_y,
-                                                    uint32_t *__restrict__ tile_start, uint32_t *__restrict__ tbase,
+// Row 5b (3/6), one block: per-row prefix of the tile difference array ->
+// per-tile counts -> tile_start[0..T] and E (capacity check); prefix of the
+// row-item difference array -> row_start[0..tiles_y] and the exclusive digit
+// bases of the row partition passes (digit ty & 255, then ty >> 8).
+__global__ void __launch_bounds__(1024) k_tile_scan(const int *__restrict__ diff, const int *__restrict__ rowdiff,
+                                                    int tiles_x, int tiles_y, uint32_t *__restrict__ tile_start,
+                                                    uint32_t *__restrict__ row_start, uint32_t *__restrict__ rbase,
                                                     Counters *ctr, int64_t max_entries) {
     extern __shared__ int sm[];  // tiles_y x (tiles_x + 1)
     __shared__ uint32_t s_sum[1024];
-    __shared__ uint32_t s_dig[2][128];
+    __shared__ uint32_t s_rows[512 + 1];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gx = tiles_x + 1, T = tiles_x * tiles_y;
     for (int k = tid; k < gx * tiles_y; k += blockDim.x) sm[k] = __ldcg(diff + k);
-    if (tid < 256) s_dig[tid >> 7][tid & 127] = 0;
+    if (tid <= tiles_y) s_rows[tid] = (uint32_t)__ldcg(rowdiff + tid);
     __syncthreads();
     for (int y = warp; y < tiles_y; y += 32) {  // row prefix, one warp per row
         int run = 0;
@@ -528,16 +570,30 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const int *__restrict__ diff
             run += __shfl_sync(0xffffffffu, val, 31);
         }
     }
+    if (tid == 1023) {  // row-item counts per tile row -> row starts and digit bases
+        int run = 0;
+        uint32_t start = 0, hi1 = 0;
+        for (int y = 0; y < tiles_y; ++y) {
+            run += (int)s_rows[y];          // items in row y
+            row_start[y] = start;
+            start += (uint32_t)run;
+            if (y < 256) hi1 += (uint32_t)run;
+            s_rows[y] = (uint32_t)run;
+        }
+        row_start[tiles_y] = start;
+        uint32_t acc = 0;
+        for (int d = 0; d < 256; ++d) {  // pass 0: digit = ty & 255
+            rbase[d] = acc;
+            acc += (d < tiles_y ? s_rows[d] : 0u) + (d + 256 < tiles_y ? s_rows[d + 256] : 0u);
+        }
+        rbase[256] = 0;  // pass 1: digit = ty >> 8 (0 or 1)
+        rbase[257] = hi1;
+    }
     __syncthreads();
     const int chunk = (T + 1023) / 1024;
     const int k0 = min(tid * chunk, T), k1 = min(k0 + chunk, T);
     uint32_t local = 0;
-    for (int k = k0; k < k1; ++k) {
-        const uint32_t c = (uint32_t)sm[(k / tiles_x) * gx + (k % tiles_x)];
-        local += c;
-        atomicAdd(&s_dig[0][k & 127], c);
-        atomicAdd(&s_dig[1][k >> 7], c);
-    }
+    for (int k = k0; k < k1; ++k) local += (uint32_t)sm[(k / tiles_x) * gx + (k % tiles_x)];
     s_sum[tid] = local;
     __syncthreads();
     for (int off = 1; off < 1024; off <<= 1) {
@@ -551,13 +607,6 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const int *__restrict__ diff
         tile_start[k] = run;
         run += (uint32_t)sm[(k / tiles_x) * gx + (k % tiles_x)];
     }
-    if (tid < 2) {  // digit bases of the two tile passes
-        uint32_t acc = 0;
-        for (int d = 0; d < 128; ++d) {
-            tbase[tid * 128 + d] = acc;
-            acc += s_dig[tid][d];
-        }
-    }
     if (tid == 1023) {
         const uint32_t E = s_sum[1023];
         tile_start[T] = E;
@@ -567,55 +616,129 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const int *__restrict__ diff
     }
 }
 
-// Row 5b (4/5): emission in canonical order: (tile id, visible slot) for every
-// covered tile of every row item, Gaussian-major, then row, then column.  One
-// block per chunk of kTileTile entries (load-balanced, coalesced stores): the
-// chunk's row items are staged in shared memory and each entry finds its item
-// by binary search there.
-constexpr int kEmitWin = 1024;  // row items staged per window
-__global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ item_pack,
-                                              const uint32_t *__restrict__ item_v, const uint32_t *__restrict__ eoff,
-                                              const uint32_t *__restrict__ chunk_first, const Counters *ctrc,
-                                              const uint32_t *n_items_ptr, int tiles_x, uint32_t *__restrict__ ekey,
-                                              uint32_t *__restrict__ eval) {
-    __shared__ uint32_t s_off[kEmitWin];
-    __shared__ uint32_t s_pack[kEmitWin];
-    __shared__ uint32_t s_v[kEmitWin];
-    const int tid = threadIdx.x;
-    if (ctrc->status != FDGS_OK) return;
-    const uint32_t ni = *n_items_ptr, E = ctrc->n_sort_entries;
-    const uint32_t chunks = (E + kTileTile - 1) / kTileTile;
-    for (uint32_t k = blockIdx.x; k < chunks; k += gridDim.x) {
-        const uint32_t e0 = k * kTileTile, e1 = min(e0 + kTileTile, E);
-        uint32_t r0 = __ldg(chunk_first + k);
-        uint32_t e = e0;
-        while (e < e1) {  // windows of kEmitWin items
-            const uint32_t m = min((uint32_t)kEmitWin, ni - r0);
-            for (uint32_t q = tid; q < m; q += blockDim.x) {
-                s_off[q] = __ldg(eoff + r0 + q);
-                s_pack[q] = __ldg(item_pack + r0 + q);
-                s_v[q] = __ldg(item_v + r0 + q);
+// Row 5b (5/6 and 6/6): per tile row, the stable scatter of its row items'
+// entries into the row's tiles.  The row's items (canonical order after the
+// stable row partition) are split into kRowSeg segments, one block each, and
+// each warp walks a contiguous run of them: 32 (item, tile) entries per round
+// in canonical order, ranked within the round by match_any on the tile, with
+// warp-private per-tile counters carrying the count across rounds.
+constexpr int kRowWarps = 8;
+
+template <bool kWrite>
+__device__ __forceinline__ void row_walk(uint32_t w0, uint32_t w1, int lane, const uint32_t *__restrict__ sorted,
+                                         const uint32_t *__restrict__ item_pack,
+                                         const uint32_t *__restrict__ item_v, uint32_t *cnt, const uint32_t *base,
+                                         uint32_t *__restrict__ entries) {
+    for (uint32_t r0 = w0; r0 < w1; r0 += 32) {
+        const uint32_t r = r0 + lane;
+        int c = 0, txa = 0;
+        uint32_t v = 0;
+        if (r < w1) {
+            const uint32_t it = __ldg(sorted + r);
+            const uint32_t pk = __ldg(item_pack + it);
+            txa = (int)(pk & 0xffffu);
+            c = max((int)(pk >> 16) - txa, 0);
+            if (kWrite) v = __ldg(item_v + it);
+        }
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        for (int e0 = 0; e0 < total; e0 += 32) {
+            const int e = e0 + lane;
+            int j = 0;  // owning item: smallest j with incl_j > e
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int cand = __shfl_sync(0xffffffffu, incl, j + step - 1);
+                if (cand <= e) j += step;
             }
-            __syncthreads();
-            const uint32_t wend = (r0 + m < ni) ? min(e1, __ldg(eoff + r0 + m)) : e1;
-            for (uint32_t i = e + tid; i < wend; i += blockDim.x) {
-                // largest q with s_off[q] <= i (empty items share the next item's offset,
-                // the largest such q is the non-empty owner)
-                int lo = 0, hi = (int)m - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (s_off[mid] <= i) lo = mid; else hi = mid - 1;
-                }
-                const uint32_t pk = s_pack[lo];
-                const uint32_t ty = pk & 0x7ffu, txa = (pk >> 11) & 0x7ffu;
-                ekey[i] = ty * (uint32_t)tiles_x + txa + (i - s_off[lo]);
-                eval[i] = s_v[lo];
-            }
-            __syncthreads();
-            e = wend;
-            r0 += m;
+            j = min(j, 31);
+            const int exj = __shfl_sync(0xffffffffu, incl - c, j);
+            const int jx = __shfl_sync(0xffffffffu, txa, j);
+            const uint32_t vj = __shfl_sync(0xffffffffu, v, j);
+            const bool valid = e < total;
+            const uint32_t tx = valid ? (uint32_t)(jx + (e - exj)) : 0xffffffffu;
+            const uint32_t peers = __match_any_sync(0xffffffffu, tx);
+            const bool leader = (__ffs(peers) - 1) == lane;
+            if (kWrite && valid) entries[base[tx] + cnt[tx] + __popc(peers & lanemask_lt())] = vj;
+            __syncwarp();
+            if (valid && leader) cnt[tx] += __popc(peers);
+            __syncwarp();
         }
     }
+}
+
+__device__ __forceinline__ void row_seg_range(const uint32_t *row_start, int ty, int seg, uint32_t &lo,
+                                              uint32_t &hi) {
+    const uint32_t a = __ldg(row_start + ty), b = __ldg(row_start + ty + 1);
+    const uint32_t per = (b - a + kRowSeg - 1) / kRowSeg;
+    lo = min(a + seg * per, b);
+    hi = min(lo + per, b);
+}
+
+// Row 5b (5/6) per (row, segment): the segment's entry count per tile -> hist[ty][seg][tx]
+__global__ void __launch_bounds__(32 * kRowWarps) k_row_count(const uint32_t *__restrict__ sorted,
+                                                              const uint32_t *__restrict__ item_pack,
+                                                              const uint32_t *__restrict__ row_start, int tiles_x,
+                                                              uint32_t *__restrict__ hist, const Counters *ctrc) {
+    extern __shared__ uint32_t s_cnt[];  // [kRowWarps][tiles_x]
+    const int ty = blockIdx.x / kRowSeg, seg = blockIdx.x % kRowSeg;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (ctrc->status != FDGS_OK) return;
+    for (int k = tid; k < kRowWarps * tiles_x; k += blockDim.x) s_cnt[k] = 0;
+    __syncthreads();
+    uint32_t lo, hi;
+    row_seg_range(row_start, ty, seg, lo, hi);
+    const uint32_t per = (hi - lo + kRowWarps - 1) / kRowWarps;
+    const uint32_t w0 = min(lo + warp * per, hi), w1 = min(w0 + per, hi);
+    row_walk<false>(w0, w1, lane, sorted, item_pack, nullptr, s_cnt + warp * tiles_x, nullptr, nullptr);
+    __syncthreads();
+    for (int x = tid; x < tiles_x; x += blockDim.x) {
+        uint32_t sum = 0;
+        for (int w = 0; w < kRowWarps; ++w) sum += s_cnt[w * tiles_x + x];
+        hist[((size_t)ty * kRowSeg + seg) * tiles_x + x] = sum;
+    }
+}
+
+// Row 5b (6/6) per (row, segment): global base of every tile (tile_start +
+// earlier segments + earlier warps), then the warp-ordered scatter of entries
+__global__ void __launch_bounds__(32 * kRowWarps) k_row_scatter(const uint32_t *__restrict__ sorted,
+                                                                const uint32_t *__restrict__ item_pack,
+                                                                const uint32_t *__restrict__ item_v,
+                                                                const uint32_t *__restrict__ row_start, int tiles_x,
+                                                                const uint32_t *__restrict__ hist,
+                                                                const uint32_t *__restrict__ tile_start,
+                                                                uint32_t *__restrict__ entries, const Counters *ctrc) {
+    extern __shared__ uint32_t s_mem[];  // [kRowWarps][tiles_x] counters, then [tiles_x] base
+    uint32_t *s_cnt = s_mem, *s_base = s_mem + kRowWarps * tiles_x;
+    const int ty = blockIdx.x / kRowSeg, seg = blockIdx.x % kRowSeg;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (ctrc->status != FDGS_OK) return;
+    for (int k = tid; k < kRowWarps * tiles_x; k += blockDim.x) s_cnt[k] = 0;
+    __syncthreads();
+    uint32_t lo, hi;
+    row_seg_range(row_start, ty, seg, lo, hi);
+    const uint32_t per = (hi - lo + kRowWarps - 1) / kRowWarps;
+    const uint32_t w0 = min(lo + warp * per, hi), w1 = min(w0 + per, hi);
+    uint32_t *my = s_cnt + warp * tiles_x;
+    row_walk<false>(w0, w1, lane, sorted, item_pack, nullptr, my, nullptr, nullptr);
+    __syncthreads();
+    for (int x = tid; x < tiles_x; x += blockDim.x) {
+        uint32_t b = __ldg(tile_start + ty * tiles_x + x);
+        for (int sg = 0; sg < seg; ++sg) b += __ldg(hist + ((size_t)ty * kRowSeg + sg) * tiles_x + x);
+        s_base[x] = b;
+        uint32_t run = 0;
+        for (int w = 0; w < kRowWarps; ++w) {
+            const uint32_t c = s_cnt[w * tiles_x + x];
+            s_cnt[w * tiles_x + x] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    row_walk<true>(w0, w1, lane, sorted, item_pack, item_v, my, s_base, entries);
 }
 
 // ---------------------------------------------------------------- row 6
@@ -1019,10 +1142,6 @@ static int tune_pgrid() {
     static const int v = std::max(1, tune_env("FDGS_PGRID", 1));
     return v;
 }
-static int tune_rgrid() {
-    static const int v = std::max(1, tune_env("FDGS_RGRID", 1));
-    return v;
-}
 
 cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint32_t *mask_r, const CamDev &cam,
                           float t, float *out_rgb, float *out_T, char *ws, const RenderLayout &L,
@@ -1065,37 +1184,47 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     const uint32_t *order = vals[1];
     if (ev && (e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
     int *diff = reinterpret_cast<int *>(ws + L.tile_diff);
-    uint32_t *tbase = reinterpret_cast<uint32_t *>(ws + L.tile_gbase);
-    uint32_t *eoff = reinterpret_cast<uint32_t *>(ws + L.emit_off);
-    uint32_t *elb = reinterpret_cast<uint32_t *>(ws + L.emit_lb);
-    uint32_t *ek[2] = {reinterpret_cast<uint32_t *>(ws + L.ekey0), reinterpret_cast<uint32_t *>(ws + L.ekey1)};
-    uint32_t *evl[2] = {reinterpret_cast<uint32_t *>(ws + L.eval0), reinterpret_cast<uint32_t *>(ws + L.eval1)};
-    uint64_t *tstat = reinterpret_cast<uint64_t *>(ws + L.tile_status);
-    constexpr int kTItems = kTileSortItems;
-    uint32_t *cfirst = reinterpret_cast<uint32_t *>(ws + L.chunk_first);
+    int *rowdiff = reinterpret_cast<int *>(ws + L.row_diff);
+    uint32_t *rbase = reinterpret_cast<uint32_t *>(ws + L.tile_gbase);  // [0..255] pass 0, [256..511] pass 1
+    uint32_t *row_start = reinterpret_cast<uint32_t *>(ws + L.row_start);
     uint32_t *roff = reinterpret_cast<uint32_t *>(ws + L.roff);
     uint32_t *rcfirst = reinterpret_cast<uint32_t *>(ws + L.rchunk_first);
+    uint32_t *ikey[2] = {reinterpret_cast<uint32_t *>(ws + L.ekey0), reinterpret_cast<uint32_t *>(ws + L.ekey1)};
+    uint32_t *ival[2] = {reinterpret_cast<uint32_t *>(ws + L.eval0), reinterpret_cast<uint32_t *>(ws + L.eval1)};
     uint32_t *ipack = reinterpret_cast<uint32_t *>(ws + L.item_pack);
     uint32_t *iv = reinterpret_cast<uint32_t *>(ws + L.item_v);
-    uint32_t *rlb = reinterpret_cast<uint32_t *>(ws + L.row_lb);
-    const uint32_t item_chunks = (uint32_t)((L.max_entries + kItemTile - 1) / kItemTile);
+    uint32_t *elb = reinterpret_cast<uint32_t *>(ws + L.emit_lb);
+    uint32_t *rhist = reinterpret_cast<uint32_t *>(ws + L.row_hist);
+    uint64_t *tstat = reinterpret_cast<uint64_t *>(ws + L.tile_status);
     BandConsts *bconst = reinterpret_cast<BandConsts *>(ws + L.band_consts);
+    const uint32_t item_chunks = (uint32_t)((L.max_entries + kItemTile - 1) / kItemTile);
     k_bin_scan<<<std::max(1, (L.n + kScanNT - 1) / kScanNT), kScanNT, 0, st>>>(rect_sorted, order, rec0, rec1, ctr,
-                                                                   &ctr->bin_ticket, elb, roff, rcfirst, item_chunks,
-                                                                   &ctr->n_items, bconst);
-    k_row_scan<<<(int)std::min<uint32_t>(item_chunks, tune_rgrid() * L.p_sort), kScanNT, 0, st>>>(
-        rect_sorted, order, rec0, rec1, bconst, roff, rcfirst, ctr, &ctr->n_items,
-                                                  L.tiles_x, &ctr->row_ticket, rlb, diff, ipack, iv, eoff, cfirst,
-                                                  (uint32_t)L.tile_parts, (uint32_t)L.max_entries);
+                                                                             &ctr->bin_ticket, elb, roff, rcfirst,
+                                                                             item_chunks, &ctr->n_items, bconst,
+                                                                             rowdiff);
+    k_row_items<<<(int)std::min<uint32_t>(item_chunks, 8 * L.p_sort), kScanNT, 0, st>>>(
+        rect_sorted, order, rec0, rec1, bconst, roff, rcfirst, ctr, &ctr->n_items, L.tiles_x, diff, ikey[0], ipack,
+        iv, (uint32_t)L.max_entries);
     const size_t scan_smem = sizeof(int) * (size_t)(L.tiles_x + 1) * (L.tiles_y + 1);
-    k_tile_scan<<<1, 1024, scan_smem, st>>>(diff, L.tiles_x, L.tiles_y, tstart, tbase, ctr, L.max_entries);
-    const int pgrid = tune_pgrid() * L.p_sort;  // persistent grids
-    k_emit<<<pgrid, 256, 0, st>>>(ipack, iv, eoff, cfirst, ctr, &ctr->n_items, L.tiles_x, ek[0], evl[0]);
-    k_onesweep<7, kTItems><<<pgrid, kSortThreads, 0, st>>>(ek[0], evl[0], ek[1], evl[1], &ctr->n_sort_entries, epoch,
-                                                           &ctr->tile_ticket[0], 0, tbase, tstat, nullptr, nullptr);
-    k_onesweep<7, kTItems><<<pgrid, kSortThreads, 0, st>>>(ek[1], evl[1], nullptr, entries, &ctr->n_sort_entries,
-                                                           epoch, &ctr->tile_ticket[1], 7, tbase + 128,
-                                                           tstat + (size_t)L.tile_parts * 128, nullptr, nullptr);
+    k_tile_scan<<<1, 1024, scan_smem, st>>>(diff, rowdiff, L.tiles_x, L.tiles_y, tstart, row_start, rbase, ctr,
+                                            L.max_entries);
+    // stable partition of the row items by tile row (canonical order kept within a row)
+    const int rgrid = std::min((int)item_chunks, tune_pgrid() * L.p_sort);
+    const uint32_t *sorted_items = ival[0];
+    k_onesweep<8, 4><<<rgrid, kSortThreads, 0, st>>>(ikey[0], nullptr, L.tiles_y > 256 ? ikey[1] : nullptr, ival[0],
+                                                   &ctr->n_items, epoch, &ctr->tile_ticket[0], 0, rbase, tstat,
+                                                   nullptr, nullptr);
+    if (L.tiles_y > 256) {
+        k_onesweep<8, 4><<<rgrid, kSortThreads, 0, st>>>(ikey[1], ival[0], nullptr, ival[1], &ctr->n_items, epoch,
+                                                       &ctr->tile_ticket[1], 8, rbase + 256,
+                                                       tstat + (size_t)L.tile_parts * 256, nullptr, nullptr);
+        sorted_items = ival[1];
+    }
+    const int nrb = L.tiles_y * kRowSeg;
+    const size_t cnt_smem = sizeof(uint32_t) * (size_t)kRowWarps * L.tiles_x;
+    k_row_count<<<nrb, 32 * kRowWarps, cnt_smem, st>>>(sorted_items, ipack, row_start, L.tiles_x, rhist, ctr);
+    k_row_scatter<<<nrb, 32 * kRowWarps, cnt_smem + sizeof(uint32_t) * L.tiles_x, st>>>(
+        sorted_items, ipack, iv, row_start, L.tiles_x, rhist, tstart, entries, ctr);
     // the blend may run on its own (lower-priority) stream, ordered after the front end
     cudaStream_t bst = st;
     if (blend_st != nullptr) {
@@ -1128,7 +1257,10 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
 
 // Opt-in to large dynamic shared memory once per process.
 __host__ cudaError_t render_set_smem_attrs() {
-    return cudaFuncSetAttribute(k_tile_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_tile_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_row_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_row_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    return e;
 }
 
 }  // namespace fdgs
