@@ -13,7 +13,8 @@ constexpr int kPreBlock = 256;         // Gaussians per preprocess partition
 constexpr int kDepthTile = 1024;       // keys per depth-sort partition (256 threads x 4)
 constexpr int kTileSortItems = 4;      // row items per thread in the row-partition passes
 constexpr int kTileTile = 256 * kTileSortItems;
-constexpr int kRowSeg = 4;             // blocks per tile row in the row scatter
+constexpr int kRowSeg = 16;            // blocks per tile row in the row scatter
+constexpr int kMaxTilesY = 512;        // 8192 px / 16
 constexpr uint32_t kFlagA = 1u << 30;  // look-back: aggregate available
 constexpr uint32_t kFlagP = 2u << 30;  // look-back: inclusive prefix available
 constexpr uint32_t kValMask = (1u << 30) - 1;

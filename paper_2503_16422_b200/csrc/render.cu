@@ -431,12 +431,15 @@ __global__ void __launch_bounds__(kScanNT) k_bin_scan(const uint2 *__restrict__ 
                                                    const Counters *ctrc, uint32_t *ticket, uint32_t *lb,
                                                    uint32_t *__restrict__ off, uint32_t *__restrict__ chunk_first,
                                                    uint32_t max_chunks, uint32_t *n_items,
-                                                   BandConsts *__restrict__ bconst, int *__restrict__ rowdiff) {
+                                                   BandConsts *__restrict__ bconst, int *__restrict__ rowdiff,
+                                                   int tiles_y) {
     __shared__ uint32_t s_w[32];
     __shared__ uint32_t s_part, s_excl;
+    __shared__ int s_rdiff[kMaxTilesY + 1];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t n = ctrc->n_vis;
     if (tid == 0) s_part = atomicAdd(ticket, 1u);
+    for (int k = tid; k <= tiles_y; k += blockDim.x) s_rdiff[k] = 0;
     __syncthreads();
     const uint32_t part = s_part;
     if (part * kScanNT >= n) return;
@@ -446,8 +449,8 @@ __global__ void __launch_bounds__(kScanNT) k_bin_scan(const uint2 *__restrict__ 
         const uint2 rc = __ldg(rects + i);
         const TileRect tr = tile_rect(rc);
         c = (uint32_t)tr.ny;
-        atomicAdd(&rowdiff[tr.ty0], 1);            // row-item counts per tile row (1D diff)
-        atomicAdd(&rowdiff[tr.ty0 + tr.ny], -1);
+        atomicAdd(&s_rdiff[tr.ty0], 1);            // row-item counts per tile row (1D diff), block-aggregated
+        atomicAdd(&s_rdiff[tr.ty0 + tr.ny], -1);
         const uint32_t v = __ldg(order + i);
         const float4 a = __ldg(rec0 + v), b = __ldg(rec1 + v);
         bconst[i] = band_consts(a.x, a.y, a.z, a.w, b.x, b.y, rc.x & 0xffff, rc.x >> 16, rc.y & 0xffff, rc.y >> 16);
@@ -460,6 +463,8 @@ __global__ void __launch_bounds__(kScanNT) k_bin_scan(const uint2 *__restrict__ 
     }
     if (lane == 31) s_w[warp] = incl;
     __syncthreads();
+    for (int k = tid; k <= tiles_y; k += blockDim.x)
+        if (s_rdiff[k]) atomicAdd(&rowdiff[k], s_rdiff[k]);
     if (warp == 0) {
         uint32_t w = lane < kScanNT / 32 ? s_w[lane] : 0u, wi = w;
 #pragma unroll
@@ -679,27 +684,43 @@ __device__ __forceinline__ void row_seg_range(const uint32_t *row_start, int ty,
     hi = min(lo + per, b);
 }
 
-// Row 5b (5/6) per (row, segment): the segment's entry count per tile -> hist[ty][seg][tx]
-__global__ void __launch_bounds__(32 * kRowWarps) k_row_count(const uint32_t *__restrict__ sorted,
-                                                              const uint32_t *__restrict__ item_pack,
-                                                              const uint32_t *__restrict__ row_start, int tiles_x,
-                                                              uint32_t *__restrict__ hist, const Counters *ctrc) {
-    extern __shared__ uint32_t s_cnt[];  // [kRowWarps][tiles_x]
+// Row 5b (5/6) per (row, segment): the segment's entry count per tile ->
+// hist[ty][seg][tx], from a shared-memory difference array over the row's
+// tiles (2 shared atomics per row item)
+__global__ void __launch_bounds__(256) k_row_count(const uint32_t *__restrict__ sorted,
+                                                   const uint32_t *__restrict__ item_pack,
+                                                   const uint32_t *__restrict__ row_start, int tiles_x,
+                                                   uint32_t *__restrict__ hist, const Counters *ctrc) {
+    extern __shared__ int s_d[];  // [tiles_x + 1]
     const int ty = blockIdx.x / kRowSeg, seg = blockIdx.x % kRowSeg;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     if (ctrc->status != FDGS_OK) return;
-    for (int k = tid; k < kRowWarps * tiles_x; k += blockDim.x) s_cnt[k] = 0;
+    for (int k = tid; k <= tiles_x; k += blockDim.x) s_d[k] = 0;
     __syncthreads();
     uint32_t lo, hi;
     row_seg_range(row_start, ty, seg, lo, hi);
-    const uint32_t per = (hi - lo + kRowWarps - 1) / kRowWarps;
-    const uint32_t w0 = min(lo + warp * per, hi), w1 = min(w0 + per, hi);
-    row_walk<false>(w0, w1, lane, sorted, item_pack, nullptr, s_cnt + warp * tiles_x, nullptr, nullptr);
+    for (uint32_t r = lo + tid; r < hi; r += blockDim.x) {
+        const uint32_t pk = __ldg(item_pack + __ldg(sorted + r));
+        const int txa = (int)(pk & 0xffffu), txe = (int)(pk >> 16);
+        if (txe > txa) {
+            atomicAdd(&s_d[txa], 1);
+            atomicAdd(&s_d[txe], -1);
+        }
+    }
     __syncthreads();
-    for (int x = tid; x < tiles_x; x += blockDim.x) {
-        uint32_t sum = 0;
-        for (int w = 0; w < kRowWarps; ++w) sum += s_cnt[w * tiles_x + x];
-        hist[((size_t)ty * kRowSeg + seg) * tiles_x + x] = sum;
+    if (tid < 32) {  // prefix over the row's tiles, one warp
+        int run = 0;
+        for (int x0 = 0; x0 < tiles_x; x0 += 32) {
+            const int x = x0 + tid;
+            int val = x < tiles_x ? s_d[x] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, val, o);
+                if (tid >= o) val += t;
+            }
+            if (x < tiles_x) hist[((size_t)ty * kRowSeg + seg) * tiles_x + x] = (uint32_t)(run + val);
+            run += __shfl_sync(0xffffffffu, val, 31);
+        }
     }
 }
 
@@ -1201,7 +1222,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     k_bin_scan<<<std::max(1, (L.n + kScanNT - 1) / kScanNT), kScanNT, 0, st>>>(rect_sorted, order, rec0, rec1, ctr,
                                                                              &ctr->bin_ticket, elb, roff, rcfirst,
                                                                              item_chunks, &ctr->n_items, bconst,
-                                                                             rowdiff);
+                                                                             rowdiff, L.tiles_y);
     k_row_items<<<(int)std::min<uint32_t>(item_chunks, 8 * L.p_sort), kScanNT, 0, st>>>(
         rect_sorted, order, rec0, rec1, bconst, roff, rcfirst, ctr, &ctr->n_items, L.tiles_x, diff, ikey[0], ipack,
         iv, (uint32_t)L.max_entries);
@@ -1222,7 +1243,8 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     }
     const int nrb = L.tiles_y * kRowSeg;
     const size_t cnt_smem = sizeof(uint32_t) * (size_t)kRowWarps * L.tiles_x;
-    k_row_count<<<nrb, 32 * kRowWarps, cnt_smem, st>>>(sorted_items, ipack, row_start, L.tiles_x, rhist, ctr);
+    k_row_count<<<nrb, 256, sizeof(int) * (L.tiles_x + 1), st>>>(sorted_items, ipack, row_start, L.tiles_x, rhist,
+                                                                  ctr);
     k_row_scatter<<<nrb, 32 * kRowWarps, cnt_smem + sizeof(uint32_t) * L.tiles_x, st>>>(
         sorted_items, ipack, iv, row_start, L.tiles_x, rhist, tstart, entries, ctr);
     // the blend may run on its own (lower-priority) stream, ordered after the front end
