@@ -745,7 +745,32 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_row_scatter(const uint32_t *
     const uint32_t per = (hi - lo + kRowWarps - 1) / kRowWarps;
     const uint32_t w0 = min(lo + warp * per, hi), w1 = min(w0 + per, hi);
     uint32_t *my = s_cnt + warp * tiles_x;
-    row_walk<false>(w0, w1, lane, sorted, item_pack, nullptr, my, nullptr, nullptr);
+    // per-warp tile counts: difference array over the warp's items (2 shared
+    // atomics per item), then a per-warp prefix over the row's tiles
+    int *md = reinterpret_cast<int *>(my);
+    for (uint32_t r = w0 + lane; r < w1; r += 32) {
+        const uint32_t pk = __ldg(item_pack + __ldg(sorted + r));
+        const int txa = (int)(pk & 0xffffu), txe = (int)(pk >> 16);
+        if (txe > txa) {
+            atomicAdd(&md[txa], 1);
+            if (txe < tiles_x) atomicAdd(&md[txe], -1);
+        }
+    }
+    __syncwarp();
+    {
+        int run = 0;
+        for (int x0 = 0; x0 < tiles_x; x0 += 32) {
+            const int x = x0 + lane;
+            int val = x < tiles_x ? md[x] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, val, o);
+                if (lane >= o) val += t;
+            }
+            if (x < tiles_x) md[x] = run + val;
+            run += __shfl_sync(0xffffffffu, val, 31);
+        }
+    }
     __syncthreads();
     for (int x = tid; x < tiles_x; x += blockDim.x) {
         uint32_t b = __ldg(tile_start + ty * tiles_x + x);
