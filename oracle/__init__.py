@@ -20,6 +20,9 @@ from .oracle import (  # noqa: F401
     canonical_order,
     tile_lists,
     band_tiles,
+    contrib,
+    stv_score,
+    tv_value,
     keyframe_mask,
     keyframes,
     bracket,

@@ -516,6 +516,7 @@ int64_t or_tile_lists(const or_scene *S, const uint32_t *mask, const or_camera *
 typedef struct {
     int32_t px0, px1;
     int32_t txa, txb;      /* tile cover of this row band (-1,-2 if empty) */
+    int32_t gid;           /* Gaussian index */
     float u, v, Ap, Bp, Cp, Q2;
     double u64, v64, A, B, C, amp, rgb[3];
 } or_cand;
@@ -540,6 +541,7 @@ typedef struct {
     double alt_C[OR_MAX_LEAVES][3], alt_T[OR_MAX_LEAVES];
     int64_t evaluated, blended;
     int knife;
+    double *contrib;       /* per-Gaussian blending weights (nullable, primary path) */
 } or_pix;
 
 static void or_leaf(or_pix *P, int primary, const double C[3], double T)
@@ -580,6 +582,7 @@ static void or_composite(const or_cand *cand, int nc, int k0, int i, float pxf, 
         }
         if (stop) { or_leaf(P, primary, C, T); return; }
         for (int ch = 0; ch < 3; ++ch) C[ch] += c->rgb[ch] * alpha * T;
+        if (primary && P->contrib) P->contrib[c->gid] += alpha * T;   /* S^S term of P:251 */
         T = test;
         if (primary) P->blended++;
     }
@@ -595,9 +598,28 @@ static void or_composite(const or_cand *cand, int nc, int k0, int i, float pxf, 
  * stats[0]=n_act stats[1]=n_vis stats[2]=evaluated pairs (in the pixel AABB and a
  * covered tile, before termination: the Eq. 2 work) stats[3]=blended
  * stats[4]=knife-edge decisions.  Returns 0. */
+static int or_render_impl(const or_scene *S, const uint32_t *mask, const or_camera *cam, float t,
+                          const int64_t *pix, int64_t n_pix, double *rgb, double *T_out, double *alt_rgb,
+                          int32_t *n_alt, int64_t *stats, double *contrib);
+
 int or_render(const or_scene *S, const uint32_t *mask, const or_camera *cam, float t,
               const int64_t *pix, int64_t n_pix,
               double *rgb, double *T_out, double *alt_rgb, int32_t *n_alt, int64_t *stats)
+{
+    return or_render_impl(S, mask, cam, t, pix, n_pix, rgb, T_out, alt_rgb, n_alt, stats, NULL);
+}
+
+/* Exported: per-Gaussian sum over all pixels of the blending weight
+ * alpha_i prod_{j<i}(1-alpha_j) of one view at t (the spatial score term of
+ * P:249-253), added into contrib[n] (binary64). */
+int or_contrib(const or_scene *S, const or_camera *cam, float t, double *contrib)
+{
+    return or_render_impl(S, NULL, cam, t, NULL, 0, NULL, NULL, NULL, NULL, NULL, contrib);
+}
+
+static int or_render_impl(const or_scene *S, const uint32_t *mask, const or_camera *cam, float t,
+                          const int64_t *pix, int64_t n_pix, double *rgb, double *T_out, double *alt_rgb,
+                          int32_t *n_alt, int64_t *stats, double *contrib)
 {
     const int W = cam->width, H = cam->height;
     int nv, na;
@@ -621,6 +643,7 @@ int or_render(const or_scene *S, const uint32_t *mask, const or_camera *cam, flo
 #pragma omp parallel reduction(+ : evaluated, blended, knife)
     {
         or_cand *cand = (or_cand *)malloc(sizeof(or_cand) * (size_t)(nv > 0 ? nv : 1));
+        double *my_contrib = contrib ? (double *)calloc((size_t)(S->n > 0 ? S->n : 1), sizeof(double)) : NULL;
 #pragma omp for schedule(dynamic, 1)
         for (int j = 0; j < H; ++j) {
             if (!need[j]) continue;
@@ -630,6 +653,7 @@ int or_render(const or_scene *S, const uint32_t *mask, const or_camera *cam, flo
                 if (j < g->py0 || j > g->py1) continue;
                 or_cand *c = &cand[nc++];
                 c->px0 = g->px0; c->px1 = g->px1;
+                c->gid = g->stage;
                 double bcq[5];
                 or_band_consts(g->f32, g->px0, g->px1, g->py0, g->py1, bcq);
                 if (!or_band_tiles(g->f32, g->px0, g->px1, g->py0, g->py1, bcq, j >> 4, &c->txa, &c->txb)) {
@@ -647,9 +671,11 @@ int or_render(const or_scene *S, const uint32_t *mask, const or_camera *cam, flo
                 const int i = (int)(flat % W);
                 or_pix P;
                 memset(&P, 0, sizeof P);
+                P.contrib = my_contrib;
                 const double C0[3] = {0.0, 0.0, 0.0};
                 or_composite(cand, nc, 0, i, (float)i + 0.5f, pyf, i + 0.5, j + 0.5, 1.0, C0, 0, 1, &P);
-                for (int ch = 0; ch < 3; ++ch) rgb[3 * k + ch] = P.prim_C[ch] + P.prim_T * (double)cam->bg[ch];
+                if (rgb)
+                    for (int ch = 0; ch < 3; ++ch) rgb[3 * k + ch] = P.prim_C[ch] + P.prim_T * (double)cam->bg[ch];
                 if (T_out) T_out[k] = P.prim_T;
                 if (n_alt) n_alt[k] = P.n_alt;
                 if (alt_rgb)
@@ -663,6 +689,11 @@ int or_render(const or_scene *S, const uint32_t *mask, const or_camera *cam, flo
             }
         }
         free(cand);
+        if (my_contrib) {
+#pragma omp critical
+            for (int q = 0; q < S->n; ++q) contrib[q] += my_contrib[q];
+            free(my_contrib);
+        }
     }
     if (stats) { stats[0] = na; stats[1] = nv; stats[2] = evaluated; stats[3] = blended; stats[4] = knife; }
     free(order);
@@ -719,6 +750,91 @@ void or_mask_or(const uint32_t *a, const uint32_t *b, int32_t n, uint32_t *out)
 {
     const int nw = (n + 31) / 32;
     for (int w = 0; w < nw; ++w) out[w] = a[w] | b[w];
+}
+
+/* ------------------------------------------------ Sec. 4.2.1
+ * Spatial-temporal variation score, time-aligned (reading R20):
+ *   S^S_i(t)  = sum over the views and pixels of alpha_i prod_{j<i}(1-alpha_j)
+ *               (or_contrib, the renderer's blending weights),
+ *   p2_i(t)   = ((t-mu_t)^2/Sigma_t^2 - 1/Sigma_t) p_i(t),
+ *   S^TV_i(t) = 1 / (0.5 tanh|p2_i(t)| + 0.5),
+ *   gamma_i   = min(V_i / V_p, 1), V_i = s_x s_y s_z s_t (binary32,
+ *               left to right), V_p the nearest-rank `percentile` of V
+ *               ("normalized following LightGaussian"),
+ *   S_i       = sum_t S^TV_i(t) gamma_i S^S_i(t).
+ * Outputs (nullable except score): score[n], spatial[n_ts][n], tv[n_ts][n],
+ * gamma[n]. */
+static int or_cmp_float(const void *a, const void *b)
+{
+    const float x = *(const float *)a, y = *(const float *)b;
+    return (x > y) - (x < y);
+}
+
+double or_sigma_t(const or_scene *S, int i)
+{
+    double R4[16];
+    or_rotor4(S->rot_l + 4 * (size_t)i, S->rot_r + 4 * (size_t)i, R4);
+    double s44 = 0.0;
+    for (int j = 0; j < 4; ++j) {
+        const double m = R4[12 + j] * (double)S->scale[4 * (size_t)i + j];
+        s44 += m * m;
+    }
+    return s44;
+}
+
+double or_tv(double t, double mu_t, double st)
+{
+    const double dt = t - mu_t;
+    const double p = exp(-(dt * dt) / (2.0 * st));
+    const double p2 = ((dt * dt) / (st * st) - 1.0 / st) * p;
+    return 1.0 / (0.5 * tanh(fabs(p2)) + 0.5);
+}
+
+float or_volume(const or_scene *S, int i)
+{
+    const float *s = S->scale + 4 * (size_t)i;
+    float v = s[0] * s[1];
+    v = v * s[2];
+    v = v * s[3];
+    return v;
+}
+
+int or_stv_score(const or_scene *S, const or_camera *cams, int32_t n_cams, const float *ts, int32_t n_ts,
+                 double percentile, double *score, double *spatial, double *tv, double *gamma)
+{
+    const int n = S->n;
+    if (n <= 0) return 0;
+    float *vol = (float *)malloc(sizeof(float) * (size_t)n);
+    for (int i = 0; i < n; ++i) vol[i] = or_volume(S, i);
+    float *sorted = (float *)malloc(sizeof(float) * (size_t)n);
+    memcpy(sorted, vol, sizeof(float) * (size_t)n);
+    qsort(sorted, (size_t)n, sizeof(float), or_cmp_float);
+    int rank = (int)ceil(percentile * (double)n) - 1;
+    if (rank < 0) rank = 0;
+    if (rank > n - 1) rank = n - 1;
+    const double vp = sorted[rank];
+    double *sig = (double *)malloc(sizeof(double) * (size_t)n);
+    for (int i = 0; i < n; ++i) sig[i] = or_sigma_t(S, i);
+    double *ss = (double *)malloc(sizeof(double) * (size_t)n);
+    for (int i = 0; i < n; ++i) score[i] = 0.0;
+    for (int k = 0; k < n_ts; ++k) {
+        memset(ss, 0, sizeof(double) * (size_t)n);
+        for (int c = 0; c < n_cams; ++c) or_contrib(S, &cams[c], ts[k], ss);
+        for (int i = 0; i < n; ++i) {
+            const double g = fmin((double)vol[i] / vp, 1.0);
+            const double v = or_tv((double)ts[k], (double)S->mean[4 * (size_t)i + 3], sig[i]);
+            score[i] += v * g * ss[i];
+            if (spatial) spatial[(size_t)k * n + i] = ss[i];
+            if (tv) tv[(size_t)k * n + i] = v;
+        }
+    }
+    if (gamma)
+        for (int i = 0; i < n; ++i) gamma[i] = fmin((double)vol[i] / vp, 1.0);
+    free(ss);
+    free(sig);
+    free(sorted);
+    free(vol);
+    return 0;
 }
 
 int or_num_threads(void)

@@ -65,6 +65,12 @@ def load():
             lib.or_band_tiles.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, P, P]
             lib.or_band_tiles.restype = C.c_int
             lib.or_num_threads.restype = C.c_int
+            lib.or_contrib.argtypes = [P, P, C.c_float, P]
+            lib.or_stv_score.argtypes = [P, P, C.c_int32, P, C.c_int32, C.c_double, P, P, P, P]
+            lib.or_tv.argtypes = [C.c_double, C.c_double, C.c_double]
+            lib.or_tv.restype = C.c_double
+            lib.or_sigma_t.argtypes = [P, C.c_int]
+            lib.or_sigma_t.restype = C.c_double
             _lib = lib
     return _lib
 
@@ -235,6 +241,35 @@ def sh_basis(d):
     out = np.zeros(16, np.float64)
     lib.or_sh_basis(d.ctypes.data, out.ctypes.data)
     return out
+
+
+def contrib(scene, cam, t):
+    """Per-Gaussian sum of blending weights of one view at t."""
+    lib = load()
+    sr = _SceneRef(scene)
+    out = np.zeros(max(sr.s.n, 1), np.float64)
+    lib.or_contrib(C.byref(sr.s), C.byref(_cam(cam)), float(t), out.ctypes.data)
+    return out[:sr.s.n]
+
+
+def stv_score(scene, cams, ts, percentile=0.9):
+    """Spatial-temporal variation score: dict(score, spatial, tv, gamma)."""
+    lib = load()
+    sr = _SceneRef(scene)
+    n = sr.s.n
+    ts = np.ascontiguousarray(ts, np.float32)
+    arr = (_Camera * len(cams))(*[_cam(c) for c in cams])
+    score = np.zeros(max(n, 1))
+    spatial = np.zeros((len(ts), max(n, 1)))
+    tv = np.zeros((len(ts), max(n, 1)))
+    gamma = np.zeros(max(n, 1))
+    lib.or_stv_score(C.byref(sr.s), arr, len(cams), ts.ctypes.data, len(ts), float(percentile), score.ctypes.data,
+                     spatial.ctypes.data, tv.ctypes.data, gamma.ctypes.data)
+    return dict(score=score[:n], spatial=spatial[:, :n], tv=tv[:, :n], gamma=gamma[:n])
+
+
+def tv_value(t, mu_t, sigma_t):
+    return float(load().or_tv(float(t), float(mu_t), float(sigma_t)))
 
 
 def num_threads():
