@@ -761,7 +761,11 @@ void or_mask_or(const uint32_t *a, const uint32_t *b, int32_t n, uint32_t *out)
  *   gamma_i   = min(V_i / V_p, 1), V_i = s_x s_y s_z s_t (binary32,
  *               left to right), V_p the nearest-rank `percentile` of V
  *               ("normalized following LightGaussian"),
- *   S_i       = sum_t S^TV_i(t) gamma_i S^S_i(t).
+ *   S_i       = sum_t S^TV_i(t) gamma_i S^S_i(t)
+ *               (mode 0, time-aligned, reading R20), or
+ *   S_i       = gamma_i (sum_t S^TV_i(t)) (sum_t S^S_i(t))           (mode 1: the
+ *               literal product of the two sums, S^TV of P:264 already summed
+ *               over t and S_i of P:270 summing S^T S^S again).
  * Outputs (nullable except score): score[n], spatial[n_ts][n], tv[n_ts][n],
  * gamma[n]. */
 static int or_cmp_float(const void *a, const void *b)
@@ -800,7 +804,7 @@ float or_volume(const or_scene *S, int i)
 }
 
 int or_stv_score(const or_scene *S, const or_camera *cams, int32_t n_cams, const float *ts, int32_t n_ts,
-                 double percentile, double *score, double *spatial, double *tv, double *gamma)
+                 double percentile, double *score, double *spatial, double *tv, double *gamma, int mode)
 {
     const int n = S->n;
     if (n <= 0) return 0;
@@ -816,6 +820,8 @@ int or_stv_score(const or_scene *S, const or_camera *cams, int32_t n_cams, const
     double *sig = (double *)malloc(sizeof(double) * (size_t)n);
     for (int i = 0; i < n; ++i) sig[i] = or_sigma_t(S, i);
     double *ss = (double *)malloc(sizeof(double) * (size_t)n);
+    double *tv_sum = (double *)calloc((size_t)n, sizeof(double));
+    double *ss_sum = (double *)calloc((size_t)n, sizeof(double));
     for (int i = 0; i < n; ++i) score[i] = 0.0;
     for (int k = 0; k < n_ts; ++k) {
         memset(ss, 0, sizeof(double) * (size_t)n);
@@ -824,10 +830,16 @@ int or_stv_score(const or_scene *S, const or_camera *cams, int32_t n_cams, const
             const double g = fmin((double)vol[i] / vp, 1.0);
             const double v = or_tv((double)ts[k], (double)S->mean[4 * (size_t)i + 3], sig[i]);
             score[i] += v * g * ss[i];
+            tv_sum[i] += v;
+            ss_sum[i] += ss[i];
             if (spatial) spatial[(size_t)k * n + i] = ss[i];
             if (tv) tv[(size_t)k * n + i] = v;
         }
     }
+    if (mode == 1)
+        for (int i = 0; i < n; ++i) score[i] = fmin((double)vol[i] / vp, 1.0) * tv_sum[i] * ss_sum[i];
+    free(tv_sum);
+    free(ss_sum);
     if (gamma)
         for (int i = 0; i < n; ++i) gamma[i] = fmin((double)vol[i] / vp, 1.0);
     free(ss);

@@ -66,7 +66,7 @@ def load():
             lib.or_band_tiles.restype = C.c_int
             lib.or_num_threads.restype = C.c_int
             lib.or_contrib.argtypes = [P, P, C.c_float, P]
-            lib.or_stv_score.argtypes = [P, P, C.c_int32, P, C.c_int32, C.c_double, P, P, P, P]
+            lib.or_stv_score.argtypes = [P, P, C.c_int32, P, C.c_int32, C.c_double, P, P, P, P, C.c_int]
             lib.or_tv.argtypes = [C.c_double, C.c_double, C.c_double]
             lib.or_tv.restype = C.c_double
             lib.or_sigma_t.argtypes = [P, C.c_int]
@@ -252,8 +252,9 @@ def contrib(scene, cam, t):
     return out[:sr.s.n]
 
 
-def stv_score(scene, cams, ts, percentile=0.9):
-    """Spatial-temporal variation score: dict(score, spatial, tv, gamma)."""
+def stv_score(scene, cams, ts, percentile=0.9, combine=0):
+    """Spatial-temporal variation score: dict(score, spatial, tv, gamma).
+    combine 0 = time-aligned sum_t S^TV gamma S^S (R20), 1 = product of the sums."""
     lib = load()
     sr = _SceneRef(scene)
     n = sr.s.n
@@ -264,7 +265,7 @@ def stv_score(scene, cams, ts, percentile=0.9):
     tv = np.zeros((len(ts), max(n, 1)))
     gamma = np.zeros(max(n, 1))
     lib.or_stv_score(C.byref(sr.s), arr, len(cams), ts.ctypes.data, len(ts), float(percentile), score.ctypes.data,
-                     spatial.ctypes.data, tv.ctypes.data, gamma.ctypes.data)
+                     spatial.ctypes.data, tv.ctypes.data, gamma.ctypes.data, int(combine))
     return dict(score=score[:n], spatial=spatial[:, :n], tv=tv[:, :n], gamma=gamma[:n])
 
 

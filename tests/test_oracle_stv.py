@@ -94,3 +94,20 @@ def test_combined_score_time_aligned_and_absorbing_zero():
     # weights of a pixel sum to 1 - T: total over Gaussians = sum (1 - T)
     out = oracle.render(scene, cams[0], ts[1])
     assert oracle.contrib(scene, cams[0], ts[1]).sum() == pytest.approx((1 - out["T"]).sum(), rel=1e-9)
+
+
+def test_combine_modes_closed_form_long_lifespan_full_cover():
+    """One splat covering the whole image with sigma = 1 and a huge temporal
+    scale: p_t ~ 1 and |p2| ~ 1/Sigma_t ~ 0, so S^TV(t) = 2 - O(1e-12) and
+    S^S(t) = 0.99 W H at every t.  With gamma = 1 (a single Gaussian is its own
+    percentile) and n_t timestamps:
+      time-aligned (R20):   S = sum_t 2 * 0.99 W H           = 2 n_t 0.99 W H
+      product of the sums:  S = (sum_t 2) (sum_t 0.99 W H)   = 2 n_t^2 0.99 W H."""
+    cam = cam_axis(8, 8, 8.0)
+    sc = fi.isotropic_scene([[0, 0, 4.0, 0.5]], [[200.0, 200.0, 200.0, 1e6]], [1.0])
+    ts = np.float32([0.0, 0.25, 0.5, 1.0])
+    a = oracle.stv_score(sc, [cam], ts, combine=0)
+    b = oracle.stv_score(sc, [cam], ts, combine=1)
+    assert a["gamma"][0] == 1.0
+    assert a["score"][0] == pytest.approx(2 * 4 * 0.99 * 64, rel=1e-9)
+    assert b["score"][0] == pytest.approx(2 * 16 * 0.99 * 64, rel=1e-9)
