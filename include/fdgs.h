@@ -209,15 +209,43 @@ size_t fdgs_mask_compact_workspace_bytes(int32_t n);
 fdgs_status fdgs_mask_compact(const uint32_t *d_a, const uint32_t *d_b, int32_t n, int32_t *d_out_idx,
                               uint32_t *d_count, void *d_ws, size_t ws_bytes, void *stream);
 
-/* Spatial-temporal variation score (Sec. 4.2.1).  Not built in this
- * round: returns FDGS_ERR_UNSUPPORTED. */
+/* Spatial-temporal variation score (Sec. 4.2.1), the global
+ * pruning criterion:
+ *   S^S_i(t)  = sum over the n_cams views and all their pixels of the blending
+ *               weight alpha_i prod_{j<i}(1 - alpha_j) of Gaussian i in the
+ *               UNMASKED render at t (the weights of fdgs_render's
+ *               composite, summed in 2^-24 fixed point: deterministic, error
+ *               <= 2^-25 per (pixel, Gaussian) beyond the fp32 weight itself)
+ *   S^TV_i(t) = 1 / (0.5 tanh|p2_i(t)| + 0.5),
+ *               p2_i(t) = ((t-mu_t)^2/Sigma_t^2 - 1/Sigma_t) p_i(t)
+ *   gamma_i   = min(V_i / V_p, 1), V_i = s_x s_y s_z s_t (fp32, left to right),
+ *               V_p = the nearest-rank volume_percentile of V over the scene,
+ *               i.e. the element of rank ceil(p n) - 1 (0-based) of sorted V
+ *               (LightGaussian normalisation; reading R20)
+ *   combine_mode 0: S_i = sum_t S^TV_i(t) gamma_i S^S_i(t)  (time-aligned, R20)
+ *   combine_mode 1: S_i = gamma_i (sum_t S^TV_i(t)) (sum_t S^S_i(t))  (the
+ *               literal product of the two sums of P:264-272)
+ * Arguments: cams HOST array of n_cams views (any sizes); ts HOST float[n_ts];
+ *   d_out_score DEVICE float[n]; d_out_spatial DEVICE float[n_ts][n] S^S_i(t)
+ *   (nullable); d_out_gamma DEVICE float[n] (nullable); d_ws DEVICE workspace
+ *   of fdgs_stv_workspace_bytes (256-aligned, no zero-fill needed);
+ *   h_max_entries HOST (nullable) receives the largest per-view tile-entry
+ *   count E, so a caller can size opts->max_entries.
+ * SYNCHRONOUS (one stream sync at the end).  Errors: INVALID_ARG (NULL
+ * pointers, bad camera, n_ts < 0, n_cams < 1, non-finite t, percentile outside
+ * (0, 1], unknown combine_mode), WORKSPACE_TOO_SMALL, UNSUPPORTED (tile grid >
+ * FDGS_MAX_TILES), OVERFLOW (some view needed more than opts->max_entries tile
+ * entries: outputs undefined; retry with *h_max_entries), CUDA. */
 typedef struct {
-    float volume_percentile;   /* gamma clip percentile (0.9)          */
-    int32_t combine_mode;      /* 0 = time-aligned sum_t S^T S^S        */
+    double volume_percentile;  /* gamma clip percentile, nearest rank (0.9)  */
+    int32_t combine_mode;      /* 0 time-aligned (default), 1 product of sums */
+    int32_t reserved;
+    int64_t max_entries;       /* tile-entry capacity of each per-view render  */
 } fdgs_stv_opts;
+size_t fdgs_stv_workspace_bytes(int32_t n, const fdgs_camera *cams, int32_t n_cams, int64_t max_entries);
 fdgs_status fdgs_stv_score(const fdgs_scene *scene, const fdgs_camera *cams, int32_t n_cams, const float *ts,
-                           int32_t n_ts, const fdgs_stv_opts *opts, float *d_out_score, void *d_ws,
-                           size_t ws_bytes, void *stream);
+                           int32_t n_ts, const fdgs_stv_opts *opts, float *d_out_score, float *d_out_spatial,
+                           float *d_out_gamma, void *d_ws, size_t ws_bytes, uint32_t *h_max_entries, void *stream);
 
 #ifdef __cplusplus
 }

@@ -23,7 +23,7 @@ EXPORTS = [
     "fdgs_render_workspace_bytes", "fdgs_render", "fdgs_render_timed", "fdgs_render_split", "fdgs_render_checked",
     "fdgs_render_debug_views",
     "fdgs_keyframe_workspace_bytes", "fdgs_keyframe_mask", "fdgs_mask_or",
-    "fdgs_mask_compact_workspace_bytes", "fdgs_mask_compact", "fdgs_stv_score",
+    "fdgs_mask_compact_workspace_bytes", "fdgs_mask_compact", "fdgs_stv_workspace_bytes", "fdgs_stv_score",
 ]
 
 
@@ -51,7 +51,8 @@ class FdgsDebugViews(C.Structure):
 
 
 class FdgsStvOpts(C.Structure):
-    _fields_ = [("volume_percentile", C.c_float), ("combine_mode", C.c_int32)]
+    _fields_ = [("volume_percentile", C.c_double), ("combine_mode", C.c_int32), ("reserved", C.c_int32),
+                ("max_entries", C.c_int64)]
 
 
 class FdgsError(RuntimeError):
@@ -93,7 +94,8 @@ def lib():
             "fdgs_mask_or": ([P, P, I32, P, P], C.c_int),
             "fdgs_mask_compact_workspace_bytes": ([I32], SZ),
             "fdgs_mask_compact": ([P, P, I32, P, P, P, SZ, P], C.c_int),
-            "fdgs_stv_score": ([P, P, I32, P, I32, P, P, P, SZ, P], C.c_int),
+            "fdgs_stv_workspace_bytes": ([I32, P, I32, I64], SZ),
+            "fdgs_stv_score": ([P, P, I32, P, I32, P, P, P, P, P, SZ, P, P], C.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

@@ -288,8 +288,35 @@ def mask_compact(a: torch.Tensor, n: int, b: torch.Tensor | None = None, stream=
     return idx[:k]
 
 
-def stv_score(*args, **kwargs):
-    check(lib().fdgs_stv_score(None, None, 0, None, 0, None, None, None, 0, None))
+def stv_score(scene: Scene, cams, ts, percentile: float = 0.9, combine: int = 0, spatial: bool = False,
+              gamma: bool = False, max_entries: int | None = None, stream=None) -> dict:
+    """fdgs_stv_score (Sec. 4.2.1, P:241-272): dict(score[n], spatial[n_ts][n] | None,
+    gamma[n] | None) as device float32 tensors.  Synchronous; grows the per-view
+    tile-entry capacity and retries on overflow."""
+    n = scene.n
+    dev = scene.device
+    cs = [camera_struct(c) for c in cams]
+    arr = (FdgsCamera * len(cs))(*cs)
+    tsa = (C.c_float * max(len(ts), 1))(*[float(t) for t in ts])
+    score = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+    sp = torch.empty((len(ts), max(n, 1)), dtype=torch.float32, device=dev) if spatial else None
+    gm = torch.empty(max(n, 1), dtype=torch.float32, device=dev) if gamma else None
+    cap = int(default_max_entries(n) if max_entries is None else max_entries)
+    while True:
+        opts = _lib.FdgsStvOpts(float(percentile), int(combine), 0, cap)
+        nb = lib().fdgs_stv_workspace_bytes(n, arr, len(cs), cap)
+        if nb == 0:
+            raise ValueError("invalid stv_score arguments")
+        ws = torch.empty(nb, dtype=torch.uint8, device=dev)
+        need = C.c_uint32(0)
+        st = lib().fdgs_stv_score(C.byref(scene.struct), arr, len(cs), tsa, len(ts), C.byref(opts), _ptr(score),
+                                  _ptr(sp), _ptr(gm), _ptr(ws), nb, C.byref(need), _stream_ptr(stream))
+        if st == _lib.FDGS_ERR_OVERFLOW:
+            cap = int(min(2 ** 32 - 1, max(2 * cap, need.value + 1)))
+            continue
+        check(st)
+        return dict(score=score[:n], spatial=None if sp is None else sp[:, :n], gamma=None if gm is None else gm[:n],
+                    max_entries=int(need.value))
 
 
 # ------------------------------------------------ Sec. 4.2.2 host logic

@@ -371,9 +371,66 @@ fdgs_status fdgs_mask_compact(const uint32_t *d_a, const uint32_t *d_b, int32_t 
     return e == cudaSuccess ? FDGS_OK : cuda_fail(e, "fdgs_mask_compact");
 }
 
-fdgs_status fdgs_stv_score(const fdgs_scene *, const fdgs_camera *, int32_t, const float *, int32_t,
-                           const fdgs_stv_opts *, float *, void *, size_t, void *) {
-    return fail(FDGS_ERR_UNSUPPORTED, "fdgs_stv_score is not built yet (SURVEY NEXT-f1)");
+size_t fdgs_stv_workspace_bytes(int32_t n, const fdgs_camera *cams, int32_t n_cams, int64_t max_entries) {
+    if (n < 0 || cams == nullptr || n_cams < 1 || max_entries < 0) return 0;
+    for (int c = 0; c < n_cams; ++c)
+        if (cams[c].width < 1 || cams[c].height < 1) return 0;
+    return stv_layout(n, cams, n_cams, max_entries).total;
+}
+
+fdgs_status fdgs_stv_score(const fdgs_scene *scene, const fdgs_camera *cams, int32_t n_cams, const float *ts,
+                           int32_t n_ts, const fdgs_stv_opts *opts, float *d_out_score, float *d_out_spatial,
+                           float *d_out_gamma, void *d_ws, size_t ws_bytes, uint32_t *h_max_entries, void *stream) {
+    if (h_max_entries) *h_max_entries = 0;
+    fdgs_status s = check_scene(scene);
+    if (s != FDGS_OK) return s;
+    if (opts == nullptr || cams == nullptr || n_cams < 1 || n_ts < 0 || (n_ts > 0 && ts == nullptr))
+        return fail(FDGS_ERR_INVALID_ARG, "opts / cameras / timestamps");
+    if (scene->n > 0 && d_out_score == nullptr) return fail(FDGS_ERR_INVALID_ARG, "d_out_score is NULL");
+    if (!(opts->volume_percentile > 0.0 && opts->volume_percentile <= 1.0))
+        return fail(FDGS_ERR_INVALID_ARG, "volume_percentile must lie in (0, 1]");
+    if (opts->combine_mode != 0 && opts->combine_mode != 1) return fail(FDGS_ERR_INVALID_ARG, "combine_mode");
+    if (opts->max_entries < 0 || opts->max_entries > 0xffffffffll) return fail(FDGS_ERR_INVALID_ARG, "max_entries");
+    for (int k = 0; k < n_ts; ++k)
+        if (!std::isfinite(ts[k])) return fail(FDGS_ERR_INVALID_ARG, "ts[%d] is not finite", k);
+    std::vector<CamDev> cd(n_cams);
+    for (int c = 0; c < n_cams; ++c) {
+        const char *why = nullptr;
+        if (!make_camdev(cams[c], cd[c], &why)) return fail(FDGS_ERR_INVALID_ARG, "camera %d: %s", c, why);
+        const RenderLayout L = render_layout(std::max(scene->n, 0), cams[c].width, cams[c].height, opts->max_entries);
+        if (L.n_tiles > FDGS_MAX_TILES) return fail(FDGS_ERR_UNSUPPORTED, "tile grid %d > %d", L.n_tiles, FDGS_MAX_TILES);
+    }
+    const int n = scene->n;
+    if (n == 0) return FDGS_OK;
+    const StvLayout SL = stv_layout(n, cams, n_cams, opts->max_entries);
+    if (d_ws == nullptr || ws_bytes < SL.total || (uintptr_t)d_ws % 256 != 0)
+        return fail(FDGS_ERR_WORKSPACE_TOO_SMALL, "stv workspace needs %zu bytes (256-aligned), got %zu", SL.total,
+                    ws_bytes);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_ts == 0) {  // empty sums
+        cudaError_t e = cudaMemsetAsync(d_out_score, 0, sizeof(float) * (size_t)n, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        return e == cudaSuccess ? FDGS_OK : cuda_fail(e, "fdgs_stv_score");
+    }
+    std::call_once(g_attr_once, [] { g_attr_err = render_set_smem_attrs(); });
+    if (g_attr_err != cudaSuccess) return cuda_fail(g_attr_err, "cudaFuncSetAttribute");
+    // nearest rank, 0-based: ceil(p n) - 1 (as the oracle)
+    long long rank = (long long)std::ceil(opts->volume_percentile * (double)n) - 1;
+    rank = std::min<long long>(std::max<long long>(rank, 0), n - 1);
+    char *ws = reinterpret_cast<char *>(d_ws);
+    // camera constants go to the device by value (kernel arguments), so cd is host-only
+    cudaError_t e = launch_stv(make_scenedev(*scene), cd.data(), cams, n_cams, ts, n_ts, (uint32_t)rank,
+                               opts->combine_mode, opts->max_entries, ws, SL, d_out_score, d_out_spatial, d_out_gamma,
+                               st);
+    uint32_t info[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(info, ws + SL.state, sizeof info, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "fdgs_stv_score");
+    if (h_max_entries) *h_max_entries = info[1];
+    if (info[0] != FDGS_OK)
+        return fail((fdgs_status)info[0], "a view needed %u tile entries > capacity %lld", info[1],
+                    (long long)opts->max_entries);
+    return FDGS_OK;
 }
 
 }  // extern "C"

@@ -83,6 +83,24 @@ __device__ __forceinline__ bool temporal_pass(float4 mean, float4 sc, float4 ql,
     return dmul(dt, dt) <= dmul(kKT, s44);
 }
 
+// Sigma_44 = (R4 S S^T R4^T)_44 alone (row 3 of R4), the same ops as the start
+// of slice_gaussian.  Used by the temporal score (Sigma_t).
+__device__ __forceinline__ double sigma44(float4 sc, float4 ql, float4 qr) {
+    const double a = ql.x, b = ql.y, c = ql.z, d = ql.w;
+    const double p = qr.x, q = qr.y, r = qr.z, s = qr.w;
+    const double Rm[4][4] = {{p, -q, -r, -s}, {q, p, s, -r}, {r, -s, p, q}, {s, r, -q, p}};
+    const double s4[4] = {(double)sc.x, (double)sc.y, (double)sc.z, (double)sc.w};
+    const double L3[4] = {d, -c, b, a};
+    double row[4], m[4];
+    rotor_row(L3, Rm, row);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) m[j] = dmul(row[j], s4[j]);
+    double s44 = dmul(m[0], m[0]);
+    s44 = dfma(m[1], m[1], s44);
+    s44 = dfma(m[2], m[2], s44);
+    return dfma(m[3], m[3], s44);
+}
+
 // Eq. 1 slice with the temporal (p_t >= 1/255) and support (sigma p_t >= 1/255)
 // culls.  Returns the stage reached (kTemporal / kSupport on cull, else kNear
 // meaning "continue to projection").

@@ -69,7 +69,23 @@ SceneDev make_scenedev(const fdgs_scene &s);
 cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint32_t *mask_r, const CamDev &cam,
                           float t, float *out_rgb, float *out_T, char *ws, const RenderLayout &L,
                           fdgs_frame_stats *stats, cudaStream_t st, cudaEvent_t const *stage_events,
-                          cudaStream_t blend_st = nullptr, cudaEvent_t split_ev = nullptr);
+                          cudaStream_t blend_st = nullptr, cudaEvent_t split_ev = nullptr,
+                          unsigned long long *contrib = nullptr, uint32_t *stv_info = nullptr);
+// Head of the fdgs_stv_score workspace.
+struct StvState {
+    uint32_t info[2];  // [0] worst frame status, [1] largest per-view entry count
+    uint32_t prefix;   // radix select: selected high bits of V_p (finally V_p's bits)
+    uint32_t rank;     // radix select: remaining rank within the prefix
+    uint32_t hist[256];
+};
+struct StvLayout {
+    size_t state, contrib, acc_a, acc_b, acc_c, render, total;
+};
+StvLayout stv_layout(int32_t n, const fdgs_camera *cams, int32_t n_cams, int64_t max_entries);
+cudaError_t launch_stv(const SceneDev &sc, const CamDev *cams, const fdgs_camera *hcams, int n_cams, const float *ts,
+                       int n_ts, uint32_t rank, int mode, int64_t max_entries, char *ws, const StvLayout &SL,
+                       float *out_score, float *out_spatial, float *out_gamma, cudaStream_t st);
+
 cudaError_t launch_keyframe(const SceneDev &sc, const CamDev *d_cams, int n_cams, float t, uint32_t *out,
                             cudaStream_t st);
 cudaError_t launch_mask_or(const uint32_t *a, const uint32_t *b, int n, uint32_t *out, cudaStream_t st);

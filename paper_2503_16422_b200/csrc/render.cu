@@ -859,7 +859,7 @@ __device__ __forceinline__ void stage_fields(int tx, int ty, const float4 &r0, c
     }
     oa = r0;
     oc = make_float4(r1.x, r1.y, r2.x, r2.y);
-    od = make_float4(r2.z, __uint_as_float(xm | (ym << 16)), __uint_as_float(yr << 16), 0.0f);
+    od = make_float4(r2.z, __uint_as_float(xm | (ym << 16)), __uint_as_float(yr << 16), r2.w);  // .w: gid bits
 }
 
 __device__ __forceinline__ void stage_store(BlendBatch &B, int tid, uint32_t k, uint32_t end, int tx, int ty,
@@ -1029,7 +1029,16 @@ __device__ __forceinline__ void mb_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
-template <bool kCount>
+// kContrib (Sec. 4.2.1 spatial score): additionally records, per
+// Gaussian, the sum over the tile's pixels of its blending weight
+// w = alpha_i prod_{j<i}(1 - alpha_j) -- exactly the weight the composite
+// uses.  Weights are rounded to fixed point (2^-24, error <= 2^-25 per pixel)
+// and summed as integers: each consumer warp reduces its 64 pixels with
+// REDUX into its own shared slot, the producer adds the four slots of a
+// released batch and issues one 64-bit global atomic per (tile, Gaussian), so
+// the per-Gaussian totals are independent of scheduling (deterministic).
+constexpr float kContribScale = 16777216.0f;  // 2^24
+template <bool kCount, bool kContrib = false>
 __global__ void __launch_bounds__(kWsThreads) k_blend_ws(const uint32_t *__restrict__ tile_start,
                                                          const uint32_t *__restrict__ entries,
                                                          const float4 *__restrict__ rec0,
@@ -1037,9 +1046,12 @@ __global__ void __launch_bounds__(kWsThreads) k_blend_ws(const uint32_t *__restr
                                                          const float4 *__restrict__ rec2, Counters *ctr, int tiles_x,
                                                          int width, int height, float bg0, float bg1, float bg2,
                                                          float *__restrict__ out_rgb, float *__restrict__ out_T,
-                                                         fdgs_frame_stats *stats) {
+                                                         fdgs_frame_stats *stats,
+                                                         unsigned long long *__restrict__ contrib = nullptr,
+                                                         uint32_t *stv_info = nullptr) {
     __shared__ WsBatch sb[kWsBuf];
     __shared__ uint32_t s_n[kWsBuf];
+    __shared__ uint32_t s_acc[kContrib ? kWsBuf : 1][4][32];
     __shared__ __align__(8) uint64_t full[kWsBuf], empty[kWsBuf];
     __shared__ uint32_t s_done;
     __shared__ bool s_last;
@@ -1058,21 +1070,44 @@ __global__ void __launch_bounds__(kWsThreads) k_blend_ws(const uint32_t *__restr
     __syncthreads();
     const uint32_t first = ok ? start : end;
     if (warp == 4) {  // ------------------------------------------------ producer
+        // kContrib: flush the four consumer sums of a released batch slot
+        auto flush = [&](int b) {
+            if (lane < (int)s_n[b]) {
+                const unsigned long long tot = (unsigned long long)s_acc[b][0][lane] + s_acc[b][1][lane] +
+                                               s_acc[b][2][lane] + s_acc[b][3][lane];
+                if (tot) atomicAdd(contrib + __float_as_uint(sb[b].d[lane].w), tot);
+            }
+        };
+        if (kContrib && tid == 128 && stv_info != nullptr) {  // frame status / entry count for the caller
+            if (!ok) atomicMax(&stv_info[0], ctr->status);
+            atomicMax(&stv_info[1], ctr->n_entries);
+        }
         uint32_t k = 0;
         for (uint32_t base = first;; base += 32, ++k) {
             const int b = (int)(k % kWsBuf);
-            if (k >= kWsBuf) mb_wait(&empty[b], ((k / kWsBuf) - 1) & 1);
+            if (k >= kWsBuf) {
+                mb_wait(&empty[b], ((k / kWsBuf) - 1) & 1);
+                if (kContrib) flush(b);
+            }
             const bool stop = base >= end || *(volatile uint32_t *)&s_done == 4;
             const uint32_t n = stop ? 0u : min(32u, end - base);
             if (lane < (int)n) {
                 const uint32_t v = __ldg(entries + base + lane);
                 const float4 r0 = __ldg(rec0 + v), r1 = __ldg(rec1 + v), r2 = __ldg(rec2 + v);
                 stage_fields(tx, ty, r0, r1, r2, sb[b].a[lane], sb[b].c[lane], sb[b].d[lane]);
+                if (kContrib) s_acc[b][0][lane] = s_acc[b][1][lane] = s_acc[b][2][lane] = s_acc[b][3][lane] = 0u;
             }
             if (lane == 0) s_n[b] = n;
             __syncwarp();
             if (lane == 0) mb_arrive(&full[b]);
-            if (n == 0) break;
+            if (n == 0) {
+                if (kContrib)  // batches still in flight: wait for their release, then flush
+                    for (uint32_t kk = k >= kWsBuf - 1 ? k - (kWsBuf - 1) : 0; kk < k; ++kk) {
+                        mb_wait(&empty[kk % kWsBuf], (kk / kWsBuf) & 1);
+                        flush((int)(kk % kWsBuf));
+                    }
+                break;
+            }
         }
     } else {  // --------------------------------------------------------- consumers
         const int ly = tid >> 3, lx = (tid & 7) * 2;
@@ -1111,7 +1146,11 @@ __global__ void __launch_bounds__(kWsThreads) k_blend_ws(const uint32_t *__restr
                     const float2 t2 = fma2(make_float2(a.z, a.z), dx, make_float2(t1, t1));
                     const float2 e2 = fma2(dx, t2, make_float2(t4, t4));
                     const bool v0 = (m & pb0) == pb0 && e2.x >= thr.x, v1 = (m & pb1) == pb1 && e2.y >= thr.y;
-                    if (!(v0 || v1)) continue;
+                    if (kContrib) {  // warp-uniform skip: the REDUX below needs the whole warp
+                        if (!__any_sync(0xffffffffu, v0 || v1)) continue;
+                    } else if (!(v0 || v1)) {
+                        continue;
+                    }
                     const float a0 = v0 ? fminf(0.99f, ex2_approx(e2.x) * (1.0f / 255.0f)) : 0.0f;
                     const float a1 = v1 ? fminf(0.99f, ex2_approx(e2.y) * (1.0f / 255.0f)) : 0.0f;
                     float2 w = mul2(make_float2(a0, a1), T);
@@ -1126,6 +1165,11 @@ __global__ void __launch_bounds__(kWsThreads) k_blend_ws(const uint32_t *__restr
                     Cr = fma2(make_float2(c.z, c.z), w, Cr);
                     Cg = fma2(make_float2(c.w, c.w), w, Cg);
                     Cb = fma2(make_float2(dq.x, dq.x), w, Cb);
+                    if (kContrib) {  // S^S term alpha_i prod_{j<i}(1 - alpha_j) of P:251, this warp's 64 pixels
+                        const uint32_t f = __float2uint_rn(w.x * kContribScale) + __float2uint_rn(w.y * kContribScale);
+                        const uint32_t sum = __reduce_add_sync(0xffffffffu, f);
+                        if (lane == 0) s_acc[b][warp][q] = sum;
+                    }
                 }
                 wdone = __all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf);
                 if (wdone && lane == 0) atomicAdd(&s_done, 1u);
@@ -1144,7 +1188,7 @@ __global__ void __launch_bounds__(kWsThreads) k_blend_ws(const uint32_t *__restr
                 atomicAdd(&ctr->n_blend, (unsigned long long)n_blend);
             }
         }
-        if (ok) {
+        if (ok && out_rgb != nullptr) {
             const size_t hw = (size_t)width * height, p = (size_t)j * width + i0;
             if (in0) {
                 out_rgb[p] = fmaf(T.x, bg0, Cr.x);
@@ -1192,7 +1236,7 @@ static int tune_pgrid() {
 cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint32_t *mask_r, const CamDev &cam,
                           float t, float *out_rgb, float *out_T, char *ws, const RenderLayout &L,
                           fdgs_frame_stats *stats, cudaStream_t st, cudaEvent_t const *ev, cudaStream_t blend_st,
-                          cudaEvent_t split_ev) {
+                          cudaEvent_t split_ev, unsigned long long *contrib, uint32_t *stv_info) {
     Counters *ctr = reinterpret_cast<Counters *>(ws + L.counters);
     uint32_t *lb = reinterpret_cast<uint32_t *>(ws + L.lookback);
     float4 *rec0 = reinterpret_cast<float4 *>(ws + L.rec0);
@@ -1281,7 +1325,11 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     }
     if (ev && (e = cudaEventRecord(ev[3], bst)) != cudaSuccess) return e;
     static const bool ws_blend = tune_env("FDGS_BLEND_WS", 1) == 1;  // FDGS_BLEND_WS=0: block-synchronous k_blend
-    if (ws_blend) {
+    if (contrib != nullptr) {  // spatial-score recording (fdgs_stv_score)
+        k_blend_ws<false, true><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x,
+                                                                   L.width, L.height, cam.bg[0], cam.bg[1], cam.bg[2],
+                                                                   out_rgb, out_T, nullptr, contrib, stv_info);
+    } else if (ws_blend) {
         if (stats != nullptr)
             k_blend_ws<true><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x,
                                                                 L.width, L.height, cam.bg[0], cam.bg[1], cam.bg[2],

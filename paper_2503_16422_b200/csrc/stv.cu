@@ -1,0 +1,174 @@
+// stv.cu -- spatial-temporal variation score of Sec. 4.2.1,
+// the pruning criterion that produces the scene the
+// render path then draws.
+//
+//   S^S_i(t)  = sum over all views and pixels of alpha_i prod_{j<i}(1-alpha_j)
+//               (P:249-253): recorded by the contribution variant of the
+//               render blend (render.cu k_blend_ws<.., kContrib>), one frame
+//               per (view, t), accumulated per Gaussian in 2^-24 fixed point
+//   p2_i(t)   = ((t-mu_t)^2/Sigma_t^2 - 1/Sigma_t) p_i(t)
+//   S^TV_i(t) = 1 / (0.5 tanh|p2_i(t)| + 0.5)
+//   gamma_i   = min(V_i / V_p, 1), V_i = s_x s_y s_z s_t (binary32, left to
+//               right), V_p the nearest-rank percentile of V ("normalized
+//               following LightGaussian"; reading R20)
+//   S_i       = sum_t S^TV_i(t) gamma_i S^S_i(t)   (combine 0, time-aligned, R20)
+//             = gamma_i (sum_t S^TV_i(t)) (sum_t S^S_i(t))   (combine 1, the
+//               literal product of the two sums of P:264-272)
+//
+//   k_stv_init / k_vol_hist / k_vol_pick : exact nearest-rank selection of
+//       V_p by a 4 x 8-bit MSD radix select over the fp32 bits of V (all V > 0,
+//       so bit order = value order)
+//   k_stv_accum : per t, fold the recorded S^S with S^TV and gamma
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "fdgs_internal.h"
+
+namespace fdgs {
+
+__device__ __forceinline__ float volume4(float4 s) {
+    float v = __fmul_rn(s.x, s.y);
+    v = __fmul_rn(v, s.z);
+    return __fmul_rn(v, s.w);
+}
+
+__global__ void k_stv_init(StvState *st, uint32_t rank) {
+    const int t = threadIdx.x;
+    st->hist[t] = 0;
+    if (t == 0) {
+        st->info[0] = st->info[1] = 0;
+        st->prefix = 0;
+        st->rank = rank;
+    }
+}
+
+// Histogram of digit (bits >> shift) & 255 over the volumes whose higher digits
+// equal the selected prefix.
+__global__ void __launch_bounds__(256) k_vol_hist(const float4 *__restrict__ scale, int n, StvState *st, int shift) {
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t hi = shift >= 24 ? 0u : ~0u << (shift + 8);
+    const uint32_t prefix = st->prefix;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t bits = __float_as_uint(volume4(__ldg(scale + i)));
+        if (((bits ^ prefix) & hi) == 0) atomicAdd(&h[(bits >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (h[threadIdx.x]) atomicAdd(&st->hist[threadIdx.x], h[threadIdx.x]);
+}
+
+// Pick the digit holding the remaining rank; clear the histogram for the next pass.
+__global__ void k_vol_pick(StvState *st, int shift) {
+    __shared__ uint32_t h[256];
+    const int t = threadIdx.x;
+    h[t] = st->hist[t];
+    st->hist[t] = 0;
+    __syncthreads();
+    if (t == 0) {
+        uint32_t cum = 0, rank = st->rank;
+        for (int d = 0; d < 256; ++d) {
+            if (rank < cum + h[d]) {
+                st->prefix |= (uint32_t)d << shift;
+                st->rank = rank - cum;
+                break;
+            }
+            cum += h[d];
+        }
+    }
+}
+
+// One t: S^S_i(t) from the fixed-point recorder (then cleared for the next t),
+// S^TV_i(t) in binary64, folded into the running sums.
+__global__ void __launch_bounds__(256) k_stv_accum(SceneDev sc, float t, unsigned long long *__restrict__ contrib,
+                                                   const StvState *st, double *__restrict__ acc_a,
+                                                   double *__restrict__ acc_b, double *__restrict__ acc_c,
+                                                   bool first, bool last, int mode, float *__restrict__ out_score,
+                                                   float *__restrict__ out_spatial, float *__restrict__ out_gamma) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= sc.n) return;
+    const double ss = (double)contrib[i] * 0x1p-24;
+    contrib[i] = 0ull;
+    const float4 mean = __ldg(sc.mean + i), s = __ldg(sc.scale + i);
+    const double sig = sigma44(s, __ldg(sc.rot_l + i), __ldg(sc.rot_r + i));
+    const double dt = (double)t - (double)mean.w;
+    const double p = exp(-(dt * dt) / (2.0 * sig));
+    const double p2 = ((dt * dt) / (sig * sig) - 1.0 / sig) * p;
+    const double tv = 1.0 / (0.5 * tanh(fabs(p2)) + 0.5);
+    double a = first ? 0.0 : acc_a[i], b = first ? 0.0 : acc_b[i], c = first ? 0.0 : acc_c[i];
+    a += tv * ss;  // time-aligned
+    b += tv;       // sum_t S^TV
+    c += ss;       // sum_t S^S
+    if (out_spatial) out_spatial[i] = (float)ss;
+    if (!last) {
+        acc_a[i] = a;
+        acc_b[i] = b;
+        acc_c[i] = c;
+        return;
+    }
+    const double vp = (double)__uint_as_float(st->prefix);
+    const double g = fmin((double)volume4(s) / vp, 1.0);
+    out_score[i] = (float)(mode == 0 ? a * g : g * b * c);
+    if (out_gamma) out_gamma[i] = (float)g;
+}
+
+StvLayout stv_layout(int32_t n, const fdgs_camera *cams, int32_t n_cams, int64_t max_entries) {
+    StvLayout L{};
+    const size_t nn = (size_t)std::max(n, 1);
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    L.state = 0;
+    L.contrib = al(sizeof(StvState));
+    L.acc_a = L.contrib + al(8 * nn);
+    L.acc_b = L.acc_a + al(8 * nn);
+    L.acc_c = L.acc_b + al(8 * nn);
+    L.render = L.acc_c + al(8 * nn);
+    size_t rb = 0;
+    for (int c = 0; c < n_cams; ++c)
+        rb = std::max(rb, render_layout(n, cams[c].width, cams[c].height, max_entries).total);
+    L.total = L.render + rb;
+    return L;
+}
+
+cudaError_t launch_stv(const SceneDev &sc, const CamDev *cams, const fdgs_camera *hcams, int n_cams, const float *ts,
+                       int n_ts, uint32_t rank, int mode, int64_t max_entries, char *ws, const StvLayout &SL,
+                       float *out_score, float *out_spatial, float *out_gamma, cudaStream_t st) {
+    StvState *state = reinterpret_cast<StvState *>(ws + SL.state);
+    auto *contrib = reinterpret_cast<unsigned long long *>(ws + SL.contrib);
+    double *acc[3] = {reinterpret_cast<double *>(ws + SL.acc_a), reinterpret_cast<double *>(ws + SL.acc_b),
+                      reinterpret_cast<double *>(ws + SL.acc_c)};
+    char *rws = ws + SL.render;
+    const int n = sc.n;
+    cudaError_t e = cudaSuccess;
+    k_stv_init<<<1, 256, 0, st>>>(state, rank);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int hgrid = std::max(1, std::min((n + 255) / 256, 4 * sms));
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        k_vol_hist<<<hgrid, 256, 0, st>>>(sc.scale, n, state, shift);
+        k_vol_pick<<<1, 256, 0, st>>>(state, shift);
+    }
+    if ((e = cudaMemsetAsync(contrib, 0, 8 * (size_t)n, st)) != cudaSuccess) return e;
+    int pw = -1, ph = -1;
+    for (int k = 0; k < n_ts; ++k) {
+        for (int c = 0; c < n_cams; ++c) {
+            const RenderLayout L = render_layout(n, hcams[c].width, hcams[c].height, max_entries);
+            if (hcams[c].width != pw || hcams[c].height != ph) {
+                // epoch-tagged look-back tables sit at size-dependent offsets: restart them
+                if ((e = cudaMemsetAsync(rws, 0, L.total, st)) != cudaSuccess) return e;
+                pw = hcams[c].width;
+                ph = hcams[c].height;
+            }
+            e = launch_render(sc, nullptr, nullptr, cams[c], ts[k], nullptr, nullptr, rws, L, nullptr, st, nullptr,
+                              nullptr, nullptr, contrib, state->info);
+            if (e != cudaSuccess) return e;
+        }
+        k_stv_accum<<<(n + 255) / 256, 256, 0, st>>>(sc, ts[k], contrib, state, acc[0], acc[1], acc[2], k == 0,
+                                                     k == n_ts - 1, mode, out_score,
+                                                     out_spatial ? out_spatial + (size_t)k * n : nullptr, out_gamma);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace fdgs

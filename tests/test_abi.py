@@ -65,13 +65,29 @@ def test_host_side_argument_errors_without_gpu(lib):
     out = C.c_float()
     st = lib.fdgs_render(C.byref(sc), None, None, C.byref(cam), 0.0, C.byref(out), None, None, 0, 0, None, None)
     assert st == _lib.FDGS_ERR_INVALID_ARG and b"camera" in lib.fdgs_last_error()
-    # stv score is declared but not built this round
-    assert lib.fdgs_stv_score(None, None, 0, None, 0, None, None, None, 0, None) == _lib.FDGS_ERR_UNSUPPORTED
+    # stv score: NULL scene / opts / cameras and a bad percentile fail on the host
+    assert lib.fdgs_stv_score(None, None, 0, None, 0, None, None, None, None, None, 0, None, None) == \
+        _lib.FDGS_ERR_INVALID_ARG
+    cams = (_lib.FdgsCamera * 1)(cam)
+    opts = _lib.FdgsStvOpts(1.5, 0, 0, 1024)
+    ts = (C.c_float * 1)(0.5)
+    st = lib.fdgs_stv_score(C.byref(sc), cams, 1, ts, 1, C.byref(opts), None, None, None, None, 0, None, None)
+    assert st == _lib.FDGS_ERR_INVALID_ARG and b"percentile" in lib.fdgs_last_error()
+    opts = _lib.FdgsStvOpts(0.9, 7, 0, 1024)
+    st = lib.fdgs_stv_score(C.byref(sc), cams, 1, ts, 1, C.byref(opts), None, None, None, None, 0, None, None)
+    assert st == _lib.FDGS_ERR_INVALID_ARG and b"combine" in lib.fdgs_last_error()
 
 
 def test_workspace_sizes(lib):
+    from paper_2503_16422_b200 import _lib
     a = lib.fdgs_render_workspace_bytes(200_000, 1352, 1014, 12_800_000)
     b = lib.fdgs_render_workspace_bytes(200_000, 1352, 1014, 25_600_000)
     assert a > 200_000 * 48 and b - a >= 4 * 12_800_000
     assert lib.fdgs_render_workspace_bytes(-1, 10, 10, 0) == 0
     assert lib.fdgs_mask_compact_workspace_bytes(1000) >= 4 * (32 + 4)
+    cam = _lib.FdgsCamera()
+    cam.width, cam.height = 1352, 1014
+    cams = (_lib.FdgsCamera * 2)(cam, cam)
+    s1 = lib.fdgs_stv_workspace_bytes(200_000, cams, 2, 12_800_000)
+    assert s1 >= lib.fdgs_render_workspace_bytes(200_000, 1352, 1014, 12_800_000) + 4 * 8 * 200_000
+    assert lib.fdgs_stv_workspace_bytes(10, None, 0, 0) == 0

@@ -1,0 +1,124 @@
+"""GPU parity of fdgs_stv_score (Sec. 4.2.1)
+against the oracle (oracle/fdgs_oracle.c or_stv_score), through the C-ABI.
+
+Bars:
+  * gamma_i bit-exact (same fp32 volume, same nearest-rank selection, the
+    ratio in binary64 on both sides, one rounding to fp32);
+  * S^S_i(t) (spatial) and S_i (score): |gpu - oracle| <= 1e-4 |oracle| + 1e-4
+    per Gaussian, except for at most one Gaussian per termination knife-edge
+    pixel of the oracle (R17), which may differ by <= 0.011 (a flipped
+    stop decision moves one weight alpha T <= 1e-4 alpha / (1 - alpha) <= 0.0099
+    plus <= 1e-4 of tail weight);
+  * at BASELINE's full C3 size (one view, one t): the same bar on every
+    Gaussian, and sum_i S^S_i = sum_p (1 - T_p) of the render within the
+    fixed-point and fp32 T-update rounding (<= 1e-7 per blended pair).
+"""
+import numpy as np
+import pytest
+import torch
+
+import fdgs_inputs as fi
+import oracle
+import paper_2503_16422_b200 as fd
+
+pytestmark = pytest.mark.gpu
+
+REL, ABS, KNIFE_ABS = 1e-4, 1e-4, 0.011
+
+
+def _knife_pixels(scene, cams, ts):
+    return sum(oracle.render(scene, c, float(t))["stats"]["knife"] for t in ts for c in cams)
+
+
+def _assert_close(gpu, ref, knife, what):
+    gpu = np.asarray(gpu, np.float64)
+    err = np.abs(gpu - ref)
+    bad = err > REL * np.abs(ref) + ABS
+    assert bad.sum() <= knife, f"{what}: {bad.sum()} Gaussians off (knife pixels {knife}), worst {err.max():.3g}"
+    assert err[bad].max(initial=0.0) <= KNIFE_ABS, f"{what}: knife-edge outlier {err[bad].max():.3g}"
+    return float(err.max(initial=0.0))
+
+
+def _check(scene, cams, ts, combine=0, percentile=0.9, max_entries=None):
+    sc = fd.Scene.from_arrays(scene)
+    r = fd.stv_score(sc, cams, ts, percentile=percentile, combine=combine, spatial=True, gamma=True,
+                     max_entries=max_entries)
+    ref = oracle.stv_score(scene, cams, np.float32(ts), percentile=percentile, combine=combine)
+    knife = _knife_pixels(scene, cams, ts)
+    g = r["gamma"].cpu().numpy()
+    assert np.array_equal(g.view(np.uint32), ref["gamma"].astype(np.float32).view(np.uint32))
+    sp = r["spatial"].cpu().numpy()
+    for k in range(len(ts)):
+        _assert_close(sp[k], ref["spatial"][k], knife, f"S^S(t={ts[k]})")
+    _assert_close(r["score"].cpu().numpy(), ref["score"], knife, "score")
+    return r, ref
+
+
+def test_c1_one_view_four_times():
+    scene = fi.make_scene("c1")
+    cams = fi.make_cameras("c1")
+    _check(scene, cams, [0.0, 1 / 3, 2 / 3, 1.0])
+
+
+@pytest.mark.parametrize("combine", [0, 1])
+def test_reduced_c2_multi_view(combine):
+    scene = fi.make_scene("c2", n=4000, seed=3)
+    cams = fi.make_cameras("c2", width=96, height=72, fx=133.0, count=4)
+    r, ref = _check(scene, cams, [0.0, 0.3, 0.7, 1.0], combine=combine)
+    assert (ref["score"] > 0).sum() > 100
+
+
+def test_mixed_view_sizes_ragged_tiles():
+    """Views of different sizes share one workspace (look-back tables restarted
+    on a size change); sizes not multiples of 16."""
+    scene = fi.make_scene("c1", n=800, seed=5)
+    cams = [fi.make_cameras("c1", width=w, height=h, fx=f)[0] for (w, h, f) in
+            [(64, 64, 64.0), (37, 53, 40.0), (64, 64, 64.0), (130, 17, 90.0)]]
+    _check(scene, cams, [0.25, 0.5], percentile=0.5)
+
+
+def test_percentile_edges_and_overflow_recovery():
+    scene = fi.make_scene("c1", n=500, seed=7)
+    cams = fi.make_cameras("c1")
+    _check(scene, cams, [0.5], percentile=1.0)            # V_p = max volume
+    _check(scene, cams, [0.5], percentile=1e-9)           # V_p = min volume
+    _check(scene, cams, [0.5], max_entries=16)            # grows the entry capacity and retries
+
+
+def test_deterministic_and_empty_cases():
+    scene = fi.make_scene("c2", n=3000, seed=1)
+    cams = fi.make_cameras("c2", width=80, height=80, fx=111.0, count=3)
+    sc = fd.Scene.from_arrays(scene)
+    a = fd.stv_score(sc, cams, [0.2, 0.6], spatial=True)
+    b = fd.stv_score(sc, cams, [0.2, 0.6], spatial=True)
+    assert torch.equal(a["score"], b["score"]) and torch.equal(a["spatial"], b["spatial"])  # fixed-point sums
+    z = fd.stv_score(sc, cams, [])
+    assert torch.count_nonzero(z["score"]).item() == 0
+    # a scene nobody sees: all spatial terms and scores are exactly 0
+    far = fi.isotropic_scene([[0, 0, -50.0, 0.5]] * 40, [[0.1, 0.1, 0.1, 0.2]], [0.9])
+    r = fd.stv_score(fd.Scene.from_arrays(far), cams, [0.5], gamma=True)
+    assert torch.count_nonzero(r["score"]).item() == 0
+    assert torch.all(r["gamma"] == 1.0)
+
+
+def test_c3_full_size_one_view():
+    """BASELINE configs[2] (200k Gaussians, 1352x1014), one view at one t, in
+    the launch configuration of the render path: every Gaussian's S^S against
+    the oracle, and the partition-of-unity property against the render."""
+    scene = fi.make_scene("c3")
+    cam = fi.make_cameras("c3")[10]
+    t = float(np.float32(0.5))
+    sc = fd.Scene.from_arrays(scene)
+    r = fd.stv_score(sc, [cam], [t], spatial=True)
+    ss = r["spatial"][0].double()
+    rr = fd.Renderer(sc, cam.width, cam.height)
+    T = torch.empty((cam.height, cam.width), dtype=torch.float32, device="cuda")
+    _, stats = rr.render_checked(cam, t, out_T=T)
+    st = torch.zeros(4, dtype=torch.int64, device="cuda")
+    rr.render(cam, t, stats=st)
+    n_blend = int(st.cpu()[3])
+    lhs, rhs = float(ss.sum()), float((1.0 - T.double()).sum())
+    assert abs(lhs - rhs) <= 1e-7 * n_blend + 1e-3, (lhs, rhs, n_blend)
+    ref = oracle.contrib(scene, cam, t)
+    knife = oracle.render(scene, cam, t)["stats"]["knife"]
+    _assert_close(ss.cpu().numpy(), ref, knife, "C3 S^S")
