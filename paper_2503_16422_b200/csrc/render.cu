@@ -817,7 +817,7 @@ constexpr int kBlendThreads = 128;  // one 16x16 tile, 2 horizontally adjacent p
 struct BlendBatch {
     float4 a[kBlendThreads];  // u, v, A', B'
     float4 c[kBlendThreads];  // C', Q2, r, g
-    float4 d[kBlendThreads];  // b, pixel-AABB mask (x bits 0-15, y bits 16-31), reached rows (bits 16-31), -
+    float4 d[kBlendThreads];  // b, ~pixel-AABB mask (x bits 0-15, y bits 16-31: set = outside), reached rows (bits 16-31), gid
 };
 
 __device__ __forceinline__ void stage_load(const uint32_t *__restrict__ entries, const float4 *__restrict__ rec0,
@@ -859,7 +859,7 @@ __device__ __forceinline__ void stage_fields(int tx, int ty, const float4 &r0, c
     }
     oa = r0;
     oc = make_float4(r1.x, r1.y, r2.x, r2.y);
-    od = make_float4(r2.z, __uint_as_float(xm | (ym << 16)), __uint_as_float(yr << 16), r2.w);  // .w: gid bits
+    od = make_float4(r2.z, __uint_as_float(~(xm | (ym << 16))), __uint_as_float(yr << 16), r2.w);  // .w: gid bits
 }
 
 __device__ __forceinline__ void stage_store(BlendBatch &B, int tid, uint32_t k, uint32_t end, int tx, int ty,
@@ -920,7 +920,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restr
                 const float4 dq = B.d[q];
                 const uint32_t m = __float_as_uint(dq.y);
                 if (kCount)  // algorithmic work: pairs in the pixel AABB of live pixels
-                    n_eval += (uint32_t)((m & pb0) == pb0 && thr.x == 0.0f) + (uint32_t)((m & pb1) == pb1 && thr.y == 0.0f);
+                    n_eval += (uint32_t)((m & pb0) == 0u && thr.x == 0.0f) + (uint32_t)((m & pb1) == 0u && thr.y == 0.0f);
                 if ((__float_as_uint(dq.z) & wrows) == 0) continue;  // warp-uniform: ellipse misses these rows
                 const float4 a = B.a[q];
                 const float4 c = B.c[q];
@@ -932,7 +932,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restr
                 const float2 dx = sub2(px, make_float2(a.x, a.x));
                 const float2 t2 = fma2(make_float2(a.z, a.z), dx, make_float2(t1, t1));
                 const float2 e2 = fma2(dx, t2, make_float2(t4, t4));
-                const bool box0 = (m & pb0) == pb0, box1 = (m & pb1) == pb1;
+                const bool box0 = (m & pb0) == 0u, box1 = (m & pb1) == 0u;  // one LOP3 each
                 const bool v0 = box0 && e2.x >= thr.x, v1 = box1 && e2.y >= thr.y;
                 if (!(v0 || v1)) continue;
                 const float a0 = v0 ? fminf(0.99f, ex2_approx(e2.x) * (1.0f / 255.0f)) : 0.0f;
@@ -1051,6 +1051,7 @@ __global__ void __launch_bounds__(kWsThreads) k_blend_ws(const uint32_t *__restr
                                                          uint32_t *stv_info = nullptr) {
     __shared__ WsBatch sb[kWsBuf];
     __shared__ uint32_t s_n[kWsBuf];
+    __shared__ uint32_t s_rel[kWsBuf][4];  // per consumer warp: records whose ellipse reaches its rows
     __shared__ uint32_t s_acc[kContrib ? kWsBuf : 1][4][32];
     __shared__ __align__(8) uint64_t full[kWsBuf], empty[kWsBuf];
     __shared__ uint32_t s_done;
@@ -1091,11 +1092,22 @@ __global__ void __launch_bounds__(kWsThreads) k_blend_ws(const uint32_t *__restr
             }
             const bool stop = base >= end || *(volatile uint32_t *)&s_done == 4;
             const uint32_t n = stop ? 0u : min(32u, end - base);
+            uint32_t rows = 0;
             if (lane < (int)n) {
                 const uint32_t v = __ldg(entries + base + lane);
                 const float4 r0 = __ldg(rec0 + v), r1 = __ldg(rec1 + v), r2 = __ldg(rec2 + v);
-                stage_fields(tx, ty, r0, r1, r2, sb[b].a[lane], sb[b].c[lane], sb[b].d[lane]);
+                float4 oa, oc, od;
+                stage_fields(tx, ty, r0, r1, r2, oa, oc, od);
+                sb[b].a[lane] = oa;
+                sb[b].c[lane] = oc;
+                sb[b].d[lane] = od;
+                rows = __float_as_uint(od.z);
                 if (kContrib) s_acc[b][0][lane] = s_acc[b][1][lane] = s_acc[b][2][lane] = s_acc[b][3][lane] = 0u;
+            }
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {  // record lists per consumer warp (rows 4w..4w+3)
+                const uint32_t rel = __ballot_sync(0xffffffffu, (rows >> (16 + 4 * w)) & 0xFu);
+                if (lane == w) s_rel[b][w] = rel;
             }
             if (lane == 0) s_n[b] = n;
             __syncwarp();
@@ -1113,10 +1125,9 @@ __global__ void __launch_bounds__(kWsThreads) k_blend_ws(const uint32_t *__restr
         const int ly = tid >> 3, lx = (tid & 7) * 2;
         const int i0 = tx * 16 + lx, j = ty * 16 + ly;
         const bool in0 = i0 < width && j < height, in1 = i0 + 1 < width && j < height;
-        const float pyf = (float)j + 0.5f;
-        const float2 px = make_float2((float)i0 + 0.5f, (float)(i0 + 1) + 0.5f);
+        float pyf = (float)j + 0.5f;
+        float2 px = make_float2((float)i0 + 0.5f, (float)(i0 + 1) + 0.5f);
         const uint32_t pb0 = (1u << lx) | (1u << (16 + ly)), pb1 = (2u << lx) | (1u << (16 + ly));
-        const uint32_t wrows = 0xFu << (16 + 4 * warp);
         const float kInf = __int_as_float(0x7f800000);
         float2 thr = make_float2(in0 ? 0.0f : kInf, in1 ? 0.0f : kInf);
         float2 T = make_float2(1.0f, 1.0f), Cr = make_float2(0.f, 0.f), Cg = Cr, Cb = Cr;
@@ -1129,15 +1140,24 @@ __global__ void __launch_bounds__(kWsThreads) k_blend_ws(const uint32_t *__restr
             if (cnt == 0) break;
             if (!wdone) {
                 const WsBatch &B = sb[b];
-                for (int q = 0; q < cnt; ++q) {
+                const uint32_t rel = s_rel[b][warp];
+                // kCount visits every record (its Eq. 2 work count includes the pairs of
+                // records whose ellipse misses this warp's rows); otherwise only the
+                // records of this warp's list
+                for (uint32_t it = kCount ? (cnt == 32 ? ~0u : (1u << cnt) - 1u) : rel; it != 0u; it &= it - 1u) {
+                    const int q = __ffs(it) - 1;
                     const float4 dq = B.d[q];
                     const uint32_t m = __float_as_uint(dq.y);
-                    if (kCount)
-                        n_eval += (uint32_t)((m & pb0) == pb0 && thr.x == 0.0f) +
-                                  (uint32_t)((m & pb1) == pb1 && thr.y == 0.0f);
-                    if ((__float_as_uint(dq.z) & wrows) == 0) continue;
+                    if (kCount) {
+                        n_eval += (uint32_t)((m & pb0) == 0u && thr.x == 0.0f) +
+                                  (uint32_t)((m & pb1) == 0u && thr.y == 0.0f);
+                        if (((rel >> q) & 1u) == 0u) continue;
+                    }
                     const float4 a = B.a[q];
                     const float4 c = B.c[q];
+                    // keep the pixel centres live in registers (the compiler otherwise
+                    // rematerialises them from the indices in every iteration)
+                    asm volatile("" : "+f"(pyf), "+f"(px.x), "+f"(px.y));
                     const float dy = __fsub_rn(pyf, a.y);
                     const float t1 = __fmul_rn(a.w, dy);
                     const float t3 = __fmul_rn(c.x, dy);
@@ -1145,12 +1165,11 @@ __global__ void __launch_bounds__(kWsThreads) k_blend_ws(const uint32_t *__restr
                     const float2 dx = sub2(px, make_float2(a.x, a.x));
                     const float2 t2 = fma2(make_float2(a.z, a.z), dx, make_float2(t1, t1));
                     const float2 e2 = fma2(dx, t2, make_float2(t4, t4));
-                    const bool v0 = (m & pb0) == pb0 && e2.x >= thr.x, v1 = (m & pb1) == pb1 && e2.y >= thr.y;
-                    if (kContrib) {  // warp-uniform skip: the REDUX below needs the whole warp
-                        if (!__any_sync(0xffffffffu, v0 || v1)) continue;
-                    } else if (!(v0 || v1)) {
-                        continue;
-                    }
+                    const bool v0 = (m & pb0) == 0u && e2.x >= thr.x, v1 = (m & pb1) == 0u && e2.y >= thr.y;
+                    // branch-free body (a skip costs more issue slots than the ~10% of
+                    // records with no eligible lane save); kContrib skips warp-uniformly
+                    // since its REDUX needs the whole warp
+                    if (kContrib && !__any_sync(0xffffffffu, v0 || v1)) continue;
                     const float a0 = v0 ? fminf(0.99f, ex2_approx(e2.x) * (1.0f / 255.0f)) : 0.0f;
                     const float a1 = v1 ? fminf(0.99f, ex2_approx(e2.y) * (1.0f / 255.0f)) : 0.0f;
                     float2 w = mul2(make_float2(a0, a1), T);
