@@ -61,3 +61,18 @@ def test_generator_recipe_and_determinism():
     assert np.allclose(t, [0, 1 / 3, 2 / 3, 1])
     c2 = fi.make_cameras("c2")
     assert len(c2) == 50 and all(np.linalg.norm(c.position) == pytest.approx(4.0) for c in c2)
+
+
+def test_alpha_clamp_premultiply_identity_exhaustive():
+    """The blend computes alpha = min(0.99, 2^e2 / 255) (Eq. 2 with the 0.99
+    clamp, reading R6) as fl(min(x, c) * k) with k = fl(1/255) and
+    c = 0x437c7332 (render.cu kAlphaPre).  Exhaustive over every float32 x in
+    [128, 256) (2^e2 < 256 since e2 <= log2 255), where the clamp can engage;
+    below 128, x k < 0.99 on both sides."""
+    k = np.float32(1.0) / np.float32(255.0)
+    c = np.uint32(0x437C7332).view(np.float32)
+    lo, hi = np.float32(128.0).view(np.uint32), np.float32(256.0).view(np.uint32)
+    x = np.arange(lo, hi, dtype=np.uint32).view(np.float32)
+    want = np.minimum(np.float32(0.99), (x * k).astype(np.float32))
+    got = (np.minimum(x, c) * k).astype(np.float32)
+    assert np.array_equal(want.view(np.uint32), got.view(np.uint32))

@@ -14,8 +14,14 @@ import numpy as np
 import torch
 
 sys.path.insert(0, ".")
+import os  # noqa: E402
+
 import fdgs_inputs as fi  # noqa: E402
 import paper_2503_16422_b200 as fd  # noqa: E402
+from paper_2503_16422_b200 import _lib  # noqa: E402
+
+if os.environ.get("AB_LIB"):  # a variant build of libfdgs.so (tools/ab_build.sh)
+    _lib.LIB_PATH = os.path.abspath(os.environ["AB_LIB"])
 
 
 def main():
