@@ -1004,6 +1004,12 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restr
 // producer stops once all four are done.  Pixel mapping and arithmetic are
 // those of k_blend.
 constexpr int kWsBuf = 6;
+// fl(x * kInv255) is monotone in x and equals 0.99f exactly for one float,
+// kAlphaPre = 252.44998f (0x437c7332), so min(0.99f, fl(x * kInv255)) ==
+// fl(min(x, kAlphaPre) * kInv255) for every x >= 0 (checked exhaustively
+// over [128, 256) by tests/test_host_logic.py).
+constexpr float kInv255 = 1.0f / 255.0f;
+constexpr float kAlphaPre = 0x1.f8e664p+7f;  // 252.44998f
 constexpr int kWsThreads = 160;
 struct WsBatch {
     float4 a[32], c[32], d[32];
@@ -1170,9 +1176,11 @@ __global__ void __launch_bounds__(kWsThreads) k_blend_ws(const uint32_t *__restr
                     // records with no eligible lane save); kContrib skips warp-uniformly
                     // since its REDUX needs the whole warp
                     if (kContrib && !__any_sync(0xffffffffu, v0 || v1)) continue;
-                    const float a0 = v0 ? fminf(0.99f, ex2_approx(e2.x) * (1.0f / 255.0f)) : 0.0f;
-                    const float a1 = v1 ? fminf(0.99f, ex2_approx(e2.y) * (1.0f / 255.0f)) : 0.0f;
-                    float2 w = mul2(make_float2(a0, a1), T);
+                    // alpha = min(0.99, 2^e2 * (1/255)) computed as min(2^e2, kAlphaPre) * (1/255)
+                    // (one packed multiply; bit-identical, see kAlphaPre)
+                    const float m0 = v0 ? fminf(ex2_approx(e2.x), kAlphaPre) : 0.0f;
+                    const float m1 = v1 ? fminf(ex2_approx(e2.y), kAlphaPre) : 0.0f;
+                    float2 w = mul2(mul2(make_float2(m0, m1), make_float2(kInv255, kInv255)), T);
                     const float2 test = sub2(T, w);
                     const bool s0 = v0 && test.x < 1e-4f, s1 = v1 && test.y < 1e-4f;
                     w.x = s0 ? 0.0f : w.x;
