@@ -53,9 +53,9 @@ def apply_config(args):
     N_FRAMES_T = cfg["frames"]
     INTERVAL = cfg["keyframe_interval"]
     MASKED = not args.unmasked
-    if CONFIG != "c3" or not MASKED:
+    if CONFIG != "c3" or not MASKED or args.vq:
         METRIC = (f"frames/sec at {cfg['width']}x{cfg['height']} ({CONFIG}, "
-                  f"{'masked' if MASKED else 'unmasked'})")
+                  f"{'masked' if MASKED else 'unmasked'}{f', VQ-SH K={args.vq}' if args.vq else ''})")
 
 
 def parse():
@@ -73,6 +73,8 @@ def parse():
     p.add_argument("--no-split", action="store_true", help="blend on the front-end stream (no priority split)")
     p.add_argument("--config", choices=["c2", "c3", "c4"], default="c3")
     p.add_argument("--unmasked", action="store_true", help="render without the key-frame filter")
+    p.add_argument("--vq", type=int, default=0, metavar="K",
+                   help="Ours-PP storage: SH vector-quantised to a K-entry codebook (P:483), 0 = dense SH")
     return p.parse_args()
 
 
@@ -207,16 +209,22 @@ def run_ours(args):
     cfg = fi.CONFIGS[CONFIG]
     n = cfg["n"]
     shapes = {"mean": (n, 4), "scale": (n, 4), "rot_l": (n, 4), "rot_r": (n, 4), "opacity": (n,),
-              "log255_opacity": (n,), "sh": (n, 16, 3)}
+              "log255_opacity": (n,), "sh": (args.vq, 16, 3) if args.vq else (n, 16, 3)}
     if rank == 0:
         arrays = fi.make_scene(CONFIG)
+        if args.vq:
+            arrays = fi.vq_scene(arrays, codebook_size=args.vq, seed=1)
         tens = {k: torch.from_numpy(v).to(dev) for k, v in arrays.arrays().items()}
     else:
         arrays = None
         tens = {k: torch.empty(s, dtype=torch.float32, device=dev) for k, s in shapes.items()}
+        if args.vq:
+            tens["sh_index"] = torch.empty(n, dtype=torch.uint16, device=dev)
     if world > 1:
         for k in shapes:
             dist.broadcast(tens[k], src=0)
+        if args.vq:  # NCCL has no uint16: broadcast the bytes
+            dist.broadcast(tens["sh_index"].view(torch.uint8), src=0)
     scene = fd.Scene(tens, device=dev)
     cams = fi.make_cameras(CONFIG)
     cam_structs = [fd.camera_struct(c) for c in cams]
@@ -342,7 +350,9 @@ def run_ours(args):
                ms_per_step=round(total_ms / args.steps, 4), higher_is_better=True, scaling="weak", vs_baseline=None,
                dtype="f32 (decision path f64)", data="synthetic",
                config={"workload": WORKLOADS[CONFIG] + (", masked (union of bracketing key-frames)" if MASKED
-                                                         else ", unmasked"),
+                                                         else ", unmasked")
+                       + (f", SH vector-quantised (K={args.vq} codebook, uint16 index; Ours-PP, P:483)"
+                          if args.vq else ""),
                        "frames_per_step": F, "frames_per_rank": frames_rank, "partition": "frame f -> rank f mod N",
                        "l2": "flushed between steps (512 MiB write)", "parallelism": f"frames x{world}",
                        "streams_per_gpu": args.streams,

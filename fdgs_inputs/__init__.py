@@ -16,4 +16,5 @@ from .scenes import (  # noqa: F401
     look_at,
     scene_sha256,
     isotropic_scene,
+    vq_scene,
 )

@@ -35,7 +35,8 @@ class SceneArrays:
     rot_r: np.ndarray     # (N,4) unit quaternion (w,x,y,z)
     opacity: np.ndarray   # (N,)  sigma in (0,1]
     log255_opacity: np.ndarray  # (N,) fp32(ln(255 sigma)) computed in fp64
-    sh: np.ndarray        # (N,16,3) degree-3 SH, coefficient index k*3+c
+    sh: np.ndarray        # (N,16,3) degree-3 SH, coefficient index k*3+c; (K,16,3) codebook if sh_index
+    sh_index: np.ndarray | None = None  # (N,) uint16 VQ codebook entry per Gaussian (Ours-PP)
 
     @property
     def n(self) -> int:
@@ -43,10 +44,16 @@ class SceneArrays:
 
     def subset(self, idx) -> "SceneArrays":
         idx = np.asarray(idx, dtype=np.int64)
-        return SceneArrays(*(np.ascontiguousarray(getattr(self, f)[idx]) for f in _FIELDS))
+        if self.sh_index is None:
+            return SceneArrays(*(np.ascontiguousarray(getattr(self, f)[idx]) for f in _FIELDS))
+        return SceneArrays(*(np.ascontiguousarray(getattr(self, f)[idx]) for f in _FIELDS[:-1]), self.sh,
+                           np.ascontiguousarray(self.sh_index[idx]))
 
     def arrays(self):
-        return {f: getattr(self, f) for f in _FIELDS}
+        d = {f: getattr(self, f) for f in _FIELDS}
+        if self.sh_index is not None:
+            d["sh_index"] = self.sh_index
+        return d
 
 
 _FIELDS = ("mean", "scale", "rot_l", "rot_r", "opacity", "log255_opacity", "sh")
@@ -223,3 +230,20 @@ def frame_times(frames: int) -> np.ndarray:
 def scene_sha256(s: SceneArrays) -> dict:
     return {k: hashlib.sha256(np.ascontiguousarray(v).tobytes()).hexdigest()[:16]
             for k, v in s.arrays().items()}
+
+
+def vq_scene(scene: SceneArrays, codebook_size: int = 4096, seed: int = 1) -> SceneArrays:
+    """The scene with vector-quantised SH storage (the "Ours-PP" decode input,
+    P:483): a codebook of ``codebook_size`` SH entries drawn with the scene's
+    SH distribution (DC ~ N(0.5, 0.2), rest ~ N(0, 0.2)) and a uniform uint16
+    entry index per Gaussian.  Synthetic stand-in: the codebook is not fitted
+    to the scene (fitting is compression-time work, out of scope)."""
+    if not 1 <= codebook_size <= 65536:
+        raise ValueError("codebook_size must lie in [1, 65536]")
+    rng = np.random.default_rng(seed)
+    dc = rng.normal(0.5, 0.2, size=(codebook_size, 1, 3))
+    rest = rng.normal(0.0, 0.2, size=(codebook_size, 15, 3))
+    book = np.ascontiguousarray(np.concatenate([dc, rest], 1).astype(np.float32))
+    idx = rng.integers(0, codebook_size, size=scene.n).astype(np.uint16)
+    return SceneArrays(scene.mean, scene.scale, scene.rot_l, scene.rot_r, scene.opacity, scene.log255_opacity,
+                       book, idx)

@@ -56,8 +56,14 @@ typedef enum {
  *   log255_opacity            : float[n], L_i = fp32(ln(255 sigma_i)) computed
  *                               in binary64 (fdgs_log255_opacity fills it)
  *   sh                        : float[n][16][3], coefficient k*3+channel
+ *   sh_index, sh_codebook_size: vector-quantised SH (the "Ours-PP" storage of
+ *                               P:483, SH "vector quantization" after CompGS):
+ *                               when sh_index != NULL, `sh` points to a
+ *                               CODEBOOK float[sh_codebook_size][16][3] and
+ *                               Gaussian i's coefficients are codebook entry
+ *                               sh_index[i] (DEVICE uint16[n]); NULL = dense SH
  * Invariants (checked by fdgs_scene_validate): |‖q‖-1| <= 1e-6, scales > 0,
- * sigma in (0,1], Sigma_44 > 1e-12. */
+ * sigma in (0,1], Sigma_44 > 1e-12, sh_index[i] < sh_codebook_size. */
 typedef struct {
     int32_t n;
     const float *mean;
@@ -67,6 +73,8 @@ typedef struct {
     const float *opacity;
     const float *log255_opacity;
     const float *sh;
+    const uint16_t *sh_index;     /* nullable: dense SH                        */
+    int32_t sh_codebook_size;     /* entries of the codebook when sh_index set */
 } fdgs_scene;
 
 /* Pinhole view "I" of P:126 (HOST struct).  world->camera rotation R

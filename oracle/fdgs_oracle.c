@@ -53,7 +53,10 @@ typedef struct {
     const float *rot_r;           /* [n][4]                                  */
     const float *opacity;         /* [n]    sigma                            */
     const float *log255_opacity;  /* [n]    L = fp32(ln(255 sigma))          */
-    const float *sh;              /* [n][16][3]                              */
+    const float *sh;              /* [n][16][3], or the VQ codebook [K][16][3] */
+    const uint16_t *sh_index;     /* VQ ("vector quantization on SH"):
+                                     Gaussian i uses codebook entry sh_index[i];
+                                     NULL = dense SH                             */
 } or_scene;
 
 typedef struct {
@@ -315,7 +318,7 @@ void or_gauss_eval(const or_scene *S, int i, const or_camera *cam, float t_f, or
     for (int k = 0; k < 3; ++k) d[k] = g->mu3[k] - ccam[k];
     const double nd = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
     for (int k = 0; k < 3; ++k) d[k] /= nd;
-    or_sh_rgb(S->sh + 48 * (size_t)i, d, g->rgb);
+    or_sh_rgb(S->sh + 48 * (size_t)(S->sh_index ? S->sh_index[i] : i), d, g->rgb);
 }
 
 /* Exported: decision records for all Gaussians (mask not applied).

@@ -31,7 +31,7 @@ def build_oracle(force: bool = False) -> str:
 class _Scene(C.Structure):
     _fields_ = [("n", C.c_int32), ("mean", C.c_void_p), ("scale", C.c_void_p),
                 ("rot_l", C.c_void_p), ("rot_r", C.c_void_p), ("opacity", C.c_void_p),
-                ("log255_opacity", C.c_void_p), ("sh", C.c_void_p)]
+                ("log255_opacity", C.c_void_p), ("sh", C.c_void_p), ("sh_index", C.c_void_p)]
 
 
 class _Camera(C.Structure):
@@ -85,7 +85,10 @@ class _SceneRef:
     def __init__(self, scene):
         self.arrs = [np.ascontiguousarray(getattr(scene, f), dtype=np.float32) for f in
                      ("mean", "scale", "rot_l", "rot_r", "opacity", "log255_opacity", "sh")]
-        self.s = _Scene(int(scene.mean.shape[0]), *[a.ctypes.data for a in self.arrs])
+        idx = getattr(scene, "sh_index", None)
+        self.idx = None if idx is None else np.ascontiguousarray(idx, dtype=np.uint16)
+        self.s = _Scene(int(scene.mean.shape[0]), *[a.ctypes.data for a in self.arrs],
+                        None if self.idx is None else self.idx.ctypes.data)
 
 
 def _cam(cam):

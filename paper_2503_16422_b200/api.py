@@ -36,6 +36,8 @@ class Scene:
     """Device-resident 4D Gaussians (fdgs_scene)."""
 
     def __init__(self, tensors: dict, device=None):
+        """tensors: the _FIELDS arrays; optional "sh_index" (N,) uint16 makes
+        "sh" a VQ codebook (K,16,3) (Ours-PP storage)."""
         dev = torch.device(device or "cuda")
         self.t = {}
         for f in _FIELDS:
@@ -45,11 +47,22 @@ class Scene:
             self.t[f] = x.to(device=dev, dtype=torch.float32).contiguous()
         self.n = int(self.t["mean"].shape[0])
         self.device = dev
-        self.struct = FdgsScene(self.n, *[self.t[f].data_ptr() for f in _FIELDS])
+        idx = tensors.get("sh_index")
+        k = 0
+        if idx is not None:
+            if isinstance(idx, np.ndarray):
+                idx = torch.from_numpy(np.ascontiguousarray(idx, dtype=np.uint16))
+            self.t["sh_index"] = idx.to(device=dev, dtype=torch.uint16).contiguous()
+            k = int(self.t["sh"].shape[0])
+        self.struct = FdgsScene(self.n, *[self.t[f].data_ptr() for f in _FIELDS],
+                                self.t["sh_index"].data_ptr() if idx is not None else None, k)
 
     @classmethod
     def from_arrays(cls, arrays, device=None):
-        return cls({f: getattr(arrays, f) for f in _FIELDS}, device)
+        d = {f: getattr(arrays, f) for f in _FIELDS}
+        if getattr(arrays, "sh_index", None) is not None:
+            d["sh_index"] = arrays.sh_index
+        return cls(d, device)
 
     def nbytes(self) -> int:
         return sum(v.numel() * 4 for v in self.t.values())

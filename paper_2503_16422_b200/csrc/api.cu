@@ -152,6 +152,8 @@ SceneDev make_scenedev(const fdgs_scene &s) {
     d.opacity = s.opacity;
     d.L = s.log255_opacity;
     d.sh = reinterpret_cast<const float4 *>(s.sh);
+    d.sh_index = s.sh_index;
+    d.sh_k = s.sh_index ? s.sh_codebook_size : 0;
     return d;
 }
 
@@ -165,6 +167,8 @@ static fdgs_status check_scene(const fdgs_scene *s) {
     const void *a16[] = {s->mean, s->scale, s->rot_l, s->rot_r, s->sh};
     for (const void *q : a16)
         if ((uintptr_t)q % 16 != 0) return fail(FDGS_ERR_INVALID_ARG, "scene float4 arrays must be 16-byte aligned");
+    if (s->sh_index != nullptr && (s->sh_codebook_size < 1 || s->sh_codebook_size > 65536))
+        return fail(FDGS_ERR_INVALID_ARG, "sh_codebook_size must lie in [1, 65536] with sh_index");
     return FDGS_OK;
 }
 

@@ -148,6 +148,7 @@ __global__ void k_validate(SceneDev sc, unsigned long long *first_bad) {
     bad |= !(s.x > 0.f && s.y > 0.f && s.z > 0.f && s.w > 0.f);
     bad |= !(op > 0.f && op <= 1.f);
     bad |= !isfinite(sc.L[i]);
+    if (sc.sh_index != nullptr) bad |= (int)sc.sh_index[i] >= sc.sh_k;
     if (!bad) {
         // Sigma_44 = sum_j (R4[3][j] s_j)^2 > 1e-12
         const double a = ql.x, b = ql.y, c = ql.z, d = ql.w, p = qr.x, q = qr.y, r = qr.z, w = qr.w;

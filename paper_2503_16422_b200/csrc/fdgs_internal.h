@@ -41,7 +41,9 @@ struct SceneDev {
     int32_t n;
     const float4 *mean, *scale, *rot_l, *rot_r;
     const float *opacity, *L;
-    const float4 *sh;  // [n][12] float4 = 48 floats
+    const float4 *sh;  // [n][12] float4 = 48 floats, or the VQ codebook [K][12]
+    const uint16_t *sh_index;  // VQ: codebook entry per Gaussian (nullable)
+    int32_t sh_k;              // VQ codebook entries
 };
 
 // Workspace layout of fdgs_render (all offsets 256-byte aligned).  The

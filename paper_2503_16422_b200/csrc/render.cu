@@ -190,7 +190,9 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess(SceneDev sc, const uin
         const PreRes &R = res[r];
         const uint32_t pos = s_excl + s_cnt[r][warp] + __popc(vb[r] & lanemask_lt());
         float rgb[3];
-        sh_color(sc.sh + (size_t)R.i * 12, R.mx - cam.campos[0], R.my - cam.campos[1], R.mz - cam.campos[2], rgb);
+        // dense SH, or the VQ codebook entry of the Gaussian (Ours-PP decode)
+        const size_t row = sc.sh_index ? (size_t)__ldg(sc.sh_index + R.i) : (size_t)R.i;
+        sh_color(sc.sh + row * 12, R.mx - cam.campos[0], R.my - cam.campos[1], R.mz - cam.campos[2], rgb);
         rec0[pos] = make_float4(R.u, R.v, R.Ap, R.Bp);
         rec1[pos] = make_float4(R.Cp, R.Q2, __uint_as_float(R.ax), __uint_as_float(R.ay));
         rec2[pos] = make_float4(rgb[0], rgb[1], rgb[2], __int_as_float(R.i));
