@@ -24,6 +24,7 @@ from .oracle import (  # noqa: F401
     stv_score,
     tv_value,
     keyframe_mask,
+    keyframe_mask_contrib,
     keyframes,
     bracket,
     active_mask,

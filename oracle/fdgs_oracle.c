@@ -729,6 +729,26 @@ void or_keyframe_mask(const or_scene *S, const or_camera *cams, int32_t n_cams, 
     }
 }
 
+/* Sec. 4.2.2 read literally (reading R3b):
+ * m_{i,j} = {Gaussians whose blending weights of Eq. 2 in the view-j render at
+ * t_key sum to more than `threshold`}, the stored mask the
+ * union over the views.  Unmasked renders, primary termination branch. */
+void or_keyframe_mask_contrib(const or_scene *S, const or_camera *cams, int32_t n_cams, float t_key,
+                              double threshold, uint32_t *out)
+{
+    const int n = S->n;
+    const int nw = (n + 31) / 32;
+    for (int w = 0; w < nw; ++w) out[w] = 0;
+    double *c = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    for (int j = 0; j < n_cams; ++j) {
+        for (int i = 0; i < n; ++i) c[i] = 0.0;
+        or_contrib(S, &cams[j], t_key, c);
+        for (int i = 0; i < n; ++i)
+            if (c[i] > threshold) out[i >> 5] |= 1u << (i & 31);
+    }
+    free(c);
+}
+
 /* Sec. 4.2.2: key-frame schedule and bracketing. */
 int or_keyframes(int32_t frames, int32_t interval, int32_t *out)
 {

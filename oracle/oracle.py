@@ -55,6 +55,7 @@ def load():
             lib.or_tile_lists.argtypes = [P, P, P, C.c_float, P, P, C.c_int64]
             lib.or_tile_lists.restype = C.c_int64
             lib.or_keyframe_mask.argtypes = [P, P, C.c_int32, C.c_float, P]
+            lib.or_keyframe_mask_contrib.argtypes = [P, P, C.c_int32, C.c_float, C.c_double, P]
             lib.or_keyframes.argtypes = [C.c_int32, C.c_int32, P]
             lib.or_keyframes.restype = C.c_int
             lib.or_bracket.argtypes = [P, C.c_int32, C.c_int32, P, P]
@@ -201,6 +202,17 @@ def keyframe_mask(scene, cams, t_key):
     out = np.zeros((sr.s.n + 31) // 32, np.uint32)
     lib.or_keyframe_mask(C.byref(sr.s), arr, len(cams), float(t_key), out.ctypes.data)
     return out
+
+
+def keyframe_mask_contrib(scene, cams, t_key, threshold=0.0):
+    """Paper-literal key-frame mask: union over views of {i : sum of
+    Gaussian i's blending weights in the view's render at t_key > threshold}."""
+    lib = load()
+    sr = _SceneRef(scene)
+    arr = (_Camera * len(cams))(*[_cam(c) for c in cams])
+    out = np.zeros(max((sr.s.n + 31) // 32, 1), np.uint32)
+    lib.or_keyframe_mask_contrib(C.byref(sr.s), arr, len(cams), float(t_key), float(threshold), out.ctypes.data)
+    return out[:(sr.s.n + 31) // 32]
 
 
 def keyframes(frames, interval):

@@ -111,3 +111,43 @@ def test_combine_modes_closed_form_long_lifespan_full_cover():
     assert a["gamma"][0] == 1.0
     assert a["score"][0] == pytest.approx(2 * 4 * 0.99 * 64, rel=1e-9)
     assert b["score"][0] == pytest.approx(2 * 16 * 0.99 * 64, rel=1e-9)
+
+
+def _bits(words, n):
+    return np.unpackbits(np.asarray(words, np.uint32).view(np.uint8), bitorder="little")[:n].astype(bool)
+
+
+def test_contribution_keyframe_mask_pins():
+    """Paper-literal m_{i,j}: Gaussians whose blending
+    weights in the view-j render sum above a threshold, unioned over views."""
+    # 1. full-cover splat: S = 0.99 W H -> set just below, clear just above
+    cam = cam_axis(8, 8, 8.0)
+    sc = fi.isotropic_scene([[0, 0, 4.0, 0.5]], [[200.0, 200.0, 200.0, 0.3]], [1.0])
+    s = 0.99 * 64
+    assert _bits(oracle.keyframe_mask_contrib(sc, [cam], 0.5, s - 1e-6), 1)[0]
+    assert not _bits(oracle.keyframe_mask_contrib(sc, [cam], 0.5, s + 1e-6), 1)[0]
+    # 2. occlusion: two opaque full-cover layers drive T to 1e-4 before the
+    #    third Gaussian -> geometrically visible (the geometric mask of R3 sets
+    #    it) but it receives no blending weight (clear in the literal mask)
+    sc3 = fi.isotropic_scene([[0, 0, 4.0, 0.5], [0, 0, 5.0, 0.5], [0, 0, 6.0, 0.5]],
+                             [[200.0, 200.0, 200.0, 0.3]], [1.0])
+    geo = _bits(oracle.keyframe_mask(sc3, [cam], 0.5), 3)
+    lit = _bits(oracle.keyframe_mask_contrib(sc3, [cam], 0.5, 0.0), 3)
+    assert geo.tolist() == [True, True, True] and lit.tolist() == [True, True, False]
+    # 3. random scene: literal (threshold 0) subset of geometric, union over
+    #    views, monotone in the threshold
+    scene = fi.make_scene("c2", n=1500, seed=4)
+    cams = fi.make_cameras("c2", width=48, height=48, fx=66.0, count=3)
+    n = scene.n
+    g = _bits(oracle.keyframe_mask(scene, cams, 0.5), n)
+    m0 = _bits(oracle.keyframe_mask_contrib(scene, cams, 0.5, 0.0), n)
+    assert m0.sum() > 100 and np.all(g[m0])
+    per_view = [_bits(oracle.keyframe_mask_contrib(scene, [c], 0.5, 0.0), n) for c in cams]
+    assert np.array_equal(m0, np.logical_or.reduce(per_view))
+    m1 = _bits(oracle.keyframe_mask_contrib(scene, cams, 0.5, 0.5), n)
+    m2 = _bits(oracle.keyframe_mask_contrib(scene, cams, 0.5, 5.0), n)
+    assert np.all(m0[m1]) and np.all(m1[m2]) and m2.sum() < m1.sum() < m0.sum()
+    # per-view threshold (not the sum over views): a Gaussian is set iff some
+    # single view's sum exceeds it
+    c = np.stack([oracle.contrib(scene, cc, 0.5) for cc in cams])
+    assert np.array_equal(m1, (c > 0.5).any(0))
