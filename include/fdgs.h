@@ -206,6 +206,28 @@ size_t fdgs_keyframe_workspace_bytes(int32_t n_cams);
 fdgs_status fdgs_keyframe_mask(const fdgs_scene *scene, const fdgs_camera *cams, int32_t n_cams, float t_key,
                                uint32_t *d_out_mask, void *d_ws, size_t ws_bytes, void *stream);
 
+/* Key-frame mask read literally: m_{i,j} = {i : the
+ * blending weights alpha_i prod_{j<i}(1 - alpha_j) of Gaussian i over all
+ * pixels of the UNMASKED view-j render at t_key (Eq. 2) sum to more than
+ * `threshold`}; bit i of d_out_mask = OR over the n_cams views (
+ * threshold 0 = any blended pixel).  Weights are summed in 2^-24 fixed point
+ * (as fdgs_stv_score); the test is sum_fixed > floor(threshold * 2^24).
+ * Every blended weight is >= (1/255) * 1e-4 > 2^-24, so at threshold 0 a bit
+ * is set iff the Gaussian is blended at least once.  Unlike
+ * fdgs_keyframe_mask (reading R3) an occluded Gaussian stays clear.
+ * cams HOST views (any sizes); d_out_mask DEVICE uint32[ceil(n/32)];
+ * workspace of fdgs_keyframe_mask_contrib_workspace_bytes (256-aligned);
+ * max_entries: tile-entry capacity of each view's render; h_max_entries HOST
+ * (nullable) receives the largest per-view entry count.  SYNCHRONOUS.
+ * Errors: INVALID_ARG (NULL, bad camera, n_cams < 1, threshold < 0 or not
+ * finite, non-finite t_key), WORKSPACE_TOO_SMALL, UNSUPPORTED, OVERFLOW
+ * (retry with *h_max_entries; mask undefined), CUDA. */
+size_t fdgs_keyframe_mask_contrib_workspace_bytes(int32_t n, const fdgs_camera *cams, int32_t n_cams,
+                                                  int64_t max_entries);
+fdgs_status fdgs_keyframe_mask_contrib(const fdgs_scene *scene, const fdgs_camera *cams, int32_t n_cams,
+                                       float t_key, double threshold, int64_t max_entries, uint32_t *d_out_mask,
+                                       void *d_ws, size_t ws_bytes, uint32_t *h_max_entries, void *stream);
+
 /* d_out = d_a | d_b over ceil(n/32) words (P:285 active set).  ASYNC. */
 fdgs_status fdgs_mask_or(const uint32_t *d_a, const uint32_t *d_b, int32_t n, uint32_t *d_out, void *stream);
 

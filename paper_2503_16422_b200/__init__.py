@@ -13,6 +13,7 @@ from .api import (  # noqa: F401
     camera_struct,
     default_max_entries,
     keyframe_mask,
+    keyframe_mask_contrib,
     keyframes,
     log255_opacity,
     mask_compact,

@@ -23,6 +23,7 @@ EXPORTS = [
     "fdgs_render_workspace_bytes", "fdgs_render", "fdgs_render_timed", "fdgs_render_split", "fdgs_render_checked",
     "fdgs_render_debug_views",
     "fdgs_keyframe_workspace_bytes", "fdgs_keyframe_mask", "fdgs_mask_or",
+    "fdgs_keyframe_mask_contrib_workspace_bytes", "fdgs_keyframe_mask_contrib",
     "fdgs_mask_compact_workspace_bytes", "fdgs_mask_compact", "fdgs_stv_workspace_bytes", "fdgs_stv_score",
 ]
 
@@ -92,6 +93,8 @@ def lib():
             "fdgs_keyframe_workspace_bytes": ([I32], SZ),
             "fdgs_keyframe_mask": ([P, P, I32, F, P, P, SZ, P], C.c_int),
             "fdgs_mask_or": ([P, P, I32, P, P], C.c_int),
+            "fdgs_keyframe_mask_contrib_workspace_bytes": ([I32, P, I32, I64], SZ),
+            "fdgs_keyframe_mask_contrib": ([P, P, I32, F, C.c_double, I64, P, P, SZ, P, P], C.c_int),
             "fdgs_mask_compact_workspace_bytes": ([I32], SZ),
             "fdgs_mask_compact": ([P, P, I32, P, P, P, SZ, P], C.c_int),
             "fdgs_stv_workspace_bytes": ([I32, P, I32, I64], SZ),

@@ -284,6 +284,29 @@ def keyframe_mask(scene: Scene, cams, t_key: float, out=None, stream=None) -> to
     return out  # ws goes back to torch's stream-ordered cache: safe to reuse after the kernel
 
 
+def keyframe_mask_contrib(scene: Scene, cams, t_key: float, threshold: float = 0.0, out=None,
+                          max_entries: int | None = None, stream=None) -> torch.Tensor:
+    """Paper-literal M(t_key): union over cams of {i : Gaussian i's Eq. 2
+    blending weights in the view's render sum above `threshold`}.  Synchronous;
+    grows the per-view entry capacity on overflow."""
+    out = torch.empty(mask_words(scene.n), dtype=torch.int32, device=scene.device) if out is None else out
+    arr = (FdgsCamera * len(cams))(*[camera_struct(c) for c in cams])
+    cap = int(default_max_entries(scene.n) if max_entries is None else max_entries)
+    while True:
+        nb = lib().fdgs_keyframe_mask_contrib_workspace_bytes(scene.n, arr, len(cams), cap)
+        if nb == 0:
+            raise ValueError("invalid keyframe_mask_contrib arguments")
+        ws = torch.empty(nb, dtype=torch.uint8, device=scene.device)
+        need = C.c_uint32(0)
+        st = lib().fdgs_keyframe_mask_contrib(C.byref(scene.struct), arr, len(cams), float(t_key), float(threshold),
+                                              cap, _ptr(out), _ptr(ws), nb, C.byref(need), _stream_ptr(stream))
+        if st == _lib.FDGS_ERR_OVERFLOW:
+            cap = int(min(2 ** 32 - 1, max(2 * cap, need.value + 1)))
+            continue
+        check(st)
+        return out
+
+
 def mask_or(a: torch.Tensor, b: torch.Tensor, n: int, out=None, stream=None) -> torch.Tensor:
     out = torch.empty_like(a) if out is None else out
     check(lib().fdgs_mask_or(_ptr(a), _ptr(b), int(n), _ptr(out), _stream_ptr(stream)))

@@ -353,6 +353,53 @@ fdgs_status fdgs_keyframe_mask(const fdgs_scene *scene, const fdgs_camera *cams,
     return e == cudaSuccess ? FDGS_OK : cuda_fail(e, "fdgs_keyframe_mask");
 }
 
+size_t fdgs_keyframe_mask_contrib_workspace_bytes(int32_t n, const fdgs_camera *cams, int32_t n_cams,
+                                                  int64_t max_entries) {
+    return fdgs_stv_workspace_bytes(n, cams, n_cams, max_entries);
+}
+
+fdgs_status fdgs_keyframe_mask_contrib(const fdgs_scene *scene, const fdgs_camera *cams, int32_t n_cams,
+                                       float t_key, double threshold, int64_t max_entries, uint32_t *d_out_mask,
+                                       void *d_ws, size_t ws_bytes, uint32_t *h_max_entries, void *stream) {
+    if (h_max_entries) *h_max_entries = 0;
+    fdgs_status s = check_scene(scene);
+    if (s != FDGS_OK) return s;
+    if (cams == nullptr || n_cams < 1 || (scene->n > 0 && d_out_mask == nullptr))
+        return fail(FDGS_ERR_INVALID_ARG, "cameras / output");
+    if (!std::isfinite(t_key)) return fail(FDGS_ERR_INVALID_ARG, "t_key is not finite");
+    if (!(threshold >= 0.0) || !std::isfinite(threshold) || threshold > 1e11)
+        return fail(FDGS_ERR_INVALID_ARG, "threshold must be finite, >= 0 and <= 1e11");
+    if (max_entries < 0 || max_entries > 0xffffffffll) return fail(FDGS_ERR_INVALID_ARG, "max_entries");
+    std::vector<CamDev> cd(n_cams);
+    for (int c = 0; c < n_cams; ++c) {
+        const char *why = nullptr;
+        if (!make_camdev(cams[c], cd[c], &why)) return fail(FDGS_ERR_INVALID_ARG, "camera %d: %s", c, why);
+        const RenderLayout L = render_layout(std::max(scene->n, 0), cams[c].width, cams[c].height, max_entries);
+        if (L.n_tiles > FDGS_MAX_TILES) return fail(FDGS_ERR_UNSUPPORTED, "tile grid %d > %d", L.n_tiles, FDGS_MAX_TILES);
+    }
+    if (scene->n == 0) return FDGS_OK;
+    const StvLayout SL = stv_layout(scene->n, cams, n_cams, max_entries);
+    if (d_ws == nullptr || ws_bytes < SL.total || (uintptr_t)d_ws % 256 != 0)
+        return fail(FDGS_ERR_WORKSPACE_TOO_SMALL, "workspace needs %zu bytes (256-aligned), got %zu", SL.total,
+                    ws_bytes);
+    std::call_once(g_attr_once, [] { g_attr_err = render_set_smem_attrs(); });
+    if (g_attr_err != cudaSuccess) return cuda_fail(g_attr_err, "cudaFuncSetAttribute");
+    const unsigned long long thr_fixed = (unsigned long long)std::floor(threshold * 16777216.0);
+    cudaStream_t st = (cudaStream_t)stream;
+    char *ws = reinterpret_cast<char *>(d_ws);
+    cudaError_t e = launch_keyframe_contrib(make_scenedev(*scene), cd.data(), cams, n_cams, t_key, thr_fixed,
+                                            max_entries, ws, SL, d_out_mask, st);
+    uint32_t info[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(info, ws + SL.state, sizeof info, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "fdgs_keyframe_mask_contrib");
+    if (h_max_entries) *h_max_entries = info[1];
+    if (info[0] != FDGS_OK)
+        return fail((fdgs_status)info[0], "a view needed %u tile entries > capacity %lld", info[1],
+                    (long long)max_entries);
+    return FDGS_OK;
+}
+
 fdgs_status fdgs_mask_or(const uint32_t *d_a, const uint32_t *d_b, int32_t n, uint32_t *d_out, void *stream) {
     if (n < 0 || (n > 0 && (d_a == nullptr || d_b == nullptr || d_out == nullptr)))
         return fail(FDGS_ERR_INVALID_ARG, "bad args");

@@ -88,6 +88,10 @@ cudaError_t launch_stv(const SceneDev &sc, const CamDev *cams, const fdgs_camera
                        int n_ts, uint32_t rank, int mode, int64_t max_entries, char *ws, const StvLayout &SL,
                        float *out_score, float *out_spatial, float *out_gamma, cudaStream_t st);
 
+cudaError_t launch_keyframe_contrib(const SceneDev &sc, const CamDev *cams, const fdgs_camera *hcams, int n_cams,
+                                    float t_key, unsigned long long thr_fixed, int64_t max_entries, char *ws,
+                                    const StvLayout &SL, uint32_t *out_mask, cudaStream_t st);
+
 cudaError_t launch_keyframe(const SceneDev &sc, const CamDev *d_cams, int n_cams, float t, uint32_t *out,
                             cudaStream_t st);
 cudaError_t launch_mask_or(const uint32_t *a, const uint32_t *b, int n, uint32_t *out, cudaStream_t st);

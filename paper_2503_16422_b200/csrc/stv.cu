@@ -113,6 +113,20 @@ __global__ void __launch_bounds__(256) k_stv_accum(SceneDev sc, float t, unsigne
     if (out_gamma) out_gamma[i] = (float)g;
 }
 
+// m_{i,j} of P:282 read literally: bit i |= (view's weight sum of i > threshold);
+// the recorder is cleared for the next view.
+__global__ void __launch_bounds__(256) k_contrib_mask(unsigned long long *__restrict__ contrib, int n,
+                                                      unsigned long long thr_fixed, uint32_t *__restrict__ mask) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool set = false;
+    if (i < n) {
+        set = contrib[i] > thr_fixed;
+        contrib[i] = 0ull;
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, set);
+    if ((threadIdx.x & 31) == 0 && i < n && word) mask[i >> 5] |= word;
+}
+
 StvLayout stv_layout(int32_t n, const fdgs_camera *cams, int32_t n_cams, int64_t max_entries) {
     StvLayout L{};
     const size_t nn = (size_t)std::max(n, 1);
@@ -167,6 +181,33 @@ cudaError_t launch_stv(const SceneDev &sc, const CamDev *cams, const fdgs_camera
         k_stv_accum<<<(n + 255) / 256, 256, 0, st>>>(sc, ts[k], contrib, state, acc[0], acc[1], acc[2], k == 0,
                                                      k == n_ts - 1, mode, out_score,
                                                      out_spatial ? out_spatial + (size_t)k * n : nullptr, out_gamma);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_keyframe_contrib(const SceneDev &sc, const CamDev *cams, const fdgs_camera *hcams, int n_cams,
+                                    float t_key, unsigned long long thr_fixed, int64_t max_entries, char *ws,
+                                    const StvLayout &SL, uint32_t *out_mask, cudaStream_t st) {
+    StvState *state = reinterpret_cast<StvState *>(ws + SL.state);
+    auto *contrib = reinterpret_cast<unsigned long long *>(ws + SL.contrib);
+    char *rws = ws + SL.render;
+    const int n = sc.n;
+    cudaError_t e;
+    k_stv_init<<<1, 256, 0, st>>>(state, 0u);
+    if ((e = cudaMemsetAsync(contrib, 0, 8 * (size_t)n, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(out_mask, 0, 4 * (size_t)((n + 31) / 32), st)) != cudaSuccess) return e;
+    int pw = -1, ph = -1;
+    for (int c = 0; c < n_cams; ++c) {
+        const RenderLayout L = render_layout(n, hcams[c].width, hcams[c].height, max_entries);
+        if (hcams[c].width != pw || hcams[c].height != ph) {
+            if ((e = cudaMemsetAsync(rws, 0, L.total, st)) != cudaSuccess) return e;
+            pw = hcams[c].width;
+            ph = hcams[c].height;
+        }
+        e = launch_render(sc, nullptr, nullptr, cams[c], t_key, nullptr, nullptr, rws, L, nullptr, st, nullptr,
+                          nullptr, nullptr, contrib, state->info);
+        if (e != cudaSuccess) return e;
+        k_contrib_mask<<<(n + 255) / 256, 256, 0, st>>>(contrib, n, thr_fixed, out_mask);
     }
     return cudaGetLastError();
 }

@@ -122,3 +122,53 @@ def test_c3_full_size_one_view():
     ref = oracle.contrib(scene, cam, t)
     knife = oracle.render(scene, cam, t)["stats"]["knife"]
     _assert_close(ss.cpu().numpy(), ref, knife, "C3 S^S")
+
+
+# ------------------------------------------- paper-literal key-frame masks
+def _mask_bits(words, n):
+    return np.unpackbits(np.asarray(words).view(np.uint32).view(np.uint8), bitorder="little")[:n].astype(bool)
+
+
+@pytest.mark.parametrize("threshold", [0.0, 0.25, 3.0])
+def test_literal_keyframe_mask_parity(threshold):
+    """P:282 m_{i,j} from the Eq. 2 weights against the oracle:
+    bit-exact except Gaussians whose per-view sum lies within the S^S tolerance
+    of the threshold, and at most one Gaussian per termination knife-edge pixel."""
+    scene = fi.make_scene("c2", n=6000, seed=8)
+    cams = fi.make_cameras("c2", width=120, height=96, fx=166.0, count=5)
+    t = float(np.float32(0.45))
+    sc = fd.Scene.from_arrays(scene)
+    got = _mask_bits(fd.keyframe_mask_contrib(sc, cams, t, threshold).cpu().numpy(), scene.n)
+    want = _mask_bits(oracle.keyframe_mask_contrib(scene, cams, t, threshold), scene.n)
+    per_view = np.stack([oracle.contrib(scene, c, t) for c in cams])
+    near = (np.abs(per_view - threshold) <= REL * threshold + ABS).any(0) if threshold > 0 else np.zeros(scene.n, bool)
+    knife = _knife_pixels(scene, cams, [t])
+    diff = (got != want) & ~near
+    assert diff.sum() <= knife, (diff.sum(), knife)
+    assert want.sum() > 200
+    # literal (threshold 0) masks are subsets of the geometric masks of reading R3
+    if threshold == 0.0:
+        geo = _mask_bits(fd.keyframe_mask(sc, cams, t).cpu().numpy(), scene.n)
+        assert np.all(geo[got]) and geo.sum() > got.sum()
+
+
+def test_literal_keyframe_mask_soundness_full_c3():
+    """Full-size C3 rig at a key-frame: rendering a mask view at t_key under the
+    literal mask (threshold 0) equals the unmasked render except where a dropped
+    Gaussian was the one that stopped a pixel (it receives no weight, yet decides
+    termination; R3b).  There the pixel continues with the
+    transmittance left at the stop, T < 1e-4 / (1 - alpha) <= 0.01, so every
+    pixel is within 0.0101 and only a sliver of pixels differs at all."""
+    scene = fi.make_scene("c3")
+    cams = fi.make_cameras("c3")[::5]
+    t = float(fi.frame_times(300)[140])
+    sc = fd.Scene.from_arrays(scene)
+    m = fd.keyframe_mask_contrib(sc, cams, t, 0.0)
+    r = fd.Renderer(sc, cams[0].width, cams[0].height)
+    for cam in cams:
+        a, _ = r.render_checked(cam, t, m, m)
+        a = a.clone()
+        b, _ = r.render_checked(cam, t)
+        d = (a - b).abs()
+        assert float(d.max()) <= 0.0101
+        assert int((d.amax(0) > 0).sum()) <= 1e-3 * cam.width * cam.height
