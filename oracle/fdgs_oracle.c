@@ -817,6 +817,16 @@ double or_tv(double t, double mu_t, double st)
     return 1.0 / (0.5 * tanh(fabs(p2)) + 0.5);
 }
 
+/* Ablation variant (d) of P:653-660: S^TV from the first derivative
+ * p1_i(t) = -((t - mu_t) / Sigma_t) p_i(t) instead of p2. */
+double or_tv_p1(double t, double mu_t, double st)
+{
+    const double dt = t - mu_t;
+    const double p = exp(-(dt * dt) / (2.0 * st));
+    const double p1 = -(dt / st) * p;
+    return 1.0 / (0.5 * tanh(fabs(p1)) + 0.5);
+}
+
 float or_volume(const or_scene *S, int i)
 {
     const float *s = S->scale + 4 * (size_t)i;
@@ -826,8 +836,16 @@ float or_volume(const or_scene *S, int i)
     return v;
 }
 
+/* variant (the score ablations of P:636-669, Table ablation_score):
+ *   0 full      S_i(t) terms: T = S^TV(p2) gamma,  S = S^S
+ *   1 S^S only  T = 1,                            S = S^S
+ *   2 S^T only  T = S^TV(p2) gamma,               S = 1
+ *   3 w. p1     T = S^TV(p1) gamma,               S = S^S
+ *   4 w. Sigma_t T = Sigma_t gamma,               S = S^S
+ * mode 0: S_i = sum_t T(t) S(t); mode 1: S_i = (sum_t T(t)) (sum_t S(t)). */
 int or_stv_score(const or_scene *S, const or_camera *cams, int32_t n_cams, const float *ts, int32_t n_ts,
-                 double percentile, double *score, double *spatial, double *tv, double *gamma, int mode)
+                 double percentile, double *score, double *spatial, double *tv, double *gamma, int mode,
+                 int variant)
 {
     const int n = S->n;
     if (n <= 0) return 0;
@@ -851,16 +869,22 @@ int or_stv_score(const or_scene *S, const or_camera *cams, int32_t n_cams, const
         for (int c = 0; c < n_cams; ++c) or_contrib(S, &cams[c], ts[k], ss);
         for (int i = 0; i < n; ++i) {
             const double g = fmin((double)vol[i] / vp, 1.0);
-            const double v = or_tv((double)ts[k], (double)S->mean[4 * (size_t)i + 3], sig[i]);
-            score[i] += v * g * ss[i];
-            tv_sum[i] += v;
-            ss_sum[i] += ss[i];
+            const double mu = (double)S->mean[4 * (size_t)i + 3];
+            const double v = or_tv((double)ts[k], mu, sig[i]);
+            double Tt = v * g, St = ss[i];
+            if (variant == 1) Tt = 1.0;
+            if (variant == 2) St = 1.0;
+            if (variant == 3) Tt = or_tv_p1((double)ts[k], mu, sig[i]) * g;
+            if (variant == 4) Tt = sig[i] * g;
+            score[i] += Tt * St;
+            tv_sum[i] += Tt;
+            ss_sum[i] += St;
             if (spatial) spatial[(size_t)k * n + i] = ss[i];
             if (tv) tv[(size_t)k * n + i] = v;
         }
     }
     if (mode == 1)
-        for (int i = 0; i < n; ++i) score[i] = fmin((double)vol[i] / vp, 1.0) * tv_sum[i] * ss_sum[i];
+        for (int i = 0; i < n; ++i) score[i] = tv_sum[i] * ss_sum[i];
     free(tv_sum);
     free(ss_sum);
     if (gamma)

@@ -67,7 +67,9 @@ def load():
             lib.or_band_tiles.restype = C.c_int
             lib.or_num_threads.restype = C.c_int
             lib.or_contrib.argtypes = [P, P, C.c_float, P]
-            lib.or_stv_score.argtypes = [P, P, C.c_int32, P, C.c_int32, C.c_double, P, P, P, P, C.c_int]
+            lib.or_stv_score.argtypes = [P, P, C.c_int32, P, C.c_int32, C.c_double, P, P, P, P, C.c_int, C.c_int]
+            lib.or_tv_p1.argtypes = [C.c_double, C.c_double, C.c_double]
+            lib.or_tv_p1.restype = C.c_double
             lib.or_tv.argtypes = [C.c_double, C.c_double, C.c_double]
             lib.or_tv.restype = C.c_double
             lib.or_sigma_t.argtypes = [P, C.c_int]
@@ -267,9 +269,10 @@ def contrib(scene, cam, t):
     return out[:sr.s.n]
 
 
-def stv_score(scene, cams, ts, percentile=0.9, combine=0):
+def stv_score(scene, cams, ts, percentile=0.9, combine=0, variant=0):
     """Spatial-temporal variation score: dict(score, spatial, tv, gamma).
-    combine 0 = time-aligned sum_t S^TV gamma S^S (R20), 1 = product of the sums."""
+    combine 0 = time-aligned sum_t S^T S^S (R20), 1 = product of the sums;
+    variant 0 full, 1 S^S only, 2 S^T only, 3 S^TV from p1, 4 Sigma_t."""
     lib = load()
     sr = _SceneRef(scene)
     n = sr.s.n
@@ -280,12 +283,14 @@ def stv_score(scene, cams, ts, percentile=0.9, combine=0):
     tv = np.zeros((len(ts), max(n, 1)))
     gamma = np.zeros(max(n, 1))
     lib.or_stv_score(C.byref(sr.s), arr, len(cams), ts.ctypes.data, len(ts), float(percentile), score.ctypes.data,
-                     spatial.ctypes.data, tv.ctypes.data, gamma.ctypes.data, int(combine))
+                     spatial.ctypes.data, tv.ctypes.data, gamma.ctypes.data, int(combine), int(variant))
     return dict(score=score[:n], spatial=spatial[:, :n], tv=tv[:, :n], gamma=gamma[:n])
 
 
-def tv_value(t, mu_t, sigma_t):
-    return float(load().or_tv(float(t), float(mu_t), float(sigma_t)))
+def tv_value(t, mu_t, sigma_t, order=2):
+    """S^TV of one Gaussian at t from p2 (order 2) or p1 (order 1)."""
+    f = load().or_tv if order == 2 else load().or_tv_p1
+    return float(f(float(t), float(mu_t), float(sigma_t)))
 
 
 def num_threads():

@@ -151,3 +151,30 @@ def test_contribution_keyframe_mask_pins():
     # single view's sum exceeds it
     c = np.stack([oracle.contrib(scene, cc, 0.5) for cc in cams])
     assert np.array_equal(m1, (c > 0.5).any(0))
+
+
+def test_score_ablation_variants_closed_forms():
+    """Variants of Table ablation_score on the full-cover splat
+    (S^S = 0.99 W H at every t, gamma = 1):
+      long lifespan (Sigma_t = 1e12): S^TV(p2) = S^TV(p1) = 2;
+      short lifespan (Sigma_t = 0.01) at t = mu_t: p1 = 0 -> S^TV(p1) = 2,
+      |p2| = 1/Sigma_t = 100 -> S^TV(p2) = 1."""
+    cam = cam_axis(8, 8, 8.0)
+    W = 0.99 * 64
+    sc = fi.isotropic_scene([[0, 0, 4.0, 0.5]], [[200.0, 200.0, 200.0, 1e6]], [1.0])
+    ts = np.float32([0.0, 0.5, 1.0])
+    n = len(ts)
+    v = lambda variant, combine=0: oracle.stv_score(sc, [cam], ts, variant=variant, combine=combine)["score"][0]
+    assert v(0) == pytest.approx(2 * W * n, rel=1e-9)
+    assert v(1) == pytest.approx(W * n, rel=1e-12)               # S^S only
+    assert v(2) == pytest.approx(2 * n, rel=1e-9)                # S^T only
+    assert v(3) == pytest.approx(2 * W * n, rel=1e-9)            # p1
+    assert v(4) == pytest.approx(1e12 * W * n, rel=1e-6)         # Sigma_t
+    assert v(1, 1) == pytest.approx(n * W * n, rel=1e-12)        # (sum_t 1)(sum_t S^S)
+    sc2 = fi.isotropic_scene([[0, 0, 4.0, 0.5]], [[200.0, 200.0, 200.0, 0.1]], [1.0])
+    t = np.float32([0.5])
+    assert oracle.tv_value(0.5, 0.5, 0.01, order=1) == pytest.approx(2.0, abs=1e-12)
+    assert oracle.tv_value(0.5, 0.5, 0.01, order=2) == pytest.approx(1.0, abs=1e-12)
+    s0 = oracle.stv_score(sc2, [cam], t, variant=0)
+    s3 = oracle.stv_score(sc2, [cam], t, variant=3)
+    assert s3["score"][0] == pytest.approx(2.0 * s0["score"][0], rel=1e-6)
