@@ -255,6 +255,10 @@ fdgs_status fdgs_mask_compact(const uint32_t *d_a, const uint32_t *d_b, int32_t 
  *   combine_mode 0: S_i = sum_t S^TV_i(t) gamma_i S^S_i(t)  (time-aligned, R20)
  *   combine_mode 1: S_i = gamma_i (sum_t S^TV_i(t)) (sum_t S^S_i(t))  (the
  *               literal product of the two sums of P:264-272)
+ *   variant (score ablations of P:636-669; the per-t factors T(t), S(t) that
+ *   the combine folds): 0 full T = S^TV gamma, S = S^S; 1 S^S only T = 1;
+ *   2 S^T only S = 1; 3 S^TV from p1_i(t) = -((t-mu_t)/Sigma_t) p_i(t);
+ *   4 T = Sigma_t gamma
  * Arguments: cams HOST array of n_cams views (any sizes); ts HOST float[n_ts];
  *   d_out_score DEVICE float[n]; d_out_spatial DEVICE float[n_ts][n] S^S_i(t)
  *   (nullable); d_out_gamma DEVICE float[n] (nullable); d_ws DEVICE workspace
@@ -263,13 +267,13 @@ fdgs_status fdgs_mask_compact(const uint32_t *d_a, const uint32_t *d_b, int32_t 
  *   count E, so a caller can size opts->max_entries.
  * SYNCHRONOUS (one stream sync at the end).  Errors: INVALID_ARG (NULL
  * pointers, bad camera, n_ts < 0, n_cams < 1, non-finite t, percentile outside
- * (0, 1], unknown combine_mode), WORKSPACE_TOO_SMALL, UNSUPPORTED (tile grid >
+ * (0, 1], unknown combine_mode or variant), WORKSPACE_TOO_SMALL, UNSUPPORTED (tile grid >
  * FDGS_MAX_TILES), OVERFLOW (some view needed more than opts->max_entries tile
  * entries: outputs undefined; retry with *h_max_entries), CUDA. */
 typedef struct {
     double volume_percentile;  /* gamma clip percentile, nearest rank (0.9)  */
     int32_t combine_mode;      /* 0 time-aligned (default), 1 product of sums */
-    int32_t reserved;
+    int32_t variant;           /* 0 full (default) .. 4, see above            */
     int64_t max_entries;       /* tile-entry capacity of each per-view render  */
 } fdgs_stv_opts;
 size_t fdgs_stv_workspace_bytes(int32_t n, const fdgs_camera *cams, int32_t n_cams, int64_t max_entries);

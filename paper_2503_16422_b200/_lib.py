@@ -52,7 +52,7 @@ class FdgsDebugViews(C.Structure):
 
 
 class FdgsStvOpts(C.Structure):
-    _fields_ = [("volume_percentile", C.c_double), ("combine_mode", C.c_int32), ("reserved", C.c_int32),
+    _fields_ = [("volume_percentile", C.c_double), ("combine_mode", C.c_int32), ("variant", C.c_int32),
                 ("max_entries", C.c_int64)]
 
 

@@ -325,7 +325,7 @@ def mask_compact(a: torch.Tensor, n: int, b: torch.Tensor | None = None, stream=
 
 
 def stv_score(scene: Scene, cams, ts, percentile: float = 0.9, combine: int = 0, spatial: bool = False,
-              gamma: bool = False, max_entries: int | None = None, stream=None) -> dict:
+              gamma: bool = False, max_entries: int | None = None, stream=None, variant: int = 0) -> dict:
     """fdgs_stv_score (Sec. 4.2.1, P:241-272): dict(score[n], spatial[n_ts][n] | None,
     gamma[n] | None) as device float32 tensors.  Synchronous; grows the per-view
     tile-entry capacity and retries on overflow."""
@@ -339,7 +339,7 @@ def stv_score(scene: Scene, cams, ts, percentile: float = 0.9, combine: int = 0,
     gm = torch.empty(max(n, 1), dtype=torch.float32, device=dev) if gamma else None
     cap = int(default_max_entries(n) if max_entries is None else max_entries)
     while True:
-        opts = _lib.FdgsStvOpts(float(percentile), int(combine), 0, cap)
+        opts = _lib.FdgsStvOpts(float(percentile), int(combine), int(variant), cap)
         nb = lib().fdgs_stv_workspace_bytes(n, arr, len(cs), cap)
         if nb == 0:
             raise ValueError("invalid stv_score arguments")

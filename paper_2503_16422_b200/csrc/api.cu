@@ -441,6 +441,7 @@ fdgs_status fdgs_stv_score(const fdgs_scene *scene, const fdgs_camera *cams, int
     if (!(opts->volume_percentile > 0.0 && opts->volume_percentile <= 1.0))
         return fail(FDGS_ERR_INVALID_ARG, "volume_percentile must lie in (0, 1]");
     if (opts->combine_mode != 0 && opts->combine_mode != 1) return fail(FDGS_ERR_INVALID_ARG, "combine_mode");
+    if (opts->variant < 0 || opts->variant > 4) return fail(FDGS_ERR_INVALID_ARG, "variant must lie in [0, 4]");
     if (opts->max_entries < 0 || opts->max_entries > 0xffffffffll) return fail(FDGS_ERR_INVALID_ARG, "max_entries");
     for (int k = 0; k < n_ts; ++k)
         if (!std::isfinite(ts[k])) return fail(FDGS_ERR_INVALID_ARG, "ts[%d] is not finite", k);
@@ -471,7 +472,7 @@ fdgs_status fdgs_stv_score(const fdgs_scene *scene, const fdgs_camera *cams, int
     char *ws = reinterpret_cast<char *>(d_ws);
     // camera constants go to the device by value (kernel arguments), so cd is host-only
     cudaError_t e = launch_stv(make_scenedev(*scene), cd.data(), cams, n_cams, ts, n_ts, (uint32_t)rank,
-                               opts->combine_mode, opts->max_entries, ws, SL, d_out_score, d_out_spatial, d_out_gamma,
+                               opts->combine_mode, opts->variant, opts->max_entries, ws, SL, d_out_score, d_out_spatial, d_out_gamma,
                                st);
     uint32_t info[2] = {0, 0};
     if (e == cudaSuccess) e = cudaMemcpyAsync(info, ws + SL.state, sizeof info, cudaMemcpyDeviceToHost, st);

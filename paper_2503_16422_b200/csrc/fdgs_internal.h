@@ -85,8 +85,9 @@ struct StvLayout {
 };
 StvLayout stv_layout(int32_t n, const fdgs_camera *cams, int32_t n_cams, int64_t max_entries);
 cudaError_t launch_stv(const SceneDev &sc, const CamDev *cams, const fdgs_camera *hcams, int n_cams, const float *ts,
-                       int n_ts, uint32_t rank, int mode, int64_t max_entries, char *ws, const StvLayout &SL,
-                       float *out_score, float *out_spatial, float *out_gamma, cudaStream_t st);
+                       int n_ts, uint32_t rank, int mode, int variant, int64_t max_entries, char *ws,
+                       const StvLayout &SL, float *out_score, float *out_spatial, float *out_gamma,
+                       cudaStream_t st);
 
 cudaError_t launch_keyframe_contrib(const SceneDev &sc, const CamDev *cams, const fdgs_camera *hcams, int n_cams,
                                     float t_key, unsigned long long thr_fixed, int64_t max_entries, char *ws,

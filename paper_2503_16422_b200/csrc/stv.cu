@@ -81,11 +81,17 @@ __global__ void k_vol_pick(StvState *st, int shift) {
 
 // One t: S^S_i(t) from the fixed-point recorder (then cleared for the next t),
 // S^TV_i(t) in binary64, folded into the running sums.
+// Per-t terms by variant (score ablations of P:636-669): the temporal factor
+// T(t) (gamma applied at the end, it is constant in t) and the spatial S(t):
+//   0 full T = S^TV(p2), S = S^S     1 S^S only T = 1 (no gamma), S = S^S
+//   2 S^T only T = S^TV(p2), S = 1   3 T = S^TV(p1) = 1/(0.5 tanh|p1| + 0.5), S = S^S
+//   4 T = Sigma_t, S = S^S
 __global__ void __launch_bounds__(256) k_stv_accum(SceneDev sc, float t, unsigned long long *__restrict__ contrib,
                                                    const StvState *st, double *__restrict__ acc_a,
                                                    double *__restrict__ acc_b, double *__restrict__ acc_c,
-                                                   bool first, bool last, int mode, float *__restrict__ out_score,
-                                                   float *__restrict__ out_spatial, float *__restrict__ out_gamma) {
+                                                   bool first, bool last, int mode, int variant,
+                                                   float *__restrict__ out_score, float *__restrict__ out_spatial,
+                                                   float *__restrict__ out_gamma) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= sc.n) return;
     const double ss = (double)contrib[i] * 0x1p-24;
@@ -94,12 +100,23 @@ __global__ void __launch_bounds__(256) k_stv_accum(SceneDev sc, float t, unsigne
     const double sig = sigma44(s, __ldg(sc.rot_l + i), __ldg(sc.rot_r + i));
     const double dt = (double)t - (double)mean.w;
     const double p = exp(-(dt * dt) / (2.0 * sig));
-    const double p2 = ((dt * dt) / (sig * sig) - 1.0 / sig) * p;
-    const double tv = 1.0 / (0.5 * tanh(fabs(p2)) + 0.5);
+    double Tt, St = ss;
+    if (variant == 3) {
+        const double p1 = -(dt / sig) * p;
+        Tt = 1.0 / (0.5 * tanh(fabs(p1)) + 0.5);
+    } else if (variant == 4) {
+        Tt = sig;
+    } else if (variant == 1) {
+        Tt = 1.0;
+    } else {
+        const double p2 = ((dt * dt) / (sig * sig) - 1.0 / sig) * p;
+        Tt = 1.0 / (0.5 * tanh(fabs(p2)) + 0.5);
+    }
+    if (variant == 2) St = 1.0;
     double a = first ? 0.0 : acc_a[i], b = first ? 0.0 : acc_b[i], c = first ? 0.0 : acc_c[i];
-    a += tv * ss;  // time-aligned
-    b += tv;       // sum_t S^TV
-    c += ss;       // sum_t S^S
+    a += Tt * St;  // time-aligned
+    b += Tt;       // sum_t T
+    c += St;       // sum_t S
     if (out_spatial) out_spatial[i] = (float)ss;
     if (!last) {
         acc_a[i] = a;
@@ -109,7 +126,8 @@ __global__ void __launch_bounds__(256) k_stv_accum(SceneDev sc, float t, unsigne
     }
     const double vp = (double)__uint_as_float(st->prefix);
     const double g = fmin((double)volume4(s) / vp, 1.0);
-    out_score[i] = (float)(mode == 0 ? a * g : g * b * c);
+    const double gg = variant == 1 ? 1.0 : g;
+    out_score[i] = (float)(mode == 0 ? a * gg : gg * b * c);
     if (out_gamma) out_gamma[i] = (float)g;
 }
 
@@ -145,8 +163,9 @@ StvLayout stv_layout(int32_t n, const fdgs_camera *cams, int32_t n_cams, int64_t
 }
 
 cudaError_t launch_stv(const SceneDev &sc, const CamDev *cams, const fdgs_camera *hcams, int n_cams, const float *ts,
-                       int n_ts, uint32_t rank, int mode, int64_t max_entries, char *ws, const StvLayout &SL,
-                       float *out_score, float *out_spatial, float *out_gamma, cudaStream_t st) {
+                       int n_ts, uint32_t rank, int mode, int variant, int64_t max_entries, char *ws,
+                       const StvLayout &SL, float *out_score, float *out_spatial, float *out_gamma,
+                       cudaStream_t st) {
     StvState *state = reinterpret_cast<StvState *>(ws + SL.state);
     auto *contrib = reinterpret_cast<unsigned long long *>(ws + SL.contrib);
     double *acc[3] = {reinterpret_cast<double *>(ws + SL.acc_a), reinterpret_cast<double *>(ws + SL.acc_b),
@@ -179,7 +198,7 @@ cudaError_t launch_stv(const SceneDev &sc, const CamDev *cams, const fdgs_camera
             if (e != cudaSuccess) return e;
         }
         k_stv_accum<<<(n + 255) / 256, 256, 0, st>>>(sc, ts[k], contrib, state, acc[0], acc[1], acc[2], k == 0,
-                                                     k == n_ts - 1, mode, out_score,
+                                                     k == n_ts - 1, mode, variant, out_score,
                                                      out_spatial ? out_spatial + (size_t)k * n : nullptr, out_gamma);
     }
     return cudaGetLastError();

@@ -76,6 +76,9 @@ def test_host_side_argument_errors_without_gpu(lib):
     opts = _lib.FdgsStvOpts(0.9, 7, 0, 1024)
     st = lib.fdgs_stv_score(C.byref(sc), cams, 1, ts, 1, C.byref(opts), None, None, None, None, 0, None, None)
     assert st == _lib.FDGS_ERR_INVALID_ARG and b"combine" in lib.fdgs_last_error()
+    opts = _lib.FdgsStvOpts(0.9, 0, 5, 1024)
+    st = lib.fdgs_stv_score(C.byref(sc), cams, 1, ts, 1, C.byref(opts), None, None, None, None, 0, None, None)
+    assert st == _lib.FDGS_ERR_INVALID_ARG and b"variant" in lib.fdgs_last_error()
 
 
 def test_workspace_sizes(lib):
