@@ -223,36 +223,50 @@ class RenderPipeline:
         self.front = [torch.cuda.Stream(device=scene.device, priority=-1 if split else 0) for _ in range(depth)]
         self.blend = [torch.cuda.Stream(device=scene.device, priority=0) for _ in range(depth)] if split else None
         self.split_ev = [torch.cuda.Event() for _ in range(depth)]
+        self.copy = torch.cuda.Stream(device=scene.device)  # D2H of finished frames (render_many host_outs)
         self.depth = depth
 
     @property
     def streams(self):
         return self.front + (self.blend or [])
 
-    def render_many(self, frames, outs, stats=None, stage_events=None, stream=None):
+    def render_many(self, frames, outs, stats=None, stage_events=None, stream=None, host_outs=None):
         """frames: list of (cam, t, mask_l, mask_r); outs: list of output tensors.
-        Ordered after the current work of `stream` (default: current stream), and
-        `stream` waits for every frame before continuing.  Async."""
+        host_outs (optional): pinned host tensors; frame k is copied D2H on a
+        copy stream as soon as its blend finishes, overlapping the rendering of
+        later frames.  Ordered after the current work of `stream` (default:
+        current stream), and `stream` waits for every frame (and copy) before
+        continuing.  Async."""
         main = stream or torch.cuda.current_stream()
         start = torch.cuda.Event()
         start.record(main)
         for s in self.streams:
             s.wait_event(start)
+        if host_outs is not None:
+            self.copy.wait_event(start)
         for k, (cam, t, ml, mr) in enumerate(frames):
             i = k % self.depth
             r = self.renderers[i]
             if not self.split:
                 r.render(cam, t, ml, mr, out=outs[k], stats=None if stats is None else stats[k], stream=self.front[i],
                          stage_events=None if stage_events is None else stage_events[k])
-                continue
-            if k >= self.depth:  # the workspace is free once its previous blend is done
-                done = torch.cuda.Event()
-                done.record(self.blend[i])
-                self.front[i].wait_event(done)
-            r.render_split(cam, t, ml, mr, out=outs[k], stats=None if stats is None else stats[k],
-                           stream=self.front[i], blend_stream=self.blend[i], split_event=self.split_ev[i],
-                           stage_events=None if stage_events is None else stage_events[k])
-        for s in self.streams:
+                last = self.front[i]
+            else:
+                if k >= self.depth:  # the workspace is free once its previous blend is done
+                    done = torch.cuda.Event()
+                    done.record(self.blend[i])
+                    self.front[i].wait_event(done)
+                r.render_split(cam, t, ml, mr, out=outs[k], stats=None if stats is None else stats[k],
+                               stream=self.front[i], blend_stream=self.blend[i], split_event=self.split_ev[i],
+                               stage_events=None if stage_events is None else stage_events[k])
+                last = self.blend[i]
+            if host_outs is not None:
+                fin = torch.cuda.Event()
+                fin.record(last)
+                self.copy.wait_event(fin)
+                with torch.cuda.stream(self.copy):
+                    host_outs[k].copy_(outs[k], non_blocking=True)
+        for s in self.streams + ([self.copy] if host_outs is not None else []):
             e = torch.cuda.Event()
             e.record(s)
             main.wait_event(e)

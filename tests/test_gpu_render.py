@@ -291,3 +291,9 @@ def test_render_pipeline_matches_sequential():
         torch.cuda.synchronize()
         for ref, o in zip(refs, outs):
             assert torch.equal(ref, o)
+        # overlapped D2H into pinned host buffers (the e2e path of bench.py)
+        host = [torch.empty_like(o, device="cpu").pin_memory() for o in outs]
+        pipe.render_many(frames, outs, host_outs=host)
+        torch.cuda.current_stream().synchronize()
+        for ref, h in zip(refs, host):
+            assert torch.equal(ref.cpu(), h)
