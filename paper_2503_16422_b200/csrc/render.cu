@@ -1251,6 +1251,165 @@ __global__ void __launch_bounds__(kWsThreads) k_blend_ws(const uint32_t *__restr
     }
 }
 
+// Warp-list blend (the timed render kernel).  Same producer / consumer
+// structure and per-pixel arithmetic as k_blend_ws, but the producer builds,
+// per batch and per consumer warp, a packed list of the records whose
+// margin-inflated ellipse reaches the warp's four rows, and evaluates the row
+// terms of the pinned e2 chain for those rows itself (dy, t1 = B' dy, t3 = C' dy,
+// t4 = fma(t3, dy, Q2): the same IEEE operations, once per (record, row)
+// instead of once per thread).  A consumer iterates its list linearly: per
+// record one 16-byte entry {u, A', ~AABB mask, q}, its row's {t1, t4} and the
+// record's colour.  Work counters (kCount) and the contribution recorder stay on
+// k_blend_ws, which visits every record.
+#ifndef FDGS_WL_BUF
+#define FDGS_WL_BUF 2
+#endif
+constexpr int kWlBuf = FDGS_WL_BUF;
+struct WlEntry {
+    float4 a;      // u, A', ~AABB mask bits, q (record of the batch)
+    float2 t[4];   // {t1, t4} of the warp's rows 4w .. 4w+3
+};
+static_assert(sizeof(WlEntry) == 48, "WlEntry layout");
+
+#ifndef FDGS_WL_MINB
+#define FDGS_WL_MINB 8
+#endif
+__global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uint32_t *__restrict__ tile_start,
+                                                         const uint32_t *__restrict__ entries,
+                                                         const float4 *__restrict__ rec0,
+                                                         const float4 *__restrict__ rec1,
+                                                         const float4 *__restrict__ rec2, const Counters *ctr,
+                                                         int tiles_x, int width, int height, float bg0, float bg1,
+                                                         float bg2, float *__restrict__ out_rgb,
+                                                         float *__restrict__ out_T) {
+    __shared__ WlEntry s_list[kWlBuf][4][32];
+    __shared__ float4 s_col[kWlBuf][32];      // r, g, b of record q
+    __shared__ uint32_t s_cnt[kWlBuf][4];     // list length per consumer warp; [.][0] bit 31 = end of tile
+    __shared__ __align__(8) uint64_t full[kWlBuf], empty[kWlBuf];
+    __shared__ uint32_t s_done;
+    constexpr uint32_t kEnd = 0x80000000u;
+    const bool ok = ctr->status == FDGS_OK;
+    const int tile = blockIdx.x, tx = tile % tiles_x, ty = tile / tiles_x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t start = __ldg(tile_start + tile), end = __ldg(tile_start + tile + 1);
+    if (tid == 0) {
+        for (int b = 0; b < kWlBuf; ++b) {
+            mb_init(&full[b], 1);
+            mb_init(&empty[b], 4);
+        }
+        s_done = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t first = ok ? start : end;
+    if (warp == 4) {  // ------------------------------------------------ producer
+        uint32_t k = 0;
+        for (uint32_t base = first;; base += 32, ++k) {
+            const int b = (int)(k % kWlBuf);
+            if (k >= kWlBuf) mb_wait(&empty[b], ((k / kWlBuf) - 1) & 1);
+            const bool stop = base >= end || *(volatile uint32_t *)&s_done == 4;
+            const uint32_t n = stop ? 0u : min(32u, end - base);
+            uint32_t rows = 0;
+            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, oa, oc, od;
+            if (lane < (int)n) {
+                const uint32_t v = __ldg(entries + base + lane);
+                r0 = __ldg(rec0 + v);
+                r1 = __ldg(rec1 + v);
+                const float4 r2 = __ldg(rec2 + v);
+                stage_fields(tx, ty, r0, r1, r2, oa, oc, od);
+                rows = __float_as_uint(od.z) >> 16;
+                s_col[b][lane] = make_float4(oc.z, oc.w, od.x, 0.f);
+            }
+            const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
+            const float mbits = od.y;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {  // per consumer warp: packed list + its rows' e2 row terms
+                const bool reach = lane < (int)n && ((rows >> (4 * w)) & 0xFu) != 0u;
+                const uint32_t bal = __ballot_sync(0xffffffffu, reach);
+                if (reach) {
+                    WlEntry &E = s_list[b][w][__popc(bal & lanemask_lt())];
+                    E.a = make_float4(u, Ap, mbits, __int_as_float(lane));
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {  // pinned e2 chain, row terms (DESIGN.md step 10)
+                        const float dy = __fsub_rn((float)(ty * 16 + 4 * w + r) + 0.5f, v);
+                        const float t1 = __fmul_rn(Bp, dy);
+                        const float t3 = __fmul_rn(Cp, dy);
+                        E.t[r] = make_float2(t1, __fmaf_rn(t3, dy, Q2));
+                    }
+                }
+                if (lane == w) s_cnt[b][w] = (uint32_t)__popc(bal) | (n == 0 ? kEnd : 0u);
+            }
+            __syncwarp();
+            if (lane == 0) mb_arrive(&full[b]);
+            if (n == 0) break;
+        }
+    } else {  // --------------------------------------------------------- consumers
+        const int ly = tid >> 3, lx = (tid & 7) * 2, rr = ly & 3;
+        const int i0 = tx * 16 + lx, j = ty * 16 + ly;
+        const bool in0 = i0 < width && j < height, in1 = i0 + 1 < width && j < height;
+        float2 px = make_float2((float)i0 + 0.5f, (float)(i0 + 1) + 0.5f);
+        const uint32_t pb0 = (1u << lx) | (1u << (16 + ly)), pb1 = (2u << lx) | (1u << (16 + ly));
+        const float kInf = __int_as_float(0x7f800000);
+        float2 thr = make_float2(in0 ? 0.0f : kInf, in1 ? 0.0f : kInf);
+        float2 T = make_float2(1.0f, 1.0f), Cr = make_float2(0.f, 0.f), Cg = Cr, Cb = Cr;
+        bool wdone = __all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf);
+        if (wdone && lane == 0) atomicAdd(&s_done, 1u);
+        for (uint32_t k = 0;; ++k) {
+            const int b = (int)(k % kWlBuf);
+            mb_wait(&full[b], (k / kWlBuf) & 1);
+            const uint32_t cw = s_cnt[b][warp];
+            if (s_cnt[b][0] & kEnd) break;
+            if (!wdone) {
+                const int cnt = (int)(cw & ~kEnd);
+                const WlEntry *E = &s_list[b][warp][0];
+                for (int q = 0; q < cnt; ++q) {
+                    const float4 a = E[q].a;
+                    const float2 tt = E[q].t[rr];
+                    const float4 col = s_col[b][__float_as_int(a.w)];
+                    asm volatile("" : "+f"(px.x), "+f"(px.y));
+                    const uint32_t m = __float_as_uint(a.z);
+                    const float2 dx = sub2(px, make_float2(a.x, a.x));
+                    const float2 t2 = fma2(make_float2(a.y, a.y), dx, make_float2(tt.x, tt.x));
+                    const float2 e2 = fma2(dx, t2, make_float2(tt.y, tt.y));
+                    const bool v0 = (m & pb0) == 0u && e2.x >= thr.x, v1 = (m & pb1) == 0u && e2.y >= thr.y;
+                    const float m0 = v0 ? fminf(ex2_approx(e2.x), kAlphaPre) : 0.0f;
+                    const float m1 = v1 ? fminf(ex2_approx(e2.y), kAlphaPre) : 0.0f;
+                    float2 w = mul2(mul2(make_float2(m0, m1), make_float2(kInv255, kInv255)), T);
+                    const float2 test = sub2(T, w);
+                    const bool s0 = v0 && test.x < 1e-4f, s1 = v1 && test.y < 1e-4f;
+                    w.x = s0 ? 0.0f : w.x;
+                    w.y = s1 ? 0.0f : w.y;
+                    thr.x = s0 ? kInf : thr.x;
+                    thr.y = s1 ? kInf : thr.y;
+                    T = sub2(T, w);
+                    Cr = fma2(make_float2(col.x, col.x), w, Cr);
+                    Cg = fma2(make_float2(col.y, col.y), w, Cg);
+                    Cb = fma2(make_float2(col.z, col.z), w, Cb);
+                }
+                wdone = __all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf);
+                if (wdone && lane == 0) atomicAdd(&s_done, 1u);
+            }
+            __syncwarp();
+            if (lane == 0) mb_arrive(&empty[b]);
+        }
+        if (ok && out_rgb != nullptr) {
+            const size_t hw = (size_t)width * height, p = (size_t)j * width + i0;
+            if (in0) {
+                out_rgb[p] = fmaf(T.x, bg0, Cr.x);
+                out_rgb[hw + p] = fmaf(T.x, bg1, Cg.x);
+                out_rgb[2 * hw + p] = fmaf(T.x, bg2, Cb.x);
+                if (out_T) out_T[p] = T.x;
+            }
+            if (in1) {
+                out_rgb[p + 1] = fmaf(T.y, bg0, Cr.y);
+                out_rgb[hw + p + 1] = fmaf(T.y, bg1, Cg.y);
+                out_rgb[2 * hw + p + 1] = fmaf(T.y, bg2, Cb.y);
+                if (out_T) out_T[p + 1] = T.y;
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- launcher
 // Persistent-grid sizes (blocks per SM); FDGS_PGRID / FDGS_RGRID override for tuning.
 static int tune_env(const char *name, int dflt) {
@@ -1354,6 +1513,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     }
     if (ev && (e = cudaEventRecord(ev[3], bst)) != cudaSuccess) return e;
     static const bool ws_blend = tune_env("FDGS_BLEND_WS", 1) == 1;  // FDGS_BLEND_WS=0: block-synchronous k_blend
+    static const bool wl_blend = tune_env("FDGS_BLEND_WL", 1) == 1;  // FDGS_BLEND_WL=0: k_blend_ws for frames too
     if (contrib != nullptr) {  // spatial-score recording (fdgs_stv_score)
         k_blend_ws<false, true><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x,
                                                                    L.width, L.height, cam.bg[0], cam.bg[1], cam.bg[2],
@@ -1363,6 +1523,9 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
             k_blend_ws<true><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x,
                                                                 L.width, L.height, cam.bg[0], cam.bg[1], cam.bg[2],
                                                                 out_rgb, out_T, stats);
+        else if (wl_blend)
+            k_blend_wl<<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
+                                                          L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
         else
             k_blend_ws<false><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x,
                                                                  L.width, L.height, cam.bg[0], cam.bg[1], cam.bg[2],
