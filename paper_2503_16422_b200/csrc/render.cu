@@ -1266,14 +1266,19 @@ __global__ void __launch_bounds__(kWsThreads) k_blend_ws(const uint32_t *__restr
 #endif
 constexpr int kWlBuf = FDGS_WL_BUF;
 struct WlEntry {
-    float4 a;      // u, A', ~AABB mask bits, q (record of the batch)
+    float4 a;      // u, A', ~AABB mask bits, r
+    float4 c;      // g, b, q (record of the batch, kContrib bookkeeping), -
     float2 t[4];   // {t1, t4} of the warp's rows 4w .. 4w+3
 };
-static_assert(sizeof(WlEntry) == 48, "WlEntry layout");
+static_assert(sizeof(WlEntry) == 64, "WlEntry layout");
 
 #ifndef FDGS_WL_MINB
-#define FDGS_WL_MINB 8
+#define FDGS_WL_MINB 7
 #endif
+#ifndef FDGS_WL_UNROLL
+#define FDGS_WL_UNROLL 4
+#endif
+constexpr int kWlUnroll = FDGS_WL_UNROLL;
 __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uint32_t *__restrict__ tile_start,
                                                          const uint32_t *__restrict__ entries,
                                                          const float4 *__restrict__ rec0,
@@ -1283,7 +1288,6 @@ __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uin
                                                          float bg2, float *__restrict__ out_rgb,
                                                          float *__restrict__ out_T) {
     __shared__ WlEntry s_list[kWlBuf][4][32];
-    __shared__ float4 s_col[kWlBuf][32];      // r, g, b of record q
     __shared__ uint32_t s_cnt[kWlBuf][4];     // list length per consumer warp; [.][0] bit 31 = end of tile
     __shared__ __align__(8) uint64_t full[kWlBuf], empty[kWlBuf];
     __shared__ uint32_t s_done;
@@ -1318,7 +1322,6 @@ __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uin
                 const float4 r2 = __ldg(rec2 + v);
                 stage_fields(tx, ty, r0, r1, r2, oa, oc, od);
                 rows = __float_as_uint(od.z) >> 16;
-                s_col[b][lane] = make_float4(oc.z, oc.w, od.x, 0.f);
             }
             const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
             const float mbits = od.y;
@@ -1328,7 +1331,8 @@ __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uin
                 const uint32_t bal = __ballot_sync(0xffffffffu, reach);
                 if (reach) {
                     WlEntry &E = s_list[b][w][__popc(bal & lanemask_lt())];
-                    E.a = make_float4(u, Ap, mbits, __int_as_float(lane));
+                    E.a = make_float4(u, Ap, mbits, oc.z);
+                    E.c = make_float4(oc.w, od.x, __int_as_float(lane), 0.f);
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {  // pinned e2 chain, row terms (DESIGN.md step 10)
                         const float dy = __fsub_rn((float)(ty * 16 + 4 * w + r) + 0.5f, v);
@@ -1362,10 +1366,14 @@ __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uin
             if (!wdone) {
                 const int cnt = (int)(cw & ~kEnd);
                 const WlEntry *E = &s_list[b][warp][0];
+                const float2 *Tp = &s_list[b][warp][0].t[rr];
+#pragma unroll kWlUnroll
                 for (int q = 0; q < cnt; ++q) {
                     const float4 a = E[q].a;
-                    const float2 tt = E[q].t[rr];
-                    const float4 col = s_col[b][__float_as_int(a.w)];
+                    const float2 gb = *reinterpret_cast<const float2 *>(&E[q].c);
+                    const float2 tt = *reinterpret_cast<const float2 *>(reinterpret_cast<const char *>(Tp) +
+                                                                         q * sizeof(WlEntry));
+                    const float4 col = make_float4(a.w, gb.x, gb.y, 0.f);
                     asm volatile("" : "+f"(px.x), "+f"(px.y));
                     const uint32_t m = __float_as_uint(a.z);
                     const float2 dx = sub2(px, make_float2(a.x, a.x));
