@@ -1448,70 +1448,76 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
 
     cudaError_t e = cudaSuccess;
     if (ev && (e = cudaEventRecord(ev[0], st)) != cudaSuccess) return e;
-    e = cudaMemsetAsync(ws + L.counters, 0, L.zero_end - L.counters, st);  // counters, look-back, histograms
-    if (e != cudaSuccess) return e;
-    if (L.n_parts > 0)
-        k_preprocess<<<L.n_parts, kPreBlock, 0, st>>>(sc, mask_l, mask_r, cam, t, ctr, lb, rec0, rec1, rec2, depth,
-                                                      rect);
-    if (ev && (e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
-    uint32_t *gbase = reinterpret_cast<uint32_t *>(ws + L.sort_gbase);  // [4][256] depth digit bases
-    uint32_t *epoch = reinterpret_cast<uint32_t *>(ws + L.epoch);
-    uint64_t *sstat = reinterpret_cast<uint64_t *>(ws + L.sort_status);
-    k_sort_hist<<<L.p_sort, kSortThreads, 0, st>>>(depth, ctr, gbase, epoch);
-    constexpr int kDItems = 4;
-    for (int pass = 0; pass < 4; ++pass) {
-        const uint32_t *kin = pass == 0 ? depth : keys[(pass - 1) & 1];
-        const uint32_t *vin = pass == 0 ? nullptr : vals[(pass - 1) & 1];
-        k_onesweep<8, kDItems><<<std::min(L.sort_parts, tune_pgrid() * L.p_sort), kSortThreads, 0, st>>>(
-            kin, vin, pass == 3 ? nullptr : keys[pass & 1], vals[pass & 1], &ctr->n_vis, epoch,
-            &ctr->sort_ticket[1 + pass], 8 * pass, gbase + 256 * pass,
-            sstat + (size_t)pass * L.sort_parts * 256, rect, pass == 3 ? rect_sorted : nullptr);
+    // FDGS_DEBUG_STAGES (experiments only): bit 0 front end, bit 1 blend; with bit 0
+    // clear the workspace's previous lists are blended again
+    static const int dbg_stages = tune_env("FDGS_DEBUG_STAGES", 3);
+    static int dbg_calls = 0;  // the first 64 frames always build lists (fills every workspace)
+    if ((dbg_stages & 1) || dbg_calls++ < 64) {
+        e = cudaMemsetAsync(ws + L.counters, 0, L.zero_end - L.counters, st);  // counters, look-back, histograms
+        if (e != cudaSuccess) return e;
+        if (L.n_parts > 0)
+            k_preprocess<<<L.n_parts, kPreBlock, 0, st>>>(sc, mask_l, mask_r, cam, t, ctr, lb, rec0, rec1, rec2, depth,
+                                                          rect);
+        if (ev && (e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
+        uint32_t *gbase = reinterpret_cast<uint32_t *>(ws + L.sort_gbase);  // [4][256] depth digit bases
+        uint32_t *epoch = reinterpret_cast<uint32_t *>(ws + L.epoch);
+        uint64_t *sstat = reinterpret_cast<uint64_t *>(ws + L.sort_status);
+        k_sort_hist<<<L.p_sort, kSortThreads, 0, st>>>(depth, ctr, gbase, epoch);
+        constexpr int kDItems = 4;
+        for (int pass = 0; pass < 4; ++pass) {
+            const uint32_t *kin = pass == 0 ? depth : keys[(pass - 1) & 1];
+            const uint32_t *vin = pass == 0 ? nullptr : vals[(pass - 1) & 1];
+            k_onesweep<8, kDItems><<<std::min(L.sort_parts, tune_pgrid() * L.p_sort), kSortThreads, 0, st>>>(
+                kin, vin, pass == 3 ? nullptr : keys[pass & 1], vals[pass & 1], &ctr->n_vis, epoch,
+                &ctr->sort_ticket[1 + pass], 8 * pass, gbase + 256 * pass,
+                sstat + (size_t)pass * L.sort_parts * 256, rect, pass == 3 ? rect_sorted : nullptr);
+        }
+        const uint32_t *order = vals[1];
+        if (ev && (e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
+        int *diff = reinterpret_cast<int *>(ws + L.tile_diff);
+        int *rowdiff = reinterpret_cast<int *>(ws + L.row_diff);
+        uint32_t *rbase = reinterpret_cast<uint32_t *>(ws + L.tile_gbase);  // [0..255] pass 0, [256..511] pass 1
+        uint32_t *row_start = reinterpret_cast<uint32_t *>(ws + L.row_start);
+        uint32_t *roff = reinterpret_cast<uint32_t *>(ws + L.roff);
+        uint32_t *rcfirst = reinterpret_cast<uint32_t *>(ws + L.rchunk_first);
+        uint32_t *ikey[2] = {reinterpret_cast<uint32_t *>(ws + L.ekey0), reinterpret_cast<uint32_t *>(ws + L.ekey1)};
+        uint32_t *ival[2] = {reinterpret_cast<uint32_t *>(ws + L.eval0), reinterpret_cast<uint32_t *>(ws + L.eval1)};
+        uint32_t *ipack = reinterpret_cast<uint32_t *>(ws + L.item_pack);
+        uint32_t *iv = reinterpret_cast<uint32_t *>(ws + L.item_v);
+        uint32_t *elb = reinterpret_cast<uint32_t *>(ws + L.emit_lb);
+        uint32_t *rhist = reinterpret_cast<uint32_t *>(ws + L.row_hist);
+        uint64_t *tstat = reinterpret_cast<uint64_t *>(ws + L.tile_status);
+        BandConsts *bconst = reinterpret_cast<BandConsts *>(ws + L.band_consts);
+        const uint32_t item_chunks = (uint32_t)((L.max_entries + kItemTile - 1) / kItemTile);
+        k_bin_scan<<<std::max(1, (L.n + kScanNT - 1) / kScanNT), kScanNT, 0, st>>>(rect_sorted, order, rec0, rec1, ctr,
+                                                                                 &ctr->bin_ticket, elb, roff, rcfirst,
+                                                                                 item_chunks, &ctr->n_items, bconst,
+                                                                                 rowdiff, L.tiles_y);
+        k_row_items<<<(int)std::min<uint32_t>(item_chunks, 8 * L.p_sort), kScanNT, 0, st>>>(
+            rect_sorted, order, rec0, rec1, bconst, roff, rcfirst, ctr, &ctr->n_items, L.tiles_x, diff, ikey[0], ipack,
+            iv, (uint32_t)L.max_entries);
+        const size_t scan_smem = sizeof(int) * (size_t)(L.tiles_x + 1) * (L.tiles_y + 1);
+        k_tile_scan<<<1, 1024, scan_smem, st>>>(diff, rowdiff, L.tiles_x, L.tiles_y, tstart, row_start, rbase, ctr,
+                                                L.max_entries);
+        // stable partition of the row items by tile row (canonical order kept within a row)
+        const int rgrid = std::min((int)item_chunks, tune_pgrid() * L.p_sort);
+        const uint32_t *sorted_items = ival[0];
+        k_onesweep<8, 4><<<rgrid, kSortThreads, 0, st>>>(ikey[0], nullptr, L.tiles_y > 256 ? ikey[1] : nullptr, ival[0],
+                                                       &ctr->n_items, epoch, &ctr->tile_ticket[0], 0, rbase, tstat,
+                                                       nullptr, nullptr);
+        if (L.tiles_y > 256) {
+            k_onesweep<8, 4><<<rgrid, kSortThreads, 0, st>>>(ikey[1], ival[0], nullptr, ival[1], &ctr->n_items, epoch,
+                                                           &ctr->tile_ticket[1], 8, rbase + 256,
+                                                           tstat + (size_t)L.tile_parts * 256, nullptr, nullptr);
+            sorted_items = ival[1];
+        }
+        const int nrb = L.tiles_y * kRowSeg;
+        const size_t cnt_smem = sizeof(uint32_t) * (size_t)kRowWarps * L.tiles_x;
+        k_row_count<<<nrb, 256, sizeof(int) * (L.tiles_x + 1), st>>>(sorted_items, ipack, row_start, L.tiles_x, rhist,
+                                                                      ctr);
+        k_row_scatter<<<nrb, 32 * kRowWarps, cnt_smem + sizeof(uint32_t) * L.tiles_x, st>>>(
+            sorted_items, ipack, iv, row_start, L.tiles_x, rhist, tstart, entries, ctr);
     }
-    const uint32_t *order = vals[1];
-    if (ev && (e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
-    int *diff = reinterpret_cast<int *>(ws + L.tile_diff);
-    int *rowdiff = reinterpret_cast<int *>(ws + L.row_diff);
-    uint32_t *rbase = reinterpret_cast<uint32_t *>(ws + L.tile_gbase);  // [0..255] pass 0, [256..511] pass 1
-    uint32_t *row_start = reinterpret_cast<uint32_t *>(ws + L.row_start);
-    uint32_t *roff = reinterpret_cast<uint32_t *>(ws + L.roff);
-    uint32_t *rcfirst = reinterpret_cast<uint32_t *>(ws + L.rchunk_first);
-    uint32_t *ikey[2] = {reinterpret_cast<uint32_t *>(ws + L.ekey0), reinterpret_cast<uint32_t *>(ws + L.ekey1)};
-    uint32_t *ival[2] = {reinterpret_cast<uint32_t *>(ws + L.eval0), reinterpret_cast<uint32_t *>(ws + L.eval1)};
-    uint32_t *ipack = reinterpret_cast<uint32_t *>(ws + L.item_pack);
-    uint32_t *iv = reinterpret_cast<uint32_t *>(ws + L.item_v);
-    uint32_t *elb = reinterpret_cast<uint32_t *>(ws + L.emit_lb);
-    uint32_t *rhist = reinterpret_cast<uint32_t *>(ws + L.row_hist);
-    uint64_t *tstat = reinterpret_cast<uint64_t *>(ws + L.tile_status);
-    BandConsts *bconst = reinterpret_cast<BandConsts *>(ws + L.band_consts);
-    const uint32_t item_chunks = (uint32_t)((L.max_entries + kItemTile - 1) / kItemTile);
-    k_bin_scan<<<std::max(1, (L.n + kScanNT - 1) / kScanNT), kScanNT, 0, st>>>(rect_sorted, order, rec0, rec1, ctr,
-                                                                             &ctr->bin_ticket, elb, roff, rcfirst,
-                                                                             item_chunks, &ctr->n_items, bconst,
-                                                                             rowdiff, L.tiles_y);
-    k_row_items<<<(int)std::min<uint32_t>(item_chunks, 8 * L.p_sort), kScanNT, 0, st>>>(
-        rect_sorted, order, rec0, rec1, bconst, roff, rcfirst, ctr, &ctr->n_items, L.tiles_x, diff, ikey[0], ipack,
-        iv, (uint32_t)L.max_entries);
-    const size_t scan_smem = sizeof(int) * (size_t)(L.tiles_x + 1) * (L.tiles_y + 1);
-    k_tile_scan<<<1, 1024, scan_smem, st>>>(diff, rowdiff, L.tiles_x, L.tiles_y, tstart, row_start, rbase, ctr,
-                                            L.max_entries);
-    // stable partition of the row items by tile row (canonical order kept within a row)
-    const int rgrid = std::min((int)item_chunks, tune_pgrid() * L.p_sort);
-    const uint32_t *sorted_items = ival[0];
-    k_onesweep<8, 4><<<rgrid, kSortThreads, 0, st>>>(ikey[0], nullptr, L.tiles_y > 256 ? ikey[1] : nullptr, ival[0],
-                                                   &ctr->n_items, epoch, &ctr->tile_ticket[0], 0, rbase, tstat,
-                                                   nullptr, nullptr);
-    if (L.tiles_y > 256) {
-        k_onesweep<8, 4><<<rgrid, kSortThreads, 0, st>>>(ikey[1], ival[0], nullptr, ival[1], &ctr->n_items, epoch,
-                                                       &ctr->tile_ticket[1], 8, rbase + 256,
-                                                       tstat + (size_t)L.tile_parts * 256, nullptr, nullptr);
-        sorted_items = ival[1];
-    }
-    const int nrb = L.tiles_y * kRowSeg;
-    const size_t cnt_smem = sizeof(uint32_t) * (size_t)kRowWarps * L.tiles_x;
-    k_row_count<<<nrb, 256, sizeof(int) * (L.tiles_x + 1), st>>>(sorted_items, ipack, row_start, L.tiles_x, rhist,
-                                                                  ctr);
-    k_row_scatter<<<nrb, 32 * kRowWarps, cnt_smem + sizeof(uint32_t) * L.tiles_x, st>>>(
-        sorted_items, ipack, iv, row_start, L.tiles_x, rhist, tstart, entries, ctr);
     // the blend may run on its own (lower-priority) stream, ordered after the front end
     cudaStream_t bst = st;
     if (blend_st != nullptr) {
@@ -1522,7 +1528,8 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     if (ev && (e = cudaEventRecord(ev[3], bst)) != cudaSuccess) return e;
     static const bool ws_blend = tune_env("FDGS_BLEND_WS", 1) == 1;  // FDGS_BLEND_WS=0: block-synchronous k_blend
     static const bool wl_blend = tune_env("FDGS_BLEND_WL", 1) == 1;  // FDGS_BLEND_WL=0: k_blend_ws for frames too
-    if (contrib != nullptr) {  // spatial-score recording (fdgs_stv_score)
+    if (!(dbg_stages & 2)) {
+    } else if (contrib != nullptr) {  // spatial-score recording (fdgs_stv_score)
         k_blend_ws<false, true><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x,
                                                                    L.width, L.height, cam.bg[0], cam.bg[1], cam.bg[2],
                                                                    out_rgb, out_T, nullptr, contrib, stv_info);
