@@ -56,6 +56,13 @@ typedef enum {
  *   log255_opacity            : float[n], L_i = fp32(ln(255 sigma_i)) computed
  *                               in binary64 (fdgs_log255_opacity fills it)
  *   sh                        : float[n][16][3], coefficient k*3+channel
+ *   param_stride              : float4 elements between consecutive Gaussians
+ *                               in mean/scale/rot_l/rot_r: 0 or 1 = four SoA
+ *                               planes; 4 = one interleaved 64-byte record per
+ *                               Gaussian {mean, scale, rot_l, rot_r} (what the
+ *                               Python Scene allocates: a sparse, mask-driven
+ *                               gather then touches one 64-byte DRAM burst per
+ *                               Gaussian instead of four)
  *   sh_index, sh_codebook_size: vector-quantised SH (the "Ours-PP" storage of
  *                               P:483, SH "vector quantization" after CompGS):
  *                               when sh_index != NULL, `sh` points to a
@@ -75,6 +82,7 @@ typedef struct {
     const float *sh;
     const uint16_t *sh_index;     /* nullable: dense SH                        */
     int32_t sh_codebook_size;     /* entries of the codebook when sh_index set */
+    int32_t param_stride;         /* 0/1 SoA planes, 4 interleaved (see above) */
 } fdgs_scene;
 
 /* Pinhole view "I" of P:126 (HOST struct).  world->camera rotation R

@@ -31,7 +31,8 @@ EXPORTS = [
 class FdgsScene(C.Structure):
     _fields_ = [("n", C.c_int32), ("mean", C.c_void_p), ("scale", C.c_void_p), ("rot_l", C.c_void_p),
                 ("rot_r", C.c_void_p), ("opacity", C.c_void_p), ("log255_opacity", C.c_void_p),
-                ("sh", C.c_void_p), ("sh_index", C.c_void_p), ("sh_codebook_size", C.c_int32)]
+                ("sh", C.c_void_p), ("sh_index", C.c_void_p), ("sh_codebook_size", C.c_int32),
+                ("param_stride", C.c_int32)]
 
 
 class FdgsCamera(C.Structure):

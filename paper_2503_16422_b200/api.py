@@ -35,9 +35,12 @@ def _ptr(t):
 class Scene:
     """Device-resident 4D Gaussians (fdgs_scene)."""
 
-    def __init__(self, tensors: dict, device=None):
+    def __init__(self, tensors: dict, device=None, interleaved: bool = True):
         """tensors: the _FIELDS arrays; optional "sh_index" (N,) uint16 makes
-        "sh" a VQ codebook (K,16,3) (Ours-PP storage)."""
+        "sh" a VQ codebook (K,16,3) (Ours-PP storage).  interleaved:
+        mean/scale/rot_l/rot_r live in one (N, 4, 4) buffer, a 64-byte record per
+        Gaussian (fdgs_scene.param_stride = 4), so the mask-driven sparse gather
+        of the cull and slice kernels reads one DRAM burst per Gaussian."""
         dev = torch.device(device or "cuda")
         self.t = {}
         for f in _FIELDS:
@@ -47,6 +50,12 @@ class Scene:
             self.t[f] = x.to(device=dev, dtype=torch.float32).contiguous()
         self.n = int(self.t["mean"].shape[0])
         self.device = dev
+        self.stride = 0
+        if interleaved:
+            self.params = torch.stack([self.t[f] for f in ("mean", "scale", "rot_l", "rot_r")], 1).contiguous()
+            for k, f in enumerate(("mean", "scale", "rot_l", "rot_r")):
+                self.t[f] = self.params[:, k]  # (N, 4) views with a 64-byte row stride
+            self.stride = 4
         idx = tensors.get("sh_index")
         k = 0
         if idx is not None:
@@ -55,7 +64,7 @@ class Scene:
             self.t["sh_index"] = idx.to(device=dev, dtype=torch.uint16).contiguous()
             k = int(self.t["sh"].shape[0])
         self.struct = FdgsScene(self.n, *[self.t[f].data_ptr() for f in _FIELDS],
-                                self.t["sh_index"].data_ptr() if idx is not None else None, k)
+                                self.t["sh_index"].data_ptr() if idx is not None else None, k, self.stride)
 
     @classmethod
     def from_arrays(cls, arrays, device=None):

@@ -49,7 +49,9 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.tiles_x = (width + FDGS_TILE - 1) / FDGS_TILE;
     L.tiles_y = (height + FDGS_TILE - 1) / FDGS_TILE;
     L.n_tiles = L.tiles_x * L.tiles_y;
-    L.n_parts = (n + 2 * kPreBlock - 1) / (2 * kPreBlock);  // preprocess partitions (kPreItems)
+    L.n_parts = (n + 2 * kPreBlock - 1) / (2 * kPreBlock);  // k_slice partitions (2 survivors per thread)
+    L.cull_parts = (n + 4 * kPreBlock - 1) / (4 * kPreBlock);  // k_cull partitions (4 Gaussians per thread)
+    L.slice_grid = std::max(1, std::min(L.n_parts, 2 * sm_count()));  // 2 resident blocks per SM
     L.p_sort = sm_count();
     L.sort_parts = std::max(1, (n + kDepthTile - 1) / kDepthTile);
     L.tile_parts = (int32_t)std::max<int64_t>(1, (max_entries + kTileTile - 1) / kTileTile);
@@ -65,6 +67,7 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     // cleared per frame
     L.counters = take(sizeof(Counters));
     L.lookback = take(sizeof(uint32_t) * (size_t)std::max(L.n_parts, 1));
+    L.lookback_cull = take(sizeof(uint32_t) * (size_t)std::max(L.cull_parts, 1));
     L.sort_gbase = take(sizeof(uint32_t) * 4 * 256);
     L.tile_diff = take(sizeof(int) * (size_t)(L.tiles_x + 1) * (L.tiles_y + 1));
     L.row_diff = take(sizeof(int) * ((size_t)L.tiles_y + 1));
@@ -75,6 +78,7 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.sort_status = take(sizeof(uint64_t) * 4 * 256 * (size_t)L.sort_parts);
     L.tile_status = take(sizeof(uint64_t) * 2 * 256 * (size_t)L.tile_parts);
     // per-frame scratch, fully written before read
+    L.surv = take(4 * nn);
     L.rec0 = take(16 * nn);
     L.rec1 = take(16 * nn);
     L.rec2 = take(16 * nn);
@@ -145,6 +149,7 @@ bool make_camdev(const fdgs_camera &c, CamDev &o, const char **why) {
 SceneDev make_scenedev(const fdgs_scene &s) {
     SceneDev d;
     d.n = s.n;
+    d.stride = s.param_stride > 0 ? s.param_stride : 1;
     d.mean = reinterpret_cast<const float4 *>(s.mean);
     d.scale = reinterpret_cast<const float4 *>(s.scale);
     d.rot_l = reinterpret_cast<const float4 *>(s.rot_l);
@@ -167,6 +172,7 @@ static fdgs_status check_scene(const fdgs_scene *s) {
     const void *a16[] = {s->mean, s->scale, s->rot_l, s->rot_r, s->sh};
     for (const void *q : a16)
         if ((uintptr_t)q % 16 != 0) return fail(FDGS_ERR_INVALID_ARG, "scene float4 arrays must be 16-byte aligned");
+    if (s->param_stride < 0 || s->param_stride > 64) return fail(FDGS_ERR_INVALID_ARG, "param_stride must lie in [0, 64]");
     if (s->sh_index != nullptr && (s->sh_codebook_size < 1 || s->sh_codebook_size > 65536))
         return fail(FDGS_ERR_INVALID_ARG, "sh_codebook_size must lie in [1, 65536] with sh_index");
     return FDGS_OK;

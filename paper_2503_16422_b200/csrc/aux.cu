@@ -17,8 +17,8 @@ __global__ void __launch_bounds__(256) k_keyframe(SceneDev sc, const CamDev *__r
     bool vis = false;
     if (i < sc.n) {
         Slice sl;
-        const int st = slice_gaussian(__ldg(sc.mean + i), __ldg(sc.scale + i), __ldg(sc.rot_l + i),
-                                      __ldg(sc.rot_r + i), __ldg(sc.L + i), t, sl);
+        const int st = slice_gaussian(sc.ld_mean(i), sc.ld_scale(i), sc.ld_rot_l(i),
+                                      sc.ld_rot_r(i), __ldg(sc.L + i), t, sl);
         if (st == kNear) {
             for (int c = 0; c < n_cams && !vis; ++c) {
                 Proj pj;
@@ -140,7 +140,7 @@ cudaError_t launch_mask_compact(const uint32_t *a, const uint32_t *b, int n, int
 __global__ void k_validate(SceneDev sc, unsigned long long *first_bad) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= sc.n) return;
-    const float4 ql = sc.rot_l[i], qr = sc.rot_r[i], s = sc.scale[i];
+    const float4 ql = sc.ld_rot_l(i), qr = sc.ld_rot_r(i), s = sc.ld_scale(i);
     const float op = sc.opacity[i];
     const double nl = sqrt((double)ql.x * ql.x + (double)ql.y * ql.y + (double)ql.z * ql.z + (double)ql.w * ql.w);
     const double nr = sqrt((double)qr.x * qr.x + (double)qr.y * qr.y + (double)qr.z * qr.z + (double)qr.w * qr.w);

@@ -33,13 +33,20 @@ struct Counters {
     unsigned long long n_blend;  // pairs composited
     uint32_t row_ticket;         // row-item scan partitions
     uint32_t n_items;            // (Gaussian, tile row) items
-    uint32_t pad2[10];
+    uint32_t n_surv;             // Gaussians passing the mask and the temporal cull (k_cull)
+    uint32_t cull_ticket;        // k_cull partitions
+    uint32_t pad2[8];
 };
 static_assert(sizeof(Counters) == 128, "Counters layout");
 
 struct SceneDev {
     int32_t n;
+    int32_t stride;  // float4 elements between consecutive Gaussians of mean/scale/rot_l/rot_r
     const float4 *mean, *scale, *rot_l, *rot_r;
+    __device__ __forceinline__ float4 ld_mean(int i) const { return __ldg(mean + (size_t)i * stride); }
+    __device__ __forceinline__ float4 ld_scale(int i) const { return __ldg(scale + (size_t)i * stride); }
+    __device__ __forceinline__ float4 ld_rot_l(int i) const { return __ldg(rot_l + (size_t)i * stride); }
+    __device__ __forceinline__ float4 ld_rot_r(int i) const { return __ldg(rot_r + (size_t)i * stride); }
     const float *opacity, *L;
     const float4 *sh;  // [n][12] float4 = 48 floats, or the VQ codebook [K][12]
     const uint16_t *sh_index;  // VQ: codebook entry per Gaussian (nullable)
@@ -52,14 +59,16 @@ struct SceneDev {
 // once before first use).
 struct RenderLayout {
     int32_t n, width, height, tiles_x, tiles_y, n_tiles;
-    int32_t n_parts;     // preprocess partitions
+    int32_t n_parts;     // k_slice partitions (upper bound: every Gaussian survives)
+    int32_t cull_parts;  // k_cull partitions
+    int32_t slice_grid;  // persistent k_slice grid
     int32_t p_sort;      // SM count (grid of the histogram kernels)
     int32_t sort_parts;  // depth-sort partitions (upper bound from n)
     int32_t tile_parts;  // row-partition partitions (upper bound from max_entries)
     int64_t max_entries;
-    size_t counters, lookback, sort_gbase, tile_diff, row_diff, emit_lb, zero_end;
+    size_t counters, lookback, lookback_cull, sort_gbase, tile_diff, row_diff, emit_lb, zero_end;
     size_t epoch, sort_status, tile_status;
-    size_t rec0, rec1, rec2, depth, rect, rect_sorted, keys0, keys1, vals0, vals1;
+    size_t surv, rec0, rec1, rec2, depth, rect, rect_sorted, keys0, keys1, vals0, vals1;
     size_t tile_gbase, tile_start, row_start, row_hist, band_consts, roff, rchunk_first, item_pack, item_v, ekey0, ekey1, eval0, eval1, entries, total;
 };
 RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max_entries);

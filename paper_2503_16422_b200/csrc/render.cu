@@ -57,40 +57,73 @@ __device__ __forceinline__ uint32_t lookback_warp(uint32_t *status, uint32_t par
 }
 
 // ---------------------------------------------------------------- rows 1-4
-// A partition is kPreItems = 2 x 256 Gaussians.  Phase A culls all of them
-// cheaply (mask bit, then the temporal cull); the survivors are compacted in
-// shared memory (ascending index) so phase B runs the binary64 slice and
-// projection on dense survivors only, instead of diverging warps.
-constexpr int kPreItems = 2 * kPreBlock;
-struct PreRes {
-    float u, v, Ap, Bp, Cp, Q2, mx, my, mz;
-    uint32_t ax, ay, depth;
-    int i;
-};
+// Two uniform-work passes instead of one fused kernel whose blocks waited on
+// their few survivor warps (ncu at C4: 59% of cycles stalled at the barriers):
+//   k_cull   rows 1-2 + the temporal cull of row 3: one thread per Gaussian,
+//            mask bit (OR of the two key-frame rows) then the pinned binary64
+//            temporal test; survivors compacted in ascending index order
+//            (warp ballot, block scan, decoupled look-back) -> surv[];
+//   k_slice  rows 3-4 on the dense survivor list: Eq. 1 slice, support and
+//            near culls, EWA projection, cover cull, SH colour; visible ones
+//            compacted again in order -> the splat records.
+constexpr int kCullItems = 4 * kPreBlock;   // Gaussians per k_cull partition
+constexpr int kSliceItems = 2 * kPreBlock;  // survivors per k_slice partition
 
-__global__ void __launch_bounds__(kPreBlock) k_preprocess(SceneDev sc, const uint32_t *__restrict__ mask_l,
-                                                          const uint32_t *__restrict__ mask_r, CamDev cam, float t,
-                                                          Counters *ctr, uint32_t *lb, float4 *__restrict__ rec0,
-                                                          float4 *__restrict__ rec1, float4 *__restrict__ rec2,
-                                                          uint32_t *__restrict__ depth, uint2 *__restrict__ rect) {
+// Block-wide exclusive offsets of per-(round, warp) counts plus the partition's
+// global offset by look-back.  cnt[r][w] in, offsets out; returns the block's
+// global exclusive base.  All threads call it.
+template <int R>
+__device__ __forceinline__ uint32_t block_offsets(uint32_t (&cnt)[R][kPreBlock / 32], uint32_t *lb, uint32_t part,
+                                                  uint32_t *s_excl, uint32_t *s_tot) {
     constexpr int NW = kPreBlock / 32;
-    __shared__ uint32_t s_part, s_excl, s_nsurv;
-    __shared__ uint32_t s_cnt[2][NW], s_act;
-    __shared__ uint16_t s_idx[kPreItems];
+    const int tid = threadIdx.x, lane = tid & 31;
+    __syncthreads();
+    if (tid < 32) {  // (round, warp) order = ascending item index
+        uint32_t run = 0;
+        uint32_t mine[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            mine[r] = 0;
+            for (int w = 0; w < NW; ++w) {
+                const uint32_t c = cnt[r][w];
+                if (w == lane) mine[r] = run;
+                run += c;
+            }
+        }
+        __syncwarp();
+        if (lane < NW) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) cnt[r][lane] = mine[r];
+        }
+        const uint32_t excl = lookback_warp(lb, part, run, lane);
+        if (lane == 0) {
+            *s_excl = excl;
+            *s_tot = run;
+        }
+    }
+    __syncthreads();
+    return *s_excl;
+}
+
+__global__ void __launch_bounds__(kPreBlock) k_cull(SceneDev sc, const uint32_t *__restrict__ mask_l,
+                                                    const uint32_t *__restrict__ mask_r, float t, Counters *ctr,
+                                                    uint32_t *lb, uint32_t *__restrict__ surv) {
+    constexpr int NW = kPreBlock / 32, R = kCullItems / kPreBlock;
+    __shared__ uint32_t s_cnt[R][NW];
+    __shared__ uint32_t s_part, s_excl, s_tot, s_act;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
-        s_part = atomicAdd(&ctr->part_ticket, 1u);
+        s_part = atomicAdd(&ctr->cull_ticket, 1u);
         s_act = 0;
     }
     __syncthreads();
     const uint32_t part = s_part;
-    // ---- phase A: mask + temporal cull, survivors compacted in index order
-    uint32_t bal[2];
+    uint32_t bal[R];
     uint32_t nact = 0;
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        const int i = (int)part * kPreItems + q * kPreBlock + tid;
-        bool act = false, surv = false;
+    for (int r = 0; r < R; ++r) {
+        const int i = (int)part * kCullItems + r * kPreBlock + tid;
+        bool act = false, keep = false;
         if (i < sc.n) {
             uint32_t w = 0xffffffffu;
             if (mask_l != nullptr) {
@@ -98,106 +131,98 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess(SceneDev sc, const uin
                 if (mask_r != nullptr) w |= __ldg(mask_r + (i >> 5));
             }
             act = (w >> (i & 31)) & 1u;
-            if (act) surv = temporal_pass(__ldg(sc.mean + i), __ldg(sc.scale + i), __ldg(sc.rot_l + i),
-                                          __ldg(sc.rot_r + i), t);
+            if (act) keep = temporal_pass(sc.ld_mean(i), sc.ld_scale(i), sc.ld_rot_l(i),
+                                          sc.ld_rot_r(i), t);
         }
         nact += __popc(__ballot_sync(0xffffffffu, act));
-        bal[q] = __ballot_sync(0xffffffffu, surv);
-        if (lane == 0) s_cnt[q][warp] = __popc(bal[q]);
+        bal[r] = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) s_cnt[r][warp] = __popc(bal[r]);
     }
     if (lane == 0 && nact) atomicAdd(&s_act, nact);
-    __syncthreads();
+    const uint32_t excl = block_offsets<R>(s_cnt, lb, part, &s_excl, &s_tot);
     if (tid == 0) {
-        uint32_t run = 0;
-        for (int q = 0; q < 2; ++q)
-            for (int w = 0; w < NW; ++w) {
-                const uint32_t c = s_cnt[q][w];
-                s_cnt[q][w] = run;
-                run += c;
-            }
-        s_nsurv = run;
         if (s_act) atomicAdd(&ctr->n_act, s_act);
+        if (part == gridDim.x - 1) ctr->n_surv = excl + s_tot;
     }
-    __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
-        if ((bal[q] >> lane) & 1u)
-            s_idx[s_cnt[q][warp] + __popc(bal[q] & lanemask_lt())] = (uint16_t)(q * kPreBlock + tid);
-    __syncthreads();
-    // ---- phase B: slice + projection on the dense survivors
-    const uint32_t ns = s_nsurv;
-    PreRes res[2];
-    uint32_t vb[2];
+    for (int r = 0; r < R; ++r)
+        if ((bal[r] >> lane) & 1u)
+            surv[excl + s_cnt[r][warp] + __popc(bal[r] & lanemask_lt())] =
+                (uint32_t)((int)part * kCullItems + r * kPreBlock + tid);
+}
+
+struct PreRes {
+    float u, v, Ap, Bp, Cp, Q2, mx, my, mz;
+    uint32_t ax, ay, depth;
+    int i;
+};
+
+// Persistent grid; partitions of kSliceItems survivors in ticket order.
+__global__ void __launch_bounds__(kPreBlock) k_slice(SceneDev sc, CamDev cam, float t, Counters *ctr, uint32_t *lb,
+                                                     const uint32_t *__restrict__ surv, float4 *__restrict__ rec0,
+                                                     float4 *__restrict__ rec1, float4 *__restrict__ rec2,
+                                                     uint32_t *__restrict__ depth, uint2 *__restrict__ rect) {
+    constexpr int NW = kPreBlock / 32, R = kSliceItems / kPreBlock;
+    __shared__ uint32_t s_cnt[R][NW];
+    __shared__ uint32_t s_part, s_excl, s_tot;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t ns = ctr->n_surv;
+    while (true) {
+        if (tid == 0) s_part = atomicAdd(&ctr->part_ticket, 1u);
+        __syncthreads();
+        const uint32_t part = s_part;
+        if ((uint64_t)part * kSliceItems >= ns) return;
+        PreRes res[R];
+        uint32_t vb[R];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        const uint32_t sidx = r * kPreBlock + tid;
-        bool vis = false;
-        if (sidx < ns) {
-            const int i = (int)part * kPreItems + s_idx[sidx];
-            Slice sl;
-            Proj pj;
-            int st = slice_gaussian(__ldg(sc.mean + i), __ldg(sc.scale + i), __ldg(sc.rot_l + i), __ldg(sc.rot_r + i),
-                                    __ldg(sc.L + i), t, sl);
-            if (st == kNear) st = project_gaussian(sl, cam, pj);
-            vis = st == kVisible;
-            if (vis) {
-                res[r].u = pj.u;
-                res[r].v = pj.v;
-                res[r].Ap = pj.Ap;
-                res[r].Bp = pj.Bp;
-                res[r].Cp = pj.Cp;
-                res[r].Q2 = pj.Q2;
-                res[r].mx = (float)sl.mu3[0];
-                res[r].my = (float)sl.mu3[1];
-                res[r].mz = (float)sl.mu3[2];
-                res[r].ax = pj.px0 | (pj.px1 << 16);
-                res[r].ay = pj.py0 | (pj.py1 << 16);
-                res[r].depth = pj.depth_bits;
-                res[r].i = i;
+        for (int r = 0; r < R; ++r) {
+            const uint32_t sidx = part * kSliceItems + r * kPreBlock + tid;
+            bool vis = false;
+            if (sidx < ns) {
+                const int i = (int)__ldg(surv + sidx);
+                Slice sl;
+                Proj pj;
+                int st = slice_gaussian(sc.ld_mean(i), sc.ld_scale(i), sc.ld_rot_l(i),
+                                        sc.ld_rot_r(i), __ldg(sc.L + i), t, sl);
+                if (st == kNear) st = project_gaussian(sl, cam, pj);
+                vis = st == kVisible;
+                if (vis) {
+                    res[r].u = pj.u;
+                    res[r].v = pj.v;
+                    res[r].Ap = pj.Ap;
+                    res[r].Bp = pj.Bp;
+                    res[r].Cp = pj.Cp;
+                    res[r].Q2 = pj.Q2;
+                    res[r].mx = (float)sl.mu3[0];
+                    res[r].my = (float)sl.mu3[1];
+                    res[r].mz = (float)sl.mu3[2];
+                    res[r].ax = pj.px0 | (pj.px1 << 16);
+                    res[r].ay = pj.py0 | (pj.py1 << 16);
+                    res[r].depth = pj.depth_bits;
+                    res[r].i = i;
+                }
             }
+            vb[r] = __ballot_sync(0xffffffffu, vis);
+            if (lane == 0) s_cnt[r][warp] = __popc(vb[r]);
         }
-        vb[r] = __ballot_sync(0xffffffffu, vis);
-    }
-    __syncthreads();  // s_cnt reuse
-    if (lane == 0) {
-        s_cnt[0][warp] = __popc(vb[0]);
-        s_cnt[1][warp] = __popc(vb[1]);
-    }
-    __syncthreads();
-    if (warp == 0) {  // survivor order = (round, warp, lane) = ascending Gaussian index
-        uint32_t run = 0, mine0 = 0, mine1 = 0;
-        for (int q = 0; q < 2; ++q)
-            for (int w = 0; w < NW; ++w) {
-                const uint32_t c = s_cnt[q][w];
-                if (w == lane) (q == 0 ? mine0 : mine1) = run;
-                run += c;
-            }
-        __syncwarp();
-        if (lane < NW) {
-            s_cnt[0][lane] = mine0;
-            s_cnt[1][lane] = mine1;
-        }
-        const uint32_t excl = lookback_warp(lb, part, run, lane);
-        if (lane == 0) {
-            s_excl = excl;
-            if (part == gridDim.x - 1) ctr->n_vis = excl + run;
-        }
-    }
-    __syncthreads();
+        const uint32_t excl = block_offsets<R>(s_cnt, lb, part, &s_excl, &s_tot);
+        if (tid == 0 && (uint64_t)(part + 1) * kSliceItems >= ns) ctr->n_vis = excl + s_tot;  // last partition
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        if (!((vb[r] >> lane) & 1u)) continue;
-        const PreRes &R = res[r];
-        const uint32_t pos = s_excl + s_cnt[r][warp] + __popc(vb[r] & lanemask_lt());
-        float rgb[3];
-        // dense SH, or the VQ codebook entry of the Gaussian (Ours-PP decode)
-        const size_t row = sc.sh_index ? (size_t)__ldg(sc.sh_index + R.i) : (size_t)R.i;
-        sh_color(sc.sh + row * 12, R.mx - cam.campos[0], R.my - cam.campos[1], R.mz - cam.campos[2], rgb);
-        rec0[pos] = make_float4(R.u, R.v, R.Ap, R.Bp);
-        rec1[pos] = make_float4(R.Cp, R.Q2, __uint_as_float(R.ax), __uint_as_float(R.ay));
-        rec2[pos] = make_float4(rgb[0], rgb[1], rgb[2], __int_as_float(R.i));
-        depth[pos] = R.depth;
-        rect[pos] = make_uint2(R.ax, R.ay);
+        for (int r = 0; r < R; ++r) {
+            if (!((vb[r] >> lane) & 1u)) continue;
+            const PreRes &Rr = res[r];
+            const uint32_t pos = excl + s_cnt[r][warp] + __popc(vb[r] & lanemask_lt());
+            float rgb[3];
+            // dense SH, or the VQ codebook entry of the Gaussian (Ours-PP decode)
+            const size_t row = sc.sh_index ? (size_t)__ldg(sc.sh_index + Rr.i) : (size_t)Rr.i;
+            sh_color(sc.sh + row * 12, Rr.mx - cam.campos[0], Rr.my - cam.campos[1], Rr.mz - cam.campos[2], rgb);
+            rec0[pos] = make_float4(Rr.u, Rr.v, Rr.Ap, Rr.Bp);
+            rec1[pos] = make_float4(Rr.Cp, Rr.Q2, __uint_as_float(Rr.ax), __uint_as_float(Rr.ay));
+            rec2[pos] = make_float4(rgb[0], rgb[1], rgb[2], __int_as_float(Rr.i));
+            depth[pos] = Rr.depth;
+            rect[pos] = make_uint2(Rr.ax, Rr.ay);
+        }
+        __syncthreads();  // s_cnt / s_part reuse by the next partition
     }
 }
 
@@ -1445,6 +1470,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     uint32_t *vals[2] = {reinterpret_cast<uint32_t *>(ws + L.vals0), reinterpret_cast<uint32_t *>(ws + L.vals1)};
     uint32_t *tstart = reinterpret_cast<uint32_t *>(ws + L.tile_start);
     uint32_t *entries = reinterpret_cast<uint32_t *>(ws + L.entries);
+    uint32_t *surv = reinterpret_cast<uint32_t *>(ws + L.surv);
 
     cudaError_t e = cudaSuccess;
     if (ev && (e = cudaEventRecord(ev[0], st)) != cudaSuccess) return e;
@@ -1455,9 +1481,11 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     if ((dbg_stages & 1) || dbg_calls++ < 64) {
         e = cudaMemsetAsync(ws + L.counters, 0, L.zero_end - L.counters, st);  // counters, look-back, histograms
         if (e != cudaSuccess) return e;
-        if (L.n_parts > 0)
-            k_preprocess<<<L.n_parts, kPreBlock, 0, st>>>(sc, mask_l, mask_r, cam, t, ctr, lb, rec0, rec1, rec2, depth,
-                                                          rect);
+        if (L.n > 0) {
+            k_cull<<<L.cull_parts, kPreBlock, 0, st>>>(sc, mask_l, mask_r, t, ctr,
+                                                        reinterpret_cast<uint32_t *>(ws + L.lookback_cull), surv);
+            k_slice<<<L.slice_grid, kPreBlock, 0, st>>>(sc, cam, t, ctr, lb, surv, rec0, rec1, rec2, depth, rect);
+        }
         if (ev && (e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
         uint32_t *gbase = reinterpret_cast<uint32_t *>(ws + L.sort_gbase);  // [4][256] depth digit bases
         uint32_t *epoch = reinterpret_cast<uint32_t *>(ws + L.epoch);

@@ -45,14 +45,15 @@ __global__ void k_stv_init(StvState *st, uint32_t rank) {
 
 // Histogram of digit (bits >> shift) & 255 over the volumes whose higher digits
 // equal the selected prefix.
-__global__ void __launch_bounds__(256) k_vol_hist(const float4 *__restrict__ scale, int n, StvState *st, int shift) {
+__global__ void __launch_bounds__(256) k_vol_hist(SceneDev sc, StvState *st, int shift) {
+    const int n = sc.n;
     __shared__ uint32_t h[256];
     h[threadIdx.x] = 0;
     __syncthreads();
     const uint32_t hi = shift >= 24 ? 0u : ~0u << (shift + 8);
     const uint32_t prefix = st->prefix;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t bits = __float_as_uint(volume4(__ldg(scale + i)));
+        const uint32_t bits = __float_as_uint(volume4(sc.ld_scale(i)));
         if (((bits ^ prefix) & hi) == 0) atomicAdd(&h[(bits >> shift) & 255u], 1u);
     }
     __syncthreads();
@@ -96,8 +97,8 @@ __global__ void __launch_bounds__(256) k_stv_accum(SceneDev sc, float t, unsigne
     if (i >= sc.n) return;
     const double ss = (double)contrib[i] * 0x1p-24;
     contrib[i] = 0ull;
-    const float4 mean = __ldg(sc.mean + i), s = __ldg(sc.scale + i);
-    const double sig = sigma44(s, __ldg(sc.rot_l + i), __ldg(sc.rot_r + i));
+    const float4 mean = sc.ld_mean(i), s = sc.ld_scale(i);
+    const double sig = sigma44(s, sc.ld_rot_l(i), sc.ld_rot_r(i));
     const double dt = (double)t - (double)mean.w;
     const double p = exp(-(dt * dt) / (2.0 * sig));
     double Tt, St = ss;
@@ -179,7 +180,7 @@ cudaError_t launch_stv(const SceneDev &sc, const CamDev *cams, const fdgs_camera
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int hgrid = std::max(1, std::min((n + 255) / 256, 4 * sms));
     for (int shift = 24; shift >= 0; shift -= 8) {
-        k_vol_hist<<<hgrid, 256, 0, st>>>(sc.scale, n, state, shift);
+        k_vol_hist<<<hgrid, 256, 0, st>>>(sc, state, shift);
         k_vol_pick<<<1, 256, 0, st>>>(state, shift);
     }
     if ((e = cudaMemsetAsync(contrib, 0, 8 * (size_t)n, st)) != cudaSuccess) return e;

@@ -139,6 +139,34 @@ def test_c4_full_size_sampled_parity_unmasked():
     assert_rgb_parity(img, orc, pixels=pix)
 
 
+def test_c4_full_size_sampled_parity_masked():
+    """BASELINE configs[3] masked (the bench's --config c4 path): key-frame
+    masks bit-exact against the oracle, records and tile lists bit-exact under
+    the OR-ed mask, sampled RGB parity."""
+    scene = fi.make_scene("c4")
+    cams = fi.make_cameras("c4")
+    times = fi.frame_times(300)
+    kf = fd.keyframes(300, 20)
+    frame = 211
+    l, r = fd.bracket(kf, frame)
+    sc = fd.Scene.from_arrays(scene)
+    ml = fd.keyframe_mask(sc, cams, float(times[kf[l]]))
+    mr = fd.keyframe_mask(sc, cams, float(times[kf[r]]))
+    assert np.array_equal(_np_mask(ml), oracle.keyframe_mask(scene, cams, times[kf[l]]))
+    assert np.array_equal(_np_mask(mr), oracle.keyframe_mask(scene, cams, times[kf[r]]))
+    active = _np_mask(ml) | _np_mask(mr)
+    cam = cams[16]
+    t = float(times[frame])
+    img, T, stats, rd = _render(scene, cam, t, ml, mr)
+    assert stats.n_act == int(mask_bits(active, scene.n).sum()) < scene.n
+    views = rd.debug_views()
+    assert_records_bit_exact(views, scene, cam, t, active)
+    assert_tile_lists_bit_exact(views, scene, cam, t, active)
+    pix = np.unique(np.random.default_rng(2).integers(0, cam.width * cam.height, 1500))
+    orc = oracle.render(scene, cam, t, mask=active, pixels=pix)
+    assert_rgb_parity(img, orc, pixels=pix)
+
+
 # ------------------------------------------------------------ invariants
 def test_all_ones_mask_equals_unmasked_and_determinism():
     n, W, H, f = 30_000, 300, 200, 220.0
@@ -297,3 +325,25 @@ def test_render_pipeline_matches_sequential():
         torch.cuda.current_stream().synchronize()
         for ref, h in zip(refs, host):
             assert torch.equal(ref.cpu(), h)
+
+
+def test_interleaved_and_planar_parameters_identical():
+    """fdgs_scene.param_stride: the interleaved 64-byte records (the Python
+    Scene's default) and four SoA planes give bit-identical frames, masks and
+    scores."""
+    scene = fi.make_scene("c3", n=40_000, seed=4)
+    cams = fi.make_cameras("c3", width=300, height=220, fx=222.0, count=3)
+    a = fd.Scene.from_arrays(scene)
+    b = fd.Scene({f: getattr(scene, f) for f in fd.api._FIELDS}, interleaved=False)
+    assert a.struct.param_stride == 4 and b.struct.param_stride == 0
+    t = float(np.float32(0.37))
+    ma, mb = fd.keyframe_mask(a, cams, t), fd.keyframe_mask(b, cams, t)
+    assert torch.equal(ma, mb)
+    ra, rb = fd.Renderer(a, 300, 220), fd.Renderer(b, 300, 220)
+    for cam in cams:
+        x, _ = ra.render_checked(cam, t, ma, ma)
+        y, _ = rb.render_checked(cam, t, mb, mb)
+        assert torch.equal(x, y)
+    sa = fd.stv_score(a, cams, [0.2, 0.6])["score"]
+    sb = fd.stv_score(b, cams, [0.2, 0.6])["score"]
+    assert torch.equal(sa, sb)
