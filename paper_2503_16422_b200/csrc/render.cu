@@ -1,17 +1,20 @@
 // render.cu -- the per-frame hot path of fdgs_render.
 //
-//   k_preprocess     rows 1-4: active mask OR + cull-first slice
-//                    (Eq. 1) + temporal marginal (Eq. 3)
-//                    + EWA projection + SH3 colour + order-preserving
-//                    compaction (warp ballot, block scan, decoupled look-back)
+//   k_cull           rows 1-2 + temporal cull: active mask OR,
+//                    binary64 p_t >= 1/255 test (Eq. 3), survivors
+//                    compacted in index order (ballot, block scan, look-back)
+//   k_slice          rows 3-4 on the survivors: Eq. 1 slice, EWA
+//                    projection + SH3 colour, visible compaction
 //   k_sort_*         row 5a: stable onesweep LSD radix sort (4 x 8-bit) of the
 //                    fp32 depth keys -> canonical (depth, index) order (P:126
 //                    "sorted by their depth", reading R8)
 //   k_bin_scan..     row 5b: tile cover per (Gaussian, tile row) (band_tiles),
-//                    per-tile counts, emission of (tile, slot) entries in
-//                    canonical order, then two stable 7-bit onesweep passes
-//   k_blend          row 6: per-tile front-to-back Eq. 2 with warp-uniform
-//                    early exit
+//                    per-tile counts, a stable 8-bit row partition of the row
+//                    items, per-row warp-ordered scatter into the tile lists
+//   k_blend_wl       row 6: per-tile front-to-back Eq. 2, warp-specialised
+//                    (producer builds per-warp record lists, 4 consumer warps
+//                    composite, warp-uniform early exit);
+//                    k_blend_ws: the counting / contribution-recording variant
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
