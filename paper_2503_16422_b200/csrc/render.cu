@@ -1289,6 +1289,53 @@ __global__ void __launch_bounds__(kWsThreads) k_blend_ws(const uint32_t *__restr
 // record one 16-byte entry {u, A', ~AABB mask, q}, its row's {t1, t4} and the
 // record's colour.  Work counters (kCount) and the contribution recorder stay on
 // k_blend_ws, which visits every record.
+// Conservative reach test of a pixel-centre box for the warp lists: does the
+// ellipse {e2 >= -margin} meet [xl, xr] x [yl, yr] (offsets from the splat
+// centre)?  The maximum of the concave quadratic e2 over a box is Q2 if the
+// centre lies inside, else the largest of its four edge maxima (each a 1-D
+// concave quadratic, maximised at its clamped stationary point).  The
+// continuous box contains the pixel centres, and the margin (1e-3 of the
+// quadratic's magnitude over the box, + 1e-3) exceeds the rounding of this
+// test and of the pinned fp32 e2 chain, so no pixel with e2 >= 0 is culled.
+__device__ __forceinline__ bool box_reach(float Ap, float Bp, float Cp, float Q2, float hA, float hC, float xl,
+                                          float xr, float yl, float yr) {
+    auto e = [&](float dx, float dy) { return fmaf(dx, fmaf(Ap, dx, Bp * dy), fmaf(Cp * dy, dy, Q2)); };
+    float best = Q2;
+    if (!(xl <= 0.f && 0.f <= xr && yl <= 0.f && 0.f <= yr)) {
+        const float x1 = fminf(fmaxf(Bp * yl * hA, xl), xr), x2 = fminf(fmaxf(Bp * yr * hA, xl), xr);
+        const float y1 = fminf(fmaxf(Bp * xl * hC, yl), yr), y2 = fminf(fmaxf(Bp * xr * hC, yl), yr);
+        best = fmaxf(fmaxf(e(x1, yl), e(x2, yr)), fmaxf(e(xl, y1), e(xr, y2)));
+    }
+    const float dxm = fmaxf(fabsf(xl), fabsf(xr)), dym = fmaxf(fabsf(yl), fabsf(yr));
+    const float mag = fabsf(Ap) * dxm * dxm + fabsf(Bp) * dxm * dym + fabsf(Cp) * dym * dym;
+    return best >= -(1e-3f * mag + 1e-3f);
+}
+
+// Producer staging of k_blend_wl: the complemented pixel-AABB mask (per-pixel
+// decision) and a 4-bit mask of the consumer warps (4-row groups of the tile)
+// whose pixel-centre box within the AABB the margin-inflated ellipse reaches.
+__device__ __forceinline__ uint32_t stage_groups(int tx, int ty, const float4 &r0, const float4 &r1,
+                                                 uint32_t &mbits) {
+    const uint32_t ax = __float_as_uint(r1.z), ay = __float_as_uint(r1.w);
+    const int x0 = max((int)(ax & 0xffff) - tx * 16, 0), x1 = min((int)(ax >> 16) - tx * 16, 15);
+    const int y0 = max((int)(ay & 0xffff) - ty * 16, 0), y1 = min((int)(ay >> 16) - ty * 16, 15);
+    const uint32_t xm = ((2u << x1) - 1u) & ~((1u << x0) - 1u);
+    const uint32_t ym = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
+    mbits = ~(xm | (ym << 16));
+    const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
+    const float hA = __fdividef(-0.5f, Ap), hC = __fdividef(-0.5f, Cp);  // stationary points only
+    const float xl = (float)(tx * 16 + x0) + 0.5f - u, xr = (float)(tx * 16 + x1) + 0.5f - u;
+    uint32_t g = 0;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        const int ra = max(y0, 4 * w), rb = min(y1, 4 * w + 3);
+        if (ra > rb) continue;
+        const float yl = (float)(ty * 16 + ra) + 0.5f - v, yr = (float)(ty * 16 + rb) + 0.5f - v;
+        if (box_reach(Ap, Bp, Cp, Q2, hA, hC, xl, xr, yl, yr)) g |= 1u << w;
+    }
+    return g;
+}
+
 #ifndef FDGS_WL_BUF
 #define FDGS_WL_BUF 2
 #endif
@@ -1341,26 +1388,25 @@ __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uin
             if (k >= kWlBuf) mb_wait(&empty[b], ((k / kWlBuf) - 1) & 1);
             const bool stop = base >= end || *(volatile uint32_t *)&s_done == 4;
             const uint32_t n = stop ? 0u : min(32u, end - base);
-            uint32_t rows = 0;
-            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, oa, oc, od;
+            uint32_t groups = 0, mb = 0;
+            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0;
             if (lane < (int)n) {
                 const uint32_t v = __ldg(entries + base + lane);
                 r0 = __ldg(rec0 + v);
                 r1 = __ldg(rec1 + v);
-                const float4 r2 = __ldg(rec2 + v);
-                stage_fields(tx, ty, r0, r1, r2, oa, oc, od);
-                rows = __float_as_uint(od.z) >> 16;
+                r2 = __ldg(rec2 + v);
+                groups = stage_groups(tx, ty, r0, r1, mb);
             }
             const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
-            const float mbits = od.y;
+            const float mbits = __uint_as_float(mb);
 #pragma unroll
             for (int w = 0; w < 4; ++w) {  // per consumer warp: packed list + its rows' e2 row terms
-                const bool reach = lane < (int)n && ((rows >> (4 * w)) & 0xFu) != 0u;
+                const bool reach = lane < (int)n && ((groups >> w) & 1u) != 0u;
                 const uint32_t bal = __ballot_sync(0xffffffffu, reach);
                 if (reach) {
                     WlEntry &E = s_list[b][w][__popc(bal & lanemask_lt())];
-                    E.a = make_float4(u, Ap, mbits, oc.z);
-                    E.c = make_float4(oc.w, od.x, __int_as_float(lane), 0.f);
+                    E.a = make_float4(u, Ap, mbits, r2.x);
+                    E.c = make_float4(r2.y, r2.z, __int_as_float(lane), 0.f);
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {  // pinned e2 chain, row terms (DESIGN.md step 10)
                         const float dy = __fsub_rn((float)(ty * 16 + 4 * w + r) + 0.5f, v);
