@@ -32,7 +32,11 @@ sys.path.insert(0, ROOT)
 METRIC = "frames/sec at 1352x1014 (N3V-shaped 200k-Gaussian masked scene)"
 UNIT = "frames/s"
 CONFIG = "c3"
-BLEND_KERNEL = "k_blend_wl"  # the timed blend (render.cu); k_blend_ws<true> supplies the work counters
+BLEND_KERNEL = "k_blend_wl"
+# launches of libfdgs kernels per frame (render.cu launch_render, tile grid <= 256 rows):
+# k_cull, k_cull_scan, k_cull_emit, k_slice, k_sort_hist, 4 x k_onesweep (depth), k_bin_scan,
+# k_row_items, k_tile_scan, k_onesweep (rows), k_row_count, k_row_scatter, k_blend_wl
+KERNELS_PER_FRAME = 16  # the timed blend (render.cu); k_blend_ws<true> supplies the work counters
 N_CAMS = 20
 N_FRAMES_T = 300
 INTERVAL = 20
@@ -358,7 +362,7 @@ def run_ours(args):
                        "l2": "flushed between steps (512 MiB write)", "parallelism": f"frames x{world}",
                        "streams_per_gpu": args.streams,
                        "stream_split": "front end high priority, blend low priority" if not args.no_split else "none"},
-               gpu_launches=13 * frames_rank)
+               gpu_launches=KERNELS_PER_FRAME * frames_rank)
     if use_ev and stage_ms.sum() > 0:
         per_frame = stage_ms / frames_rank
         dom = int(np.argmax(stage_ms))

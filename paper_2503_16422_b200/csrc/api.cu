@@ -67,7 +67,6 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     // cleared per frame
     L.counters = take(sizeof(Counters));
     L.lookback = take(sizeof(uint32_t) * (size_t)std::max(L.n_parts, 1));
-    L.lookback_cull = take(sizeof(uint32_t) * (size_t)std::max(L.cull_parts, 1));
     L.sort_gbase = take(sizeof(uint32_t) * 4 * 256);
     L.tile_diff = take(sizeof(int) * (size_t)(L.tiles_x + 1) * (L.tiles_y + 1));
     L.row_diff = take(sizeof(int) * ((size_t)L.tiles_y + 1));
@@ -79,6 +78,8 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.tile_status = take(sizeof(uint64_t) * 2 * 256 * (size_t)L.tile_parts);
     // per-frame scratch, fully written before read
     L.surv = take(4 * nn);
+    L.surv_bits = take(4 * ((nn + 31) / 32 + 32));                     // survivor bits (k_cull)
+    L.cull_cnt = take(4 * (size_t)std::max(L.cull_parts, 1));          // survivors per k_cull partition
     L.rec0 = take(16 * nn);
     L.rec1 = take(16 * nn);
     L.rec2 = take(16 * nn);

@@ -108,21 +108,20 @@ __device__ __forceinline__ uint32_t block_offsets(uint32_t (&cnt)[R][kPreBlock /
     return *s_excl;
 }
 
+// k_cull runs as three non-blocking passes (a decoupled look-back here left
+// 53% of the warps waiting at the block barrier at C4): the survivor bits and
+// per-partition counts, a one-block scan of the counts, then the ordered
+// emission of the survivor indices.
 __global__ void __launch_bounds__(kPreBlock) k_cull(SceneDev sc, const uint32_t *__restrict__ mask_l,
                                                     const uint32_t *__restrict__ mask_r, float t, Counters *ctr,
-                                                    uint32_t *lb, uint32_t *__restrict__ surv) {
-    constexpr int NW = kPreBlock / 32, R = kCullItems / kPreBlock;
-    __shared__ uint32_t s_cnt[R][NW];
-    __shared__ uint32_t s_part, s_excl, s_tot, s_act;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) {
-        s_part = atomicAdd(&ctr->cull_ticket, 1u);
-        s_act = 0;
-    }
+                                                    uint32_t *__restrict__ bits, uint32_t *__restrict__ cnt) {
+    constexpr int R = kCullItems / kPreBlock;
+    __shared__ uint32_t s_act, s_n;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint32_t part = blockIdx.x;
+    if (tid == 0) s_act = s_n = 0;
     __syncthreads();
-    const uint32_t part = s_part;
-    uint32_t bal[R];
-    uint32_t nact = 0;
+    uint32_t nact = 0, nsurv = 0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int i = (int)part * kCullItems + r * kPreBlock + tid;
@@ -134,24 +133,92 @@ __global__ void __launch_bounds__(kPreBlock) k_cull(SceneDev sc, const uint32_t 
                 if (mask_r != nullptr) w |= __ldg(mask_r + (i >> 5));
             }
             act = (w >> (i & 31)) & 1u;
-            if (act) keep = temporal_pass(sc.ld_mean(i), sc.ld_scale(i), sc.ld_rot_l(i),
-                                          sc.ld_rot_r(i), t);
+            if (act) keep = temporal_pass(sc.ld_mean(i), sc.ld_scale(i), sc.ld_rot_l(i), sc.ld_rot_r(i), t);
         }
         nact += __popc(__ballot_sync(0xffffffffu, act));
-        bal[r] = __ballot_sync(0xffffffffu, keep);
-        if (lane == 0) s_cnt[r][warp] = __popc(bal[r]);
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        nsurv += __popc(bal);
+        if (lane == 0 && i - lane < sc.n) bits[i >> 5] = bal;
     }
-    if (lane == 0 && nact) atomicAdd(&s_act, nact);
-    const uint32_t excl = block_offsets<R>(s_cnt, lb, part, &s_excl, &s_tot);
+    if (lane == 0) {
+        if (nact) atomicAdd(&s_act, nact);
+        if (nsurv) atomicAdd(&s_n, nsurv);
+    }
+    __syncthreads();
     if (tid == 0) {
+        cnt[part] = s_n;
         if (s_act) atomicAdd(&ctr->n_act, s_act);
-        if (part == gridDim.x - 1) ctr->n_surv = excl + s_tot;
     }
+}
+
+// One block: exclusive scan of the per-partition survivor counts (in place);
+// the total is the survivor count n_surv.
+__global__ void __launch_bounds__(1024) k_cull_scan(uint32_t *__restrict__ cnt, int parts, Counters *ctr) {
+    __shared__ uint32_t s_w[32];
+    __shared__ uint32_t s_carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (int c0 = 0; c0 < parts; c0 += 1024) {
+        const int i = c0 + tid;
+        const uint32_t x = i < parts ? cnt[i] : 0u;
+        uint32_t inc = x;
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-        if ((bal[r] >> lane) & 1u)
-            surv[excl + s_cnt[r][warp] + __popc(bal[r] & lanemask_lt())] =
-                (uint32_t)((int)part * kCullItems + r * kPreBlock + tid);
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) s_w[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t wv = s_w[lane];
+            uint32_t wi = wv;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += y;
+            }
+            s_w[lane] = wi - wv;
+        }
+        __syncthreads();
+        const uint32_t carry = s_carry;
+        if (i < parts) cnt[i] = carry + s_w[warp] + inc - x;
+        __syncthreads();
+        if (tid == 1023) s_carry = carry + s_w[31] + inc;
+        __syncthreads();
+    }
+    if (tid == 0) ctr->n_surv = s_carry;
+}
+
+// Ordered emission: partition p's survivors go to [base_p, base_p + count).
+__global__ void __launch_bounds__(kPreBlock) k_cull_emit(const uint32_t *__restrict__ bits,
+                                                         const uint32_t *__restrict__ base, int n,
+                                                         uint32_t *__restrict__ surv) {
+    constexpr int WORDS = kCullItems / 32;  // 32 bit-words per partition
+    __shared__ uint32_t s_off[WORDS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t part = blockIdx.x;
+    const int nw = (n + 31) / 32;
+    if (warp == 0) {
+        const int wi = (int)part * WORDS + lane;
+        const uint32_t c = wi < nw ? __popc(__ldg(bits + wi)) : 0u;
+        uint32_t inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        s_off[lane] = __ldg(base + part) + inc - c;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < WORDS / (kPreBlock / 32); ++k) {
+        const int w = warp * (WORDS / (kPreBlock / 32)) + k;  // word of this partition
+        const int wi = (int)part * WORDS + w;
+        if (wi >= nw) break;
+        const uint32_t word = __ldg(bits + wi);
+        if ((word >> lane) & 1u) surv[s_off[w] + __popc(word & lanemask_lt())] = (uint32_t)(wi * 32 + lane);
+    }
 }
 
 struct PreRes {
@@ -1531,8 +1598,11 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         e = cudaMemsetAsync(ws + L.counters, 0, L.zero_end - L.counters, st);  // counters, look-back, histograms
         if (e != cudaSuccess) return e;
         if (L.n > 0) {
-            k_cull<<<L.cull_parts, kPreBlock, 0, st>>>(sc, mask_l, mask_r, t, ctr,
-                                                        reinterpret_cast<uint32_t *>(ws + L.lookback_cull), surv);
+            uint32_t *cbits = reinterpret_cast<uint32_t *>(ws + L.surv_bits);
+            uint32_t *ccnt = reinterpret_cast<uint32_t *>(ws + L.cull_cnt);
+            k_cull<<<L.cull_parts, kPreBlock, 0, st>>>(sc, mask_l, mask_r, t, ctr, cbits, ccnt);
+            k_cull_scan<<<1, 1024, 0, st>>>(ccnt, L.cull_parts, ctr);
+            k_cull_emit<<<L.cull_parts, kPreBlock, 0, st>>>(cbits, ccnt, L.n, surv);
             k_slice<<<L.slice_grid, kPreBlock, 0, st>>>(sc, cam, t, ctr, lb, surv, rec0, rec1, rec2, depth, rect);
         }
         if (ev && (e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
