@@ -187,15 +187,18 @@ fdgs_status fdgs_render_checked(const fdgs_scene *scene, const uint32_t *d_mask_
                                 void *stream);
 
 /* Device views into a render workspace after fdgs_render (tests/debug only).
- * Arrays are indexed by the visible slot v < n_vis (ascending Gaussian index):
+ * Records are indexed by the SLOT of a Gaussian that passed the mask and the
+ * temporal cull (survivor order = ascending Gaussian index); only the slots of
+ * visible Gaussians hold data, and vis uint32[n_vis] lists them ascending:
  *   rec0 float4 {u, v, A', B'}, rec1 float4 {C', Q2, aabb_x, aabb_y}
  *   (aabb_x = px0 | px1 << 16 as int bits), rec2 float4 {r, g, b, gid bits},
- *   depth uint32 (fp32 bits of camera z), order uint32[n_vis] (visible slots
- *   in canonical (depth, index) order), tile_start uint32[n_tiles + 1],
- *   entries uint32[E] (visible slots, per tile in canonical order). */
+ *   depth uint32 (fp32 bits of camera z), order uint32[n_vis] (slots in
+ *   canonical (depth, index) order), tile_start uint32[n_tiles + 1],
+ *   entries uint32[E] (slots, per tile in canonical order). */
 typedef struct {
     const void *rec0, *rec1, *rec2;
     const uint32_t *depth;
+    const uint32_t *vis;
     const uint32_t *order;
     const uint32_t *tile_start;
     const uint32_t *entries;

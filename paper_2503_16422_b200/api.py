@@ -200,15 +200,20 @@ class Renderer:
         def arr(ptr, count, itemsize, dtype):
             return self._slice(ptr, base, count * itemsize).view(dtype)
 
+        # records live at survivor slots; re-index everything by the visible
+        # rank (ascending Gaussian index) for the caller
+        vis = arr(v.vis, n, 4, torch.int32)[:n_vis].long()
+        rank = torch.full((max(n, 1),), -1, dtype=torch.long, device=self.ws.device)
+        rank[vis] = torch.arange(n_vis, device=self.ws.device)
         return dict(
             n_act=n_act, n_vis=n_vis, n_entries=E, status=status,
-            rec0=arr(v.rec0, n, 16, torch.float32).view(n, 4)[:n_vis],
-            rec1=arr(v.rec1, n, 16, torch.float32).view(n, 4)[:n_vis],
-            rec2=arr(v.rec2, n, 16, torch.float32).view(n, 4)[:n_vis],
-            depth=arr(v.depth, n, 4, torch.int32)[:n_vis],
-            order=arr(v.order, n, 4, torch.int32)[:n_vis],
+            rec0=arr(v.rec0, n, 16, torch.float32).view(n, 4)[vis],
+            rec1=arr(v.rec1, n, 16, torch.float32).view(n, 4)[vis],
+            rec2=arr(v.rec2, n, 16, torch.float32).view(n, 4)[vis],
+            depth=arr(v.depth, n, 4, torch.int32)[vis],
+            order=rank[arr(v.order, n, 4, torch.int32)[:n_vis].long()].int(),
             tile_start=arr(v.tile_start, v.n_tiles + 1, 4, torch.int32),
-            entries=arr(v.entries, max(E, 1), 4, torch.int32)[:E],
+            entries=rank[arr(v.entries, max(E, 1), 4, torch.int32)[:E].long()].int(),
             n_tiles=v.n_tiles,
         )
 

@@ -51,7 +51,7 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.n_tiles = L.tiles_x * L.tiles_y;
     L.n_parts = (n + 2 * kPreBlock - 1) / (2 * kPreBlock);  // k_slice partitions (2 survivors per thread)
     L.cull_parts = (n + 4 * kPreBlock - 1) / (4 * kPreBlock);  // k_cull partitions (4 Gaussians per thread)
-    L.slice_grid = std::max(1, std::min(L.n_parts, 2 * sm_count()));  // 2 resident blocks per SM
+    L.slice_grid = std::max(1, std::min(L.n_parts, 2 * sm_count()));  // grid-stride k_slice / k_vis_emit
     L.p_sort = sm_count();
     L.sort_parts = std::max(1, (n + kDepthTile - 1) / kDepthTile);
     L.tile_parts = (int32_t)std::max<int64_t>(1, (max_entries + kTileTile - 1) / kTileTile);
@@ -80,6 +80,9 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.surv = take(4 * nn);
     L.surv_bits = take(4 * ((nn + 31) / 32 + 32));                     // survivor bits (k_cull)
     L.cull_cnt = take(4 * (size_t)std::max(L.cull_parts, 1));          // survivors per k_cull partition
+    L.vis = take(4 * nn);                                               // visible survivor slots, ascending
+    L.vis_bits = take(4 * ((nn + 31) / 32 + 32));                      // visibility bits per survivor slot
+    L.vis_cnt = take(4 * (size_t)std::max(L.n_parts, 1));              // visible per k_slice partition
     L.rec0 = take(16 * nn);
     L.rec1 = take(16 * nn);
     L.rec2 = take(16 * nn);
@@ -326,6 +329,7 @@ fdgs_status fdgs_render_debug_views(void *d_ws, size_t ws_bytes, int32_t n, int3
     out->rec1 = w + L.rec1;
     out->rec2 = w + L.rec2;
     out->depth = reinterpret_cast<const uint32_t *>(w + L.depth);
+    out->vis = reinterpret_cast<const uint32_t *>(w + L.vis);
     out->order = reinterpret_cast<const uint32_t *>(w + L.vals1);
     out->tile_start = reinterpret_cast<const uint32_t *>(w + L.tile_start);
     out->entries = reinterpret_cast<const uint32_t *>(w + L.entries);

@@ -60,53 +60,19 @@ __device__ __forceinline__ uint32_t lookback_warp(uint32_t *status, uint32_t par
 }
 
 // ---------------------------------------------------------------- rows 1-4
-// Two uniform-work passes instead of one fused kernel whose blocks waited on
-// their few survivor warps (ncu at C4: 59% of cycles stalled at the barriers):
-//   k_cull   rows 1-2 + the temporal cull of row 3: one thread per Gaussian,
-//            mask bit (OR of the two key-frame rows) then the pinned binary64
-//            temporal test; survivors compacted in ascending index order
-//            (warp ballot, block scan, decoupled look-back) -> surv[];
-//   k_slice  rows 3-4 on the dense survivor list: Eq. 1 slice, support and
-//            near culls, EWA projection, cover cull, SH colour; visible ones
-//            compacted again in order -> the splat records.
+// Uniform-work passes instead of one fused kernel whose blocks waited on their
+// few survivor warps (ncu at C4: 59% of cycles stalled at the barriers), and
+// no in-kernel look-back (blocks waiting on predecessors):
+//   k_cull + k_count_scan + k_cull_emit   rows 1-2 + the temporal cull of row
+//            3: one thread per Gaussian, mask bit (OR of the two key-frame
+//            rows) then the pinned binary64 temporal test; survivor bits and
+//            counts, scanned, emitted in ascending index order -> surv[];
+//   k_slice + k_count_scan + k_vis_emit   rows 3-4 on the dense survivor list:
+//            Eq. 1 slice, support and near culls, EWA projection, cover cull,
+//            SH colour; records at the survivor slot, the visible slots
+//            compacted in order (vis[], and their depth keys for the sort).
 constexpr int kCullItems = 4 * kPreBlock;   // Gaussians per k_cull partition
 constexpr int kSliceItems = 2 * kPreBlock;  // survivors per k_slice partition
-
-// Block-wide exclusive offsets of per-(round, warp) counts plus the partition's
-// global offset by look-back.  cnt[r][w] in, offsets out; returns the block's
-// global exclusive base.  All threads call it.
-template <int R>
-__device__ __forceinline__ uint32_t block_offsets(uint32_t (&cnt)[R][kPreBlock / 32], uint32_t *lb, uint32_t part,
-                                                  uint32_t *s_excl, uint32_t *s_tot) {
-    constexpr int NW = kPreBlock / 32;
-    const int tid = threadIdx.x, lane = tid & 31;
-    __syncthreads();
-    if (tid < 32) {  // (round, warp) order = ascending item index
-        uint32_t run = 0;
-        uint32_t mine[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            mine[r] = 0;
-            for (int w = 0; w < NW; ++w) {
-                const uint32_t c = cnt[r][w];
-                if (w == lane) mine[r] = run;
-                run += c;
-            }
-        }
-        __syncwarp();
-        if (lane < NW) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) cnt[r][lane] = mine[r];
-        }
-        const uint32_t excl = lookback_warp(lb, part, run, lane);
-        if (lane == 0) {
-            *s_excl = excl;
-            *s_tot = run;
-        }
-    }
-    __syncthreads();
-    return *s_excl;
-}
 
 // k_cull runs as three non-blocking passes (a decoupled look-back here left
 // 53% of the warps waiting at the block barrier at C4): the survivor bits and
@@ -151,12 +117,15 @@ __global__ void __launch_bounds__(kPreBlock) k_cull(SceneDev sc, const uint32_t 
     }
 }
 
-// One block: exclusive scan of the per-partition survivor counts (in place);
-// the total is the survivor count n_surv.
-__global__ void __launch_bounds__(1024) k_cull_scan(uint32_t *__restrict__ cnt, int parts, Counters *ctr) {
+// One block: exclusive scan of per-partition counts (in place), the total to
+// *total.  parts = parts_ub, or ceil(*items / per_part) when items != NULL (the
+// item count is only known on the device).
+__global__ void __launch_bounds__(1024) k_count_scan(uint32_t *__restrict__ cnt, int parts_ub,
+                                                     const uint32_t *items, int per_part, uint32_t *total) {
     __shared__ uint32_t s_w[32];
     __shared__ uint32_t s_carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int parts = items ? min(parts_ub, (int)((*items + per_part - 1) / per_part)) : parts_ub;
     if (tid == 0) s_carry = 0;
     __syncthreads();
     for (int c0 = 0; c0 < parts; c0 += 1024) {
@@ -187,7 +156,7 @@ __global__ void __launch_bounds__(1024) k_cull_scan(uint32_t *__restrict__ cnt, 
         if (tid == 1023) s_carry = carry + s_w[31] + inc;
         __syncthreads();
     }
-    if (tid == 0) ctr->n_surv = s_carry;
+    if (tid == 0) *total = s_carry;
 }
 
 // Ordered emission: partition p's survivors go to [base_p, base_p + count).
@@ -221,29 +190,24 @@ __global__ void __launch_bounds__(kPreBlock) k_cull_emit(const uint32_t *__restr
     }
 }
 
-struct PreRes {
-    float u, v, Ap, Bp, Cp, Q2, mx, my, mz;
-    uint32_t ax, ay, depth;
-    int i;
-};
-
-// Persistent grid; partitions of kSliceItems survivors in ticket order.
-__global__ void __launch_bounds__(kPreBlock) k_slice(SceneDev sc, CamDev cam, float t, Counters *ctr, uint32_t *lb,
+// Grid-stride over partitions of kSliceItems survivors.  Records of visible
+// Gaussians are written at their survivor slot (sparse); the visibility bits
+// and per-partition counts feed k_count_scan + k_vis_emit, which compact the
+// slots in order without any block waiting on another.
+__global__ void __launch_bounds__(kPreBlock) k_slice(SceneDev sc, CamDev cam, float t, Counters *ctr,
                                                      const uint32_t *__restrict__ surv, float4 *__restrict__ rec0,
                                                      float4 *__restrict__ rec1, float4 *__restrict__ rec2,
-                                                     uint32_t *__restrict__ depth, uint2 *__restrict__ rect) {
-    constexpr int NW = kPreBlock / 32, R = kSliceItems / kPreBlock;
-    __shared__ uint32_t s_cnt[R][NW];
-    __shared__ uint32_t s_part, s_excl, s_tot;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+                                                     uint32_t *__restrict__ depth, uint2 *__restrict__ rect,
+                                                     uint32_t *__restrict__ vbits, uint32_t *__restrict__ vcnt) {
+    constexpr int R = kSliceItems / kPreBlock;
+    __shared__ uint32_t s_n;
+    const int tid = threadIdx.x, lane = tid & 31;
     const uint32_t ns = ctr->n_surv;
-    while (true) {
-        if (tid == 0) s_part = atomicAdd(&ctr->part_ticket, 1u);
+    const uint32_t parts = (ns + kSliceItems - 1) / kSliceItems;
+    for (uint32_t part = blockIdx.x; part < parts; part += gridDim.x) {
+        if (tid == 0) s_n = 0;
         __syncthreads();
-        const uint32_t part = s_part;
-        if ((uint64_t)part * kSliceItems >= ns) return;
-        PreRes res[R];
-        uint32_t vb[R];
+        uint32_t nv = 0;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const uint32_t sidx = part * kSliceItems + r * kPreBlock + tid;
@@ -252,47 +216,73 @@ __global__ void __launch_bounds__(kPreBlock) k_slice(SceneDev sc, CamDev cam, fl
                 const int i = (int)__ldg(surv + sidx);
                 Slice sl;
                 Proj pj;
-                int st = slice_gaussian(sc.ld_mean(i), sc.ld_scale(i), sc.ld_rot_l(i),
-                                        sc.ld_rot_r(i), __ldg(sc.L + i), t, sl);
+                int st = slice_gaussian(sc.ld_mean(i), sc.ld_scale(i), sc.ld_rot_l(i), sc.ld_rot_r(i), __ldg(sc.L + i),
+                                        t, sl);
                 if (st == kNear) st = project_gaussian(sl, cam, pj);
                 vis = st == kVisible;
                 if (vis) {
-                    res[r].u = pj.u;
-                    res[r].v = pj.v;
-                    res[r].Ap = pj.Ap;
-                    res[r].Bp = pj.Bp;
-                    res[r].Cp = pj.Cp;
-                    res[r].Q2 = pj.Q2;
-                    res[r].mx = (float)sl.mu3[0];
-                    res[r].my = (float)sl.mu3[1];
-                    res[r].mz = (float)sl.mu3[2];
-                    res[r].ax = pj.px0 | (pj.px1 << 16);
-                    res[r].ay = pj.py0 | (pj.py1 << 16);
-                    res[r].depth = pj.depth_bits;
-                    res[r].i = i;
+                    float rgb[3];
+                    const float mx = (float)sl.mu3[0], my = (float)sl.mu3[1], mz = (float)sl.mu3[2];
+                    // dense SH, or the VQ codebook entry of the Gaussian (Ours-PP decode)
+                    const size_t row = sc.sh_index ? (size_t)__ldg(sc.sh_index + i) : (size_t)i;
+                    sh_color(sc.sh + row * 12, mx - cam.campos[0], my - cam.campos[1], mz - cam.campos[2], rgb);
+                    const uint32_t ax = pj.px0 | (pj.px1 << 16), ay = pj.py0 | (pj.py1 << 16);
+                    rec0[sidx] = make_float4(pj.u, pj.v, pj.Ap, pj.Bp);
+                    rec1[sidx] = make_float4(pj.Cp, pj.Q2, __uint_as_float(ax), __uint_as_float(ay));
+                    rec2[sidx] = make_float4(rgb[0], rgb[1], rgb[2], __int_as_float(i));
+                    depth[sidx] = pj.depth_bits;
+                    rect[sidx] = make_uint2(ax, ay);
                 }
             }
-            vb[r] = __ballot_sync(0xffffffffu, vis);
-            if (lane == 0) s_cnt[r][warp] = __popc(vb[r]);
+            const uint32_t bal = __ballot_sync(0xffffffffu, vis);
+            nv += __popc(bal);
+            if (lane == 0 && sidx - lane < ns) vbits[sidx >> 5] = bal;
         }
-        const uint32_t excl = block_offsets<R>(s_cnt, lb, part, &s_excl, &s_tot);
-        if (tid == 0 && (uint64_t)(part + 1) * kSliceItems >= ns) ctr->n_vis = excl + s_tot;  // last partition
+        if (lane == 0 && nv) atomicAdd(&s_n, nv);
+        __syncthreads();
+        if (tid == 0) vcnt[part] = s_n;
+    }
+}
+
+// Ordered compaction of the visible survivor slots: vis[pos] = slot and the
+// depth key beside it (the depth sort's input), pos = partition base + rank.
+__global__ void __launch_bounds__(kPreBlock) k_vis_emit(const uint32_t *__restrict__ vbits,
+                                                        const uint32_t *__restrict__ base, const Counters *ctr,
+                                                        const uint32_t *__restrict__ depth, uint32_t *__restrict__ vis,
+                                                        uint32_t *__restrict__ keys) {
+    constexpr int WORDS = kSliceItems / 32;  // 16 bit-words per partition
+    __shared__ uint32_t s_off[WORDS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t ns = ctr->n_surv;
+    const uint32_t parts = (ns + kSliceItems - 1) / kSliceItems;
+    const int nw = (int)((ns + 31) / 32);
+    for (uint32_t part = blockIdx.x; part < parts; part += gridDim.x) {
+        if (warp == 0) {
+            const int wi = (int)part * WORDS + lane;
+            const uint32_t c = (lane < WORDS && wi < nw) ? __popc(__ldg(vbits + wi)) : 0u;
+            uint32_t inc = c;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            if (!((vb[r] >> lane) & 1u)) continue;
-            const PreRes &Rr = res[r];
-            const uint32_t pos = excl + s_cnt[r][warp] + __popc(vb[r] & lanemask_lt());
-            float rgb[3];
-            // dense SH, or the VQ codebook entry of the Gaussian (Ours-PP decode)
-            const size_t row = sc.sh_index ? (size_t)__ldg(sc.sh_index + Rr.i) : (size_t)Rr.i;
-            sh_color(sc.sh + row * 12, Rr.mx - cam.campos[0], Rr.my - cam.campos[1], Rr.mz - cam.campos[2], rgb);
-            rec0[pos] = make_float4(Rr.u, Rr.v, Rr.Ap, Rr.Bp);
-            rec1[pos] = make_float4(Rr.Cp, Rr.Q2, __uint_as_float(Rr.ax), __uint_as_float(Rr.ay));
-            rec2[pos] = make_float4(rgb[0], rgb[1], rgb[2], __int_as_float(Rr.i));
-            depth[pos] = Rr.depth;
-            rect[pos] = make_uint2(Rr.ax, Rr.ay);
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (lane < WORDS) s_off[lane] = __ldg(base + part) + inc - c;
         }
-        __syncthreads();  // s_cnt / s_part reuse by the next partition
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < WORDS / (kPreBlock / 32); ++k) {
+            const int w = warp * (WORDS / (kPreBlock / 32)) + k;
+            const int wi = (int)part * WORDS + w;
+            if (wi < nw) {
+                const uint32_t word = __ldg(vbits + wi);
+                if ((word >> lane) & 1u) {
+                    const uint32_t slot = (uint32_t)(wi * 32 + lane), pos = s_off[w] + __popc(word & lanemask_lt());
+                    vis[pos] = slot;
+                    keys[pos] = __ldg(depth + slot);
+                }
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -1575,7 +1565,6 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
                           fdgs_frame_stats *stats, cudaStream_t st, cudaEvent_t const *ev, cudaStream_t blend_st,
                           cudaEvent_t split_ev, unsigned long long *contrib, uint32_t *stv_info) {
     Counters *ctr = reinterpret_cast<Counters *>(ws + L.counters);
-    uint32_t *lb = reinterpret_cast<uint32_t *>(ws + L.lookback);
     float4 *rec0 = reinterpret_cast<float4 *>(ws + L.rec0);
     float4 *rec1 = reinterpret_cast<float4 *>(ws + L.rec1);
     float4 *rec2 = reinterpret_cast<float4 *>(ws + L.rec2);
@@ -1587,6 +1576,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     uint32_t *tstart = reinterpret_cast<uint32_t *>(ws + L.tile_start);
     uint32_t *entries = reinterpret_cast<uint32_t *>(ws + L.entries);
     uint32_t *surv = reinterpret_cast<uint32_t *>(ws + L.surv);
+    uint32_t *vis = reinterpret_cast<uint32_t *>(ws + L.vis);
 
     cudaError_t e = cudaSuccess;
     if (ev && (e = cudaEventRecord(ev[0], st)) != cudaSuccess) return e;
@@ -1601,19 +1591,25 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
             uint32_t *cbits = reinterpret_cast<uint32_t *>(ws + L.surv_bits);
             uint32_t *ccnt = reinterpret_cast<uint32_t *>(ws + L.cull_cnt);
             k_cull<<<L.cull_parts, kPreBlock, 0, st>>>(sc, mask_l, mask_r, t, ctr, cbits, ccnt);
-            k_cull_scan<<<1, 1024, 0, st>>>(ccnt, L.cull_parts, ctr);
+            k_count_scan<<<1, 1024, 0, st>>>(ccnt, L.cull_parts, nullptr, kCullItems, &ctr->n_surv);
             k_cull_emit<<<L.cull_parts, kPreBlock, 0, st>>>(cbits, ccnt, L.n, surv);
-            k_slice<<<L.slice_grid, kPreBlock, 0, st>>>(sc, cam, t, ctr, lb, surv, rec0, rec1, rec2, depth, rect);
+            uint32_t *vbits = reinterpret_cast<uint32_t *>(ws + L.vis_bits);
+            uint32_t *vcnt = reinterpret_cast<uint32_t *>(ws + L.vis_cnt);
+            k_slice<<<L.slice_grid, kPreBlock, 0, st>>>(sc, cam, t, ctr, surv, rec0, rec1, rec2, depth, rect, vbits,
+                                                        vcnt);
+            k_count_scan<<<1, 1024, 0, st>>>(vcnt, L.n_parts, &ctr->n_surv, kSliceItems, &ctr->n_vis);
+            k_vis_emit<<<L.slice_grid, kPreBlock, 0, st>>>(vbits, vcnt, ctr, depth, vis, keys[1]);
         }
         if (ev && (e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
         uint32_t *gbase = reinterpret_cast<uint32_t *>(ws + L.sort_gbase);  // [4][256] depth digit bases
         uint32_t *epoch = reinterpret_cast<uint32_t *>(ws + L.epoch);
         uint64_t *sstat = reinterpret_cast<uint64_t *>(ws + L.sort_status);
-        k_sort_hist<<<L.p_sort, kSortThreads, 0, st>>>(depth, ctr, gbase, epoch);
+        k_sort_hist<<<L.p_sort, kSortThreads, 0, st>>>(keys[1], ctr, gbase, epoch);
         constexpr int kDItems = 4;
         for (int pass = 0; pass < 4; ++pass) {
-            const uint32_t *kin = pass == 0 ? depth : keys[(pass - 1) & 1];
-            const uint32_t *vin = pass == 0 ? nullptr : vals[(pass - 1) & 1];
+            // pass 0 reads the compacted keys (keys[1]) and the visible survivor slots
+            const uint32_t *kin = pass == 0 ? keys[1] : keys[(pass - 1) & 1];
+            const uint32_t *vin = pass == 0 ? vis : vals[(pass - 1) & 1];
             k_onesweep<8, kDItems><<<std::min(L.sort_parts, tune_pgrid() * L.p_sort), kSortThreads, 0, st>>>(
                 kin, vin, pass == 3 ? nullptr : keys[pass & 1], vals[pass & 1], &ctr->n_vis, epoch,
                 &ctr->sort_ticket[1 + pass], 8 * pass, gbase + 256 * pass,
