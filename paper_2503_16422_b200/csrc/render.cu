@@ -508,71 +508,84 @@ __device__ __forceinline__ TileRect tile_rect(uint2 r) {
     return t;
 }
 
-// Row 5b (1/5): tile rows per Gaussian (ny of its pixel AABB) in canonical
-// order -> their exclusive scan = row-item offsets (single pass, warp
-// look-back), and the first Gaussian of every row-item chunk.
+// Row 5b (1/6): tile rows per Gaussian (ny of its pixel AABB) in canonical
+// order -> their exclusive scan = row-item offsets, and the first Gaussian of
+// every row-item chunk.  Three non-blocking passes: k_bin_count (per partition
+// of kScanNT Gaussians: the ny total, the band constants of the tile cover and
+// the per-tile-row item counts), k_count_scan over the partitions, then
+// k_bin_offsets (block scan + partition base).
 constexpr int kScanNT = 256;     // threads (= items) per scan partition
 constexpr int kItemTile = kScanNT;  // row items per chunk / partition
-__global__ void __launch_bounds__(kScanNT) k_bin_scan(const uint2 *__restrict__ rects, const uint32_t *__restrict__ order,
-                                                   const float4 *__restrict__ rec0, const float4 *__restrict__ rec1,
-                                                   const Counters *ctrc, uint32_t *ticket, uint32_t *lb,
-                                                   uint32_t *__restrict__ off, uint32_t *__restrict__ chunk_first,
-                                                   uint32_t max_chunks, uint32_t *n_items,
-                                                   BandConsts *__restrict__ bconst, int *__restrict__ rowdiff,
-                                                   int tiles_y) {
-    __shared__ uint32_t s_w[32];
-    __shared__ uint32_t s_part, s_excl;
+__global__ void __launch_bounds__(kScanNT) k_bin_count(const uint2 *__restrict__ rects,
+                                                       const uint32_t *__restrict__ order,
+                                                       const float4 *__restrict__ rec0,
+                                                       const float4 *__restrict__ rec1, const Counters *ctrc,
+                                                       BandConsts *__restrict__ bconst, int *__restrict__ rowdiff,
+                                                       int tiles_y, uint32_t *__restrict__ pcnt) {
     __shared__ int s_rdiff[kMaxTilesY + 1];
+    __shared__ uint32_t s_tot;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint32_t n = ctrc->n_vis;
+    const uint32_t parts = (n + kScanNT - 1) / kScanNT;
+    for (uint32_t part = blockIdx.x; part < parts; part += gridDim.x) {
+        for (int k = tid; k <= tiles_y; k += blockDim.x) s_rdiff[k] = 0;
+        if (tid == 0) s_tot = 0;
+        __syncthreads();
+        const uint32_t i = part * kScanNT + tid;
+        uint32_t c = 0;
+        if (i < n) {
+            const uint2 rc = __ldg(rects + i);
+            const TileRect tr = tile_rect(rc);
+            c = (uint32_t)tr.ny;
+            atomicAdd(&s_rdiff[tr.ty0], 1);  // row-item counts per tile row (1D diff), block-aggregated
+            atomicAdd(&s_rdiff[tr.ty0 + tr.ny], -1);
+            const uint32_t v = __ldg(order + i);
+            const float4 a = __ldg(rec0 + v), b = __ldg(rec1 + v);
+            bconst[i] = band_consts(a.x, a.y, a.z, a.w, b.x, b.y, rc.x & 0xffff, rc.x >> 16, rc.y & 0xffff,
+                                    rc.y >> 16);
+        }
+        uint32_t w = c;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+        if (lane == 0 && w) atomicAdd(&s_tot, w);
+        __syncthreads();
+        for (int k = tid; k <= tiles_y; k += blockDim.x)
+            if (s_rdiff[k]) atomicAdd(&rowdiff[k], s_rdiff[k]);
+        if (tid == 0) pcnt[part] = s_tot;
+        __syncthreads();
+    }
+}
+
+// Row 5b (1b/6): per partition, the block scan of ny plus the partition's base
+// -> off[i]; chunk_first[k] = the Gaussian owning row item k * kItemTile.
+__global__ void __launch_bounds__(kScanNT) k_bin_offsets(const uint2 *__restrict__ rects, const Counters *ctrc,
+                                                         const uint32_t *__restrict__ pbase,
+                                                         uint32_t *__restrict__ off,
+                                                         uint32_t *__restrict__ chunk_first, uint32_t max_chunks) {
+    __shared__ uint32_t s_w[kScanNT / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t n = ctrc->n_vis;
-    if (tid == 0) s_part = atomicAdd(ticket, 1u);
-    for (int k = tid; k <= tiles_y; k += blockDim.x) s_rdiff[k] = 0;
-    __syncthreads();
-    const uint32_t part = s_part;
-    if (part * kScanNT >= n) return;
-    const uint32_t i = part * kScanNT + tid;
-    uint32_t c = 0;
-    if (i < n) {
-        const uint2 rc = __ldg(rects + i);
-        const TileRect tr = tile_rect(rc);
-        c = (uint32_t)tr.ny;
-        atomicAdd(&s_rdiff[tr.ty0], 1);            // row-item counts per tile row (1D diff), block-aggregated
-        atomicAdd(&s_rdiff[tr.ty0 + tr.ny], -1);
-        const uint32_t v = __ldg(order + i);
-        const float4 a = __ldg(rec0 + v), b = __ldg(rec1 + v);
-        bconst[i] = band_consts(a.x, a.y, a.z, a.w, b.x, b.y, rc.x & 0xffff, rc.x >> 16, rc.y & 0xffff, rc.y >> 16);
-    }
-    uint32_t incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_w[warp] = incl;
-    __syncthreads();
-    for (int k = tid; k <= tiles_y; k += blockDim.x)
-        if (s_rdiff[k]) atomicAdd(&rowdiff[k], s_rdiff[k]);
-    if (warp == 0) {
-        uint32_t w = lane < kScanNT / 32 ? s_w[lane] : 0u, wi = w;
+    const uint32_t parts = (n + kScanNT - 1) / kScanNT;
+    for (uint32_t part = blockIdx.x; part < parts; part += gridDim.x) {
+        const uint32_t i = part * kScanNT + tid;
+        const uint32_t c = i < n ? (uint32_t)tile_rect(__ldg(rects + i)).ny : 0u;
+        uint32_t incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= o) wi += y;
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
         }
-        if (lane < kScanNT / 32) s_w[lane] = wi - w;
-        const uint32_t tot = __shfl_sync(0xffffffffu, wi, 31);
-        const uint32_t excl = lookback_warp(lb, part, tot, lane);
-        if (lane == 0) {
-            s_excl = excl;
-            if ((part + 1) * kScanNT >= n) *n_items = excl + tot;  // last partition
+        if (lane == 31) s_w[warp] = incl;
+        __syncthreads();
+        uint32_t wbase = __ldg(pbase + part);
+        for (int k = 0; k < warp; ++k) wbase += s_w[k];
+        if (i < n) {
+            const uint32_t o = wbase + incl - c;
+            off[i] = o;
+            for (uint32_t k = (o + kItemTile - 1) / kItemTile; k * kItemTile < o + c && k < max_chunks; ++k)
+                chunk_first[k] = i;
         }
-    }
-    __syncthreads();
-    if (i < n) {
-        const uint32_t o = s_excl + s_w[warp] + incl - c;
-        off[i] = o;
-        for (uint32_t k = (o + kItemTile - 1) / kItemTile; k * kItemTile < o + c && k < max_chunks; ++k)
-            chunk_first[k] = i;
+        __syncthreads();
     }
 }
 
@@ -1627,15 +1640,19 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         uint32_t *ival[2] = {reinterpret_cast<uint32_t *>(ws + L.eval0), reinterpret_cast<uint32_t *>(ws + L.eval1)};
         uint32_t *ipack = reinterpret_cast<uint32_t *>(ws + L.item_pack);
         uint32_t *iv = reinterpret_cast<uint32_t *>(ws + L.item_v);
-        uint32_t *elb = reinterpret_cast<uint32_t *>(ws + L.emit_lb);
         uint32_t *rhist = reinterpret_cast<uint32_t *>(ws + L.row_hist);
         uint64_t *tstat = reinterpret_cast<uint64_t *>(ws + L.tile_status);
         BandConsts *bconst = reinterpret_cast<BandConsts *>(ws + L.band_consts);
         const uint32_t item_chunks = (uint32_t)((L.max_entries + kItemTile - 1) / kItemTile);
-        k_bin_scan<<<std::max(1, (L.n + kScanNT - 1) / kScanNT), kScanNT, 0, st>>>(rect_sorted, order, rec0, rec1, ctr,
-                                                                                 &ctr->bin_ticket, elb, roff, rcfirst,
-                                                                                 item_chunks, &ctr->n_items, bconst,
-                                                                                 rowdiff, L.tiles_y);
+        {
+            uint32_t *pcnt = reinterpret_cast<uint32_t *>(ws + L.emit_lb);  // items per k_bin_count partition
+            const int bparts = std::max(1, (L.n + kScanNT - 1) / kScanNT);
+            const int bgrid = std::min(bparts, 8 * L.p_sort);
+            k_bin_count<<<bgrid, kScanNT, 0, st>>>(rect_sorted, order, rec0, rec1, ctr, bconst, rowdiff, L.tiles_y,
+                                                   pcnt);
+            k_count_scan<<<1, 1024, 0, st>>>(pcnt, bparts, &ctr->n_vis, kScanNT, &ctr->n_items);
+            k_bin_offsets<<<bgrid, kScanNT, 0, st>>>(rect_sorted, ctr, pcnt, roff, rcfirst, item_chunks);
+        }
         k_row_items<<<(int)std::min<uint32_t>(item_chunks, 8 * L.p_sort), kScanNT, 0, st>>>(
             rect_sorted, order, rec0, rec1, bconst, roff, rcfirst, ctr, &ctr->n_items, L.tiles_x, diff, ikey[0], ipack,
             iv, (uint32_t)L.max_entries);
