@@ -600,8 +600,8 @@ __global__ void __launch_bounds__(kScanNT) k_row_items(const uint2 *__restrict__
                                                        const BandConsts *__restrict__ bconst,
                                                        const uint32_t *__restrict__ roff,
                                                        const uint32_t *__restrict__ rchunk_first,
-                                                       const Counters *ctrc, const uint32_t *n_items_ptr, int tiles_x,
-                                                       int *__restrict__ diff, uint32_t *__restrict__ item_key,
+                                                       const Counters *ctrc, const uint32_t *n_items_ptr,
+                                                       uint32_t *__restrict__ item_key,
                                                        uint32_t *__restrict__ item_pack, uint32_t *__restrict__ item_v,
                                                        uint32_t item_cap) {
     __shared__ uint32_t s_off[kItemTile + 1];
@@ -632,11 +632,8 @@ __global__ void __launch_bounds__(kScanNT) k_row_items(const uint2 *__restrict__
             const float4 a = __ldg(rec0 + v), b = __ldg(rec1 + v);
             int txa, txb;
             uint32_t pack = 0u;  // empty row: txb + 1 <= txa
-            if (band_tiles(bconst[r], a.x, a.y, a.z, a.w, b.x, px0, px1, py0, py1, ty, txa, txb)) {
+            if (band_tiles(bconst[r], a.x, a.y, a.z, a.w, b.x, px0, px1, py0, py1, ty, txa, txb))
                 pack = (uint32_t)txa | ((uint32_t)(txb + 1) << 16);
-                atomicAdd(&diff[ty * (tiles_x + 1) + txa], 1);
-                atomicAdd(&diff[ty * (tiles_x + 1) + txb + 1], -1);
-            }
             item_key[i] = (uint32_t)ty;
             item_pack[i] = pack;
             item_v[i] = v;
@@ -645,60 +642,52 @@ __global__ void __launch_bounds__(kScanNT) k_row_items(const uint2 *__restrict__
     }
 }
 
-// Row 5b (3/6), one block: per-row prefix of the tile difference array ->
-// per-tile counts -> tile_start[0..T] and E (capacity check); prefix of the
-// row-item difference array -> row_start[0..tiles_y] and the exclusive digit
-// bases of the row partition passes (digit ty & 255, then ty >> 8).
-__global__ void __launch_bounds__(1024) k_tile_scan(const int *__restrict__ diff, const int *__restrict__ rowdiff,
-                                                    int tiles_x, int tiles_y, uint32_t *__restrict__ tile_start,
-                                                    uint32_t *__restrict__ row_start, uint32_t *__restrict__ rbase,
-                                                    Counters *ctr, int64_t max_entries) {
-    extern __shared__ int sm[];  // tiles_y x (tiles_x + 1)
+// Row 5b (3/6), one thread: prefix of the row-item difference array ->
+// row_start[0..tiles_y] and the exclusive digit bases of the row partition
+// passes (digit ty & 255, then ty >> 8).
+__global__ void k_row_scan(const int *__restrict__ rowdiff, int tiles_y, uint32_t *__restrict__ row_start,
+                           uint32_t *__restrict__ rbase) {
+    __shared__ uint32_t s_rows[kMaxTilesY + 1];
+    if (threadIdx.x != 0) return;
+    int run = 0;
+    uint32_t start = 0, hi1 = 0;
+    for (int y = 0; y < tiles_y; ++y) {
+        run += __ldcg(rowdiff + y);  // items in row y
+        row_start[y] = start;
+        start += (uint32_t)run;
+        if (y < 256) hi1 += (uint32_t)run;
+        s_rows[y] = (uint32_t)run;
+    }
+    row_start[tiles_y] = start;
+    uint32_t acc = 0;
+    for (int d = 0; d < 256; ++d) {  // pass 0: digit = ty & 255
+        rbase[d] = acc;
+        acc += (d < tiles_y ? s_rows[d] : 0u) + (d + 256 < tiles_y ? s_rows[d + 256] : 0u);
+    }
+    rbase[256] = 0;  // pass 1: digit = ty >> 8 (0 or 1)
+    rbase[257] = hi1;
+}
+
+// Row 5b (5/6), one block: per-tile entry counts = sums over the row
+// segments of k_row_count's histograms -> tile_start[0..T] and E (capacity
+// check before the scatter writes any entry).
+__global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t *__restrict__ hist, int tiles_x, int tiles_y,
+                                                    uint32_t *__restrict__ tile_start, Counters *ctr,
+                                                    int64_t max_entries) {
     __shared__ uint32_t s_sum[1024];
-    __shared__ uint32_t s_rows[512 + 1];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int gx = tiles_x + 1, T = tiles_x * tiles_y;
-    for (int k = tid; k < gx * tiles_y; k += blockDim.x) sm[k] = __ldcg(diff + k);
-    if (tid <= tiles_y) s_rows[tid] = (uint32_t)__ldcg(rowdiff + tid);
-    __syncthreads();
-    for (int y = warp; y < tiles_y; y += 32) {  // row prefix, one warp per row
-        int run = 0;
-        for (int x0 = 0; x0 < tiles_x; x0 += 32) {
-            const int x = x0 + lane;
-            int val = x < tiles_x ? sm[y * gx + x] : 0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, val, o);
-                if (lane >= o) val += t;
-            }
-            if (x < tiles_x) sm[y * gx + x] = run + val;
-            run += __shfl_sync(0xffffffffu, val, 31);
-        }
-    }
-    if (tid == 1023) {  // row-item counts per tile row -> row starts and digit bases
-        int run = 0;
-        uint32_t start = 0, hi1 = 0;
-        for (int y = 0; y < tiles_y; ++y) {
-            run += (int)s_rows[y];          // items in row y
-            row_start[y] = start;
-            start += (uint32_t)run;
-            if (y < 256) hi1 += (uint32_t)run;
-            s_rows[y] = (uint32_t)run;
-        }
-        row_start[tiles_y] = start;
-        uint32_t acc = 0;
-        for (int d = 0; d < 256; ++d) {  // pass 0: digit = ty & 255
-            rbase[d] = acc;
-            acc += (d < tiles_y ? s_rows[d] : 0u) + (d + 256 < tiles_y ? s_rows[d + 256] : 0u);
-        }
-        rbase[256] = 0;  // pass 1: digit = ty >> 8 (0 or 1)
-        rbase[257] = hi1;
-    }
-    __syncthreads();
+    const int tid = threadIdx.x;
+    const int T = tiles_x * tiles_y;
     const int chunk = (T + 1023) / 1024;
     const int k0 = min(tid * chunk, T), k1 = min(k0 + chunk, T);
+    auto count = [&](int k) {
+        const int ty = k / tiles_x, tx = k - ty * tiles_x;
+        uint32_t c = 0;
+#pragma unroll 4
+        for (int sg = 0; sg < kRowSeg; ++sg) c += __ldcg(hist + ((size_t)ty * kRowSeg + sg) * tiles_x + tx);
+        return c;
+    };
     uint32_t local = 0;
-    for (int k = k0; k < k1; ++k) local += (uint32_t)sm[(k / tiles_x) * gx + (k % tiles_x)];
+    for (int k = k0; k < k1; ++k) local += count(k);
     s_sum[tid] = local;
     __syncthreads();
     for (int off = 1; off < 1024; off <<= 1) {
@@ -710,7 +699,7 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const int *__restrict__ diff
     uint32_t run = s_sum[tid] - local;
     for (int k = k0; k < k1; ++k) {
         tile_start[k] = run;
-        run += (uint32_t)sm[(k / tiles_x) * gx + (k % tiles_x)];
+        run += count(k);
     }
     if (tid == 1023) {
         const uint32_t E = s_sum[1023];
@@ -1630,7 +1619,6 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         }
         const uint32_t *order = vals[1];
         if (ev && (e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
-        int *diff = reinterpret_cast<int *>(ws + L.tile_diff);
         int *rowdiff = reinterpret_cast<int *>(ws + L.row_diff);
         uint32_t *rbase = reinterpret_cast<uint32_t *>(ws + L.tile_gbase);  // [0..255] pass 0, [256..511] pass 1
         uint32_t *row_start = reinterpret_cast<uint32_t *>(ws + L.row_start);
@@ -1654,11 +1642,9 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
             k_bin_offsets<<<bgrid, kScanNT, 0, st>>>(rect_sorted, ctr, pcnt, roff, rcfirst, item_chunks);
         }
         k_row_items<<<(int)std::min<uint32_t>(item_chunks, 8 * L.p_sort), kScanNT, 0, st>>>(
-            rect_sorted, order, rec0, rec1, bconst, roff, rcfirst, ctr, &ctr->n_items, L.tiles_x, diff, ikey[0], ipack,
-            iv, (uint32_t)L.max_entries);
-        const size_t scan_smem = sizeof(int) * (size_t)(L.tiles_x + 1) * (L.tiles_y + 1);
-        k_tile_scan<<<1, 1024, scan_smem, st>>>(diff, rowdiff, L.tiles_x, L.tiles_y, tstart, row_start, rbase, ctr,
-                                                L.max_entries);
+            rect_sorted, order, rec0, rec1, bconst, roff, rcfirst, ctr, &ctr->n_items, ikey[0], ipack, iv,
+            (uint32_t)L.max_entries);
+        k_row_scan<<<1, 32, 0, st>>>(rowdiff, L.tiles_y, row_start, rbase);
         // stable partition of the row items by tile row (canonical order kept within a row)
         const int rgrid = std::min((int)item_chunks, tune_pgrid() * L.p_sort);
         const uint32_t *sorted_items = ival[0];
@@ -1675,6 +1661,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         const size_t cnt_smem = sizeof(uint32_t) * (size_t)kRowWarps * L.tiles_x;
         k_row_count<<<nrb, 256, sizeof(int) * (L.tiles_x + 1), st>>>(sorted_items, ipack, row_start, L.tiles_x, rhist,
                                                                       ctr);
+        k_tile_scan<<<1, 1024, 0, st>>>(rhist, L.tiles_x, L.tiles_y, tstart, ctr, L.max_entries);
         k_row_scatter<<<nrb, 32 * kRowWarps, cnt_smem + sizeof(uint32_t) * L.tiles_x, st>>>(
             sorted_items, ipack, iv, row_start, L.tiles_x, rhist, tstart, entries, ctr);
     }
@@ -1719,8 +1706,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
 
 // Opt-in to large dynamic shared memory once per process.
 __host__ cudaError_t render_set_smem_attrs() {
-    cudaError_t e = cudaFuncSetAttribute(k_tile_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_row_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_row_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_row_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     return e;
 }
