@@ -557,11 +557,12 @@ __global__ void __launch_bounds__(kScanNT) k_bin_count(const uint2 *__restrict__
 }
 
 // Row 5b (1b/6): per partition, the block scan of ny plus the partition's base
-// -> off[i]; chunk_first[k] = the Gaussian owning row item k * kItemTile.
+// -> the item offset o of Gaussian i; its row items o .. o+ny-1 are expanded
+// here (row key ty and owner i), so k_row_items needs no search.
 __global__ void __launch_bounds__(kScanNT) k_bin_offsets(const uint2 *__restrict__ rects, const Counters *ctrc,
                                                          const uint32_t *__restrict__ pbase,
-                                                         uint32_t *__restrict__ off,
-                                                         uint32_t *__restrict__ chunk_first, uint32_t max_chunks) {
+                                                         uint32_t *__restrict__ item_key,
+                                                         uint32_t *__restrict__ item_owner, uint32_t item_cap) {
     __shared__ uint32_t s_w[kScanNT / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t n = ctrc->n_vis;
@@ -579,11 +580,13 @@ __global__ void __launch_bounds__(kScanNT) k_bin_offsets(const uint2 *__restrict
         __syncthreads();
         uint32_t wbase = __ldg(pbase + part);
         for (int k = 0; k < warp; ++k) wbase += s_w[k];
-        if (i < n) {
+        if (i < n) {  // expand: row items o .. o+c-1 of Gaussian i (rows ty0 ..), within the capacity
             const uint32_t o = wbase + incl - c;
-            off[i] = o;
-            for (uint32_t k = (o + kItemTile - 1) / kItemTile; k * kItemTile < o + c && k < max_chunks; ++k)
-                chunk_first[k] = i;
+            const int ty0 = tile_rect(__ldg(rects + i)).ty0;
+            for (uint32_t k = 0; k < c && o + k < item_cap; ++k) {
+                item_key[o + k] = (uint32_t)(ty0 + (int)k);
+                item_owner[o + k] = i;
+            }
         }
         __syncthreads();
     }
@@ -597,48 +600,29 @@ __global__ void __launch_bounds__(kScanNT) k_row_items(const uint2 *__restrict__
                                                        const uint32_t *__restrict__ order,
                                                        const float4 *__restrict__ rec0,
                                                        const float4 *__restrict__ rec1,
-                                                       const BandConsts *__restrict__ bconst,
-                                                       const uint32_t *__restrict__ roff,
-                                                       const uint32_t *__restrict__ rchunk_first,
-                                                       const Counters *ctrc, const uint32_t *n_items_ptr,
-                                                       uint32_t *__restrict__ item_key,
+                                                       const BandConsts *__restrict__ bconst, const Counters *ctrc,
+                                                       const uint32_t *n_items_ptr,
+                                                       const uint32_t *__restrict__ item_key,
                                                        uint32_t *__restrict__ item_pack, uint32_t *__restrict__ item_v,
                                                        uint32_t item_cap) {
-    __shared__ uint32_t s_off[kItemTile + 1];
-    const int tid = threadIdx.x;
-    const uint32_t n = ctrc->n_vis, ni = *n_items_ptr;
+    const uint32_t ni = *n_items_ptr;
     if (ni > item_cap) {  // more row items than the workspace holds
-        if (blockIdx.x == 0 && tid == 0) const_cast<Counters *>(ctrc)->status = FDGS_ERR_OVERFLOW;
+        if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<Counters *>(ctrc)->status = FDGS_ERR_OVERFLOW;
         return;
     }
-    for (uint32_t part = blockIdx.x; part * kItemTile < ni; part += gridDim.x) {
-        // window of Gaussians owning this chunk's items (each owns >= 1 item)
-        const uint32_t r0 = __ldg(rchunk_first + part);
-        const uint32_t m = min((uint32_t)kItemTile, n - r0);
-        for (uint32_t q = tid; q < m; q += blockDim.x) s_off[q] = __ldg(roff + r0 + q);
-        __syncthreads();
-        const uint32_t i = part * kItemTile + tid;
-        if (i < ni) {
-            int lo = 0, hi = (int)m - 1;  // largest q with s_off[q] <= i
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (s_off[mid] <= i) lo = mid; else hi = mid - 1;
-            }
-            const uint32_t r = r0 + lo;
-            const uint2 rc = __ldg(rects + r);
-            const int px0 = rc.x & 0xffff, px1 = rc.x >> 16, py0 = rc.y & 0xffff, py1 = rc.y >> 16;
-            const int ty = (py0 >> 4) + (int)(i - s_off[lo]);
-            const uint32_t v = __ldg(order + r);
-            const float4 a = __ldg(rec0 + v), b = __ldg(rec1 + v);
-            int txa, txb;
-            uint32_t pack = 0u;  // empty row: txb + 1 <= txa
-            if (band_tiles(bconst[r], a.x, a.y, a.z, a.w, b.x, px0, px1, py0, py1, ty, txa, txb))
-                pack = (uint32_t)txa | ((uint32_t)(txb + 1) << 16);
-            item_key[i] = (uint32_t)ty;
-            item_pack[i] = pack;
-            item_v[i] = v;
-        }
-        __syncthreads();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ni; i += gridDim.x * blockDim.x) {
+        const uint32_t r = __ldg(item_v + i);  // owning Gaussian (canonical rank), from k_bin_offsets
+        const int ty = (int)__ldg(item_key + i);
+        const uint2 rc = __ldg(rects + r);
+        const int px0 = rc.x & 0xffff, px1 = rc.x >> 16, py0 = rc.y & 0xffff, py1 = rc.y >> 16;
+        const uint32_t v = __ldg(order + r);
+        const float4 a = __ldg(rec0 + v), b = __ldg(rec1 + v);
+        int txa, txb;
+        uint32_t pack = 0u;  // empty row: txb + 1 <= txa
+        if (band_tiles(bconst[r], a.x, a.y, a.z, a.w, b.x, px0, px1, py0, py1, ty, txa, txb))
+            pack = (uint32_t)txa | ((uint32_t)(txb + 1) << 16);
+        item_pack[i] = pack;
+        item_v[i] = v;  // the owner index is replaced by the record slot
     }
 }
 
@@ -1622,8 +1606,6 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         int *rowdiff = reinterpret_cast<int *>(ws + L.row_diff);
         uint32_t *rbase = reinterpret_cast<uint32_t *>(ws + L.tile_gbase);  // [0..255] pass 0, [256..511] pass 1
         uint32_t *row_start = reinterpret_cast<uint32_t *>(ws + L.row_start);
-        uint32_t *roff = reinterpret_cast<uint32_t *>(ws + L.roff);
-        uint32_t *rcfirst = reinterpret_cast<uint32_t *>(ws + L.rchunk_first);
         uint32_t *ikey[2] = {reinterpret_cast<uint32_t *>(ws + L.ekey0), reinterpret_cast<uint32_t *>(ws + L.ekey1)};
         uint32_t *ival[2] = {reinterpret_cast<uint32_t *>(ws + L.eval0), reinterpret_cast<uint32_t *>(ws + L.eval1)};
         uint32_t *ipack = reinterpret_cast<uint32_t *>(ws + L.item_pack);
@@ -1639,11 +1621,10 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
             k_bin_count<<<bgrid, kScanNT, 0, st>>>(rect_sorted, order, rec0, rec1, ctr, bconst, rowdiff, L.tiles_y,
                                                    pcnt);
             k_count_scan<<<1, 1024, 0, st>>>(pcnt, bparts, &ctr->n_vis, kScanNT, &ctr->n_items);
-            k_bin_offsets<<<bgrid, kScanNT, 0, st>>>(rect_sorted, ctr, pcnt, roff, rcfirst, item_chunks);
+            k_bin_offsets<<<bgrid, kScanNT, 0, st>>>(rect_sorted, ctr, pcnt, ikey[0], iv, (uint32_t)L.max_entries);
         }
         k_row_items<<<(int)std::min<uint32_t>(item_chunks, 8 * L.p_sort), kScanNT, 0, st>>>(
-            rect_sorted, order, rec0, rec1, bconst, roff, rcfirst, ctr, &ctr->n_items, ikey[0], ipack, iv,
-            (uint32_t)L.max_entries);
+            rect_sorted, order, rec0, rec1, bconst, ctr, &ctr->n_items, ikey[0], ipack, iv, (uint32_t)L.max_entries);
         k_row_scan<<<1, 32, 0, st>>>(rowdiff, L.tiles_y, row_start, rbase);
         // stable partition of the row items by tile row (canonical order kept within a row)
         const int rgrid = std::min((int)item_chunks, tune_pgrid() * L.p_sort);
