@@ -1354,8 +1354,17 @@ __device__ __forceinline__ bool box_reach(float Ap, float Bp, float Cp, float Q2
     return best >= -(1e-3f * mag + 1e-3f);
 }
 
+// Footprint of consumer warp w in the tile: FDGS_WL_QUAD=0: 4 rows x 16
+// columns (strips); 1: 8 x 8 quadrants (tighter boxes for the reach test).
+#ifndef FDGS_WL_QUAD
+#define FDGS_WL_QUAD 0
+#endif
+constexpr int kWlRows = FDGS_WL_QUAD ? 8 : 4, kWlCols = FDGS_WL_QUAD ? 8 : 16;
+__host__ __device__ constexpr int wl_row0(int w) { return FDGS_WL_QUAD ? 8 * (w >> 1) : 4 * w; }
+__host__ __device__ constexpr int wl_col0(int w) { return FDGS_WL_QUAD ? 8 * (w & 1) : 0; }
+
 // Producer staging of k_blend_wl: the complemented pixel-AABB mask (per-pixel
-// decision) and a 4-bit mask of the consumer warps (4-row groups of the tile)
+// decision) and a 4-bit mask of the consumer warps (their footprints in the tile)
 // whose pixel-centre box within the AABB the margin-inflated ellipse reaches.
 __device__ __forceinline__ uint32_t stage_groups(int tx, int ty, const float4 &r0, const float4 &r1,
                                                  uint32_t &mbits) {
@@ -1367,12 +1376,13 @@ __device__ __forceinline__ uint32_t stage_groups(int tx, int ty, const float4 &r
     mbits = ~(xm | (ym << 16));
     const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
     const float hA = __fdividef(-0.5f, Ap), hC = __fdividef(-0.5f, Cp);  // stationary points only
-    const float xl = (float)(tx * 16 + x0) + 0.5f - u, xr = (float)(tx * 16 + x1) + 0.5f - u;
     uint32_t g = 0;
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-        const int ra = max(y0, 4 * w), rb = min(y1, 4 * w + 3);
-        if (ra > rb) continue;
+        const int ra = max(y0, wl_row0(w)), rb = min(y1, wl_row0(w) + kWlRows - 1);
+        const int ca = max(x0, wl_col0(w)), cb = min(x1, wl_col0(w) + kWlCols - 1);
+        if (ra > rb || ca > cb) continue;
+        const float xl = (float)(tx * 16 + ca) + 0.5f - u, xr = (float)(tx * 16 + cb) + 0.5f - u;
         const float yl = (float)(ty * 16 + ra) + 0.5f - v, yr = (float)(ty * 16 + rb) + 0.5f - v;
         if (box_reach(Ap, Bp, Cp, Q2, hA, hC, xl, xr, yl, yr)) g |= 1u << w;
     }
@@ -1384,11 +1394,11 @@ __device__ __forceinline__ uint32_t stage_groups(int tx, int ty, const float4 &r
 #endif
 constexpr int kWlBuf = FDGS_WL_BUF;
 struct WlEntry {
-    float4 a;      // u, A', ~AABB mask bits, r
-    float4 c;      // g, b, q (record of the batch, kContrib bookkeeping), -
-    float2 t[4];   // {t1, t4} of the warp's rows 4w .. 4w+3
+    float4 a;            // u, A', ~AABB mask bits, r
+    float4 c;            // g, b, q (record of the batch), -
+    float2 t[kWlRows];   // {t1, t4} of the warp's rows
 };
-static_assert(sizeof(WlEntry) == 64, "WlEntry layout");
+static_assert(sizeof(WlEntry) == 32 + 8 * kWlRows, "WlEntry layout");
 
 #ifndef FDGS_WL_MINB
 #define FDGS_WL_MINB 7
@@ -1451,8 +1461,8 @@ __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uin
                     E.a = make_float4(u, Ap, mbits, r2.x);
                     E.c = make_float4(r2.y, r2.z, __int_as_float(lane), 0.f);
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) {  // pinned e2 chain, row terms (DESIGN.md step 10)
-                        const float dy = __fsub_rn((float)(ty * 16 + 4 * w + r) + 0.5f, v);
+                    for (int r = 0; r < kWlRows; ++r) {  // pinned e2 chain, row terms (DESIGN.md step 10)
+                        const float dy = __fsub_rn((float)(ty * 16 + wl_row0(w) + r) + 0.5f, v);
                         const float t1 = __fmul_rn(Bp, dy);
                         const float t3 = __fmul_rn(Cp, dy);
                         E.t[r] = make_float2(t1, __fmaf_rn(t3, dy, Q2));
@@ -1465,7 +1475,8 @@ __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uin
             if (n == 0) break;
         }
     } else {  // --------------------------------------------------------- consumers
-        const int ly = tid >> 3, lx = (tid & 7) * 2, rr = ly & 3;
+        // 2 horizontally adjacent pixels per thread; the warp covers its footprint
+        const int rr = lane / (kWlCols / 2), ly = wl_row0(warp) + rr, lx = wl_col0(warp) + (lane % (kWlCols / 2)) * 2;
         const int i0 = tx * 16 + lx, j = ty * 16 + ly;
         const bool in0 = i0 < width && j < height, in1 = i0 + 1 < width && j < height;
         float2 px = make_float2((float)i0 + 0.5f, (float)(i0 + 1) + 0.5f);
