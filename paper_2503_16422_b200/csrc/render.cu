@@ -626,36 +626,68 @@ __global__ void __launch_bounds__(kScanNT) k_row_items(const uint2 *__restrict__
     }
 }
 
-// Row 5b (3/6), one thread: prefix of the row-item difference array ->
+// Row 5b (3/6), one warp: prefix of the row-item difference array ->
 // row_start[0..tiles_y] and the exclusive digit bases of the row partition
 // passes (digit ty & 255, then ty >> 8).
 __global__ void k_row_scan(const int *__restrict__ rowdiff, int tiles_y, uint32_t *__restrict__ row_start,
                            uint32_t *__restrict__ rbase) {
     __shared__ uint32_t s_rows[kMaxTilesY + 1];
-    if (threadIdx.x != 0) return;
+    const int lane = threadIdx.x;  // one warp
+    // items per row = prefix of the difference array; row starts = prefix of the items
     int run = 0;
-    uint32_t start = 0, hi1 = 0;
-    for (int y = 0; y < tiles_y; ++y) {
-        run += __ldcg(rowdiff + y);  // items in row y
-        row_start[y] = start;
-        start += (uint32_t)run;
-        if (y < 256) hi1 += (uint32_t)run;
-        s_rows[y] = (uint32_t)run;
+    uint32_t start = 0;
+    for (int y0 = 0; y0 < tiles_y; y0 += 32) {
+        const int y = y0 + lane;
+        int d = y < tiles_y ? __ldcg(rowdiff + y) : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, d, o);
+            if (lane >= o) d += t;
+        }
+        const uint32_t items = (uint32_t)(run + d);
+        uint32_t inc = y < tiles_y ? items : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (y < tiles_y) {
+            s_rows[y] = items;
+            row_start[y] = start + inc - items;
+        }
+        run += __shfl_sync(0xffffffffu, d, 31);
+        start += __shfl_sync(0xffffffffu, inc, 31);
     }
-    row_start[tiles_y] = start;
+    if (lane == 0) row_start[tiles_y] = start;
+    __syncwarp();
+    // digit bases of the row partition: pass 0 digit = ty & 255, pass 1 digit = ty >> 8
+    uint32_t hi1 = 0;
+    for (int y = lane; y < min(tiles_y, 256); y += 32) hi1 += s_rows[y];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) hi1 += __shfl_xor_sync(0xffffffffu, hi1, o);
     uint32_t acc = 0;
-    for (int d = 0; d < 256; ++d) {  // pass 0: digit = ty & 255
-        rbase[d] = acc;
-        acc += (d < tiles_y ? s_rows[d] : 0u) + (d + 256 < tiles_y ? s_rows[d + 256] : 0u);
+    for (int d0 = 0; d0 < 256; d0 += 32) {
+        const int d = d0 + lane;
+        const uint32_t c = (d < tiles_y ? s_rows[d] : 0u) + (d + 256 < tiles_y ? s_rows[d + 256] : 0u);
+        uint32_t inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        rbase[d] = acc + inc - c;
+        acc += __shfl_sync(0xffffffffu, inc, 31);
     }
-    rbase[256] = 0;  // pass 1: digit = ty >> 8 (0 or 1)
-    rbase[257] = hi1;
+    if (lane == 0) {
+        rbase[256] = 0;
+        rbase[257] = hi1;
+    }
 }
 
-// Row 5b (5/6), one block: per-tile entry counts = sums over the row
-// segments of k_row_count's histograms -> tile_start[0..T] and E (capacity
-// check before the scatter writes any entry).
-__global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t *__restrict__ hist, int tiles_x, int tiles_y,
+// Row 5b (5/6), one block: per-tile entry counts (summed over the row
+// segments by k_row_count) -> tile_start[0..T] and E (capacity check before
+// the scatter writes any entry).
+__global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t *__restrict__ tile_cnt, int tiles_x, int tiles_y,
                                                     uint32_t *__restrict__ tile_start, Counters *ctr,
                                                     int64_t max_entries) {
     __shared__ uint32_t s_sum[1024];
@@ -663,13 +695,7 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t *__restrict__
     const int T = tiles_x * tiles_y;
     const int chunk = (T + 1023) / 1024;
     const int k0 = min(tid * chunk, T), k1 = min(k0 + chunk, T);
-    auto count = [&](int k) {
-        const int ty = k / tiles_x, tx = k - ty * tiles_x;
-        uint32_t c = 0;
-#pragma unroll 4
-        for (int sg = 0; sg < kRowSeg; ++sg) c += __ldcg(hist + ((size_t)ty * kRowSeg + sg) * tiles_x + tx);
-        return c;
-    };
+    auto count = [&](int k) { return __ldcg(tile_cnt + k); };
     uint32_t local = 0;
     for (int k = k0; k < k1; ++k) local += count(k);
     s_sum[tid] = local;
@@ -763,7 +789,8 @@ __device__ __forceinline__ void row_seg_range(const uint32_t *row_start, int ty,
 __global__ void __launch_bounds__(256) k_row_count(const uint32_t *__restrict__ sorted,
                                                    const uint32_t *__restrict__ item_pack,
                                                    const uint32_t *__restrict__ row_start, int tiles_x,
-                                                   uint32_t *__restrict__ hist, const Counters *ctrc) {
+                                                   uint32_t *__restrict__ hist, uint32_t *__restrict__ tile_cnt,
+                                                   const Counters *ctrc) {
     extern __shared__ int s_d[];  // [tiles_x + 1]
     const int ty = blockIdx.x / kRowSeg, seg = blockIdx.x % kRowSeg;
     const int tid = threadIdx.x;
@@ -791,7 +818,10 @@ __global__ void __launch_bounds__(256) k_row_count(const uint32_t *__restrict__ 
                 const int t = __shfl_up_sync(0xffffffffu, val, o);
                 if (tid >= o) val += t;
             }
-            if (x < tiles_x) hist[((size_t)ty * kRowSeg + seg) * tiles_x + x] = (uint32_t)(run + val);
+            if (x < tiles_x) {
+                hist[((size_t)ty * kRowSeg + seg) * tiles_x + x] = (uint32_t)(run + val);
+                if (run + val) atomicAdd(&tile_cnt[ty * tiles_x + x], (uint32_t)(run + val));  // per-tile total
+            }
             run += __shfl_sync(0xffffffffu, val, 31);
         }
     }
@@ -1651,9 +1681,10 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         }
         const int nrb = L.tiles_y * kRowSeg;
         const size_t cnt_smem = sizeof(uint32_t) * (size_t)kRowWarps * L.tiles_x;
+        uint32_t *tcnt = reinterpret_cast<uint32_t *>(ws + L.tile_diff);  // per-tile totals (zeroed per frame)
         k_row_count<<<nrb, 256, sizeof(int) * (L.tiles_x + 1), st>>>(sorted_items, ipack, row_start, L.tiles_x, rhist,
-                                                                      ctr);
-        k_tile_scan<<<1, 1024, 0, st>>>(rhist, L.tiles_x, L.tiles_y, tstart, ctr, L.max_entries);
+                                                                      tcnt, ctr);
+        k_tile_scan<<<1, 1024, 0, st>>>(tcnt, L.tiles_x, L.tiles_y, tstart, ctr, L.max_entries);
         k_row_scatter<<<nrb, 32 * kRowWarps, cnt_smem + sizeof(uint32_t) * L.tiles_x, st>>>(
             sorted_items, ipack, iv, row_start, L.tiles_x, rhist, tstart, entries, ctr);
     }
