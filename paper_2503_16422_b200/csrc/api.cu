@@ -66,11 +66,10 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     };
     // cleared per frame
     L.counters = take(sizeof(Counters));
-    L.lookback = take(sizeof(uint32_t) * (size_t)std::max(L.n_parts, 1));
     L.sort_gbase = take(sizeof(uint32_t) * 4 * 256);
-    L.tile_diff = take(sizeof(int) * (size_t)(L.tiles_x + 1) * (L.tiles_y + 1));
+    L.tile_cnt = take(sizeof(uint32_t) * (size_t)L.n_tiles);  // entries per tile (k_row_count totals)
     L.row_diff = take(sizeof(int) * ((size_t)L.tiles_y + 1));
-    L.emit_lb = take(sizeof(uint32_t) * ((nn + 255) / 256));
+    L.bin_cnt = take(sizeof(uint32_t) * ((nn + 255) / 256));  // row items per k_bin_count partition
     L.zero_end = off;
     // persistent (zero-filled once)
     L.epoch = take(sizeof(uint32_t));
@@ -98,8 +97,6 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.row_start = take(sizeof(uint32_t) * ((size_t)L.tiles_y + 1));
     L.row_hist = take(sizeof(uint32_t) * (size_t)L.tiles_y * kRowSeg * L.tiles_x);  // [tiles_y][kRowSeg][tiles_x]
     L.band_consts = take(sizeof(BandConsts) * nn);          // tile-cover constants per Gaussian
-    L.roff = take(4 * nn);                                  // row-item offset per Gaussian
-    L.rchunk_first = take(4 * ((cap + 255) / 256 + 1));      // first Gaussian of each item chunk
     L.item_pack = take(4 * cap);                            // (ty, txa, txb) per row item
     L.item_v = take(4 * cap);                               // visible slot per row item
     L.ekey0 = take(4 * cap);

@@ -31,33 +31,6 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
-// Decoupled look-back, one warp: publish `total` for partition `part`, return
-// the exclusive prefix (all lanes).  Status word = flag(2 bits) | value(30
-// bits); the warp inspects 32 predecessors per round trip.
-__device__ __forceinline__ uint32_t lookback_warp(uint32_t *status, uint32_t part, uint32_t total, int lane) {
-    if (part == 0) {
-        if (lane == 0) st_volatile(&status[0], kFlagP | total);
-        return 0;
-    }
-    if (lane == 0) st_volatile(&status[part], kFlagA | total);
-    uint32_t excl = 0;
-    int base = (int)part - 1;
-    while (true) {
-        const int j = base - lane;
-        uint32_t s = j >= 0 ? ld_volatile(&status[j]) : (kFlagP | 0u);
-        if (__any_sync(0xffffffffu, (s & ~kValMask) == 0)) continue;  // a predecessor is not published yet
-        const uint32_t pmask = __ballot_sync(0xffffffffu, (s & ~kValMask) == kFlagP);
-        const int stop = pmask ? __ffs(pmask) - 1 : 31;
-        uint32_t v = lane <= stop ? (s & kValMask) : 0u;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        excl += v;
-        if (pmask) break;
-        base -= 32;
-    }
-    if (lane == 0) st_volatile(&status[part], kFlagP | (excl + total));
-    return excl;
-}
 
 // ---------------------------------------------------------------- rows 1-4
 // Uniform-work passes instead of one fused kernel whose blocks waited on their
@@ -1656,7 +1629,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         BandConsts *bconst = reinterpret_cast<BandConsts *>(ws + L.band_consts);
         const uint32_t item_chunks = (uint32_t)((L.max_entries + kItemTile - 1) / kItemTile);
         {
-            uint32_t *pcnt = reinterpret_cast<uint32_t *>(ws + L.emit_lb);  // items per k_bin_count partition
+            uint32_t *pcnt = reinterpret_cast<uint32_t *>(ws + L.bin_cnt);  // items per k_bin_count partition
             const int bparts = std::max(1, (L.n + kScanNT - 1) / kScanNT);
             const int bgrid = std::min(bparts, 8 * L.p_sort);
             k_bin_count<<<bgrid, kScanNT, 0, st>>>(rect_sorted, order, rec0, rec1, ctr, bconst, rowdiff, L.tiles_y,
@@ -1681,7 +1654,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         }
         const int nrb = L.tiles_y * kRowSeg;
         const size_t cnt_smem = sizeof(uint32_t) * (size_t)kRowWarps * L.tiles_x;
-        uint32_t *tcnt = reinterpret_cast<uint32_t *>(ws + L.tile_diff);  // per-tile totals (zeroed per frame)
+        uint32_t *tcnt = reinterpret_cast<uint32_t *>(ws + L.tile_cnt);  // per-tile totals (zeroed per frame)
         k_row_count<<<nrb, 256, sizeof(int) * (L.tiles_x + 1), st>>>(sorted_items, ipack, row_start, L.tiles_x, rhist,
                                                                       tcnt, ctr);
         k_tile_scan<<<1, 1024, 0, st>>>(tcnt, L.tiles_x, L.tiles_y, tstart, ctr, L.max_entries);
