@@ -244,13 +244,46 @@ class RenderPipeline:
     def streams(self):
         return self.front + (self.blend or [])
 
-    def render_many(self, frames, outs, stats=None, stage_events=None, stream=None, host_outs=None):
+    def counters_view(self, i: int) -> torch.Tensor:
+        """The 16-byte counter block {n_act, n_vis, n_entries, status} at the head
+        of workspace i (include/fdgs.h fdgs_debug_views.counters)."""
+        r = self.renderers[i]
+        v = FdgsDebugViews()
+        check(lib().fdgs_render_debug_views(_ptr(r.ws), r.ws_bytes, r.scene.n, r.width, r.height, r.max_entries,
+                                            C.byref(v)))
+        off = int(v.counters) - r.ws.data_ptr()
+        return r.ws[off:off + 16]
+
+    def render_many_checked(self, frames, outs, stream=None, host_outs=None):
+        """render_many, then a check of every frame's status: frames that exceeded
+        the tile-entry capacity are re-rendered (synchronously) after growing the
+        workspaces.  Returns the per-frame {n_act, n_vis, n_entries, status}."""
+        main = stream or torch.cuda.current_stream()
+        status = torch.zeros((len(frames), 16), dtype=torch.uint8, device=self.renderers[0].ws.device)
+        self.render_many(frames, outs, stream=main, host_outs=host_outs, status_out=status)
+        main.synchronize()
+        st = status.cpu().view(torch.int32).view(len(frames), 4)
+        bad = [k for k in range(len(frames)) if int(st[k, 3]) != _lib.FDGS_OK]
+        for k in bad:
+            cam, t, ml, mr = frames[k]
+            r = self.renderers[k % self.depth]
+            _, fs = r.render_checked(cam, t, ml, mr, out=outs[k], stream=main)
+            st[k] = torch.tensor([fs.n_act, fs.n_vis, fs.n_entries, fs.status], dtype=torch.int32)
+            if host_outs is not None:
+                host_outs[k].copy_(outs[k])
+        return st
+
+    def render_many(self, frames, outs, stats=None, stage_events=None, stream=None, host_outs=None,
+                    status_out=None):
         """frames: list of (cam, t, mask_l, mask_r); outs: list of output tensors.
         host_outs (optional): pinned host tensors; frame k is copied D2H on a
         copy stream as soon as its blend finishes, overlapping the rendering of
-        later frames.  Ordered after the current work of `stream` (default:
-        current stream), and `stream` waits for every frame (and copy) before
-        continuing.  Async."""
+        later frames.  status_out (optional): uint8 device tensor [len(frames),
+        16] receiving each frame's counter block (an async device copy after
+        its blend; status != 0 means the frame overflowed its tile-entry
+        capacity and is undefined -- see render_many_checked).  Ordered after
+        the current work of `stream` (default: current stream), and `stream`
+        waits for every frame (and copy) before continuing.  Async."""
         main = stream or torch.cuda.current_stream()
         start = torch.cuda.Event()
         start.record(main)
@@ -274,6 +307,9 @@ class RenderPipeline:
                                stream=self.front[i], blend_stream=self.blend[i], split_event=self.split_ev[i],
                                stage_events=None if stage_events is None else stage_events[k])
                 last = self.blend[i]
+            if status_out is not None:  # counters of this frame, before the workspace is reused
+                with torch.cuda.stream(last):
+                    status_out[k].copy_(self.counters_view(i), non_blocking=True)
             if host_outs is not None:
                 fin = torch.cuda.Event()
                 fin.record(last)

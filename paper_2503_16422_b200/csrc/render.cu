@@ -266,6 +266,10 @@ __global__ void __launch_bounds__(kPreBlock) k_vis_emit(const uint32_t *__restri
 // are 64-bit {epoch:32 | flag:2 | count:30}; the epoch (bumped once per frame)
 // retires the previous frame's words, so no per-frame zeroing is needed.
 constexpr int kSortThreads = 256;
+#ifndef FDGS_LB_WIN
+#define FDGS_LB_WIN 8
+#endif
+constexpr int kLbWin = FDGS_LB_WIN;  // predecessors read per look-back round trip
 constexpr uint64_t kStA = 1ull << 30, kStP = 2ull << 30;
 
 __device__ __forceinline__ uint64_t ld_volatile64(const uint64_t *p) { return *(const volatile uint64_t *)p; }
@@ -377,16 +381,16 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint32_t *__res
             st_volatile64(st, epoch | kStP | tot);
         } else {
             st_volatile64(st, epoch | kStA | tot);
-            // windowed look-back: 8 predecessors per round trip, nearest first
+            // windowed look-back: kLbWin predecessors per round trip, nearest first
             int q = (int)part - 1;
             bool found = false;
             while (!found) {
-                uint64_t w[8];
+                uint64_t w[kLbWin];
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
+                for (int k = 0; k < kLbWin; ++k)
                     w[k] = q - k >= 0 ? ld_volatile64(status + (size_t)(q - k) * D + d) : (epoch | kStP);
                 int k = 0;
-                for (; k < 8; ++k) {
+                for (; k < kLbWin; ++k) {
                     const uint64_t sv = w[k];
                     if ((sv & 0xffffffff00000000ull) != epoch || (sv & (3ull << 30)) == 0) break;
                     excl += (uint32_t)(sv & kValMask);

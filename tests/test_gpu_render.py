@@ -347,3 +347,21 @@ def test_interleaved_and_planar_parameters_identical():
     sa = fd.stv_score(a, cams, [0.2, 0.6])["score"]
     sb = fd.stv_score(b, cams, [0.2, 0.6])["score"]
     assert torch.equal(sa, sb)
+
+
+def test_pipeline_overflow_detected_and_re_rendered():
+    """render_many_checked: frames that exceed a deliberately tiny tile-entry
+    capacity are flagged by their counter block and re-rendered (after growing
+    the workspace) to exactly the frames of an ample sequential renderer."""
+    scene = fi.make_scene("c3", n=20_000, seed=2)
+    cams = fi.make_cameras("c3", width=200, height=150, fx=150.0, count=3)
+    sc = fd.Scene.from_arrays(scene)
+    frames = [(cams[k % 3], float(np.float32(0.1 * k)), None, None) for k in range(9)]
+    seq = fd.Renderer(sc, 200, 150)
+    refs = [seq.render_checked(cam, t)[0].clone() for (cam, t, _, _) in frames]
+    pipe = fd.RenderPipeline(sc, 200, 150, depth=3, max_entries=4096)
+    outs = [pipe.renderers[0].new_output() for _ in frames]
+    st = pipe.render_many_checked(frames, outs)
+    assert (st[:, 3] == 0).all() and (st[:, 2] > 4096).any()
+    for ref, o in zip(refs, outs):
+        assert torch.equal(ref, o)
