@@ -51,7 +51,10 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.n_tiles = L.tiles_x * L.tiles_y;
     L.n_parts = (n + 2 * kPreBlock - 1) / (2 * kPreBlock);  // k_slice partitions (2 survivors per thread)
     L.cull_parts = (n + 4 * kPreBlock - 1) / (4 * kPreBlock);  // k_cull partitions (4 Gaussians per thread)
-    L.slice_grid = std::max(1, std::min(L.n_parts, 2 * sm_count()));  // grid-stride k_slice / k_vis_emit
+#ifndef FDGS_SLICE_GRID
+#define FDGS_SLICE_GRID 2
+#endif
+    L.slice_grid = std::max(1, std::min(L.n_parts, FDGS_SLICE_GRID * sm_count()));  // grid-stride k_slice / k_vis_emit
     L.p_sort = sm_count();
     L.sort_parts = std::max(1, (n + kDepthTile - 1) / kDepthTile);
     L.tile_parts = (int32_t)std::max<int64_t>(1, (max_entries + kTileTile - 1) / kTileTile);

@@ -167,7 +167,10 @@ __global__ void __launch_bounds__(kPreBlock) k_cull_emit(const uint32_t *__restr
 // Gaussians are written at their survivor slot (sparse); the visibility bits
 // and per-partition counts feed k_count_scan + k_vis_emit, which compact the
 // slots in order without any block waiting on another.
-__global__ void __launch_bounds__(kPreBlock) k_slice(SceneDev sc, CamDev cam, float t, Counters *ctr,
+#ifndef FDGS_SLICE_MINB
+#define FDGS_SLICE_MINB 3
+#endif
+__global__ void __launch_bounds__(kPreBlock, FDGS_SLICE_MINB) k_slice(SceneDev sc, CamDev cam, float t, Counters *ctr,
                                                      const uint32_t *__restrict__ surv, float4 *__restrict__ rec0,
                                                      float4 *__restrict__ rec1, float4 *__restrict__ rec2,
                                                      uint32_t *__restrict__ depth, uint2 *__restrict__ rect,
