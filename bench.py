@@ -67,7 +67,7 @@ def apply_config(args):
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=40)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--frames-per-step", type=int, default=60)
@@ -105,7 +105,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -414,6 +414,18 @@ def run_ours(args):
     res["work_per_frame"] = {"n_act": round(n_act_tot / frames_rank), "n_vis": round(n_vis_tot / frames_rank),
                              "entries": round(n_ent_tot / frames_rank), "evaluated_pairs": round(n_eval / frames_rank),
                              "blended_pairs": round(n_blend / frames_rank)}
+    # whole-frame HBM model of SURVEY.md §8(d) d.4 (BASELINE "% HBM roofline"): algorithmic
+    # bytes per frame from the device counters, over the frame time, against the measured copy peak
+    na, nv, ne = n_act_tot / frames_rank, n_vis_tot / frames_rank, n_ent_tot / frames_rank
+    px = cams[0].width * cams[0].height
+    mask_terms = (8.0 * ((n + 31) // 32) + 8.0 * na) if MASKED else 0.0
+    bpf = mask_terms + 68.0 * na + (192.0 + 96.0 + 72.0) * nv + (8.0 + 32.0 + 52.0) * ne + 12.0 * px
+    hbm = float(load_peaks()[0].get("hbm_gbs", 6650.0))
+    achieved_gbs = bpf * value / world / 1e9
+    res["frame_hbm"] = {"bytes_per_frame": round(bpf), "achieved": round(achieved_gbs, 1), "peak": hbm,
+                        "unit": "GB/s", "frac": round(achieved_gbs / hbm, 4),
+                        "model": "SURVEY.md 8(d) d.4: mask words + index + 68 B/active + (192+96+72) B/visible + "
+                                 "(8+32+52) B/entry + 12 B/pixel, per GPU"}
     res["clocks"] = clocks
     res["setup"] = {"keyframe_masks_s": round(mask_build_s, 3), "n_keyframes": len(kf)}
 
