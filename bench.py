@@ -67,7 +67,7 @@ def apply_config(args):
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=40)
+    p.add_argument("--steps", type=int, default=100)  # 100 x 60 = the whole 6000-frame C3 sequence
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--frames-per-step", type=int, default=60)
