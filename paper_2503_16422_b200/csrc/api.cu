@@ -29,15 +29,14 @@ static fdgs_status cuda_fail(cudaError_t e, const char *where) {
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static int sm_count() {
-    static int cached = 0;
-    if (cached == 0) {
+    // the SM count of the current device, queried once per process (thread-safe static init)
+    static const int cached = [] {
         int dev = 0, c = 148;
         if (cudaGetDevice(&dev) == cudaSuccess &&
             cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && c > 0)
-            cached = c;
-        else
-            cached = 148;
-    }
+            return c;
+        return 148;
+    }();
     return cached;
 }
 

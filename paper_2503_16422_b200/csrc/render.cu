@@ -16,6 +16,7 @@
 //                    composite, warp-uniform early exit);
 //                    k_blend_ws: the counting / contribution-recording variant
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 
@@ -1590,8 +1591,8 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     // FDGS_DEBUG_STAGES (experiments only): bit 0 front end, bit 1 blend; with bit 0
     // clear the workspace's previous lists are blended again
     static const int dbg_stages = tune_env("FDGS_DEBUG_STAGES", 3);
-    static int dbg_calls = 0;  // the first 64 frames always build lists (fills every workspace)
-    if ((dbg_stages & 1) || dbg_calls++ < 64) {
+    static std::atomic<int> dbg_calls{0};  // the first 64 frames always build lists (fills every workspace)
+    if ((dbg_stages & 1) || dbg_calls.fetch_add(1, std::memory_order_relaxed) < 64) {
         e = cudaMemsetAsync(ws + L.counters, 0, L.zero_end - L.counters, st);  // counters, look-back, histograms
         if (e != cudaSuccess) return e;
         if (L.n > 0) {
