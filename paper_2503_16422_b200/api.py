@@ -230,14 +230,15 @@ class RenderPipeline:
     is scheduled ahead of, and overlaps, the ALU-bound blends."""
 
     def __init__(self, scene: Scene, width: int, height: int, depth: int = 4, max_entries: int | None = None,
-                 split: bool = True):
+                 split: bool = True, copy_streams: int = 1):
         self.renderers = [Renderer(scene, width, height, max_entries) for _ in range(depth)]
         lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
         self.split = split
         self.front = [torch.cuda.Stream(device=scene.device, priority=-1 if split else 0) for _ in range(depth)]
         self.blend = [torch.cuda.Stream(device=scene.device, priority=0) for _ in range(depth)] if split else None
         self.split_ev = [torch.cuda.Event() for _ in range(depth)]
-        self.copy = torch.cuda.Stream(device=scene.device)  # D2H of finished frames (render_many host_outs)
+        # D2H of finished frames (render_many host_outs), alternating over copy streams
+        self.copies = [torch.cuda.Stream(device=scene.device) for _ in range(copy_streams)]
         self.depth = depth
 
     @property
@@ -290,7 +291,8 @@ class RenderPipeline:
         for s in self.streams:
             s.wait_event(start)
         if host_outs is not None:
-            self.copy.wait_event(start)
+            for c in self.copies:
+                c.wait_event(start)
         for k, (cam, t, ml, mr) in enumerate(frames):
             i = k % self.depth
             r = self.renderers[i]
@@ -313,10 +315,11 @@ class RenderPipeline:
             if host_outs is not None:
                 fin = torch.cuda.Event()
                 fin.record(last)
-                self.copy.wait_event(fin)
-                with torch.cuda.stream(self.copy):
+                cp = self.copies[k % len(self.copies)]
+                cp.wait_event(fin)
+                with torch.cuda.stream(cp):
                     host_outs[k].copy_(outs[k], non_blocking=True)
-        for s in self.streams + ([self.copy] if host_outs is not None else []):
+        for s in self.streams + (self.copies if host_outs is not None else []):
             e = torch.cuda.Event()
             e.record(s)
             main.wait_event(e)
