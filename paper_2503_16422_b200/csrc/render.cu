@@ -274,6 +274,9 @@ constexpr int kSortThreads = 256;
 #define FDGS_LB_WIN 8
 #endif
 constexpr int kLbWin = FDGS_LB_WIN;  // predecessors read per look-back round trip
+#ifndef FDGS_LB_SLEEP
+#define FDGS_LB_SLEEP 0
+#endif
 constexpr uint64_t kStA = 1ull << 30, kStP = 2ull << 30;
 
 __device__ __forceinline__ uint64_t ld_volatile64(const uint64_t *p) { return *(const volatile uint64_t *)p; }
@@ -404,6 +407,11 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint32_t *__res
                     }
                 }
                 q -= k;  // resume at the first unpublished predecessor
+#if FDGS_LB_SLEEP > 0
+                // no progress: back off instead of re-polling at full issue rate (the
+                // spinning warps would take issue slots from co-resident blend warps)
+                if (!found && k == 0) __nanosleep(FDGS_LB_SLEEP);
+#endif
             }
             st_volatile64(st, epoch | kStP | (excl + tot));
         }
