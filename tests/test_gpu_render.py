@@ -219,6 +219,33 @@ def test_ragged_and_tiny_images(W, H):
     assert_rgb_parity(img, oracle.render(scene, cam, 0.5))
 
 
+@pytest.mark.parametrize("W,H", [(48, 4160), (2048, 2048)])
+def test_large_tile_grids(W, H):
+    """Edge of the tile-grid limits: more than 256 tile rows (the row partition
+    then takes its second 8-bit pass) and the FDGS_MAX_TILES grid (128 x 128
+    tiles).  Records and tile lists bit-exact, sampled RGB parity."""
+    scene = fi.make_scene("c1", n=3000, seed=13)
+    cam = fi.make_cameras("c1", width=W, height=H, fx=64.0 * max(W, H) / 64)[0]
+    assert ((W + 15) // 16) * ((H + 15) // 16) <= 16384
+    img, T, stats, rd = _render(scene, cam, 0.4)
+    views = rd.debug_views()
+    assert_records_bit_exact(views, scene, cam, 0.4)
+    assert_tile_lists_bit_exact(views, scene, cam, 0.4)
+    pix = np.unique(np.random.default_rng(3).integers(0, W * H, 6000))
+    assert_rgb_parity(img, oracle.render(scene, cam, 0.4, pixels=pix), pixels=pix)
+    if H > 4096:
+        assert stats.n_vis > 100
+
+
+def test_tile_grid_above_the_limit_is_unsupported():
+    scene = fi.make_scene("c1", n=100)
+    cam = fi.make_cameras("c1", width=2064, height=2048, fx=2000.0)[0]
+    sc = fd.Scene.from_arrays(scene)
+    with pytest.raises(fd.FdgsError) as e:
+        fd.Renderer(sc, 2064, 2048).render_checked(cam, 0.5)
+    assert e.value.status == _lib.FDGS_ERR_UNSUPPORTED
+
+
 def test_single_gaussian_closed_form_on_gpu():
     """North-star pin, on the GPU: one on-axis isotropic Gaussian."""
     cam = fi.scenes._cam(65, 65, 64.0, np.eye(3), np.zeros(3), np.zeros(3), bg=(0.1, 0.2, 0.3))
