@@ -7,9 +7,11 @@ code (see oracle/fdgs_oracle.c header).
 
 Parity status per function:
   rotor4, slice (Eq. 1), temporal marginal (Eq. 3), projection, SH basis,
-  per-pixel compositing (Eq. 2), masks, key-frame schedule, tile lists: pinned
-  by tests/test_oracle_pins.py.  The SH *sign convention* is a reading (R9);
-  orthonormality and the pole case pin everything but the signs.
+  per-pixel compositing (Eq. 2), masks, key-frame schedule, tile lists, VQ-SH
+  lookup: pinned by tests/test_oracle_pins.py; contributions, the STV score
+  (both combine readings, all variants), paper-literal masks: pinned by
+  tests/test_oracle_stv.py.  Parity unpinned: the SH *sign convention* only, a
+  reading (R9); orthonormality and the pole case pin everything but the signs.
 """
 from .oracle import (  # noqa: F401
     build_oracle,

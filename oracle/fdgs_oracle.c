@@ -16,7 +16,15 @@
  *   - Eq. 2: I(u,v,t) = sum_i c_i(d) alpha_i prod_{j<i}(1-alpha_j)
  *     over Gaussians sorted by depth, evaluated PER PIXEL (no tiles).
  *   - Sec. 4.2.2: key-frame visibility masks (union over views)
- *     and the active set of a frame = union of the two bracketing masks.
+ *     and the active set of a frame = union of the two bracketing masks;
+ *     the paper-literal masks from the Eq. 2 blending weights.
+ *   - Sec. 4.2.1: the spatial-temporal variation score
+ *     (spatial term from the blending weights, S^TV from p2 / p1, gamma, both
+ *     combine readings, the ablation variants).
+ *   - P:483 (Ours-PP): SH read through a vector-quantised codebook.
+ *
+ * Parity unpinned: the SH sign convention only (R9); everything
+ * else is pinned by tests/test_oracle_pins.py and tests/test_oracle_stv.py.
  *
  * Numeric paths:
  *   - every DECISION (temporal/support/near/cover culls, pixel AABB, depth key,
