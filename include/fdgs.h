@@ -63,6 +63,10 @@ typedef enum {
  *                               Python Scene allocates: a sparse, mask-driven
  *                               gather then touches one 64-byte DRAM burst per
  *                               Gaussian instead of four)
+ *   gid                       : DEVICE uint32[n] or NULL: the ORIGINAL index of
+ *                               Gaussian i when this scene is a compacted
+ *                               working set (fdgs_scene_compact, ascending
+ *                               order kept); records report gid[i].  NULL = i
  *   sh_index, sh_codebook_size: vector-quantised SH (the "Ours-PP" storage of
  *                               P:483, SH "vector quantization" after CompGS):
  *                               when sh_index != NULL, `sh` points to a
@@ -83,6 +87,11 @@ typedef struct {
     const uint16_t *sh_index;     /* nullable: dense SH                        */
     int32_t sh_codebook_size;     /* entries of the codebook when sh_index set */
     int32_t param_stride;         /* 0/1 SoA planes, 4 interleaved (see above) */
+    const uint32_t *gid;          /* nullable: original indices (compacted set) */
+    int32_t n_capacity;           /* 0, or >= n: render workspaces are laid out
+                                     for max(n, n_capacity) Gaussians, so a full
+                                     scene and its working sets share one
+                                     workspace layout (no re-zeroing)           */
 } fdgs_scene;
 
 /* Pinhole view "I" of P:126 (HOST struct).  world->camera rotation R
@@ -126,8 +135,9 @@ fdgs_status fdgs_log255_opacity(const float *d_opacity, int32_t n, float *d_out,
 
 /* Workspace bytes of fdgs_render for n Gaussians, a width x height image and
  * room for max_entries (tile, Gaussian) entries.  A render workspace must be
- * zero-filled (cudaMemset 0) once before its first fdgs_render; it can then be
- * reused by any number of frames on one stream (its look-back tables are
+ * zero-filled (cudaMemset 0) before its first fdgs_render and again whenever
+ * it is reused for a different (n, width, height, max_entries); between those
+ * it serves any number of frames on one stream (its look-back tables are
  * epoch-tagged). */
 size_t fdgs_render_workspace_bytes(int32_t n, int32_t width, int32_t height, int64_t max_entries);
 
@@ -238,6 +248,27 @@ size_t fdgs_keyframe_mask_contrib_workspace_bytes(int32_t n, const fdgs_camera *
 fdgs_status fdgs_keyframe_mask_contrib(const fdgs_scene *scene, const fdgs_camera *cams, int32_t n_cams,
                                        float t_key, double threshold, int64_t max_entries, uint32_t *d_out_mask,
                                        void *d_ws, size_t ws_bytes, uint32_t *h_max_entries, void *stream);
+
+/* Compacted working set of a key-frame window (Sec. 4.2.2: "perform
+ * rasterization while only considering the Gaussians marked by mask"): the
+ * Gaussians of d_mask_l | d_mask_r (d_mask_r nullable) in ascending index
+ * order, copied into caller-owned DEVICE arrays of capacity scene->n:
+ *   d_params float[n][16] (mean, scale, rot_l, rot_r interleaved: use
+ *   param_stride 4), d_opacity float[n], d_L float[n], d_sh float[n][48]
+ *   (dense SH; NULL for a VQ scene), d_sh_index uint16[n] (VQ scene; NULL
+ *   otherwise; the codebook is shared), d_gid uint32[n] (original indices).
+ * *d_count (DEVICE uint32) receives the count m; the caller builds an
+ * fdgs_scene of n = m over these arrays with gid = d_gid and renders it with
+ * NULL masks: frames are bit-identical to masked renders of the full scene
+ * (same decisions, same canonical order), while the per-frame culls read a
+ * dense 64-byte record per active Gaussian instead of a scattered one.
+ * Workspace: fdgs_scene_compact_workspace_bytes(n).  ASYNC.  Errors:
+ * INVALID_ARG (NULL outputs, d_mask_l NULL, scene already compacted),
+ * WORKSPACE_TOO_SMALL, CUDA. */
+size_t fdgs_scene_compact_workspace_bytes(int32_t n);
+fdgs_status fdgs_scene_compact(const fdgs_scene *scene, const uint32_t *d_mask_l, const uint32_t *d_mask_r,
+                               float *d_params, float *d_opacity, float *d_L, float *d_sh, uint16_t *d_sh_index,
+                               uint32_t *d_gid, uint32_t *d_count, void *d_ws, size_t ws_bytes, void *stream);
 
 /* d_out = d_a | d_b over ceil(n/32) words (P:285 active set).  ASYNC. */
 fdgs_status fdgs_mask_or(const uint32_t *d_a, const uint32_t *d_b, int32_t n, uint32_t *d_out, void *stream);

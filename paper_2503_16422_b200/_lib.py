@@ -25,6 +25,7 @@ EXPORTS = [
     "fdgs_keyframe_workspace_bytes", "fdgs_keyframe_mask", "fdgs_mask_or",
     "fdgs_keyframe_mask_contrib_workspace_bytes", "fdgs_keyframe_mask_contrib",
     "fdgs_mask_compact_workspace_bytes", "fdgs_mask_compact", "fdgs_stv_workspace_bytes", "fdgs_stv_score",
+    "fdgs_scene_compact_workspace_bytes", "fdgs_scene_compact",
 ]
 
 
@@ -32,7 +33,7 @@ class FdgsScene(C.Structure):
     _fields_ = [("n", C.c_int32), ("mean", C.c_void_p), ("scale", C.c_void_p), ("rot_l", C.c_void_p),
                 ("rot_r", C.c_void_p), ("opacity", C.c_void_p), ("log255_opacity", C.c_void_p),
                 ("sh", C.c_void_p), ("sh_index", C.c_void_p), ("sh_codebook_size", C.c_int32),
-                ("param_stride", C.c_int32)]
+                ("param_stride", C.c_int32), ("gid", C.c_void_p), ("n_capacity", C.c_int32)]
 
 
 class FdgsCamera(C.Structure):
@@ -99,6 +100,8 @@ def lib():
             "fdgs_mask_compact_workspace_bytes": ([I32], SZ),
             "fdgs_mask_compact": ([P, P, I32, P, P, P, SZ, P], C.c_int),
             "fdgs_stv_workspace_bytes": ([I32, P, I32, I64], SZ),
+            "fdgs_scene_compact_workspace_bytes": ([I32], SZ),
+            "fdgs_scene_compact": ([P, P, P, P, P, P, P, P, P, P, P, SZ, P], C.c_int),
             "fdgs_stv_score": ([P, P, I32, P, I32, P, P, P, P, P, SZ, P, P], C.c_int),
         }
         for name, (args, res) in sig.items():

@@ -64,7 +64,43 @@ class Scene:
             self.t["sh_index"] = idx.to(device=dev, dtype=torch.uint16).contiguous()
             k = int(self.t["sh"].shape[0])
         self.struct = FdgsScene(self.n, *[self.t[f].data_ptr() for f in _FIELDS],
-                                self.t["sh_index"].data_ptr() if idx is not None else None, k, self.stride)
+                                self.t["sh_index"].data_ptr() if idx is not None else None, k, self.stride, None, 0)
+
+    def compact(self, mask_l: torch.Tensor, mask_r: torch.Tensor | None = None, stream=None) -> "Scene":
+        """fdgs_scene_compact: the working set of a key-frame window (the
+        Gaussians of mask_l | mask_r, ascending) as a dense Scene whose records
+        report the original indices.  Render it with no mask: frames equal the
+        masked renders of this scene bit for bit.  Synchronises once (count)."""
+        if self.struct.gid:
+            raise ValueError("already a compacted working set")
+        n, dev = self.n, self.device
+        vq = "sh_index" in self.t
+        params = torch.empty((max(n, 1), 4, 4), dtype=torch.float32, device=dev)
+        opacity = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+        L = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+        sh = None if vq else torch.empty((max(n, 1), 16, 3), dtype=torch.float32, device=dev)
+        sh_index = torch.empty(max(n, 1), dtype=torch.uint16, device=dev) if vq else None
+        gid = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        count = torch.zeros(1, dtype=torch.int32, device=dev)
+        nb = lib().fdgs_scene_compact_workspace_bytes(n)
+        ws = torch.empty(nb, dtype=torch.uint8, device=dev)
+        check(lib().fdgs_scene_compact(C.byref(self.struct), _ptr(mask_l), _ptr(mask_r), _ptr(params), _ptr(opacity),
+                                       _ptr(L), _ptr(sh), _ptr(sh_index), _ptr(gid), _ptr(count), _ptr(ws), nb,
+                                       _stream_ptr(stream)))
+        m = int(count.item())
+        out = Scene.__new__(Scene)
+        out.n, out.device, out.stride = m, dev, 4
+        out.params = params
+        out.t = {"mean": params[:m, 0], "scale": params[:m, 1], "rot_l": params[:m, 2], "rot_r": params[:m, 3],
+                 "opacity": opacity[:m], "log255_opacity": L[:m], "gid": gid[:m],
+                 "sh": self.t["sh"] if vq else sh[:m]}
+        if vq:
+            out.t["sh_index"] = sh_index[:m]
+        out.struct = FdgsScene(m, *[out.t[f].data_ptr() for f in _FIELDS],
+                               out.t["sh_index"].data_ptr() if vq else None,
+                               int(self.t["sh"].shape[0]) if vq else 0, 4, gid.data_ptr(), n)
+        out.source = self
+        return out
 
     @classmethod
     def from_arrays(cls, arrays, device=None):
@@ -120,50 +156,69 @@ class Renderer:
         nbytes = lib().fdgs_render_workspace_bytes(self.scene.n, self.width, self.height, self.max_entries)
         if nbytes == 0:
             raise ValueError("invalid render size")
-        # zero-filled once: the epoch-tagged look-back tables require it (include/fdgs.h)
+        # zero-filled: the epoch-tagged look-back tables require it (include/fdgs.h)
         self.ws = torch.zeros(nbytes, dtype=torch.uint8, device=self.scene.device)
         self.ws_bytes = nbytes
+        self._layout_n = self.scene.n
 
-    def _masks(self, mask_l, mask_r):
+    def _scene_for(self, scene, stream):
+        """The scene to render (default: the renderer's), resetting the workspace
+        when its layout changes (another n; include/fdgs.h fdgs_render_workspace_bytes)."""
+        scene = self.scene if scene is None else scene
+        ln = max(scene.n, int(scene.struct.n_capacity))  # the layout fdgs_render uses
+        if ln > self.scene.n:
+            raise ValueError("scene larger than the workspace's")
+        if ln != self._layout_n:
+            with torch.cuda.stream(stream or torch.cuda.current_stream()):
+                self.ws.zero_()
+            self._layout_n = ln
+        return scene
+
+    def _masks(self, mask_l, mask_r, scene=None):
+        scene = self.scene if scene is None else scene
         for m in (mask_l, mask_r):
             if m is not None:
-                if m.dtype != torch.int32 or m.numel() != mask_words(self.scene.n) or not m.is_cuda:
-                    raise ValueError(f"mask must be a cuda int32 tensor of {mask_words(self.scene.n)} words")
+                if m.dtype != torch.int32 or m.numel() != mask_words(scene.n) or not m.is_cuda:
+                    raise ValueError(f"mask must be a cuda int32 tensor of {mask_words(scene.n)} words")
         return _ptr(mask_l), _ptr(mask_r)
 
     def new_output(self):
         return torch.empty((3, self.height, self.width), dtype=torch.float32, device=self.scene.device)
 
     def render(self, cam, t, mask_l=None, mask_r=None, out=None, out_T=None, stats=None, stream=None,
-               stage_events=None):
+               stage_events=None, scene=None):
         """Async render (no host sync).  Returns the CHW float32 output tensor.
-        stage_events: optional 5 torch.cuda.Event recorded at the stage boundaries."""
+        stage_events: optional 5 torch.cuda.Event recorded at the stage boundaries.
+        scene: another Scene to render in this workspace (e.g. a compacted
+        working set, Scene.compact), at most the renderer's n."""
         if cam.width != self.width or cam.height != self.height:
             raise ValueError("camera size differs from the renderer's")
         out = self.new_output() if out is None else out
-        ml, mr = self._masks(mask_l, mask_r)
+        sc = self._scene_for(scene, stream)
+        ml, mr = self._masks(mask_l, mask_r, sc)
         cs = camera_struct(cam) if not isinstance(cam, FdgsCamera) else cam
         if stage_events is None:
-            check(lib().fdgs_render(C.byref(self.scene.struct), ml, mr, C.byref(cs), float(t), _ptr(out),
+            check(lib().fdgs_render(C.byref(sc.struct), ml, mr, C.byref(cs), float(t), _ptr(out),
                                     _ptr(out_T), _ptr(self.ws), self.ws_bytes, self.max_entries, _ptr(stats),
                                     _stream_ptr(stream)))
         else:
             evs = (C.c_void_p * 5)(*[e.cuda_event for e in stage_events])
-            check(lib().fdgs_render_timed(C.byref(self.scene.struct), ml, mr, C.byref(cs), float(t), _ptr(out),
+            check(lib().fdgs_render_timed(C.byref(sc.struct), ml, mr, C.byref(cs), float(t), _ptr(out),
                                           _ptr(out_T), _ptr(self.ws), self.ws_bytes, self.max_entries, _ptr(stats),
                                           _stream_ptr(stream), evs))
         return out
 
     def render_split(self, cam, t, mask_l=None, mask_r=None, out=None, out_T=None, stats=None, stream=None,
-                     blend_stream=None, split_event=None, stage_events=None):
+                     blend_stream=None, split_event=None, stage_events=None, scene=None):
         """fdgs_render_split: front end on `stream`, blend on `blend_stream`."""
         out = self.new_output() if out is None else out
-        ml, mr = self._masks(mask_l, mask_r)
+        sc = self._scene_for(scene, stream)
+        ml, mr = self._masks(mask_l, mask_r, sc)
         cs = camera_struct(cam) if not isinstance(cam, FdgsCamera) else cam
         if split_event.cuda_event == 0:
             split_event.record(stream)  # materialise the CUDA event
         evs = None if stage_events is None else (C.c_void_p * 5)(*[e.cuda_event for e in stage_events])
-        check(lib().fdgs_render_split(C.byref(self.scene.struct), ml, mr, C.byref(cs), float(t), _ptr(out),
+        check(lib().fdgs_render_split(C.byref(sc.struct), ml, mr, C.byref(cs), float(t), _ptr(out),
                                       _ptr(out_T), _ptr(self.ws), self.ws_bytes, self.max_entries, _ptr(stats),
                                       _stream_ptr(stream), _stream_ptr(blend_stream),
                                       C.c_void_p(split_event.cuda_event), evs))
@@ -173,6 +228,7 @@ class Renderer:
                        grow: bool = True):
         """Synchronous render; grows the entry capacity and retries on overflow."""
         out = self.new_output() if out is None else out
+        self._scene_for(None, stream)
         ml, mr = self._masks(mask_l, mask_r)
         cs = camera_struct(cam)
         while True:
@@ -190,12 +246,12 @@ class Renderer:
     def debug_views(self) -> dict:
         """Device views (torch tensors into the workspace) after a render."""
         v = FdgsDebugViews()
-        check(lib().fdgs_render_debug_views(_ptr(self.ws), self.ws_bytes, self.scene.n, self.width, self.height,
+        n = self._layout_n  # the n of the last frame rendered in this workspace
+        check(lib().fdgs_render_debug_views(_ptr(self.ws), self.ws_bytes, n, self.width, self.height,
                                             self.max_entries, C.byref(v)))
         base = self.ws.data_ptr()
         cnt = self._slice(v.counters, base, 16).view(torch.int32)
         n_act, n_vis, E, status = [int(x) for x in cnt.cpu()]
-        n = self.scene.n
 
         def arr(ptr, count, itemsize, dtype):
             return self._slice(ptr, base, count * itemsize).view(dtype)
@@ -250,7 +306,7 @@ class RenderPipeline:
         of workspace i (include/fdgs.h fdgs_debug_views.counters)."""
         r = self.renderers[i]
         v = FdgsDebugViews()
-        check(lib().fdgs_render_debug_views(_ptr(r.ws), r.ws_bytes, r.scene.n, r.width, r.height, r.max_entries,
+        check(lib().fdgs_render_debug_views(_ptr(r.ws), r.ws_bytes, r._layout_n, r.width, r.height, r.max_entries,
                                             C.byref(v)))
         off = int(v.counters) - r.ws.data_ptr()
         return r.ws[off:off + 16]
@@ -293,12 +349,14 @@ class RenderPipeline:
         if host_outs is not None:
             for c in self.copies:
                 c.wait_event(start)
-        for k, (cam, t, ml, mr) in enumerate(frames):
+        for k, fr in enumerate(frames):
+            cam, t, ml, mr = fr[:4]
+            sc = fr[4] if len(fr) > 4 else None  # optional per-frame scene (a compacted working set)
             i = k % self.depth
             r = self.renderers[i]
             if not self.split:
                 r.render(cam, t, ml, mr, out=outs[k], stats=None if stats is None else stats[k], stream=self.front[i],
-                         stage_events=None if stage_events is None else stage_events[k])
+                         stage_events=None if stage_events is None else stage_events[k], scene=sc)
                 last = self.front[i]
             else:
                 if k >= self.depth:  # the workspace is free once its previous blend is done
@@ -307,7 +365,7 @@ class RenderPipeline:
                     self.front[i].wait_event(done)
                 r.render_split(cam, t, ml, mr, out=outs[k], stats=None if stats is None else stats[k],
                                stream=self.front[i], blend_stream=self.blend[i], split_event=self.split_ev[i],
-                               stage_events=None if stage_events is None else stage_events[k])
+                               stage_events=None if stage_events is None else stage_events[k], scene=sc)
                 last = self.blend[i]
             if status_out is not None:  # counters of this frame, before the workspace is reused
                 with torch.cuda.stream(last):

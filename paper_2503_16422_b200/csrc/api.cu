@@ -66,6 +66,10 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
         off = align256(off + bytes);
         return o;
     };
+    // persistent, at a FIXED offset whatever the layout: the look-back epoch.  It
+    // only ever increases, so epoch-tagged status words left by frames of any
+    // other layout (another n, image size or capacity) can never look current
+    L.epoch = take(sizeof(uint32_t));
     // cleared per frame
     L.counters = take(sizeof(Counters));
     L.sort_gbase = take(sizeof(uint32_t) * 4 * 256);
@@ -74,7 +78,6 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.bin_cnt = take(sizeof(uint32_t) * ((nn + 255) / 256));  // row items per k_bin_count partition
     L.zero_end = off;
     // persistent (zero-filled once)
-    L.epoch = take(sizeof(uint32_t));
     L.sort_status = take(sizeof(uint64_t) * 4 * 256 * (size_t)L.sort_parts);
     L.tile_status = take(sizeof(uint64_t) * 2 * 256 * (size_t)L.tile_parts);
     // per-frame scratch, fully written before read
@@ -162,8 +165,12 @@ SceneDev make_scenedev(const fdgs_scene &s) {
     d.sh = reinterpret_cast<const float4 *>(s.sh);
     d.sh_index = s.sh_index;
     d.sh_k = s.sh_index ? s.sh_codebook_size : 0;
+    d.gid = s.gid;
     return d;
 }
+
+// Gaussians the render workspace layout is computed for (include/fdgs.h n_capacity)
+static int32_t layout_n(const fdgs_scene &s) { return std::max(s.n, s.n_capacity); }
 
 static fdgs_status check_scene(const fdgs_scene *s) {
     if (s == nullptr) return fail(FDGS_ERR_INVALID_ARG, "scene is NULL");
@@ -176,6 +183,7 @@ static fdgs_status check_scene(const fdgs_scene *s) {
     for (const void *q : a16)
         if ((uintptr_t)q % 16 != 0) return fail(FDGS_ERR_INVALID_ARG, "scene float4 arrays must be 16-byte aligned");
     if (s->param_stride < 0 || s->param_stride > 64) return fail(FDGS_ERR_INVALID_ARG, "param_stride must lie in [0, 64]");
+    if (s->n_capacity < 0) return fail(FDGS_ERR_INVALID_ARG, "n_capacity < 0");
     if (s->sh_index != nullptr && (s->sh_codebook_size < 1 || s->sh_codebook_size > 65536))
         return fail(FDGS_ERR_INVALID_ARG, "sh_codebook_size must lie in [1, 65536] with sh_index");
     return FDGS_OK;
@@ -252,7 +260,7 @@ static fdgs_status render_impl(const fdgs_scene *scene, const uint32_t *d_mask_l
     CamDev cd;
     const char *why = nullptr;
     if (!make_camdev(*cam, cd, &why)) return fail(FDGS_ERR_INVALID_ARG, "camera: %s", why);
-    const RenderLayout L = render_layout(scene->n, cam->width, cam->height, max_entries);
+    const RenderLayout L = render_layout(layout_n(*scene), cam->width, cam->height, max_entries);
     if (L.n_tiles > FDGS_MAX_TILES) return fail(FDGS_ERR_UNSUPPORTED, "tile grid %d > %d", L.n_tiles, FDGS_MAX_TILES);
     if (d_ws == nullptr || ws_bytes < L.total || (uintptr_t)d_ws % 256 != 0)
         return fail(FDGS_ERR_WORKSPACE_TOO_SMALL, "workspace needs %zu bytes (256-aligned), got %zu", L.total, ws_bytes);
@@ -298,7 +306,7 @@ fdgs_status fdgs_render_checked(const fdgs_scene *scene, const uint32_t *d_mask_
     fdgs_status s = fdgs_render(scene, d_mask_l, d_mask_r, cam, t, d_out_rgb, d_out_T, d_ws, ws_bytes, max_entries,
                                 nullptr, stream);
     if (s != FDGS_OK) return s;
-    const RenderLayout L = render_layout(scene->n, cam->width, cam->height, max_entries);
+    const RenderLayout L = render_layout(layout_n(*scene), cam->width, cam->height, max_entries);
     Counters c;
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = cudaMemcpyAsync(&c, reinterpret_cast<char *>(d_ws) + L.counters, sizeof c, cudaMemcpyDeviceToHost, st);
@@ -347,6 +355,7 @@ fdgs_status fdgs_keyframe_mask(const fdgs_scene *scene, const fdgs_camera *cams,
     if (s != FDGS_OK) return s;
     if (cams == nullptr || n_cams <= 0 || n_cams > 1024 || d_out_mask == nullptr)
         return fail(FDGS_ERR_INVALID_ARG, "cameras / output");
+    if (scene->gid != nullptr) return fail(FDGS_ERR_INVALID_ARG, "masks index the full scene, not a working set");
     if (!std::isfinite(t_key)) return fail(FDGS_ERR_INVALID_ARG, "t_key is not finite");
     if (d_ws == nullptr || ws_bytes < fdgs_keyframe_workspace_bytes(n_cams))
         return fail(FDGS_ERR_WORKSPACE_TOO_SMALL, "keyframe workspace");
@@ -376,6 +385,7 @@ fdgs_status fdgs_keyframe_mask_contrib(const fdgs_scene *scene, const fdgs_camer
     if (s != FDGS_OK) return s;
     if (cams == nullptr || n_cams < 1 || (scene->n > 0 && d_out_mask == nullptr))
         return fail(FDGS_ERR_INVALID_ARG, "cameras / output");
+    if (scene->gid != nullptr) return fail(FDGS_ERR_INVALID_ARG, "masks index the full scene, not a working set");
     if (!std::isfinite(t_key)) return fail(FDGS_ERR_INVALID_ARG, "t_key is not finite");
     if (!(threshold >= 0.0) || !std::isfinite(threshold) || threshold > 1e11)
         return fail(FDGS_ERR_INVALID_ARG, "threshold must be finite, >= 0 and <= 1e11");
@@ -408,6 +418,33 @@ fdgs_status fdgs_keyframe_mask_contrib(const fdgs_scene *scene, const fdgs_camer
         return fail((fdgs_status)info[0], "a view needed %u tile entries > capacity %lld", info[1],
                     (long long)max_entries);
     return FDGS_OK;
+}
+
+size_t fdgs_scene_compact_workspace_bytes(int32_t n) {
+    if (n < 0) return 0;
+    return align256(sizeof(uint32_t) * (size_t)n) + fdgs_mask_compact_workspace_bytes(n);
+}
+
+fdgs_status fdgs_scene_compact(const fdgs_scene *scene, const uint32_t *d_mask_l, const uint32_t *d_mask_r,
+                               float *d_params, float *d_opacity, float *d_L, float *d_sh, uint16_t *d_sh_index,
+                               uint32_t *d_gid, uint32_t *d_count, void *d_ws, size_t ws_bytes, void *stream) {
+    fdgs_status s = check_scene(scene);
+    if (s != FDGS_OK) return s;
+    if (scene->gid != nullptr) return fail(FDGS_ERR_INVALID_ARG, "the scene is already a compacted working set");
+    if (d_count == nullptr || (scene->n > 0 && (d_mask_l == nullptr || d_params == nullptr || d_opacity == nullptr ||
+                                                d_L == nullptr || d_gid == nullptr)))
+        return fail(FDGS_ERR_INVALID_ARG, "NULL mask / output");
+    if (scene->n > 0 && ((scene->sh_index == nullptr) != (d_sh_index == nullptr) ||
+                         (scene->sh_index == nullptr && d_sh == nullptr)))
+        return fail(FDGS_ERR_INVALID_ARG, "SH output must match the scene's storage (dense d_sh or VQ d_sh_index)");
+    if ((uintptr_t)d_params % 16 != 0 || (d_sh && (uintptr_t)d_sh % 16 != 0))
+        return fail(FDGS_ERR_INVALID_ARG, "d_params / d_sh must be 16-byte aligned");
+    if (d_ws == nullptr || ws_bytes < fdgs_scene_compact_workspace_bytes(scene->n))
+        return fail(FDGS_ERR_WORKSPACE_TOO_SMALL, "compact workspace");
+    cudaError_t e = launch_scene_compact(make_scenedev(*scene), d_mask_l, d_mask_r, reinterpret_cast<float4 *>(d_params),
+                                         d_opacity, d_L, reinterpret_cast<float4 *>(d_sh), d_sh_index, d_gid, d_count,
+                                         reinterpret_cast<uint32_t *>(d_ws), (cudaStream_t)stream);
+    return e == cudaSuccess ? FDGS_OK : cuda_fail(e, "fdgs_scene_compact");
 }
 
 fdgs_status fdgs_mask_or(const uint32_t *d_a, const uint32_t *d_b, int32_t n, uint32_t *d_out, void *stream) {
@@ -447,6 +484,7 @@ fdgs_status fdgs_stv_score(const fdgs_scene *scene, const fdgs_camera *cams, int
     if (s != FDGS_OK) return s;
     if (opts == nullptr || cams == nullptr || n_cams < 1 || n_ts < 0 || (n_ts > 0 && ts == nullptr))
         return fail(FDGS_ERR_INVALID_ARG, "opts / cameras / timestamps");
+    if (scene->gid != nullptr) return fail(FDGS_ERR_INVALID_ARG, "score the full scene, not a compacted working set");
     if (scene->n > 0 && d_out_score == nullptr) return fail(FDGS_ERR_INVALID_ARG, "d_out_score is NULL");
     if (!(opts->volume_percentile > 0.0 && opts->volume_percentile <= 1.0))
         return fail(FDGS_ERR_INVALID_ARG, "volume_percentile must lie in (0, 1]");

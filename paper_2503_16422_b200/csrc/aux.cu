@@ -1,5 +1,7 @@
 // aux.cu -- key-frame masks, mask OR / compaction,
 // scene validation and the derived L_i = ln(255 sigma_i) field.
+#include <algorithm>
+
 #include "fdgs_internal.h"
 
 namespace fdgs {
@@ -181,6 +183,50 @@ __global__ void k_log255(const float *__restrict__ op, int n, float *__restrict_
 cudaError_t launch_log255(const float *op, int n, float *out, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     k_log255<<<(n + 255) / 256, 256, 0, st>>>(op, n, out);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ working set
+// Gather of the compacted working set: one thread per active Gaussian (the
+// ascending index list of k_mask_compact), a 64-byte parameter record, the
+// opacity terms and the SH record (or VQ index).
+__global__ void __launch_bounds__(256) k_scene_gather(SceneDev sc, const int32_t *__restrict__ idx,
+                                                      const uint32_t *__restrict__ count, float4 *__restrict__ params,
+                                                      float *__restrict__ opacity, float *__restrict__ L,
+                                                      float4 *__restrict__ sh, uint16_t *__restrict__ sh_index,
+                                                      uint32_t *__restrict__ gid) {
+    const uint32_t m = *count;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+        const int i = __ldg(idx + j);
+        params[4 * (size_t)j + 0] = sc.ld_mean(i);
+        params[4 * (size_t)j + 1] = sc.ld_scale(i);
+        params[4 * (size_t)j + 2] = sc.ld_rot_l(i);
+        params[4 * (size_t)j + 3] = sc.ld_rot_r(i);
+        opacity[j] = __ldg(sc.opacity + i);
+        L[j] = __ldg(sc.L + i);
+        if (sh_index) {
+            sh_index[j] = __ldg(sc.sh_index + i);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 12; ++k) sh[12 * (size_t)j + k] = __ldg(sc.sh + 12 * (size_t)i + k);
+        }
+        gid[j] = (uint32_t)i;
+    }
+}
+
+cudaError_t launch_scene_compact(const SceneDev &sc, const uint32_t *mask_l, const uint32_t *mask_r, float4 *params,
+                                 float *opacity, float *L, float4 *sh, uint16_t *sh_index, uint32_t *gid,
+                                 uint32_t *count, uint32_t *ws, cudaStream_t st) {
+    if (sc.n == 0) return cudaMemsetAsync(count, 0, sizeof(uint32_t), st);
+    int32_t *idx = reinterpret_cast<int32_t *>(ws);
+    uint32_t *cws = ws + (size_t)sc.n;
+    cudaError_t e = launch_mask_compact(mask_l, mask_r, sc.n, idx, count, cws, st);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    k_scene_gather<<<std::min((sc.n + 255) / 256, 8 * sms), 256, 0, st>>>(sc, idx, count, params, opacity, L, sh,
+                                                                          sh_index, gid);
     return cudaGetLastError();
 }
 

@@ -51,6 +51,8 @@ struct SceneDev {
     const float4 *sh;  // [n][12] float4 = 48 floats, or the VQ codebook [K][12]
     const uint16_t *sh_index;  // VQ: codebook entry per Gaussian (nullable)
     int32_t sh_k;              // VQ codebook entries
+    const uint32_t *gid;       // compacted working set: original index of Gaussian i (nullable)
+    __device__ __forceinline__ uint32_t orig(int i) const { return gid ? __ldg(gid + i) : (uint32_t)i; }
 };
 
 // Workspace layout of fdgs_render (all offsets 256-byte aligned).  The
@@ -107,6 +109,9 @@ cudaError_t launch_keyframe(const SceneDev &sc, const CamDev *d_cams, int n_cams
 cudaError_t launch_mask_or(const uint32_t *a, const uint32_t *b, int n, uint32_t *out, cudaStream_t st);
 cudaError_t launch_mask_compact(const uint32_t *a, const uint32_t *b, int n, int32_t *idx, uint32_t *count,
                                 uint32_t *ws_ticket_and_status, cudaStream_t st);
+cudaError_t launch_scene_compact(const SceneDev &sc, const uint32_t *mask_l, const uint32_t *mask_r, float4 *params,
+                                 float *opacity, float *L, float4 *sh, uint16_t *sh_index, uint32_t *gid,
+                                 uint32_t *count, uint32_t *ws, cudaStream_t st);
 cudaError_t launch_validate(const SceneDev &sc, unsigned long long *d_first_bad, cudaStream_t st);
 cudaError_t launch_log255(const float *op, int n, float *out, cudaStream_t st);
 

@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(kPreBlock, FDGS_SLICE_MINB) k_slice(SceneDev s
                     const uint32_t ax = pj.px0 | (pj.px1 << 16), ay = pj.py0 | (pj.py1 << 16);
                     rec0[sidx] = make_float4(pj.u, pj.v, pj.Ap, pj.Bp);
                     rec1[sidx] = make_float4(pj.Cp, pj.Q2, __uint_as_float(ax), __uint_as_float(ay));
-                    rec2[sidx] = make_float4(rgb[0], rgb[1], rgb[2], __int_as_float(i));
+                    rec2[sidx] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(sc.orig(i)));
                     depth[sidx] = pj.depth_bits;
                     rect[sidx] = make_uint2(ax, ay);
                 }
@@ -1603,12 +1603,12 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     if ((dbg_stages & 1) || dbg_calls.fetch_add(1, std::memory_order_relaxed) < 64) {
         e = cudaMemsetAsync(ws + L.counters, 0, L.zero_end - L.counters, st);  // counters, look-back, histograms
         if (e != cudaSuccess) return e;
-        if (L.n > 0) {
+        if (sc.n > 0) {
             uint32_t *cbits = reinterpret_cast<uint32_t *>(ws + L.surv_bits);
             uint32_t *ccnt = reinterpret_cast<uint32_t *>(ws + L.cull_cnt);
             k_cull<<<L.cull_parts, kPreBlock, 0, st>>>(sc, mask_l, mask_r, t, ctr, cbits, ccnt);
             k_count_scan<<<1, 1024, 0, st>>>(ccnt, L.cull_parts, nullptr, kCullItems, &ctr->n_surv);
-            k_cull_emit<<<L.cull_parts, kPreBlock, 0, st>>>(cbits, ccnt, L.n, surv);
+            k_cull_emit<<<L.cull_parts, kPreBlock, 0, st>>>(cbits, ccnt, sc.n, surv);
             uint32_t *vbits = reinterpret_cast<uint32_t *>(ws + L.vis_bits);
             uint32_t *vcnt = reinterpret_cast<uint32_t *>(ws + L.vis_cnt);
             k_slice<<<L.slice_grid, kPreBlock, 0, st>>>(sc, cam, t, ctr, surv, rec0, rec1, rec2, depth, rect, vbits,
