@@ -196,6 +196,31 @@ fdgs_status fdgs_render_checked(const fdgs_scene *scene, const uint32_t *d_mask_
                                 size_t ws_bytes, int64_t max_entries, fdgs_frame_stats *host_stats,
                                 void *stream);
 
+/* CUDA-graph form of fdgs_render (the same kernels and results): the frame's
+ * ~21 launches are captured once per (workspace, layout) and replayed with
+ * one host call per frame; only the arguments that change between frames are
+ * updated (scene, masks, t, camera, outputs).  Front-end nodes carry the
+ * device's greatest stream priority and the blend its least (as
+ * fdgs_render_split), so graphs of several workspaces on several streams
+ * interleave.  The blend is the timed k_blend_wl (no work counters).
+ *   create: `scene` fixes the layout (max(n, n_capacity)); d_ws / ws_bytes /
+ *           max_entries / width / height as for fdgs_render; *out (HOST)
+ *           receives an opaque handle.  Synchronous (captures, instantiates).
+ *   launch: a scene of the same layout n, camera of the same size; otherwise
+ *           as fdgs_render (ASYNC on `stream`; frame status in the workspace
+ *           counters).  The handle may not be launched concurrently from two
+ *           host threads.
+ *   destroy: frees the handle (NULL is a no-op).
+ * Errors: INVALID_ARG (NULL, layout / size mismatch, bad camera),
+ * WORKSPACE_TOO_SMALL, UNSUPPORTED, CUDA. */
+typedef struct fdgs_render_graph fdgs_render_graph;
+fdgs_status fdgs_render_graph_create(const fdgs_scene *scene, int32_t width, int32_t height, void *d_ws,
+                                     size_t ws_bytes, int64_t max_entries, fdgs_render_graph **out);
+fdgs_status fdgs_render_graph_launch(fdgs_render_graph *graph, const fdgs_scene *scene, const uint32_t *d_mask_l,
+                                     const uint32_t *d_mask_r, const fdgs_camera *cam, float t, float *d_out_rgb,
+                                     float *d_out_T, void *stream);
+fdgs_status fdgs_render_graph_destroy(fdgs_render_graph *graph);
+
 /* Device views into a render workspace after fdgs_render (tests/debug only).
  * Records are indexed by the SLOT of a Gaussian that passed the mask and the
  * temporal cull (survivor order = ascending Gaussian index); only the slots of

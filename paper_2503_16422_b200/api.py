@@ -157,9 +157,41 @@ class Renderer:
         if nbytes == 0:
             raise ValueError("invalid render size")
         # zero-filled: the epoch-tagged look-back tables require it (include/fdgs.h)
+        self._drop_graph()
         self.ws = torch.zeros(nbytes, dtype=torch.uint8, device=self.scene.device)
         self.ws_bytes = nbytes
         self._layout_n = self.scene.n
+
+    def _drop_graph(self):
+        g = getattr(self, "_graph", None)
+        if g:
+            lib().fdgs_render_graph_destroy(g)
+        self._graph = None
+
+    def __del__(self):
+        try:
+            self._drop_graph()
+        except Exception:
+            pass
+
+    def render_graph(self, cam, t, mask_l=None, mask_r=None, out=None, out_T=None, stream=None, scene=None):
+        """fdgs_render_graph_launch: the frame as one CUDA-graph launch (captured on
+        first use for this workspace; results identical to render()).  Async."""
+        if cam.width != self.width or cam.height != self.height:
+            raise ValueError("camera size differs from the renderer's")
+        out = self.new_output() if out is None else out
+        sc = self._scene_for(scene, stream)
+        ml, mr = self._masks(mask_l, mask_r, sc)
+        cs = camera_struct(cam) if not isinstance(cam, FdgsCamera) else cam
+        if not self._graph:
+            h = C.c_void_p()
+            base = self.scene  # the layout is the full scene's (working sets share it, n_capacity)
+            check(lib().fdgs_render_graph_create(C.byref(base.struct), self.width, self.height, _ptr(self.ws),
+                                                 self.ws_bytes, self.max_entries, C.byref(h)))
+            self._graph = h
+        check(lib().fdgs_render_graph_launch(self._graph, C.byref(sc.struct), ml, mr, C.byref(cs), float(t),
+                                             _ptr(out), _ptr(out_T), _stream_ptr(stream)))
+        return out
 
     def _scene_for(self, scene, stream):
         """The scene to render (default: the renderer's), resetting the workspace
@@ -286,10 +318,11 @@ class RenderPipeline:
     is scheduled ahead of, and overlaps, the ALU-bound blends."""
 
     def __init__(self, scene: Scene, width: int, height: int, depth: int = 4, max_entries: int | None = None,
-                 split: bool = True, copy_streams: int = 1):
+                 split: bool = True, copy_streams: int = 1, graphs: bool = False):
         self.renderers = [Renderer(scene, width, height, max_entries) for _ in range(depth)]
         lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
         self.split = split
+        self.graphs = graphs  # one CUDA-graph launch per frame (node priorities replace the stream split)
         self.front = [torch.cuda.Stream(device=scene.device, priority=-1 if split else 0) for _ in range(depth)]
         self.blend = [torch.cuda.Stream(device=scene.device, priority=0) for _ in range(depth)] if split else None
         self.split_ev = [torch.cuda.Event() for _ in range(depth)]
@@ -354,7 +387,10 @@ class RenderPipeline:
             sc = fr[4] if len(fr) > 4 else None  # optional per-frame scene (a compacted working set)
             i = k % self.depth
             r = self.renderers[i]
-            if not self.split:
+            if self.graphs:
+                r.render_graph(cam, t, ml, mr, out=outs[k], stream=self.front[i], scene=sc)
+                last = self.front[i]
+            elif not self.split:
                 r.render(cam, t, ml, mr, out=outs[k], stats=None if stats is None else stats[k], stream=self.front[i],
                          stage_events=None if stage_events is None else stage_events[k], scene=sc)
                 last = self.front[i]

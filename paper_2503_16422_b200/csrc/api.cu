@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <new>
 #include <vector>
 
 #include "fdgs_internal.h"
@@ -323,6 +324,72 @@ fdgs_status fdgs_render_checked(const fdgs_scene *scene, const uint32_t *d_mask_
     }
     if (h[3] != FDGS_OK)
         return fail((fdgs_status)h[3], "frame status %u: %u entries > capacity %lld", h[3], h[2], (long long)max_entries);
+    return FDGS_OK;
+}
+
+struct fdgs_render_graph {
+    fdgs::RenderGraphImpl *impl;
+    int32_t layout_n, width, height;
+    int64_t max_entries;
+};
+
+fdgs_status fdgs_render_graph_create(const fdgs_scene *scene, int32_t width, int32_t height, void *d_ws,
+                                     size_t ws_bytes, int64_t max_entries, fdgs_render_graph **out) {
+    if (out == nullptr) return fail(FDGS_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    fdgs_status s = check_scene(scene);
+    if (s != FDGS_OK) return s;
+    if (width < 1 || height < 1 || width > 8192 || height > 8192) return fail(FDGS_ERR_INVALID_ARG, "image size");
+    if (max_entries < 0 || max_entries > 0xffffffffll) return fail(FDGS_ERR_INVALID_ARG, "max_entries out of range");
+    if (scene->n < 1) return fail(FDGS_ERR_INVALID_ARG, "capture needs a non-empty scene");
+    const RenderLayout L = render_layout(layout_n(*scene), width, height, max_entries);
+    if (L.n_tiles > FDGS_MAX_TILES) return fail(FDGS_ERR_UNSUPPORTED, "tile grid %d > %d", L.n_tiles, FDGS_MAX_TILES);
+    if (d_ws == nullptr || ws_bytes < L.total || (uintptr_t)d_ws % 256 != 0)
+        return fail(FDGS_ERR_WORKSPACE_TOO_SMALL, "workspace needs %zu bytes (256-aligned), got %zu", L.total, ws_bytes);
+    std::call_once(g_attr_once, [] { g_attr_err = render_set_smem_attrs(); });
+    if (g_attr_err != cudaSuccess) return cuda_fail(g_attr_err, "cudaFuncSetAttribute");
+    CamDev cd{};  // placeholder camera: the arguments are replaced at every launch
+    cd.width = width;
+    cd.height = height;
+    RenderGraphImpl *impl = render_graph_new();
+    if (impl == nullptr) return fail(FDGS_ERR_CUDA, "out of host memory");
+    cudaError_t e = render_graph_build(*impl, make_scenedev(*scene), cd, reinterpret_cast<char *>(d_ws), L);
+    if (e != cudaSuccess) {
+        render_graph_delete(impl);
+        return cuda_fail(e, "fdgs_render_graph_create");
+    }
+    *out = new (std::nothrow) fdgs_render_graph{impl, layout_n(*scene), width, height, max_entries};
+    if (*out == nullptr) {
+        render_graph_delete(impl);
+        return fail(FDGS_ERR_CUDA, "out of host memory");
+    }
+    return FDGS_OK;
+}
+
+fdgs_status fdgs_render_graph_launch(fdgs_render_graph *graph, const fdgs_scene *scene, const uint32_t *d_mask_l,
+                                     const uint32_t *d_mask_r, const fdgs_camera *cam, float t, float *d_out_rgb,
+                                     float *d_out_T, void *stream) {
+    if (graph == nullptr) return fail(FDGS_ERR_INVALID_ARG, "graph is NULL");
+    fdgs_status s = check_scene(scene);
+    if (s != FDGS_OK) return s;
+    if (cam == nullptr || d_out_rgb == nullptr) return fail(FDGS_ERR_INVALID_ARG, "camera / output is NULL");
+    if (!std::isfinite(t)) return fail(FDGS_ERR_INVALID_ARG, "t is not finite");
+    if (layout_n(*scene) != graph->layout_n || cam->width != graph->width || cam->height != graph->height)
+        return fail(FDGS_ERR_INVALID_ARG, "scene layout / image size differ from the graph's");
+    CamDev cd;
+    const char *why = nullptr;
+    if (!make_camdev(*cam, cd, &why)) return fail(FDGS_ERR_INVALID_ARG, "camera: %s", why);
+    if (d_mask_l == nullptr && d_mask_r != nullptr) d_mask_l = d_mask_r, d_mask_r = nullptr;
+    cudaError_t e = render_graph_launch(*graph->impl, make_scenedev(*scene), d_mask_l, d_mask_r, cd, t, d_out_rgb,
+                                        d_out_T, (cudaStream_t)stream);
+    return e == cudaSuccess ? FDGS_OK : cuda_fail(e, "fdgs_render_graph_launch");
+}
+
+fdgs_status fdgs_render_graph_destroy(fdgs_render_graph *graph) {
+    if (graph) {
+        render_graph_delete(graph->impl);
+        delete graph;
+    }
     return FDGS_OK;
 }
 

@@ -104,6 +104,17 @@ cudaError_t launch_keyframe_contrib(const SceneDev &sc, const CamDev *cams, cons
                                     float t_key, unsigned long long thr_fixed, int64_t max_entries, char *ws,
                                     const StvLayout &SL, uint32_t *out_mask, cudaStream_t st);
 
+struct RenderGraphImpl;
+cudaError_t render_graph_build(RenderGraphImpl &g, const SceneDev &sc, const CamDev &cam, char *ws,
+                               const RenderLayout &L);
+cudaError_t render_graph_launch(RenderGraphImpl &g, const SceneDev &sc, const uint32_t *mask_l,
+                                const uint32_t *mask_r, const CamDev &cam, float t, float *out_rgb, float *out_T,
+                                cudaStream_t st);
+void render_graph_free(RenderGraphImpl &g);
+RenderGraphImpl *render_graph_new();
+void render_graph_delete(RenderGraphImpl *g);
+const RenderLayout &render_graph_layout(const RenderGraphImpl &g);
+
 cudaError_t launch_keyframe(const SceneDev &sc, const CamDev *d_cams, int n_cams, float t, uint32_t *out,
                             cudaStream_t st);
 cudaError_t launch_mask_or(const uint32_t *a, const uint32_t *b, int n, uint32_t *out, cudaStream_t st);

@@ -19,6 +19,8 @@
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <new>
+#include <vector>
 
 #include "fdgs_internal.h"
 
@@ -1722,5 +1724,149 @@ __host__ cudaError_t render_set_smem_attrs() {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_row_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     return e;
 }
+
+}  // namespace fdgs
+
+// ---------------------------------------------------------------- CUDA graph
+// One captured frame (launch_render with the blend on a second captured
+// stream) per workspace layout.  Per frame only the four kernel nodes whose
+// arguments change are re-parameterised (cull: scene, masks, t; cull emission:
+// n; slice: scene, camera, t; blend: background, outputs) and the graph is
+// launched: one host call instead of ~21 launches.  Front-end nodes run at the
+// device's greatest stream priority, the blend at the least (as
+// fdgs_render_split), so frames of different workspaces interleave.
+namespace fdgs {
+
+struct RenderGraphImpl {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t n_cull = nullptr, n_emit = nullptr, n_slice = nullptr, n_blend = nullptr;
+    cudaKernelNodeParams p_cull{}, p_emit{}, p_slice{}, p_blend{};
+    RenderLayout L{};
+    char *ws = nullptr;
+};
+
+cudaError_t render_graph_build(RenderGraphImpl &g, const SceneDev &sc, const CamDev &cam, char *ws,
+                               const RenderLayout &L) {
+    g.L = L;
+    g.ws = ws;
+    cudaStream_t s1 = nullptr, s2 = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamBeginCapture(s1, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+        cudaError_t le = launch_render(sc, nullptr, nullptr, cam, 0.0f, nullptr, nullptr, ws, L, nullptr, s1, nullptr,
+                                       s2, fork);
+        cudaError_t je = cudaEventRecord(join, s2);
+        if (je == cudaSuccess) je = cudaStreamWaitEvent(s1, join, 0);
+        cudaError_t ee = cudaStreamEndCapture(s1, &g.graph);
+        e = le != cudaSuccess ? le : (je != cudaSuccess ? je : ee);
+    }
+    if (e == cudaSuccess) {
+        size_t nn = 0;
+        e = cudaGraphGetNodes(g.graph, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        if (e == cudaSuccess) e = cudaGraphGetNodes(g.graph, nodes.data(), &nn);
+        int least = 0, greatest = 0;
+        if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+        for (size_t k = 0; e == cudaSuccess && k < nn; ++k) {
+            cudaGraphNodeType ty;
+            if ((e = cudaGraphNodeGetType(nodes[k], &ty)) != cudaSuccess || ty != cudaGraphNodeTypeKernel) continue;
+            cudaKernelNodeParams p{};
+            if ((e = cudaGraphKernelNodeGetParams(nodes[k], &p)) != cudaSuccess) break;
+            cudaKernelNodeAttrValue pr{};
+            pr.priority = p.func == (void *)k_blend_wl ? least : greatest;
+            e = cudaGraphKernelNodeSetAttribute(nodes[k], cudaKernelNodeAttributePriority, &pr);
+            if (p.func == (void *)k_cull) g.n_cull = nodes[k], g.p_cull = p;
+            else if (p.func == (void *)k_cull_emit) g.n_emit = nodes[k], g.p_emit = p;
+            else if (p.func == (void *)k_slice) g.n_slice = nodes[k], g.p_slice = p;
+            else if (p.func == (void *)k_blend_wl) g.n_blend = nodes[k], g.p_blend = p;
+        }
+        if (e == cudaSuccess && (!g.n_cull || !g.n_emit || !g.n_slice || !g.n_blend)) e = cudaErrorInvalidValue;
+    }
+    // per-node priorities (front end high, blend low) instead of the launching stream's
+    if (e == cudaSuccess) e = cudaGraphInstantiateWithFlags(&g.exec, g.graph, cudaGraphInstantiateFlagUseNodePriority);
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (s1) cudaStreamDestroy(s1);
+    if (s2) cudaStreamDestroy(s2);
+    return e;
+}
+
+cudaError_t render_graph_launch(RenderGraphImpl &g, const SceneDev &sc, const uint32_t *mask_l,
+                                const uint32_t *mask_r, const CamDev &cam, float t, float *out_rgb, float *out_T,
+                                cudaStream_t st) {
+    const RenderLayout &L = g.L;
+    char *ws = g.ws;
+    Counters *ctr = reinterpret_cast<Counters *>(ws + L.counters);
+    uint32_t *cbits = reinterpret_cast<uint32_t *>(ws + L.surv_bits);
+    uint32_t *ccnt = reinterpret_cast<uint32_t *>(ws + L.cull_cnt);
+    uint32_t *surv = reinterpret_cast<uint32_t *>(ws + L.surv);
+    float4 *rec0 = reinterpret_cast<float4 *>(ws + L.rec0);
+    float4 *rec1 = reinterpret_cast<float4 *>(ws + L.rec1);
+    float4 *rec2 = reinterpret_cast<float4 *>(ws + L.rec2);
+    uint32_t *depth = reinterpret_cast<uint32_t *>(ws + L.depth);
+    uint2 *rect = reinterpret_cast<uint2 *>(ws + L.rect);
+    uint32_t *vbits = reinterpret_cast<uint32_t *>(ws + L.vis_bits);
+    uint32_t *vcnt = reinterpret_cast<uint32_t *>(ws + L.vis_cnt);
+    uint32_t *tstart = reinterpret_cast<uint32_t *>(ws + L.tile_start);
+    uint32_t *entries = reinterpret_cast<uint32_t *>(ws + L.entries);
+    // k_cull(sc, mask_l, mask_r, t, ctr, bits, cnt)
+    const Counters *cctr = ctr;
+    void *a_cull[] = {(void *)&sc, (void *)&mask_l, (void *)&mask_r, (void *)&t, (void *)&ctr, (void *)&cbits,
+                      (void *)&ccnt};
+    cudaKernelNodeParams p = g.p_cull;
+    p.kernelParams = a_cull;
+    p.extra = nullptr;
+    cudaError_t e = cudaGraphExecKernelNodeSetParams(g.exec, g.n_cull, &p);
+    // k_cull_emit(bits, base, n, surv)
+    const uint32_t *cbits_c = cbits, *ccnt_c = ccnt;
+    int n = sc.n;
+    void *a_emit[] = {(void *)&cbits_c, (void *)&ccnt_c, (void *)&n, (void *)&surv};
+    p = g.p_emit;
+    p.kernelParams = a_emit;
+    p.extra = nullptr;
+    if (e == cudaSuccess) e = cudaGraphExecKernelNodeSetParams(g.exec, g.n_emit, &p);
+    // k_slice(sc, cam, t, ctr, surv, rec0, rec1, rec2, depth, rect, vbits, vcnt)
+    const uint32_t *surv_c = surv;
+    void *a_slice[] = {(void *)&sc,   (void *)&cam,  (void *)&t,     (void *)&ctr,   (void *)&surv_c, (void *)&rec0,
+                       (void *)&rec1, (void *)&rec2, (void *)&depth, (void *)&rect, (void *)&vbits,  (void *)&vcnt};
+    p = g.p_slice;
+    p.kernelParams = a_slice;
+    p.extra = nullptr;
+    if (e == cudaSuccess) e = cudaGraphExecKernelNodeSetParams(g.exec, g.n_slice, &p);
+    // k_blend_wl(tile_start, entries, rec0, rec1, rec2, ctr, tiles_x, width, height, bg0, bg1, bg2, out_rgb, out_T)
+    const uint32_t *tstart_c = tstart, *entries_c = entries;
+    const float4 *r0c = rec0, *r1c = rec1, *r2c = rec2;
+    int tiles_x = L.tiles_x, width = L.width, height = L.height;
+    float bg0 = cam.bg[0], bg1 = cam.bg[1], bg2 = cam.bg[2];
+    void *a_blend[] = {(void *)&tstart_c, (void *)&entries_c, (void *)&r0c,    (void *)&r1c,   (void *)&r2c,
+                       (void *)&cctr,     (void *)&tiles_x,   (void *)&width,  (void *)&height, (void *)&bg0,
+                       (void *)&bg1,      (void *)&bg2,       (void *)&out_rgb, (void *)&out_T};
+    p = g.p_blend;
+    p.kernelParams = a_blend;
+    p.extra = nullptr;
+    if (e == cudaSuccess) e = cudaGraphExecKernelNodeSetParams(g.exec, g.n_blend, &p);
+    if (e == cudaSuccess) e = cudaGraphLaunch(g.exec, st);
+    return e;
+}
+
+void render_graph_free(RenderGraphImpl &g) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+    g.exec = nullptr;
+    g.graph = nullptr;
+}
+RenderGraphImpl *render_graph_new() { return new (std::nothrow) RenderGraphImpl(); }
+void render_graph_delete(RenderGraphImpl *g) {
+    if (g) {
+        render_graph_free(*g);
+        delete g;
+    }
+}
+const RenderLayout &render_graph_layout(const RenderGraphImpl &g) { return g.L; }
 
 }  // namespace fdgs

@@ -94,3 +94,12 @@ def test_workspace_sizes(lib):
     s1 = lib.fdgs_stv_workspace_bytes(200_000, cams, 2, 12_800_000)
     assert s1 >= lib.fdgs_render_workspace_bytes(200_000, 1352, 1014, 12_800_000) + 4 * 8 * 200_000
     assert lib.fdgs_stv_workspace_bytes(10, None, 0, 0) == 0
+
+
+def test_graph_entry_points_host_errors(lib):
+    from paper_2503_16422_b200 import _lib
+    h = C.c_void_p()
+    assert lib.fdgs_render_graph_create(None, 64, 64, None, 0, 0, C.byref(h)) == _lib.FDGS_ERR_INVALID_ARG
+    assert lib.fdgs_render_graph_launch(None, None, None, None, None, 0.0, None, None, None) == \
+        _lib.FDGS_ERR_INVALID_ARG
+    assert lib.fdgs_render_graph_destroy(None) == _lib.FDGS_OK

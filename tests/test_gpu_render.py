@@ -392,3 +392,38 @@ def test_pipeline_overflow_detected_and_re_rendered():
     assert (st[:, 3] == 0).all() and (st[:, 2] > 4096).any()
     for ref, o in zip(refs, outs):
         assert torch.equal(ref, o)
+
+
+def test_cuda_graph_frames_equal_launched_frames():
+    """fdgs_render_graph_*: the captured frame replayed with new arguments
+    (camera, t, masks, output, working set) gives the frames of fdgs_render bit
+    for bit, also inside the pipeline."""
+    scene = fi.make_scene("c3", n=25_000, seed=6)
+    cams = fi.make_cameras("c3", width=240, height=180, fx=180.0, count=4)
+    sc = fd.Scene.from_arrays(scene)
+    kf = fd.keyframes(300, 20)
+    times = fi.frame_times(300)
+    masks = [fd.keyframe_mask(sc, cams, float(times[k])) for k in kf]
+    frames = []
+    for fr in range(95, 113):
+        l, r = fd.bracket(kf, fr)
+        frames.append((cams[fr % 4], float(times[fr]), masks[l], masks[r]))
+    seq = fd.Renderer(sc, 240, 180)
+    refs = [seq.render_checked(cam, t, ml, mr)[0].clone() for (cam, t, ml, mr) in frames]
+    g = fd.Renderer(sc, 240, 180)
+    for (cam, t, ml, mr), ref in zip(frames, refs):
+        out = g.render_graph(cam, t, ml, mr)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+    # working sets through the same graph (n_capacity keeps the layout)
+    l, r = fd.bracket(kf, 100)
+    ws = sc.compact(masks[l], masks[r])
+    out = g.render_graph(frames[5][0], frames[5][1], scene=ws)
+    torch.cuda.synchronize()
+    assert torch.equal(out, refs[5])
+    pipe = fd.RenderPipeline(sc, 240, 180, depth=3, graphs=True)
+    outs = [pipe.renderers[0].new_output() for _ in frames]
+    pipe.render_many(frames, outs)
+    torch.cuda.synchronize()
+    for ref, o in zip(refs, outs):
+        assert torch.equal(ref, o)
