@@ -552,6 +552,8 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if os.environ.get("FDGS_DEBUG_STAGES", "3") != "3":
+        raise SystemExit("FDGS_DEBUG_STAGES skips render stages (experiments only): unset it to benchmark")
     apply_config(args)
     if args.impl == "reference":
         run_reference(args)
