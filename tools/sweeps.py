@@ -45,10 +45,47 @@ def fps_of(pipe, frames, outs, reps=3):
     return len(frames) / (best / 1e3)
 
 
+def pruning_study(name, ratios=(0.0, 0.5, 0.8, 0.9), t_stride=10):
+    """Sec. 4.2.1 end to end on the GPU (Table 3 d/e analogue, speed only): the
+    STV score over the rig, prune the lowest-scored fraction, then render the
+    pruned scene under its own key-frame masks.  No fine-tuning (needs
+    training data): this measures speed, not quality."""
+    cfg = fi.CONFIGS[name]
+    scene = fi.make_scene(name)
+    cams = fi.make_cameras(name)
+    F = cfg["frames"]
+    times = fi.frame_times(F)
+    sc = fd.Scene.from_arrays(scene)
+    t0 = time.perf_counter()
+    score = fd.stv_score(sc, cams, [float(x) for x in times[::t_stride]])["score"].cpu().numpy()
+    score_s = time.perf_counter() - t0
+    order = np.argsort(-score, kind="stable")
+    seq = [(f, c) for f in range(0, F, 5) for c in range(0, len(cams), 4)]
+    out = {"config": name, "n": scene.n, "score_views": len(cams) * len(times[::t_stride]),
+           "score_s": round(score_s, 3), "curve": []}
+    for r in ratios:
+        keep = np.sort(order[: max(1, int(round(scene.n * (1.0 - r))))])
+        sub = fd.Scene.from_arrays(scene.subset(keep))
+        kf = fd.keyframes(F, cfg["keyframe_interval"])
+        masks = [fd.keyframe_mask(sub, cams, float(times[k])) for k in kf]
+        pipe = fd.RenderPipeline(sub, cams[0].width, cams[0].height, depth=4)
+        outs = [pipe.renderers[0].new_output() for _ in seq]
+        frames = []
+        for f, c in seq:
+            lo, hi = fd.bracket(kf, f)
+            frames.append((fd.camera_struct(cams[c]), float(times[f]), masks[lo], masks[hi]))
+        fps_of(pipe, frames, outs, reps=1)
+        out["curve"].append({"prune_ratio": r, "n": int(keep.size), "fps_masked": round(fps_of(pipe, frames, outs), 1)})
+        del pipe, outs, sub, masks
+        torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c3")
     ap.add_argument("--t-stride", type=int, default=10, help="timestamps sampled for the ratio / IoU curves")
+    ap.add_argument("--prune-config", default="c4", help="config of the pruning study ('' to skip)")
     a = ap.parse_args()
     cfg = fi.CONFIGS[a.config]
     scene = fi.make_scene(a.config)
@@ -137,6 +174,8 @@ def main():
                     "psnr_vs_unmasked_mean_of_differing": round(float(np.mean(psnr)), 2) if psnr else None,
                     "psnr_vs_unmasked_min": round(float(np.min(psnr)), 2) if psnr else None})
         del outs_m
+    if a.prune_config:
+        out["pruning_study"] = pruning_study(a.prune_config)
     out["interval_study"] = {"unmasked_fps": round(fps_u, 1), "frames": len(seq), "curve": res,
                              "note": "geometric key-frame masks (reading R3); PSNR on [0,1] rgb over the frames that differ at all"}
     print(json.dumps(out))
