@@ -905,26 +905,6 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
     return d;
 }
 
-constexpr int kBlendThreads = 128;  // one 16x16 tile, 2 horizontally adjacent pixels per thread
-
-// Staged splat record in shared memory (double-buffered batches).
-struct BlendBatch {
-    float4 a[kBlendThreads];  // u, v, A', B'
-    float4 c[kBlendThreads];  // C', Q2, r, g
-    float4 d[kBlendThreads];  // b, ~pixel-AABB mask (x bits 0-15, y bits 16-31: set = outside), reached rows (bits 16-31), gid
-};
-
-__device__ __forceinline__ void stage_load(const uint32_t *__restrict__ entries, const float4 *__restrict__ rec0,
-                                           const float4 *__restrict__ rec1, const float4 *__restrict__ rec2,
-                                           uint32_t k, uint32_t end, float4 &r0, float4 &r1, float4 &r2) {
-    if (k < end) {
-        const uint32_t v = __ldg(entries + k);
-        r0 = __ldg(rec0 + v);
-        r1 = __ldg(rec1 + v);
-        r2 = __ldg(rec2 + v);
-    }
-}
-
 // Stage one splat record for the tile.  Besides the pixel-AABB mask (the
 // per-pixel decision), a refined row mask culls whole warps: row r is kept only
 // if the ellipse {e2 >= -margin} reaches the row's segment of pixel centres
@@ -956,11 +936,6 @@ __device__ __forceinline__ void stage_fields(int tx, int ty, const float4 &r0, c
     od = make_float4(r2.z, __uint_as_float(~(xm | (ym << 16))), __uint_as_float(yr << 16), r2.w);  // .w: gid bits
 }
 
-__device__ __forceinline__ void stage_store(BlendBatch &B, int tid, uint32_t k, uint32_t end, int tx, int ty,
-                                            const float4 &r0, const float4 &r1, const float4 &r2) {
-    if (k < end) stage_fields(tx, ty, r0, r1, r2, B.a[tid], B.c[tid], B.d[tid]);
-}
-
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
     float2 d;
     asm("mul.rn.f32x2 %0, %1, %2;"
@@ -969,126 +944,6 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
     return d;
 }
 
-template <bool kCount>
-__global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restrict__ tile_start,
-                                                         const uint32_t *__restrict__ entries,
-                                                         const float4 *__restrict__ rec0,
-                                                         const float4 *__restrict__ rec1,
-                                                         const float4 *__restrict__ rec2, Counters *ctr,
-                                                         int tiles_x, int width, int height, float bg0, float bg1,
-                                                         float bg2, float *__restrict__ out_rgb,
-                                                         float *__restrict__ out_T, fdgs_frame_stats *stats) {
-    __shared__ BlendBatch sb[2];
-    __shared__ bool s_last;
-    const bool ok = ctr->status == FDGS_OK;
-    const int tile = blockIdx.x, tx = tile % tiles_x, ty = tile / tiles_x;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    // warp w owns rows 4w..4w+3; thread: row tid >> 3, columns 2*(tid & 7) + {0,1}
-    const int ly = tid >> 3, lx = (tid & 7) * 2;
-    const int i0 = tx * 16 + lx, j = ty * 16 + ly;
-    const bool in0 = i0 < width && j < height, in1 = i0 + 1 < width && j < height;
-    const uint32_t start = __ldg(tile_start + tile), end = __ldg(tile_start + tile + 1);
-    const float pyf = (float)j + 0.5f;
-    const float2 px = make_float2((float)i0 + 0.5f, (float)(i0 + 1) + 0.5f);
-    const uint32_t pb0 = (1u << lx) | (1u << (16 + ly)), pb1 = (2u << lx) | (1u << (16 + ly));
-    const uint32_t wrows = 0xFu << (16 + 4 * warp);  // this warp's 4 rows
-    const float kInf = __int_as_float(0x7f800000);
-    // eligibility threshold on e2: 0 while the pixel is live, +inf once it is
-    // outside the image or terminated (e2 is finite, so e2 >= +inf is false)
-    float2 thr = make_float2(in0 ? 0.0f : kInf, in1 ? 0.0f : kInf);
-    float2 T = make_float2(1.0f, 1.0f), Cr = make_float2(0.f, 0.f), Cg = Cr, Cb = Cr;
-    uint32_t n_eval = 0, n_blend = 0;
-    const uint32_t first = ok ? start : end;
-    float4 r0, r1, r2;
-    stage_load(entries, rec0, rec1, rec2, first + tid, end, r0, r1, r2);
-    stage_store(sb[0], tid, first + tid, end, tx, ty, r0, r1, r2);
-    __syncthreads();
-    int buf = 0;
-    for (uint32_t base = first; base < end; base += kBlendThreads) {
-        const uint32_t nxt = base + kBlendThreads;
-        stage_load(entries, rec0, rec1, rec2, nxt + tid, end, r0, r1, r2);  // prefetch the next batch
-        const BlendBatch &B = sb[buf];
-        if (!__all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf)) {
-            const int cnt = (int)min((uint32_t)kBlendThreads, end - base);
-            for (int q = 0; q < cnt; ++q) {
-                const float4 dq = B.d[q];
-                const uint32_t m = __float_as_uint(dq.y);
-                if (kCount)  // algorithmic work: pairs in the pixel AABB of live pixels
-                    n_eval += (uint32_t)((m & pb0) == 0u && thr.x == 0.0f) + (uint32_t)((m & pb1) == 0u && thr.y == 0.0f);
-                if ((__float_as_uint(dq.z) & wrows) == 0) continue;  // warp-uniform: ellipse misses these rows
-                const float4 a = B.a[q];
-                const float4 c = B.c[q];
-                // pinned e2 chain: dy terms once per row, dx terms per pixel
-                const float dy = __fsub_rn(pyf, a.y);
-                const float t1 = __fmul_rn(a.w, dy);
-                const float t3 = __fmul_rn(c.x, dy);
-                const float t4 = __fmaf_rn(t3, dy, c.y);
-                const float2 dx = sub2(px, make_float2(a.x, a.x));
-                const float2 t2 = fma2(make_float2(a.z, a.z), dx, make_float2(t1, t1));
-                const float2 e2 = fma2(dx, t2, make_float2(t4, t4));
-                const bool box0 = (m & pb0) == 0u, box1 = (m & pb1) == 0u;  // one LOP3 each
-                const bool v0 = box0 && e2.x >= thr.x, v1 = box1 && e2.y >= thr.y;
-                if (!(v0 || v1)) continue;
-                const float a0 = v0 ? fminf(0.99f, ex2_approx(e2.x) * (1.0f / 255.0f)) : 0.0f;
-                const float a1 = v1 ? fminf(0.99f, ex2_approx(e2.y) * (1.0f / 255.0f)) : 0.0f;
-                float2 w = mul2(make_float2(a0, a1), T);
-                const float2 test = sub2(T, w);
-                const bool s0 = v0 && test.x < 1e-4f, s1 = v1 && test.y < 1e-4f;
-                w.x = s0 ? 0.0f : w.x;
-                w.y = s1 ? 0.0f : w.y;
-                thr.x = s0 ? kInf : thr.x;
-                thr.y = s1 ? kInf : thr.y;
-                if (kCount) n_blend += (uint32_t)(v0 && !s0) + (uint32_t)(v1 && !s1);
-                T = sub2(T, w);
-                Cr = fma2(make_float2(c.z, c.z), w, Cr);
-                Cg = fma2(make_float2(c.w, c.w), w, Cg);
-                Cb = fma2(make_float2(dq.x, dq.x), w, Cb);
-            }
-        }
-        stage_store(sb[buf ^ 1], tid, nxt + tid, end, tx, ty, r0, r1, r2);
-        buf ^= 1;
-        if (__syncthreads_count(thr.x == kInf && thr.y == kInf) == kBlendThreads) break;
-    }
-    if (kCount) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            n_eval += __shfl_xor_sync(0xffffffffu, n_eval, o);
-            n_blend += __shfl_xor_sync(0xffffffffu, n_blend, o);
-        }
-        if ((tid & 31) == 0 && n_eval) {
-            atomicAdd(&ctr->n_eval, (unsigned long long)n_eval);
-            atomicAdd(&ctr->n_blend, (unsigned long long)n_blend);
-        }
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) s_last = atomicAdd(&ctr->blend_ticket, 1u) == gridDim.x - 1;
-        __syncthreads();
-        if (s_last && tid == 0 && stats != nullptr) {
-            __threadfence();
-            volatile Counters *vc = ctr;
-            stats->n_act = vc->n_act;
-            stats->n_vis = vc->n_vis;
-            stats->n_entries = vc->n_entries;
-            stats->status = vc->status;
-            stats->n_evaluated = vc->n_eval;
-            stats->n_blended = vc->n_blend;
-        }
-    }
-    if (!ok) return;
-    const size_t hw = (size_t)width * height, p = (size_t)j * width + i0;
-    if (in0) {
-        out_rgb[p] = fmaf(T.x, bg0, Cr.x);
-        out_rgb[hw + p] = fmaf(T.x, bg1, Cg.x);
-        out_rgb[2 * hw + p] = fmaf(T.x, bg2, Cb.x);
-        if (out_T) out_T[p] = T.x;
-    }
-    if (in1) {
-        out_rgb[p + 1] = fmaf(T.y, bg0, Cr.y);
-        out_rgb[hw + p + 1] = fmaf(T.y, bg1, Cg.y);
-        out_rgb[2 * hw + p + 1] = fmaf(T.y, bg2, Cb.y);
-        if (out_T) out_T[p + 1] = T.y;
-    }
-}
 
 // Warp-specialised blend: one producer warp stages records 32 at a time into
 // a ring of kWsBuf shared-memory batches (gathers + the row-culling mask), four
@@ -1096,7 +951,8 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const uint32_t *__restr
 // barriers, so consumer warps drift independently; a consumer whose pixels
 // have all terminated keeps releasing batches without computing, and the
 // producer stops once all four are done.  Pixel mapping and arithmetic are
-// those of k_blend.
+// those of k_blend_wl; this kernel visits every record of the tile (for the
+// Eq. 2 work counters) and records contributions (fdgs_stv_score).
 constexpr int kWsBuf = 6;
 // fl(x * kInv255) is monotone in x and equals 0.99f exactly for one float,
 // kAlphaPre = 252.44998f (0x437c7332), so min(0.99f, fl(x * kInv255)) ==
@@ -1687,33 +1543,24 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         bst = blend_st;
     }
     if (ev && (e = cudaEventRecord(ev[3], bst)) != cudaSuccess) return e;
-    static const bool ws_blend = tune_env("FDGS_BLEND_WS", 1) == 1;  // FDGS_BLEND_WS=0: block-synchronous k_blend
     static const bool wl_blend = tune_env("FDGS_BLEND_WL", 1) == 1;  // FDGS_BLEND_WL=0: k_blend_ws for frames too
     if (!(dbg_stages & 2)) {
     } else if (contrib != nullptr) {  // spatial-score recording (fdgs_stv_score)
         k_blend_ws<false, true><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x,
                                                                    L.width, L.height, cam.bg[0], cam.bg[1], cam.bg[2],
                                                                    out_rgb, out_T, nullptr, contrib, stv_info);
-    } else if (ws_blend) {
-        if (stats != nullptr)
-            k_blend_ws<true><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x,
-                                                                L.width, L.height, cam.bg[0], cam.bg[1], cam.bg[2],
-                                                                out_rgb, out_T, stats);
-        else if (wl_blend)
-            k_blend_wl<<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
-                                                          L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
-        else
-            k_blend_ws<false><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x,
-                                                                 L.width, L.height, cam.bg[0], cam.bg[1], cam.bg[2],
-                                                                 out_rgb, out_T, nullptr);
-    } else if (stats != nullptr)
-        k_blend<true><<<L.n_tiles, kBlendThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
+    } else if (stats != nullptr) {  // Eq. 2 work counters (visits every record)
+        k_blend_ws<true><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
                                                             L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T,
                                                             stats);
-    else
-        k_blend<false><<<L.n_tiles, kBlendThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x,
-                                                             L.width, L.height, cam.bg[0], cam.bg[1], cam.bg[2],
-                                                             out_rgb, out_T, nullptr);
+    } else if (wl_blend) {  // the timed blend
+        k_blend_wl<<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
+                                                      L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
+    } else {
+        k_blend_ws<false><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
+                                                             L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T,
+                                                             nullptr);
+    }
     if (ev && (e = cudaEventRecord(ev[4], bst)) != cudaSuccess) return e;
     return cudaGetLastError();
 }
