@@ -399,8 +399,11 @@ def run_ours(args):
             achieved = nb / (stage_ms[dom] / 1e3) / 1e9
             rl = {"kernel": stage_names[dom], "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                   "unit": "GB/s", "frac": round(achieved / hbm, 4), "peak_src": peak_src}
-        tr = load_traffic().get(rl["kernel"])
-        rl["traffic"] = tr
+        trj = load_traffic()
+        rl["traffic"] = trj.get(rl["kernel"])
+        if trj.get(rl["kernel"] + "_issue_slots_busy") is not None:
+            # the blend is issue-bound: the share of issue slots it uses (ncu, profiles/)
+            rl["ncu_issue_slots_busy"] = trj[rl["kernel"] + "_issue_slots_busy"]
         res["roofline"] = rl
         res["stages"] = {nm: {"ms_per_frame": round(float(per_frame[i]), 4),
                               "share": round(float(stage_ms[i] / sum(step_ms)), 4)} for i, nm in enumerate(stage_names)}
