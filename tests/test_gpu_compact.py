@@ -71,3 +71,38 @@ def test_working_sets_in_the_pipeline_and_errors():
     with pytest.raises(fd.FdgsError) as e:
         fd.keyframe_mask(ws, cams, t)
     assert e.value.status == _lib.FDGS_ERR_INVALID_ARG
+
+
+def test_bench_launch_configuration_full_c3():
+    """BASELINE configs[2] at full size in the launch configuration bench.py
+    times: RenderPipeline on 4 stream pairs, frames across a key-frame boundary
+    rendered from their windows' working sets, against single-stream masked
+    renders (bit-identical) and, for one frame, the oracle (sampled pixels)."""
+    from parity import assert_rgb_parity
+    scene = fi.make_scene("c3")
+    cams = fi.make_cameras("c3")
+    times = fi.frame_times(300)
+    kf = fd.keyframes(300, 20)
+    sc = fd.Scene.from_arrays(scene)
+    masks = [fd.keyframe_mask(sc, cams, float(times[k])) for k in kf]
+    seq = [(ti, ci) for ti in (99, 100, 101) for ci in (0, 7, 13)]
+    sets, frames, refs = {}, [], []
+    r = fd.Renderer(sc, 1352, 1014)
+    for ti, ci in seq:
+        l, rr = fd.bracket(kf, ti)
+        if (l, rr) not in sets:
+            sets[(l, rr)] = sc.compact(masks[l], masks[rr])
+        frames.append((fd.camera_struct(cams[ci]), float(times[ti]), None, None, sets[(l, rr)]))
+        refs.append(r.render_checked(cams[ci], float(times[ti]), masks[l], masks[rr])[0].clone())
+    pipe = fd.RenderPipeline(sc, 1352, 1014, depth=4)
+    outs = [pipe.renderers[0].new_output() for _ in frames]
+    pipe.render_many(frames, outs)
+    torch.cuda.synchronize()
+    for a, b in zip(outs, refs):
+        assert torch.equal(a, b)
+    ti, ci = seq[4]
+    l, rr = fd.bracket(kf, ti)
+    active = masks[l].cpu().numpy().view(np.uint32) | masks[rr].cpu().numpy().view(np.uint32)
+    pix = np.unique(np.random.default_rng(5).integers(0, 1352 * 1014, 2500))
+    orc = oracle.render(scene, cams[ci], float(times[ti]), mask=active, pixels=pix)
+    assert_rgb_parity(outs[4].cpu().numpy(), orc, pixels=pix)
