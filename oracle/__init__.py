@@ -27,6 +27,7 @@ from .oracle import (  # noqa: F401
     tv_value,
     keyframe_mask,
     keyframe_mask_contrib,
+    prune_mask,
     keyframes,
     bracket,
     active_mask,

@@ -757,6 +757,32 @@ void or_keyframe_mask_contrib(const or_scene *S, const or_camera *cams, int32_t 
     free(c);
 }
 
+/* Sec. 4.2.1 "Pruning": "All 4D Gaussians are ranked based on their
+ * spatial-temporal variation score S_i, and Gaussians with lower scores are
+ * pruned."  The kept set is the `keep` highest scores; equal scores are ranked
+ * by ascending index (reading R23).  out: bitmask (LSB-first words)
+ * of the kept Gaussians. */
+static const float *or_prune_scores;
+static int or_cmp_rank(const void *a, const void *b)
+{
+    const int i = *(const int *)a, j = *(const int *)b;
+    const float x = or_prune_scores[i], y = or_prune_scores[j];
+    if (x != y) return x > y ? -1 : 1;  /* higher score first */
+    return (i > j) - (i < j);           /* then lower index   */
+}
+
+void or_prune_mask(const float *score, int32_t n, int64_t keep, uint32_t *out)
+{
+    const int nw = (n + 31) / 32;
+    for (int w = 0; w < nw; ++w) out[w] = 0;
+    int *idx = (int *)malloc(sizeof(int) * (size_t)(n > 0 ? n : 1));
+    for (int i = 0; i < n; ++i) idx[i] = i;
+    or_prune_scores = score;
+    qsort(idx, (size_t)n, sizeof(int), or_cmp_rank);
+    for (int64_t r = 0; r < keep && r < n; ++r) out[idx[r] >> 5] |= 1u << (idx[r] & 31);
+    free(idx);
+}
+
 /* Sec. 4.2.2: key-frame schedule and bracketing. */
 int or_keyframes(int32_t frames, int32_t interval, int32_t *out)
 {

@@ -56,6 +56,7 @@ def load():
             lib.or_tile_lists.restype = C.c_int64
             lib.or_keyframe_mask.argtypes = [P, P, C.c_int32, C.c_float, P]
             lib.or_keyframe_mask_contrib.argtypes = [P, P, C.c_int32, C.c_float, C.c_double, P]
+            lib.or_prune_mask.argtypes = [P, C.c_int32, C.c_int64, P]
             lib.or_keyframes.argtypes = [C.c_int32, C.c_int32, P]
             lib.or_keyframes.restype = C.c_int
             lib.or_bracket.argtypes = [P, C.c_int32, C.c_int32, P, P]
@@ -215,6 +216,16 @@ def keyframe_mask_contrib(scene, cams, t_key, threshold=0.0):
     out = np.zeros(max((sr.s.n + 31) // 32, 1), np.uint32)
     lib.or_keyframe_mask_contrib(C.byref(sr.s), arr, len(cams), float(t_key), float(threshold), out.ctypes.data)
     return out[:(sr.s.n + 31) // 32]
+
+
+def prune_mask(score, keep):
+    """bitmask of the `keep` highest scores (ties by ascending index)."""
+    lib = load()
+    sc = np.ascontiguousarray(score, np.float32)
+    n = sc.shape[0]
+    out = np.zeros(max((n + 31) // 32, 1), np.uint32)
+    lib.or_prune_mask(sc.ctypes.data, n, int(keep), out.ctypes.data)
+    return out[:(n + 31) // 32]
 
 
 def keyframes(frames, interval):

@@ -178,3 +178,21 @@ def test_score_ablation_variants_closed_forms():
     s0 = oracle.stv_score(sc2, [cam], t, variant=0)
     s3 = oracle.stv_score(sc2, [cam], t, variant=3)
     assert s3["score"][0] == pytest.approx(2.0 * s0["score"][0], rel=1e-6)
+
+
+def test_prune_mask_ranking_rule():
+    """keep the highest scores; equal scores ranked by ascending index
+    (reading R23).  Hand example, the edges keep = 0 / n, and a brute-force
+    check against numpy's stable argsort on tie-heavy scores."""
+    s = np.float32([0.5, 2.0, 0.5, 3.0, 0.5, 1.0])
+    m = _bits(oracle.prune_mask(s, 3), 6)
+    assert m.tolist() == [False, True, False, True, False, True]
+    m = _bits(oracle.prune_mask(s, 4), 6)      # one of the three 0.5s: the lowest index
+    assert m.tolist() == [True, True, False, True, False, True]
+    assert not _bits(oracle.prune_mask(s, 0), 6).any() and _bits(oracle.prune_mask(s, 6), 6).all()
+    rng = np.random.default_rng(3)
+    s = np.round(rng.random(5000) * 20).astype(np.float32)   # many ties
+    for keep in (1, 777, 2500, 4999):
+        want = np.zeros(5000, bool)
+        want[np.argsort(-s, kind="stable")[:keep]] = True
+        assert np.array_equal(_bits(oracle.prune_mask(s, keep), 5000), want)
