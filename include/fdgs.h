@@ -348,6 +348,22 @@ fdgs_status fdgs_stv_score(const fdgs_scene *scene, const fdgs_camera *cams, int
                            int32_t n_ts, const fdgs_stv_opts *opts, float *d_out_score, float *d_out_spatial,
                            float *d_out_gamma, void *d_ws, size_t ws_bytes, uint32_t *h_max_entries, void *stream);
 
+/* Pruning selection (Sec. 4.2.1 "Pruning": "All 4D Gaussians are
+ * ranked based on their spatial-temporal variation score S_i, and Gaussians
+ * with lower scores are pruned"; SURVEY NEXT-f1 top-k select): bit i of
+ * d_out_mask (DEVICE uint32[ceil(n/32)], LSB-first, bits >= n zero) is set iff
+ * Gaussian i is among the `keep` highest d_score values (DEVICE float[n]);
+ * equal scores are ranked by ascending index (reading R23), -0 equals +0.
+ * Scores must not be NaN (the ranking is then undefined).  keep >= n keeps all,
+ * keep == 0 none.  Radix select (4 x 8-bit passes over the scores) + ordered
+ * tie emission; d_ws DEVICE workspace of fdgs_prune_workspace_bytes(n), no
+ * zero-fill needed.  The pruned scene is fdgs_scene_compact(scene, mask).
+ * ASYNC on `stream`.  Errors: INVALID_ARG (n < 0, keep < 0, NULL pointers),
+ * WORKSPACE_TOO_SMALL, CUDA. */
+size_t fdgs_prune_workspace_bytes(int32_t n);
+fdgs_status fdgs_prune_mask(const float *d_score, int32_t n, int64_t keep, uint32_t *d_out_mask, void *d_ws,
+                            size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

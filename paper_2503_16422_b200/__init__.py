@@ -17,6 +17,7 @@ from .api import (  # noqa: F401
     keyframes,
     log255_opacity,
     mask_compact,
+    prune_mask,
     mask_or,
     mask_words,
     stv_score,

@@ -25,7 +25,7 @@ EXPORTS = [
     "fdgs_keyframe_workspace_bytes", "fdgs_keyframe_mask", "fdgs_mask_or",
     "fdgs_keyframe_mask_contrib_workspace_bytes", "fdgs_keyframe_mask_contrib",
     "fdgs_mask_compact_workspace_bytes", "fdgs_mask_compact", "fdgs_stv_workspace_bytes", "fdgs_stv_score",
-    "fdgs_scene_compact_workspace_bytes", "fdgs_scene_compact",
+    "fdgs_scene_compact_workspace_bytes", "fdgs_scene_compact", "fdgs_prune_workspace_bytes", "fdgs_prune_mask",
 ]
 
 
@@ -106,6 +106,8 @@ def lib():
             "fdgs_scene_compact_workspace_bytes": ([I32], SZ),
             "fdgs_scene_compact": ([P, P, P, P, P, P, P, P, P, P, P, SZ, P], C.c_int),
             "fdgs_stv_score": ([P, P, I32, P, I32, P, P, P, P, P, SZ, P, P], C.c_int),
+            "fdgs_prune_workspace_bytes": ([I32], SZ),
+            "fdgs_prune_mask": ([P, I32, C.c_int64, P, P, SZ, P], C.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

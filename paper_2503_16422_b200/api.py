@@ -66,11 +66,15 @@ class Scene:
         self.struct = FdgsScene(self.n, *[self.t[f].data_ptr() for f in _FIELDS],
                                 self.t["sh_index"].data_ptr() if idx is not None else None, k, self.stride, None, 0)
 
-    def compact(self, mask_l: torch.Tensor, mask_r: torch.Tensor | None = None, stream=None) -> "Scene":
+    def compact(self, mask_l: torch.Tensor, mask_r: torch.Tensor | None = None, stream=None,
+                standalone: bool = False) -> "Scene":
         """fdgs_scene_compact: the working set of a key-frame window (the
         Gaussians of mask_l | mask_r, ascending) as a dense Scene whose records
         report the original indices.  Render it with no mask: frames equal the
-        masked renders of this scene bit for bit.  Synchronises once (count)."""
+        masked renders of this scene bit for bit.  Synchronises once (count).
+        standalone: a new scene in its own right (a pruned scene: records,
+        masks and scores index the kept Gaussians 0..m-1); `.kept` holds the
+        original indices either way."""
         if self.struct.gid:
             raise ValueError("already a compacted working set")
         n, dev = self.n, self.device
@@ -98,9 +102,21 @@ class Scene:
             out.t["sh_index"] = sh_index[:m]
         out.struct = FdgsScene(m, *[out.t[f].data_ptr() for f in _FIELDS],
                                out.t["sh_index"].data_ptr() if vq else None,
-                               int(self.t["sh"].shape[0]) if vq else 0, 4, gid.data_ptr(), n)
+                               int(self.t["sh"].shape[0]) if vq else 0, 4,
+                               None if standalone else gid.data_ptr(), 0 if standalone else n)
         out.source = self
+        out.kept = gid[:m]
+        if standalone:
+            del out.t["gid"]
         return out
+
+    def prune(self, score: torch.Tensor, keep: int, stream=None) -> "Scene":
+        """Pruning of Sec. 4.2.1: the scene of the `keep` highest-scored
+        Gaussians (fdgs_prune_mask, ties by ascending index), compacted in index
+        order (fdgs_scene_compact).  `.kept` = their original indices."""
+        if self.struct.gid:
+            raise ValueError("prune the full scene, not a working set")
+        return self.compact(prune_mask(score, self.n, keep, stream=stream), stream=stream, standalone=True)
 
     @classmethod
     def from_arrays(cls, arrays, device=None):
@@ -483,6 +499,18 @@ def mask_compact(a: torch.Tensor, n: int, b: torch.Tensor | None = None, stream=
     check(lib().fdgs_mask_compact(_ptr(a), _ptr(b), int(n), _ptr(idx), _ptr(cnt), _ptr(ws), nb, _stream_ptr(stream)))
     k = int(cnt.item())
     return idx[:k]
+
+
+def prune_mask(score: torch.Tensor, n: int, keep: int, out=None, stream=None) -> torch.Tensor:
+    """fdgs_prune_mask: bitmask of the `keep` highest scores, ties by
+    ascending index.  Asynchronous."""
+    if score.dtype != torch.float32 or not score.is_cuda or not score.is_contiguous():
+        raise ValueError("score must be a contiguous CUDA float32 tensor")
+    out = torch.empty(max(mask_words(n), 1), dtype=torch.int32, device=score.device) if out is None else out
+    nb = lib().fdgs_prune_workspace_bytes(int(n))
+    ws = torch.empty(nb, dtype=torch.uint8, device=score.device)
+    check(lib().fdgs_prune_mask(_ptr(score), int(n), int(keep), _ptr(out), _ptr(ws), nb, _stream_ptr(stream)))
+    return out
 
 
 def stv_score(scene: Scene, cams, ts, percentile: float = 0.9, combine: int = 0, spatial: bool = False,

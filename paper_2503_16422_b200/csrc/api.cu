@@ -536,6 +536,18 @@ fdgs_status fdgs_mask_compact(const uint32_t *d_a, const uint32_t *d_b, int32_t 
     return e == cudaSuccess ? FDGS_OK : cuda_fail(e, "fdgs_mask_compact");
 }
 
+size_t fdgs_prune_workspace_bytes(int32_t n) { return n < 0 ? 0 : prune_workspace_bytes(n); }
+
+fdgs_status fdgs_prune_mask(const float *d_score, int32_t n, int64_t keep, uint32_t *d_out_mask, void *d_ws,
+                            size_t ws_bytes, void *stream) {
+    if (n < 0 || keep < 0 || (n > 0 && (d_score == nullptr || d_out_mask == nullptr)))
+        return fail(FDGS_ERR_INVALID_ARG, "bad args");
+    if (d_ws == nullptr || ws_bytes < prune_workspace_bytes(n))
+        return fail(FDGS_ERR_WORKSPACE_TOO_SMALL, "prune workspace needs %zu bytes", prune_workspace_bytes(n));
+    cudaError_t e = launch_prune_mask(d_score, n, keep, d_out_mask, reinterpret_cast<char *>(d_ws), (cudaStream_t)stream);
+    return e == cudaSuccess ? FDGS_OK : cuda_fail(e, "fdgs_prune_mask");
+}
+
 size_t fdgs_stv_workspace_bytes(int32_t n, const fdgs_camera *cams, int32_t n_cams, int64_t max_entries) {
     if (n < 0 || cams == nullptr || n_cams < 1 || max_entries < 0) return 0;
     for (int c = 0; c < n_cams; ++c)

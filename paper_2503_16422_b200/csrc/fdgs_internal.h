@@ -100,6 +100,10 @@ cudaError_t launch_stv(const SceneDev &sc, const CamDev *cams, const fdgs_camera
                        const StvLayout &SL, float *out_score, float *out_spatial, float *out_gamma,
                        cudaStream_t st);
 
+__global__ void k_count_scan(uint32_t *__restrict__ cnt, int parts_ub, const uint32_t *items, int per_part,
+                             uint32_t *total);
+size_t prune_workspace_bytes(int32_t n);
+cudaError_t launch_prune_mask(const float *score, int n, int64_t keep, uint32_t *mask, char *ws, cudaStream_t st);
 cudaError_t launch_keyframe_contrib(const SceneDev &sc, const CamDev *cams, const fdgs_camera *hcams, int n_cams,
                                     float t_key, unsigned long long thr_fixed, int64_t max_entries, char *ws,
                                     const StvLayout &SL, uint32_t *out_mask, cudaStream_t st);

@@ -146,6 +146,115 @@ __global__ void __launch_bounds__(256) k_contrib_mask(unsigned long long *__rest
     if ((threadIdx.x & 31) == 0 && i < n && word) mask[i >> 5] |= word;
 }
 
+// ---- pruning selection: keep the `keep` highest scores, equal
+// scores ranked by ascending index (reading R23).
+//
+// key = the score's bits remapped so that ascending key = descending score
+// (-0 folded onto +0, so equal values have equal keys).  A 4 x 8-bit MSD radix
+// select finds T = the key of rank keep-1 and the remaining rank r within T's
+// equal range; then per 1024-element chunk the count of keys == T, a one-block
+// scan of the counts, and the emission: bit i = key_i < T, or key_i == T and
+// i is among the first r+1 indices holding T.
+constexpr int kPruneChunk = 1024;
+
+__device__ __forceinline__ uint32_t prune_key(float s) {
+    uint32_t b = __float_as_uint(s);
+    if ((b << 1) == 0u) b = 0u;
+    const uint32_t ord = (b & 0x80000000u) ? ~b : (b | 0x80000000u);  // ascending in value
+    return ~ord;
+}
+
+__global__ void __launch_bounds__(256) k_prune_hist(const float *__restrict__ score, int n, StvState *st,
+                                                    int shift) {
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t hi = shift >= 24 ? 0u : ~0u << (shift + 8);
+    const uint32_t prefix = st->prefix;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t k = prune_key(__ldg(score + i));
+        if (((k ^ prefix) & hi) == 0) atomicAdd(&h[(k >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (h[threadIdx.x]) atomicAdd(&st->hist[threadIdx.x], h[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(256) k_prune_count(const float *__restrict__ score, int n, const StvState *st,
+                                                     uint32_t *__restrict__ cnt) {
+    __shared__ uint32_t s_n;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    const uint32_t T = st->prefix;
+    uint32_t c = 0;
+    for (int r = 0; r < kPruneChunk / 256; ++r) {
+        const int i = blockIdx.x * kPruneChunk + r * 256 + threadIdx.x;
+        c += __popc(__ballot_sync(0xffffffffu, i < n && prune_key(__ldg(score + i)) == T));
+    }
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_n, c);
+    __syncthreads();
+    if (threadIdx.x == 0) cnt[blockIdx.x] = s_n;
+}
+
+// all: keep >= n (every bit below n set, T unused).
+__global__ void __launch_bounds__(256) k_prune_emit(const float *__restrict__ score, int n, const StvState *st,
+                                                    const uint32_t *__restrict__ base, bool all,
+                                                    uint32_t *__restrict__ mask) {
+    __shared__ uint32_t s_w[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t T = all ? 0u : st->prefix;
+    const uint32_t r = all ? 0u : st->rank;  // T-valued elements kept: the first r + 1
+    uint32_t carry = all ? 0u : base[blockIdx.x];
+    for (int k = 0; k < kPruneChunk / 256; ++k) {
+        const int i = blockIdx.x * kPruneChunk + k * 256 + tid;
+        const uint32_t key = i < n ? prune_key(__ldg(score + i)) : 0xffffffffu;
+        const bool eq = i < n && key == T;
+        const uint32_t be = __ballot_sync(0xffffffffu, eq);
+        if (lane == 0) s_w[warp] = __popc(be);
+        __syncthreads();
+        uint32_t before = carry, tot = 0;
+        for (int w = 0; w < 8; ++w) {
+            if (w < warp) before += s_w[w];
+            tot += s_w[w];
+        }
+        __syncthreads();
+        const uint32_t pos = before + __popc(be & ((1u << lane) - 1u));  // rank among T-valued, by index
+        const bool set = i < n && (all || key < T || (eq && pos <= r));
+        const uint32_t word = __ballot_sync(0xffffffffu, set);
+        if (lane == 0 && i < n) mask[i >> 5] = word;
+        carry += tot;
+    }
+}
+
+size_t prune_workspace_bytes(int32_t n) {
+    const size_t chunks = (size_t)(std::max(n, 0) + kPruneChunk - 1) / kPruneChunk;
+    return ((sizeof(StvState) + 255) & ~size_t(255)) + ((4 * std::max<size_t>(chunks, 1) + 255) & ~size_t(255));
+}
+
+cudaError_t launch_prune_mask(const float *score, int n, int64_t keep, uint32_t *mask, char *ws, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    if (keep <= 0) return cudaMemsetAsync(mask, 0, 4 * (size_t)((n + 31) / 32), st);
+    StvState *state = reinterpret_cast<StvState *>(ws);
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(ws + ((sizeof(StvState) + 255) & ~size_t(255)));
+    const int chunks = (n + kPruneChunk - 1) / kPruneChunk;
+    if (keep >= n) {
+        k_prune_emit<<<chunks, 256, 0, st>>>(score, n, state, cnt, true, mask);
+        return cudaGetLastError();
+    }
+    k_stv_init<<<1, 256, 0, st>>>(state, (uint32_t)(keep - 1));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int hgrid = std::max(1, std::min((n + 255) / 256, 4 * sms));
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        k_prune_hist<<<hgrid, 256, 0, st>>>(score, n, state, shift);
+        k_vol_pick<<<1, 256, 0, st>>>(state, shift);
+    }
+    k_prune_count<<<chunks, 256, 0, st>>>(score, n, state, cnt);
+    k_count_scan<<<1, 1024, 0, st>>>(cnt, chunks, nullptr, 0, &state->info[0]);
+    k_prune_emit<<<chunks, 256, 0, st>>>(score, n, state, cnt, false, mask);
+    return cudaGetLastError();
+}
+
 StvLayout stv_layout(int32_t n, const fdgs_camera *cams, int32_t n_cams, int64_t max_entries) {
     StvLayout L{};
     const size_t nn = (size_t)std::max(n, 1);

@@ -57,15 +57,16 @@ def pruning_study(name, ratios=(0.0, 0.5, 0.8, 0.9), t_stride=10):
     times = fi.frame_times(F)
     sc = fd.Scene.from_arrays(scene)
     t0 = time.perf_counter()
-    score = fd.stv_score(sc, cams, [float(x) for x in times[::t_stride]])["score"].cpu().numpy()
+    score = fd.stv_score(sc, cams, [float(x) for x in times[::t_stride]])["score"]
     score_s = time.perf_counter() - t0
-    order = np.argsort(-score, kind="stable")
     seq = [(f, c) for f in range(0, F, 5) for c in range(0, len(cams), 4)]
     out = {"config": name, "n": scene.n, "score_views": len(cams) * len(times[::t_stride]),
            "score_s": round(score_s, 3), "curve": []}
     for r in ratios:
-        keep = np.sort(order[: max(1, int(round(scene.n * (1.0 - r))))])
-        sub = fd.Scene.from_arrays(scene.subset(keep))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sub = sc.prune(score, max(1, int(round(scene.n * (1.0 - r)))))  # fdgs_prune_mask + fdgs_scene_compact
+        prune_s = time.perf_counter() - t0
         kf = fd.keyframes(F, cfg["keyframe_interval"])
         masks = [fd.keyframe_mask(sub, cams, float(times[k])) for k in kf]
         pipe = fd.RenderPipeline(sub, cams[0].width, cams[0].height, depth=4)
@@ -75,7 +76,8 @@ def pruning_study(name, ratios=(0.0, 0.5, 0.8, 0.9), t_stride=10):
             lo, hi = fd.bracket(kf, f)
             frames.append((fd.camera_struct(cams[c]), float(times[f]), masks[lo], masks[hi]))
         fps_of(pipe, frames, outs, reps=1)
-        out["curve"].append({"prune_ratio": r, "n": int(keep.size), "fps_masked": round(fps_of(pipe, frames, outs), 1)})
+        out["curve"].append({"prune_ratio": r, "n": sub.n, "prune_s": round(prune_s, 4),
+                             "fps_masked": round(fps_of(pipe, frames, outs), 1)})
         del pipe, outs, sub, masks
         torch.cuda.empty_cache()
     return out
