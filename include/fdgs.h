@@ -226,7 +226,9 @@ fdgs_status fdgs_render_graph_destroy(fdgs_render_graph *graph);
  * temporal cull (survivor order = ascending Gaussian index); only the slots of
  * visible Gaussians hold data, and vis uint32[n_vis] lists them ascending:
  *   rec0 float4 {u, v, A', B'}, rec1 float4 {C', Q2, aabb_x, aabb_y}
- *   (aabb_x = px0 | px1 << 16 as int bits), rec2 float4 {r, g, b, gid bits},
+ *   (aabb_x = px0 | px1 << 16 as int bits, aabb_y likewise with bit 31 set
+ *   when the per-pixel AABB test is provably redundant for the record),
+ *   rec2 float4 {r, g, b, gid bits},
  *   depth uint32 (fp32 bits of camera z), order uint32[n_vis] (slots in
  *   canonical (depth, index) order), tile_start uint32[n_tiles + 1],
  *   entries uint32[E] (slots, per tile in canonical order). */

@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <new>
+#include <type_traits>
 #include <vector>
 
 #include "fdgs_internal.h"
@@ -173,6 +174,31 @@ __global__ void __launch_bounds__(kPreBlock) k_cull_emit(const uint32_t *__restr
 #ifndef FDGS_SLICE_MINB
 #define FDGS_SLICE_MINB 3
 #endif
+
+// Is the pixel-AABB test redundant for this record?  True if every pixel centre
+// of the image whose pinned fp32 e2 chain (DESIGN.md §3 step 10) can reach
+// e2 >= 0 lies inside the AABB.  The chain has 7 roundings, each <= 2^-24 of a
+// term bounded by |A'|dx^2 + |B'||dx dy| + |C'|dy^2 + |Q2|, so fp32 e2 <= the
+// exact quadratic with A', C' scaled by (1 - d), |B'| by (1 + d), Q2 raised by
+// d|Q2|, d = 2^-19 (> 9 x 2^-24 with slack); that quadratic's superlevel set
+// {>= 0} lies in the box u +- dxm, v +- dym (dxm^2 = -4C''Q''/K'',
+// K'' = 4A''C'' - B''^2, for either sign of B''), evaluated in binary64 and
+// widened by 2^-30.  The blend then skips the per-pixel AABB test for lists of
+// such records (bit 31 of rec1.w; results identical by construction).
+__device__ __forceinline__ bool aabb_redundant(const Proj &pj, int W, int H) {
+    constexpr double d = 0x1p-19, s = 1.0 + 0x1p-30;
+    const double A = (double)pj.Ap * (1.0 - d), C = (double)pj.Cp * (1.0 - d);
+    const double B = fabs((double)pj.Bp) * (1.0 + d), Q = (double)pj.Q2 + d * fabs((double)pj.Q2);
+    if (Q < 0.0) return true;  // no pixel reaches e2 >= 0
+    const double K = 4.0 * A * C - B * B;
+    if (!(K > 0.0) || !(A < 0.0) || !(C < 0.0)) return false;
+    const double dxm = sqrt((-4.0 * C * Q) / K) * s + 0x1p-30, dym = sqrt((-4.0 * A * Q) / K) * s + 0x1p-30;
+    const double u = pj.u, v = pj.v;
+    const double cx0 = fmax(ceil(u - dxm - 0.5), 0.0), cx1 = fmin(floor(u + dxm - 0.5), W - 1.0);
+    const double cy0 = fmax(ceil(v - dym - 0.5), 0.0), cy1 = fmin(floor(v + dym - 0.5), H - 1.0);
+    if (cx0 > cx1 || cy0 > cy1) return true;
+    return cx0 >= pj.px0 && cx1 <= pj.px1 && cy0 >= pj.py0 && cy1 <= pj.py1;
+}
 __global__ void __launch_bounds__(kPreBlock, FDGS_SLICE_MINB) k_slice(SceneDev sc, CamDev cam, float t, Counters *ctr,
                                                      const uint32_t *__restrict__ surv, float4 *__restrict__ rec0,
                                                      float4 *__restrict__ rec1, float4 *__restrict__ rec2,
@@ -207,7 +233,8 @@ __global__ void __launch_bounds__(kPreBlock, FDGS_SLICE_MINB) k_slice(SceneDev s
                     sh_color(sc.sh + row * 12, mx - cam.campos[0], my - cam.campos[1], mz - cam.campos[2], rgb);
                     const uint32_t ax = pj.px0 | (pj.px1 << 16), ay = pj.py0 | (pj.py1 << 16);
                     rec0[sidx] = make_float4(pj.u, pj.v, pj.Ap, pj.Bp);
-                    rec1[sidx] = make_float4(pj.Cp, pj.Q2, __uint_as_float(ax), __uint_as_float(ay));
+                    const uint32_t inside = aabb_redundant(pj, cam.width, cam.height) ? 0x80000000u : 0u;
+                    rec1[sidx] = make_float4(pj.Cp, pj.Q2, __uint_as_float(ax), __uint_as_float(ay | inside));
                     rec2[sidx] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(sc.orig(i)));
                     depth[sidx] = pj.depth_bits;
                     rect[sidx] = make_uint2(ax, ay);
@@ -916,7 +943,7 @@ __device__ __forceinline__ void stage_fields(int tx, int ty, const float4 &r0, c
                                              float4 &oa, float4 &oc, float4 &od) {
     const uint32_t ax = __float_as_uint(r1.z), ay = __float_as_uint(r1.w);
     const int x0 = max((int)(ax & 0xffff) - tx * 16, 0), x1 = min((int)(ax >> 16) - tx * 16, 15);
-    const int y0 = max((int)(ay & 0xffff) - ty * 16, 0), y1 = min((int)(ay >> 16) - ty * 16, 15);
+    const int y0 = max((int)(ay & 0xffff) - ty * 16, 0), y1 = min((int)((ay >> 16) & 0x7fffu) - ty * 16, 15);
     const uint32_t xm = ((2u << x1) - 1u) & ~((1u << x0) - 1u);
     const uint32_t ym = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
     uint32_t yr = 0;
@@ -1247,7 +1274,7 @@ __device__ __forceinline__ uint32_t stage_groups(int tx, int ty, const float4 &r
                                                  uint32_t &mbits) {
     const uint32_t ax = __float_as_uint(r1.z), ay = __float_as_uint(r1.w);
     const int x0 = max((int)(ax & 0xffff) - tx * 16, 0), x1 = min((int)(ax >> 16) - tx * 16, 15);
-    const int y0 = max((int)(ay & 0xffff) - ty * 16, 0), y1 = min((int)(ay >> 16) - ty * 16, 15);
+    const int y0 = max((int)(ay & 0xffff) - ty * 16, 0), y1 = min((int)((ay >> 16) & 0x7fffu) - ty * 16, 15);
     const uint32_t xm = ((2u << x1) - 1u) & ~((1u << x0) - 1u);
     const uint32_t ym = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
     mbits = ~(xm | (ym << 16));
@@ -1270,12 +1297,13 @@ __device__ __forceinline__ uint32_t stage_groups(int tx, int ty, const float4 &r
 #define FDGS_WL_BUF 2
 #endif
 constexpr int kWlBuf = FDGS_WL_BUF;
+// Two 16-byte loads per record for a consumer thread: the common part and its
+// row's part (colour b and the mask repeated per row).
 struct WlEntry {
-    float4 a;            // u, A', ~AABB mask bits, r
-    float4 c;            // g, b, q (record of the batch), -
-    float2 t[kWlRows];   // {t1, t4} of the warp's rows
+    float4 a;            // u, A', r, g
+    float4 t[kWlRows];   // per row of the warp: b, ~AABB mask bits, t1, t4
 };
-static_assert(sizeof(WlEntry) == 32 + 8 * kWlRows, "WlEntry layout");
+static_assert(sizeof(WlEntry) == 16 + 16 * kWlRows, "WlEntry layout");
 
 #ifndef FDGS_WL_MINB
 #define FDGS_WL_MINB 7
@@ -1284,6 +1312,11 @@ static_assert(sizeof(WlEntry) == 32 + 8 * kWlRows, "WlEntry layout");
 #define FDGS_WL_UNROLL 4
 #endif
 constexpr int kWlUnroll = FDGS_WL_UNROLL;
+#ifndef FDGS_WL_MASKFREE
+#define FDGS_WL_MASKFREE 1
+#endif
+constexpr bool kWlMaskFree = FDGS_WL_MASKFREE;  // mask-free loop for lists of aabb_redundant records
+constexpr float kStopU = 1e-4f / 255.0f;  // the stop threshold 1e-4 on T, on U = T / 255
 __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uint32_t *__restrict__ tile_start,
                                                          const uint32_t *__restrict__ entries,
                                                          const float4 *__restrict__ rec0,
@@ -1293,10 +1326,12 @@ __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uin
                                                          float bg2, float *__restrict__ out_rgb,
                                                          float *__restrict__ out_T) {
     __shared__ WlEntry s_list[kWlBuf][4][32];
-    __shared__ uint32_t s_cnt[kWlBuf][4];     // list length per consumer warp; [.][0] bit 31 = end of tile
+    // list length per consumer warp; [.][0] bit 31 = end of tile; bit 30: some
+    // record of the list needs the per-pixel AABB test
+    __shared__ uint32_t s_cnt[kWlBuf][4];
     __shared__ __align__(8) uint64_t full[kWlBuf], empty[kWlBuf];
     __shared__ uint32_t s_done;
-    constexpr uint32_t kEnd = 0x80000000u;
+    constexpr uint32_t kEnd = 0x80000000u, kMasked = 0x40000000u;
     const bool ok = ctr->status == FDGS_OK;
     const int tile = blockIdx.x, tx = tile % tiles_x, ty = tile / tiles_x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1325,27 +1360,33 @@ __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uin
                 r0 = __ldg(rec0 + v);
                 r1 = __ldg(rec1 + v);
                 r2 = __ldg(rec2 + v);
-                groups = stage_groups(tx, ty, r0, r1, mb);
             }
+            if (lane < (int)n) groups = stage_groups(tx, ty, r0, r1, mb);
             const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
             const float mbits = __uint_as_float(mb);
+            const bool redundant = (__float_as_uint(r1.w) & 0x80000000u) != 0u;  // aabb_redundant (k_slice)
 #pragma unroll
             for (int w = 0; w < 4; ++w) {  // per consumer warp: packed list + its rows' e2 row terms
                 const bool reach = lane < (int)n && ((groups >> w) & 1u) != 0u;
                 const uint32_t bal = __ballot_sync(0xffffffffu, reach);
+                // the AABB test matters for warp w unless proven redundant or the
+                // AABB covers the warp's footprint
+                const uint32_t foot = (((2u << (wl_col0(w) + kWlCols - 1)) - 1u) & ~((1u << wl_col0(w)) - 1u)) |
+                                      (((1u << kWlRows) - 1u) << (16 + wl_row0(w)));
+                const bool masked = __any_sync(0xffffffffu, reach && !redundant && (mb & foot) != 0u);
                 if (reach) {
                     WlEntry &E = s_list[b][w][__popc(bal & lanemask_lt())];
-                    E.a = make_float4(u, Ap, mbits, r2.x);
-                    E.c = make_float4(r2.y, r2.z, __int_as_float(lane), 0.f);
+                    E.a = make_float4(u, Ap, r2.x, r2.y);
 #pragma unroll
                     for (int r = 0; r < kWlRows; ++r) {  // pinned e2 chain, row terms (DESIGN.md step 10)
                         const float dy = __fsub_rn((float)(ty * 16 + wl_row0(w) + r) + 0.5f, v);
                         const float t1 = __fmul_rn(Bp, dy);
                         const float t3 = __fmul_rn(Cp, dy);
-                        E.t[r] = make_float2(t1, __fmaf_rn(t3, dy, Q2));
+                        E.t[r] = make_float4(r2.z, mbits, t1, __fmaf_rn(t3, dy, Q2));
                     }
                 }
-                if (lane == w) s_cnt[b][w] = (uint32_t)__popc(bal) | (n == 0 ? kEnd : 0u);
+                if (lane == w)
+                    s_cnt[b][w] = (uint32_t)__popc(bal) | (n == 0 ? kEnd : 0u) | (kWlMaskFree && !masked ? 0u : kMasked);
             }
             __syncwarp();
             if (lane == 0) mb_arrive(&full[b]);
@@ -1360,7 +1401,52 @@ __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uin
         const uint32_t pb0 = (1u << lx) | (1u << (16 + ly)), pb1 = (2u << lx) | (1u << (16 + ly));
         const float kInf = __int_as_float(0x7f800000);
         float2 thr = make_float2(in0 ? 0.0f : kInf, in1 ? 0.0f : kInf);
-        float2 T = make_float2(1.0f, 1.0f), Cr = make_float2(0.f, 0.f), Cg = Cr, Cb = Cr;
+        // U = T / 255: w = min(2^e2, 0.99 * 255) U = alpha T without the 1/255
+        // multiply; a stop decision (T - w < 1e-4, i.e. U - w/255 < 1e-4/255)
+        // undoes the step in a rare branch instead of selecting every record.
+        float2 T = make_float2(kInv255, kInv255), Cr = make_float2(0.f, 0.f), Cg = Cr, Cb = Cr;
+        // one record (q) of the list; kAabb: apply the per-pixel AABB test
+        auto step = [&](const WlEntry *E, const float4 *Tp, int q, auto kAabb) {
+            const float4 a = E[q].a;
+            const float4 rt = *reinterpret_cast<const float4 *>(reinterpret_cast<const char *>(Tp) + q * sizeof(WlEntry));
+            asm volatile("" : "+f"(px.x), "+f"(px.y));
+            const float2 dx = sub2(px, make_float2(a.x, a.x));
+            const float2 t2 = fma2(make_float2(a.y, a.y), dx, make_float2(rt.z, rt.z));
+            const float2 e2 = fma2(dx, t2, make_float2(rt.w, rt.w));
+            bool v0 = e2.x >= thr.x, v1 = e2.y >= thr.y;
+            if constexpr (decltype(kAabb)::value) {
+                const uint32_t m = __float_as_uint(rt.y);
+                v0 = v0 && (m & pb0) == 0u;
+                v1 = v1 && (m & pb1) == 0u;
+            }
+            const float m0 = v0 ? fminf(ex2_approx(e2.x), kAlphaPre) : 0.0f;
+            const float m1 = v1 ? fminf(ex2_approx(e2.y), kAlphaPre) : 0.0f;
+            const float2 w = mul2(make_float2(m0, m1), T);
+            const float2 Tprev = T;
+            T = fma2(make_float2(-kInv255, -kInv255), w, T);
+            Cr = fma2(make_float2(a.z, a.z), w, Cr);
+            Cg = fma2(make_float2(a.w, a.w), w, Cg);
+            Cb = fma2(make_float2(rt.x, rt.x), w, Cb);
+            // T >= kStopU holds before every step (a stop restores it), so only
+            // a blended record can bring T below the threshold
+            const bool s0 = T.x < kStopU, s1 = T.y < kStopU;
+            if (__builtin_expect(s0 || s1, 0)) {
+                if (s0) {
+                    Cr.x = fmaf(-a.z, w.x, Cr.x);
+                    Cg.x = fmaf(-a.w, w.x, Cg.x);
+                    Cb.x = fmaf(-rt.x, w.x, Cb.x);
+                    T.x = Tprev.x;
+                    thr.x = kInf;
+                }
+                if (s1) {
+                    Cr.y = fmaf(-a.z, w.y, Cr.y);
+                    Cg.y = fmaf(-a.w, w.y, Cg.y);
+                    Cb.y = fmaf(-rt.x, w.y, Cb.y);
+                    T.y = Tprev.y;
+                    thr.y = kInf;
+                }
+            }
+        };
         bool wdone = __all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf);
         if (wdone && lane == 0) atomicAdd(&s_done, 1u);
         for (uint32_t k = 0;; ++k) {
@@ -1369,35 +1455,15 @@ __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uin
             const uint32_t cw = s_cnt[b][warp];
             if (s_cnt[b][0] & kEnd) break;
             if (!wdone) {
-                const int cnt = (int)(cw & ~kEnd);
+                const int cnt = (int)(cw & 0xffffu);
                 const WlEntry *E = &s_list[b][warp][0];
-                const float2 *Tp = &s_list[b][warp][0].t[rr];
+                const float4 *Tp = &s_list[b][warp][0].t[rr];
+                if (cw & kMasked) {
 #pragma unroll kWlUnroll
-                for (int q = 0; q < cnt; ++q) {
-                    const float4 a = E[q].a;
-                    const float2 gb = *reinterpret_cast<const float2 *>(&E[q].c);
-                    const float2 tt = *reinterpret_cast<const float2 *>(reinterpret_cast<const char *>(Tp) +
-                                                                         q * sizeof(WlEntry));
-                    const float4 col = make_float4(a.w, gb.x, gb.y, 0.f);
-                    asm volatile("" : "+f"(px.x), "+f"(px.y));
-                    const uint32_t m = __float_as_uint(a.z);
-                    const float2 dx = sub2(px, make_float2(a.x, a.x));
-                    const float2 t2 = fma2(make_float2(a.y, a.y), dx, make_float2(tt.x, tt.x));
-                    const float2 e2 = fma2(dx, t2, make_float2(tt.y, tt.y));
-                    const bool v0 = (m & pb0) == 0u && e2.x >= thr.x, v1 = (m & pb1) == 0u && e2.y >= thr.y;
-                    const float m0 = v0 ? fminf(ex2_approx(e2.x), kAlphaPre) : 0.0f;
-                    const float m1 = v1 ? fminf(ex2_approx(e2.y), kAlphaPre) : 0.0f;
-                    float2 w = mul2(mul2(make_float2(m0, m1), make_float2(kInv255, kInv255)), T);
-                    const float2 test = sub2(T, w);
-                    const bool s0 = v0 && test.x < 1e-4f, s1 = v1 && test.y < 1e-4f;
-                    w.x = s0 ? 0.0f : w.x;
-                    w.y = s1 ? 0.0f : w.y;
-                    thr.x = s0 ? kInf : thr.x;
-                    thr.y = s1 ? kInf : thr.y;
-                    T = sub2(T, w);
-                    Cr = fma2(make_float2(col.x, col.x), w, Cr);
-                    Cg = fma2(make_float2(col.y, col.y), w, Cg);
-                    Cb = fma2(make_float2(col.z, col.z), w, Cb);
+                    for (int q = 0; q < cnt; ++q) step(E, Tp, q, std::true_type{});
+                } else {
+#pragma unroll kWlUnroll
+                    for (int q = 0; q < cnt; ++q) step(E, Tp, q, std::false_type{});
                 }
                 wdone = __all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf);
                 if (wdone && lane == 0) atomicAdd(&s_done, 1u);
@@ -1405,6 +1471,7 @@ __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uin
             __syncwarp();
             if (lane == 0) mb_arrive(&empty[b]);
         }
+        T = mul2(T, make_float2(255.0f, 255.0f));
         if (ok && out_rgb != nullptr) {
             const size_t hw = (size_t)width * height, p = (size_t)j * width + i0;
             if (in0) {

@@ -45,7 +45,7 @@ def gpu_records(views):
     gid = r2[:, 3].view(np.int32).copy()
     ax = r1[:, 2].view(np.uint32)
     ay = r1[:, 3].view(np.uint32)
-    rect = np.stack([ax & 0xFFFF, ax >> 16, ay & 0xFFFF, ay >> 16], 1).astype(np.int32)
+    rect = np.stack([ax & 0xFFFF, ax >> 16, ay & 0xFFFF, (ay >> 16) & 0x7FFF], 1).astype(np.int32)
     f32 = np.stack([r0[:, 0], r0[:, 1], r0[:, 2], r0[:, 3], r1[:, 0], r1[:, 1]], 1)
     depth = views["depth"].cpu().numpy().view(np.uint32)
     order = views["order"].cpu().numpy()

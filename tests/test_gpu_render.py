@@ -427,3 +427,41 @@ def test_cuda_graph_frames_equal_launched_frames():
     torch.cuda.synchronize()
     for ref, o in zip(refs, outs):
         assert torch.equal(ref, o)
+
+
+def test_aabb_redundant_flag_sound():
+    """k_slice's aabb_redundant bit (rec1.w bit 31): for every flagged record of
+    a C2 frame, no pixel centre outside the pixel AABB has e2 >= 0.  e2 is
+    evaluated in binary64 from the fp32 record fields with the pinned chain's
+    rounding budget (9 x 2^-24 of the absolute terms) added, over every pixel of
+    the image outside the AABB within the record's tile-cover box + 2 px.  Also
+    checks that the flag holds for the bulk of the records (the mask-free blend
+    loop is the common case)."""
+    scene = fi.make_scene("c2")
+    cam = fi.make_cameras("c2")[3]
+    t = 0.5
+    _, _, _, r = _render(scene, cam, t)
+    v = r.debug_views()
+    n = v["n_vis"]
+    r0 = v["rec0"].cpu().numpy().astype(np.float64)
+    r1 = v["rec1"].cpu().numpy()
+    ax = r1[:, 2].view(np.uint32)
+    ay = r1[:, 3].view(np.uint32)
+    flag = (ay >> 31) == 1
+    assert r0.shape[0] == n and flag.mean() > 0.9, flag.mean()
+    px0, px1, py0, py1 = ax & 0xFFFF, ax >> 16, ay & 0xFFFF, (ay >> 16) & 0x7FFF
+    u, vv, A, B = r0.T
+    C, Q2 = r1[:, 0].astype(np.float64), r1[:, 1].astype(np.float64)
+    budget = 9 * 2.0 ** -24
+    checked = 0
+    for i in np.nonzero(flag)[0][::7]:
+        x0, x1 = max(int(px0[i]) - 40, 0), min(int(px1[i]) + 40, cam.width - 1)
+        y0, y1 = max(int(py0[i]) - 40, 0), min(int(py1[i]) + 40, cam.height - 1)
+        X, Y = np.meshgrid(np.arange(x0, x1 + 1) + 0.5 - u[i], np.arange(y0, y1 + 1) + 0.5 - vv[i])
+        q = A[i] * X * X + B[i] * X * Y + C[i] * Y * Y + Q2[i]
+        err = budget * (abs(A[i]) * X * X + abs(B[i]) * abs(X * Y) + abs(C[i]) * Y * Y + abs(Q2[i]))
+        gx, gy = np.meshgrid(np.arange(x0, x1 + 1), np.arange(y0, y1 + 1))
+        outside = (gx < px0[i]) | (gx > px1[i]) | (gy < py0[i]) | (gy > py1[i])
+        assert not np.any(outside & (q + err >= 0.0)), i
+        checked += 1
+    assert checked > 100
