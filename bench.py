@@ -75,7 +75,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-stage-events", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
-    p.add_argument("--streams", type=int, default=4, help="frame-pipelining depth (workspaces/streams)")
+    p.add_argument("--streams", type=int, default=6, help="frame-pipelining depth (workspaces/streams)")
     p.add_argument("--no-split", action="store_true", help="blend on the front-end stream (no priority split)")
     p.add_argument("--config", choices=["c2", "c3", "c4"], default="c3")
     p.add_argument("--unmasked", action="store_true", help="render without the key-frame filter")
