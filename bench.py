@@ -32,11 +32,11 @@ sys.path.insert(0, ROOT)
 METRIC = "frames/sec at 1352x1014 (N3V-shaped 200k-Gaussian masked scene)"
 UNIT = "frames/s"
 CONFIG = "c3"
-BLEND_KERNEL = "k_blend_wl"
+BLEND_KERNEL = "k_blend_wi"
 # launches of libfdgs kernels per frame (render.cu launch_render, tile grid <= 256 rows):
 # k_cull, k_count_scan, k_cull_emit, k_slice, k_count_scan, k_vis_emit, k_sort_hist,
 # 4 x k_onesweep (depth), k_bin_count, k_count_scan, k_bin_offsets, k_row_items, k_row_scan,
-# k_onesweep (rows), k_row_count, k_tile_scan, k_row_scatter, k_blend_wl
+# k_onesweep (rows), k_row_count, k_tile_scan, k_row_scatter, k_blend_wi
 KERNELS_PER_FRAME = 21  # the timed blend (render.cu); k_blend_ws<true> supplies the work counters
 N_CAMS = 20
 N_FRAMES_T = 300

@@ -202,7 +202,7 @@ fdgs_status fdgs_render_checked(const fdgs_scene *scene, const uint32_t *d_mask_
  * updated (scene, masks, t, camera, outputs).  Front-end nodes carry the
  * device's greatest stream priority and the blend its least (as
  * fdgs_render_split), so graphs of several workspaces on several streams
- * interleave.  The blend is the timed k_blend_wl (no work counters).
+ * interleave.  The blend is the timed k_blend_wi (no work counters).
  *   create: `scene` fixes the layout (max(n, n_capacity)); d_ws / ws_bytes /
  *           max_entries / width / height as for fdgs_render; *out (HOST)
  *           receives an opaque handle.  Synchronous (captures, instantiates).

@@ -11,7 +11,10 @@
 //   k_bin_scan..     row 5b: tile cover per (Gaussian, tile row) (band_tiles),
 //                    per-tile counts, a stable 8-bit row partition of the row
 //                    items, per-row warp-ordered scatter into the tile lists
-//   k_blend_wl       row 6: per-tile front-to-back Eq. 2, warp-specialised
+//   k_blend_wi       row 6: per-tile front-to-back Eq. 2, four independent
+//                    warps per tile, each staging and compositing its own
+//                    record lists (the timed kernel)
+//   k_blend_wl       row 6: the warp-specialised predecessor of k_blend_wi
 //                    (producer builds per-warp record lists, 4 consumer warps
 //                    composite, warp-uniform early exit);
 //                    k_blend_ws: the counting / contribution-recording variant
@@ -1474,6 +1477,192 @@ __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uin
     }
 }
 
+// Warp-independent blend (the timed kernel; FDGS_BLEND_WI=0 selects k_blend_wl):
+// no producer warp and no barriers
+// between warps.  Each of the 4 warps of a tile block stages its own batches of
+// 32 records (one per lane: the gather, the AABB mask, the per-row reach test
+// and the pinned row terms of its 4-row strip, exactly as k_blend_wl's
+// producer does for that warp) into a private shared list, then composites
+// it; the next batch's records are gathered into registers while the current
+// list is composited.  Same arithmetic and results as k_blend_wl.
+#ifndef FDGS_WI_MINB
+#define FDGS_WI_MINB 8
+#endif
+#ifndef FDGS_WI_PREFETCH
+#define FDGS_WI_PREFETCH 1
+#endif
+constexpr int kWiThreads = 128;
+__global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uint32_t *__restrict__ tile_start,
+                                                         const uint32_t *__restrict__ entries,
+                                                         const float4 *__restrict__ rec0,
+                                                         const float4 *__restrict__ rec1,
+                                                         const float4 *__restrict__ rec2, const Counters *ctr,
+                                                         int tiles_x, int width, int height, float bg0, float bg1,
+                                                         float bg2, float *__restrict__ out_rgb,
+                                                         float *__restrict__ out_T) {
+    __shared__ WlEntry s_list[4][32];
+    const bool ok = ctr->status == FDGS_OK;
+    const int tile = blockIdx.x, tx = tile % tiles_x, ty = tile / tiles_x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t start = __ldg(tile_start + tile), end = ok ? __ldg(tile_start + tile + 1) : start;
+    // consumer geometry: 2 horizontally adjacent pixels per thread
+    const int rr = lane / (kWlCols / 2), ly = wl_row0(warp) + rr, lx = wl_col0(warp) + (lane % (kWlCols / 2)) * 2;
+    const int i0 = tx * 16 + lx, j = ty * 16 + ly;
+    const bool in0 = i0 < width && j < height, in1 = i0 + 1 < width && j < height;
+    float2 px = make_float2((float)i0 + 0.5f, (float)(i0 + 1) + 0.5f);
+    const uint32_t pb0 = (1u << lx) | (1u << (16 + ly)), pb1 = (2u << lx) | (1u << (16 + ly));
+    const float kInf = __int_as_float(0x7f800000);
+    float2 thr = make_float2(in0 ? 0.0f : kInf, in1 ? 0.0f : kInf);
+    float2 T = make_float2(kInv255, kInv255), Cr = make_float2(0.f, 0.f), Cg = Cr, Cb = Cr;
+    // footprint bits of this warp in the complemented AABB mask
+    const uint32_t foot = 0xffffu | (((1u << kWlRows) - 1u) << (16 + wl_row0(warp)));
+    auto step = [&](int q, auto kAabb) {
+        const float4 a = s_list[warp][q].a;
+        const float4 rt = s_list[warp][q].t[rr];
+        asm volatile("" : "+f"(px.x), "+f"(px.y));
+        const float2 dx = sub2(px, make_float2(a.x, a.x));
+        const float2 t2 = fma2(make_float2(a.y, a.y), dx, make_float2(rt.z, rt.z));
+        const float2 e2 = fma2(dx, t2, make_float2(rt.w, rt.w));
+        bool v0 = e2.x >= thr.x, v1 = e2.y >= thr.y;
+        if constexpr (decltype(kAabb)::value) {
+            const uint32_t m = __float_as_uint(rt.y);
+            v0 = v0 && (m & pb0) == 0u;
+            v1 = v1 && (m & pb1) == 0u;
+        }
+        const float m0 = v0 ? fminf(ex2_approx(e2.x), kAlphaPre) : 0.0f;
+        const float m1 = v1 ? fminf(ex2_approx(e2.y), kAlphaPre) : 0.0f;
+        const float2 w = mul2(make_float2(m0, m1), T);
+        const float2 Tprev = T;
+        T = fma2(make_float2(-kInv255, -kInv255), w, T);
+        Cr = fma2(make_float2(a.z, a.z), w, Cr);
+        Cg = fma2(make_float2(a.w, a.w), w, Cg);
+        Cb = fma2(make_float2(rt.x, rt.x), w, Cb);
+        const bool s0 = T.x < kStopU, s1 = T.y < kStopU;
+        if (__builtin_expect(s0 || s1, 0)) {
+            if (s0) {
+                Cr.x = fmaf(-a.z, w.x, Cr.x);
+                Cg.x = fmaf(-a.w, w.x, Cg.x);
+                Cb.x = fmaf(-rt.x, w.x, Cb.x);
+                T.x = Tprev.x;
+                thr.x = kInf;
+            }
+            if (s1) {
+                Cr.y = fmaf(-a.z, w.y, Cr.y);
+                Cg.y = fmaf(-a.w, w.y, Cg.y);
+                Cb.y = fmaf(-rt.x, w.y, Cb.y);
+                T.y = Tprev.y;
+                thr.y = kInf;
+            }
+        }
+    };
+    auto fetch = [&](uint32_t bs, float4 &a0, float4 &a1, float4 &a2) {
+        a0 = a1 = a2 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (bs + lane < end) {
+            const uint32_t v = __ldg(entries + bs + lane);
+            a0 = __ldg(rec0 + v);
+            a1 = __ldg(rec1 + v);
+            a2 = __ldg(rec2 + v);
+        }
+    };
+    bool wdone = __all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf);
+    float4 r0, r1, r2;
+#if FDGS_WI_PREFETCH
+    fetch(start, r0, r1, r2);
+#endif
+    for (uint32_t base = start; base < end && !wdone; base += 32) {
+        const int n = (int)min(32u, end - base);
+#if !FDGS_WI_PREFETCH
+        fetch(base, r0, r1, r2);
+#endif
+        // ---- stage this warp's list of the batch
+        const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
+        const bool redundant = (__float_as_uint(r1.w) & 0x80000000u) != 0u;
+        uint32_t mb = 0;
+        float xl = 0.f, xr = 0.f, hA = 0.f, marg = 0.f;
+        int y0 = 16, y1 = -1;
+        if (lane < n) {
+            const uint32_t ax = __float_as_uint(r1.z), ay = __float_as_uint(r1.w);
+            const int x0 = max((int)(ax & 0xffff) - tx * 16, 0), x1 = min((int)(ax >> 16) - tx * 16, 15);
+            y0 = max((int)(ay & 0xffff) - ty * 16, 0);
+            y1 = min((int)((ay >> 16) & 0x7fffu) - ty * 16, 15);
+            const uint32_t xm = ((2u << x1) - 1u) & ~((1u << x0) - 1u);
+            const uint32_t ym = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
+            mb = ~(xm | (ym << 16));
+            if (x0 > x1) y1 = -1;
+            xl = __fsub_rn((float)(tx * 16 + x0) + 0.5f, u);
+            xr = __fsub_rn((float)(tx * 16 + x1) + 0.5f, u);
+            const float yl = (float)(ty * 16 + y0) + 0.5f - v, yr = (float)(ty * 16 + y1) + 0.5f - v;
+            const float X = fmaxf(fabsf(xl), fabsf(xr)), Y = fmaxf(fabsf(yl), fabsf(yr));
+            marg = -(1e-3f * (fabsf(Ap) * X * X + fabsf(Bp) * X * Y + fabsf(Cp) * Y * Y) + 1e-3f);
+            hA = __fdividef(-0.5f, Ap);
+        }
+        float4 tr[kWlRows];
+        bool rw = false;
+#pragma unroll
+        for (int r = 0; r < kWlRows; ++r) {  // pinned e2 chain, row terms (DESIGN.md step 10)
+            const int row = wl_row0(warp) + r;
+            const float dy = __fsub_rn((float)(ty * 16 + row) + 0.5f, v);
+            const float t1 = __fmul_rn(Bp, dy);
+            const float t3 = __fmul_rn(Cp, dy);
+            const float t4 = __fmaf_rn(t3, dy, Q2);
+            const float xs = fminf(fmaxf(t1 * hA, xl), xr);
+            rw |= row >= y0 && row <= y1 && fmaf(xs, fmaf(Ap, xs, t1), t4) >= marg;
+            tr[r] = make_float4(r2.z, __uint_as_float(mb), t1, t4);
+        }
+        const bool reach = lane < n && rw;
+        const uint32_t bal = __ballot_sync(0xffffffffu, reach);
+        const bool masked = __any_sync(0xffffffffu, reach && !redundant && (mb & foot) != 0u);
+        __syncwarp();  // the previous list has been read
+        if (reach) {
+            WlEntry &E = s_list[warp][__popc(bal & lanemask_lt())];
+            E.a = make_float4(u, Ap, r2.x, r2.y);
+#pragma unroll
+            for (int r = 0; r < kWlRows; ++r) E.t[r] = tr[r];
+        }
+#if FDGS_WI_PREFETCH
+        // ---- gather the next batch while this one is composited
+        fetch(base + 32, r0, r1, r2);
+#endif
+        __syncwarp();
+        const int cnt = __popc(bal);
+        if (masked) {
+#pragma unroll kWlUnroll
+            for (int q = 0; q < cnt; ++q) step(q, std::true_type{});
+        } else {
+#pragma unroll kWlUnroll
+            for (int q = 0; q < cnt; ++q) step(q, std::false_type{});
+        }
+        wdone = __all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf);
+    }
+    T = mul2(T, make_float2(255.0f, 255.0f));
+    if (ok && out_rgb != nullptr) {
+        const size_t hw = (size_t)width * height, p = (size_t)j * width + i0;
+        if (in0) {
+            out_rgb[p] = fmaf(T.x, bg0, Cr.x);
+            out_rgb[hw + p] = fmaf(T.x, bg1, Cg.x);
+            out_rgb[2 * hw + p] = fmaf(T.x, bg2, Cb.x);
+            if (out_T) out_T[p] = T.x;
+        }
+        if (in1) {
+            out_rgb[p + 1] = fmaf(T.y, bg0, Cr.y);
+            out_rgb[hw + p + 1] = fmaf(T.y, bg1, Cg.y);
+            out_rgb[2 * hw + p + 1] = fmaf(T.y, bg2, Cb.y);
+            if (out_T) out_T[p + 1] = T.y;
+        }
+    }
+}
+
+#ifndef FDGS_BLEND_WI
+#define FDGS_BLEND_WI 1
+#endif
+#if FDGS_BLEND_WI
+#define FDGS_BLEND_KERNEL k_blend_wi
+constexpr int kBlendThreads = kWiThreads;
+#else
+#define FDGS_BLEND_KERNEL k_blend_wl
+constexpr int kBlendThreads = kWsThreads;
+#endif
+
 // ---------------------------------------------------------------- launcher
 // Persistent-grid sizes (blocks per SM); FDGS_PGRID / FDGS_RGRID override for tuning.
 static int tune_env(const char *name, int dflt) {
@@ -1605,7 +1794,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
                                                             L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T,
                                                             stats);
     } else if (wl_blend) {  // the timed blend
-        k_blend_wl<<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
+        FDGS_BLEND_KERNEL<<<L.n_tiles, kBlendThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
                                                       L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
     } else {
         k_blend_ws<false><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
@@ -1676,12 +1865,12 @@ cudaError_t render_graph_build(RenderGraphImpl &g, const SceneDev &sc, const Cam
             cudaKernelNodeParams p{};
             if ((e = cudaGraphKernelNodeGetParams(nodes[k], &p)) != cudaSuccess) break;
             cudaKernelNodeAttrValue pr{};
-            pr.priority = p.func == (void *)k_blend_wl ? least : greatest;
+            pr.priority = p.func == (void *)FDGS_BLEND_KERNEL ? least : greatest;
             e = cudaGraphKernelNodeSetAttribute(nodes[k], cudaKernelNodeAttributePriority, &pr);
             if (p.func == (void *)k_cull) g.n_cull = nodes[k], g.p_cull = p;
             else if (p.func == (void *)k_cull_emit) g.n_emit = nodes[k], g.p_emit = p;
             else if (p.func == (void *)k_slice) g.n_slice = nodes[k], g.p_slice = p;
-            else if (p.func == (void *)k_blend_wl) g.n_blend = nodes[k], g.p_blend = p;
+            else if (p.func == (void *)FDGS_BLEND_KERNEL) g.n_blend = nodes[k], g.p_blend = p;
         }
         if (e == cudaSuccess && (!g.n_cull || !g.n_emit || !g.n_slice || !g.n_blend)) e = cudaErrorInvalidValue;
     }
