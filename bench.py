@@ -107,7 +107,8 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                          "--format=csv,noheader,nounits", "-lms",
+                                          os.environ.get("FDGS_BENCH_CLOCK_MS", "200")],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -293,9 +294,11 @@ def run_ours(args):
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
         start.record(stream)
+        h0 = time.perf_counter()
         pipe.render_many([frame_args(x) for x in step_frames], outs[:len(step_frames)],
                          stats=stats if count else None,
                          stage_events=evs if (use_ev and timed) else None, stream=stream)
+        host_ms.append((time.perf_counter() - h0) * 1e3)
         end.record(stream)
         end.synchronize()
         ms = start.elapsed_time(end)
@@ -318,6 +321,7 @@ def run_ours(args):
         return ms, stage
 
     ptr = 0
+    host_ms = []  # host enqueue time of each step (render_many returning)
 
     def next_frames():
         nonlocal ptr
@@ -330,6 +334,7 @@ def run_ours(args):
     sampler = ClockSampler(local)
     sampler.start()
     step_ms, stage_ms = [], np.zeros(4)
+    h_first = len(host_ms)
     n_eval = n_blend = 0
     n_vis_tot = n_ent_tot = n_act_tot = 0
     timed_frames = []
@@ -341,6 +346,7 @@ def run_ours(args):
         if stg is not None:
             stage_ms += stg
     clocks = sampler.stop()
+    host_timed = host_ms[h_first:h_first + args.steps]
     # work counters of the same frames (counting blend variant, not timed)
     for fr in timed_frames:
         run_step(fr, False, count=True)
@@ -446,6 +452,11 @@ def run_ours(args):
                         "model": "SURVEY.md 8(d) d.4: mask words + index + 68 B/active + (192+96+72) B/visible + "
                                  "(8+32+52) B/entry + 12 B/pixel, per GPU"}
     res["clocks"] = clocks
+    # host time to enqueue a step (render_many returning) vs the step's device
+    # time: the pipeline is host-bound if the ratio approaches 1
+    res["host_enqueue"] = {"ms_per_frame_median": round(float(np.median(host_timed)) / F, 4),
+                           "ms_per_frame_max": round(float(np.max(host_timed)) / F, 4),
+                           "vs_device": round(float(np.median(host_timed)) / float(np.median(step_ms)), 3)}
     res["setup"] = {"keyframe_masks_s": round(mask_build_s, 3), "n_keyframes": len(kf)}
 
     # ---- e2e through the public API with host buffers
