@@ -77,8 +77,12 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--streams", type=int, default=6, help="frame-pipelining depth (workspaces/streams)")
     p.add_argument("--no-split", action="store_true", help="blend on the front-end stream (no priority split)")
+    p.add_argument("--graphs", action="store_true", help="one CUDA-graph launch per frame (RenderPipeline(graphs=True))")
     p.add_argument("--config", choices=["c2", "c3", "c4"], default="c3")
     p.add_argument("--unmasked", action="store_true", help="render without the key-frame filter")
+    p.add_argument("--literal-masks", action="store_true",
+                   help="key-frame masks from the Eq. 2 blending weights (P:282 literal, R3b) instead of the "
+                        "BASELINE config's geometric visibility")
     p.add_argument("--no-working-set", dest="working_set", action="store_false",
                    help="render the full scene under the masks instead of the window's compacted working set")
     p.add_argument("--vq", type=int, default=0, metavar="K",
@@ -174,7 +178,7 @@ def cpu_oracle_run(scene, cams, masks, kf, frames, seconds, row_stride=8):
     W, H = cams[0].width, cams[0].height
     rows = np.arange(0, H, row_stride)
     pix = (rows[:, None] * W + np.arange(W)[None, :]).ravel()
-    done_px, k, t0 = 0, 0, time.perf_counter()
+    done_px, k, n_pairs, t0 = 0, 0, 0, time.perf_counter()
     oracle.load()
     t0 = time.perf_counter()
     while True:
@@ -183,14 +187,18 @@ def cpu_oracle_run(scene, cams, masks, kf, frames, seconds, row_stride=8):
         if masks is not None:
             li, ri = bracket(kf, ti)
             act = masks[li] | masks[ri]
-        oracle.render(scene, cams[ci], float(times[ti]), mask=act, pixels=pix)
+        r = oracle.render(scene, cams[ci], float(times[ti]), mask=act, pixels=pix)
         done_px += pix.size
+        n_pairs += r["stats"]["evaluated"]
         k += 1
         el = time.perf_counter() - t0
         if el >= seconds:
             break
     fps = done_px / (W * H) / el
-    return fps, dict(cores=oracle.num_threads(), frames=k, seconds=round(el, 2),
+    cores = oracle.num_threads()
+    return fps, dict(cores=cores, frames=k, seconds=round(el, 2),
+                     ns_per_evaluated_pair=round(el * 1e9 / max(n_pairs, 1), 3),
+                     core_ns_per_evaluated_pair=round(el * 1e9 * cores / max(n_pairs, 1), 2),
                      sample=f"oracle per-pixel render of rows j%{row_stride}==0 ({pix.size} px) of {k} "
                             f"consecutive {'masked' if masks is not None else 'unmasked'} {CONFIG} frames; "
                             f"fps = sampled pixels/(W*H)/wall")
@@ -245,7 +253,10 @@ def run_ours(args):
     t_mask0 = time.perf_counter()
     for k in range(len(kf)):
         if k % world == rank:
-            fd.keyframe_mask(scene, cams, float(times[kf[k]]), out=masks[k])
+            if args.literal_masks:  # P:282 read literally (R3b): blending weight > 0 in some view
+                masks[k].copy_(fd.keyframe_mask_contrib(scene, cams, float(times[kf[k]]), 0.0))
+            else:
+                fd.keyframe_mask(scene, cams, float(times[kf[k]]), out=masks[k])
     if world > 1:
         dist.all_reduce(masks, op=dist.ReduceOp.SUM)
     torch.cuda.synchronize()
@@ -254,7 +265,8 @@ def run_ours(args):
     seq = sequence()
     mine = [x for x in seq if x[0] % world == rank]
     F = args.frames_per_step
-    pipe = fd.RenderPipeline(scene, cams[0].width, cams[0].height, depth=args.streams, split=not args.no_split)
+    pipe = fd.RenderPipeline(scene, cams[0].width, cams[0].height, depth=args.streams, split=not args.no_split,
+                             graphs=args.graphs)
     renderer = pipe.renderers[0]
     outs = [renderer.new_output() for _ in range(F)]
     stats = torch.zeros((F, 4), dtype=torch.int64, device=dev)  # fdgs_frame_stats is 32 bytes
@@ -376,6 +388,8 @@ def run_ours(args):
                dtype="f32 (decision path f64)", data="synthetic",
                config={"workload": WORKLOADS[CONFIG] + (", masked (union of bracketing key-frames)" if MASKED
                                                          else ", unmasked")
+                       + (", literal key-frame masks (Eq. 2 weight > 0 in some view; P:282, R3b)"
+                          if MASKED and args.literal_masks else "")
                        + (f", SH vector-quantised (K={args.vq} codebook, uint16 index; Ours-PP, P:483)"
                           if args.vq else ""),
                        "frames_per_step": F, "frames_per_rank": frames_rank, "partition": "frame f -> rank f mod N",
@@ -519,7 +533,8 @@ def run_ours(args):
         fps, info = cpu_oracle_run(arrays, cams, masks.cpu().numpy().view(np.uint32) if MASKED else None, kf, mine,
                                    args.cpu_seconds)
         res["cpu_baseline"] = {"value": round(fps, 5), "unit": UNIT, "cores": info["cores"], "kind": "oracle",
-                               "sample": info["sample"]}
+                               "sample": info["sample"], "ns_per_evaluated_pair": info["ns_per_evaluated_pair"],
+                               "core_ns_per_evaluated_pair": info["core_ns_per_evaluated_pair"]}
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -111,6 +111,12 @@ def main():
     iou = lambda x, y: float((x & y).sum() / max(1, (x | y).sum()))
     out["active_ratio"] = {"t_index": ts_idx, "literal": [round(float(lit[f].mean()), 4) for f in ts_idx],
                            "geometric": [round(float(geo[f].mean()), 4) for f in ts_idx]}
+    # set difference of the two mask readings (R3 geometric vs R3b literal)
+    out["mask_set_difference"] = {
+        "t_index": ts_idx,
+        "literal_not_geometric": [int((lit[f] & ~geo[f]).sum()) for f in ts_idx],
+        "geometric_not_literal_fraction": [round(float((geo[f] & ~lit[f]).sum() / max(1, geo[f].sum())), 4)
+                                           for f in ts_idx]}
     out["activation_iou_vs_frame0"] = {"t_index": ts_idx, "literal": [round(iou(lit[ts_idx[0]], lit[f]), 4)
                                                                       for f in ts_idx]}
     win = [iou(lit[f], lit[f + a.t_stride]) for f in ts_idx[:-1] if f + a.t_stride in lit]
@@ -152,9 +158,12 @@ def main():
     frames_u = [(fd.camera_struct(cams[c]), float(times[f]), None, None) for f, c in seq]
     fps_u = fps_of(pipe, frames_u, outs_u)
     res = []
-    for delta in [1, 5, 10, 20, 50, 100, F]:
+    for kind, delta in [(k, d) for k in ("geometric", "literal") for d in [1, 5, 10, 20, 50, 100, F]]:
         kf = fd.keyframes(F, delta)
-        masks = [fd.keyframe_mask(sc, cams, float(times[k])) for k in kf]
+        if kind == "geometric":
+            masks = [fd.keyframe_mask(sc, cams, float(times[k])) for k in kf]
+        else:  # P:282 read literally: blending weight > 0 in some view
+            masks = [fd.keyframe_mask_contrib(sc, cams, float(times[k]), 0.0) for k in kf]
         outs_m = [pipe.renderers[0].new_output() for _ in seq]
         frames_m = []
         act = []
@@ -170,7 +179,7 @@ def main():
                 same += 1
             else:
                 psnr.append(10 * math.log10(1.0 / mse))
-        res.append({"delta": delta, "keyframes": len(kf), "fps": round(fps_m, 1),
+        res.append({"masks": kind, "delta": delta, "keyframes": len(kf), "fps": round(fps_m, 1),
                     "mean_active_fraction": round(float(np.mean(act)), 4),
                     "identical_frames": same,
                     "psnr_vs_unmasked_mean_of_differing": round(float(np.mean(psnr)), 2) if psnr else None,
@@ -179,7 +188,8 @@ def main():
     if a.prune_config:
         out["pruning_study"] = pruning_study(a.prune_config)
     out["interval_study"] = {"unmasked_fps": round(fps_u, 1), "frames": len(seq), "curve": res,
-                             "note": "geometric key-frame masks (reading R3); PSNR on [0,1] rgb over the frames that differ at all"}
+                             "note": "geometric (reading R3) and literal (R3b, weight > 0) key-frame masks; PSNR on [0,1] "
+                                     "rgb over the frames that differ at all"}
     print(json.dumps(out))
 
 
