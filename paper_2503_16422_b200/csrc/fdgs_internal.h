@@ -10,7 +10,11 @@
 namespace fdgs {
 
 constexpr int kPreBlock = 256;         // Gaussians per preprocess partition
-constexpr int kDepthTile = 1024;       // keys per depth-sort partition (256 threads x 4)
+#ifndef FDGS_SORT_ITEMS
+#define FDGS_SORT_ITEMS 4
+#endif
+constexpr int kDepthItems = FDGS_SORT_ITEMS;
+constexpr int kDepthTile = 256 * kDepthItems;  // keys per depth-sort partition (256 threads x items)
 constexpr int kTileSortItems = 4;      // row items per thread in the row-partition passes
 constexpr int kTileTile = 256 * kTileSortItems;
 constexpr int kRowSeg = 16;            // blocks per tile row in the row scatter

@@ -1477,7 +1477,8 @@ __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uin
     }
 }
 
-// Warp-independent blend (the timed kernel; FDGS_BLEND_WI=0 selects k_blend_wl):
+// Warp-independent blend (the timed kernel; the environment variable
+// FDGS_BLEND=wl selects k_blend_wl instead, read once per process):
 // no producer warp and no barriers
 // between warps.  Each of the 4 warps of a tile block stages its own batches of
 // 32 records (one per lane: the gather, the AABB mask, the per-row reach test
@@ -1652,16 +1653,15 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
     }
 }
 
-#ifndef FDGS_BLEND_WI
-#define FDGS_BLEND_WI 1
-#endif
-#if FDGS_BLEND_WI
-#define FDGS_BLEND_KERNEL k_blend_wi
-constexpr int kBlendThreads = kWiThreads;
-#else
-#define FDGS_BLEND_KERNEL k_blend_wl
-constexpr int kBlendThreads = kWsThreads;
-#endif
+// Blend kernel of the timed path: k_blend_wi, or k_blend_wl when FDGS_BLEND=wl.
+static bool blend_wl() {
+    static const bool v = [] {
+        const char *e = getenv("FDGS_BLEND");
+        return e != nullptr && e[0] == 'w' && e[1] == 'l' && e[2] == 0;
+    }();
+    return v;
+}
+static const void *blend_fn() { return blend_wl() ? (const void *)k_blend_wl : (const void *)k_blend_wi; }
 
 // ---------------------------------------------------------------- launcher
 // Persistent-grid sizes (blocks per SM); FDGS_PGRID / FDGS_RGRID override for tuning.
@@ -1794,8 +1794,12 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
                                                             L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T,
                                                             stats);
     } else if (wl_blend) {  // the timed blend
-        FDGS_BLEND_KERNEL<<<L.n_tiles, kBlendThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
-                                                      L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
+        if (blend_wl())
+            k_blend_wl<<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
+                                                          L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
+        else
+            k_blend_wi<<<L.n_tiles, kWiThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
+                                                          L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
     } else {
         k_blend_ws<false><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
                                                              L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T,
@@ -1865,12 +1869,12 @@ cudaError_t render_graph_build(RenderGraphImpl &g, const SceneDev &sc, const Cam
             cudaKernelNodeParams p{};
             if ((e = cudaGraphKernelNodeGetParams(nodes[k], &p)) != cudaSuccess) break;
             cudaKernelNodeAttrValue pr{};
-            pr.priority = p.func == (void *)FDGS_BLEND_KERNEL ? least : greatest;
+            pr.priority = p.func == blend_fn() ? least : greatest;
             e = cudaGraphKernelNodeSetAttribute(nodes[k], cudaKernelNodeAttributePriority, &pr);
             if (p.func == (void *)k_cull) g.n_cull = nodes[k], g.p_cull = p;
             else if (p.func == (void *)k_cull_emit) g.n_emit = nodes[k], g.p_emit = p;
             else if (p.func == (void *)k_slice) g.n_slice = nodes[k], g.p_slice = p;
-            else if (p.func == (void *)FDGS_BLEND_KERNEL) g.n_blend = nodes[k], g.p_blend = p;
+            else if (p.func == blend_fn()) g.n_blend = nodes[k], g.p_blend = p;
         }
         if (e == cudaSuccess && (!g.n_cull || !g.n_emit || !g.n_slice || !g.n_blend)) e = cudaErrorInvalidValue;
     }

@@ -465,3 +465,29 @@ def test_aabb_redundant_flag_sound():
         assert not np.any(outside & (q + err >= 0.0)), i
         checked += 1
     assert checked > 100
+
+
+def test_blend_wl_alternative_matches():
+    """FDGS_BLEND=wl selects the warp-specialised k_blend_wl for the timed
+    blend (read once per process, so in a subprocess): its C2 frame must equal
+    k_blend_wi's bit for bit (same arithmetic, same record lists; k_blend_wi
+    itself is parity-tested against the oracle above)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, fdgs_inputs as fi, paper_2503_16422_b200 as fd\n"
+        "sc = fd.Scene.from_arrays(fi.make_scene('c2')); cam = fi.make_cameras('c2')[5]\n"
+        "r = fd.Renderer(sc, cam.width, cam.height)\n"
+        "out = r.render(cam, 0.4); torch.cuda.synchronize()\n"
+        "import sys; np.save(sys.stdout.buffer, out.cpu().numpy())\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    imgs = []
+    for sel in ("wi", "wl"):
+        env = dict(os.environ, FDGS_BLEND=sel, PYTHONPATH=root)
+        res = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, timeout=300)
+        assert res.returncode == 0, res.stderr.decode()[-2000:]
+        import io
+        imgs.append(np.load(io.BytesIO(res.stdout)))
+    assert imgs[0].shape == (3, 800, 800)
+    assert np.array_equal(imgs[0], imgs[1])
