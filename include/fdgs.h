@@ -197,12 +197,12 @@ fdgs_status fdgs_render_checked(const fdgs_scene *scene, const uint32_t *d_mask_
                                 void *stream);
 
 /* CUDA-graph form of fdgs_render (the same kernels and results): the frame's
- * ~21 launches are captured once per (workspace, layout) and replayed with
- * one host call per frame; only the arguments that change between frames are
- * updated (scene, masks, t, camera, outputs).  Front-end nodes carry the
- * device's greatest stream priority and the blend its least (as
- * fdgs_render_split), so graphs of several workspaces on several streams
- * interleave.  The blend is the timed k_blend_wi (no work counters).
+ * the ~20 front-end launches are captured once per (workspace, layout) and
+ * replayed with one graph launch per frame; only the arguments that change
+ * between frames are updated (scene, masks, t, camera).  Front-end nodes
+ * carry the device's greatest stream priority.  The blend (the timed
+ * k_blend_wi, no work counters) is launched directly after the graph, on the
+ * same stream or (fdgs_render_graph_launch_split) on a blend stream.
  *   create: `scene` fixes the layout (max(n, n_capacity)); d_ws / ws_bytes /
  *           max_entries / width / height as for fdgs_render; *out (HOST)
  *           receives an opaque handle.  Synchronous (captures, instantiates).
@@ -219,6 +219,14 @@ fdgs_status fdgs_render_graph_create(const fdgs_scene *scene, int32_t width, int
 fdgs_status fdgs_render_graph_launch(fdgs_render_graph *graph, const fdgs_scene *scene, const uint32_t *d_mask_l,
                                      const uint32_t *d_mask_r, const fdgs_camera *cam, float t, float *d_out_rgb,
                                      float *d_out_T, void *stream);
+/* As fdgs_render_graph_launch, with the blend on `blend_stream` ordered after
+ * the front end by `split_event` (a HOST cudaEvent_t the caller owns), as
+ * fdgs_render_split does: the front-end graph on `stream`, the blend launched
+ * directly on the (lower-priority) blend stream.  ASYNC. */
+fdgs_status fdgs_render_graph_launch_split(fdgs_render_graph *graph, const fdgs_scene *scene,
+                                           const uint32_t *d_mask_l, const uint32_t *d_mask_r,
+                                           const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T,
+                                           void *stream, void *blend_stream, void *split_event);
 fdgs_status fdgs_render_graph_destroy(fdgs_render_graph *graph);
 
 /* Device views into a render workspace after fdgs_render (tests/debug only).

@@ -190,9 +190,12 @@ class Renderer:
         except Exception:
             pass
 
-    def render_graph(self, cam, t, mask_l=None, mask_r=None, out=None, out_T=None, stream=None, scene=None):
-        """fdgs_render_graph_launch: the frame as one CUDA-graph launch (captured on
-        first use for this workspace; results identical to render()).  Async."""
+    def render_graph(self, cam, t, mask_l=None, mask_r=None, out=None, out_T=None, stream=None, scene=None,
+                     blend_stream=None, split_event=None):
+        """fdgs_render_graph_launch: the front end as one CUDA-graph launch (captured
+        on first use for this workspace) and the blend launched after it -- on
+        `blend_stream` ordered by `split_event` when given
+        (fdgs_render_graph_launch_split); results identical to render().  Async."""
         if cam.width != self.width or cam.height != self.height:
             raise ValueError("camera size differs from the renderer's")
         out = self.new_output() if out is None else out
@@ -205,8 +208,15 @@ class Renderer:
             check(lib().fdgs_render_graph_create(C.byref(base.struct), self.width, self.height, _ptr(self.ws),
                                                  self.ws_bytes, self.max_entries, C.byref(h)))
             self._graph = h
-        check(lib().fdgs_render_graph_launch(self._graph, C.byref(sc.struct), ml, mr, C.byref(cs), float(t),
-                                             _ptr(out), _ptr(out_T), _stream_ptr(stream)))
+        if blend_stream is None:
+            check(lib().fdgs_render_graph_launch(self._graph, C.byref(sc.struct), ml, mr, C.byref(cs), float(t),
+                                                 _ptr(out), _ptr(out_T), _stream_ptr(stream)))
+            return out
+        if split_event.cuda_event == 0:
+            split_event.record(stream)  # materialise the CUDA event
+        check(lib().fdgs_render_graph_launch_split(self._graph, C.byref(sc.struct), ml, mr, C.byref(cs), float(t),
+                                                   _ptr(out), _ptr(out_T), _stream_ptr(stream),
+                                                   _stream_ptr(blend_stream), C.c_void_p(split_event.cuda_event)))
         return out
 
     def _scene_for(self, scene, stream):
@@ -338,7 +348,7 @@ class RenderPipeline:
         self.renderers = [Renderer(scene, width, height, max_entries) for _ in range(depth)]
         lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
         self.split = split
-        self.graphs = graphs  # one CUDA-graph launch per frame (node priorities replace the stream split)
+        self.graphs = graphs  # the front end as one CUDA-graph launch per frame, the blend launched after it
         self.front = [torch.cuda.Stream(device=scene.device, priority=-1 if split else 0) for _ in range(depth)]
         self.blend = [torch.cuda.Stream(device=scene.device, priority=0) for _ in range(depth)] if split else None
         self.split_ev = [torch.cuda.Event() for _ in range(depth)]
@@ -403,7 +413,15 @@ class RenderPipeline:
             sc = fr[4] if len(fr) > 4 else None  # optional per-frame scene (a compacted working set)
             i = k % self.depth
             r = self.renderers[i]
-            if self.graphs:
+            if self.graphs and self.split:
+                if k >= self.depth:  # the workspace is free once its previous blend is done
+                    done = torch.cuda.Event()
+                    done.record(self.blend[i])
+                    self.front[i].wait_event(done)
+                r.render_graph(cam, t, ml, mr, out=outs[k], stream=self.front[i], scene=sc,
+                               blend_stream=self.blend[i], split_event=self.split_ev[i])
+                last = self.blend[i]
+            elif self.graphs:
                 r.render_graph(cam, t, ml, mr, out=outs[k], stream=self.front[i], scene=sc)
                 last = self.front[i]
             elif not self.split:

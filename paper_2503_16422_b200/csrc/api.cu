@@ -369,6 +369,16 @@ fdgs_status fdgs_render_graph_create(const fdgs_scene *scene, int32_t width, int
 fdgs_status fdgs_render_graph_launch(fdgs_render_graph *graph, const fdgs_scene *scene, const uint32_t *d_mask_l,
                                      const uint32_t *d_mask_r, const fdgs_camera *cam, float t, float *d_out_rgb,
                                      float *d_out_T, void *stream) {
+    return fdgs_render_graph_launch_split(graph, scene, d_mask_l, d_mask_r, cam, t, d_out_rgb, d_out_T, stream,
+                                          nullptr, nullptr);
+}
+
+fdgs_status fdgs_render_graph_launch_split(fdgs_render_graph *graph, const fdgs_scene *scene,
+                                           const uint32_t *d_mask_l, const uint32_t *d_mask_r,
+                                           const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T,
+                                           void *stream, void *blend_stream, void *split_event) {
+    if ((blend_stream == nullptr) != (split_event == nullptr))
+        return fail(FDGS_ERR_INVALID_ARG, "blend_stream and split_event go together");
     if (graph == nullptr) return fail(FDGS_ERR_INVALID_ARG, "graph is NULL");
     fdgs_status s = check_scene(scene);
     if (s != FDGS_OK) return s;
@@ -381,7 +391,8 @@ fdgs_status fdgs_render_graph_launch(fdgs_render_graph *graph, const fdgs_scene 
     if (!make_camdev(*cam, cd, &why)) return fail(FDGS_ERR_INVALID_ARG, "camera: %s", why);
     if (d_mask_l == nullptr && d_mask_r != nullptr) d_mask_l = d_mask_r, d_mask_r = nullptr;
     cudaError_t e = render_graph_launch(*graph->impl, make_scenedev(*scene), d_mask_l, d_mask_r, cd, t, d_out_rgb,
-                                        d_out_T, (cudaStream_t)stream);
+                                        d_out_T, (cudaStream_t)stream, (cudaStream_t)blend_stream,
+                                        (cudaEvent_t)split_event);
     return e == cudaSuccess ? FDGS_OK : cuda_fail(e, "fdgs_render_graph_launch");
 }
 

@@ -87,7 +87,8 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
                           float t, float *out_rgb, float *out_T, char *ws, const RenderLayout &L,
                           fdgs_frame_stats *stats, cudaStream_t st, cudaEvent_t const *stage_events,
                           cudaStream_t blend_st = nullptr, cudaEvent_t split_ev = nullptr,
-                          unsigned long long *contrib = nullptr, uint32_t *stv_info = nullptr);
+                          unsigned long long *contrib = nullptr, uint32_t *stv_info = nullptr,
+                          bool front_only = false);
 // Head of the fdgs_stv_score workspace.
 struct StvState {
     uint32_t info[2];  // [0] worst frame status, [1] largest per-view entry count
@@ -117,7 +118,7 @@ cudaError_t render_graph_build(RenderGraphImpl &g, const SceneDev &sc, const Cam
                                const RenderLayout &L);
 cudaError_t render_graph_launch(RenderGraphImpl &g, const SceneDev &sc, const uint32_t *mask_l,
                                 const uint32_t *mask_r, const CamDev &cam, float t, float *out_rgb, float *out_T,
-                                cudaStream_t st);
+                                cudaStream_t st, cudaStream_t blend_st = nullptr, cudaEvent_t split_ev = nullptr);
 void render_graph_free(RenderGraphImpl &g);
 RenderGraphImpl *render_graph_new();
 void render_graph_delete(RenderGraphImpl *g);

@@ -1489,6 +1489,10 @@ __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uin
 #ifndef FDGS_WI_MINB
 #define FDGS_WI_MINB 8
 #endif
+#ifndef FDGS_WI_PAIR
+#define FDGS_WI_PAIR 1
+#endif
+
 #ifndef FDGS_WI_PREFETCH
 #define FDGS_WI_PREFETCH 1
 #endif
@@ -1554,6 +1558,58 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
                 T.y = Tprev.y;
                 thr.y = kInf;
             }
+        }
+    };
+    // Two records, one stop test (FDGS_WI_PAIR): U after both is checked; a
+    // pixel that fell below the threshold is rolled back to the record that
+    // crossed it (U restored to before that record, the colour steps of the
+    // crossing record and of any later one subtracted, colours reloaded from
+    // the list).  Same stop decisions as the per-record test.
+    auto blend1 = [&](const float4 &a, const float4 &rt, auto kAabb, float2 &w) {
+        asm volatile("" : "+f"(px.x), "+f"(px.y));
+        const float2 dx = sub2(px, make_float2(a.x, a.x));
+        const float2 t2 = fma2(make_float2(a.y, a.y), dx, make_float2(rt.z, rt.z));
+        const float2 e2 = fma2(dx, t2, make_float2(rt.w, rt.w));
+        bool v0 = e2.x >= thr.x, v1 = e2.y >= thr.y;
+        if constexpr (decltype(kAabb)::value) {
+            const uint32_t m = __float_as_uint(rt.y);
+            v0 = v0 && (m & pb0) == 0u;
+            v1 = v1 && (m & pb1) == 0u;
+        }
+        const float m0 = v0 ? fminf(ex2_approx(e2.x), kAlphaPre) : 0.0f;
+        const float m1 = v1 ? fminf(ex2_approx(e2.y), kAlphaPre) : 0.0f;
+        w = mul2(make_float2(m0, m1), T);
+        T = fma2(make_float2(-kInv255, -kInv255), w, T);
+        Cr = fma2(make_float2(a.z, a.z), w, Cr);
+        Cg = fma2(make_float2(a.w, a.w), w, Cg);
+        Cb = fma2(make_float2(rt.x, rt.x), w, Cb);
+    };
+    auto step2 = [&](int q, auto kAabb) {
+        const float2 T0 = T;
+        float2 w1, w2;
+        blend1(s_list[warp][q].a, s_list[warp][q].t[rr], kAabb, w1);
+        const float2 T1 = T;
+        blend1(s_list[warp][q + 1].a, s_list[warp][q + 1].t[rr], kAabb, w2);
+        if (__builtin_expect(fminf(T.x, T.y) < kStopU, 0)) {
+            const float4 a1 = s_list[warp][q].a, r1 = s_list[warp][q].t[rr];
+            const float4 a2 = s_list[warp][q + 1].a, r2 = s_list[warp][q + 1].t[rr];
+            auto undo = [&](float &cr, float &cg, float &cb, float &t, float &th, float t0, float t1, float x1,
+                            float x2) {
+                if (!(t < kStopU)) return;
+                cr = fmaf(-a2.z, x2, cr);  // the second record's step, always
+                cg = fmaf(-a2.w, x2, cg);
+                cb = fmaf(-r2.x, x2, cb);
+                t = t1;
+                if (t1 < kStopU) {  // the first record crossed
+                    cr = fmaf(-a1.z, x1, cr);
+                    cg = fmaf(-a1.w, x1, cg);
+                    cb = fmaf(-r1.x, x1, cb);
+                    t = t0;
+                }
+                th = __int_as_float(0x7f800000);
+            };
+            undo(Cr.x, Cg.x, Cb.x, T.x, thr.x, T0.x, T1.x, w1.x, w2.x);
+            undo(Cr.y, Cg.y, Cb.y, T.y, thr.y, T0.y, T1.y, w1.y, w2.y);
         }
     };
     auto fetch = [&](uint32_t bs, float4 &a0, float4 &a1, float4 &a2) {
@@ -1630,8 +1686,15 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
 #pragma unroll kWlUnroll
             for (int q = 0; q < cnt; ++q) step(q, std::true_type{});
         } else {
+#if FDGS_WI_PAIR
+            int q = 0;
+#pragma unroll 2
+            for (; q + 1 < cnt; q += 2) step2(q, std::false_type{});
+            if (q < cnt) step(q, std::false_type{});
+#else
 #pragma unroll kWlUnroll
             for (int q = 0; q < cnt; ++q) step(q, std::false_type{});
+#endif
         }
         wdone = __all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf);
     }
@@ -1661,7 +1724,6 @@ static bool blend_wl() {
     }();
     return v;
 }
-static const void *blend_fn() { return blend_wl() ? (const void *)k_blend_wl : (const void *)k_blend_wi; }
 
 // ---------------------------------------------------------------- launcher
 // Persistent-grid sizes (blocks per SM); FDGS_PGRID / FDGS_RGRID override for tuning.
@@ -1677,7 +1739,7 @@ static int tune_pgrid() {
 cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint32_t *mask_r, const CamDev &cam,
                           float t, float *out_rgb, float *out_T, char *ws, const RenderLayout &L,
                           fdgs_frame_stats *stats, cudaStream_t st, cudaEvent_t const *ev, cudaStream_t blend_st,
-                          cudaEvent_t split_ev, unsigned long long *contrib, uint32_t *stv_info) {
+                          cudaEvent_t split_ev, unsigned long long *contrib, uint32_t *stv_info, bool front_only) {
     Counters *ctr = reinterpret_cast<Counters *>(ws + L.counters);
     float4 *rec0 = reinterpret_cast<float4 *>(ws + L.rec0);
     float4 *rec1 = reinterpret_cast<float4 *>(ws + L.rec1);
@@ -1775,6 +1837,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         k_row_scatter<<<nrb, 32 * kRowWarps, cnt_smem + sizeof(uint32_t) * L.tiles_x, st>>>(
             sorted_items, ipack, iv, row_start, L.tiles_x, rhist, tstart, entries, ctr);
     }
+    if (front_only) return cudaGetLastError();  // graph capture of the front end
     // the blend may run on its own (lower-priority) stream, ordered after the front end
     cudaStream_t bst = st;
     if (blend_st != nullptr) {
@@ -1831,8 +1894,8 @@ namespace fdgs {
 struct RenderGraphImpl {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
-    cudaGraphNode_t n_cull = nullptr, n_emit = nullptr, n_slice = nullptr, n_blend = nullptr;
-    cudaKernelNodeParams p_cull{}, p_emit{}, p_slice{}, p_blend{};
+    cudaGraphNode_t n_cull = nullptr, n_emit = nullptr, n_slice = nullptr;
+    cudaKernelNodeParams p_cull{}, p_emit{}, p_slice{};
     RenderLayout L{};
     char *ws = nullptr;
 };
@@ -1841,20 +1904,16 @@ cudaError_t render_graph_build(RenderGraphImpl &g, const SceneDev &sc, const Cam
                                const RenderLayout &L) {
     g.L = L;
     g.ws = ws;
-    cudaStream_t s1 = nullptr, s2 = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
+    // the front end only: the blend is launched directly after the graph (on
+    // the caller's blend stream), so it keeps the stream-priority split
+    cudaStream_t s1 = nullptr;
     cudaError_t e = cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaStreamBeginCapture(s1, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
         cudaError_t le = launch_render(sc, nullptr, nullptr, cam, 0.0f, nullptr, nullptr, ws, L, nullptr, s1, nullptr,
-                                       s2, fork);
-        cudaError_t je = cudaEventRecord(join, s2);
-        if (je == cudaSuccess) je = cudaStreamWaitEvent(s1, join, 0);
+                                       nullptr, nullptr, nullptr, nullptr, true);
         cudaError_t ee = cudaStreamEndCapture(s1, &g.graph);
-        e = le != cudaSuccess ? le : (je != cudaSuccess ? je : ee);
+        e = le != cudaSuccess ? le : ee;
     }
     if (e == cudaSuccess) {
         size_t nn = 0;
@@ -1869,27 +1928,23 @@ cudaError_t render_graph_build(RenderGraphImpl &g, const SceneDev &sc, const Cam
             cudaKernelNodeParams p{};
             if ((e = cudaGraphKernelNodeGetParams(nodes[k], &p)) != cudaSuccess) break;
             cudaKernelNodeAttrValue pr{};
-            pr.priority = p.func == blend_fn() ? least : greatest;
+            pr.priority = greatest;
             e = cudaGraphKernelNodeSetAttribute(nodes[k], cudaKernelNodeAttributePriority, &pr);
             if (p.func == (void *)k_cull) g.n_cull = nodes[k], g.p_cull = p;
             else if (p.func == (void *)k_cull_emit) g.n_emit = nodes[k], g.p_emit = p;
             else if (p.func == (void *)k_slice) g.n_slice = nodes[k], g.p_slice = p;
-            else if (p.func == blend_fn()) g.n_blend = nodes[k], g.p_blend = p;
         }
-        if (e == cudaSuccess && (!g.n_cull || !g.n_emit || !g.n_slice || !g.n_blend)) e = cudaErrorInvalidValue;
+        if (e == cudaSuccess && (!g.n_cull || !g.n_emit || !g.n_slice)) e = cudaErrorInvalidValue;
     }
-    // per-node priorities (front end high, blend low) instead of the launching stream's
+    // front-end nodes at the device's greatest priority, whatever the launching stream's
     if (e == cudaSuccess) e = cudaGraphInstantiateWithFlags(&g.exec, g.graph, cudaGraphInstantiateFlagUseNodePriority);
-    if (fork) cudaEventDestroy(fork);
-    if (join) cudaEventDestroy(join);
     if (s1) cudaStreamDestroy(s1);
-    if (s2) cudaStreamDestroy(s2);
     return e;
 }
 
 cudaError_t render_graph_launch(RenderGraphImpl &g, const SceneDev &sc, const uint32_t *mask_l,
                                 const uint32_t *mask_r, const CamDev &cam, float t, float *out_rgb, float *out_T,
-                                cudaStream_t st) {
+                                cudaStream_t st, cudaStream_t blend_st, cudaEvent_t split_ev) {
     const RenderLayout &L = g.L;
     char *ws = g.ws;
     Counters *ctr = reinterpret_cast<Counters *>(ws + L.counters);
@@ -1929,20 +1984,22 @@ cudaError_t render_graph_launch(RenderGraphImpl &g, const SceneDev &sc, const ui
     p.kernelParams = a_slice;
     p.extra = nullptr;
     if (e == cudaSuccess) e = cudaGraphExecKernelNodeSetParams(g.exec, g.n_slice, &p);
-    // k_blend_wl(tile_start, entries, rec0, rec1, rec2, ctr, tiles_x, width, height, bg0, bg1, bg2, out_rgb, out_T)
-    const uint32_t *tstart_c = tstart, *entries_c = entries;
-    const float4 *r0c = rec0, *r1c = rec1, *r2c = rec2;
-    int tiles_x = L.tiles_x, width = L.width, height = L.height;
-    float bg0 = cam.bg[0], bg1 = cam.bg[1], bg2 = cam.bg[2];
-    void *a_blend[] = {(void *)&tstart_c, (void *)&entries_c, (void *)&r0c,    (void *)&r1c,   (void *)&r2c,
-                       (void *)&cctr,     (void *)&tiles_x,   (void *)&width,  (void *)&height, (void *)&bg0,
-                       (void *)&bg1,      (void *)&bg2,       (void *)&out_rgb, (void *)&out_T};
-    p = g.p_blend;
-    p.kernelParams = a_blend;
-    p.extra = nullptr;
-    if (e == cudaSuccess) e = cudaGraphExecKernelNodeSetParams(g.exec, g.n_blend, &p);
     if (e == cudaSuccess) e = cudaGraphLaunch(g.exec, st);
-    return e;
+    if (e != cudaSuccess) return e;
+    // the timed blend, launched directly (on the blend stream when given)
+    cudaStream_t bst = st;
+    if (blend_st != nullptr) {
+        if ((e = cudaEventRecord(split_ev, st)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(blend_st, split_ev, 0)) != cudaSuccess) return e;
+        bst = blend_st;
+    }
+    if (blend_wl())
+        k_blend_wl<<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, cctr, L.tiles_x, L.width,
+                                                      L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
+    else
+        k_blend_wi<<<L.n_tiles, kWiThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, cctr, L.tiles_x, L.width,
+                                                      L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
+    return cudaGetLastError();
 }
 
 void render_graph_free(RenderGraphImpl &g) {

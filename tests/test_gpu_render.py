@@ -469,9 +469,11 @@ def test_aabb_redundant_flag_sound():
 
 def test_blend_wl_alternative_matches():
     """FDGS_BLEND=wl selects the warp-specialised k_blend_wl for the timed
-    blend (read once per process, so in a subprocess): its C2 frame must equal
-    k_blend_wi's bit for bit (same arithmetic, same record lists; k_blend_wi
-    itself is parity-tested against the oracle above)."""
+    blend (read once per process, so in a subprocess): its C2 frame must match
+    k_blend_wi's (same arithmetic, same record lists and stop decisions; only
+    k_blend_wi's paired stop test undoes a terminal step by subtraction, a
+    rounding-level difference <= 1e-6; k_blend_wi itself is parity-tested
+    against the oracle above)."""
     import os
     import subprocess
     import sys
@@ -490,4 +492,4 @@ def test_blend_wl_alternative_matches():
         import io
         imgs.append(np.load(io.BytesIO(res.stdout)))
     assert imgs[0].shape == (3, 800, 800)
-    assert np.array_equal(imgs[0], imgs[1])
+    assert np.abs(imgs[0] - imgs[1]).max() <= 1e-6
