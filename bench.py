@@ -16,6 +16,7 @@ tier's reference arm) on bounded samples of the same workload.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -354,6 +355,10 @@ def run_ours(args):
     n_vis_tot = n_ent_tot = n_act_tot = 0
     timed_frames = []
     timing_now[0] = True
+    # no cyclic-GC pauses while steps are enqueued (a pause longer than the
+    # host's lead over the GPU starves the queue); collected after timing
+    gc.collect()
+    gc.disable()
     for _ in range(args.steps):
         fr = next_frames()
         timed_frames.append(fr)
@@ -362,6 +367,7 @@ def run_ours(args):
         if stg is not None:
             stage_ms += stg
     clocks = sampler.stop()
+    gc.enable()
     timing_now[0] = False
     # k_mask_compact + k_scene_gather per working set built inside the timed steps
     compact_launches = 2 * sum(1 for x in compacts if x)
@@ -477,7 +483,8 @@ def run_ours(args):
     # time: the pipeline is host-bound if the ratio approaches 1
     res["host_enqueue"] = {"ms_per_frame_median": round(float(np.median(host_timed)) / F, 4),
                            "ms_per_frame_max": round(float(np.max(host_timed)) / F, 4),
-                           "vs_device": round(float(np.median(host_timed)) / float(np.median(step_ms)), 3)}
+                           "vs_device": round(float(np.median(host_timed)) / float(np.median(step_ms)), 3),
+                           "slowest_step": int(np.argmax(host_timed))}
     res["setup"] = {"keyframe_masks_s": round(mask_build_s, 3), "n_keyframes": len(kf)}
 
     # ---- e2e through the public API with host buffers

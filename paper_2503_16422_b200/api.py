@@ -352,6 +352,11 @@ class RenderPipeline:
         self.front = [torch.cuda.Stream(device=scene.device, priority=-1 if split else 0) for _ in range(depth)]
         self.blend = [torch.cuda.Stream(device=scene.device, priority=0) for _ in range(depth)] if split else None
         self.split_ev = [torch.cuda.Event() for _ in range(depth)]
+        # reused per-workspace events (created once: no event creation per frame)
+        self.done_ev = [torch.cuda.Event() for _ in range(depth)]
+        self.fin_ev = [torch.cuda.Event() for _ in range(depth)]
+        self.start_ev = torch.cuda.Event()
+        self.join_ev = [torch.cuda.Event() for _ in range(2 * depth + copy_streams)]
         # D2H of finished frames (render_many host_outs), alternating over copy streams
         self.copies = [torch.cuda.Stream(device=scene.device) for _ in range(copy_streams)]
         self.depth = depth
@@ -401,7 +406,7 @@ class RenderPipeline:
         the current work of `stream` (default: current stream), and `stream`
         waits for every frame (and copy) before continuing.  Async."""
         main = stream or torch.cuda.current_stream()
-        start = torch.cuda.Event()
+        start = self.start_ev
         start.record(main)
         for s in self.streams:
             s.wait_event(start)
@@ -415,9 +420,8 @@ class RenderPipeline:
             r = self.renderers[i]
             if self.graphs and self.split:
                 if k >= self.depth:  # the workspace is free once its previous blend is done
-                    done = torch.cuda.Event()
-                    done.record(self.blend[i])
-                    self.front[i].wait_event(done)
+                    self.done_ev[i].record(self.blend[i])
+                    self.front[i].wait_event(self.done_ev[i])
                 r.render_graph(cam, t, ml, mr, out=outs[k], stream=self.front[i], scene=sc,
                                blend_stream=self.blend[i], split_event=self.split_ev[i])
                 last = self.blend[i]
@@ -430,9 +434,8 @@ class RenderPipeline:
                 last = self.front[i]
             else:
                 if k >= self.depth:  # the workspace is free once its previous blend is done
-                    done = torch.cuda.Event()
-                    done.record(self.blend[i])
-                    self.front[i].wait_event(done)
+                    self.done_ev[i].record(self.blend[i])
+                    self.front[i].wait_event(self.done_ev[i])
                 r.render_split(cam, t, ml, mr, out=outs[k], stats=None if stats is None else stats[k],
                                stream=self.front[i], blend_stream=self.blend[i], split_event=self.split_ev[i],
                                stage_events=None if stage_events is None else stage_events[k], scene=sc)
@@ -441,14 +444,13 @@ class RenderPipeline:
                 with torch.cuda.stream(last):
                     status_out[k].copy_(self.counters_view(i), non_blocking=True)
             if host_outs is not None:
-                fin = torch.cuda.Event()
+                fin = self.fin_ev[i]
                 fin.record(last)
                 cp = self.copies[k % len(self.copies)]
                 cp.wait_event(fin)
                 with torch.cuda.stream(cp):
                     host_outs[k].copy_(outs[k], non_blocking=True)
-        for s in self.streams + (self.copies if host_outs is not None else []):
-            e = torch.cuda.Event()
+        for s, e in zip(self.streams + (self.copies if host_outs is not None else []), self.join_ev):
             e.record(s)
             main.wait_event(e)
         return outs
