@@ -1716,14 +1716,20 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
     }
 }
 
-// Blend kernel of the timed path: k_blend_wi, or k_blend_wl when FDGS_BLEND=wl.
-static bool blend_wl() {
-    static const bool v = [] {
+// Blend kernel of the timed path, from the environment variable FDGS_BLEND
+// (read once per process): "wi" (default) k_blend_wi, "wl" k_blend_wl, "ws"
+// k_blend_ws<false> (the variant that visits every record).
+static int blend_sel() {
+    static const int v = [] {
         const char *e = getenv("FDGS_BLEND");
-        return e != nullptr && e[0] == 'w' && e[1] == 'l' && e[2] == 0;
+        if (e == nullptr) return 0;
+        if (e[0] == 'w' && e[1] == 'l' && e[2] == 0) return 1;
+        if (e[0] == 'w' && e[1] == 's' && e[2] == 0) return 2;
+        return 0;
     }();
     return v;
 }
+static bool blend_wl() { return blend_sel() == 1; }
 
 // ---------------------------------------------------------------- launcher
 // Persistent-grid sizes (blocks per SM); FDGS_PGRID / FDGS_RGRID override for tuning.
@@ -1846,7 +1852,6 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         bst = blend_st;
     }
     if (ev && (e = cudaEventRecord(ev[3], bst)) != cudaSuccess) return e;
-    static const bool wl_blend = tune_env("FDGS_BLEND_WL", 1) == 1;  // FDGS_BLEND_WL=0: k_blend_ws for frames too
     if (!(dbg_stages & 2)) {
     } else if (contrib != nullptr) {  // spatial-score recording (fdgs_stv_score)
         k_blend_ws<false, true><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x,
@@ -1856,7 +1861,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         k_blend_ws<true><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
                                                             L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T,
                                                             stats);
-    } else if (wl_blend) {  // the timed blend
+    } else if (blend_sel() != 2) {  // the timed blend
         if (blend_wl())
             k_blend_wl<<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
                                                           L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
