@@ -468,7 +468,7 @@ def test_aabb_redundant_flag_sound():
 
 
 def test_blend_wl_alternative_matches():
-    """FDGS_BLEND=wl selects the warp-specialised k_blend_wl for the timed
+    """FDGS_BLEND=wl / ws select k_blend_wl / k_blend_ws for the timed
     blend (read once per process, so in a subprocess): its C2 frame must match
     k_blend_wi's (same arithmetic, same record lists and stop decisions; only
     k_blend_wi's paired stop test undoes a terminal step by subtraction, a
@@ -485,7 +485,7 @@ def test_blend_wl_alternative_matches():
         "import sys; np.save(sys.stdout.buffer, out.cpu().numpy())\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     imgs = []
-    for sel in ("wi", "wl"):
+    for sel in ("wi", "wl", "ws"):
         env = dict(os.environ, FDGS_BLEND=sel, PYTHONPATH=root)
         res = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, timeout=300)
         assert res.returncode == 0, res.stderr.decode()[-2000:]
@@ -493,3 +493,6 @@ def test_blend_wl_alternative_matches():
         imgs.append(np.load(io.BytesIO(res.stdout)))
     assert imgs[0].shape == (3, 800, 800)
     assert np.abs(imgs[0] - imgs[1]).max() <= 1e-6
+    # k_blend_ws (FDGS_BLEND=ws) carries T instead of U = T/255: the same
+    # decisions except at termination knife edges, within the parity bar
+    assert np.abs(imgs[0] - imgs[2]).max() <= 2e-4
