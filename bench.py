@@ -273,7 +273,7 @@ def run_ours(args):
     stats = torch.zeros((F, 4), dtype=torch.int64, device=dev)  # fdgs_frame_stats is 32 bytes
     flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device=dev)  # 512 MiB > L2
     stream = torch.cuda.current_stream()
-    use_ev = not args.no_stage_events
+    use_ev = not args.no_stage_events and not args.graphs  # graph frames record no stage events
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(F)]
     for row in evs:
         for e in row:
