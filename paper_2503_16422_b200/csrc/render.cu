@@ -1492,6 +1492,10 @@ __global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uin
 #ifndef FDGS_WI_PAIR
 #define FDGS_WI_PAIR 1
 #endif
+#ifndef FDGS_WI_PAIR_UNROLL
+#define FDGS_WI_PAIR_UNROLL 2
+#endif
+constexpr int kWiPairUnroll = FDGS_WI_PAIR_UNROLL;
 
 #ifndef FDGS_WI_PREFETCH
 #define FDGS_WI_PREFETCH 1
@@ -1688,7 +1692,7 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
         } else {
 #if FDGS_WI_PAIR
             int q = 0;
-#pragma unroll 2
+#pragma unroll kWiPairUnroll
             for (; q + 1 < cnt; q += 2) step2(q, std::false_type{});
             if (q < cnt) step(q, std::false_type{});
 #else
