@@ -747,7 +747,10 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t *__restrict__
 // each warp walks a contiguous run of them: 32 (item, tile) entries per round
 // in canonical order, ranked within the round by match_any on the tile, with
 // warp-private per-tile counters carrying the count across rounds.
-constexpr int kRowWarps = 8;
+#ifndef FDGS_ROW_WARPS
+#define FDGS_ROW_WARPS 2
+#endif
+constexpr int kRowWarps = FDGS_ROW_WARPS;
 
 template <bool kWrite>
 __device__ __forceinline__ void row_walk(uint32_t w0, uint32_t w1, int lane, const uint32_t *__restrict__ sorted,
@@ -807,7 +810,10 @@ __device__ __forceinline__ void row_seg_range(const uint32_t *row_start, int ty,
 // Row 5b (5/6) per (row, segment): the segment's entry count per tile ->
 // hist[ty][seg][tx], from a shared-memory difference array over the row's
 // tiles (2 shared atomics per row item)
-__global__ void __launch_bounds__(256) k_row_count(const uint32_t *__restrict__ sorted,
+#ifndef FDGS_ROWCNT_THREADS
+#define FDGS_ROWCNT_THREADS 256
+#endif
+__global__ void __launch_bounds__(FDGS_ROWCNT_THREADS) k_row_count(const uint32_t *__restrict__ sorted,
                                                    const uint32_t *__restrict__ item_pack,
                                                    const uint32_t *__restrict__ row_start, int tiles_x,
                                                    uint32_t *__restrict__ hist, uint32_t *__restrict__ tile_cnt,
@@ -1817,13 +1823,15 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         {
             uint32_t *pcnt = reinterpret_cast<uint32_t *>(ws + L.bin_cnt);  // items per k_bin_count partition
             const int bparts = std::max(1, (L.n + kScanNT - 1) / kScanNT);
-            const int bgrid = std::min(bparts, 8 * L.p_sort);
+            static const int bin_grid = std::max(1, tune_env("FDGS_BIN_GRID", 2));  // blocks per SM (tuning)
+            const int bgrid = std::min(bparts, bin_grid * L.p_sort);
             k_bin_count<<<bgrid, kScanNT, 0, st>>>(rect_sorted, order, rec0, rec1, ctr, bconst, rowdiff, L.tiles_y,
                                                    pcnt);
             k_count_scan<<<1, 1024, 0, st>>>(pcnt, bparts, &ctr->n_vis, kScanNT, &ctr->n_items);
             k_bin_offsets<<<bgrid, kScanNT, 0, st>>>(rect_sorted, ctr, pcnt, ikey[0], iv, (uint32_t)L.max_entries);
         }
-        k_row_items<<<(int)std::min<uint32_t>(item_chunks, 8 * L.p_sort), kScanNT, 0, st>>>(
+        static const int item_grid = std::max(1, tune_env("FDGS_ITEM_GRID", 2));  // blocks per SM (tuning)
+        k_row_items<<<(int)std::min<uint32_t>(item_chunks, item_grid * L.p_sort), kScanNT, 0, st>>>(
             rect_sorted, order, rec0, rec1, bconst, ctr, &ctr->n_items, ikey[0], ipack, iv, (uint32_t)L.max_entries);
         k_row_scan<<<1, 32, 0, st>>>(rowdiff, L.tiles_y, row_start, rbase);
         // stable partition of the row items by tile row (canonical order kept within a row)
@@ -1841,7 +1849,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         const int nrb = L.tiles_y * kRowSeg;
         const size_t cnt_smem = sizeof(uint32_t) * (size_t)kRowWarps * L.tiles_x;
         uint32_t *tcnt = reinterpret_cast<uint32_t *>(ws + L.tile_cnt);  // per-tile totals (zeroed per frame)
-        k_row_count<<<nrb, 256, sizeof(int) * (L.tiles_x + 1), st>>>(sorted_items, ipack, row_start, L.tiles_x, rhist,
+        k_row_count<<<nrb, FDGS_ROWCNT_THREADS, sizeof(int) * (L.tiles_x + 1), st>>>(sorted_items, ipack, row_start, L.tiles_x, rhist,
                                                                       tcnt, ctr);
         k_tile_scan<<<1, 1024, 0, st>>>(tcnt, L.tiles_x, L.tiles_y, tstart, ctr, L.max_entries);
         k_row_scatter<<<nrb, 32 * kRowWarps, cnt_smem + sizeof(uint32_t) * L.tiles_x, st>>>(
