@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -54,7 +55,12 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
 #ifndef FDGS_SLICE_GRID
 #define FDGS_SLICE_GRID 2
 #endif
-    L.slice_grid = std::max(1, std::min(L.n_parts, FDGS_SLICE_GRID * sm_count()));  // grid-stride k_slice / k_vis_emit
+    // grid-stride k_slice / k_vis_emit: blocks per SM (FDGS_SLICE_GRID, env for tuning)
+    static const int slice_grid = [] {
+        const char *e = getenv("FDGS_SLICE_GRID");
+        return e ? std::max(1, atoi(e)) : FDGS_SLICE_GRID;
+    }();
+    L.slice_grid = std::max(1, std::min(L.n_parts, slice_grid * sm_count()));
     L.p_sort = sm_count();
     L.sort_parts = std::max(1, (n + kDepthTile - 1) / kDepthTile);
     L.tile_parts = (int32_t)std::max<int64_t>(1, (max_entries + kTileTile - 1) / kTileTile);

@@ -17,7 +17,10 @@ constexpr int kDepthItems = FDGS_SORT_ITEMS;
 constexpr int kDepthTile = 256 * kDepthItems;  // keys per depth-sort partition (256 threads x items)
 constexpr int kTileSortItems = 4;      // row items per thread in the row-partition passes
 constexpr int kTileTile = 256 * kTileSortItems;
-constexpr int kRowSeg = 16;            // blocks per tile row in the row scatter
+#ifndef FDGS_ROWSEG
+#define FDGS_ROWSEG 16
+#endif
+constexpr int kRowSeg = FDGS_ROWSEG;   // blocks per tile row in the row count / scatter
 constexpr int kMaxTilesY = 512;        // 8192 px / 16
 constexpr uint32_t kFlagA = 1u << 30;  // look-back: aggregate available
 constexpr uint32_t kFlagP = 2u << 30;  // look-back: inclusive prefix available
