@@ -1,19 +1,22 @@
 // render.cu -- the per-frame hot path of fdgs_render.
 //
 //   k_cull           rows 1-2 + temporal cull: active mask OR,
-//                    binary64 p_t >= 1/255 test (Eq. 3), survivors
-//                    compacted in index order (ballot, block scan, look-back)
+//                    binary64 p_t >= 1/255 test (Eq. 3); survivor
+//                    bits and per-partition counts -> k_count_scan ->
+//                    k_cull_emit (survivors compacted in index order)
 //   k_slice          rows 3-4 on the survivors: Eq. 1 slice, EWA
-//                    projection + SH3 colour, visible compaction
+//                    projection + SH3 colour, the aabb_redundant bit;
+//                    visible counts -> k_count_scan -> k_vis_emit
 //   k_sort_*         row 5a: stable onesweep LSD radix sort (4 x 8-bit) of the
 //                    fp32 depth keys -> canonical (depth, index) order (P:126
 //                    "sorted by their depth", reading R8)
-//   k_bin_scan..     row 5b: tile cover per (Gaussian, tile row) (band_tiles),
-//                    per-tile counts, a stable 8-bit row partition of the row
+//   k_bin_count..    row 5b: tile cover per (Gaussian, tile row) (band_tiles),
+//   k_row_scatter    per-tile counts, a stable 8-bit row partition of the row
 //                    items, per-row warp-ordered scatter into the tile lists
 //   k_blend_wi       row 6: per-tile front-to-back Eq. 2, four independent
 //                    warps per tile, each staging and compositing its own
-//                    record lists (the timed kernel)
+//                    record lists, U = T/255 carried, one stop test per pair
+//                    of records (the timed kernel; FDGS_BLEND selects another)
 //   k_blend_wl       row 6: the warp-specialised predecessor of k_blend_wi
 //                    (producer builds per-warp record lists, 4 consumer warps
 //                    composite, warp-uniform early exit);
