@@ -1754,6 +1754,11 @@ static int tune_pgrid() {
     static const int v = std::max(1, tune_env("FDGS_PGRID", 1));
     return v;
 }
+// persistent onesweep grids: tune_pgrid() blocks per SM, divided by FDGS_PGRID_DIV (tuning)
+static int sort_grid(int p_sort) {
+    static const int d = std::max(1, tune_env("FDGS_PGRID_DIV", 2));
+    return std::max(1, tune_pgrid() * p_sort / d);
+}
 
 cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint32_t *mask_r, const CamDev &cam,
                           float t, float *out_rgb, float *out_T, char *ws, const RenderLayout &L,
@@ -1805,7 +1810,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
             // pass 0 reads the compacted keys (keys[1]) and the visible survivor slots
             const uint32_t *kin = pass == 0 ? keys[1] : keys[(pass - 1) & 1];
             const uint32_t *vin = pass == 0 ? vis : vals[(pass - 1) & 1];
-            k_onesweep<8, kDItems><<<std::min(L.sort_parts, tune_pgrid() * L.p_sort), kSortThreads, 0, st>>>(
+            k_onesweep<8, kDItems><<<std::min(L.sort_parts, sort_grid(L.p_sort)), kSortThreads, 0, st>>>(
                 kin, vin, pass == 3 ? nullptr : keys[pass & 1], vals[pass & 1], &ctr->n_vis, epoch,
                 &ctr->sort_ticket[1 + pass], 8 * pass, gbase + 256 * pass,
                 sstat + (size_t)pass * L.sort_parts * 256, rect, pass == 3 ? rect_sorted : nullptr);
@@ -1838,7 +1843,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
             rect_sorted, order, rec0, rec1, bconst, ctr, &ctr->n_items, ikey[0], ipack, iv, (uint32_t)L.max_entries);
         k_row_scan<<<1, 32, 0, st>>>(rowdiff, L.tiles_y, row_start, rbase);
         // stable partition of the row items by tile row (canonical order kept within a row)
-        const int rgrid = std::min((int)item_chunks, tune_pgrid() * L.p_sort);
+        const int rgrid = std::min((int)item_chunks, sort_grid(L.p_sort));
         const uint32_t *sorted_items = ival[0];
         k_onesweep<8, 4><<<rgrid, kSortThreads, 0, st>>>(ikey[0], nullptr, L.tiles_y > 256 ? ikey[1] : nullptr, ival[0],
                                                        &ctr->n_items, epoch, &ctr->tile_ticket[0], 0, rbase, tstat,
