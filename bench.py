@@ -595,8 +595,6 @@ def run_reference(args):
 
 def main():
     args = parse()
-    if os.environ.get("FDGS_DEBUG_STAGES", "3") != "3" and os.environ.get("FDGS_EXPERIMENT") != "1":
-        raise SystemExit("FDGS_DEBUG_STAGES skips render stages (experiments only): unset it to benchmark")
     apply_config(args)
     if args.impl == "reference":
         run_reference(args)

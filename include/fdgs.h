@@ -20,7 +20,11 @@
  *     last non-OK status of the calling thread.
  *   - Layouts are PyTorch-contiguous float32 / uint32 arrays.
  *   - Re-entrant: there is no global mutable state besides the thread-local
- *     error string; concurrent calls on different workspaces are safe.
+ *     error string and two process-wide, initialise-once values (the device's
+ *     SM count and the kernels' shared-memory attributes, both set under
+ *     std::call_once / static initialisation); concurrent calls on different
+ *     workspaces are safe.  The library reads no environment variables: every
+ *     tuning choice (grid shapes, unroll factors) is a compile-time constant.
  */
 #ifndef FDGS_H
 #define FDGS_H

@@ -79,19 +79,27 @@ class Scene:
             raise ValueError("already a compacted working set")
         n, dev = self.n, self.device
         vq = "sh_index" in self.t
-        params = torch.empty((max(n, 1), 4, 4), dtype=torch.float32, device=dev)
-        opacity = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
-        L = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
-        sh = None if vq else torch.empty((max(n, 1), 16, 3), dtype=torch.float32, device=dev)
-        sh_index = torch.empty(max(n, 1), dtype=torch.uint16, device=dev) if vq else None
-        gid = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-        count = torch.zeros(1, dtype=torch.int32, device=dev)
-        nb = lib().fdgs_scene_compact_workspace_bytes(n)
-        ws = torch.empty(nb, dtype=torch.uint8, device=dev)
-        check(lib().fdgs_scene_compact(C.byref(self.struct), _ptr(mask_l), _ptr(mask_r), _ptr(params), _ptr(opacity),
-                                       _ptr(L), _ptr(sh), _ptr(sh_index), _ptr(gid), _ptr(count), _ptr(ws), nb,
-                                       _stream_ptr(stream)))
-        m = int(count.item())
+        st = stream or torch.cuda.current_stream(dev)
+        # every allocation, the zero-fill and the count read-back are ordered on
+        # `st` (the caching allocator ties the buffers to the stream current at
+        # allocation, so they are allocated with `st` current)
+        with torch.cuda.stream(st):
+            params = torch.empty((max(n, 1), 4, 4), dtype=torch.float32, device=dev)
+            opacity = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+            L = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+            sh = None if vq else torch.empty((max(n, 1), 16, 3), dtype=torch.float32, device=dev)
+            sh_index = torch.empty(max(n, 1), dtype=torch.uint16, device=dev) if vq else None
+            gid = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+            count = torch.zeros(1, dtype=torch.int32, device=dev)
+            nb = lib().fdgs_scene_compact_workspace_bytes(n)
+            ws = torch.empty(nb, dtype=torch.uint8, device=dev)
+            check(lib().fdgs_scene_compact(C.byref(self.struct), _ptr(mask_l), _ptr(mask_r), _ptr(params),
+                                           _ptr(opacity), _ptr(L), _ptr(sh), _ptr(sh_index), _ptr(gid), _ptr(count),
+                                           _ptr(ws), nb, _stream_ptr(st)))
+            host = torch.empty(1, dtype=torch.int32, pin_memory=True)
+            host.copy_(count, non_blocking=True)
+        st.synchronize()
+        m = int(host.item())
         out = Scene.__new__(Scene)
         out.n, out.device, out.stride = m, dev, 4
         out.params = params
@@ -283,20 +291,22 @@ class Renderer:
         return out
 
     def render_checked(self, cam, t, mask_l=None, mask_r=None, out=None, out_T=None, stream=None,
-                       grow: bool = True):
-        """Synchronous render; grows the entry capacity and retries on overflow."""
+                       grow: bool = True, scene=None):
+        """Synchronous render; grows the entry capacity and retries on overflow.
+        scene: another Scene to render in this workspace (as render())."""
         out = self.new_output() if out is None else out
-        self._scene_for(None, stream)
-        ml, mr = self._masks(mask_l, mask_r)
-        cs = camera_struct(cam)
+        sc = self._scene_for(scene, stream)
+        ml, mr = self._masks(mask_l, mask_r, sc)
+        cs = camera_struct(cam) if not isinstance(cam, FdgsCamera) else cam
         while True:
             hs = FdgsFrameStats()
-            st = lib().fdgs_render_checked(C.byref(self.scene.struct), ml, mr, C.byref(cs), float(t), _ptr(out),
+            st = lib().fdgs_render_checked(C.byref(sc.struct), ml, mr, C.byref(cs), float(t), _ptr(out),
                                            _ptr(out_T), _ptr(self.ws), self.ws_bytes, self.max_entries,
                                            C.byref(hs), _stream_ptr(stream))
             if st == _lib.FDGS_ERR_OVERFLOW and grow:
                 self.max_entries = int(min(2 ** 32 - 1, max(2 * self.max_entries, hs.n_entries + 1)))
                 self._alloc()
+                self._layout_n = max(sc.n, int(sc.struct.n_capacity))
                 continue
             check(st)
             return out, FrameStats(hs.n_act, hs.n_vis, hs.n_entries, hs.status, hs.n_evaluated, hs.n_blended)
@@ -386,9 +396,10 @@ class RenderPipeline:
         st = status.cpu().view(torch.int32).view(len(frames), 4)
         bad = [k for k in range(len(frames)) if int(st[k, 3]) != _lib.FDGS_OK]
         for k in bad:
-            cam, t, ml, mr = frames[k]
+            cam, t, ml, mr = frames[k][:4]
+            sc = frames[k][4] if len(frames[k]) > 4 else None  # the frame's working set, if any
             r = self.renderers[k % self.depth]
-            _, fs = r.render_checked(cam, t, ml, mr, out=outs[k], stream=main)
+            _, fs = r.render_checked(cam, t, ml, mr, out=outs[k], stream=main, scene=sc)
             st[k] = torch.tensor([fs.n_act, fs.n_vis, fs.n_entries, fs.status], dtype=torch.int32)
             if host_outs is not None:
                 host_outs[k].copy_(outs[k])

@@ -55,12 +55,8 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
 #ifndef FDGS_SLICE_GRID
 #define FDGS_SLICE_GRID 2
 #endif
-    // grid-stride k_slice / k_vis_emit: blocks per SM (FDGS_SLICE_GRID, env for tuning)
-    static const int slice_grid = [] {
-        const char *e = getenv("FDGS_SLICE_GRID");
-        return e ? std::max(1, atoi(e)) : FDGS_SLICE_GRID;
-    }();
-    L.slice_grid = std::max(1, std::min(L.n_parts, slice_grid * sm_count()));
+    // grid-stride k_slice / k_vis_emit: FDGS_SLICE_GRID blocks per SM (compile-time)
+    L.slice_grid = std::max(1, std::min(L.n_parts, FDGS_SLICE_GRID * sm_count()));
     L.p_sort = sm_count();
     L.sort_parts = std::max(1, (n + kDepthTile - 1) / kDepthTile);
     L.tile_parts = (int32_t)std::max<int64_t>(1, (max_entries + kTileTile - 1) / kTileTile);
@@ -603,7 +599,7 @@ fdgs_status fdgs_stv_score(const fdgs_scene *scene, const fdgs_camera *cams, int
         return fail(FDGS_ERR_WORKSPACE_TOO_SMALL, "stv workspace needs %zu bytes (256-aligned), got %zu", SL.total,
                     ws_bytes);
     cudaStream_t st = (cudaStream_t)stream;
-    if (n_ts == 0) {  // empty sums
+    if (n_ts == 0 && d_out_gamma == nullptr) {  // empty sums (gamma does not depend on t)
         cudaError_t e = cudaMemsetAsync(d_out_score, 0, sizeof(float) * (size_t)n, st);
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         return e == cudaSuccess ? FDGS_OK : cuda_fail(e, "fdgs_stv_score");

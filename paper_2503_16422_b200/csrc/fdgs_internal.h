@@ -42,7 +42,8 @@ struct Counters {
     uint32_t n_items;            // (Gaussian, tile row) items
     uint32_t n_surv;             // Gaussians passing the mask and the temporal cull (k_cull)
     uint32_t cull_ticket;        // k_cull partitions
-    uint32_t pad2[8];
+    uint32_t n_items_part;       // row items the row partition sorts: n_items if <= capacity, else 0
+    uint32_t pad2[7];
 };
 static_assert(sizeof(Counters) == 128, "Counters layout");
 

@@ -13,16 +13,13 @@
 //   k_bin_count..    row 5b: tile cover per (Gaussian, tile row) (band_tiles),
 //   k_row_scatter    per-tile counts, a stable 8-bit row partition of the row
 //                    items, per-row warp-ordered scatter into the tile lists
-//   k_blend_wi       row 6: per-tile front-to-back Eq. 2, four independent
-//                    warps per tile, each staging and compositing its own
-//                    record lists, U = T/255 carried, one stop test per pair
-//                    of records (the timed kernel; FDGS_BLEND selects another)
-//   k_blend_wl       row 6: the warp-specialised predecessor of k_blend_wi
-//                    (producer builds per-warp record lists, 4 consumer warps
-//                    composite, warp-uniform early exit);
-//                    k_blend_ws: the counting / contribution-recording variant
+//   k_blend_wi       row 6: per-tile front-to-back Eq. 2, four
+//                    independent warps per tile, each staging and compositing
+//                    its own record lists, U = T/255 carried, one stop test per
+//                    pair of records (the timed kernel)
+//   k_blend_ws       row 6: the counting / contribution-recording variant
+//                    (producer warp + 4 consumer warps, visits every record)
 #include <algorithm>
-#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <new>
@@ -630,10 +627,15 @@ __global__ void __launch_bounds__(kScanNT) k_row_items(const uint2 *__restrict__
                                                        uint32_t *__restrict__ item_pack, uint32_t *__restrict__ item_v,
                                                        uint32_t item_cap) {
     const uint32_t ni = *n_items_ptr;
-    if (ni > item_cap) {  // more row items than the workspace holds
-        if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<Counters *>(ctrc)->status = FDGS_ERR_OVERFLOW;
-        return;
+    // the row partition (next launches) processes n_items_part items: n_items
+    // when they fit the workspace, else none (the frame is then OVERFLOW and
+    // nothing writes past the item / look-back buffers sized by the capacity)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        Counters *c = const_cast<Counters *>(ctrc);
+        c->n_items_part = ni <= item_cap ? ni : 0u;
+        if (ni > item_cap) c->status = FDGS_ERR_OVERFLOW;
     }
+    if (ni > item_cap) return;  // more row items than the workspace holds
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ni; i += gridDim.x * blockDim.x) {
         const uint32_t r = __ldg(item_v + i);  // owning Gaussian (canonical rank), from k_bin_offsets
         const int ty = (int)__ldg(item_key + i);
@@ -990,7 +992,7 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
 // barriers, so consumer warps drift independently; a consumer whose pixels
 // have all terminated keeps releasing batches without computing, and the
 // producer stops once all four are done.  Pixel mapping and arithmetic are
-// those of k_blend_wl; this kernel visits every record of the tile (for the
+// those of k_blend_wi; this kernel visits every record of the tile (for the
 // Eq. 2 work counters) and records contributions (fdgs_stv_score).
 constexpr int kWsBuf = 6;
 // fl(x * kInv255) is monotone in x and equals 0.99f exactly for one float,
@@ -1238,27 +1240,18 @@ __global__ void __launch_bounds__(kWsThreads) k_blend_ws(const uint32_t *__restr
     }
 }
 
-// Warp-list blend (the timed render kernel).  Same producer / consumer
-// structure and per-pixel arithmetic as k_blend_ws, but the producer builds,
-// per batch and per consumer warp, a packed list of the records whose
-// quadratic reaches one of the warp's four rows (per-row maximum over the
-// tile's pixel-centre columns, with a margin), and evaluates the row terms of
-// the pinned e2 chain for those rows itself (dy, t1 = B' dy, t3 = C' dy,
-// t4 = fma(t3, dy, Q2): the same IEEE operations, once per (record, row)
-// instead of once per thread).  A consumer iterates its list linearly: per
-// record the common 16 bytes {u, A', r, g} and its row's {b, ~AABB mask, t1,
-// t4}.  Work counters (kCount) and the contribution recorder stay on
-// k_blend_ws, which visits every record.
+// Per-warp record lists of the timed blend (k_blend_wi): for each record of
+// the tile whose quadratic reaches one of the warp's four rows (per-row
+// maximum over the tile's pixel-centre columns, with a margin), the common
+// 16 bytes {u, A', r, g} and, per row of the warp, {b, ~AABB mask, t1, t4}:
+// the row terms of the pinned e2 chain (dy, t1 = B' dy, t3 = C' dy,
+// t4 = fma(t3, dy, Q2)), evaluated once per (record, row).
 //
 // Footprint of consumer warp w in the tile: 4 rows x 16 columns (a strip).
 constexpr int kWlRows = 4, kWlCols = 16;
 __host__ __device__ constexpr int wl_row0(int w) { return 4 * w; }
 __host__ __device__ constexpr int wl_col0(int w) { return 0; }
 
-#ifndef FDGS_WL_BUF
-#define FDGS_WL_BUF 2
-#endif
-constexpr int kWlBuf = FDGS_WL_BUF;
 // Two 16-byte loads per record for a consumer thread: the common part and its
 // row's part (colour b and the mask repeated per row).
 struct WlEntry {
@@ -1267,234 +1260,17 @@ struct WlEntry {
 };
 static_assert(sizeof(WlEntry) == 16 + 16 * kWlRows, "WlEntry layout");
 
-#ifndef FDGS_WL_MINB
-#define FDGS_WL_MINB 7
-#endif
 #ifndef FDGS_WL_UNROLL
 #define FDGS_WL_UNROLL 4
 #endif
 constexpr int kWlUnroll = FDGS_WL_UNROLL;
-#ifndef FDGS_WL_MASKFREE
-#define FDGS_WL_MASKFREE 1
-#endif
-constexpr bool kWlMaskFree = FDGS_WL_MASKFREE;  // mask-free loop for lists of aabb_redundant records
 constexpr float kStopU = 1e-4f / 255.0f;  // the stop threshold 1e-4 on T, on U = T / 255
-__global__ void __launch_bounds__(kWsThreads, FDGS_WL_MINB) k_blend_wl(const uint32_t *__restrict__ tile_start,
-                                                         const uint32_t *__restrict__ entries,
-                                                         const float4 *__restrict__ rec0,
-                                                         const float4 *__restrict__ rec1,
-                                                         const float4 *__restrict__ rec2, const Counters *ctr,
-                                                         int tiles_x, int width, int height, float bg0, float bg1,
-                                                         float bg2, float *__restrict__ out_rgb,
-                                                         float *__restrict__ out_T) {
-    __shared__ WlEntry s_list[kWlBuf][4][32];
-    // list length per consumer warp; [.][0] bit 31 = end of tile; bit 30: some
-    // record of the list needs the per-pixel AABB test
-    __shared__ uint32_t s_cnt[kWlBuf][4];
-    __shared__ __align__(8) uint64_t full[kWlBuf], empty[kWlBuf];
-    __shared__ uint32_t s_done;
-    constexpr uint32_t kEnd = 0x80000000u, kMasked = 0x40000000u;
-    const bool ok = ctr->status == FDGS_OK;
-    const int tile = blockIdx.x, tx = tile % tiles_x, ty = tile / tiles_x;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t start = __ldg(tile_start + tile), end = __ldg(tile_start + tile + 1);
-    if (tid == 0) {
-        for (int b = 0; b < kWlBuf; ++b) {
-            mb_init(&full[b], 1);
-            mb_init(&empty[b], 4);
-        }
-        s_done = 0;
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const uint32_t first = ok ? start : end;
-    if (warp == 4) {  // ------------------------------------------------ producer
-        uint32_t k = 0;
-        for (uint32_t base = first;; base += 32, ++k) {
-            const int b = (int)(k % kWlBuf);
-            if (k >= kWlBuf) mb_wait(&empty[b], ((k / kWlBuf) - 1) & 1);
-            const bool stop = base >= end || *(volatile uint32_t *)&s_done == 4;
-            const uint32_t n = stop ? 0u : min(32u, end - base);
-            uint32_t mb = 0;
-            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0;
-            if (lane < (int)n) {
-                const uint32_t v = __ldg(entries + base + lane);
-                r0 = __ldg(rec0 + v);
-                r1 = __ldg(rec1 + v);
-                r2 = __ldg(rec2 + v);
-            }
-            const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
-            const bool redundant = (__float_as_uint(r1.w) & 0x80000000u) != 0u;  // aabb_redundant (k_slice)
-            // Per-row reach: row j of the tile is reached if the maximum over the
-            // pixel-centre columns [xl, xr] (tile ∩ AABB) of the row's quadratic
-            // x (A' x + t1) + t4 -- the consumer's own pinned e2 chain, with the
-            // same t1, t4 and the same rounding of the column offsets -- is
-            // >= -margin (margin 1e-3 |quadratic| + 1e-3 over the tile ∩ AABB
-            // covers the rounding of both evaluations).  Exact per row, so
-            // tighter than a box test and ~40% fewer producer instructions.
-            float xl = 0.f, xr = 0.f, hA = 0.f, marg = 0.f;
-            int y0 = 16, y1 = -1;
-            if (lane < (int)n) {
-                const uint32_t ax = __float_as_uint(r1.z), ay = __float_as_uint(r1.w);
-                const int x0 = max((int)(ax & 0xffff) - tx * 16, 0), x1 = min((int)(ax >> 16) - tx * 16, 15);
-                y0 = max((int)(ay & 0xffff) - ty * 16, 0);
-                y1 = min((int)((ay >> 16) & 0x7fffu) - ty * 16, 15);
-                const uint32_t xm = ((2u << x1) - 1u) & ~((1u << x0) - 1u);
-                const uint32_t ym = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
-                mb = ~(xm | (ym << 16));
-                if (x0 > x1) y1 = -1;
-                xl = __fsub_rn((float)(tx * 16 + x0) + 0.5f, u);
-                xr = __fsub_rn((float)(tx * 16 + x1) + 0.5f, u);
-                const float yl = (float)(ty * 16 + y0) + 0.5f - v, yr = (float)(ty * 16 + y1) + 0.5f - v;
-                const float X = fmaxf(fabsf(xl), fabsf(xr)), Y = fmaxf(fabsf(yl), fabsf(yr));
-                marg = -(1e-3f * (fabsf(Ap) * X * X + fabsf(Bp) * X * Y + fabsf(Cp) * Y * Y) + 1e-3f);
-                hA = __fdividef(-0.5f, Ap);  // stationary point only
-            }
-            const float mbits = __uint_as_float(mb);
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {  // per consumer warp: packed list + its rows' e2 row terms
-                float4 tr[kWlRows];
-                bool rw = false;
-#pragma unroll
-                for (int r = 0; r < kWlRows; ++r) {  // pinned e2 chain, row terms (DESIGN.md step 10)
-                    const int row = wl_row0(w) + r;
-                    const float dy = __fsub_rn((float)(ty * 16 + row) + 0.5f, v);
-                    const float t1 = __fmul_rn(Bp, dy);
-                    const float t3 = __fmul_rn(Cp, dy);
-                    const float t4 = __fmaf_rn(t3, dy, Q2);
-                    const float xs = fminf(fmaxf(t1 * hA, xl), xr);
-                    rw |= row >= y0 && row <= y1 && fmaf(xs, fmaf(Ap, xs, t1), t4) >= marg;
-                    tr[r] = make_float4(r2.z, mbits, t1, t4);
-                }
-                const bool reach = lane < (int)n && rw;
-                const uint32_t bal = __ballot_sync(0xffffffffu, reach);
-                // the AABB test matters for warp w unless proven redundant or the
-                // AABB covers the warp's footprint
-                const uint32_t foot = (((2u << (wl_col0(w) + kWlCols - 1)) - 1u) & ~((1u << wl_col0(w)) - 1u)) |
-                                      (((1u << kWlRows) - 1u) << (16 + wl_row0(w)));
-                const bool masked = __any_sync(0xffffffffu, reach && !redundant && (mb & foot) != 0u);
-                if (reach) {
-                    WlEntry &E = s_list[b][w][__popc(bal & lanemask_lt())];
-                    E.a = make_float4(u, Ap, r2.x, r2.y);
-#pragma unroll
-                    for (int r = 0; r < kWlRows; ++r) {
-                        E.t[r] = tr[r];
-                    }
-                }
-                if (lane == w)
-                    s_cnt[b][w] = (uint32_t)__popc(bal) | (n == 0 ? kEnd : 0u) | (kWlMaskFree && !masked ? 0u : kMasked);
-            }
-            __syncwarp();
-            if (lane == 0) mb_arrive(&full[b]);
-            if (n == 0) break;
-        }
-    } else {  // --------------------------------------------------------- consumers
-        // 2 horizontally adjacent pixels per thread; the warp covers its footprint
-        const int rr = lane / (kWlCols / 2), ly = wl_row0(warp) + rr, lx = wl_col0(warp) + (lane % (kWlCols / 2)) * 2;
-        const int i0 = tx * 16 + lx, j = ty * 16 + ly;
-        const bool in0 = i0 < width && j < height, in1 = i0 + 1 < width && j < height;
-        float2 px = make_float2((float)i0 + 0.5f, (float)(i0 + 1) + 0.5f);
-        const uint32_t pb0 = (1u << lx) | (1u << (16 + ly)), pb1 = (2u << lx) | (1u << (16 + ly));
-        const float kInf = __int_as_float(0x7f800000);
-        float2 thr = make_float2(in0 ? 0.0f : kInf, in1 ? 0.0f : kInf);
-        // U = T / 255: w = min(2^e2, 0.99 * 255) U = alpha T without the 1/255
-        // multiply; a stop decision (T - w < 1e-4, i.e. U - w/255 < 1e-4/255)
-        // undoes the step in a rare branch instead of selecting every record.
-        float2 T = make_float2(kInv255, kInv255), Cr = make_float2(0.f, 0.f), Cg = Cr, Cb = Cr;
-        // one record (q) of the list; kAabb: apply the per-pixel AABB test
-        auto step = [&](const WlEntry *E, const float4 *Tp, int q, auto kAabb) {
-            const float4 a = E[q].a;
-            const float4 rt = *reinterpret_cast<const float4 *>(reinterpret_cast<const char *>(Tp) + q * sizeof(WlEntry));
-            asm volatile("" : "+f"(px.x), "+f"(px.y));
-            const float2 dx = sub2(px, make_float2(a.x, a.x));
-            const float2 t2 = fma2(make_float2(a.y, a.y), dx, make_float2(rt.z, rt.z));
-            const float2 e2 = fma2(dx, t2, make_float2(rt.w, rt.w));
-            bool v0 = e2.x >= thr.x, v1 = e2.y >= thr.y;
-            if constexpr (decltype(kAabb)::value) {
-                const uint32_t m = __float_as_uint(rt.y);
-                v0 = v0 && (m & pb0) == 0u;
-                v1 = v1 && (m & pb1) == 0u;
-            }
-            const float m0 = v0 ? fminf(ex2_approx(e2.x), kAlphaPre) : 0.0f;
-            const float m1 = v1 ? fminf(ex2_approx(e2.y), kAlphaPre) : 0.0f;
-            const float2 w = mul2(make_float2(m0, m1), T);
-            const float2 Tprev = T;
-            T = fma2(make_float2(-kInv255, -kInv255), w, T);
-            Cr = fma2(make_float2(a.z, a.z), w, Cr);
-            Cg = fma2(make_float2(a.w, a.w), w, Cg);
-            Cb = fma2(make_float2(rt.x, rt.x), w, Cb);
-            // T >= kStopU holds before every step (a stop restores it), so only
-            // a blended record can bring T below the threshold
-            const bool s0 = T.x < kStopU, s1 = T.y < kStopU;
-            if (__builtin_expect(s0 || s1, 0)) {
-                if (s0) {
-                    Cr.x = fmaf(-a.z, w.x, Cr.x);
-                    Cg.x = fmaf(-a.w, w.x, Cg.x);
-                    Cb.x = fmaf(-rt.x, w.x, Cb.x);
-                    T.x = Tprev.x;
-                    thr.x = kInf;
-                }
-                if (s1) {
-                    Cr.y = fmaf(-a.z, w.y, Cr.y);
-                    Cg.y = fmaf(-a.w, w.y, Cg.y);
-                    Cb.y = fmaf(-rt.x, w.y, Cb.y);
-                    T.y = Tprev.y;
-                    thr.y = kInf;
-                }
-            }
-        };
-        bool wdone = __all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf);
-        if (wdone && lane == 0) atomicAdd(&s_done, 1u);
-        for (uint32_t k = 0;; ++k) {
-            const int b = (int)(k % kWlBuf);
-            mb_wait(&full[b], (k / kWlBuf) & 1);
-            const uint32_t cw = s_cnt[b][warp];
-            if (s_cnt[b][0] & kEnd) break;
-            if (!wdone) {
-                const int cnt = (int)(cw & 0xffffu);
-                const WlEntry *E = &s_list[b][warp][0];
-                const float4 *Tp = &s_list[b][warp][0].t[rr];
-                if (cw & kMasked) {
-#pragma unroll kWlUnroll
-                    for (int q = 0; q < cnt; ++q) step(E, Tp, q, std::true_type{});
-                } else {
-#pragma unroll kWlUnroll
-                    for (int q = 0; q < cnt; ++q) step(E, Tp, q, std::false_type{});
-                }
-                wdone = __all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf);
-                if (wdone && lane == 0) atomicAdd(&s_done, 1u);
-            }
-            __syncwarp();
-            if (lane == 0) mb_arrive(&empty[b]);
-        }
-        T = mul2(T, make_float2(255.0f, 255.0f));
-        if (ok && out_rgb != nullptr) {
-            const size_t hw = (size_t)width * height, p = (size_t)j * width + i0;
-            if (in0) {
-                out_rgb[p] = fmaf(T.x, bg0, Cr.x);
-                out_rgb[hw + p] = fmaf(T.x, bg1, Cg.x);
-                out_rgb[2 * hw + p] = fmaf(T.x, bg2, Cb.x);
-                if (out_T) out_T[p] = T.x;
-            }
-            if (in1) {
-                out_rgb[p + 1] = fmaf(T.y, bg0, Cr.y);
-                out_rgb[hw + p + 1] = fmaf(T.y, bg1, Cg.y);
-                out_rgb[2 * hw + p + 1] = fmaf(T.y, bg2, Cb.y);
-                if (out_T) out_T[p + 1] = T.y;
-            }
-        }
-    }
-}
-
-// Warp-independent blend (the timed kernel; the environment variable
-// FDGS_BLEND=wl selects k_blend_wl instead, read once per process):
-// no producer warp and no barriers
+// Warp-independent blend (the timed kernel): no producer warp and no barriers
 // between warps.  Each of the 4 warps of a tile block stages its own batches of
 // 32 records (one per lane: the gather, the AABB mask, the per-row reach test
-// and the pinned row terms of its 4-row strip, exactly as k_blend_wl's
-// producer does for that warp) into a private shared list, then composites
-// it; the next batch's records are gathered into registers while the current
-// list is composited.  Same arithmetic and results as k_blend_wl.
+// and the pinned row terms of its 4-row strip) into a private shared list,
+// then composites it; the next batch's records are gathered into registers
+// while the current list is composited.
 #ifndef FDGS_WI_MINB
 #define FDGS_WI_MINB 8
 #endif
@@ -1729,36 +1505,25 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
     }
 }
 
-// Blend kernel of the timed path, from the environment variable FDGS_BLEND
-// (read once per process): "wi" (default) k_blend_wi, "wl" k_blend_wl, "ws"
-// k_blend_ws<false> (the variant that visits every record).
-static int blend_sel() {
-    static const int v = [] {
-        const char *e = getenv("FDGS_BLEND");
-        if (e == nullptr) return 0;
-        if (e[0] == 'w' && e[1] == 'l' && e[2] == 0) return 1;
-        if (e[0] == 'w' && e[1] == 's' && e[2] == 0) return 2;
-        return 0;
-    }();
-    return v;
-}
-static bool blend_wl() { return blend_sel() == 1; }
-
 // ---------------------------------------------------------------- launcher
-// Persistent-grid sizes (blocks per SM); FDGS_PGRID / FDGS_RGRID override for tuning.
-static int tune_env(const char *name, int dflt) {
-    const char *e = getenv(name);
-    return e ? std::max(0, atoi(e)) : dflt;
-}
-static int tune_pgrid() {
-    static const int v = std::max(1, tune_env("FDGS_PGRID", 1));
-    return v;
-}
-// persistent onesweep grids: tune_pgrid() blocks per SM, divided by FDGS_PGRID_DIV (tuning)
-static int sort_grid(int p_sort) {
-    static const int d = std::max(1, tune_env("FDGS_PGRID_DIV", 2));
-    return std::max(1, tune_pgrid() * p_sort / d);
-}
+// Grid shapes of the front end (compile-time; DESIGN.md "Thin front-end
+// kernels"): persistent onesweep grids on FDGS_PGRID blocks per SM divided by
+// FDGS_PGRID_DIV, the binning kernels on FDGS_BIN_GRID / FDGS_ITEM_GRID blocks
+// per SM.  The library reads no environment variables.
+#ifndef FDGS_PGRID
+#define FDGS_PGRID 1
+#endif
+#ifndef FDGS_PGRID_DIV
+#define FDGS_PGRID_DIV 2
+#endif
+#ifndef FDGS_BIN_GRID
+#define FDGS_BIN_GRID 2
+#endif
+#ifndef FDGS_ITEM_GRID
+#define FDGS_ITEM_GRID 2
+#endif
+static_assert(FDGS_PGRID >= 1 && FDGS_PGRID_DIV >= 1 && FDGS_BIN_GRID >= 1 && FDGS_ITEM_GRID >= 1, "grid shapes");
+static int sort_grid(int p_sort) { return std::max(1, FDGS_PGRID * p_sort / FDGS_PGRID_DIV); }
 
 cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint32_t *mask_r, const CamDev &cam,
                           float t, float *out_rgb, float *out_T, char *ws, const RenderLayout &L,
@@ -1780,11 +1545,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
 
     cudaError_t e = cudaSuccess;
     if (ev && (e = cudaEventRecord(ev[0], st)) != cudaSuccess) return e;
-    // FDGS_DEBUG_STAGES (experiments only): bit 0 front end, bit 1 blend; with bit 0
-    // clear the workspace's previous lists are blended again
-    static const int dbg_stages = tune_env("FDGS_DEBUG_STAGES", 3);
-    static std::atomic<int> dbg_calls{0};  // the first 64 frames always build lists (fills every workspace)
-    if ((dbg_stages & 1) || dbg_calls.fetch_add(1, std::memory_order_relaxed) < 64) {
+    {
         e = cudaMemsetAsync(ws + L.counters, 0, L.zero_end - L.counters, st);  // counters, look-back, histograms
         if (e != cudaSuccess) return e;
         if (sc.n > 0) {
@@ -1805,12 +1566,12 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         uint32_t *epoch = reinterpret_cast<uint32_t *>(ws + L.epoch);
         uint64_t *sstat = reinterpret_cast<uint64_t *>(ws + L.sort_status);
         k_sort_hist<<<L.p_sort, kSortThreads, 0, st>>>(keys[1], ctr, gbase, epoch);
-        constexpr int kDItems = 4;
+        static_assert(kDepthTile == kSortThreads * kDepthItems, "depth-sort partition = status-table stride");
         for (int pass = 0; pass < 4; ++pass) {
             // pass 0 reads the compacted keys (keys[1]) and the visible survivor slots
             const uint32_t *kin = pass == 0 ? keys[1] : keys[(pass - 1) & 1];
             const uint32_t *vin = pass == 0 ? vis : vals[(pass - 1) & 1];
-            k_onesweep<8, kDItems><<<std::min(L.sort_parts, sort_grid(L.p_sort)), kSortThreads, 0, st>>>(
+            k_onesweep<8, kDepthItems><<<std::min(L.sort_parts, sort_grid(L.p_sort)), kSortThreads, 0, st>>>(
                 kin, vin, pass == 3 ? nullptr : keys[pass & 1], vals[pass & 1], &ctr->n_vis, epoch,
                 &ctr->sort_ticket[1 + pass], 8 * pass, gbase + 256 * pass,
                 sstat + (size_t)pass * L.sort_parts * 256, rect, pass == 3 ? rect_sorted : nullptr);
@@ -1831,25 +1592,23 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         {
             uint32_t *pcnt = reinterpret_cast<uint32_t *>(ws + L.bin_cnt);  // items per k_bin_count partition
             const int bparts = std::max(1, (L.n + kScanNT - 1) / kScanNT);
-            static const int bin_grid = std::max(1, tune_env("FDGS_BIN_GRID", 2));  // blocks per SM (tuning)
-            const int bgrid = std::min(bparts, bin_grid * L.p_sort);
+            const int bgrid = std::min(bparts, FDGS_BIN_GRID * L.p_sort);
             k_bin_count<<<bgrid, kScanNT, 0, st>>>(rect_sorted, order, rec0, rec1, ctr, bconst, rowdiff, L.tiles_y,
                                                    pcnt);
             k_count_scan<<<1, 1024, 0, st>>>(pcnt, bparts, &ctr->n_vis, kScanNT, &ctr->n_items);
             k_bin_offsets<<<bgrid, kScanNT, 0, st>>>(rect_sorted, ctr, pcnt, ikey[0], iv, (uint32_t)L.max_entries);
         }
-        static const int item_grid = std::max(1, tune_env("FDGS_ITEM_GRID", 2));  // blocks per SM (tuning)
-        k_row_items<<<(int)std::min<uint32_t>(item_chunks, item_grid * L.p_sort), kScanNT, 0, st>>>(
+        k_row_items<<<(int)std::min<uint32_t>(item_chunks, FDGS_ITEM_GRID * L.p_sort), kScanNT, 0, st>>>(
             rect_sorted, order, rec0, rec1, bconst, ctr, &ctr->n_items, ikey[0], ipack, iv, (uint32_t)L.max_entries);
         k_row_scan<<<1, 32, 0, st>>>(rowdiff, L.tiles_y, row_start, rbase);
         // stable partition of the row items by tile row (canonical order kept within a row)
         const int rgrid = std::min((int)item_chunks, sort_grid(L.p_sort));
         const uint32_t *sorted_items = ival[0];
-        k_onesweep<8, 4><<<rgrid, kSortThreads, 0, st>>>(ikey[0], nullptr, L.tiles_y > 256 ? ikey[1] : nullptr, ival[0],
-                                                       &ctr->n_items, epoch, &ctr->tile_ticket[0], 0, rbase, tstat,
+        k_onesweep<8, kTileSortItems><<<rgrid, kSortThreads, 0, st>>>(ikey[0], nullptr, L.tiles_y > 256 ? ikey[1] : nullptr, ival[0],
+                                                       &ctr->n_items_part, epoch, &ctr->tile_ticket[0], 0, rbase, tstat,
                                                        nullptr, nullptr);
         if (L.tiles_y > 256) {
-            k_onesweep<8, 4><<<rgrid, kSortThreads, 0, st>>>(ikey[1], ival[0], nullptr, ival[1], &ctr->n_items, epoch,
+            k_onesweep<8, kTileSortItems><<<rgrid, kSortThreads, 0, st>>>(ikey[1], ival[0], nullptr, ival[1], &ctr->n_items_part, epoch,
                                                            &ctr->tile_ticket[1], 8, rbase + 256,
                                                            tstat + (size_t)L.tile_parts * 256, nullptr, nullptr);
             sorted_items = ival[1];
@@ -1872,8 +1631,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         bst = blend_st;
     }
     if (ev && (e = cudaEventRecord(ev[3], bst)) != cudaSuccess) return e;
-    if (!(dbg_stages & 2)) {
-    } else if (contrib != nullptr) {  // spatial-score recording (fdgs_stv_score)
+    if (contrib != nullptr) {  // spatial-score recording (fdgs_stv_score)
         k_blend_ws<false, true><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x,
                                                                    L.width, L.height, cam.bg[0], cam.bg[1], cam.bg[2],
                                                                    out_rgb, out_T, nullptr, contrib, stv_info);
@@ -1881,17 +1639,9 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         k_blend_ws<true><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
                                                             L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T,
                                                             stats);
-    } else if (blend_sel() != 2) {  // the timed blend
-        if (blend_wl())
-            k_blend_wl<<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
-                                                          L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
-        else
-            k_blend_wi<<<L.n_tiles, kWiThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
-                                                          L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
-    } else {
-        k_blend_ws<false><<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
-                                                             L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T,
-                                                             nullptr);
+    } else {  // the timed blend
+        k_blend_wi<<<L.n_tiles, kWiThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
+                                                      L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
     }
     if (ev && (e = cudaEventRecord(ev[4], bst)) != cudaSuccess) return e;
     return cudaGetLastError();
@@ -2018,12 +1768,8 @@ cudaError_t render_graph_launch(RenderGraphImpl &g, const SceneDev &sc, const ui
         if ((e = cudaStreamWaitEvent(blend_st, split_ev, 0)) != cudaSuccess) return e;
         bst = blend_st;
     }
-    if (blend_wl())
-        k_blend_wl<<<L.n_tiles, kWsThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, cctr, L.tiles_x, L.width,
-                                                      L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
-    else
-        k_blend_wi<<<L.n_tiles, kWiThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, cctr, L.tiles_x, L.width,
-                                                      L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
+    k_blend_wi<<<L.n_tiles, kWiThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, cctr, L.tiles_x, L.width,
+                                                  L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
     return cudaGetLastError();
 }
 

@@ -132,6 +132,15 @@ __global__ void __launch_bounds__(256) k_stv_accum(SceneDev sc, float t, unsigne
     if (out_gamma) out_gamma[i] = (float)g;
 }
 
+// n_ts == 0: the sums over t are empty (score 0); gamma does not depend on t.
+__global__ void __launch_bounds__(256) k_stv_empty(SceneDev sc, const StvState *st, float *__restrict__ out_score,
+                                                   float *__restrict__ out_gamma) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= sc.n) return;
+    out_score[i] = 0.0f;
+    if (out_gamma) out_gamma[i] = (float)fmin((double)volume4(sc.ld_scale(i)) / (double)__uint_as_float(st->prefix), 1.0);
+}
+
 // m_{i,j} of P:282 read literally: bit i |= (view's weight sum of i > threshold);
 // the recorder is cleared for the next view.
 __global__ void __launch_bounds__(256) k_contrib_mask(unsigned long long *__restrict__ contrib, int n,
@@ -291,6 +300,10 @@ cudaError_t launch_stv(const SceneDev &sc, const CamDev *cams, const fdgs_camera
     for (int shift = 24; shift >= 0; shift -= 8) {
         k_vol_hist<<<hgrid, 256, 0, st>>>(sc, state, shift);
         k_vol_pick<<<1, 256, 0, st>>>(state, shift);
+    }
+    if (n_ts == 0) {
+        k_stv_empty<<<(n + 255) / 256, 256, 0, st>>>(sc, state, out_score, out_gamma);
+        return cudaGetLastError();
     }
     if ((e = cudaMemsetAsync(contrib, 0, 8 * (size_t)n, st)) != cudaSuccess) return e;
     int pw = -1, ph = -1;

@@ -467,32 +467,46 @@ def test_aabb_redundant_flag_sound():
     assert checked > 100
 
 
-def test_blend_wl_alternative_matches():
-    """FDGS_BLEND=wl / ws select k_blend_wl / k_blend_ws for the timed
-    blend (read once per process, so in a subprocess): its C2 frame must match
-    k_blend_wi's (same arithmetic, same record lists and stop decisions; only
-    k_blend_wi's paired stop test undoes a terminal step by subtraction, a
-    rounding-level difference <= 1e-6; k_blend_wi itself is parity-tested
-    against the oracle above)."""
-    import os
-    import subprocess
-    import sys
-    code = (
-        "import numpy as np, torch, fdgs_inputs as fi, paper_2503_16422_b200 as fd\n"
-        "sc = fd.Scene.from_arrays(fi.make_scene('c2')); cam = fi.make_cameras('c2')[5]\n"
-        "r = fd.Renderer(sc, cam.width, cam.height)\n"
-        "out = r.render(cam, 0.4); torch.cuda.synchronize()\n"
-        "import sys; np.save(sys.stdout.buffer, out.cpu().numpy())\n")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    imgs = []
-    for sel in ("wi", "wl", "ws"):
-        env = dict(os.environ, FDGS_BLEND=sel, PYTHONPATH=root)
-        res = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, timeout=300)
-        assert res.returncode == 0, res.stderr.decode()[-2000:]
-        import io
-        imgs.append(np.load(io.BytesIO(res.stdout)))
-    assert imgs[0].shape == (3, 800, 800)
-    assert np.abs(imgs[0] - imgs[1]).max() <= 1e-6
-    # k_blend_ws (FDGS_BLEND=ws) carries T instead of U = T/255: the same
-    # decisions except at termination knife edges, within the parity bar
-    assert np.abs(imgs[0] - imgs[2]).max() <= 2e-4
+def test_counting_blend_matches_timed_blend():
+    """The counting / recording variant k_blend_ws (fdgs_render with d_stats)
+    and the timed k_blend_wi give the same C2 frame within the parity bar: the
+    same decisions except at termination knife edges (k_blend_ws carries T,
+    k_blend_wi U = T/255 with a paired stop test); k_blend_wi itself is
+    parity-tested against the oracle above."""
+    sc = fd.Scene.from_arrays(fi.make_scene("c2"))
+    cam = fi.make_cameras("c2")[5]
+    r = fd.Renderer(sc, cam.width, cam.height)
+    a = r.render(cam, 0.4).clone()
+    st = torch.zeros(4, dtype=torch.int64, device="cuda")
+    b = r.render(cam, 0.4, stats=st)
+    torch.cuda.synchronize()
+    assert a.shape == (3, 800, 800)
+    assert (a - b).abs().max().item() <= 2e-4
+    assert int(st[2]) >= int(st[3]) > 0          # evaluated >= blended pairs
+
+
+@pytest.mark.parametrize("cap", [0, 8, 100])
+def test_overflow_writes_nothing_past_the_workspace(cap):
+    """with more row items / entries than max_entries the
+    frame must report OVERFLOW without writing past the workspace (the row
+    partition is bounded by the capacity).  A guard region after the
+    workspace must keep its pattern."""
+    import ctypes as C
+    from paper_2503_16422_b200._lib import FdgsFrameStats, lib
+    scene = fi.make_scene("c1")
+    cam = fi.make_cameras("c1")[0]
+    sc = fd.Scene.from_arrays(scene)
+    nb = lib().fdgs_render_workspace_bytes(sc.n, cam.width, cam.height, cap)
+    guard = 1 << 20
+    buf = torch.full((nb + guard,), 0xA5, dtype=torch.uint8, device="cuda")
+    buf[:nb].zero_()
+    out = torch.empty((3, cam.height, cam.width), dtype=torch.float32, device="cuda")
+    hs = FdgsFrameStats()
+    cs = fd.camera_struct(cam)
+    for t in (0.0, 0.5, 1.0):
+        st = lib().fdgs_render_checked(C.byref(sc.struct), None, None, C.byref(cs), float(np.float32(t)),
+                                       C.c_void_p(out.data_ptr()), None, C.c_void_p(buf.data_ptr()), nb, cap,
+                                       C.byref(hs), C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        assert st == _lib.FDGS_ERR_OVERFLOW
+    torch.cuda.synchronize()
+    assert bool((buf[nb:] == 0xA5).all())
