@@ -168,11 +168,21 @@ def load_traffic():
         return {}
 
 
+def oracle_masks(scene, cams):
+    """(key-frame indices, masks) from the oracle itself: the CPU
+    legs take no input from the CUDA path."""
+    import oracle
+    import fdgs_inputs as fi
+    times = fi.frame_times(N_FRAMES_T)
+    kf = oracle.keyframes(N_FRAMES_T, INTERVAL)
+    return kf, np.stack([oracle.keyframe_mask(scene, cams, times[k]) for k in kf])
+
+
 def cpu_oracle_run(scene, cams, masks, kf, frames, seconds, row_stride=8):
     """Time the oracle as it stands on bounded samples: rows j = 0 mod row_stride
-    of consecutive frames until `seconds` elapse.  Returns (frames/s, info)."""
-    import oracle
-    from paper_2503_16422_b200.api import bracket
+    of consecutive frames until `seconds` elapse.  Returns (frames/s, info).
+    masks / kf: the oracle's own (oracle_masks), None = unmasked."""
+    import oracle  # the oracle's own schedule, bracketing and mask OR (P:280-285)
     import fdgs_inputs as fi
 
     times = fi.frame_times(N_FRAMES_T)
@@ -186,8 +196,7 @@ def cpu_oracle_run(scene, cams, masks, kf, frames, seconds, row_stride=8):
         f, ti, ci = frames[k % len(frames)]
         act = None
         if masks is not None:
-            li, ri = bracket(kf, ti)
-            act = masks[li] | masks[ri]
+            act = oracle.active_mask(masks, kf, ti)
         r = oracle.render(scene, cams[ci], float(times[ti]), mask=act, pixels=pix)
         done_px += pix.size
         n_pairs += r["stats"]["evaluated"]
@@ -544,8 +553,8 @@ def run_ours(args):
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        fps, info = cpu_oracle_run(arrays, cams, masks.cpu().numpy().view(np.uint32) if MASKED else None, kf, mine,
-                                   args.cpu_seconds)
+        okf, omasks = oracle_masks(arrays, cams) if MASKED else (None, None)
+        fps, info = cpu_oracle_run(arrays, cams, omasks, okf, mine, args.cpu_seconds)
         res["cpu_baseline"] = {"value": round(fps, 5), "unit": UNIT, "cores": info["cores"], "kind": "oracle",
                                "sample": info["sample"], "ns_per_evaluated_pair": info["ns_per_evaluated_pair"],
                                "core_ns_per_evaluated_pair": info["core_ns_per_evaluated_pair"]}
@@ -569,9 +578,7 @@ def run_reference(args):
     scene = fi.make_scene(CONFIG)
     cams = fi.make_cameras(CONFIG)
     times = fi.frame_times(N_FRAMES_T)
-    from paper_2503_16422_b200.api import keyframes  # host schedule only (no CUDA)
-    kf = keyframes(N_FRAMES_T, INTERVAL)
-    masks = np.stack([oracle.keyframe_mask(scene, cams, times[k]) for k in kf])
+    kf, masks = oracle_masks(scene, cams)  # the oracle's schedule and masks (no product code on this arm)
     seq = sequence()
     per_step = max(1.0, 60.0 / max(1, args.steps + args.warmup))
     vals = []

@@ -8,10 +8,15 @@ code (see oracle/fdgs_oracle.c header).
 Parity status per function:
   rotor4, slice (Eq. 1), temporal marginal (Eq. 3), projection, SH basis,
   per-pixel compositing (Eq. 2), masks, key-frame schedule, tile lists, VQ-SH
-  lookup: pinned by tests/test_oracle_pins.py; contributions, the STV score
-  (both combine readings, all variants), paper-literal masks: pinned by
-  tests/test_oracle_stv.py.  Parity unpinned: the SH *sign convention* only, a
-  reading (R9); orthonormality and the pole case pin everything but the signs.
+  lookup: pinned by tests/test_oracle_pins.py; the off-axis projection
+  (pinhole image, Sigma_2D against a complex-step Jacobian of the world->pixel
+  map under rotated cameras with the EWA clamp exercised, conic, pixel AABB),
+  the SH basis against scipy's spherical harmonics (sign convention of R9) and
+  the view direction: tests/test_oracle_projection_pins.py; contributions, the
+  STV score (both combine readings, all variants), paper-literal masks:
+  tests/test_oracle_stv.py.  tools/mutate_oracle.py (run by
+  tests/test_oracle_mutants.py) checks that every listed mutant of the oracle
+  fails a pin.  No function is parity-unpinned.
 """
 from .oracle import (  # noqa: F401
     build_oracle,

@@ -23,8 +23,10 @@
  *     combine readings, the ablation variants).
  *   - P:483 (Ours-PP): SH read through a vector-quantised codebook.
  *
- * Parity unpinned: the SH sign convention only (R9); everything
- * else is pinned by tests/test_oracle_pins.py and tests/test_oracle_stv.py.
+ * Pinned by tests/test_oracle_pins.py, tests/test_oracle_projection_pins.py
+ * (off-axis projection, SH basis vs scipy, view direction) and
+ * tests/test_oracle_stv.py; tools/mutate_oracle.py checks every listed
+ * mutant of this file fails one of them.  No function is parity-unpinned.
  *
  * Numeric paths:
  *   - every DECISION (temporal/support/near/cover culls, pixel AABB, depth key,

@@ -44,8 +44,12 @@ def load():
     global _lib
     with _lock:
         if _lib is None:
-            build_oracle()
-            lib = C.CDLL(LIB)
+            # ORACLE_LIB: a mutated build (tools/mutate_oracle.py checks that the
+            # pins kill every mutant); default the in-tree liboracle.so
+            alt = os.environ.get("ORACLE_LIB")
+            if not alt:
+                build_oracle()
+            lib = C.CDLL(alt or LIB)
             P = C.c_void_p
             lib.or_records.argtypes = [P, P, C.c_float, P, P, P, P, P]
             lib.or_render.argtypes = [P, P, P, C.c_float, P, C.c_int64, P, P, P, P, P]

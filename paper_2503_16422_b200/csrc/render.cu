@@ -1588,7 +1588,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         uint32_t *rhist = reinterpret_cast<uint32_t *>(ws + L.row_hist);
         uint64_t *tstat = reinterpret_cast<uint64_t *>(ws + L.tile_status);
         BandConsts *bconst = reinterpret_cast<BandConsts *>(ws + L.band_consts);
-        const uint32_t item_chunks = (uint32_t)((L.max_entries + kItemTile - 1) / kItemTile);
+        const uint32_t item_chunks = (uint32_t)std::max<int64_t>(1, (L.max_entries + kItemTile - 1) / kItemTile);
         {
             uint32_t *pcnt = reinterpret_cast<uint32_t *>(ws + L.bin_cnt);  // items per k_bin_count partition
             const int bparts = std::max(1, (L.n + kScanNT - 1) / kScanNT);
