@@ -88,6 +88,13 @@ def parse():
                    help="render the full scene under the masks instead of the window's compacted working set")
     p.add_argument("--vq", type=int, default=0, metavar="K",
                    help="Ours-PP storage: SH vector-quantised to a K-entry codebook (P:483), 0 = dense SH")
+    p.add_argument("--gather-chunk", type=int, default=10,
+                   help="N > 1: frames per grouped send/recv of the frame gather to rank 0")
+    p.add_argument("--no-gather", action="store_true", help="N > 1: do not gather the frames to rank 0")
+    p.add_argument("--cpu-single-core", action="store_true",
+                   help="also time the oracle on one host core (cpu_baseline.single_core)")
+    p.add_argument("--fake-render", action="store_true", help=argparse.SUPPRESS)  # CPU orchestration test (gloo)
+    p.add_argument("--fake-n", type=int, default=300, help=argparse.SUPPRESS)
     return p.parse_args()
 
 
@@ -178,7 +185,7 @@ def oracle_masks(scene, cams):
     return kf, np.stack([oracle.keyframe_mask(scene, cams, times[k]) for k in kf])
 
 
-def cpu_oracle_run(scene, cams, masks, kf, frames, seconds, row_stride=8):
+def cpu_oracle_run(scene, cams, masks, kf, frames, seconds, row_stride=8, threads=None):
     """Time the oracle as it stands on bounded samples: rows j = 0 mod row_stride
     of consecutive frames until `seconds` elapse.  Returns (frames/s, info).
     masks / kf: the oracle's own (oracle_masks), None = unmasked."""
@@ -191,6 +198,9 @@ def cpu_oracle_run(scene, cams, masks, kf, frames, seconds, row_stride=8):
     pix = (rows[:, None] * W + np.arange(W)[None, :]).ravel()
     done_px, k, n_pairs, t0 = 0, 0, 0, time.perf_counter()
     oracle.load()
+    prev = oracle.num_threads()
+    if threads:
+        oracle.set_num_threads(threads)
     t0 = time.perf_counter()
     while True:
         f, ti, ci = frames[k % len(frames)]
@@ -206,6 +216,8 @@ def cpu_oracle_run(scene, cams, masks, kf, frames, seconds, row_stride=8):
             break
     fps = done_px / (W * H) / el
     cores = oracle.num_threads()
+    if threads:
+        oracle.set_num_threads(prev)
     return fps, dict(cores=cores, frames=k, seconds=round(el, 2),
                      ns_per_evaluated_pair=round(el * 1e9 / max(n_pairs, 1), 3),
                      core_ns_per_evaluated_pair=round(el * 1e9 * cores / max(n_pairs, 1), 2),
@@ -215,30 +227,54 @@ def cpu_oracle_run(scene, cams, masks, kf, frames, seconds, row_stride=8):
 
 
 # ----------------------------------------------------------------- ours
+class _FakePipeline:
+    """--fake-render: the orchestration of run_ours on CPU ranks (gloo) with a
+    deterministic stand-in for the CUDA render, so that the multi-rank logic
+    bench.py runs (partition, broadcast, mask sharing, frame gather, timing
+    reduction) is tested without a GPU (tests/test_dist_gloo.py).  Frame f's
+    image is filled with the value f."""
+
+    def __init__(self, shape):
+        self.shape = shape
+
+    def render_many(self, frames, outs, stream=None, frame_done=None, **_):
+        for k, x in enumerate(frames):
+            outs[k].fill_(float(x[0]))
+            if frame_done is not None:
+                frame_done(k, outs[k], None)
+
+
+def _fake_mask(k, words):
+    rng = np.random.default_rng(1000 + k)
+    return rng.integers(0, 2 ** 32, words, dtype=np.uint64).astype(np.uint32).view(np.int32)
+
+
 def run_ours(args):
     import torch
-    import torch.distributed as dist
 
     import fdgs_inputs as fi
-    import paper_2503_16422_b200 as fd
+    from paper_2503_16422_b200 import dist as fdist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import paper_2503_16422_b200 as fd  # (the library itself loads on first use: not in --fake-render)
+
+    fake = args.fake_render
+    rank, world, local = fdist.env_ranks()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if fake:
+        dev = torch.device("cpu")
+    else:
+        torch.cuda.set_device(local)
+        dev = torch.device("cuda", local)
+    fdist.init("gloo" if fake else "nccl", dev)
 
-    # ---- scene: rank 0 draws it, NCCL broadcast to the others
+    # ---- scene: rank 0 draws it, broadcast to the others (NCCL over NVLink)
     cfg = fi.CONFIGS[CONFIG]
-    n = cfg["n"]
+    n = args.fake_n if fake else cfg["n"]
     shapes = {"mean": (n, 4), "scale": (n, 4), "rot_l": (n, 4), "rot_r": (n, 4), "opacity": (n,),
               "log255_opacity": (n,), "sh": (args.vq, 16, 3) if args.vq else (n, 16, 3)}
     if rank == 0:
-        arrays = fi.make_scene(CONFIG)
+        arrays = fi.make_scene(CONFIG, n=n)
         if args.vq:
             arrays = fi.vq_scene(arrays, codebook_size=args.vq, seed=1)
         tens = {k: torch.from_numpy(v).to(dev) for k, v in arrays.arrays().items()}
@@ -247,48 +283,60 @@ def run_ours(args):
         tens = {k: torch.empty(s, dtype=torch.float32, device=dev) for k, s in shapes.items()}
         if args.vq:
             tens["sh_index"] = torch.empty(n, dtype=torch.uint16, device=dev)
-    if world > 1:
-        for k in shapes:
-            dist.broadcast(tens[k], src=0)
-        if args.vq:  # NCCL has no uint16: broadcast the bytes
-            dist.broadcast(tens["sh_index"].view(torch.uint8), src=0)
-    scene = fd.Scene(tens, device=dev)
+    fdist.broadcast_scene(tens)
+    scene_ok = True
+    if fake:  # every rank holds rank 0's scene (checked against the generator)
+        ref = fi.make_scene(CONFIG, n=n).arrays()
+        scene_ok = all(np.array_equal(tens[k].numpy(), ref[k]) for k in ref)
+    scene = None if fake else fd.Scene(tens, device=dev)
     cams = fi.make_cameras(CONFIG)
-    cam_structs = [fd.camera_struct(c) for c in cams]
+    W, H = (8, 6) if fake else (cams[0].width, cams[0].height)
+    cam_structs = None if fake else [fd.camera_struct(c) for c in cams]
     times = fi.frame_times(N_FRAMES_T)
     kf = fd.keyframes(N_FRAMES_T, INTERVAL)
+    bracket = fd.bracket
     # ---- key-frame masks: key-frame k built by rank k mod N, all-reduced (disjoint rows)
-    words = fd.mask_words(n)
-    masks = torch.zeros((len(kf), words), dtype=torch.int32, device=dev)
+    words = (n + 31) // 32
+
+    def build(k, out):
+        if fake:
+            out.copy_(torch.from_numpy(_fake_mask(k, words)))
+        elif args.literal_masks:  # P:282 read literally (R3b): blending weight > 0 in some view
+            out.copy_(fd.keyframe_mask_contrib(scene, cams, float(times[kf[k]]), 0.0))
+        else:
+            fd.keyframe_mask(scene, cams, float(times[kf[k]]), out=out)
+
     t_mask0 = time.perf_counter()
-    for k in range(len(kf)):
-        if k % world == rank:
-            if args.literal_masks:  # P:282 read literally (R3b): blending weight > 0 in some view
-                masks[k].copy_(fd.keyframe_mask_contrib(scene, cams, float(times[kf[k]]), 0.0))
-            else:
-                fd.keyframe_mask(scene, cams, float(times[kf[k]]), out=masks[k])
-    if world > 1:
-        dist.all_reduce(masks, op=dist.ReduceOp.SUM)
-    torch.cuda.synchronize()
+    masks = fdist.share_keyframe_masks(len(kf), words, build, dev)
+    if not fake:
+        torch.cuda.synchronize()
     mask_build_s = time.perf_counter() - t_mask0
+    masks_ok = (not fake) or all(np.array_equal(masks[k].numpy(), _fake_mask(k, words)) for k in range(len(kf)))
 
     seq = sequence()
-    mine = [x for x in seq if x[0] % world == rank]
+    mine = fdist.shard_frames(seq, rank, world)
     F = args.frames_per_step
-    pipe = fd.RenderPipeline(scene, cams[0].width, cams[0].height, depth=args.streams, split=not args.no_split,
-                             graphs=args.graphs)
-    renderer = pipe.renderers[0]
-    outs = [renderer.new_output() for _ in range(F)]
-    stats = torch.zeros((F, 4), dtype=torch.int64, device=dev)  # fdgs_frame_stats is 32 bytes
-    flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device=dev)  # 512 MiB > L2
-    stream = torch.cuda.current_stream()
-    use_ev = not args.no_stage_events and not args.graphs  # graph frames record no stage events
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(F)]
-    for row in evs:
-        for e in row:
-            e.record(stream)  # materialise the CUDA events
-    torch.cuda.synchronize()
-
+    if fake:
+        pipe = _FakePipeline((3, H, W))
+        outs = [torch.empty((3, H, W), dtype=torch.float32) for _ in range(F)]
+        stream = None
+    else:
+        pipe = fd.RenderPipeline(scene, W, H, depth=args.streams, split=not args.no_split, graphs=args.graphs)
+        renderer = pipe.renderers[0]
+        outs = [renderer.new_output() for _ in range(F)]
+        stats = torch.zeros((F, 4), dtype=torch.int64, device=dev)  # fdgs_frame_stats is 32 bytes
+        flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device=dev)  # 512 MiB > L2
+        stream = torch.cuda.current_stream()
+    gather = None
+    if world > 1 and not args.no_gather:
+        gather = fdist.FrameGather((3, H, W), args.gather_chunk, dev)
+    use_ev = not fake and not args.no_stage_events and not args.graphs  # graph frames record no stage events
+    if use_ev:
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(F)]
+        for row in evs:
+            for e in row:
+                e.record(stream)  # materialise the CUDA events
+        torch.cuda.synchronize()
 
     # key-frame windows as compacted working sets (Scene.compact): built the
     # first time a window is rendered (inside that step's timed region), kept
@@ -298,10 +346,12 @@ def run_ours(args):
     timing_now = [False]
 
     def frame_args(x):
+        if fake:
+            return x
         f, ti, ci = x
         if not MASKED:
             return cam_structs[ci], float(times[ti]), None, None
-        li, ri = fd.bracket(kf, ti)
+        li, ri = bracket(kf, ti)
         if not args.working_set:
             return cam_structs[ci], float(times[ti]), masks[li], masks[ri]
         if (li, ri) not in wsets:
@@ -311,19 +361,33 @@ def run_ours(args):
             compacts.append(timing_now[0])
         return cam_structs[ci], float(times[ti]), None, None, wsets[(li, ri)]
 
+    host_ms = []  # host enqueue time of each step (render_many returning)
+
     def run_step(step_frames, timed, count=False):
-        flush.zero_()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        start = torch.cuda.Event(enable_timing=True)
-        end = torch.cuda.Event(enable_timing=True)
-        start.record(stream)
+        """One step: this rank's next F frames (and, N > 1, their gather to
+        rank 0), bracketed by a barrier and device events on both sides."""
+        if not fake:
+            flush.zero_()
+            torch.cuda.synchronize()
+        fdist.barrier()
+        if fake:
+            t0 = time.perf_counter()
+        else:
+            start = torch.cuda.Event(enable_timing=True)
+            end = torch.cuda.Event(enable_timing=True)
+            start.record(stream)
         h0 = time.perf_counter()
-        pipe.render_many([frame_args(x) for x in step_frames], outs[:len(step_frames)],
-                         stats=stats if count else None,
-                         stage_events=evs if (use_ev and timed) else None, stream=stream)
+        g = gather if (gather is not None and not count) else None
+        if g is not None:
+            g.begin_step(len(step_frames))
+        kw = {} if fake else dict(stats=stats if count else None, stage_events=evs if (use_ev and timed) else None)
+        pipe.render_many([frame_args(x) for x in step_frames], outs[:len(step_frames)], stream=stream,
+                         frame_done=g.frame_done if g is not None else None, **kw)
+        if g is not None:
+            g.end_step(stream)
         host_ms.append((time.perf_counter() - h0) * 1e3)
+        if fake:
+            return (time.perf_counter() - t0) * 1e3, None
         end.record(stream)
         end.synchronize()
         ms = start.elapsed_time(end)
@@ -346,7 +410,6 @@ def run_ours(args):
         return ms, stage
 
     ptr = 0
-    host_ms = []  # host enqueue time of each step (render_many returning)
 
     def next_frames():
         nonlocal ptr
@@ -356,12 +419,11 @@ def run_ours(args):
 
     for _ in range(args.warmup):
         run_step(next_frames(), False)
-    sampler = ClockSampler(local)
-    sampler.start()
+    sampler = ClockSampler(local) if not fake else None
+    if sampler:
+        sampler.start()
     step_ms, stage_ms = [], np.zeros(4)
     h_first = len(host_ms)
-    n_eval = n_blend = 0
-    n_vis_tot = n_ent_tot = n_act_tot = 0
     timed_frames = []
     timing_now[0] = True
     # no cyclic-GC pauses while steps are enqueued (a pause longer than the
@@ -375,36 +437,20 @@ def run_ours(args):
         step_ms.append(ms)
         if stg is not None:
             stage_ms += stg
-    clocks = sampler.stop()
+    clocks = sampler.stop() if sampler else None
     gc.enable()
     timing_now[0] = False
     # k_mask_compact + k_scene_gather per working set built inside the timed steps
     compact_launches = 2 * sum(1 for x in compacts if x)
     host_timed = host_ms[h_first:h_first + args.steps]
-    # work counters of the same frames (counting blend variant, not timed)
-    for fr in timed_frames:
-        run_step(fr, False, count=True)
-        s = stats.cpu().numpy()
-        lo = np.ascontiguousarray(s[:, 0]).view(np.uint32).reshape(F, 2)
-        hi = np.ascontiguousarray(s[:, 1]).view(np.uint32).reshape(F, 2)
-        n_act_tot += int(lo[:, 0].sum())
-        n_vis_tot += int(lo[:, 1].sum())
-        n_ent_tot += int(hi[:, 0].sum())
-        assert np.all(hi[:, 1] == 0), "a frame overflowed its entry capacity"
-        n_eval += int(s[:, 2].sum())
-        n_blend += int(s[:, 3].sum())
-    total_ms = float(sum(step_ms))
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    # the job time is the slowest rank's device time (max over ranks), per step too
+    per_rank = fdist.gather_timings(step_ms, dev)
+    total_ms = max(sum(r) for r in per_rank)
+    step_max = [max(r[k] for r in per_rank) for k in range(args.steps)]
     frames_total = world * args.steps * F
     value = frames_total / (total_ms / 1e3)
     frames_rank = args.steps * F
-
-    # ---- roofline of the dominant stage
-    peaks, peak_src = load_peaks()
-    stage_names = ["preprocess", "depth_sort", "binning", "blend"]
+    med = statistics.median(step_max)
     res = dict(metric=METRIC, value=round(value, 2), unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
                ms_per_step=round(total_ms / args.steps, 4), higher_is_better=True, scaling="weak", vs_baseline=None,
                dtype="f32 (decision path f64)", data="synthetic",
@@ -421,19 +467,85 @@ def run_ours(args):
                        "filter": ("compacted working set per key-frame window (Scene.compact, built inside the timed "
                                   "region when the sequence enters the window)") if MASKED and args.working_set
                        else ("masks OR-ed per frame" if MASKED else "none")},
-               gpu_launches=KERNELS_PER_FRAME * frames_rank + compact_launches)
+               step_stats={"median_frames_per_s": round(world * F / (med / 1e3), 2),
+                           "min_ms": round(min(step_max), 4), "median_ms": round(med, 4),
+                           "max_ms": round(max(step_max), 4),
+                           "note": "per-step max-over-ranks device time; value = all frames / sum of per-rank totals "
+                                   "(max over ranks)"})
+    if not fake:
+        res["gpu_launches"] = KERNELS_PER_FRAME * frames_rank + compact_launches
+    if gather is not None:
+        chk = gather.validate(outs[:F])  # one more gather of the last step's frames, checksums compared on rank 0
+        g = {"chunk_frames": gather.chunk, "bytes_per_frame": gather.frame_bytes,
+             "bytes_into_rank0_per_step": (world - 1) * F * gather.frame_bytes,
+             "in_timed_region": True,
+             "how": "grouped P2P send/recv (torch.distributed batch_isend_irecv: NCCL over NVLink) on a side stream "
+                    "per chunk as soon as its frames' blends finish; each step's end waits for its transfers",
+             "validated_frames": chk.get("frames"), "validated_ok": chk.get("ok")}
+        if fake and rank == 0:
+            # the last validated chunk holds, for every sender r, the fake frames of r's last step
+            slot, cnt = gather.last
+            c0 = ((F - 1) // gather.chunk) * gather.chunk
+            ok = True
+            for r in range(1, world):
+                theirs = fdist.shard_frames(seq, r, world)
+                base = (args.warmup + args.steps - 1) * F
+                for gi in range(cnt):
+                    f = theirs[(base + c0 + gi) % len(theirs)][0]
+                    ok &= bool(torch.all(gather.ring[slot, r - 1, gi] == float(f)))
+            g["fake_content_ok"] = ok
+        res["gather"] = g
+    if fake:
+        res["fake_render"] = {"scene_broadcast_ok": scene_ok, "masks_ok": masks_ok,
+                              "frames_rank0": [x[0] for x in mine[:4]],
+                              "per_rank_total_ms": [round(sum(r), 4) for r in per_rank]}
+        fdist.shutdown()
+        if rank == 0:
+            print(json.dumps(res), flush=True)
+        return
+
+    n_eval = n_blend = 0
+    n_vis_tot = n_ent_tot = n_act_tot = 0
+    # work counters of the same frames (counting blend variant, not timed)
+    for fr in timed_frames:
+        run_step(fr, False, count=True)
+        s = stats.cpu().numpy()
+        lo = np.ascontiguousarray(s[:, 0]).view(np.uint32).reshape(F, 2)
+        hi = np.ascontiguousarray(s[:, 1]).view(np.uint32).reshape(F, 2)
+        n_act_tot += int(lo[:, 0].sum())
+        n_vis_tot += int(lo[:, 1].sum())
+        n_ent_tot += int(hi[:, 0].sum())
+        assert np.all(hi[:, 1] == 0), "a frame overflowed its entry capacity"
+        n_eval += int(s[:, 2].sum())
+        n_blend += int(s[:, 3].sum())
+
+    # ---- roofline of the dominant stage
+    peaks, peak_src = load_peaks()
+    stage_names = ["preprocess", "depth_sort", "binning", "blend"]
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    lane_peak = 148 * 128 * sm_mhz * 1e6  # FP32 lane-ops/s
+
+    def blend_rl(ms_total, frames):
+        """SURVEY §8(d) lane-op model: 8 FP32 lane-ops per evaluated pair + 9 per
+        blended pair, over 148 SMs x 128 lanes x clock; the flop model beside it."""
+        ops = (8.0 * n_eval + 9.0 * n_blend) * frames / max(frames_rank, 1)
+        ach = ops / (ms_total / 1e3)
+        fl = (10.0 * n_eval + 12.0 * n_blend) * frames / max(frames_rank, 1) / (ms_total / 1e3) / 1e12
+        return ach, fl
+
     if use_ev and stage_ms.sum() > 0:
         per_frame = stage_ms / frames_rank
         dom = int(np.argmax(stage_ms))
-        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
         if dom == 3:
-            flops = 10.0 * n_eval + 12.0 * n_blend
-            achieved = flops / (stage_ms[3] / 1e3) / 1e12
-            peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
-            rl = {"kernel": BLEND_KERNEL, "bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2),
-                  "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                  "peak_src": f"148 SMs x 128 FP32 lanes x 2 (FMA) x {sm_mhz:.0f} MHz (sm_max from {peak_src} peaks)",
-                  "work": "10 flops per evaluated (pixel,Gaussian) pair + 12 per blended pair (DESIGN.md)"}
+            ach, fl = blend_rl(stage_ms[3], frames_rank)
+            rl = {"kernel": BLEND_KERNEL, "bound": "alu", "achieved": round(ach / 1e12, 3),
+                  "peak": round(lane_peak / 1e12, 3), "unit": "T lane-ops/s", "frac": round(ach / lane_peak, 4),
+                  "peak_src": f"148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (sm_max, {peak_src} peaks)",
+                  "work": "SURVEY 8(d): 8 FP32 lane-ops per evaluated (pixel, Gaussian) pair + 9 per blended pair; "
+                          "pairs from the counting blend on the same frames",
+                  "flop_model": {"achieved_tflops": round(fl, 3), "peak_tflops": round(2 * lane_peak / 1e12, 2),
+                                 "frac": round(fl * 1e12 / (2 * lane_peak), 4),
+                                 "work": "10 flops per evaluated + 12 per blended pair, FMA = 2"}}
         else:
             hbm = float(peaks.get("hbm_gbs", 6650.0))
             nb = {0: 68.0 * n_act_tot + 192.0 * n_vis_tot + 68.0 * n_vis_tot,
@@ -443,9 +555,9 @@ def run_ours(args):
                   "unit": "GB/s", "frac": round(achieved / hbm, 4), "peak_src": peak_src}
         trj = load_traffic()
         rl["traffic"] = trj.get(rl["kernel"])
-        if trj.get(rl["kernel"] + "_issue_slots_busy") is not None:
-            # the blend is issue-bound: the share of issue slots it uses (ncu, profiles/)
-            rl["ncu_issue_slots_busy"] = trj[rl["kernel"] + "_issue_slots_busy"]
+        for key in ("issue_slots_busy", "pipes"):
+            if trj.get(rl["kernel"] + "_" + key) is not None:
+                rl["ncu_" + key] = trj[rl["kernel"] + "_" + key]
         res["roofline"] = rl
         res["stages"] = {nm: {"ms_per_frame": round(float(per_frame[i]), 4),
                               "share": round(float(stage_ms[i] / sum(step_ms)), 4)} for i, nm in enumerate(stage_names)}
@@ -456,7 +568,7 @@ def run_ours(args):
     # isolated (one stream, nothing overlapping) per-stage times of one extra step
     # of the same frames, outside the timed region: the blend's own throughput
     if use_ev and stage_ms.sum() > 0 and "roofline" in res:
-        iso = fd.RenderPipeline(scene, cams[0].width, cams[0].height, depth=1, split=False)
+        iso = fd.RenderPipeline(scene, W, H, depth=1, split=False)
         iso.renderers[0] = renderer
         fr = timed_frames[0]
         flush.zero_()
@@ -465,9 +577,9 @@ def run_ours(args):
         torch.cuda.synchronize()
         iso_ms = np.array([sum(evs[k][s_].elapsed_time(evs[k][s_ + 1]) for k in range(len(fr))) for s_ in range(4)])
         if res["roofline"]["kernel"] == BLEND_KERNEL:
-            fl = (10.0 * n_eval + 12.0 * n_blend) / len(timed_frames)
-            ach = fl / (iso_ms[3] / 1e3) / 1e12
-            res["roofline"]["isolated"] = {"achieved": round(ach, 3), "frac": round(ach / res["roofline"]["peak"], 4),
+            # the counters cover all timed frames, this pass the first step's
+            ach, fl = blend_rl(iso_ms[3] * len(timed_frames), frames_rank)
+            res["roofline"]["isolated"] = {"achieved": round(ach / 1e12, 3), "frac": round(ach / lane_peak, 4),
                                            "ms_per_frame": round(float(iso_ms[3] / len(fr)), 4),
                                            "note": "same frames on one stream, no overlap (outside the timed region)"}
         res["stages_isolated_ms_per_frame"] = {nm: round(float(iso_ms[i] / len(fr)), 4)
@@ -478,7 +590,7 @@ def run_ours(args):
     # whole-frame HBM model of SURVEY.md §8(d) d.4 (BASELINE "% HBM roofline"): algorithmic
     # bytes per frame from the device counters, over the frame time, against the measured copy peak
     na, nv, ne = n_act_tot / frames_rank, n_vis_tot / frames_rank, n_ent_tot / frames_rank
-    px = cams[0].width * cams[0].height
+    px = W * H
     mask_terms = (8.0 * ((n + 31) // 32) + 8.0 * na) if MASKED else 0.0
     bpf = mask_terms + 68.0 * na + (192.0 + 96.0 + 72.0) * nv + (8.0 + 32.0 + 52.0) * ne + 12.0 * px
     hbm = float(load_peaks()[0].get("hbm_gbs", 6650.0))
@@ -487,6 +599,9 @@ def run_ours(args):
                         "unit": "GB/s", "frac": round(achieved_gbs / hbm, 4),
                         "model": "SURVEY.md 8(d) d.4: mask words + index + 68 B/active + (192+96+72) B/visible + "
                                  "(8+32+52) B/entry + 12 B/pixel, per GPU"}
+    dram = load_traffic().get("frame_dram_bytes")
+    if dram is not None:
+        res["frame_hbm"]["ncu_dram_bytes_per_frame"] = dram
     res["clocks"] = clocks
     # host time to enqueue a step (render_many returning) vs the step's device
     # time: the pipeline is host-bound if the ratio approaches 1
@@ -498,29 +613,27 @@ def run_ours(args):
 
     # ---- e2e through the public API with host buffers
     if not args.no_e2e:
-        import torch as _t
         host_masks = masks.cpu().pin_memory()
-        dev_masks = _t.empty_like(masks)
-        host_out = _t.empty((F, 3, cams[0].height, cams[0].width), dtype=_t.float32).pin_memory()
+        dev_masks = torch.empty_like(masks)
+        host_out = torch.empty((F, 3, H, W), dtype=torch.float32).pin_memory()
         e2e_ms = []
         h2d_bytes = d2h_bytes = 0
         e2e_sets = {}
         for it in range(args.warmup + max(1, args.steps // 2)):
             fr = next_frames()
-            need = sorted({i for x in fr for i in fd.bracket(kf, x[1])}) if MASKED else []
+            need = sorted({i for x in fr for i in bracket(kf, x[1])}) if MASKED else []
             flush.zero_()
-            _t.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
-            a = _t.cuda.Event(enable_timing=True)
-            b = _t.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            fdist.barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
             for i in need:
                 dev_masks[i].copy_(host_masks[i], non_blocking=True)
             jobs = []
             for k, x in enumerate(fr):
                 f, ti, ci = x
-                li, ri = fd.bracket(kf, ti)
+                li, ri = bracket(kf, ti)
                 if MASKED and args.working_set:
                     # a window's working set is built (from the masks copied H2D) when the
                     # sequence enters it, as in the device-timed loop
@@ -533,23 +646,27 @@ def run_ours(args):
                     jobs.append((cam_structs[ci], float(times[ti]), dev_masks[li] if MASKED else None,
                                  dev_masks[ri] if MASKED else None))
             # each frame goes D2H on the pipeline's copy stream as soon as its blend is done
-            pipe.render_many(jobs, outs[:len(fr)], stream=stream, host_outs=host_out)
+            # (and, N > 1, to rank 0 over NVLink as in the device-timed loop)
+            if gather is not None:
+                gather.begin_step(len(fr))
+            pipe.render_many(jobs, outs[:len(fr)], stream=stream, host_outs=host_out,
+                             frame_done=gather.frame_done if gather is not None else None)
+            if gather is not None:
+                gather.end_step(stream)
             b.record(stream)
             b.synchronize()
             if it >= args.warmup:
                 e2e_ms.append(a.elapsed_time(b))
                 h2d_bytes = len(need) * words * 4
-                d2h_bytes = F * 3 * cams[0].height * cams[0].width * 4
-        tot = float(sum(e2e_ms))
-        if world > 1:
-            t = _t.tensor([tot], dtype=_t.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            tot = float(t.item())
+                d2h_bytes = F * 3 * H * W * 4
+        tot = fdist.max_over_ranks(float(sum(e2e_ms)), dev)
         res["e2e"] = {"value": round(world * len(e2e_ms) * F / (tot / 1e3), 2), "unit": UNIT,
                       "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
                       "path": "RenderPipeline.render_many (fdgs_render_split) with the step's key-frame masks H2D "
                               "from pinned host and every frame D2H to pinned host (copy stream, overlapping later "
-                              "frames) inside the timed region"}
+                              "frames) inside the timed region" +
+                              ("; N > 1: every rank copies its own frames D2H and gathers them to rank 0 over "
+                               "NVLink (FrameGather)" if gather is not None else "")}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -558,9 +675,12 @@ def run_ours(args):
         res["cpu_baseline"] = {"value": round(fps, 5), "unit": UNIT, "cores": info["cores"], "kind": "oracle",
                                "sample": info["sample"], "ns_per_evaluated_pair": info["ns_per_evaluated_pair"],
                                "core_ns_per_evaluated_pair": info["core_ns_per_evaluated_pair"]}
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+        if args.cpu_single_core:
+            fps1, info1 = cpu_oracle_run(arrays, cams, omasks, okf, mine, args.cpu_seconds, row_stride=64,
+                                         threads=1)
+            res["cpu_baseline"]["single_core"] = {"value": round(fps1, 6), "cores": 1, "sample": info1["sample"],
+                                                  "ns_per_evaluated_pair": info1["ns_per_evaluated_pair"]}
+    fdist.shutdown()
     if rank == 0:
         print(json.dumps(res), flush=True)
 
@@ -602,6 +722,10 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-run this command under torch.distributed.run
+        from paper_2503_16422_b200.dist import launch_self
+        launch_self(args.gpus)
     apply_config(args)
     if args.impl == "reference":
         run_reference(args)

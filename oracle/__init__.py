@@ -39,6 +39,7 @@ from .oracle import (  # noqa: F401
     rotor4,
     sh_basis,
     num_threads,
+    set_num_threads,
     MAX_LEAVES,
     ST_TEMPORAL, ST_SUPPORT, ST_NEAR, ST_COVER, ST_VISIBLE,
 )

@@ -932,6 +932,15 @@ int or_stv_score(const or_scene *S, const or_camera *cams, int32_t n_cams, const
     return 0;
 }
 
+void or_set_num_threads(int n)
+{
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 int or_num_threads(void)
 {
 #ifdef _OPENMP

@@ -71,6 +71,7 @@ def load():
             lib.or_band_tiles.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, P, P]
             lib.or_band_tiles.restype = C.c_int
             lib.or_num_threads.restype = C.c_int
+            lib.or_set_num_threads.argtypes = [C.c_int]
             lib.or_contrib.argtypes = [P, P, C.c_float, P]
             lib.or_stv_score.argtypes = [P, P, C.c_int32, P, C.c_int32, C.c_double, P, P, P, P, C.c_int, C.c_int]
             lib.or_tv_p1.argtypes = [C.c_double, C.c_double, C.c_double]
@@ -310,3 +311,8 @@ def tv_value(t, mu_t, sigma_t, order=2):
 
 def num_threads():
     return int(load().or_num_threads())
+
+
+def set_num_threads(n):
+    """OpenMP threads of the oracle (bench.py's single-core baseline)."""
+    load().or_set_num_threads(int(n))

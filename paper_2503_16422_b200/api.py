@@ -406,7 +406,7 @@ class RenderPipeline:
         return st
 
     def render_many(self, frames, outs, stats=None, stage_events=None, stream=None, host_outs=None,
-                    status_out=None):
+                    status_out=None, frame_done=None):
         """frames: list of (cam, t, mask_l, mask_r); outs: list of output tensors.
         host_outs (optional): pinned host tensors; frame k is copied D2H on a
         copy stream as soon as its blend finishes, overlapping the rendering of
@@ -415,7 +415,10 @@ class RenderPipeline:
         its blend; status != 0 means the frame overflowed its tile-entry
         capacity and is undefined -- see render_many_checked).  Ordered after
         the current work of `stream` (default: current stream), and `stream`
-        waits for every frame (and copy) before continuing.  Async."""
+        waits for every frame (and copy) before continuing.  frame_done
+        (optional): called as frame_done(k, outs[k], s) right after frame k is
+        enqueued, s the stream on which it completes (dist.FrameGather hooks
+        the multi-GPU frame gather here).  Async."""
         main = stream or torch.cuda.current_stream()
         start = self.start_ev
         start.record(main)
@@ -454,6 +457,8 @@ class RenderPipeline:
             if status_out is not None:  # counters of this frame, before the workspace is reused
                 with torch.cuda.stream(last):
                     status_out[k].copy_(self.counters_view(i), non_blocking=True)
+            if frame_done is not None:
+                frame_done(k, outs[k], last)
             if host_outs is not None:
                 fin = self.fin_ev[i]
                 fin.record(last)
