@@ -107,7 +107,6 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.band_consts = take(sizeof(BandConsts) * nn);          // tile-cover constants per Gaussian
     L.item_pack = take(4 * cap);                            // (ty, txa, txb) per row item
     L.item_v = take(4 * cap);                               // visible slot per row item
-    L.item_spans = take(8 * cap);                           // reached rows of the item's first 8 tiles
     L.ekey0 = take(4 * cap);
     L.ekey1 = take(4 * cap);
     L.eval0 = take(4 * cap);

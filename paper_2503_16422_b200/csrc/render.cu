@@ -613,70 +613,6 @@ __global__ void __launch_bounds__(kScanNT) k_bin_offsets(const uint2 *__restrict
     }
 }
 
-// Rows of tile (tx, ty) that a splat's ellipse reaches (pure culling for the
-// blend, DESIGN.md "Row spans"): the y-extent of the margin-inflated ellipse
-// {A'dx^2 + B'dx dy + C'dy^2 + Q2 + m >= 0} within the tile's pixel-centre
-// columns ∩ AABB, as the tile's pixel rows ∩ AABB.  The ellipse is convex, so
-// the rows whose chord meets the column strip form one interval: its top is
-// the ellipse's topmost point if that lies in the strip, else the larger root
-// at the strip edge nearest to it (the bottom likewise).  binary32, widened
-// well beyond its rounding; m (2^-11 of the quadratic's magnitude over the
-// AABB + 2^-9) covers the rounding of the pinned fp32 e2 chain, so every pixel
-// of the tile with e2 >= 0 lies in a listed row (brute-force soundness tests:
-// tests/test_gpu_render.py).  Span byte: lo | hi << 4 (tile-relative rows),
-// lo > hi when no row is reached.
-constexpr uint32_t kSpanEmpty = 0x0Fu;  // lo = 15 > hi = 0
-struct SpanConsts {
-    float u, v, Ap, Bp, Cp, Qm, dym, dxt;
-    int px0, px1, py0, py1;
-    bool full;  // (near-)degenerate conic: every row of the tile ∩ AABB
-};
-__device__ __forceinline__ SpanConsts span_consts(const float4 &a, const float4 &b, int px0, int px1, int py0,
-                                                  int py1) {
-    SpanConsts c;
-    c.u = a.x, c.v = a.y, c.Ap = a.z, c.Bp = a.w, c.Cp = b.x;
-    c.px0 = px0, c.px1 = px1, c.py0 = py0, c.py1 = py1;
-    const float X = fmaxf(fabsf(((float)px0 + 0.5f) - c.u), fabsf(((float)px1 + 0.5f) - c.u));
-    const float Y = fmaxf(fabsf(((float)py0 + 0.5f) - c.v), fabsf(((float)py1 + 0.5f) - c.v));
-    const float mag = fabsf(c.Ap) * X * X + fabsf(c.Bp) * X * Y + fabsf(c.Cp) * Y * Y;
-    c.Qm = b.y + fmaf(mag, 0x1p-11f, 0x1p-9f);
-    const float K = 4.0f * c.Ap * c.Cp - c.Bp * c.Bp;
-    c.full = !(K > 1e-4f * 4.0f * c.Ap * c.Cp) || !(c.Ap < 0.0f) || !(c.Cp < 0.0f);
-    c.dym = c.full ? 0.0f : sqrtf(-4.0f * c.Ap * c.Qm / K);  // half height of the inflated ellipse
-    c.dxt = c.full ? 0.0f : -c.Bp * c.dym / (2.0f * c.Ap);   // x of its topmost point (the bottom: -dxt)
-    return c;
-}
-__device__ __forceinline__ uint32_t tile_row_span(const SpanConsts &c, int tx, int ty) {
-    const int xa = max(16 * tx, c.px0), xb = min(16 * tx + 15, c.px1);
-    const int ya = max(16 * ty, c.py0), yb = min(16 * ty + 15, c.py1);
-    if (xa > xb || ya > yb) return kSpanEmpty;
-    const int r_a = ya - 16 * ty, r_b = yb - 16 * ty;
-    if (c.full) return (uint32_t)r_a | ((uint32_t)r_b << 4);
-    const float dxa = ((float)xa + 0.5f) - c.u, dxb = ((float)xb + 0.5f) - c.u;
-    // y-roots of the ellipse on the vertical line dx = x: C'y^2 + (B'x) y + (A'x^2 + Qm) = 0 (C' < 0)
-    bool hit = true;
-    auto root = [&](float x, bool upper) {
-        const float b = c.Bp * x, cc = fmaf(c.Ap * x, x, c.Qm);
-        const float scale = b * b + 4.0f * fabsf(c.Cp) * (fabsf(c.Ap) * x * x + fabsf(c.Qm));
-        float D = fmaf(-4.0f * c.Cp, cc, b * b);
-        if (D < -1e-5f * scale) hit = false;  // the line misses the ellipse
-        const float s = sqrtf(fmaxf(D, 0.0f));
-        return upper ? (-b - s) / (2.0f * c.Cp) : (-b + s) / (2.0f * c.Cp);
-    };
-    const float xt = fminf(fmaxf(c.dxt, dxa), dxb), xbm = fminf(fmaxf(-c.dxt, dxa), dxb);
-    const float yh = xt == c.dxt ? c.dym : root(xt, true);
-    const float yl = xbm == -c.dxt ? -c.dym : root(xbm, false);
-    if (!hit) return kSpanEmpty;
-    // widening: a relative 2^-10 of the extents, the cancellation of -b +- s
-    // (2^-16 |B' x / C'|) and 1/32 px absolute
-    const float w = 0x1p-10f * (fabsf(yh) + fabsf(yl) + c.dym) +
-                    0x1p-16f * fabsf(c.Bp) * fmaxf(fabsf(dxa), fabsf(dxb)) / fabsf(c.Cp) + 0.03125f;
-    const int lo = max((int)ceilf(((c.v + (yl - w)) - 0.5f)), ya) - 16 * ty;
-    const int hi = min((int)floorf(((c.v + (yh + w)) - 0.5f)), yb) - 16 * ty;
-    if (lo > hi) return kSpanEmpty;
-    return (uint32_t)lo | ((uint32_t)hi << 4);
-}
-
 // Row 5b (2/6): one thread per row item (Gaussian r, tile row ty): its tile
 // cover [txa, txb] (band_tiles, binary64 pinned), the row key for the stable
 // row partition, and the per-row difference array of the per-tile counts.
@@ -689,7 +625,7 @@ __global__ void __launch_bounds__(kScanNT) k_row_items(const uint2 *__restrict__
                                                        const uint32_t *n_items_ptr,
                                                        const uint32_t *__restrict__ item_key,
                                                        uint32_t *__restrict__ item_pack, uint32_t *__restrict__ item_v,
-                                                       uint2 *__restrict__ item_spans, uint32_t item_cap) {
+                                                       uint32_t item_cap) {
     const uint32_t ni = *n_items_ptr;
     // the row partition (next launches) processes n_items_part items: n_items
     // when they fit the workspace, else none (the frame is then OVERFLOW and
@@ -709,28 +645,10 @@ __global__ void __launch_bounds__(kScanNT) k_row_items(const uint2 *__restrict__
         const float4 a = __ldg(rec0 + v), b = __ldg(rec1 + v);
         int txa, txb;
         uint32_t pack = 0u;  // empty row: txb + 1 <= txa
-        uint32_t sp[2] = {0u, 0u};
-        if (band_tiles(bconst[r], a.x, a.y, a.z, a.w, b.x, px0, px1, py0, py1, ty, txa, txb)) {
+        if (band_tiles(bconst[r], a.x, a.y, a.z, a.w, b.x, px0, px1, py0, py1, ty, txa, txb))
             pack = (uint32_t)txa | ((uint32_t)(txb + 1) << 16);
-            // reached rows of the item's first 7 tiles; byte 7: the 8th tile if it
-            // is the last, else every row of the band ∩ AABB (sound for all later tiles)
-            const SpanConsts sc = span_consts(a, b, px0, px1, py0, py1);
-            const int nt = txb - txa + 1;
-#pragma unroll 1
-            for (int k = 0; k < min(nt, 8); ++k) {
-                uint32_t span;
-                if (k == 7 && nt > 8) {
-                    const int ya = max(16 * ty, py0) - 16 * ty, yb = min(16 * ty + 15, py1) - 16 * ty;
-                    span = (uint32_t)ya | ((uint32_t)yb << 4);
-                } else {
-                    span = tile_row_span(sc, txa + k, ty);
-                }
-                sp[k >> 2] |= span << (8 * (k & 3));
-            }
-        }
         item_pack[i] = pack;
         item_v[i] = v;  // the owner index is replaced by the record slot
-        item_spans[i] = make_uint2(sp[0], sp[1]);
     }
 }
 
@@ -839,26 +757,78 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t *__restrict__
 #endif
 constexpr int kRowWarps = FDGS_ROW_WARPS;
 
+// Rows of tile (tx, ty) that a splat's ellipse reaches (pure culling for the
+// blend, DESIGN.md "Row spans"): the y-extent of the margin-inflated ellipse
+// {A'dx^2 + B'dx dy + C'dy^2 + Q2 + m >= 0} within the tile's pixel-centre
+// columns (tile ∩ AABB), as pixel rows of the tile ∩ AABB.  The ellipse is
+// convex, so the rows whose chord meets the column strip form one interval:
+// its top is the ellipse's topmost point if that lies in the strip, else the
+// larger root at the strip edge nearest to it (bottom likewise).  Computed in
+// binary32 and widened well beyond its rounding; m (2^-11 of the quadratic's
+// magnitude over the AABB + 2^-9) covers the rounding of the pinned fp32 e2
+// chain, so every pixel of the tile with e2 >= 0 lies in a listed row
+// (brute-force soundness test: tests/test_gpu_render.py).  Returns lo | hi << 4
+// (tile-relative rows), lo > hi when no row is reached.
+constexpr uint32_t kSpanEmpty = 0x0Fu;  // lo = 15 > hi = 0
+__device__ __forceinline__ uint32_t tile_row_span(const float4 &r0, const float4 &r1, int tx, int ty) {
+    const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
+    const uint32_t ax = __float_as_uint(r1.z), ay = __float_as_uint(r1.w) & 0x7fffffffu;
+    const int px0 = ax & 0xffff, px1 = ax >> 16, py0 = ay & 0xffff, py1 = ay >> 16;
+    const int xa = max(16 * tx, px0), xb = min(16 * tx + 15, px1);
+    const int ya = max(16 * ty, py0), yb = min(16 * ty + 15, py1);
+    if (xa > xb || ya > yb) return kSpanEmpty;
+    const float dxa = ((float)xa + 0.5f) - u, dxb = ((float)xb + 0.5f) - u;
+    const float X = fmaxf(fabsf(((float)px0 + 0.5f) - u), fabsf(((float)px1 + 0.5f) - u));
+    const float Y = fmaxf(fabsf(((float)py0 + 0.5f) - v), fabsf(((float)py1 + 0.5f) - v));
+    const float mag = fabsf(Ap) * X * X + fabsf(Bp) * X * Y + fabsf(Cp) * Y * Y;
+    const float Qm = Q2 + fmaf(mag, 0x1p-11f, 0x1p-9f);
+    const float K = 4.0f * Ap * Cp - Bp * Bp;
+    const int r_a = ya - 16 * ty, r_b = yb - 16 * ty;
+    if (!(K > 1e-4f * 4.0f * Ap * Cp) || !(Ap < 0.0f) || !(Cp < 0.0f))  // (near-)degenerate: every row
+        return (uint32_t)r_a | ((uint32_t)r_b << 4);
+    const float dym = sqrtf(-4.0f * Ap * Qm / K);  // half height of the inflated ellipse
+    const float dxt = -Bp * dym / (2.0f * Ap);     // x of its topmost point (the bottom one is at -dxt)
+    // y-roots of the ellipse on the vertical line dx = x: C'y^2 + (B'x) y + (A'x^2 + Qm) = 0 (C' < 0)
+    bool hit = true;
+    auto root = [&](float x, bool upper) {
+        const float b = Bp * x, c = fmaf(Ap * x, x, Qm);
+        const float scale = b * b + 4.0f * fabsf(Cp) * (fabsf(Ap) * x * x + fabsf(Qm));
+        float D = fmaf(-4.0f * Cp, c, b * b);
+        if (D < -1e-5f * scale) hit = false;  // the line misses the ellipse
+        D = fmaxf(D, 0.0f);
+        const float s = sqrtf(D);
+        return upper ? (-b - s) / (2.0f * Cp) : (-b + s) / (2.0f * Cp);
+    };
+    const float xt = fminf(fmaxf(dxt, dxa), dxb), xbm = fminf(fmaxf(-dxt, dxa), dxb);
+    const float yh = xt == dxt ? dym : root(xt, true);
+    const float yl = xbm == -dxt ? -dym : root(xbm, false);
+    if (!hit) return kSpanEmpty;
+    // widening: a relative 2^-10 of the extents, the cancellation of -b +- s
+    // (2^-16 |B' x / C'|) and 1/32 px absolute
+    const float w = 0x1p-10f * (fabsf(yh) + fabsf(yl) + dym) + 0x1p-16f * fabsf(Bp) * fmaxf(fabsf(dxa), fabsf(dxb)) /
+                    fabsf(Cp) + 0.03125f;
+    const int lo = max((int)ceilf(((v + (yl - w)) - 0.5f)), ya) - 16 * ty;
+    const int hi = min((int)floorf(((v + (yh + w)) - 0.5f)), yb) - 16 * ty;
+    if (lo > hi) return kSpanEmpty;
+    return (uint32_t)lo | ((uint32_t)hi << 4);
+}
+
 template <bool kWrite>
 __device__ __forceinline__ void row_walk(uint32_t w0, uint32_t w1, int lane, const uint32_t *__restrict__ sorted,
                                          const uint32_t *__restrict__ item_pack,
                                          const uint32_t *__restrict__ item_v, uint32_t *cnt, const uint32_t *base,
                                          uint32_t *__restrict__ entries, uint8_t *__restrict__ entry_rows,
-                                         const uint2 *__restrict__ item_spans) {
+                                         const float4 *__restrict__ rec0, const float4 *__restrict__ rec1, int ty) {
     for (uint32_t r0 = w0; r0 < w1; r0 += 32) {
         const uint32_t r = r0 + lane;
         int c = 0, txa = 0;
         uint32_t v = 0;
-        uint2 sp = make_uint2(0u, 0u);
         if (r < w1) {
             const uint32_t it = __ldg(sorted + r);
             const uint32_t pk = __ldg(item_pack + it);
             txa = (int)(pk & 0xffffu);
             c = max((int)(pk >> 16) - txa, 0);
-            if (kWrite) {
-                v = __ldg(item_v + it);
-                sp = __ldg(item_spans + it);
-            }
+            if (kWrite) v = __ldg(item_v + it);
         }
         int incl = c;
 #pragma unroll
@@ -879,7 +849,6 @@ __device__ __forceinline__ void row_walk(uint32_t w0, uint32_t w1, int lane, con
             const int exj = __shfl_sync(0xffffffffu, incl - c, j);
             const int jx = __shfl_sync(0xffffffffu, txa, j);
             const uint32_t vj = __shfl_sync(0xffffffffu, v, j);
-            const uint32_t spx = __shfl_sync(0xffffffffu, sp.x, j), spy = __shfl_sync(0xffffffffu, sp.y, j);
             const bool valid = e < total;
             const uint32_t tx = valid ? (uint32_t)(jx + (e - exj)) : 0xffffffffu;
             const uint32_t peers = __match_any_sync(0xffffffffu, tx);
@@ -887,9 +856,7 @@ __device__ __forceinline__ void row_walk(uint32_t w0, uint32_t w1, int lane, con
             if (kWrite && valid) {
                 const uint32_t pos = base[tx] + cnt[tx] + __popc(peers & lanemask_lt());
                 entries[pos] = vj;
-                // the entry's reached rows: byte min(tx - txa, 7) of its item's spans
-                const int k = min(e - exj, 7);
-                entry_rows[pos] = (uint8_t)(((k < 4 ? spx : spy) >> (8 * (k & 3))) & 0xffu);
+                entry_rows[pos] = (uint8_t)tile_row_span(__ldg(rec0 + vj), __ldg(rec1 + vj), (int)tx, ty);
             }
             __syncwarp();
             if (valid && leader) cnt[tx] += __popc(peers);
@@ -963,8 +930,8 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_row_scatter(const uint32_t *
                                                                 const uint32_t *__restrict__ tile_start,
                                                                 uint32_t *__restrict__ entries,
                                                                 uint8_t *__restrict__ entry_rows,
-                                                                const uint2 *__restrict__ item_spans,
-                                                                const Counters *ctrc) {
+                                                                const float4 *__restrict__ rec0,
+                                                                const float4 *__restrict__ rec1, const Counters *ctrc) {
     extern __shared__ uint32_t s_mem[];  // [kRowWarps][tiles_x] counters, then [tiles_x] base
     uint32_t *s_cnt = s_mem, *s_base = s_mem + kRowWarps * tiles_x;
     const int ty = blockIdx.x / kRowSeg, seg = blockIdx.x % kRowSeg;
@@ -1016,7 +983,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_row_scatter(const uint32_t *
         }
     }
     __syncthreads();
-    row_walk<true>(w0, w1, lane, sorted, item_pack, item_v, my, s_base, entries, entry_rows, item_spans);
+    row_walk<true>(w0, w1, lane, sorted, item_pack, item_v, my, s_base, entries, entry_rows, rec0, rec1, ty);
 }
 
 // ---------------------------------------------------------------- row 6
@@ -1672,7 +1639,6 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         uint32_t *ikey[2] = {reinterpret_cast<uint32_t *>(ws + L.ekey0), reinterpret_cast<uint32_t *>(ws + L.ekey1)};
         uint32_t *ival[2] = {reinterpret_cast<uint32_t *>(ws + L.eval0), reinterpret_cast<uint32_t *>(ws + L.eval1)};
         uint32_t *ipack = reinterpret_cast<uint32_t *>(ws + L.item_pack);
-        uint2 *ispans = reinterpret_cast<uint2 *>(ws + L.item_spans);
         uint32_t *iv = reinterpret_cast<uint32_t *>(ws + L.item_v);
         uint32_t *rhist = reinterpret_cast<uint32_t *>(ws + L.row_hist);
         uint64_t *tstat = reinterpret_cast<uint64_t *>(ws + L.tile_status);
@@ -1688,8 +1654,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
             k_bin_offsets<<<bgrid, kScanNT, 0, st>>>(rect_sorted, ctr, pcnt, ikey[0], iv, (uint32_t)L.max_entries);
         }
         k_row_items<<<(int)std::min<uint32_t>(item_chunks, FDGS_ITEM_GRID * L.p_sort), kScanNT, 0, st>>>(
-            rect_sorted, order, rec0, rec1, bconst, ctr, &ctr->n_items, ikey[0], ipack, iv, ispans,
-            (uint32_t)L.max_entries);
+            rect_sorted, order, rec0, rec1, bconst, ctr, &ctr->n_items, ikey[0], ipack, iv, (uint32_t)L.max_entries);
         k_row_scan<<<1, 32, 0, st>>>(rowdiff, L.tiles_y, row_start, rbase);
         // stable partition of the row items by tile row (canonical order kept within a row)
         const int rgrid = std::min((int)item_chunks, sort_grid(L.p_sort));
@@ -1710,7 +1675,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
                                                                       tcnt, ctr);
         k_tile_scan<<<1, 1024, 0, st>>>(tcnt, L.tiles_x, L.tiles_y, tstart, ctr, L.max_entries);
         k_row_scatter<<<nrb, 32 * kRowWarps, cnt_smem + sizeof(uint32_t) * L.tiles_x, st>>>(
-            sorted_items, ipack, iv, row_start, L.tiles_x, rhist, tstart, entries, erows, ispans, ctr);
+            sorted_items, ipack, iv, row_start, L.tiles_x, rhist, tstart, entries, erows, rec0, rec1, ctr);
     }
     if (front_only) return cudaGetLastError();  // graph capture of the front end
     // the blend may run on its own (lower-priority) stream, ordered after the front end
