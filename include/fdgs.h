@@ -243,8 +243,7 @@ fdgs_status fdgs_render_graph_destroy(fdgs_render_graph *graph);
  *   rec2 float4 {r, g, b, gid bits},
  *   depth uint32 (fp32 bits of camera z), order uint32[n_vis] (slots in
  *   canonical (depth, index) order), tile_start uint32[n_tiles + 1],
- *   entries uint32[E] (slots, per tile in canonical order), entry_rows
- *   uint8[E] (see the struct). */
+ *   entries uint32[E] (slots, per tile in canonical order). */
 typedef struct {
     const void *rec0, *rec1, *rec2;
     const uint32_t *depth;
@@ -254,9 +253,6 @@ typedef struct {
     const uint32_t *entries;
     const uint32_t *counters; /* [0]=n_act [1]=n_vis [2]=E [3]=status */
     int32_t n_tiles;
-    const uint8_t *entry_rows; /* uint8[E]: rows of the entry's tile its splat
-                                  reaches, lo | hi << 4 (tile-relative, lo > hi:
-                                  none) -- the blend's row culling */
 } fdgs_debug_views;
 fdgs_status fdgs_render_debug_views(void *d_ws, size_t ws_bytes, int32_t n, int32_t width, int32_t height,
                                     int64_t max_entries, fdgs_debug_views *out);

@@ -51,7 +51,7 @@ class FdgsFrameStats(C.Structure):
 class FdgsDebugViews(C.Structure):
     _fields_ = [("rec0", C.c_void_p), ("rec1", C.c_void_p), ("rec2", C.c_void_p), ("depth", C.c_void_p),
                 ("vis", C.c_void_p), ("order", C.c_void_p), ("tile_start", C.c_void_p), ("entries", C.c_void_p),
-                ("counters", C.c_void_p), ("n_tiles", C.c_int32), ("entry_rows", C.c_void_p)]
+                ("counters", C.c_void_p), ("n_tiles", C.c_int32)]
 
 
 class FdgsStvOpts(C.Structure):

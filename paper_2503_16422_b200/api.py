@@ -338,7 +338,6 @@ class Renderer:
             order=rank[arr(v.order, n, 4, torch.int32)[:n_vis].long()].int(),
             tile_start=arr(v.tile_start, v.n_tiles + 1, 4, torch.int32),
             entries=rank[arr(v.entries, max(E, 1), 4, torch.int32)[:E].long()].int(),
-            entry_rows=arr(v.entry_rows, max(E, 1), 1, torch.uint8)[:E],
             n_tiles=v.n_tiles,
         )
 

@@ -112,7 +112,6 @@ RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max
     L.eval0 = take(4 * cap);
     L.eval1 = take(4 * cap);
     L.entries = take(4 * cap);
-    L.entry_rows = take(cap);                               // reached tile rows per entry (k_row_scatter)
     L.total = off;
     return L;
 }
@@ -423,7 +422,6 @@ fdgs_status fdgs_render_debug_views(void *d_ws, size_t ws_bytes, int32_t n, int3
     out->entries = reinterpret_cast<const uint32_t *>(w + L.entries);
     out->counters = reinterpret_cast<const uint32_t *>(w + L.counters);
     out->n_tiles = L.n_tiles;
-    out->entry_rows = reinterpret_cast<const uint8_t *>(w + L.entry_rows);
     return FDGS_OK;
 }
 

@@ -79,7 +79,7 @@ struct RenderLayout {
     size_t counters, sort_gbase, tile_cnt, row_diff, bin_cnt, zero_end;
     size_t epoch, sort_status, tile_status;
     size_t surv, surv_bits, cull_cnt, vis, vis_bits, vis_cnt, rec0, rec1, rec2, depth, rect, rect_sorted, keys0, keys1, vals0, vals1;
-    size_t tile_gbase, tile_start, row_start, row_hist, band_consts, item_pack, item_v, ekey0, ekey1, eval0, eval1, entries, entry_rows, total;
+    size_t tile_gbase, tile_start, row_start, row_hist, band_consts, item_pack, item_v, ekey0, ekey1, eval0, eval1, entries, total;
 };
 RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max_entries);
 

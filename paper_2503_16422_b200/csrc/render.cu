@@ -757,68 +757,11 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t *__restrict__
 #endif
 constexpr int kRowWarps = FDGS_ROW_WARPS;
 
-// Rows of tile (tx, ty) that a splat's ellipse reaches (pure culling for the
-// blend): the y-extent of the margin-inflated ellipse
-// {A'dx^2 + B'dx dy + C'dy^2 + Q2 + m >= 0} within the tile's pixel-centre
-// columns (tile ∩ AABB), as pixel rows of the tile ∩ AABB.  The ellipse is
-// convex, so the rows whose chord meets the column strip form one interval:
-// its top is the ellipse's topmost point if that lies in the strip, else the
-// larger root at the strip edge nearest to it (bottom likewise).  Computed in
-// binary32 and widened well beyond its rounding; m (2^-11 of the quadratic's
-// magnitude over the AABB + 2^-9) covers the rounding of the pinned fp32 e2
-// chain, so every pixel of the tile with e2 >= 0 lies in a listed row
-// (brute-force soundness test: tests/test_gpu_render.py).  Returns lo | hi << 4
-// (tile-relative rows), lo > hi when no row is reached.
-constexpr uint32_t kSpanEmpty = 0x0Fu;  // lo = 15 > hi = 0
-__device__ __forceinline__ uint32_t tile_row_span(const float4 &r0, const float4 &r1, int tx, int ty) {
-    const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
-    const uint32_t ax = __float_as_uint(r1.z), ay = __float_as_uint(r1.w) & 0x7fffffffu;
-    const int px0 = ax & 0xffff, px1 = ax >> 16, py0 = ay & 0xffff, py1 = ay >> 16;
-    const int xa = max(16 * tx, px0), xb = min(16 * tx + 15, px1);
-    const int ya = max(16 * ty, py0), yb = min(16 * ty + 15, py1);
-    if (xa > xb || ya > yb) return kSpanEmpty;
-    const float dxa = ((float)xa + 0.5f) - u, dxb = ((float)xb + 0.5f) - u;
-    const float X = fmaxf(fabsf(((float)px0 + 0.5f) - u), fabsf(((float)px1 + 0.5f) - u));
-    const float Y = fmaxf(fabsf(((float)py0 + 0.5f) - v), fabsf(((float)py1 + 0.5f) - v));
-    const float mag = fabsf(Ap) * X * X + fabsf(Bp) * X * Y + fabsf(Cp) * Y * Y;
-    const float Qm = Q2 + fmaf(mag, 0x1p-11f, 0x1p-9f);
-    const float K = 4.0f * Ap * Cp - Bp * Bp;
-    const int r_a = ya - 16 * ty, r_b = yb - 16 * ty;
-    if (!(K > 1e-4f * 4.0f * Ap * Cp) || !(Ap < 0.0f) || !(Cp < 0.0f))  // (near-)degenerate: every row
-        return (uint32_t)r_a | ((uint32_t)r_b << 4);
-    const float dym = sqrtf(-4.0f * Ap * Qm / K);  // half height of the inflated ellipse
-    const float dxt = -Bp * dym / (2.0f * Ap);     // x of its topmost point (the bottom one is at -dxt)
-    // y-roots of the ellipse on the vertical line dx = x: C'y^2 + (B'x) y + (A'x^2 + Qm) = 0 (C' < 0)
-    bool hit = true;
-    auto root = [&](float x, bool upper) {
-        const float b = Bp * x, c = fmaf(Ap * x, x, Qm);
-        const float scale = b * b + 4.0f * fabsf(Cp) * (fabsf(Ap) * x * x + fabsf(Qm));
-        float D = fmaf(-4.0f * Cp, c, b * b);
-        if (D < -1e-5f * scale) hit = false;  // the line misses the ellipse
-        D = fmaxf(D, 0.0f);
-        const float s = sqrtf(D);
-        return upper ? (-b - s) / (2.0f * Cp) : (-b + s) / (2.0f * Cp);
-    };
-    const float xt = fminf(fmaxf(dxt, dxa), dxb), xbm = fminf(fmaxf(-dxt, dxa), dxb);
-    const float yh = xt == dxt ? dym : root(xt, true);
-    const float yl = xbm == -dxt ? -dym : root(xbm, false);
-    if (!hit) return kSpanEmpty;
-    // widening: a relative 2^-10 of the extents, the cancellation of -b +- s
-    // (2^-16 |B' x / C'|) and 1/32 px absolute
-    const float w = 0x1p-10f * (fabsf(yh) + fabsf(yl) + dym) + 0x1p-16f * fabsf(Bp) * fmaxf(fabsf(dxa), fabsf(dxb)) /
-                    fabsf(Cp) + 0.03125f;
-    const int lo = max((int)ceilf(((v + (yl - w)) - 0.5f)), ya) - 16 * ty;
-    const int hi = min((int)floorf(((v + (yh + w)) - 0.5f)), yb) - 16 * ty;
-    if (lo > hi) return kSpanEmpty;
-    return (uint32_t)lo | ((uint32_t)hi << 4);
-}
-
 template <bool kWrite>
 __device__ __forceinline__ void row_walk(uint32_t w0, uint32_t w1, int lane, const uint32_t *__restrict__ sorted,
                                          const uint32_t *__restrict__ item_pack,
                                          const uint32_t *__restrict__ item_v, uint32_t *cnt, const uint32_t *base,
-                                         uint32_t *__restrict__ entries, uint8_t *__restrict__ entry_rows,
-                                         const float4 *__restrict__ rec0, const float4 *__restrict__ rec1, int ty) {
+                                         uint32_t *__restrict__ entries) {
     for (uint32_t r0 = w0; r0 < w1; r0 += 32) {
         const uint32_t r = r0 + lane;
         int c = 0, txa = 0;
@@ -853,11 +796,7 @@ __device__ __forceinline__ void row_walk(uint32_t w0, uint32_t w1, int lane, con
             const uint32_t tx = valid ? (uint32_t)(jx + (e - exj)) : 0xffffffffu;
             const uint32_t peers = __match_any_sync(0xffffffffu, tx);
             const bool leader = (__ffs(peers) - 1) == lane;
-            if (kWrite && valid) {
-                const uint32_t pos = base[tx] + cnt[tx] + __popc(peers & lanemask_lt());
-                entries[pos] = vj;
-                entry_rows[pos] = (uint8_t)tile_row_span(__ldg(rec0 + vj), __ldg(rec1 + vj), (int)tx, ty);
-            }
+            if (kWrite && valid) entries[base[tx] + cnt[tx] + __popc(peers & lanemask_lt())] = vj;
             __syncwarp();
             if (valid && leader) cnt[tx] += __popc(peers);
             __syncwarp();
@@ -928,10 +867,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_row_scatter(const uint32_t *
                                                                 const uint32_t *__restrict__ row_start, int tiles_x,
                                                                 const uint32_t *__restrict__ hist,
                                                                 const uint32_t *__restrict__ tile_start,
-                                                                uint32_t *__restrict__ entries,
-                                                                uint8_t *__restrict__ entry_rows,
-                                                                const float4 *__restrict__ rec0,
-                                                                const float4 *__restrict__ rec1, const Counters *ctrc) {
+                                                                uint32_t *__restrict__ entries, const Counters *ctrc) {
     extern __shared__ uint32_t s_mem[];  // [kRowWarps][tiles_x] counters, then [tiles_x] base
     uint32_t *s_cnt = s_mem, *s_base = s_mem + kRowWarps * tiles_x;
     const int ty = blockIdx.x / kRowSeg, seg = blockIdx.x % kRowSeg;
@@ -983,7 +919,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_row_scatter(const uint32_t *
         }
     }
     __syncthreads();
-    row_walk<true>(w0, w1, lane, sorted, item_pack, item_v, my, s_base, entries, entry_rows, rec0, rec1, ty);
+    row_walk<true>(w0, w1, lane, sorted, item_pack, item_v, my, s_base, entries);
 }
 
 // ---------------------------------------------------------------- row 6
@@ -1346,10 +1282,12 @@ constexpr float kStopU = 1e-4f / 255.0f;  // the stop threshold 1e-4 on T, on U 
 #endif
 constexpr int kWiPairUnroll = FDGS_WI_PAIR_UNROLL;
 
+#ifndef FDGS_WI_PREFETCH
+#define FDGS_WI_PREFETCH 1
+#endif
 constexpr int kWiThreads = 128;
 __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uint32_t *__restrict__ tile_start,
                                                          const uint32_t *__restrict__ entries,
-                                                         const uint8_t *__restrict__ entry_rows,
                                                          const float4 *__restrict__ rec0,
                                                          const float4 *__restrict__ rec1,
                                                          const float4 *__restrict__ rec2, const Counters *ctr,
@@ -1463,66 +1401,74 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
             undo(Cr.y, Cg.y, Cb.y, T.y, thr.y, T0.y, T1.y, w1.y, w2.y);
         }
     };
-    // Batches of 32 entries, one per lane: the entry's reached tile rows (from the
-    // binning, tile_row_span) decide whether the record reaches this warp's
-    // strip; only records that do are gathered (rec0..2, L2-resident) and
-    // staged with the pinned row terms of the strip's 4 rows.
-    const int wlo = wl_row0(warp), whi = wlo + kWlRows - 1;
-    float rowc[kWlRows];  // pixel-centre y of the strip's rows
-#pragma unroll
-    for (int r = 0; r < kWlRows; ++r) rowc[r] = (float)(ty * 16 + wlo + r) + 0.5f;
-    auto fetch = [&](uint32_t bs, bool &reach, float4 &a0, float4 &a1, float4 &a2) {
-        reach = false;
+    auto fetch = [&](uint32_t bs, float4 &a0, float4 &a1, float4 &a2) {
+        a0 = a1 = a2 = make_float4(0.f, 0.f, 0.f, 0.f);
         if (bs + lane < end) {
-            const uint32_t span = __ldg(entry_rows + bs + lane);
-            const int lo = (int)(span & 15u), hi = (int)(span >> 4);
-            reach = lo <= whi && hi >= wlo && lo <= hi;
-            if (reach) {
-                const uint32_t v = __ldg(entries + bs + lane);
-                a0 = __ldg(rec0 + v);
-                a1 = __ldg(rec1 + v);
-                a2 = __ldg(rec2 + v);
-            }
+            const uint32_t v = __ldg(entries + bs + lane);
+            a0 = __ldg(rec0 + v);
+            a1 = __ldg(rec1 + v);
+            a2 = __ldg(rec2 + v);
         }
     };
     bool wdone = __all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf);
-    float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0;
-    bool reach;
-    fetch(start, reach, r0, r1, r2);
+    float4 r0, r1, r2;
+#if FDGS_WI_PREFETCH
+    fetch(start, r0, r1, r2);
+#endif
     for (uint32_t base = start; base < end && !wdone; base += 32) {
+        const int n = (int)min(32u, end - base);
+#if !FDGS_WI_PREFETCH
+        fetch(base, r0, r1, r2);
+#endif
         // ---- stage this warp's list of the batch
+        const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
+        const bool redundant = (__float_as_uint(r1.w) & 0x80000000u) != 0u;
+        uint32_t mb = 0;
+        float xl = 0.f, xr = 0.f, hA = 0.f, marg = 0.f;
+        int y0 = 16, y1 = -1;
+        if (lane < n) {
+            const uint32_t ax = __float_as_uint(r1.z), ay = __float_as_uint(r1.w);
+            const int x0 = max((int)(ax & 0xffff) - tx * 16, 0), x1 = min((int)(ax >> 16) - tx * 16, 15);
+            y0 = max((int)(ay & 0xffff) - ty * 16, 0);
+            y1 = min((int)((ay >> 16) & 0x7fffu) - ty * 16, 15);
+            const uint32_t xm = ((2u << x1) - 1u) & ~((1u << x0) - 1u);
+            const uint32_t ym = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
+            mb = ~(xm | (ym << 16));
+            if (x0 > x1) y1 = -1;
+            xl = __fsub_rn((float)(tx * 16 + x0) + 0.5f, u);
+            xr = __fsub_rn((float)(tx * 16 + x1) + 0.5f, u);
+            const float yl = (float)(ty * 16 + y0) + 0.5f - v, yr = (float)(ty * 16 + y1) + 0.5f - v;
+            const float X = fmaxf(fabsf(xl), fabsf(xr)), Y = fmaxf(fabsf(yl), fabsf(yr));
+            marg = -(1e-3f * (fabsf(Ap) * X * X + fabsf(Bp) * X * Y + fabsf(Cp) * Y * Y) + 1e-3f);
+            hA = __fdividef(-0.5f, Ap);
+        }
+        float4 tr[kWlRows];
+        bool rw = false;
+#pragma unroll
+        for (int r = 0; r < kWlRows; ++r) {  // pinned e2 chain, row terms (DESIGN.md step 10)
+            const int row = wl_row0(warp) + r;
+            const float dy = __fsub_rn((float)(ty * 16 + row) + 0.5f, v);
+            const float t1 = __fmul_rn(Bp, dy);
+            const float t3 = __fmul_rn(Cp, dy);
+            const float t4 = __fmaf_rn(t3, dy, Q2);
+            const float xs = fminf(fmaxf(t1 * hA, xl), xr);
+            rw |= row >= y0 && row <= y1 && fmaf(xs, fmaf(Ap, xs, t1), t4) >= marg;
+            tr[r] = make_float4(r2.z, __uint_as_float(mb), t1, t4);
+        }
+        const bool reach = lane < n && rw;
         const uint32_t bal = __ballot_sync(0xffffffffu, reach);
-        bool masked = false;
+        const bool masked = __any_sync(0xffffffffu, reach && !redundant && (mb & foot) != 0u);
         __syncwarp();  // the previous list has been read
         if (reach) {
-            const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
-            // complemented pixel-AABB mask, needed unless k_slice proved the
-            // AABB test redundant for this record (then 0: no pixel excluded)
-            uint32_t mb = 0;
-            if ((__float_as_uint(r1.w) & 0x80000000u) == 0u) {
-                const uint32_t ax = __float_as_uint(r1.z), ay = __float_as_uint(r1.w);
-                const int x0 = max((int)(ax & 0xffff) - tx * 16, 0), x1 = min((int)(ax >> 16) - tx * 16, 15);
-                const int y0 = max((int)(ay & 0xffff) - ty * 16, 0);
-                const int y1 = min((int)((ay >> 16) & 0x7fffu) - ty * 16, 15);
-                const uint32_t xm = ((2u << x1) - 1u) & ~((1u << x0) - 1u);
-                const uint32_t ym = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
-                mb = ~(xm | (ym << 16));
-                masked = (mb & foot) != 0u;
-            }
             WlEntry &E = s_list[warp][__popc(bal & lanemask_lt())];
             E.a = make_float4(u, Ap, r2.x, r2.y);
 #pragma unroll
-            for (int r = 0; r < kWlRows; ++r) {  // pinned e2 chain, row terms (DESIGN.md step 10)
-                const float dy = __fsub_rn(rowc[r], v);
-                const float t1 = __fmul_rn(Bp, dy);
-                const float t3 = __fmul_rn(Cp, dy);
-                const float t4 = __fmaf_rn(t3, dy, Q2);
-                E.t[r] = make_float4(r2.z, __uint_as_float(mb), t1, t4);
-            }
+            for (int r = 0; r < kWlRows; ++r) E.t[r] = tr[r];
         }
-        masked = __any_sync(0xffffffffu, masked);
+#if FDGS_WI_PREFETCH
         // ---- gather the next batch while this one is composited
-        fetch(base + 32, reach, r0, r1, r2);
+        fetch(base + 32, r0, r1, r2);
+#endif
         __syncwarp();
         const int cnt = __popc(bal);
         if (masked) {
@@ -1594,7 +1540,6 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     uint32_t *vals[2] = {reinterpret_cast<uint32_t *>(ws + L.vals0), reinterpret_cast<uint32_t *>(ws + L.vals1)};
     uint32_t *tstart = reinterpret_cast<uint32_t *>(ws + L.tile_start);
     uint32_t *entries = reinterpret_cast<uint32_t *>(ws + L.entries);
-    uint8_t *erows = reinterpret_cast<uint8_t *>(ws + L.entry_rows);
     uint32_t *surv = reinterpret_cast<uint32_t *>(ws + L.surv);
     uint32_t *vis = reinterpret_cast<uint32_t *>(ws + L.vis);
 
@@ -1675,7 +1620,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
                                                                       tcnt, ctr);
         k_tile_scan<<<1, 1024, 0, st>>>(tcnt, L.tiles_x, L.tiles_y, tstart, ctr, L.max_entries);
         k_row_scatter<<<nrb, 32 * kRowWarps, cnt_smem + sizeof(uint32_t) * L.tiles_x, st>>>(
-            sorted_items, ipack, iv, row_start, L.tiles_x, rhist, tstart, entries, erows, rec0, rec1, ctr);
+            sorted_items, ipack, iv, row_start, L.tiles_x, rhist, tstart, entries, ctr);
     }
     if (front_only) return cudaGetLastError();  // graph capture of the front end
     // the blend may run on its own (lower-priority) stream, ordered after the front end
@@ -1695,9 +1640,8 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
                                                             L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T,
                                                             stats);
     } else {  // the timed blend
-        k_blend_wi<<<L.n_tiles, kWiThreads, 0, bst>>>(tstart, entries, erows, rec0, rec1, rec2, ctr, L.tiles_x,
-                                                      L.width, L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb,
-                                                      out_T);
+        k_blend_wi<<<L.n_tiles, kWiThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
+                                                      L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
     }
     if (ev && (e = cudaEventRecord(ev[4], bst)) != cudaSuccess) return e;
     return cudaGetLastError();
@@ -1791,7 +1735,6 @@ cudaError_t render_graph_launch(RenderGraphImpl &g, const SceneDev &sc, const ui
     uint32_t *vcnt = reinterpret_cast<uint32_t *>(ws + L.vis_cnt);
     uint32_t *tstart = reinterpret_cast<uint32_t *>(ws + L.tile_start);
     uint32_t *entries = reinterpret_cast<uint32_t *>(ws + L.entries);
-    const uint8_t *erows = reinterpret_cast<const uint8_t *>(ws + L.entry_rows);
     // k_cull(sc, mask_l, mask_r, t, ctr, bits, cnt)
     const Counters *cctr = ctr;
     void *a_cull[] = {(void *)&sc, (void *)&mask_l, (void *)&mask_r, (void *)&t, (void *)&ctr, (void *)&cbits,
@@ -1825,8 +1768,8 @@ cudaError_t render_graph_launch(RenderGraphImpl &g, const SceneDev &sc, const ui
         if ((e = cudaStreamWaitEvent(blend_st, split_ev, 0)) != cudaSuccess) return e;
         bst = blend_st;
     }
-    k_blend_wi<<<L.n_tiles, kWiThreads, 0, bst>>>(tstart, entries, erows, rec0, rec1, rec2, cctr, L.tiles_x,
-                                                  L.width, L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
+    k_blend_wi<<<L.n_tiles, kWiThreads, 0, bst>>>(tstart, entries, rec0, rec1, rec2, cctr, L.tiles_x, L.width,
+                                                  L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
     return cudaGetLastError();
 }
 

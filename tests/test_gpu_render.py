@@ -510,84 +510,3 @@ def test_overflow_writes_nothing_past_the_workspace(cap):
         assert st == _lib.FDGS_ERR_OVERFLOW
     torch.cuda.synchronize()
     assert bool((buf[nb:] == 0xA5).all())
-
-
-def _row_span_violations(views, W, H, chunk=1 << 18):
-    """Brute force over every (entry, pixel of its tile ∩ AABB) in binary64 on
-    the GPU: a pixel whose pinned fp32 e2 chain can reach >= 0 (exact quadratic
-    + the chain's rounding budget, 9 x 2^-24 of the absolute terms) must lie in
-    a row of the entry's span.  Returns (violations, reached rows, AABB rows)."""
-    E = views["n_entries"]
-    ts = views["tile_start"].long()
-    T = ts.numel() - 1
-    tiles_x = (W + 15) // 16
-    tile = torch.repeat_interleave(torch.arange(T, device=ts.device), ts[1:] - ts[:-1])
-    assert tile.numel() == E
-    g_all = views["entries"].long()
-    span = views["entry_rows"].int()
-    r0 = views["rec0"].double()
-    r1 = views["rec1"]
-    bits = r1[:, 2:4].contiguous().view(torch.int32).long() & 0x7FFFFFFF
-    bad = reached = rows_aabb = 0
-    k = torch.arange(16, device=ts.device, dtype=torch.float64)
-    for c0 in range(0, E, chunk):
-        g = g_all[c0:c0 + chunk]
-        t = tile[c0:c0 + chunk]
-        tx, ty = (t % tiles_x).double(), (t // tiles_x).double()
-        u, v, A, B = [r0[g, i][:, None, None] for i in range(4)]
-        C, Q = [r1[g, i].double()[:, None, None] for i in (0, 1)]
-        ax, ay = bits[g, 0], bits[g, 1]
-        px0, px1 = (ax & 0xFFFF).double(), (ax >> 16).double()
-        py0, py1 = (ay & 0xFFFF).double(), (ay >> 16).double()
-        ii = 16 * tx[:, None] + k[None]            # [e, 16] pixel columns
-        jj = 16 * ty[:, None] + k[None]            # [e, 16] pixel rows
-        inx = (ii >= px0[:, None]) & (ii <= px1[:, None]) & (ii < W)
-        iny = (jj >= py0[:, None]) & (jj <= py1[:, None]) & (jj < H)
-        dx = (ii + 0.5)[:, None, :] - u
-        dy = (jj + 0.5)[:, :, None] - v
-        q = A * dx * dx + B * dx * dy + C * dy * dy + Q
-        err = 9 * 2.0 ** -24 * (A.abs() * dx * dx + B.abs() * (dx * dy).abs() + C.abs() * dy * dy + Q.abs())
-        possible = (q + err >= 0) & inx[:, None, :] & iny[:, :, None]
-        lo, hi = (span[c0:c0 + chunk] & 15), (span[c0:c0 + chunk] >> 4)
-        rr = torch.arange(16, device=ts.device)[None]
-        inspan = (rr >= lo[:, None]) & (rr <= hi[:, None])
-        bad += int((possible & ~inspan[:, :, None]).sum())
-        reached += int((inspan & iny).sum())
-        rows_aabb += int((iny & inx.any(1, keepdim=True)).sum())
-    return bad, reached, rows_aabb
-
-
-@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
-def test_entry_row_spans_sound_brute_force(name):
-    """The blend's row culling (entry_rows from k_row_scatter, tile_row_span):
-    no pixel with e2 >= 0 lies outside its entry's row span -- brute force over
-    every entry and pixel of full-size frames -- and the spans cull (fewer
-    rows than the tile ∩ AABB)."""
-    scene = fi.make_scene(name, n={"c2": None, "c3": None, "c4": 600_000}[name])
-    cam = fi.make_cameras(name)[{"c2": 11, "c3": 5, "c4": 14}[name]]
-    _, _, stats, r = _render(scene, cam, 0.45)
-    v = r.debug_views()
-    bad, reached, rows = _row_span_violations(v, cam.width, cam.height)
-    assert bad == 0
-    assert v["n_entries"] > 100_000 and reached < 0.9 * rows, (reached, rows)
-
-
-def test_entry_row_spans_sound_adversarial():
-    """Thin, strongly sheared and very large splats (the hard cases of the
-    span's fp32 root computation) over tile edges: still sound."""
-    rng = np.random.default_rng(17)
-    n = 4000
-    means = np.stack([rng.uniform(-3, 3, n), rng.uniform(-2, 2, n), rng.uniform(2.5, 9, n), np.full(n, 0.5)], 1)
-    sx = np.exp(rng.uniform(-6, 0.5, n))
-    scales = np.stack([sx, sx * np.exp(rng.uniform(-6, 0, n)), sx * np.exp(rng.uniform(-6, 0, n)),
-                       np.full(n, 0.4)], 1)
-    q = rng.standard_normal((n, 4))
-    q /= np.linalg.norm(q, axis=1, keepdims=True)
-    sc = fi.isotropic_scene(means, scales, rng.uniform(0.05, 1.0, n), colors=rng.uniform(0, 1, (n, 3)),
-                            rot_l=q, rot_r=np.tile([1.0, 0, 0, 0], (n, 1)))
-    cam = fi.make_cameras("c3", width=640, height=480, fx=600.0, count=3)[1]
-    img, _, stats, r = _render(sc, cam, 0.5)
-    v = r.debug_views()
-    bad, reached, rows = _row_span_violations(v, cam.width, cam.height)
-    assert bad == 0 and v["n_entries"] > 10_000
-    assert_rgb_parity(img, oracle.render(sc, cam, 0.5))
