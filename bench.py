@@ -79,6 +79,11 @@ def parse():
     p.add_argument("--streams", type=int, default=6, help="frame-pipelining depth (workspaces/streams)")
     p.add_argument("--no-split", action="store_true", help="blend on the front-end stream (no priority split)")
     p.add_argument("--graphs", action="store_true", help="one CUDA-graph launch per frame (RenderPipeline(graphs=True))")
+    p.add_argument("--py-submit", action="store_true",
+                   help="submit frames from the Python loop (one C call per frame) instead of fdgs_pipeline_render")
+    p.add_argument("--submit-threads", type=int, default=3, help="host threads of fdgs_pipeline_render")
+    p.add_argument("--sync-compact", action="store_true",
+                   help="read each working set's size back to the host (Scene.compact sync=True)")
     p.add_argument("--config", choices=["c2", "c3", "c4"], default="c3")
     p.add_argument("--unmasked", action="store_true", help="render without the key-frame filter")
     p.add_argument("--literal-masks", action="store_true",
@@ -241,7 +246,7 @@ class _FakePipeline:
         for k, x in enumerate(frames):
             outs[k].fill_(float(x[0]))
             if frame_done is not None:
-                frame_done(k, outs[k], None)
+                frame_done(k, outs[k], None, None)
 
 
 def _fake_mask(k, words):
@@ -321,7 +326,9 @@ def run_ours(args):
         outs = [torch.empty((3, H, W), dtype=torch.float32) for _ in range(F)]
         stream = None
     else:
-        pipe = fd.RenderPipeline(scene, W, H, depth=args.streams, split=not args.no_split, graphs=args.graphs)
+        pipe = fd.RenderPipeline(scene, W, H, depth=args.streams, split=not args.no_split, graphs=args.graphs,
+                                 native=False if (args.py_submit or args.graphs) else None,
+                                 threads=args.submit_threads)
         renderer = pipe.renderers[0]
         outs = [renderer.new_output() for _ in range(F)]
         stats = torch.zeros((F, 4), dtype=torch.int64, device=dev)  # fdgs_frame_stats is 32 bytes
@@ -357,7 +364,7 @@ def run_ours(args):
         if (li, ri) not in wsets:
             if len(wsets) >= 2:
                 wsets.pop(next(iter(wsets)))
-            wsets[(li, ri)] = scene.compact(masks[li], masks[ri], stream=stream)
+            wsets[(li, ri)] = scene.compact(masks[li], masks[ri], stream=stream, sync=args.sync_compact)
             compacts.append(timing_now[0])
         return cam_structs[ci], float(times[ti]), None, None, wsets[(li, ri)]
 
@@ -640,7 +647,8 @@ def run_ours(args):
                     if (li, ri) not in e2e_sets:
                         if len(e2e_sets) >= 2:
                             e2e_sets.pop(next(iter(e2e_sets)))
-                        e2e_sets[(li, ri)] = scene.compact(dev_masks[li], dev_masks[ri], stream=stream)
+                        e2e_sets[(li, ri)] = scene.compact(dev_masks[li], dev_masks[ri], stream=stream,
+                                                           sync=args.sync_compact)
                     jobs.append((cam_structs[ci], float(times[ti]), None, None, e2e_sets[(li, ri)]))
                 else:
                     jobs.append((cam_structs[ci], float(times[ti]), dev_masks[li] if MASKED else None,

@@ -96,6 +96,11 @@ typedef struct {
                                      for max(n, n_capacity) Gaussians, so a full
                                      scene and its working sets share one
                                      workspace layout (no re-zeroing)           */
+    const uint32_t *d_n;          /* nullable DEVICE count: the render uses the
+                                     first min(*d_n, n) Gaussians (n then is the
+                                     arrays' capacity).  Lets a working set whose
+                                     size fdgs_scene_compact wrote on the device
+                                     be rendered with no host synchronisation   */
 } fdgs_scene;
 
 /* Pinhole view "I" of P:126 (HOST struct).  world->camera rotation R
@@ -232,6 +237,52 @@ fdgs_status fdgs_render_graph_launch_split(fdgs_render_graph *graph, const fdgs_
                                            const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T,
                                            void *stream, void *blend_stream, void *split_event);
 fdgs_status fdgs_render_graph_destroy(fdgs_render_graph *graph);
+
+/* Batched submission of frames over a pipeline of render workspaces (the
+ * host side of the render path).  A pipeline has
+ * `depth` slots, each a render workspace (zero-filled once, as for
+ * fdgs_render) with a front-end stream and a blend stream (cudaStream_t as
+ * void*; blend_stream NULL = the blend on the front stream); streams should
+ * have the front end at a higher priority than the blend.  Frame k of a batch
+ * renders in slot k mod depth (fdgs_render_split); a slot's next frame is
+ * ordered after its previous blend.  The handle owns n_threads host threads
+ * that issue the batch's launches in parallel (one group of slots per
+ * thread; 1 = the caller's thread), plus its own CUDA events.
+ *   fdgs_frame_job: the frame (scene and camera BY VALUE, masks, t, outputs
+ *   as for fdgs_render; d_stats nullable = the timed blend, else the counting
+ *   blend); h_out_rgb (nullable, pinned HOST float[3][H][W]): copied D2H on
+ *   copy stream k mod n_copy after the blend; d_status (nullable, DEVICE 16
+ *   bytes): the frame's {n_act, n_vis, n_entries, status} after the blend;
+ *   done_event (nullable cudaEvent_t): recorded once the frame is complete.
+ *   fdgs_pipeline_render: ASYNC on `stream`: every slot and copy stream first
+ *   waits for `stream`'s work, and `stream` waits for every frame and copy of
+ *   the batch; stage_events (nullable): 5 caller-created events per job, as
+ *   fdgs_render_timed.  Returns when every launch is issued.  One batch at a
+ *   time per handle.
+ * Errors: INVALID_ARG, those of fdgs_render_split, CUDA. */
+typedef struct {
+    void *d_ws;
+    size_t ws_bytes;
+    int64_t max_entries;
+    void *front_stream, *blend_stream;
+} fdgs_pipeline_slot;
+typedef struct {
+    fdgs_scene scene;
+    const uint32_t *d_mask_l, *d_mask_r;
+    fdgs_camera cam;
+    float t;
+    float *d_out_rgb, *d_out_T;
+    fdgs_frame_stats *d_stats;
+    float *h_out_rgb;
+    void *d_status;
+    void *done_event;
+} fdgs_frame_job;
+typedef struct fdgs_pipeline fdgs_pipeline;
+fdgs_status fdgs_pipeline_create(const fdgs_pipeline_slot *slots, int32_t depth, void *const *copy_streams,
+                                 int32_t n_copy, int32_t n_threads, fdgs_pipeline **out);
+fdgs_status fdgs_pipeline_render(fdgs_pipeline *pipeline, const fdgs_frame_job *jobs, int32_t n_jobs, void *stream,
+                                 void *const *stage_events);
+fdgs_status fdgs_pipeline_destroy(fdgs_pipeline *pipeline);
 
 /* Device views into a render workspace after fdgs_render (tests/debug only).
  * Records are indexed by the SLOT of a Gaussian that passed the mask and the

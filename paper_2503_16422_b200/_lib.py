@@ -27,6 +27,7 @@ EXPORTS = [
     "fdgs_keyframe_mask_contrib_workspace_bytes", "fdgs_keyframe_mask_contrib",
     "fdgs_mask_compact_workspace_bytes", "fdgs_mask_compact", "fdgs_stv_workspace_bytes", "fdgs_stv_score",
     "fdgs_scene_compact_workspace_bytes", "fdgs_scene_compact", "fdgs_prune_workspace_bytes", "fdgs_prune_mask",
+    "fdgs_pipeline_create", "fdgs_pipeline_render", "fdgs_pipeline_destroy",
 ]
 
 
@@ -34,7 +35,8 @@ class FdgsScene(C.Structure):
     _fields_ = [("n", C.c_int32), ("mean", C.c_void_p), ("scale", C.c_void_p), ("rot_l", C.c_void_p),
                 ("rot_r", C.c_void_p), ("opacity", C.c_void_p), ("log255_opacity", C.c_void_p),
                 ("sh", C.c_void_p), ("sh_index", C.c_void_p), ("sh_codebook_size", C.c_int32),
-                ("param_stride", C.c_int32), ("gid", C.c_void_p), ("n_capacity", C.c_int32)]
+                ("param_stride", C.c_int32), ("gid", C.c_void_p), ("n_capacity", C.c_int32),
+                ("d_n", C.c_void_p)]
 
 
 class FdgsCamera(C.Structure):
@@ -52,6 +54,17 @@ class FdgsDebugViews(C.Structure):
     _fields_ = [("rec0", C.c_void_p), ("rec1", C.c_void_p), ("rec2", C.c_void_p), ("depth", C.c_void_p),
                 ("vis", C.c_void_p), ("order", C.c_void_p), ("tile_start", C.c_void_p), ("entries", C.c_void_p),
                 ("counters", C.c_void_p), ("n_tiles", C.c_int32)]
+
+
+class FdgsPipelineSlot(C.Structure):
+    _fields_ = [("d_ws", C.c_void_p), ("ws_bytes", C.c_size_t), ("max_entries", C.c_int64),
+                ("front_stream", C.c_void_p), ("blend_stream", C.c_void_p)]
+
+
+class FdgsFrameJob(C.Structure):
+    _fields_ = [("scene", FdgsScene), ("d_mask_l", C.c_void_p), ("d_mask_r", C.c_void_p), ("cam", FdgsCamera),
+                ("t", C.c_float), ("d_out_rgb", C.c_void_p), ("d_out_T", C.c_void_p), ("d_stats", C.c_void_p),
+                ("h_out_rgb", C.c_void_p), ("d_status", C.c_void_p), ("done_event", C.c_void_p)]
 
 
 class FdgsStvOpts(C.Structure):
@@ -110,6 +123,9 @@ def lib():
             "fdgs_stv_score": ([P, P, I32, P, I32, P, P, P, P, P, SZ, P, P], C.c_int),
             "fdgs_prune_workspace_bytes": ([I32], SZ),
             "fdgs_prune_mask": ([P, I32, C.c_int64, P, P, SZ, P], C.c_int),
+            "fdgs_pipeline_create": ([P, I32, P, I32, I32, P], C.c_int),
+            "fdgs_pipeline_render": ([P, P, I32, P, P], C.c_int),
+            "fdgs_pipeline_destroy": ([P], C.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import FdgsCamera, FdgsDebugViews, FdgsFrameStats, FdgsScene, check, lib
+from ._lib import FdgsCamera, FdgsDebugViews, FdgsFrameJob, FdgsFrameStats, FdgsPipelineSlot, FdgsScene, check, lib
 
 _FIELDS = ("mean", "scale", "rot_l", "rot_r", "opacity", "log255_opacity", "sh")
 
@@ -64,17 +64,21 @@ class Scene:
             self.t["sh_index"] = idx.to(device=dev, dtype=torch.uint16).contiguous()
             k = int(self.t["sh"].shape[0])
         self.struct = FdgsScene(self.n, *[self.t[f].data_ptr() for f in _FIELDS],
-                                self.t["sh_index"].data_ptr() if idx is not None else None, k, self.stride, None, 0)
+                                self.t["sh_index"].data_ptr() if idx is not None else None, k, self.stride, None, 0,
+                                None)
 
     def compact(self, mask_l: torch.Tensor, mask_r: torch.Tensor | None = None, stream=None,
-                standalone: bool = False) -> "Scene":
+                standalone: bool = False, sync: bool = True) -> "Scene":
         """fdgs_scene_compact: the working set of a key-frame window (the
         Gaussians of mask_l | mask_r, ascending) as a dense Scene whose records
         report the original indices.  Render it with no mask: frames equal the
-        masked renders of this scene bit for bit.  Synchronises once (count).
+        masked renders of this scene bit for bit.  sync=True reads the count
+        back (one synchronisation; `.n` is exact); sync=False keeps it on the
+        device (fdgs_scene.d_n: `.n` is the capacity, the render reads the
+        count itself -- no host synchronisation, bench.py's timed path).
         standalone: a new scene in its own right (a pruned scene: records,
         masks and scores index the kept Gaussians 0..m-1); `.kept` holds the
-        original indices either way."""
+        original indices either way (standalone implies sync)."""
         if self.struct.gid:
             raise ValueError("already a compacted working set")
         n, dev = self.n, self.device
@@ -96,10 +100,14 @@ class Scene:
             check(lib().fdgs_scene_compact(C.byref(self.struct), _ptr(mask_l), _ptr(mask_r), _ptr(params),
                                            _ptr(opacity), _ptr(L), _ptr(sh), _ptr(sh_index), _ptr(gid), _ptr(count),
                                            _ptr(ws), nb, _stream_ptr(st)))
-            host = torch.empty(1, dtype=torch.int32, pin_memory=True)
-            host.copy_(count, non_blocking=True)
-        st.synchronize()
-        m = int(host.item())
+            if sync or standalone:
+                host = torch.empty(1, dtype=torch.int32, pin_memory=True)
+                host.copy_(count, non_blocking=True)
+        if sync or standalone:
+            st.synchronize()
+            m = int(host.item())
+        else:
+            m = n  # capacity; the device count decides
         out = Scene.__new__(Scene)
         out.n, out.device, out.stride = m, dev, 4
         out.params = params
@@ -111,8 +119,10 @@ class Scene:
         out.struct = FdgsScene(m, *[out.t[f].data_ptr() for f in _FIELDS],
                                out.t["sh_index"].data_ptr() if vq else None,
                                int(self.t["sh"].shape[0]) if vq else 0, 4,
-                               None if standalone else gid.data_ptr(), 0 if standalone else n)
+                               None if standalone else gid.data_ptr(), 0 if standalone else n,
+                               None if (sync or standalone) else count.data_ptr())
         out.source = self
+        out.count = count  # DEVICE uint32 count (the exact size)
         out.kept = gid[:m]
         if standalone:
             del out.t["gid"]
@@ -351,11 +361,24 @@ class RenderPipeline:
     frame k on workspace k mod depth.  Each workspace has a high-priority
     front-end stream (preprocess, sorts, binning) and a low-priority blend
     stream (fdgs_render_split), so the latency-bound front end of later frames
-    is scheduled ahead of, and overlaps, the ALU-bound blends."""
+    is scheduled ahead of, and overlaps, the ALU-bound blends.
+
+    native (default, unless graphs): render_many submits the whole batch
+    through fdgs_pipeline_render -- one C call whose `threads` host threads
+    issue the frames' launches in parallel (the Python loop below remains for
+    graphs=True and as the reference path, native=False)."""
 
     def __init__(self, scene: Scene, width: int, height: int, depth: int = 4, max_entries: int | None = None,
-                 split: bool = True, copy_streams: int = 1, graphs: bool = False):
+                 split: bool = True, copy_streams: int = 1, graphs: bool = False, native: bool | None = None,
+                 threads: int | None = None):
         self.renderers = [Renderer(scene, width, height, max_entries) for _ in range(depth)]
+        self.native = (not graphs) if native is None else bool(native)
+        if self.native and graphs:
+            raise ValueError("the native batch submission launches streams, not graphs")
+        self.threads = int(threads) if threads else min(depth, 3)
+        self._handle = None
+        self._handle_key = None
+        self._frame_ev = []
         lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
         self.split = split
         self.graphs = graphs  # the front end as one CUDA-graph launch per frame, the blend launched after it
@@ -374,6 +397,70 @@ class RenderPipeline:
     @property
     def streams(self):
         return self.front + (self.blend or [])
+
+    def __del__(self):
+        try:
+            self._drop_handle()
+        except Exception:
+            pass
+
+    def _drop_handle(self):
+        if self._handle:
+            lib().fdgs_pipeline_destroy(self._handle)
+        self._handle = None
+
+    def _native_handle(self):
+        """fdgs_pipeline over the current workspaces (re-created when one grew)."""
+        key = tuple((r.ws.data_ptr(), r.ws_bytes, r.max_entries) for r in self.renderers)
+        if self._handle is None or key != self._handle_key:
+            self._drop_handle()
+            slots = (FdgsPipelineSlot * self.depth)()
+            for i, r in enumerate(self.renderers):
+                slots[i] = FdgsPipelineSlot(r.ws.data_ptr(), r.ws_bytes, r.max_entries, self.front[i].cuda_stream,
+                                            self.blend[i].cuda_stream if self.split else None)
+            cps = (C.c_void_p * len(self.copies))(*[c.cuda_stream for c in self.copies])
+            h = C.c_void_p()
+            check(lib().fdgs_pipeline_create(slots, self.depth, cps, len(self.copies), self.threads, C.byref(h)))
+            self._handle, self._handle_key = h, key
+        return self._handle
+
+    def _render_native(self, frames, outs, stats, stage_events, main, host_outs, status_out, frame_done):
+        n = len(frames)
+        jobs = (FdgsFrameJob * max(n, 1))()
+        if frame_done is not None:
+            while len(self._frame_ev) < n:
+                ev = torch.cuda.Event()
+                ev.record(main)  # materialise the CUDA event
+                self._frame_ev.append(ev)
+        for k, fr in enumerate(frames):
+            cam, t, ml, mr = fr[:4]
+            r = self.renderers[k % self.depth]
+            if cam.width != r.width or cam.height != r.height:
+                raise ValueError("camera size differs from the renderer's")
+            sc = r._scene_for(fr[4] if len(fr) > 4 else None, main)
+            pl, pr = r._masks(ml, mr, sc)
+            J = jobs[k]
+            J.scene = sc.struct
+            J.d_mask_l, J.d_mask_r = pl, pr
+            J.cam = cam if isinstance(cam, FdgsCamera) else camera_struct(cam)
+            J.t = float(t)
+            J.d_out_rgb = outs[k].data_ptr()
+            if stats is not None:
+                J.d_stats = stats[k].data_ptr()
+            if host_outs is not None:
+                J.h_out_rgb = host_outs[k].data_ptr()
+            if status_out is not None:
+                J.d_status = status_out[k].data_ptr()
+            if frame_done is not None:
+                J.done_event = self._frame_ev[k].cuda_event
+        evs = None
+        if stage_events is not None:
+            evs = (C.c_void_p * (5 * n))(*[e.cuda_event for row in stage_events[:n] for e in row])
+        check(lib().fdgs_pipeline_render(self._native_handle(), jobs, n, _stream_ptr(main), evs))
+        if frame_done is not None:
+            for k in range(n):
+                frame_done(k, outs[k], None, self._frame_ev[k])
+        return outs
 
     def counters_view(self, i: int) -> torch.Tensor:
         """The 16-byte counter block {n_act, n_vis, n_entries, status} at the head
@@ -416,10 +503,13 @@ class RenderPipeline:
         capacity and is undefined -- see render_many_checked).  Ordered after
         the current work of `stream` (default: current stream), and `stream`
         waits for every frame (and copy) before continuing.  frame_done
-        (optional): called as frame_done(k, outs[k], s) right after frame k is
-        enqueued, s the stream on which it completes (dist.FrameGather hooks
+        (optional): called as frame_done(k, outs[k], s, ev) after frame k is
+        enqueued: it completes where stream s is now, or (native submission)
+        when event ev completes (dist.FrameGather hooks
         the multi-GPU frame gather here).  Async."""
         main = stream or torch.cuda.current_stream()
+        if self.native:
+            return self._render_native(frames, outs, stats, stage_events, main, host_outs, status_out, frame_done)
         start = self.start_ev
         start.record(main)
         for s in self.streams:
@@ -458,7 +548,7 @@ class RenderPipeline:
                 with torch.cuda.stream(last):
                     status_out[k].copy_(self.counters_view(i), non_blocking=True)
             if frame_done is not None:
-                frame_done(k, outs[k], last)
+                frame_done(k, outs[k], last, None)
             if host_outs is not None:
                 fin = self.fin_ev[i]
                 fin.record(last)

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfdgs.so")
-SOURCES = ["render.cu", "aux.cu", "stv.cu", "api.cu"]
+SOURCES = ["render.cu", "aux.cu", "stv.cu", "api.cu", "pipeline.cu"]
 HEADERS = ["fdgs_device.cuh", "fdgs_internal.h", os.path.join("..", "..", "include", "fdgs.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]

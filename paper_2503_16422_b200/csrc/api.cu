@@ -24,6 +24,8 @@ static fdgs_status fail(fdgs_status s, const char *fmt, ...) {
     return s;
 }
 
+fdgs_status set_error(fdgs_status s, const char *msg) { return fail(s, "%s", msg); }
+
 static fdgs_status cuda_fail(cudaError_t e, const char *where) {
     return fail(FDGS_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
 }
@@ -169,6 +171,7 @@ SceneDev make_scenedev(const fdgs_scene &s) {
     d.sh_index = s.sh_index;
     d.sh_k = s.sh_index ? s.sh_codebook_size : 0;
     d.gid = s.gid;
+    d.d_n = s.d_n;
     return d;
 }
 
@@ -177,6 +180,8 @@ static int32_t layout_n(const fdgs_scene &s) { return std::max(s.n, s.n_capacity
 
 static fdgs_status check_scene(const fdgs_scene *s) {
     if (s == nullptr) return fail(FDGS_ERR_INVALID_ARG, "scene is NULL");
+    if (s->d_n != nullptr && s->gid == nullptr)
+        return fail(FDGS_ERR_INVALID_ARG, "a device count (d_n) is only allowed for a compacted working set (gid)");
     if (s->n < 0) return fail(FDGS_ERR_INVALID_ARG, "scene->n < 0");
     if (s->n == 0) return FDGS_OK;
     const void *p[] = {s->mean, s->scale, s->rot_l, s->rot_r, s->opacity, s->log255_opacity, s->sh};

@@ -60,6 +60,7 @@ struct SceneDev {
     const uint16_t *sh_index;  // VQ: codebook entry per Gaussian (nullable)
     int32_t sh_k;              // VQ codebook entries
     const uint32_t *gid;       // compacted working set: original index of Gaussian i (nullable)
+    const uint32_t *d_n;       // device count (nullable): Gaussians [0, min(*d_n, n)) are the scene
     __device__ __forceinline__ uint32_t orig(int i) const { return gid ? __ldg(gid + i) : (uint32_t)i; }
 };
 
@@ -82,6 +83,8 @@ struct RenderLayout {
     size_t tile_gbase, tile_start, row_start, row_hist, band_consts, item_pack, item_v, ekey0, ekey1, eval0, eval1, entries, total;
 };
 RenderLayout render_layout(int32_t n, int32_t width, int32_t height, int64_t max_entries);
+// Sets the calling thread's fdgs_last_error() message; returns s.
+fdgs_status set_error(fdgs_status s, const char *msg);
 
 bool make_camdev(const fdgs_camera &c, CamDev &out, const char **why);
 SceneDev make_scenedev(const fdgs_scene &s);

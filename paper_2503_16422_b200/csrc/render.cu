@@ -65,6 +65,9 @@ __global__ void __launch_bounds__(kPreBlock) k_cull(SceneDev sc, const uint32_t 
     __shared__ uint32_t s_act, s_n;
     const int tid = threadIdx.x, lane = tid & 31;
     const uint32_t part = blockIdx.x;
+    // the scene's Gaussians: n, or a device count (a working set compacted on the
+    // device); bits and counts are written for the whole capacity n
+    const int n = sc.d_n ? min((int)__ldg(sc.d_n), sc.n) : sc.n;
     if (tid == 0) s_act = s_n = 0;
     __syncthreads();
     uint32_t nact = 0, nsurv = 0;
@@ -72,7 +75,7 @@ __global__ void __launch_bounds__(kPreBlock) k_cull(SceneDev sc, const uint32_t 
     for (int r = 0; r < R; ++r) {
         const int i = (int)part * kCullItems + r * kPreBlock + tid;
         bool act = false, keep = false;
-        if (i < sc.n) {
+        if (i < n) {
             uint32_t w = 0xffffffffu;
             if (mask_l != nullptr) {
                 w = __ldg(mask_l + (i >> 5));

@@ -156,8 +156,9 @@ class FrameGather:
     Protocol, identical on every rank (all ranks render the same number of
     frames per step, in submission order):
       begin_step(n)            n frames follow in this step;
-      frame_done(k, out, st)   frame k's output `out` is complete once stream
-                               `st` reaches this point (None on CPU);
+      frame_done(k, out, st, ev) frame k's output `out` is complete once stream
+                               `st` reaches this point, or once event `ev`
+                               completes (None, None on CPU);
       end_step(main)           issues the last partial chunk and makes stream
                                `main` wait for every transfer of the step, so
                                a step's time includes its gather.
@@ -203,10 +204,14 @@ class FrameGather:
             self._events.append(torch.cuda.Event())
         return self._events[i]
 
-    def frame_done(self, k: int, out: torch.Tensor, stream=None):
+    def frame_done(self, k: int, out: torch.Tensor, stream=None, event=None):
+        """Frame k's output is complete once `stream` reaches this point, or
+        once `event` (already recorded) completes."""
         if self.world == 1:
             return
-        if self.cuda and stream is not None:
+        if self.cuda and event is not None:
+            self.stream.wait_event(event)
+        elif self.cuda and stream is not None:
             ev = self._event(len(self._pending))
             ev.record(stream)
             self.stream.wait_event(ev)

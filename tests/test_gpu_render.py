@@ -338,8 +338,9 @@ def test_render_pipeline_matches_sequential():
         frames.append((cams[fr % 4], float(times[fr]), masks[l], masks[r]))
     seq = fd.Renderer(sc, W, H)
     refs = [seq.render_checked(cam, t, ml, mr)[0] for (cam, t, ml, mr) in frames]
-    for split in (False, True):
-        pipe = fd.RenderPipeline(sc, W, H, depth=3, split=split)
+    for split, native, threads in ((False, False, 1), (True, False, 1), (False, True, 1), (True, True, 3),
+                                   (True, True, 2)):
+        pipe = fd.RenderPipeline(sc, W, H, depth=3, split=split, native=native, threads=threads)
         outs = [pipe.renderers[0].new_output() for _ in frames]
         pipe.render_many(frames, outs)
         pipe.render_many(frames[::-1], outs[::-1])   # reuse every workspace again
@@ -374,6 +375,36 @@ def test_interleaved_and_planar_parameters_identical():
     sa = fd.stv_score(a, cams, [0.2, 0.6])["score"]
     sb = fd.stv_score(b, cams, [0.2, 0.6])["score"]
     assert torch.equal(sa, sb)
+
+
+def test_native_pipeline_working_sets_without_host_sync():
+    """fdgs_pipeline_render with compacted working sets whose size stays on the
+    device (Scene.compact sync=False, fdgs_scene.d_n): the frames equal the
+    masked renders bit for bit, with stats and status copies."""
+    scene = fi.make_scene("c3", n=30_000, seed=8)
+    cams = fi.make_cameras("c3", width=300, height=200, fx=220.0, count=4)
+    sc = fd.Scene.from_arrays(scene)
+    kf = fd.keyframes(300, 20)
+    times = fi.frame_times(300)
+    masks = [fd.keyframe_mask(sc, cams, float(times[k])) for k in kf]
+    seq = fd.Renderer(sc, 300, 200)
+    frames, refs, wsets = [], [], {}
+    for fr in range(35, 65):
+        l, r = fd.bracket(kf, fr)
+        if (l, r) not in wsets:
+            wsets[(l, r)] = sc.compact(masks[l], masks[r], sync=False)
+            assert wsets[(l, r)].n == sc.n and wsets[(l, r)].struct.d_n
+        frames.append((cams[fr % 4], float(times[fr]), None, None, wsets[(l, r)]))
+        refs.append(seq.render_checked(cams[fr % 4], float(times[fr]), masks[l], masks[r])[0].clone())
+    pipe = fd.RenderPipeline(sc, 300, 200, depth=4, threads=2)
+    outs = [pipe.renderers[0].new_output() for _ in frames]
+    st = pipe.render_many_checked(frames, outs)
+    assert (st[:, 3] == 0).all()
+    for ref, o in zip(refs, outs):
+        assert torch.equal(ref, o)
+    m = wsets[(1, 2)]
+    exact = sc.compact(masks[1], masks[2])
+    assert int(m.count.item()) == exact.n and int(st[0, 0]) == exact.n
 
 
 def test_pipeline_overflow_detected_and_re_rendered():
