@@ -28,7 +28,8 @@ def test_bench_json_contract():
     assert abs(d["value"] - 20 / (d["ms_per_step"] / 1e3)) <= 0.01 * d["value"]
     assert "workload" in d["config"] and "l2" in d["config"]
     rl = d["roofline"]
-    assert rl["kernel"] == "k_blend_wi" and rl["bound"] == "alu" and rl["unit"] == "TFLOP/s"
+    assert rl["kernel"] == "k_blend_wi" and rl["bound"] == "alu" and rl["unit"] == "T lane-ops/s"
+    assert 0 < rl["flop_model"]["frac"] < 1
     assert 0 < rl["frac"] < 1 and abs(rl["frac"] - rl["achieved"] / rl["peak"]) < 1e-3
     assert rl["traffic"] is None or rl["traffic"] > 0
     e2e = d["e2e"]
