@@ -308,6 +308,14 @@ typedef struct {
 fdgs_status fdgs_render_debug_views(void *d_ws, size_t ws_bytes, int32_t n, int32_t width, int32_t height,
                                     int64_t max_entries, fdgs_debug_views *out);
 
+/* Tests/debug: the timed blend's record-to-strip culling decisions for the
+ * frame last rendered in the workspace (same layout arguments as
+ * fdgs_render_debug_views): bit w of d_out[k] (DEVICE uint8[E]) is set iff
+ * entry k's record is staged for warp strip w (pixel rows 4w..4w+3 of its
+ * tile) -- the device function k_blend_wi uses, replayed.  ASYNC. */
+fdgs_status fdgs_debug_strip_reach(void *d_ws, size_t ws_bytes, int32_t n, int32_t width, int32_t height,
+                                   int64_t max_entries, uint8_t *d_out, void *stream);
+
 /* Key-frame visibility mask (Sec. 4.2.2): bit i of d_out_mask is set
  * iff Gaussian i is visible at t_key from at least one of the n_cams HOST
  * cameras, "visible" = temporal & support & near & cover culls of the render

@@ -27,7 +27,7 @@ EXPORTS = [
     "fdgs_keyframe_mask_contrib_workspace_bytes", "fdgs_keyframe_mask_contrib",
     "fdgs_mask_compact_workspace_bytes", "fdgs_mask_compact", "fdgs_stv_workspace_bytes", "fdgs_stv_score",
     "fdgs_scene_compact_workspace_bytes", "fdgs_scene_compact", "fdgs_prune_workspace_bytes", "fdgs_prune_mask",
-    "fdgs_pipeline_create", "fdgs_pipeline_render", "fdgs_pipeline_destroy",
+    "fdgs_pipeline_create", "fdgs_pipeline_render", "fdgs_pipeline_destroy", "fdgs_debug_strip_reach",
 ]
 
 
@@ -126,6 +126,7 @@ def lib():
             "fdgs_pipeline_create": ([P, I32, P, I32, I32, P], C.c_int),
             "fdgs_pipeline_render": ([P, P, I32, P, P], C.c_int),
             "fdgs_pipeline_destroy": ([P], C.c_int),
+            "fdgs_debug_strip_reach": ([P, SZ, I32, I32, I32, I64, P, P], C.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

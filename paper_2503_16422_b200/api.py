@@ -351,6 +351,15 @@ class Renderer:
             n_tiles=v.n_tiles,
         )
 
+    def strip_reach(self) -> torch.Tensor:
+        """fdgs_debug_strip_reach: uint8[E] strip-culling bits of the last frame
+        (bit w: entry staged for warp strip w), entries in debug_views order."""
+        cnt = self.debug_views()["n_entries"]
+        out = torch.zeros(max(cnt, 1), dtype=torch.uint8, device=self.ws.device)
+        check(lib().fdgs_debug_strip_reach(_ptr(self.ws), self.ws_bytes, self._layout_n, self.width, self.height,
+                                           self.max_entries, _ptr(out), _stream_ptr(None)))
+        return out[:cnt]
+
     def _slice(self, ptr, base, nbytes):
         off = int(ptr) - base
         return self.ws[off:off + nbytes]

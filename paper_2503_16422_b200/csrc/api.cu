@@ -430,6 +430,16 @@ fdgs_status fdgs_render_debug_views(void *d_ws, size_t ws_bytes, int32_t n, int3
     return FDGS_OK;
 }
 
+fdgs_status fdgs_debug_strip_reach(void *d_ws, size_t ws_bytes, int32_t n, int32_t width, int32_t height,
+                                   int64_t max_entries, uint8_t *d_out, void *stream) {
+    if (d_ws == nullptr || d_out == nullptr || n < 0 || width < 1 || height < 1 || max_entries < 0)
+        return fail(FDGS_ERR_INVALID_ARG, "bad args");
+    const RenderLayout L = render_layout(n, width, height, max_entries);
+    if (ws_bytes < L.total) return fail(FDGS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
+    cudaError_t e = launch_debug_strip_reach(reinterpret_cast<char *>(d_ws), L, d_out, (cudaStream_t)stream);
+    return e == cudaSuccess ? FDGS_OK : cuda_fail(e, "fdgs_debug_strip_reach");
+}
+
 size_t fdgs_keyframe_workspace_bytes(int32_t n_cams) {
     return n_cams <= 0 ? 256 : align256(sizeof(CamDev) * (size_t)n_cams);
 }

@@ -131,6 +131,7 @@ RenderGraphImpl *render_graph_new();
 void render_graph_delete(RenderGraphImpl *g);
 const RenderLayout &render_graph_layout(const RenderGraphImpl &g);
 
+cudaError_t launch_debug_strip_reach(char *ws, const RenderLayout &L, uint8_t *out, cudaStream_t st);
 cudaError_t launch_keyframe(const SceneDev &sc, const CamDev *d_cams, int n_cams, float t, uint32_t *out,
                             cudaStream_t st);
 cudaError_t launch_mask_or(const uint32_t *a, const uint32_t *b, int n, uint32_t *out, cudaStream_t st);

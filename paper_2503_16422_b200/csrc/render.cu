@@ -1268,6 +1268,82 @@ static_assert(sizeof(WlEntry) == 16 + 16 * kWlRows, "WlEntry layout");
 #endif
 constexpr int kWlUnroll = FDGS_WL_UNROLL;
 constexpr float kStopU = 1e-4f / 255.0f;  // the stop threshold 1e-4 on T, on U = T / 255
+// Stage one record for warp strip `warp` (rows 4w..4w+3) of tile (tx, ty)
+// (k_blend_wi): the complemented pixel-AABB mask mb, the pinned e2 row terms
+// {b, mb, t1, t4} of the strip's rows (DESIGN.md §3 step 10), and whether the
+// record reaches the strip.  Reach: for some row of the strip inside the
+// AABB, the maximum over the tile ∩ AABB pixel-centre columns of the row's
+// quadratic x (A' x + t1) + t4 (the consumer's own chain, at the stationary
+// point clamped to the columns) is >= -margin, margin = 1e-3 |quadratic| +
+// 1e-3 over the tile ∩ AABB -- well above the rounding of this test and of the
+// pinned fp32 chain, so no pixel with e2 >= 0 is dropped (pure culling;
+// brute-force soundness test: tests/test_gpu_fullsize.py).  Explicit IEEE
+// intrinsics throughout, so every inlined copy takes the same decisions
+// (fdgs_debug_strip_reach replays it).
+__device__ __forceinline__ bool strip_stage(const float4 &r0, const float4 &r1, float b, int tx, int ty, int warp,
+                                            uint32_t &mb, float4 (&tr)[kWlRows]) {
+    const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
+    const uint32_t ax = __float_as_uint(r1.z), ay = __float_as_uint(r1.w);
+    const int x0 = max((int)(ax & 0xffff) - tx * 16, 0), x1 = min((int)(ax >> 16) - tx * 16, 15);
+    const int y0 = max((int)(ay & 0xffff) - ty * 16, 0);
+    const int y1 = x0 > x1 ? -1 : min((int)((ay >> 16) & 0x7fffu) - ty * 16, 15);
+    const uint32_t xm = ((2u << x1) - 1u) & ~((1u << x0) - 1u);
+    const uint32_t ym = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
+    mb = ~(xm | (ym << 16));
+    const float xl = __fsub_rn((float)(tx * 16 + x0) + 0.5f, u);
+    const float xr = __fsub_rn((float)(tx * 16 + x1) + 0.5f, u);
+    const float yl = __fsub_rn((float)(ty * 16 + y0) + 0.5f, v), yr = __fsub_rn((float)(ty * 16 + y1) + 0.5f, v);
+    const float X = fmaxf(fabsf(xl), fabsf(xr)), Y = fmaxf(fabsf(yl), fabsf(yr));
+    const float mag = __fadd_rn(__fadd_rn(__fmul_rn(__fmul_rn(fabsf(Ap), X), X), __fmul_rn(__fmul_rn(fabsf(Bp), X), Y)),
+                                __fmul_rn(__fmul_rn(fabsf(Cp), Y), Y));
+    const float marg = -__fmaf_rn(1e-3f, mag, 1e-3f);
+    const float hA = __fdividef(-0.5f, Ap);  // stationary point only
+    bool rw = false;
+#pragma unroll
+    for (int r = 0; r < kWlRows; ++r) {  // pinned e2 chain, row terms (DESIGN.md step 10)
+        const int row = wl_row0(warp) + r;
+        const float dy = __fsub_rn((float)(ty * 16 + row) + 0.5f, v);
+        const float t1 = __fmul_rn(Bp, dy);
+        const float t3 = __fmul_rn(Cp, dy);
+        const float t4 = __fmaf_rn(t3, dy, Q2);
+        const float xs = fminf(fmaxf(__fmul_rn(t1, hA), xl), xr);
+        rw |= row >= y0 && row <= y1 && __fmaf_rn(xs, __fmaf_rn(Ap, xs, t1), t4) >= marg;
+        tr[r] = make_float4(b, __uint_as_float(mb), t1, t4);
+    }
+    return rw;
+}
+
+// Tests: the strip-reach decisions of every entry of the frame last rendered
+// in the workspace (bit w of out[k]: entry k is staged for warp strip w).
+__global__ void __launch_bounds__(128) k_debug_strip_reach(const uint32_t *__restrict__ tile_start,
+                                                           const uint32_t *__restrict__ entries,
+                                                           const float4 *__restrict__ rec0,
+                                                           const float4 *__restrict__ rec1, const Counters *ctr,
+                                                           int tiles_x, uint8_t *__restrict__ out) {
+    if (ctr->status != FDGS_OK) return;
+    const int tile = blockIdx.x, tx = tile % tiles_x, ty = tile / tiles_x;
+    const uint32_t start = tile_start[tile], end = tile_start[tile + 1];
+    for (uint32_t k = start + threadIdx.x; k < end; k += blockDim.x) {
+        const uint32_t v = entries[k];
+        const float4 r0 = rec0[v], r1 = rec1[v];
+        uint32_t bits = 0, mb;
+        float4 tr[kWlRows];
+        for (int w = 0; w < 4; ++w)
+            if (strip_stage(r0, r1, 0.0f, tx, ty, w, mb, tr)) bits |= 1u << w;
+        out[k] = (uint8_t)bits;
+    }
+}
+
+cudaError_t launch_debug_strip_reach(char *ws, const RenderLayout &L, uint8_t *out, cudaStream_t st) {
+    k_debug_strip_reach<<<L.n_tiles, 128, 0, st>>>(reinterpret_cast<const uint32_t *>(ws + L.tile_start),
+                                                   reinterpret_cast<const uint32_t *>(ws + L.entries),
+                                                   reinterpret_cast<const float4 *>(ws + L.rec0),
+                                                   reinterpret_cast<const float4 *>(ws + L.rec1),
+                                                   reinterpret_cast<const Counters *>(ws + L.counters), L.tiles_x,
+                                                   out);
+    return cudaGetLastError();
+}
+
 // Warp-independent blend (the timed kernel): no producer warp and no barriers
 // between warps.  Each of the 4 warps of a tile block stages its own batches of
 // 32 records (one per lane: the gather, the AABB mask, the per-row reach test
@@ -1424,40 +1500,11 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
         fetch(base, r0, r1, r2);
 #endif
         // ---- stage this warp's list of the batch
-        const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
         const bool redundant = (__float_as_uint(r1.w) & 0x80000000u) != 0u;
         uint32_t mb = 0;
-        float xl = 0.f, xr = 0.f, hA = 0.f, marg = 0.f;
-        int y0 = 16, y1 = -1;
-        if (lane < n) {
-            const uint32_t ax = __float_as_uint(r1.z), ay = __float_as_uint(r1.w);
-            const int x0 = max((int)(ax & 0xffff) - tx * 16, 0), x1 = min((int)(ax >> 16) - tx * 16, 15);
-            y0 = max((int)(ay & 0xffff) - ty * 16, 0);
-            y1 = min((int)((ay >> 16) & 0x7fffu) - ty * 16, 15);
-            const uint32_t xm = ((2u << x1) - 1u) & ~((1u << x0) - 1u);
-            const uint32_t ym = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
-            mb = ~(xm | (ym << 16));
-            if (x0 > x1) y1 = -1;
-            xl = __fsub_rn((float)(tx * 16 + x0) + 0.5f, u);
-            xr = __fsub_rn((float)(tx * 16 + x1) + 0.5f, u);
-            const float yl = (float)(ty * 16 + y0) + 0.5f - v, yr = (float)(ty * 16 + y1) + 0.5f - v;
-            const float X = fmaxf(fabsf(xl), fabsf(xr)), Y = fmaxf(fabsf(yl), fabsf(yr));
-            marg = -(1e-3f * (fabsf(Ap) * X * X + fabsf(Bp) * X * Y + fabsf(Cp) * Y * Y) + 1e-3f);
-            hA = __fdividef(-0.5f, Ap);
-        }
         float4 tr[kWlRows];
-        bool rw = false;
-#pragma unroll
-        for (int r = 0; r < kWlRows; ++r) {  // pinned e2 chain, row terms (DESIGN.md step 10)
-            const int row = wl_row0(warp) + r;
-            const float dy = __fsub_rn((float)(ty * 16 + row) + 0.5f, v);
-            const float t1 = __fmul_rn(Bp, dy);
-            const float t3 = __fmul_rn(Cp, dy);
-            const float t4 = __fmaf_rn(t3, dy, Q2);
-            const float xs = fminf(fmaxf(t1 * hA, xl), xr);
-            rw |= row >= y0 && row <= y1 && fmaf(xs, fmaf(Ap, xs, t1), t4) >= marg;
-            tr[r] = make_float4(r2.z, __uint_as_float(mb), t1, t4);
-        }
+        const bool rw = strip_stage(r0, r1, r2.z, tx, ty, warp, mb, tr);
+        const float u = r0.x, Ap = r0.z;
         const bool reach = lane < n && rw;
         const uint32_t bal = __ballot_sync(0xffffffffu, reach);
         const bool masked = __any_sync(0xffffffffu, reach && !redundant && (mb & foot) != 0u);

@@ -1,0 +1,96 @@
+"""Interleaved A/B of frame-submission variants on the C3 bench workload (GPU box).
+
+One process builds the scene, the key-frame masks and the working sets once,
+then times each variant's steps (60 frames, device events, L2 flushed between
+steps) in rounds A B C A B C ..., so slow drifts and one-off stalls hit every
+variant alike; prints the median frames/s per variant and its host enqueue
+time per frame.
+
+    python tools/pipe_ab.py --rounds 5 --steps 6 py native:3 native:1 native:6
+"""
+import argparse
+import json
+import statistics
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import fdgs_inputs as fi  # noqa: E402
+import paper_2503_16422_b200 as fd  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("variants", nargs="+", help="py | native:T | graphs, optionally @depth (native:3@8)")
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--rounds", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--frames", type=int, default=60)
+    a = ap.parse_args()
+    cfg = fi.CONFIGS[a.config]
+    scene = fi.make_scene(a.config)
+    cams = fi.make_cameras(a.config)
+    F, D = cfg["frames"], cfg["keyframe_interval"]
+    times = fi.frame_times(F)
+    kf = fd.keyframes(F, D)
+    sc = fd.Scene.from_arrays(scene)
+    masks = [fd.keyframe_mask(sc, cams, float(times[k])) for k in kf]
+    cs = [fd.camera_struct(c) for c in cams]
+    seq = [(f, f // len(cams), f % len(cams)) for f in range(len(cams) * F)]
+    wsets = {}
+
+    def frame(x):
+        f, ti, ci = x
+        li, ri = fd.bracket(kf, ti)
+        if (li, ri) not in wsets:
+            wsets[(li, ri)] = sc.compact(masks[li], masks[ri], sync=False)
+        return cs[ci], float(times[ti]), None, None, wsets[(li, ri)]
+
+    flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    pipes = {}
+    for v in a.variants:
+        name, _, depth = v.partition("@")
+        depth = int(depth or 6)
+        kind, _, thr = name.partition(":")
+        pipes[v] = fd.RenderPipeline(sc, cams[0].width, cams[0].height, depth=depth, graphs=kind == "graphs",
+                                     native=kind == "native", threads=int(thr or 3))
+    outs = [pipes[a.variants[0]].renderers[0].new_output() for _ in range(a.frames)]
+    res = {v: [] for v in a.variants}
+    host = {v: [] for v in a.variants}
+    ptr = [0]
+
+    def step(p, timed):
+        fr = [seq[(ptr[0] + k) % len(seq)] for k in range(a.frames)]
+        ptr[0] += a.frames
+        jobs = [frame(x) for x in fr]
+        flush.zero_()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        h0 = time.perf_counter()
+        p.render_many(jobs, outs)
+        h = time.perf_counter() - h0
+        e.record()
+        e.synchronize()
+        return s.elapsed_time(e), h
+
+    for v in a.variants:  # warm every variant
+        for _ in range(2):
+            step(pipes[v], False)
+    for r in range(a.rounds):
+        for v in a.variants:
+            for _ in range(a.steps):
+                ms, h = step(pipes[v], True)
+                res[v].append(ms)
+                host[v].append(h * 1e3)
+    out = {v: {"fps_median": round(a.frames / (statistics.median(res[v]) / 1e3), 1),
+               "fps_mean": round(a.frames * len(res[v]) / (sum(res[v]) / 1e3), 1),
+               "host_ms_per_frame": round(statistics.median(host[v]) / a.frames, 4)} for v in a.variants}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
