@@ -24,7 +24,8 @@ import paper_2503_16422_b200 as fd  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("variants", nargs="+", help="py | native:T | graphs, optionally @depth (native:3@8)")
+    ap.add_argument("variants", nargs="+",
+                    help="py | native:T | graphs, optionally @depth and ~K front-end limit (native:3@6~3)")
     ap.add_argument("--config", default="c3")
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--steps", type=int, default=6)
@@ -52,11 +53,14 @@ def main():
     flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device="cuda")
     pipes = {}
     for v in a.variants:
-        name, _, depth = v.partition("@")
+        name, _, rest = v.partition("@")
+        depth, _, lim = rest.partition("~")
+        if "~" in name:
+            name, _, lim = name.partition("~")
         depth = int(depth or 6)
         kind, _, thr = name.partition(":")
         pipes[v] = fd.RenderPipeline(sc, cams[0].width, cams[0].height, depth=depth, graphs=kind == "graphs",
-                                     native=kind == "native", threads=int(thr or 3))
+                                     native=kind == "native", threads=int(thr or 3), front_limit=int(lim or 0))
     outs = [pipes[a.variants[0]].renderers[0].new_output() for _ in range(a.frames)]
     res = {v: [] for v in a.variants}
     host = {v: [] for v in a.variants}
