@@ -384,7 +384,7 @@ class RenderPipeline:
         self.native = (not graphs) if native is None else bool(native)
         if self.native and graphs:
             raise ValueError("the native batch submission launches streams, not graphs")
-        self.threads = int(threads) if threads else min(depth, 3)
+        self.threads = int(threads) if threads else min(depth, 4)
         self._handle = None
         self._handle_key = None
         self._frame_ev = []
