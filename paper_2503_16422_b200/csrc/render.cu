@@ -1281,7 +1281,7 @@ constexpr float kStopU = 1e-4f / 255.0f;  // the stop threshold 1e-4 on T, on U 
 // intrinsics throughout, so every inlined copy takes the same decisions
 // (fdgs_debug_strip_reach replays it).
 __device__ __forceinline__ bool strip_stage(const float4 &r0, const float4 &r1, float b, int tx, int ty, int warp,
-                                            uint32_t &mb, float4 (&tr)[kWlRows]) {
+                                            const float (&rowc)[kWlRows], uint32_t &mb, float4 (&tr)[kWlRows]) {
     const float u = r0.x, v = r0.y, Ap = r0.z, Bp = r0.w, Cp = r1.x, Q2 = r1.y;
     const uint32_t ax = __float_as_uint(r1.z), ay = __float_as_uint(r1.w);
     const int x0 = max((int)(ax & 0xffff) - tx * 16, 0), x1 = min((int)(ax >> 16) - tx * 16, 15);
@@ -1302,7 +1302,7 @@ __device__ __forceinline__ bool strip_stage(const float4 &r0, const float4 &r1, 
 #pragma unroll
     for (int r = 0; r < kWlRows; ++r) {  // pinned e2 chain, row terms (DESIGN.md step 10)
         const int row = wl_row0(warp) + r;
-        const float dy = __fsub_rn((float)(ty * 16 + row) + 0.5f, v);
+        const float dy = __fsub_rn(rowc[r], v);  // rowc[r] = pixel-centre y of the strip's row r
         const float t1 = __fmul_rn(Bp, dy);
         const float t3 = __fmul_rn(Cp, dy);
         const float t4 = __fmaf_rn(t3, dy, Q2);
@@ -1328,8 +1328,11 @@ __global__ void __launch_bounds__(128) k_debug_strip_reach(const uint32_t *__res
         const float4 r0 = rec0[v], r1 = rec1[v];
         uint32_t bits = 0, mb;
         float4 tr[kWlRows];
-        for (int w = 0; w < 4; ++w)
-            if (strip_stage(r0, r1, 0.0f, tx, ty, w, mb, tr)) bits |= 1u << w;
+        for (int w = 0; w < 4; ++w) {
+            float rowc[kWlRows];
+            for (int r = 0; r < kWlRows; ++r) rowc[r] = (float)(ty * 16 + wl_row0(w) + r) + 0.5f;
+            if (strip_stage(r0, r1, 0.0f, tx, ty, w, rowc, mb, tr)) bits |= 1u << w;
+        }
         out[k] = (uint8_t)bits;
     }
 }
@@ -1361,9 +1364,6 @@ cudaError_t launch_debug_strip_reach(char *ws, const RenderLayout &L, uint8_t *o
 #endif
 constexpr int kWiPairUnroll = FDGS_WI_PAIR_UNROLL;
 
-#ifndef FDGS_WI_PREFETCH
-#define FDGS_WI_PREFETCH 1
-#endif
 constexpr int kWiThreads = 128;
 __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uint32_t *__restrict__ tile_start,
                                                          const uint32_t *__restrict__ entries,
@@ -1480,30 +1480,28 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
             undo(Cr.y, Cg.y, Cb.y, T.y, thr.y, T0.y, T1.y, w1.y, w2.y);
         }
     };
+    // pixel-centre y of this warp's strip rows (per-warp constants)
+    float rowc[kWlRows];
+#pragma unroll
+    for (int r = 0; r < kWlRows; ++r) rowc[r] = (float)(ty * 16 + wl_row0(warp) + r) + 0.5f;
+    // gather a batch (warp-uniform bs < end): lanes past the tile's last entry
+    // re-load that entry (valid memory, culled by lane < n below) -- no zeroing
     auto fetch = [&](uint32_t bs, float4 &a0, float4 &a1, float4 &a2) {
-        a0 = a1 = a2 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (bs + lane < end) {
-            const uint32_t v = __ldg(entries + bs + lane);
-            a0 = __ldg(rec0 + v);
-            a1 = __ldg(rec1 + v);
-            a2 = __ldg(rec2 + v);
-        }
+        const uint32_t v = __ldg(entries + min(bs + lane, end - 1));
+        a0 = __ldg(rec0 + v);
+        a1 = __ldg(rec1 + v);
+        a2 = __ldg(rec2 + v);
     };
     bool wdone = __all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf);
     float4 r0, r1, r2;
-#if FDGS_WI_PREFETCH
-    fetch(start, r0, r1, r2);
-#endif
+    if (start < end) fetch(start, r0, r1, r2);
     for (uint32_t base = start; base < end && !wdone; base += 32) {
         const int n = (int)min(32u, end - base);
-#if !FDGS_WI_PREFETCH
-        fetch(base, r0, r1, r2);
-#endif
         // ---- stage this warp's list of the batch
         const bool redundant = (__float_as_uint(r1.w) & 0x80000000u) != 0u;
         uint32_t mb = 0;
         float4 tr[kWlRows];
-        const bool rw = strip_stage(r0, r1, r2.z, tx, ty, warp, mb, tr);
+        const bool rw = strip_stage(r0, r1, r2.z, tx, ty, warp, rowc, mb, tr);
         const float u = r0.x, Ap = r0.z;
         const bool reach = lane < n && rw;
         const uint32_t bal = __ballot_sync(0xffffffffu, reach);
@@ -1515,10 +1513,8 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
 #pragma unroll
             for (int r = 0; r < kWlRows; ++r) E.t[r] = tr[r];
         }
-#if FDGS_WI_PREFETCH
         // ---- gather the next batch while this one is composited
-        fetch(base + 32, r0, r1, r2);
-#endif
+        if (base + 32 < end) fetch(base + 32, r0, r1, r2);
         __syncwarp();
         const int cnt = __popc(bal);
         if (masked) {

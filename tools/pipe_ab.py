@@ -20,12 +20,29 @@ import torch
 sys.path.insert(0, ".")
 import fdgs_inputs as fi  # noqa: E402
 import paper_2503_16422_b200 as fd  # noqa: E402
+from paper_2503_16422_b200 import _lib  # noqa: E402
+
+_LIBS = {}
+
+
+def use_lib(name):
+    """Route the binding to tools/variants/libfdgs_<name>.so ('' = the in-tree
+    build): every variant library is loaded once, side by side."""
+    if name not in _LIBS:
+        saved_path, saved = _lib.LIB_PATH, _lib._lib
+        _lib._lib = None
+        if name:
+            _lib.LIB_PATH = f"tools/variants/libfdgs_{name}.so"
+        _LIBS[name] = _lib.lib()
+        _lib.LIB_PATH, _lib._lib = saved_path, saved
+    _lib._lib = _LIBS[name]
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("variants", nargs="+",
-                    help="py | native:T | graphs, optionally @depth and ~K front-end limit (native:3@6~3)")
+                    help="py | native:T | graphs, optionally @depth, ~K front-end limit, #lib variant "
+                         "(native:3@6~3#sleep200)")
     ap.add_argument("--config", default="c3")
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--steps", type=int, default=6)
@@ -37,6 +54,7 @@ def main():
     F, D = cfg["frames"], cfg["keyframe_interval"]
     times = fi.frame_times(F)
     kf = fd.keyframes(F, D)
+    use_lib("")
     sc = fd.Scene.from_arrays(scene)
     masks = [fd.keyframe_mask(sc, cams, float(times[k])) for k in kf]
     cs = [fd.camera_struct(c) for c in cams]
@@ -52,8 +70,13 @@ def main():
 
     flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device="cuda")
     pipes = {}
+    use_lib("")
+    libs = {}
     for v in a.variants:
-        name, _, rest = v.partition("@")
+        spec, _, libname = v.partition("#")
+        libs[v] = libname
+        use_lib(libname)
+        name, _, rest = spec.partition("@")
         depth, _, lim = rest.partition("~")
         if "~" in name:
             name, _, lim = name.partition("~")
@@ -82,10 +105,12 @@ def main():
         return s.elapsed_time(e), h
 
     for v in a.variants:  # warm every variant
+        use_lib(libs[v])
         for _ in range(2):
             step(pipes[v], False)
     for r in range(a.rounds):
         for v in a.variants:
+            use_lib(libs[v])
             for _ in range(a.steps):
                 ms, h = step(pipes[v], True)
                 res[v].append(ms)
