@@ -1317,12 +1317,7 @@ __device__ __forceinline__ bool strip_stage(const float4 &r0, const float4 &r1, 
     return rw;
 }
 
-// The timed blend: k_blend_q (2x2 pixels per thread, 8-row strips) or k_blend_wi
-// (2x1 pixels per thread, 4-row strips).
-#ifndef FDGS_BLEND_QUAD
-#define FDGS_BLEND_QUAD 1
-#endif
-constexpr int kBlendRows = FDGS_BLEND_QUAD ? 8 : 4;
+constexpr int kBlendRows = kWlRows;  // strip height of the timed blend (k_blend_wi)
 
 // Tests: the strip-reach decisions of every entry of the frame last rendered
 // in the workspace (bit w of out[k]: entry k is staged for warp strip w).
@@ -1564,167 +1559,6 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
 }
 
 
-// Quad blend (the timed kernel when FDGS_BLEND_QUAD): two warps per 16x16
-// tile, warp w owning the 8-row strip 8w..8w+7 and each thread a 2x2 pixel
-// quad (columns 2c, 2c+1 of rows 2r, 2r+1 of the strip).  Per record a thread
-// reads the common {u, A', r, g} and its two rows' {b, ~AABB mask, t1, t4}
-// (three 16-byte shared loads for four pixels) and evaluates the pinned e2
-// chain, alpha and the composite in packed fp32x2 -- the same arithmetic per
-// pixel as k_blend_wi, with the list loads, the row-term staging and the stop
-// test shared by four pixels instead of two.  Staging (strip_stage<8>) and
-// the U = T/255 carrying as in k_blend_wi; one stop test per record.
-constexpr int kQRows = 8, kQThreads = 64;
-struct QEntry {
-    float4 a;            // u, A', r, g
-    float4 t[kQRows];    // per row of the strip: b, ~AABB mask bits, t1, t4
-};
-static_assert(sizeof(QEntry) == 16 + 16 * kQRows, "QEntry layout");
-#ifndef FDGS_Q_MINB
-#define FDGS_Q_MINB 12
-#endif
-#ifndef FDGS_Q_UNROLL
-#define FDGS_Q_UNROLL 2
-#endif
-constexpr int kQUnroll = FDGS_Q_UNROLL;
-__global__ void __launch_bounds__(kQThreads, FDGS_Q_MINB) k_blend_q(const uint32_t *__restrict__ tile_start,
-                                                                   const uint32_t *__restrict__ entries,
-                                                                   const float4 *__restrict__ rec0,
-                                                                   const float4 *__restrict__ rec1,
-                                                                   const float4 *__restrict__ rec2,
-                                                                   const Counters *ctr, int tiles_x, int width,
-                                                                   int height, float bg0, float bg1, float bg2,
-                                                                   float *__restrict__ out_rgb,
-                                                                   float *__restrict__ out_T) {
-    __shared__ QEntry s_list[2][32];
-    const bool ok = ctr->status == FDGS_OK;
-    const int tile = blockIdx.x, tx = tile % tiles_x, ty = tile / tiles_x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t start = __ldg(tile_start + tile), end = ok ? __ldg(tile_start + tile + 1) : start;
-    const int cp = lane & 7, rp = lane >> 3;                  // column pair, row pair of the strip
-    const int lx = 2 * cp, ly = kQRows * warp + 2 * rp;       // the quad's top-left pixel in the tile
-    const int i0 = tx * 16 + lx, j0 = ty * 16 + ly;
-    const bool in00 = i0 < width && j0 < height, in10 = i0 + 1 < width && j0 < height;
-    const bool in01 = i0 < width && j0 + 1 < height, in11 = i0 + 1 < width && j0 + 1 < height;
-    float2 px = make_float2((float)i0 + 0.5f, (float)(i0 + 1) + 0.5f);
-    const uint32_t pa0 = (1u << lx) | (1u << (16 + ly)), pa1 = (2u << lx) | (1u << (16 + ly));
-    const uint32_t pb0 = (1u << lx) | (2u << (16 + ly)), pb1 = (2u << lx) | (2u << (16 + ly));
-    const float kInf = __int_as_float(0x7f800000);
-    float2 tha = make_float2(in00 ? 0.0f : kInf, in10 ? 0.0f : kInf);  // row a (2rp), row b (2rp + 1)
-    float2 thb = make_float2(in01 ? 0.0f : kInf, in11 ? 0.0f : kInf);
-    float2 Ta = make_float2(kInv255, kInv255), Tb = Ta;
-    float2 Cra = make_float2(0.f, 0.f), Cga = Cra, Cba = Cra, Crb = Cra, Cgb = Cra, Cbb = Cra;
-    const uint32_t foot = 0xffffu | (0xffu << (16 + kQRows * warp));
-    // one record for the quad; kAabb: apply the per-pixel AABB test
-    auto step = [&](int q, auto kAabb) {
-        const float4 a = s_list[warp][q].a;
-        const float4 ra = s_list[warp][q].t[2 * rp];
-        const float4 rb = s_list[warp][q].t[2 * rp + 1];
-        asm volatile("" : "+f"(px.x), "+f"(px.y));
-        const float2 dx = sub2(px, make_float2(a.x, a.x));
-        const float2 e2a = fma2(dx, fma2(make_float2(a.y, a.y), dx, make_float2(ra.z, ra.z)), make_float2(ra.w, ra.w));
-        const float2 e2b = fma2(dx, fma2(make_float2(a.y, a.y), dx, make_float2(rb.z, rb.z)), make_float2(rb.w, rb.w));
-        bool va0 = e2a.x >= tha.x, va1 = e2a.y >= tha.y, vb0 = e2b.x >= thb.x, vb1 = e2b.y >= thb.y;
-        if constexpr (decltype(kAabb)::value) {
-            const uint32_t ma = __float_as_uint(ra.y), mbb = __float_as_uint(rb.y);
-            va0 = va0 && (ma & pa0) == 0u;
-            va1 = va1 && (ma & pa1) == 0u;
-            vb0 = vb0 && (mbb & pb0) == 0u;
-            vb1 = vb1 && (mbb & pb1) == 0u;
-        }
-        const float ma0 = va0 ? fminf(ex2_approx(e2a.x), kAlphaPre) : 0.0f;
-        const float ma1 = va1 ? fminf(ex2_approx(e2a.y), kAlphaPre) : 0.0f;
-        const float mb0 = vb0 ? fminf(ex2_approx(e2b.x), kAlphaPre) : 0.0f;
-        const float mb1 = vb1 ? fminf(ex2_approx(e2b.y), kAlphaPre) : 0.0f;
-        const float2 wa = mul2(make_float2(ma0, ma1), Ta), wb = mul2(make_float2(mb0, mb1), Tb);
-        const float2 Tpa = Ta, Tpb = Tb;
-        Ta = fma2(make_float2(-kInv255, -kInv255), wa, Ta);
-        Tb = fma2(make_float2(-kInv255, -kInv255), wb, Tb);
-        Cra = fma2(make_float2(a.z, a.z), wa, Cra);
-        Cga = fma2(make_float2(a.w, a.w), wa, Cga);
-        Cba = fma2(make_float2(ra.x, ra.x), wa, Cba);
-        Crb = fma2(make_float2(a.z, a.z), wb, Crb);
-        Cgb = fma2(make_float2(a.w, a.w), wb, Cgb);
-        Cbb = fma2(make_float2(rb.x, rb.x), wb, Cbb);
-        // U >= kStopU holds before every step (a stop restores it): only a
-        // blended record can bring a pixel below the threshold
-        if (__builtin_expect(fminf(fminf(Ta.x, Ta.y), fminf(Tb.x, Tb.y)) < kStopU, 0)) {
-            auto undo = [&](float &cr, float &cg, float &cb, float &t, float &th, float tp, float w, float b) {
-                if (!(t < kStopU)) return;
-                cr = fmaf(-a.z, w, cr);
-                cg = fmaf(-a.w, w, cg);
-                cb = fmaf(-b, w, cb);
-                t = tp;
-                th = __int_as_float(0x7f800000);
-            };
-            undo(Cra.x, Cga.x, Cba.x, Ta.x, tha.x, Tpa.x, wa.x, ra.x);
-            undo(Cra.y, Cga.y, Cba.y, Ta.y, tha.y, Tpa.y, wa.y, ra.x);
-            undo(Crb.x, Cgb.x, Cbb.x, Tb.x, thb.x, Tpb.x, wb.x, rb.x);
-            undo(Crb.y, Cgb.y, Cbb.y, Tb.y, thb.y, Tpb.y, wb.y, rb.x);
-        }
-    };
-    float rowc[kQRows];  // pixel-centre y of the strip's rows
-#pragma unroll
-    for (int r = 0; r < kQRows; ++r) rowc[r] = (float)(ty * 16 + kQRows * warp + r) + 0.5f;
-    auto fetch = [&](uint32_t bs, float4 &a0, float4 &a1, float4 &a2) {
-        const uint32_t v = __ldg(entries + min(bs + lane, end - 1));
-        a0 = __ldg(rec0 + v);
-        a1 = __ldg(rec1 + v);
-        a2 = __ldg(rec2 + v);
-    };
-    auto all_done = [&] {
-        return __all_sync(0xffffffffu, tha.x == kInf && tha.y == kInf && thb.x == kInf && thb.y == kInf);
-    };
-    bool wdone = all_done();
-    float4 r0, r1, r2;
-    if (start < end) fetch(start, r0, r1, r2);
-    for (uint32_t base = start; base < end && !wdone; base += 32) {
-        const int n = (int)min(32u, end - base);
-        // ---- stage this warp's list of the batch
-        const bool redundant = (__float_as_uint(r1.w) & 0x80000000u) != 0u;
-        uint32_t mb = 0;
-        float t1s[kQRows], t4s[kQRows];
-        const bool rw = strip_stage<kQRows>(r0, r1, r2.z, tx, ty, kQRows * warp, rowc, mb, t1s, t4s);
-        const bool reach = lane < n && rw;
-        const uint32_t bal = __ballot_sync(0xffffffffu, reach);
-        const bool masked = __any_sync(0xffffffffu, reach && !redundant && (mb & foot) != 0u);
-        __syncwarp();  // the previous list has been read
-        if (reach) {
-            QEntry &E = s_list[warp][__popc(bal & lanemask_lt())];
-            E.a = make_float4(r0.x, r0.z, r2.x, r2.y);
-#pragma unroll
-            for (int r = 0; r < kQRows; ++r) E.t[r] = make_float4(r2.z, __uint_as_float(mb), t1s[r], t4s[r]);
-        }
-        // ---- gather the next batch while this one is composited
-        if (base + 32 < end) fetch(base + 32, r0, r1, r2);
-        __syncwarp();
-        const int cnt = __popc(bal);
-        if (masked) {
-#pragma unroll kQUnroll
-            for (int q = 0; q < cnt; ++q) step(q, std::true_type{});
-        } else {
-#pragma unroll kQUnroll
-            for (int q = 0; q < cnt; ++q) step(q, std::false_type{});
-        }
-        wdone = all_done();
-    }
-    Ta = mul2(Ta, make_float2(255.0f, 255.0f));
-    Tb = mul2(Tb, make_float2(255.0f, 255.0f));
-    if (ok && out_rgb != nullptr) {
-        const size_t hw = (size_t)width * height, p = (size_t)j0 * width + i0;
-        auto put = [&](bool in, size_t o, float T, float cr, float cg, float cb) {
-            if (!in) return;
-            out_rgb[o] = fmaf(T, bg0, cr);
-            out_rgb[hw + o] = fmaf(T, bg1, cg);
-            out_rgb[2 * hw + o] = fmaf(T, bg2, cb);
-            if (out_T) out_T[o] = T;
-        };
-        put(in00, p, Ta.x, Cra.x, Cga.x, Cba.x);
-        put(in10, p + 1, Ta.y, Cra.y, Cga.y, Cba.y);
-        put(in01, p + width, Tb.x, Crb.x, Cgb.x, Cbb.x);
-        put(in11, p + width + 1, Tb.y, Crb.y, Cgb.y, Cbb.y);
-    }
-}
-
 // ---------------------------------------------------------------- launcher
 // Grid shapes of the front end (compile-time; DESIGN.md "Thin front-end
 // kernels"): persistent onesweep grids on FDGS_PGRID blocks per SM divided by
@@ -1748,13 +1582,8 @@ static int sort_grid(int p_sort) { return std::max(1, FDGS_PGRID * p_sort / FDGS
 static void launch_timed_blend(const uint32_t *tstart, const uint32_t *entries, const float4 *rec0,
                                const float4 *rec1, const float4 *rec2, const Counters *ctr, const RenderLayout &L,
                                const CamDev &cam, float *out_rgb, float *out_T, cudaStream_t st) {
-#if FDGS_BLEND_QUAD
-    k_blend_q<<<L.n_tiles, kQThreads, 0, st>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width, L.height,
-                                               cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
-#else
     k_blend_wi<<<L.n_tiles, kWiThreads, 0, st>>>(tstart, entries, rec0, rec1, rec2, ctr, L.tiles_x, L.width,
                                                  L.height, cam.bg[0], cam.bg[1], cam.bg[2], out_rgb, out_T);
-#endif
 }
 
 cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint32_t *mask_r, const CamDev &cam,
