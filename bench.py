@@ -44,6 +44,7 @@ N_FRAMES_T = 300
 INTERVAL = 20
 MASKED = True
 WORKLOADS = {
+    "c1": "c1: tiny 1000 4D Gaussians, 64x64, 1 camera x 4 t, no key-frame filter",
     "c2": "c2: D-NeRF-shaped 100k 4D Gaussians, 800x800, 50 cams x 150 t, key-frame interval 10",
     "c3": "c3: N3V-shaped 200k 4D Gaussians, 1352x1014, 20 cams x 300 t, key-frame interval 20",
     "c4": "c4: N3V-shaped 3M 4D Gaussians (vanilla-4DGS scale), 1352x1014, 20 cams x 300 t, key-frame interval 20",
@@ -51,15 +52,16 @@ WORKLOADS = {
 
 
 def apply_config(args):
-    """BASELINE configs[1..3]; c3 is the metric's named workload (the default)."""
+    """BASELINE configs[0..3]; c3 is the metric's named workload (the default);
+    c1 (configs[0], the tiny oracle-sized case) has no key-frame filter."""
     global CONFIG, N_CAMS, N_FRAMES_T, INTERVAL, MASKED, METRIC
     import fdgs_inputs as fi
     CONFIG = args.config
     cfg = fi.CONFIGS[CONFIG]
-    N_CAMS = {"hemisphere50": 50, "arc20": 20}[cfg["rig"]]
+    N_CAMS = {"hemisphere50": 50, "arc20": 20, "c1": 1}[cfg["rig"]]
     N_FRAMES_T = cfg["frames"]
     INTERVAL = cfg["keyframe_interval"]
-    MASKED = not args.unmasked
+    MASKED = not args.unmasked and INTERVAL is not None
     if CONFIG != "c3" or not MASKED or args.vq:
         METRIC = (f"frames/sec at {cfg['width']}x{cfg['height']} ({CONFIG}, "
                   f"{'masked' if MASKED else 'unmasked'}{f', VQ-SH K={args.vq}' if args.vq else ''})")
@@ -84,7 +86,7 @@ def parse():
     p.add_argument("--submit-threads", type=int, default=4, help="host threads of fdgs_pipeline_render")
     p.add_argument("--sync-compact", action="store_true",
                    help="read each working set's size back to the host (Scene.compact sync=True)")
-    p.add_argument("--config", choices=["c2", "c3", "c4"], default="c3")
+    p.add_argument("--config", choices=["c1", "c2", "c3", "c4"], default="c3")
     p.add_argument("--unmasked", action="store_true", help="render without the key-frame filter")
     p.add_argument("--literal-masks", action="store_true",
                    help="key-frame masks from the Eq. 2 blending weights (P:282 literal, R3b) instead of the "
@@ -180,20 +182,34 @@ def load_traffic():
         return {}
 
 
-def oracle_masks(scene, cams):
-    """(key-frame indices, masks) from the oracle itself: the CPU
-    legs take no input from the CUDA path."""
-    import oracle
-    import fdgs_inputs as fi
-    times = fi.frame_times(N_FRAMES_T)
-    kf = oracle.keyframes(N_FRAMES_T, INTERVAL)
-    return kf, np.stack([oracle.keyframe_mask(scene, cams, times[k]) for k in kf])
+class OracleMasks:
+    """Key-frame masks from the oracle itself, built on first use:
+    the CPU legs take no input from the CUDA path."""
+
+    def __init__(self, scene, cams):
+        import oracle
+        import fdgs_inputs as fi
+        self.scene, self.cams = scene, cams
+        self.times = fi.frame_times(N_FRAMES_T)
+        self.kf = oracle.keyframes(N_FRAMES_T, INTERVAL)
+        self.rows = {}
+
+    def active(self, ti):
+        import oracle
+        l, r = oracle.bracket(self.kf, ti)
+        for k in (l, r):
+            if k not in self.rows:
+                self.rows[k] = oracle.keyframe_mask(self.scene, self.cams, self.times[self.kf[k]])
+        full = np.zeros((len(self.kf), self.rows[l].shape[0]), np.uint32)
+        full[l], full[r] = self.rows[l], self.rows[r]
+        return oracle.active_mask(full, self.kf, ti)  # the oracle's own bracketing and OR
 
 
-def cpu_oracle_run(scene, cams, masks, kf, frames, seconds, row_stride=8, threads=None):
+def cpu_oracle_run(scene, cams, masks, frames, seconds, row_stride=8, threads=None):
     """Time the oracle as it stands on bounded samples: rows j = 0 mod row_stride
     of consecutive frames until `seconds` elapse.  Returns (frames/s, info).
-    masks / kf: the oracle's own (oracle_masks), None = unmasked."""
+    masks: the oracle's own (OracleMasks; built outside the timed loop), None =
+    unmasked."""
     import oracle  # the oracle's own schedule, bracketing and mask OR (P:280-285)
     import fdgs_inputs as fi
 
@@ -206,12 +222,19 @@ def cpu_oracle_run(scene, cams, masks, kf, frames, seconds, row_stride=8, thread
     prev = oracle.num_threads()
     if threads:
         oracle.set_num_threads(threads)
+    acts = {}
+    if masks is not None:  # the sampled frames' active masks, built before the timed loop
+        for x in frames[:400]:
+            if x[1] not in acts and len(acts) < 6:
+                acts[x[1]] = masks.active(x[1])
     t0 = time.perf_counter()
     while True:
         f, ti, ci = frames[k % len(frames)]
         act = None
         if masks is not None:
-            act = oracle.active_mask(masks, kf, ti)
+            if ti not in acts:
+                acts[ti] = masks.active(ti)
+            act = acts[ti]
         r = oracle.render(scene, cams[ci], float(times[ti]), mask=act, pixels=pix)
         done_px += pix.size
         n_pairs += r["stats"]["evaluated"]
@@ -298,7 +321,7 @@ def run_ours(args):
     W, H = (8, 6) if fake else (cams[0].width, cams[0].height)
     cam_structs = None if fake else [fd.camera_struct(c) for c in cams]
     times = fi.frame_times(N_FRAMES_T)
-    kf = fd.keyframes(N_FRAMES_T, INTERVAL)
+    kf = fd.keyframes(N_FRAMES_T, INTERVAL or N_FRAMES_T)
     bracket = fd.bracket
     # ---- key-frame masks: key-frame k built by rank k mod N, all-reduced (disjoint rows)
     words = (n + 31) // 32
@@ -678,14 +701,13 @@ def run_ours(args):
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        okf, omasks = oracle_masks(arrays, cams) if MASKED else (None, None)
-        fps, info = cpu_oracle_run(arrays, cams, omasks, okf, mine, args.cpu_seconds)
+        omasks = OracleMasks(arrays, cams) if MASKED else None
+        fps, info = cpu_oracle_run(arrays, cams, omasks, mine, args.cpu_seconds)
         res["cpu_baseline"] = {"value": round(fps, 5), "unit": UNIT, "cores": info["cores"], "kind": "oracle",
                                "sample": info["sample"], "ns_per_evaluated_pair": info["ns_per_evaluated_pair"],
                                "core_ns_per_evaluated_pair": info["core_ns_per_evaluated_pair"]}
         if args.cpu_single_core:
-            fps1, info1 = cpu_oracle_run(arrays, cams, omasks, okf, mine, args.cpu_seconds, row_stride=64,
-                                         threads=1)
+            fps1, info1 = cpu_oracle_run(arrays, cams, omasks, mine, args.cpu_seconds, row_stride=64, threads=1)
             res["cpu_baseline"]["single_core"] = {"value": round(fps1, 6), "cores": 1, "sample": info1["sample"],
                                                   "ns_per_evaluated_pair": info1["ns_per_evaluated_pair"]}
     fdist.shutdown()
@@ -706,22 +728,22 @@ def run_reference(args):
     scene = fi.make_scene(CONFIG)
     cams = fi.make_cameras(CONFIG)
     times = fi.frame_times(N_FRAMES_T)
-    kf, masks = oracle_masks(scene, cams)  # the oracle's schedule and masks (no product code on this arm)
+    masks = OracleMasks(scene, cams) if MASKED else None  # the oracle's own schedule and masks
     seq = sequence()
     per_step = max(1.0, 60.0 / max(1, args.steps + args.warmup))
     vals = []
     info = None
     for s in range(args.warmup + args.steps):
         frames = seq[(s * 7) % len(seq):] + seq
-        fps, info = cpu_oracle_run(scene, cams, masks, kf, frames, per_step, row_stride=16)
+        fps, info = cpu_oracle_run(scene, cams, masks, frames, per_step, row_stride=16)
         if s >= args.warmup:
             vals.append(fps)
     value = float(np.mean(vals))
     res = dict(metric=METRIC, value=round(value, 5), unit=UNIT, n_gpus=world, steps=args.steps,
                warmup=args.warmup, ms_per_step=round(per_step * 1e3, 1), higher_is_better=True, scaling="weak",
                vs_baseline=None, dtype="f64", data="synthetic", impl="reference",
-               config={"workload": "c3: N3V-shaped 200k 4D Gaussians, 1352x1014, masked; each step a bounded "
-                                   "row sample (rows j%16==0) of consecutive frames"},
+               config={"workload": WORKLOADS[CONFIG] + (", masked" if MASKED else ", unmasked")
+                                   + "; each step a bounded row sample (rows j%16==0) of consecutive frames"},
                cpu_baseline={"value": round(value, 5), "unit": UNIT, "kind": "oracle", "cores": info["cores"],
                              "sample": info["sample"]},
                e2e={"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
