@@ -84,8 +84,6 @@ def parse():
     p.add_argument("--py-submit", action="store_true",
                    help="submit frames from the Python loop (one C call per frame) instead of fdgs_pipeline_render")
     p.add_argument("--submit-threads", type=int, default=4, help="host threads of fdgs_pipeline_render")
-    p.add_argument("--max-lead", type=int, default=0,
-                   help="fdgs_pipeline_render: issue frame k once frame k - W has completed (0: unbounded)")
     p.add_argument("--sync-compact", action="store_true",
                    help="read each working set's size back to the host (Scene.compact sync=True)")
     p.add_argument("--config", choices=["c1", "c2", "c3", "c4"], default="c3")
@@ -353,7 +351,7 @@ def run_ours(args):
     else:
         pipe = fd.RenderPipeline(scene, W, H, depth=args.streams, split=not args.no_split, graphs=args.graphs,
                                  native=False if (args.py_submit or args.graphs) else None,
-                                 threads=args.submit_threads, max_lead=args.max_lead)
+                                 threads=args.submit_threads)
         renderer = pipe.renderers[0]
         outs = [renderer.new_output() for _ in range(F)]
         stats = torch.zeros((F, 4), dtype=torch.int64, device=dev)  # fdgs_frame_stats is 32 bytes

@@ -11,12 +11,10 @@
 // frames are issued in order by one thread, so stream order alone orders
 // their work; threads share only the copy streams (independent copies).
 #include <algorithm>
-#include <atomic>
 #include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
-#include <memory>
 #include <mutex>
 #include <new>
 #include <thread>
@@ -33,9 +31,7 @@ struct fdgs_pipeline {
     std::vector<cudaStream_t> copies;
     std::vector<cudaEvent_t> done_ev, fin_ev, split_ev, join_ev;  // per slot (join: per stream)
     cudaEvent_t start_ev = nullptr;
-    int max_lead = 0;  // > 0: frame k is issued once frame k - max_lead has completed on the device
-    std::vector<cudaEvent_t> lead_ev;                 // ring: completion of frame k at k mod size
-    std::unique_ptr<std::atomic<int64_t>[]> lead_tag;  // frame whose event the ring slot holds
+    int front_limit = 0;  // > 0: at most this many frames' front ends in flight
     // worker pool
     int n_threads = 1;
     std::vector<std::thread> workers;
@@ -85,15 +81,14 @@ fdgs_status submit(fdgs_pipeline *p, int w, int nw) {
             if ((e = cudaEventRecord(p->done_ev[s], last)) != cudaSuccess) return cuda_status(e, "record");
             if ((e = cudaStreamWaitEvent(front, p->done_ev[s], 0)) != cudaSuccess) return cuda_status(e, "wait");
         }
-        if (p->max_lead > 0 && k >= p->max_lead) {
-            // bounded lead: issue frame k only once frame k - W has completed on
-            // the device, so the streams never hold more than ~W frames of queued
-            // work (a deeper queue measurably slows the device's scheduling of
-            // the 12 streams)
-            const int64_t m = k - p->max_lead;
-            const size_t slot = (size_t)m % p->lead_ev.size();
-            while (p->lead_tag[slot].load(std::memory_order_acquire) != m) std::this_thread::yield();
-            if ((e = cudaEventSynchronize(p->lead_ev[slot])) != cudaSuccess) return cuda_status(e, "lead wait");
+        if (p->front_limit > 0 && blend && k >= p->front_limit) {
+            // front-end concurrency limit: frame k's front end starts after frame
+            // k - K's (its split event, recorded at the end of its front end).
+            // Slot (k - K) mod depth belongs to this thread (K and depth are
+            // multiples of the thread count) and its next frame k - K + depth > k
+            // is not issued yet, so the event still marks frame k - K.
+            const int s2 = (k - p->front_limit) % p->depth;
+            if ((e = cudaStreamWaitEvent(front, p->split_ev[s2], 0)) != cudaSuccess) return cuda_status(e, "wait");
         }
         void *const *evs = p->stage_events ? p->stage_events + 5 * (size_t)k : nullptr;
         fdgs_status st = blend ? fdgs_render_split(&J.scene, J.d_mask_l, J.d_mask_r, &J.cam, J.t, J.d_out_rgb,
@@ -113,11 +108,6 @@ fdgs_status submit(fdgs_pipeline *p, int w, int nw) {
         }
         if (J.done_event != nullptr && (e = cudaEventRecord((cudaEvent_t)J.done_event, last)) != cudaSuccess)
             return cuda_status(e, "done event");
-        if (p->max_lead > 0) {  // this frame's completion, for frame k + W's issue
-            const size_t slot = (size_t)k % p->lead_ev.size();
-            if ((e = cudaEventRecord(p->lead_ev[slot], last)) != cudaSuccess) return cuda_status(e, "lead event");
-            p->lead_tag[slot].store(k, std::memory_order_release);
-        }
         if (J.h_out_rgb != nullptr) {  // D2H of the finished frame on a copy stream
             if (p->copies.empty()) return set_error(FDGS_ERR_INVALID_ARG, "h_out_rgb needs a copy stream");
             cudaStream_t cp = p->copies[k % p->copies.size()];
@@ -151,7 +141,7 @@ void worker_main(fdgs_pipeline *p, int w) {
 }
 
 void destroy_events(fdgs_pipeline *p) {
-    for (auto *v : {&p->done_ev, &p->fin_ev, &p->split_ev, &p->join_ev, &p->lead_ev})
+    for (auto *v : {&p->done_ev, &p->fin_ev, &p->split_ev, &p->join_ev})
         for (cudaEvent_t e : *v)
             if (e) cudaEventDestroy(e);
     if (p->start_ev) cudaEventDestroy(p->start_ev);
@@ -162,11 +152,11 @@ void destroy_events(fdgs_pipeline *p) {
 extern "C" {
 
 fdgs_status fdgs_pipeline_create(const fdgs_pipeline_slot *slots, int32_t depth, void *const *copy_streams,
-                                 int32_t n_copy, int32_t n_threads, int32_t max_lead, fdgs_pipeline **out) {
+                                 int32_t n_copy, int32_t n_threads, int32_t front_limit, fdgs_pipeline **out) {
     if (out == nullptr) return set_error(FDGS_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
     if (slots == nullptr || depth < 1 || depth > 64 || n_copy < 0 || (n_copy > 0 && copy_streams == nullptr) ||
-        n_threads < 1 || n_threads > 64 || max_lead < 0)
+        n_threads < 1 || n_threads > 64 || front_limit < 0)
         return set_error(FDGS_ERR_INVALID_ARG, "slots / depth in [1, 64] / copy streams / n_threads in [1, 64]");
     for (int s = 0; s < depth; ++s)
         if (slots[s].d_ws == nullptr || slots[s].front_stream == nullptr)
@@ -190,21 +180,12 @@ fdgs_status fdgs_pipeline_create(const fdgs_pipeline_slot *slots, int32_t depth,
         delete p;
         return cuda_status(e, "fdgs_pipeline_create");
     }
-    p->max_lead = max_lead;
-    if (max_lead > 0) {  // ring of completion events: a slot is reused 4W + 64 frames later
-        const size_t R = 4 * (size_t)max_lead + 64;
-        p->lead_ev.resize(R, nullptr);
-        p->lead_tag.reset(new std::atomic<int64_t>[R]);
-        for (size_t i = 0; i < R; ++i) p->lead_tag[i].store(-1);
-        for (auto &ev : p->lead_ev)
-            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventBlockingSync);
-        if (e != cudaSuccess) {
-            destroy_events(p);
-            delete p;
-            return cuda_status(e, "fdgs_pipeline_create");
-        }
-    }
-    p->n_threads = std::min(n_threads, depth);
+    p->front_limit = front_limit < depth ? front_limit : 0;
+    // with a front-end limit K, frames k and k - K must be issued by one thread:
+    // the largest thread count <= n_threads dividing both depth and K
+    int nt = std::min(n_threads, depth);
+    while (p->front_limit > 0 && (depth % nt != 0 || p->front_limit % nt != 0)) --nt;
+    p->n_threads = nt;
     if (p->n_threads > 1)
         for (int w = 0; w < p->n_threads; ++w) p->workers.emplace_back(worker_main, p, w);
     *out = p;
@@ -226,7 +207,6 @@ fdgs_status fdgs_pipeline_render(fdgs_pipeline *p, const fdgs_frame_job *jobs, i
     for (cudaStream_t s : streams)
         if (e == cudaSuccess) e = cudaStreamWaitEvent(s, p->start_ev, 0);
     if (e != cudaSuccess) return cuda_status(e, "fdgs_pipeline_render");
-    for (size_t i = 0; i < p->lead_ev.size(); ++i) p->lead_tag[i].store(-1, std::memory_order_relaxed);
     p->jobs = jobs;
     p->n_jobs = n_jobs;
     p->stage_events = stage_events;
