@@ -83,7 +83,8 @@ def parse():
     p.add_argument("--graphs", action="store_true", help="one CUDA-graph launch per frame (RenderPipeline(graphs=True))")
     p.add_argument("--py-submit", action="store_true",
                    help="submit frames from the Python loop (one C call per frame) instead of fdgs_pipeline_render")
-    p.add_argument("--submit-threads", type=int, default=4, help="host threads of fdgs_pipeline_render")
+    p.add_argument("--submit-threads", type=int, default=1,
+                   help="host threads of fdgs_pipeline_render (1: frames issued in order; more cost device throughput)")
     p.add_argument("--sync-compact", action="store_true",
                    help="read each working set's size back to the host (Scene.compact sync=True)")
     p.add_argument("--config", choices=["c1", "c2", "c3", "c4"], default="c3")

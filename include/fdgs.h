@@ -247,10 +247,10 @@ fdgs_status fdgs_render_graph_destroy(fdgs_render_graph *graph);
  * renders in slot k mod depth (fdgs_render_split); a slot's next frame is
  * ordered after its previous blend.  The handle owns n_threads host threads
  * that issue the batch's launches in parallel (one group of slots per
- * thread; 1 = the caller's thread), plus its own CUDA events.  front_limit
- * K > 0 (split slots only): frame k's front end starts only after frame
- * k - K's has finished, so at most K front ends compete with the blends for
- * the SMs (the thread count is lowered to divide both depth and K).
+ * thread; 1 = the caller's thread, frames in order), plus its own CUDA
+ * events.  Several threads cut the host time per frame but interleave the
+ * frames' launches, which costs device throughput with 12 streams (measured;
+ * DESIGN.md "Host submission"): 1 is the default of the Python binding.
  *   fdgs_frame_job: the frame (scene and camera BY VALUE, masks, t, outputs
  *   as for fdgs_render; d_stats nullable = the timed blend, else the counting
  *   blend); h_out_rgb (nullable, pinned HOST float[3][H][W]): copied D2H on
@@ -282,7 +282,7 @@ typedef struct {
 } fdgs_frame_job;
 typedef struct fdgs_pipeline fdgs_pipeline;
 fdgs_status fdgs_pipeline_create(const fdgs_pipeline_slot *slots, int32_t depth, void *const *copy_streams,
-                                 int32_t n_copy, int32_t n_threads, int32_t front_limit, fdgs_pipeline **out);
+                                 int32_t n_copy, int32_t n_threads, fdgs_pipeline **out);
 fdgs_status fdgs_pipeline_render(fdgs_pipeline *pipeline, const fdgs_frame_job *jobs, int32_t n_jobs, void *stream,
                                  void *const *stage_events);
 fdgs_status fdgs_pipeline_destroy(fdgs_pipeline *pipeline);

@@ -123,7 +123,7 @@ def lib():
             "fdgs_stv_score": ([P, P, I32, P, I32, P, P, P, P, P, SZ, P, P], C.c_int),
             "fdgs_prune_workspace_bytes": ([I32], SZ),
             "fdgs_prune_mask": ([P, I32, C.c_int64, P, P, SZ, P], C.c_int),
-            "fdgs_pipeline_create": ([P, I32, P, I32, I32, I32, P], C.c_int),
+            "fdgs_pipeline_create": ([P, I32, P, I32, I32, P], C.c_int),
             "fdgs_pipeline_render": ([P, P, I32, P, P], C.c_int),
             "fdgs_pipeline_destroy": ([P], C.c_int),
             "fdgs_debug_strip_reach": ([P, SZ, I32, I32, I32, I64, P, P], C.c_int),

@@ -373,23 +373,22 @@ class RenderPipeline:
     is scheduled ahead of, and overlaps, the ALU-bound blends.
 
     native (default, unless graphs): render_many submits the whole batch
-    through fdgs_pipeline_render -- one C call whose `threads` host threads
-    issue the frames' launches in parallel (the Python loop below remains for
-    graphs=True and as the reference path, native=False)."""
+    through fdgs_pipeline_render -- one C call, frames issued in order on the
+    calling thread (threads > 1: issued in parallel by that many host threads,
+    cheaper on the host but slower on the device); the Python loop below
+    remains for graphs=True and as the reference path (native=False)."""
 
     def __init__(self, scene: Scene, width: int, height: int, depth: int = 4, max_entries: int | None = None,
                  split: bool = True, copy_streams: int = 1, graphs: bool = False, native: bool | None = None,
-                 threads: int | None = None, front_limit: int = 0):
+                 threads: int = 1):
         self.renderers = [Renderer(scene, width, height, max_entries) for _ in range(depth)]
         self.native = (not graphs) if native is None else bool(native)
         if self.native and graphs:
             raise ValueError("the native batch submission launches streams, not graphs")
-        self.threads = int(threads) if threads else min(depth, 4)
+        self.threads = max(1, int(threads))
         self._handle = None
         self._handle_key = None
         self._frame_ev = []
-        # frame k's front end waits for frame k - front_limit's (0: no limit)
-        self.front_limit = int(front_limit) if front_limit and front_limit < depth else 0
         lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
         self.split = split
         self.graphs = graphs  # the front end as one CUDA-graph launch per frame, the blend launched after it
@@ -431,8 +430,7 @@ class RenderPipeline:
                                             self.blend[i].cuda_stream if self.split else None)
             cps = (C.c_void_p * len(self.copies))(*[c.cuda_stream for c in self.copies])
             h = C.c_void_p()
-            check(lib().fdgs_pipeline_create(slots, self.depth, cps, len(self.copies), self.threads, self.front_limit,
-                                             C.byref(h)))
+            check(lib().fdgs_pipeline_create(slots, self.depth, cps, len(self.copies), self.threads, C.byref(h)))
             self._handle, self._handle_key = h, key
         return self._handle
 
@@ -552,8 +550,6 @@ class RenderPipeline:
                 if k >= self.depth:  # the workspace is free once its previous blend is done
                     self.done_ev[i].record(self.blend[i])
                     self.front[i].wait_event(self.done_ev[i])
-                if self.front_limit and k >= self.front_limit:  # frame k - K's front end has finished
-                    self.front[i].wait_event(self.split_ev[(k - self.front_limit) % self.depth])
                 r.render_split(cam, t, ml, mr, out=outs[k], stats=None if stats is None else stats[k],
                                stream=self.front[i], blend_stream=self.blend[i], split_event=self.split_ev[i],
                                stage_events=None if stage_events is None else stage_events[k], scene=sc)

@@ -4,12 +4,14 @@
 // Frame k of a batch renders in workspace slot k mod depth: its front end on
 // the slot's (high-priority) front stream, its blend on the slot's blend
 // stream (fdgs_render_split), the slot's next frame ordered after this blend.
-// The ~20 launches of a frame cost ~60 us of host time (CUDA launch calls),
-// more than a third of the frame's device time at C3; here they are issued by
-// worker threads owned by the handle, one group of slots per thread, so the
-// host keeps ahead of the device.  Every slot's
-// frames are issued in order by one thread, so stream order alone orders
-// their work; threads share only the copy streams (independent copies).
+// The ~20 launches of a frame cost ~60 us of host time (CUDA API calls), a
+// third of the frame's device time at C3.  One call submits the whole batch,
+// in frame order on the caller's thread by default; optionally worker threads
+// owned by the handle issue it in parallel (one group of slots per thread),
+// which cuts the host time but measurably slows the device's scheduling of the
+// 12 streams.  Every slot's frames are issued in
+// order by one thread, so stream order alone orders their work; threads share
+// only the copy streams (independent copies).
 #include <algorithm>
 #include <condition_variable>
 #include <cstdarg>
@@ -31,7 +33,6 @@ struct fdgs_pipeline {
     std::vector<cudaStream_t> copies;
     std::vector<cudaEvent_t> done_ev, fin_ev, split_ev, join_ev;  // per slot (join: per stream)
     cudaEvent_t start_ev = nullptr;
-    int front_limit = 0;  // > 0: at most this many frames' front ends in flight
     // worker pool
     int n_threads = 1;
     std::vector<std::thread> workers;
@@ -80,15 +81,6 @@ fdgs_status submit(fdgs_pipeline *p, int w, int nw) {
         if (seen[s]++) {  // the slot's previous frame must have left the workspace
             if ((e = cudaEventRecord(p->done_ev[s], last)) != cudaSuccess) return cuda_status(e, "record");
             if ((e = cudaStreamWaitEvent(front, p->done_ev[s], 0)) != cudaSuccess) return cuda_status(e, "wait");
-        }
-        if (p->front_limit > 0 && blend && k >= p->front_limit) {
-            // front-end concurrency limit: frame k's front end starts after frame
-            // k - K's (its split event, recorded at the end of its front end).
-            // Slot (k - K) mod depth belongs to this thread (K and depth are
-            // multiples of the thread count) and its next frame k - K + depth > k
-            // is not issued yet, so the event still marks frame k - K.
-            const int s2 = (k - p->front_limit) % p->depth;
-            if ((e = cudaStreamWaitEvent(front, p->split_ev[s2], 0)) != cudaSuccess) return cuda_status(e, "wait");
         }
         void *const *evs = p->stage_events ? p->stage_events + 5 * (size_t)k : nullptr;
         fdgs_status st = blend ? fdgs_render_split(&J.scene, J.d_mask_l, J.d_mask_r, &J.cam, J.t, J.d_out_rgb,
@@ -152,11 +144,11 @@ void destroy_events(fdgs_pipeline *p) {
 extern "C" {
 
 fdgs_status fdgs_pipeline_create(const fdgs_pipeline_slot *slots, int32_t depth, void *const *copy_streams,
-                                 int32_t n_copy, int32_t n_threads, int32_t front_limit, fdgs_pipeline **out) {
+                                 int32_t n_copy, int32_t n_threads, fdgs_pipeline **out) {
     if (out == nullptr) return set_error(FDGS_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
     if (slots == nullptr || depth < 1 || depth > 64 || n_copy < 0 || (n_copy > 0 && copy_streams == nullptr) ||
-        n_threads < 1 || n_threads > 64 || front_limit < 0)
+        n_threads < 1 || n_threads > 64)
         return set_error(FDGS_ERR_INVALID_ARG, "slots / depth in [1, 64] / copy streams / n_threads in [1, 64]");
     for (int s = 0; s < depth; ++s)
         if (slots[s].d_ws == nullptr || slots[s].front_stream == nullptr)
@@ -180,12 +172,7 @@ fdgs_status fdgs_pipeline_create(const fdgs_pipeline_slot *slots, int32_t depth,
         delete p;
         return cuda_status(e, "fdgs_pipeline_create");
     }
-    p->front_limit = front_limit < depth ? front_limit : 0;
-    // with a front-end limit K, frames k and k - K must be issued by one thread:
-    // the largest thread count <= n_threads dividing both depth and K
-    int nt = std::min(n_threads, depth);
-    while (p->front_limit > 0 && (depth % nt != 0 || p->front_limit % nt != 0)) --nt;
-    p->n_threads = nt;
+    p->n_threads = std::min(n_threads, depth);
     if (p->n_threads > 1)
         for (int w = 0; w < p->n_threads; ++w) p->workers.emplace_back(worker_main, p, w);
     *out = p;

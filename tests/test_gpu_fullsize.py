@@ -6,7 +6,7 @@ against the nearest admissible termination branch, mean-abs 1e-5):
 
 * C3 (the metric's workload): a key-frame, a mid-window frame and the first
   frame after a window switch, rendered by RenderPipeline on 6 stream pairs
-  (fdgs_pipeline_render, 3 submission threads) from each window's compacted
+  (fdgs_pipeline_render) from each window's compacted
   working set whose size stays on the device (Scene.compact sync=False) --
   exactly what bench.py times; masks from the oracle itself (bit-exact
   against the GPU's);
@@ -62,7 +62,7 @@ def _pipeline_frames(name, picks, fill_cams=6):
             if c == ci:
                 keep.append(len(frames))
             frames.append((fd.camera_struct(cams[c]), float(times[ti]), None, None, wsets[(li, ri)]))
-    pipe = fd.RenderPipeline(sc, cams[0].width, cams[0].height, depth=6, threads=3)
+    pipe = fd.RenderPipeline(sc, cams[0].width, cams[0].height, depth=6)
     outs = [pipe.renderers[0].new_output() for _ in frames]
     st = pipe.render_many_checked(frames, outs)
     assert (st[:, 3] == 0).all()

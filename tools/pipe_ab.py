@@ -41,8 +41,7 @@ def use_lib(name):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("variants", nargs="+",
-                    help="py | native:T | graphs, optionally @depth, ~K front-end limit, #lib variant "
-                         "(native:3@6~3#sleep200)")
+                    help="py | native:T | graphs, optionally @depth (native:3@8), #lib variant (native:1#sleep200)")
     ap.add_argument("--config", default="c3")
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--steps", type=int, default=6)
@@ -77,13 +76,10 @@ def main():
         libs[v] = libname
         use_lib(libname)
         name, _, rest = spec.partition("@")
-        depth, _, lim = rest.partition("~")
-        if "~" in name:
-            name, _, lim = name.partition("~")
-        depth = int(depth or 6)
+        depth = int(rest or 6)
         kind, _, thr = name.partition(":")
         pipes[v] = fd.RenderPipeline(sc, cams[0].width, cams[0].height, depth=depth, graphs=kind == "graphs",
-                                     native=kind == "native", threads=int(thr or 3), front_limit=int(lim or 0))
+                                     native=kind == "native", threads=int(thr or 3))
     outs = [pipes[a.variants[0]].renderers[0].new_output() for _ in range(a.frames)]
     res = {v: [] for v in a.variants}
     host = {v: [] for v in a.variants}
