@@ -59,20 +59,25 @@ def main():
     cs = [fd.camera_struct(c) for c in cams]
     seq = [(f, f // len(cams), f % len(cams)) for f in range(len(cams) * F)]
     wsets = {}
+    sync_now = [False]
 
     def frame(x):
         f, ti, ci = x
         li, ri = fd.bracket(kf, ti)
-        if (li, ri) not in wsets:
-            wsets[(li, ri)] = sc.compact(masks[li], masks[ri], sync=False)
-        return cs[ci], float(times[ti]), None, None, wsets[(li, ri)]
+        key = (li, ri, sync_now[0])
+        if key not in wsets:
+            wsets[key] = sc.compact(masks[li], masks[ri], sync=sync_now[0])
+        return cs[ci], float(times[ti]), None, None, wsets[key]
 
     flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device="cuda")
     pipes = {}
     use_lib("")
     libs = {}
+    syncs = {}
     for v in a.variants:
         spec, _, libname = v.partition("#")
+        syncs[v] = spec.endswith("+sync") or libname == "r01"   # r01: no device-count working sets
+        spec = spec.replace("+sync", "")
         libs[v] = libname
         use_lib(libname)
         name, _, rest = spec.partition("@")
@@ -102,11 +107,13 @@ def main():
 
     for v in a.variants:  # warm every variant
         use_lib(libs[v])
+        sync_now[0] = syncs[v]
         for _ in range(2):
             step(pipes[v], False)
     for r in range(a.rounds):
         for v in a.variants:
             use_lib(libs[v])
+            sync_now[0] = syncs[v]
             for _ in range(a.steps):
                 ms, h = step(pipes[v], True)
                 res[v].append(ms)
