@@ -1296,8 +1296,8 @@ __device__ __forceinline__ bool strip_stage(const float4 &r0, const float4 &r1, 
     const float xr = __fsub_rn((float)(tx * 16 + x1) + 0.5f, u);
     const float yl = __fsub_rn((float)(ty * 16 + y0) + 0.5f, v), yr = __fsub_rn((float)(ty * 16 + y1) + 0.5f, v);
     const float X = fmaxf(fabsf(xl), fabsf(xr)), Y = fmaxf(fabsf(yl), fabsf(yr));
-    const float mag = __fadd_rn(__fadd_rn(__fmul_rn(__fmul_rn(fabsf(Ap), X), X), __fmul_rn(__fmul_rn(fabsf(Bp), X), Y)),
-                                __fmul_rn(__fmul_rn(fabsf(Cp), Y), Y));
+    const float mag = __fmaf_rn(__fmul_rn(fabsf(Ap), X), X,
+                                __fmaf_rn(__fmul_rn(fabsf(Bp), X), Y, __fmul_rn(__fmul_rn(fabsf(Cp), Y), Y)));
     const float marg = -__fmaf_rn(1e-3f, mag, 1e-3f);
     const float hA = __fdividef(-0.5f, Ap);  // stationary point only
     bool rw = false;
