@@ -81,8 +81,8 @@ def parse():
     p.add_argument("--streams", type=int, default=6, help="frame-pipelining depth (workspaces/streams)")
     p.add_argument("--no-split", action="store_true", help="blend on the front-end stream (no priority split)")
     p.add_argument("--graphs", action="store_true", help="one CUDA-graph launch per frame (RenderPipeline(graphs=True))")
-    p.add_argument("--py-submit", action="store_true",
-                   help="submit frames from the Python loop (one C call per frame) instead of fdgs_pipeline_render")
+    p.add_argument("--native-submit", action="store_true",
+                   help="submit each step's frames with one fdgs_pipeline_render call instead of the per-frame loop")
     p.add_argument("--submit-threads", type=int, default=1,
                    help="host threads of fdgs_pipeline_render (1: frames issued in order; more cost device throughput)")
     p.add_argument("--sync-compact", action="store_true",
@@ -351,7 +351,7 @@ def run_ours(args):
         stream = None
     else:
         pipe = fd.RenderPipeline(scene, W, H, depth=args.streams, split=not args.no_split, graphs=args.graphs,
-                                 native=False if (args.py_submit or args.graphs) else None,
+                                 native=args.native_submit and not args.graphs,
                                  threads=args.submit_threads)
         renderer = pipe.renderers[0]
         outs = [renderer.new_output() for _ in range(F)]
