@@ -396,7 +396,7 @@ def test_native_pipeline_working_sets_without_host_sync():
             assert wsets[(l, r)].n == sc.n and wsets[(l, r)].struct.d_n
         frames.append((cams[fr % 4], float(times[fr]), None, None, wsets[(l, r)]))
         refs.append(seq.render_checked(cams[fr % 4], float(times[fr]), masks[l], masks[r])[0].clone())
-    pipe = fd.RenderPipeline(sc, 300, 200, depth=4, threads=2)
+    pipe = fd.RenderPipeline(sc, 300, 200, depth=4, native=True, threads=2)
     outs = [pipe.renderers[0].new_output() for _ in frames]
     st = pipe.render_many_checked(frames, outs)
     assert (st[:, 3] == 0).all()
