@@ -586,7 +586,7 @@ def run_ours(args):
                   "unit": "GB/s", "frac": round(achieved / hbm, 4), "peak_src": peak_src}
         trj = load_traffic()
         rl["traffic"] = trj.get(rl["kernel"])
-        for key in ("issue_slots_busy", "pipes"):
+        for key in ("issue_slots_busy", "pipes"):  # ncu of the blend (profiles/traffic.json)
             if trj.get(rl["kernel"] + "_" + key) is not None:
                 rl["ncu_" + key] = trj[rl["kernel"] + "_" + key]
         res["roofline"] = rl
@@ -631,7 +631,7 @@ def run_ours(args):
                         "model": "SURVEY.md 8(d) d.4: mask words + index + 68 B/active + (192+96+72) B/visible + "
                                  "(8+32+52) B/entry + 12 B/pixel, per GPU"}
     dram = load_traffic().get("frame_dram_bytes")
-    if dram is not None:
+    if dram is not None and CONFIG == "c3" and MASKED:  # the committed capture is of this workload
         res["frame_hbm"]["ncu_dram_bytes_per_frame"] = dram
     res["clocks"] = clocks
     # host time to enqueue a step (render_many returning) vs the step's device
