@@ -85,6 +85,7 @@ def parse():
                    help="submit each step's frames with one fdgs_pipeline_render call instead of the per-frame loop")
     p.add_argument("--submit-threads", type=int, default=1,
                    help="host threads of fdgs_pipeline_render (1: frames issued in order; more cost device throughput)")
+    p.add_argument("--copy-streams", type=int, default=1, help="e2e: D2H copy streams of the pipeline")
     p.add_argument("--sync-compact", action="store_true",
                    help="read each working set's size back to the host (Scene.compact sync=True)")
     p.add_argument("--config", choices=["c1", "c2", "c3", "c4"], default="c3")
@@ -351,7 +352,7 @@ def run_ours(args):
         stream = None
     else:
         pipe = fd.RenderPipeline(scene, W, H, depth=args.streams, split=not args.no_split, graphs=args.graphs,
-                                 native=args.native_submit and not args.graphs,
+                                 native=args.native_submit and not args.graphs, copy_streams=args.copy_streams,
                                  threads=args.submit_threads)
         renderer = pipe.renderers[0]
         outs = [renderer.new_output() for _ in range(F)]
