@@ -106,3 +106,32 @@ def test_bench_launch_configuration_full_c3():
     pix = np.unique(np.random.default_rng(5).integers(0, 1352 * 1014, 2500))
     orc = oracle.render(scene, cams[ci], float(times[ti]), mask=active, pixels=pix)
     assert_rgb_parity(outs[4].cpu().numpy(), orc, pixels=pix)
+
+
+def test_compact_on_a_side_stream():
+    """Scene.compact on a non-current stream orders its
+    zero-fill, kernel and count read-back on that stream; a working set whose
+    count stays on the device (sync=False) renders the same frame."""
+    scene = fi.make_scene("c3", n=40_000, seed=12)
+    cams = fi.make_cameras("c3", width=240, height=180, fx=180.0, count=3)
+    sc = fd.Scene.from_arrays(scene)
+    t0, t1 = float(np.float32(0.2)), float(np.float32(0.26))
+    ml, mr = fd.keyframe_mask(sc, cams, t0), fd.keyframe_mask(sc, cams, t1)
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    busy = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    with torch.cuda.stream(side):
+        busy.fill_(1.0)                     # keep the side stream busy when compact starts
+    a = sc.compact(ml, mr, stream=side)
+    want = int(np.count_nonzero(np.unpackbits((ml.cpu().numpy().view(np.uint32) | mr.cpu().numpy().view(np.uint32))
+                                              .view(np.uint8), bitorder="little")[:sc.n]))
+    assert a.n == want
+    b = sc.compact(ml, mr, stream=side, sync=False)
+    assert b.n == sc.n and int(b.count.item()) == want
+    r = fd.Renderer(sc, 240, 180)
+    ref, _ = r.render_checked(cams[1], 0.23, ml, mr)
+    ref = ref.clone()
+    for ws in (a, b):
+        out = r.render(cams[1], 0.23, scene=ws)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
