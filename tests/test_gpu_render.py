@@ -541,3 +541,21 @@ def test_overflow_writes_nothing_past_the_workspace(cap):
         assert st == _lib.FDGS_ERR_OVERFLOW
     torch.cuda.synchronize()
     assert bool((buf[nb:] == 0xA5).all())
+
+
+def test_anamorphic_camera_parity():
+    """fx != fy and an off-centre principal point (reading R13): records, tile
+    lists bit-exact and RGB within the bar on a C3-shaped scene (the oracle's
+    projection for such cameras is pinned by test_oracle_projection_pins.py)."""
+    scene = fi.make_scene("c3", n=40_000, seed=14)
+    cam = fi.make_cameras("c3", width=420, height=300, fx=310.0, count=5)[3]
+    cam.fy = float(np.float32(0.7 * cam.fx))
+    cam.cx = float(np.float32(0.43 * cam.width))
+    cam.cy = float(np.float32(0.58 * cam.height))
+    t = float(np.float32(0.41))
+    img, T, stats, r = _render(scene, cam, t)
+    views = r.debug_views()
+    assert_records_bit_exact(views, scene, cam, t)
+    assert_tile_lists_bit_exact(views, scene, cam, t)
+    assert_rgb_parity(img, oracle.render(scene, cam, t))
+    assert stats.n_vis > 1000

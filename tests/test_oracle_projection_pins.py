@@ -34,18 +34,31 @@ import fdgs_inputs as fi
 import oracle
 
 RIGS = {
-    # config: (scene n, camera indices, timestamps)
+    # config: (scene n, camera indices, timestamps); "c3a": the C3 arc rig with
+    # anamorphic intrinsics (fy = 0.7 fx) and an off-centre principal point
     "c2": (8000, [0, 5, 9, 17, 23, 31, 41, 47], [0.25, 0.6]),
     "c3": (6000, [0, 11, 19], [0.3, 0.7]),
+    "c3a": (6000, [2, 14], [0.3, 0.7]),
 }
+
+
+def anamorphic(cam):
+    """fy = 0.7 fx, principal point at (0.43 W, 0.58 H) (reading R13 allows any)."""
+    cam.fy = float(np.float32(0.7 * cam.fx))
+    cam.cx = float(np.float32(0.43 * cam.width))
+    cam.cy = float(np.float32(0.58 * cam.height))
+    return cam
 
 
 def _projected(name):
     """(scene, cam, t, rec, idx) with idx the Gaussians that reach the
     projection (stage COVER or VISIBLE: Sigma_2D and (u, v) are defined)."""
     n, cam_ids, ts = RIGS[name]
-    scene = fi.make_scene(name, n=n, seed=21)
-    cams = fi.make_cameras(name)
+    base = "c3" if name == "c3a" else name
+    scene = fi.make_scene(base, n=n, seed=21)
+    cams = fi.make_cameras(base)
+    if name == "c3a":
+        cams = [anamorphic(c) for c in cams]
     for c in cam_ids:
         for t in ts:
             t32 = float(np.float32(t))
@@ -97,7 +110,7 @@ def _cov3(rec, idx):
                      np.stack([c[:, 2], c[:, 4], c[:, 5]], 1)], 1)
 
 
-@pytest.mark.parametrize("name", ["c2", "c3"])
+@pytest.mark.parametrize("name", ["c2", "c3", "c3a"])
 def test_pixel_position_is_the_pinhole_image(name):
     seen = 0
     for scene, cam, t, rec, idx in _projected(name):
@@ -111,7 +124,7 @@ def test_pixel_position_is_the_pinhole_image(name):
     assert seen >= 1000
 
 
-@pytest.mark.parametrize("name", ["c2", "c3"])
+@pytest.mark.parametrize("name", ["c2", "c3", "c3a"])
 def test_sigma2d_is_the_complex_step_ewa_projection(name):
     """Sigma_2D = J_w Sigma_3 J_w^T + 0.3 I (R6) to 1e-9 relative, with
     the Jacobian clamp exercised; the unclamped Jacobian would differ there."""
@@ -142,7 +155,7 @@ def test_sigma2d_is_the_complex_step_ewa_projection(name):
     assert seen >= 1000 and clamped_seen >= 50, (seen, clamped_seen)
 
 
-@pytest.mark.parametrize("name", ["c2", "c3"])
+@pytest.mark.parametrize("name", ["c2", "c3", "c3a"])
 def test_pixel_aabb_contains_the_alpha_ellipse(name):
     """The pixel AABB of a splat (reading R7) covers the closed-form extent of
     {power <= Q} = {d^T Sigma_2D^-1 d <= 2Q}, half-widths sqrt(2Q Sigma_2D,xx)
@@ -196,7 +209,7 @@ def test_sh_basis_equals_scipy_real_sh():
         assert np.max(np.abs(oracle.sh_basis(d) - _real_sh_scipy(d))) < 1e-12
 
 
-@pytest.mark.parametrize("name", ["c2", "c3"])
+@pytest.mark.parametrize("name", ["c2", "c3", "c3a"])
 def test_view_dependent_colour_from_the_camera_centre(name):
     """c_i(d) with d = (mu3 - C)/|mu3 - C|, C the generator's float64
     camera centre (reading R10), rgb = max(0, sum_k Y_k(d) sh_k + 0.5) with the

@@ -53,6 +53,11 @@ MUTANTS = [
     ("mask OR -> AND", "out[w] = a[w] | b[w];", "out[w] = a[w] & b[w];"),
     ("bracket: right key-frame off by one", "for (int k = nk - 1; k >= 0; --k) if (kf[k] >= frame) ri = k;",
      "for (int k = nk - 1; k >= 0; --k) if (kf[k] > frame) ri = k;"),
+    ("j00 from fy", "const double j00 = fx * rz, j11 = fy * rz;", "const double j00 = fy * rz, j11 = fy * rz;"),
+    ("Jacobian y clamp from the width", "const double limy = OR_JCLAMP * ((double)cam->height / (2.0 * fy));",
+     "const double limy = OR_JCLAMP * ((double)cam->width / (2.0 * fy));"),
+    ("u from cy", "const double u = fma(fx, xz, cx), vv = fma(fy, yz, cy);",
+     "const double u = fma(fx, xz, cy), vv = fma(fy, yz, cy);"),
     ("S^TV uses p instead of p2", "return 1.0 / (0.5 * tanh(fabs(p2)) + 0.5);", "return 1.0 / (0.5 * tanh(fabs(p)) + 0.5);"),
 ]
 
