@@ -559,3 +559,48 @@ def test_anamorphic_camera_parity():
     assert_tile_lists_bit_exact(views, scene, cam, t)
     assert_rgb_parity(img, oracle.render(scene, cam, t))
     assert stats.n_vis > 1000
+
+
+def test_stress_scene_parity():
+    """Edge cases of the conic and the composite together, whole frame: splats
+    just beyond z_near (screen-filling, Jacobian clamp active), opacity 1
+    (alpha clamped at 0.99 on every layer: termination after 2-3 layers),
+    sub-pixel splats (the 0.3 px^2 dilation dominates), strongly anisotropic
+    ones, and Gaussians far outside the frustum."""
+    rng = np.random.default_rng(29)
+    parts = []
+    n1 = 200    # near the camera plane: z in (0.21, 0.6)
+    parts.append((np.stack([rng.uniform(-0.2, 0.2, n1), rng.uniform(-0.15, 0.15, n1), rng.uniform(0.21, 0.6, n1),
+                            np.full(n1, 0.5)], 1), np.exp(rng.uniform(-4, -2, (n1, 3))), rng.uniform(0.2, 1.0, n1)))
+    n2 = 3000   # opacity 1 layers
+    parts.append((np.stack([rng.uniform(-2, 2, n2), rng.uniform(-1.5, 1.5, n2), rng.uniform(3, 8, n2),
+                            np.full(n2, 0.5)], 1), np.exp(rng.uniform(-3, -1.5, (n2, 3))), np.ones(n2)))
+    n3 = 6000   # sub-pixel
+    parts.append((np.stack([rng.uniform(-2, 2, n3), rng.uniform(-1.5, 1.5, n3), rng.uniform(2, 9, n3),
+                            np.full(n3, 0.5)], 1), np.exp(rng.uniform(-9, -7, (n3, 3))), rng.uniform(0.3, 1.0, n3)))
+    n4 = 2000   # anisotropic (one long axis)
+    s4 = np.exp(rng.uniform(-6, -4, (n4, 3)))
+    s4[:, 0] = np.exp(rng.uniform(-1.5, -0.5, n4))
+    parts.append((np.stack([rng.uniform(-2, 2, n4), rng.uniform(-1.5, 1.5, n4), rng.uniform(2, 9, n4),
+                            np.full(n4, 0.5)], 1), s4, rng.uniform(0.3, 1.0, n4)))
+    n5 = 500    # behind the camera and far to the side
+    parts.append((np.stack([rng.uniform(-50, 50, n5), rng.uniform(-50, 50, n5), rng.uniform(-20, 2, n5),
+                            np.full(n5, 0.5)], 1), np.exp(rng.uniform(-3, 0, (n5, 3))), rng.uniform(0.3, 1.0, n5)))
+    means = np.concatenate([p[0] for p in parts])
+    scales = np.concatenate([np.concatenate([p[1], np.full((len(p[1]), 1), 0.4)], 1) for p in parts])
+    ops = np.concatenate([p[2] for p in parts])
+    n = means.shape[0]
+    ql = rng.standard_normal((n, 4))
+    ql /= np.linalg.norm(ql, axis=1, keepdims=True)
+    ql[:, 0] = np.abs(ql[:, 0])
+    sc = fi.isotropic_scene(means, scales, ops, colors=rng.uniform(0, 1, (n, 3)), rot_l=ql,
+                            rot_r=np.tile([1.0, 0, 0, 0], (n, 1)))
+    cam = fi.scenes._cam(480, 360, 420.0, np.eye(3), np.zeros(3), np.zeros(3), bg=(0.3, 0.2, 0.1))
+    for t in (0.5, 0.62):
+        img, T, stats, r = _render(sc, cam, t)
+        views = r.debug_views()
+        assert_records_bit_exact(views, sc, cam, t)
+        assert_tile_lists_bit_exact(views, sc, cam, t)
+        orc = oracle.render(sc, cam, t)
+        assert_rgb_parity(img, orc)
+        assert stats.n_vis > 5000 and orc["stats"]["knife"] >= 0
