@@ -1372,6 +1372,9 @@ cudaError_t launch_debug_strip_reach(char *ws, const RenderLayout &L, uint8_t *o
 constexpr int kWiPairUnroll = FDGS_WI_PAIR_UNROLL;
 
 constexpr int kWiThreads = 128;
+#ifndef FDGS_WI_PREFETCH
+#define FDGS_WI_PREFETCH 1  // gather the next batch's records while this one is composited
+#endif
 __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uint32_t *__restrict__ tile_start,
                                                          const uint32_t *__restrict__ entries,
                                                          const float4 *__restrict__ rec0,
@@ -1501,8 +1504,13 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
     };
     bool wdone = __all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf);
     float4 r0, r1, r2;
+#if FDGS_WI_PREFETCH
     if (start < end) fetch(start, r0, r1, r2);
+#endif
     for (uint32_t base = start; base < end && !wdone; base += 32) {
+#if !FDGS_WI_PREFETCH
+        fetch(base, r0, r1, r2);
+#endif
         const int n = (int)min(32u, end - base);
         // ---- stage this warp's list of the batch
         const bool redundant = (__float_as_uint(r1.w) & 0x80000000u) != 0u;
@@ -1521,7 +1529,9 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
             for (int r = 0; r < kWlRows; ++r) E.t[r] = make_float4(r2.z, __uint_as_float(mb), t1s[r], t4s[r]);
         }
         // ---- gather the next batch while this one is composited
+#if FDGS_WI_PREFETCH
         if (base + 32 < end) fetch(base + 32, r0, r1, r2);
+#endif
         __syncwarp();
         const int cnt = __popc(bal);
         if (masked) {
