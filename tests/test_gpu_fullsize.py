@@ -207,3 +207,67 @@ def test_blend_strip_culling_sound_adversarial():
     bad, staged, pairs = _strip_violations(v, r.strip_reach(), cam.width, cam.height)
     assert bad == 0 and v["n_entries"] > 10_000
     assert_rgb_parity(img.cpu().numpy(), oracle.render(sc, cam, 0.5))
+
+
+def _cover_violations(views, W, H, chunk=1 << 16):
+    """Brute force (binary64 on the GPU) over every (visible Gaussian, tile of
+    its pixel-AABB rectangle) pair that is NOT in the tile lists: no pixel of
+    tile ∩ AABB may reach e2 >= 0 (exact quadratic + the pinned fp32 chain's
+    rounding budget).  Returns (violations, pairs checked, listed entries)."""
+    dev = views["tile_start"].device
+    tiles_x = (W + 15) // 16
+    ts = views["tile_start"].long()
+    T = ts.numel() - 1
+    tile = torch.repeat_interleave(torch.arange(T, device=dev), ts[1:] - ts[:-1])
+    g_list = views["entries"].long()
+    nv = views["n_vis"]
+    listed = torch.sort(tile * nv + g_list).values
+    r0 = views["rec0"].double()
+    r1 = views["rec1"]
+    bits = r1[:, 2:4].contiguous().view(torch.int32).long() & 0x7FFFFFFF
+    px0, px1 = bits[:, 0] & 0xFFFF, bits[:, 0] >> 16
+    py0, py1 = bits[:, 1] & 0xFFFF, bits[:, 1] >> 16
+    ntx = (px1 >> 4) - (px0 >> 4) + 1
+    nty = (py1 >> 4) - (py0 >> 4) + 1
+    cnt = ntx * nty
+    g_of = torch.repeat_interleave(torch.arange(nv, device=dev), cnt)
+    first = torch.cumsum(cnt, 0) - cnt
+    k = torch.arange(g_of.numel(), device=dev) - first[g_of]
+    tx = (px0[g_of] >> 4) + k % ntx[g_of]
+    ty = (py0[g_of] >> 4) + k // ntx[g_of]
+    key = (ty * tiles_x + tx) * nv + g_of
+    pos = torch.searchsorted(listed, key).clamp(max=listed.numel() - 1)
+    unl = listed[pos] != key
+    g_u, tx_u, ty_u = g_of[unl], tx[unl].double(), ty[unl].double()
+    kk = torch.arange(16, device=dev, dtype=torch.float64)
+    bad = 0
+    for c0 in range(0, g_u.numel(), chunk):
+        g = g_u[c0:c0 + chunk]
+        u, v, A, B = [r0[g, i][:, None, None] for i in range(4)]
+        C, Q = [r1[g, i].double()[:, None, None] for i in (0, 1)]
+        ii = 16 * tx_u[c0:c0 + chunk, None] + kk[None]
+        jj = 16 * ty_u[c0:c0 + chunk, None] + kk[None]
+        inx = (ii >= px0[g, None]) & (ii <= px1[g, None]) & (ii < W)
+        iny = (jj >= py0[g, None]) & (jj <= py1[g, None]) & (jj < H)
+        dx = (ii + 0.5)[:, None, :] - u
+        dy = (jj + 0.5)[:, :, None] - v
+        q = A * dx * dx + B * dx * dy + C * dy * dy + Q
+        err = 9 * 2.0 ** -24 * (A.abs() * dx * dx + B.abs() * (dx * dy).abs() + C.abs() * dy * dy + Q.abs())
+        bad += int(((q + err >= 0) & inx[:, None, :] & iny[:, :, None]).sum())
+    return bad, int(g_u.numel()), int(g_list.numel())
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_tile_cover_sound_full_size(name):
+    """The tile cover (reading R7b, the same definition in the oracle and the
+    kernel, so bit-exact lists cannot catch a shared error): at full size, no
+    tile of a splat's pixel AABB that the lists omit holds a pixel with
+    e2 >= 0 -- checked independently of both, by brute force."""
+    scene = fi.make_scene(name, n={"c2": None, "c3": None, "c4": 600_000}[name])
+    cam = fi.make_cameras(name)[{"c2": 19, "c3": 13, "c4": 6}[name]]
+    sc = fd.Scene.from_arrays(scene)
+    r = fd.Renderer(sc, cam.width, cam.height)
+    r.render_checked(cam, 0.55)
+    bad, omitted, listed = _cover_violations(r.debug_views(), cam.width, cam.height)
+    assert bad == 0
+    assert listed > 100_000 and omitted > 0.1 * listed     # the cover is tighter than the AABB rectangles
