@@ -140,6 +140,15 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def settle(self, timeout=10.0):
+        """Wait for nvidia-smi's first sample (its NVML start-up can stall the
+        CUDA launch path for ~0.2 s), then drop the samples taken so far: the
+        timed region starts after this."""
+        t0 = time.perf_counter()
+        while self.proc is not None and not self.lines and time.perf_counter() - t0 < timeout:
+            time.sleep(0.01)
+        self.lines.clear()
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -376,6 +385,7 @@ def run_ours(args):
     wsets = {}
     compacts = []  # one entry per Scene.compact: whether it ran inside a timed step
     timing_now = [False]
+    cur_step = [0]  # index of the timed step being enqueued (1-based; 0 = untimed)
 
     def frame_args(x):
         if fake:
@@ -390,7 +400,7 @@ def run_ours(args):
             if len(wsets) >= 2:
                 wsets.pop(next(iter(wsets)))
             wsets[(li, ri)] = scene.compact(masks[li], masks[ri], stream=stream, sync=args.sync_compact)
-            compacts.append(timing_now[0])
+            compacts.append(timing_now[0] and cur_step[0])
         return cam_structs[ci], float(times[ti]), None, None, wsets[(li, ri)]
 
     host_ms = []  # host enqueue time of each step (render_many returning)
@@ -449,11 +459,13 @@ def run_ours(args):
         ptr += F
         return out
 
-    for _ in range(args.warmup):
-        run_step(next_frames(), False)
     sampler = ClockSampler(local) if not fake else None
     if sampler:
         sampler.start()
+    for _ in range(args.warmup):
+        run_step(next_frames(), False)
+    if sampler:
+        sampler.settle()
     step_ms, stage_ms = [], np.zeros(4)
     h_first = len(host_ms)
     timed_frames = []
@@ -462,7 +474,8 @@ def run_ours(args):
     # host's lead over the GPU starves the queue); collected after timing
     gc.collect()
     gc.disable()
-    for _ in range(args.steps):
+    for k_step in range(args.steps):
+        cur_step[0] = k_step + 1
         fr = next_frames()
         timed_frames.append(fr)
         ms, stg = run_step(fr, True)
@@ -474,6 +487,7 @@ def run_ours(args):
     timing_now[0] = False
     # k_mask_compact + k_scene_gather per working set built inside the timed steps
     compact_launches = 2 * sum(1 for x in compacts if x)
+    compact_steps = {x - 1 for x in compacts if x}
     host_timed = host_ms[h_first:h_first + args.steps]
     # the job time is the slowest rank's device time (max over ranks), per step too
     per_rank = fdist.gather_timings(step_ms, dev)
@@ -502,6 +516,9 @@ def run_ours(args):
                step_stats={"median_frames_per_s": round(world * F / (med / 1e3), 2),
                            "min_ms": round(min(step_max), 4), "median_ms": round(med, 4),
                            "max_ms": round(max(step_max), 4),
+                           "outliers": [{"step": k, "ms": round(step_max[k], 3), "host_ms": round(host_timed[k], 3),
+                                         "new_working_set": k in compact_steps}
+                                        for k in range(args.steps) if step_max[k] > 1.5 * med][:8],
                            "note": "per-step max-over-ranks device time; value = all frames / sum of per-rank totals "
                                    "(max over ranks)"})
     if not fake:
