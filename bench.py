@@ -35,10 +35,11 @@ UNIT = "frames/s"
 CONFIG = "c3"
 BLEND_KERNEL = "k_blend_wi"
 # launches of libfdgs kernels per frame (render.cu launch_render, tile grid <= 256 rows):
-# k_cull, k_count_scan, k_cull_emit, k_slice, k_count_scan, k_vis_emit, k_sort_hist,
+# k_zero, k_cull, k_count_scan, k_cull_emit, k_slice, k_count_scan, k_vis_emit, k_sort_hist,
 # 4 x k_onesweep (depth), k_bin_count, k_count_scan, k_bin_offsets, k_row_items, k_row_scan,
-# k_onesweep (rows), k_row_count, k_tile_scan, k_row_scatter, k_blend_wi
-KERNELS_PER_FRAME = 21  # the timed blend (render.cu); k_blend_ws<true> supplies the work counters
+# k_onesweep (rows), k_row_count, k_tile_scan, k_row_scatter (the front end: one CUDA-graph
+# launch per frame by default), k_blend_wi
+KERNELS_PER_FRAME = 22  # the timed blend (render.cu); k_blend_ws<true> supplies the work counters
 N_CAMS = 20
 N_FRAMES_T = 300
 INTERVAL = 20
@@ -80,9 +81,11 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--streams", type=int, default=6, help="frame-pipelining depth (workspaces/streams)")
     p.add_argument("--no-split", action="store_true", help="blend on the front-end stream (no priority split)")
-    p.add_argument("--graphs", action="store_true", help="one CUDA-graph launch per frame (RenderPipeline(graphs=True))")
+    p.add_argument("--no-graphs", action="store_true",
+                   help="launch the front end's kernels one by one instead of one CUDA-graph launch per frame")
     p.add_argument("--native-submit", action="store_true",
-                   help="submit each step's frames with one fdgs_pipeline_render call instead of the per-frame loop")
+                   help="submit each step's frames with one fdgs_pipeline_render call (stream launches, implies "
+                        "--no-graphs) instead of the per-frame loop")
     p.add_argument("--submit-threads", type=int, default=1,
                    help="host threads of fdgs_pipeline_render (1: frames issued in order; more cost device throughput)")
     p.add_argument("--copy-streams", type=int, default=1, help="e2e: D2H copy streams of the pipeline")
@@ -297,6 +300,7 @@ def run_ours(args):
     import paper_2503_16422_b200 as fd  # (the library itself loads on first use: not in --fake-render)
 
     fake = args.fake_render
+    graphs = not (args.no_graphs or args.native_submit)
     rank, world, local = fdist.env_ranks()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
@@ -360,8 +364,8 @@ def run_ours(args):
         outs = [torch.empty((3, H, W), dtype=torch.float32) for _ in range(F)]
         stream = None
     else:
-        pipe = fd.RenderPipeline(scene, W, H, depth=args.streams, split=not args.no_split, graphs=args.graphs,
-                                 native=args.native_submit and not args.graphs, copy_streams=args.copy_streams,
+        pipe = fd.RenderPipeline(scene, W, H, depth=args.streams, split=not args.no_split, graphs=graphs,
+                                 native=args.native_submit, copy_streams=args.copy_streams,
                                  threads=args.submit_threads)
         renderer = pipe.renderers[0]
         outs = [renderer.new_output() for _ in range(F)]
@@ -371,7 +375,7 @@ def run_ours(args):
     gather = None
     if world > 1 and not args.no_gather:
         gather = fdist.FrameGather((3, H, W), args.gather_chunk, dev)
-    use_ev = not fake and not args.no_stage_events and not args.graphs  # graph frames record no stage events
+    use_ev = not fake and not args.no_stage_events
     if use_ev:
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(F)]
         for row in evs:
@@ -509,6 +513,9 @@ def run_ours(args):
                        "frames_per_step": F, "frames_per_rank": frames_rank, "partition": "frame f -> rank f mod N",
                        "l2": "flushed between steps (512 MiB write)", "parallelism": f"frames x{world}",
                        "streams_per_gpu": args.streams,
+                       "submission": ("native batch (fdgs_pipeline_render)" if args.native_submit else
+                                      "per frame: one CUDA-graph launch of the front end + the blend launch"
+                                      if graphs else "per frame: ~22 kernel launches"),
                        "stream_split": "front end high priority, blend low priority" if not args.no_split else "none",
                        "filter": ("compacted working set per key-frame window (Scene.compact, built inside the timed "
                                   "region when the sequence enters the window)") if MASKED and args.working_set

@@ -236,6 +236,16 @@ fdgs_status fdgs_render_graph_launch_split(fdgs_render_graph *graph, const fdgs_
                                            const uint32_t *d_mask_l, const uint32_t *d_mask_r,
                                            const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T,
                                            void *stream, void *blend_stream, void *split_event);
+/* As fdgs_render_graph_launch_split (blend_stream / split_event both NULL =
+ * the blend on `stream`), with optional stage events: stage_events NULL or 5
+ * caller-created cudaEvent_t (HOST handles, timing enabled) recorded as in
+ * fdgs_render_timed -- events 0-2 by event-record nodes inside the graph
+ * (re-pointed at this frame's events), 3-4 around the blend.  ASYNC. */
+fdgs_status fdgs_render_graph_launch_timed(fdgs_render_graph *graph, const fdgs_scene *scene,
+                                           const uint32_t *d_mask_l, const uint32_t *d_mask_r,
+                                           const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T,
+                                           void *stream, void *blend_stream, void *split_event,
+                                           void *const *stage_events);
 fdgs_status fdgs_render_graph_destroy(fdgs_render_graph *graph);
 
 /* Batched submission of frames over a pipeline of render workspaces (the

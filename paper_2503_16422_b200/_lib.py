@@ -23,6 +23,7 @@ EXPORTS = [
     "fdgs_render_workspace_bytes", "fdgs_render", "fdgs_render_timed", "fdgs_render_split", "fdgs_render_checked",
     "fdgs_render_debug_views", "fdgs_render_graph_create", "fdgs_render_graph_launch", "fdgs_render_graph_destroy",
     "fdgs_render_graph_launch_split",
+    "fdgs_render_graph_launch_timed",
     "fdgs_keyframe_workspace_bytes", "fdgs_keyframe_mask", "fdgs_mask_or",
     "fdgs_keyframe_mask_contrib_workspace_bytes", "fdgs_keyframe_mask_contrib",
     "fdgs_mask_compact_workspace_bytes", "fdgs_mask_compact", "fdgs_stv_workspace_bytes", "fdgs_stv_score",
@@ -109,6 +110,7 @@ def lib():
             "fdgs_render_graph_create": ([P, I32, I32, P, SZ, I64, P], C.c_int),
             "fdgs_render_graph_launch": ([P, P, P, P, P, F, P, P, P], C.c_int),
             "fdgs_render_graph_launch_split": ([P, P, P, P, P, F, P, P, P, P, P], C.c_int),
+            "fdgs_render_graph_launch_timed": ([P, P, P, P, P, F, P, P, P, P, P, P], C.c_int),
             "fdgs_render_graph_destroy": ([P], C.c_int),
             "fdgs_keyframe_workspace_bytes": ([I32], SZ),
             "fdgs_keyframe_mask": ([P, P, I32, F, P, P, SZ, P], C.c_int),

@@ -209,11 +209,12 @@ class Renderer:
             pass
 
     def render_graph(self, cam, t, mask_l=None, mask_r=None, out=None, out_T=None, stream=None, scene=None,
-                     blend_stream=None, split_event=None):
-        """fdgs_render_graph_launch: the front end as one CUDA-graph launch (captured
-        on first use for this workspace) and the blend launched after it -- on
-        `blend_stream` ordered by `split_event` when given
-        (fdgs_render_graph_launch_split); results identical to render().  Async."""
+                     blend_stream=None, split_event=None, stage_events=None):
+        """fdgs_render_graph_launch_timed: the front end as one CUDA-graph launch
+        (captured on first use for this workspace) and the blend launched after
+        it -- on `blend_stream` ordered by `split_event` when given; optional
+        stage_events (5 torch.cuda.Event, as render()); results identical to
+        render().  Async."""
         if cam.width != self.width or cam.height != self.height:
             raise ValueError("camera size differs from the renderer's")
         out = self.new_output() if out is None else out
@@ -226,15 +227,21 @@ class Renderer:
             check(lib().fdgs_render_graph_create(C.byref(base.struct), self.width, self.height, _ptr(self.ws),
                                                  self.ws_bytes, self.max_entries, C.byref(h)))
             self._graph = h
-        if blend_stream is None:
-            check(lib().fdgs_render_graph_launch(self._graph, C.byref(sc.struct), ml, mr, C.byref(cs), float(t),
-                                                 _ptr(out), _ptr(out_T), _stream_ptr(stream)))
-            return out
-        if split_event.cuda_event == 0:
-            split_event.record(stream)  # materialise the CUDA event
-        check(lib().fdgs_render_graph_launch_split(self._graph, C.byref(sc.struct), ml, mr, C.byref(cs), float(t),
+        evs = None
+        if stage_events is not None:
+            for e in stage_events:
+                if e.cuda_event == 0:
+                    e.record(stream)  # materialise the CUDA event
+            evs = (C.c_void_p * 5)(*[e.cuda_event for e in stage_events])
+        split = None
+        if blend_stream is not None:
+            if split_event.cuda_event == 0:
+                split_event.record(stream)
+            split = C.c_void_p(split_event.cuda_event)
+        check(lib().fdgs_render_graph_launch_timed(self._graph, C.byref(sc.struct), ml, mr, C.byref(cs), float(t),
                                                    _ptr(out), _ptr(out_T), _stream_ptr(stream),
-                                                   _stream_ptr(blend_stream), C.c_void_p(split_event.cuda_event)))
+                                                   None if blend_stream is None else _stream_ptr(blend_stream),
+                                                   split, evs))
         return out
 
     def _scene_for(self, scene, stream):
@@ -533,15 +540,18 @@ class RenderPipeline:
             sc = fr[4] if len(fr) > 4 else None  # optional per-frame scene (a compacted working set)
             i = k % self.depth
             r = self.renderers[i]
-            if self.graphs and self.split:
+            graph = self.graphs and stats is None  # work counters: the counting blend, stream launches
+            if graph and self.split:
                 if k >= self.depth:  # the workspace is free once its previous blend is done
                     self.done_ev[i].record(self.blend[i])
                     self.front[i].wait_event(self.done_ev[i])
                 r.render_graph(cam, t, ml, mr, out=outs[k], stream=self.front[i], scene=sc,
-                               blend_stream=self.blend[i], split_event=self.split_ev[i])
+                               blend_stream=self.blend[i], split_event=self.split_ev[i],
+                               stage_events=None if stage_events is None else stage_events[k])
                 last = self.blend[i]
-            elif self.graphs:
-                r.render_graph(cam, t, ml, mr, out=outs[k], stream=self.front[i], scene=sc)
+            elif graph:
+                r.render_graph(cam, t, ml, mr, out=outs[k], stream=self.front[i], scene=sc,
+                               stage_events=None if stage_events is None else stage_events[k])
                 last = self.front[i]
             elif not self.split:
                 r.render(cam, t, ml, mr, out=outs[k], stats=None if stats is None else stats[k], stream=self.front[i],

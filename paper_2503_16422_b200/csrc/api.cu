@@ -384,6 +384,15 @@ fdgs_status fdgs_render_graph_launch_split(fdgs_render_graph *graph, const fdgs_
                                            const uint32_t *d_mask_l, const uint32_t *d_mask_r,
                                            const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T,
                                            void *stream, void *blend_stream, void *split_event) {
+    return fdgs_render_graph_launch_timed(graph, scene, d_mask_l, d_mask_r, cam, t, d_out_rgb, d_out_T, stream,
+                                          blend_stream, split_event, nullptr);
+}
+
+fdgs_status fdgs_render_graph_launch_timed(fdgs_render_graph *graph, const fdgs_scene *scene,
+                                           const uint32_t *d_mask_l, const uint32_t *d_mask_r,
+                                           const fdgs_camera *cam, float t, float *d_out_rgb, float *d_out_T,
+                                           void *stream, void *blend_stream, void *split_event,
+                                           void *const *stage_events) {
     if ((blend_stream == nullptr) != (split_event == nullptr))
         return fail(FDGS_ERR_INVALID_ARG, "blend_stream and split_event go together");
     if (graph == nullptr) return fail(FDGS_ERR_INVALID_ARG, "graph is NULL");
@@ -399,7 +408,7 @@ fdgs_status fdgs_render_graph_launch_split(fdgs_render_graph *graph, const fdgs_
     if (d_mask_l == nullptr && d_mask_r != nullptr) d_mask_l = d_mask_r, d_mask_r = nullptr;
     cudaError_t e = render_graph_launch(*graph->impl, make_scenedev(*scene), d_mask_l, d_mask_r, cd, t, d_out_rgb,
                                         d_out_T, (cudaStream_t)stream, (cudaStream_t)blend_stream,
-                                        (cudaEvent_t)split_event);
+                                        (cudaEvent_t)split_event, reinterpret_cast<cudaEvent_t const *>(stage_events));
     return e == cudaSuccess ? FDGS_OK : cuda_fail(e, "fdgs_render_graph_launch");
 }
 

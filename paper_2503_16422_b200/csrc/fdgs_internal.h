@@ -125,7 +125,8 @@ cudaError_t render_graph_build(RenderGraphImpl &g, const SceneDev &sc, const Cam
                                const RenderLayout &L);
 cudaError_t render_graph_launch(RenderGraphImpl &g, const SceneDev &sc, const uint32_t *mask_l,
                                 const uint32_t *mask_r, const CamDev &cam, float t, float *out_rgb, float *out_T,
-                                cudaStream_t st, cudaStream_t blend_st = nullptr, cudaEvent_t split_ev = nullptr);
+                                cudaStream_t st, cudaStream_t blend_st = nullptr, cudaEvent_t split_ev = nullptr,
+                                cudaEvent_t const *ev = nullptr);
 void render_graph_free(RenderGraphImpl &g);
 RenderGraphImpl *render_graph_new();
 void render_graph_delete(RenderGraphImpl *g);

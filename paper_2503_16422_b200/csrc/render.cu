@@ -1587,6 +1587,15 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
 #define FDGS_ITEM_GRID 2
 #endif
 static_assert(FDGS_PGRID >= 1 && FDGS_PGRID_DIV >= 1 && FDGS_BIN_GRID >= 1 && FDGS_ITEM_GRID >= 1, "grid shapes");
+#ifndef FDGS_ZERO_KERNEL
+#define FDGS_ZERO_KERNEL 1
+#endif
+__global__ void __launch_bounds__(256) k_zero(uint4 *__restrict__ p, size_t n16) {
+    for (size_t i = threadIdx.x; i < n16; i += 256) p[i] = make_uint4(0u, 0u, 0u, 0u);
+}
+#ifndef FDGS_ROW_BITS_ADAPT
+#define FDGS_ROW_BITS_ADAPT 1
+#endif
 static int sort_grid(int p_sort) { return std::max(1, FDGS_PGRID * p_sort / FDGS_PGRID_DIV); }
 
 static void launch_timed_blend(const uint32_t *tstart, const uint32_t *entries, const float4 *rec0,
@@ -1615,10 +1624,20 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     uint32_t *vis = reinterpret_cast<uint32_t *>(ws + L.vis);
 
     cudaError_t e = cudaSuccess;
-    if (ev && (e = cudaEventRecord(ev[0], st)) != cudaSuccess) return e;
+    // stage events; captured (front_only) as event-record nodes of the graph
+    auto rec = [&](int k) {
+        return front_only ? cudaEventRecordWithFlags(ev[k], st, cudaEventRecordExternal) : cudaEventRecord(ev[k], st);
+    };
+    if (ev && (e = rec(0)) != cudaSuccess) return e;
     {
+#if FDGS_ZERO_KERNEL
+        // counters, digit bases, histograms: a kernel, not a memset (a memset
+        // node in a captured graph adds a copy-engine hop to every frame)
+        k_zero<<<1, 256, 0, st>>>(reinterpret_cast<uint4 *>(ws + L.counters), (L.zero_end - L.counters) / 16);
+#else
         e = cudaMemsetAsync(ws + L.counters, 0, L.zero_end - L.counters, st);  // counters, look-back, histograms
         if (e != cudaSuccess) return e;
+#endif
         if (sc.n > 0) {
             uint32_t *cbits = reinterpret_cast<uint32_t *>(ws + L.surv_bits);
             uint32_t *ccnt = reinterpret_cast<uint32_t *>(ws + L.cull_cnt);
@@ -1632,7 +1651,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
             k_count_scan<<<1, 1024, 0, st>>>(vcnt, L.n_parts, &ctr->n_surv, kSliceItems, &ctr->n_vis);
             k_vis_emit<<<L.slice_grid, kPreBlock, 0, st>>>(vbits, vcnt, ctr, depth, vis, keys[1]);
         }
-        if (ev && (e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
+        if (ev && (e = rec(1)) != cudaSuccess) return e;
         uint32_t *gbase = reinterpret_cast<uint32_t *>(ws + L.sort_gbase);  // [4][256] depth digit bases
         uint32_t *epoch = reinterpret_cast<uint32_t *>(ws + L.epoch);
         uint64_t *sstat = reinterpret_cast<uint64_t *>(ws + L.sort_status);
@@ -1648,7 +1667,7 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
                 sstat + (size_t)pass * L.sort_parts * 256, rect, pass == 3 ? rect_sorted : nullptr);
         }
         const uint32_t *order = vals[1];
-        if (ev && (e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
+        if (ev && (e = rec(2)) != cudaSuccess) return e;
         int *rowdiff = reinterpret_cast<int *>(ws + L.row_diff);
         uint32_t *rbase = reinterpret_cast<uint32_t *>(ws + L.tile_gbase);  // [0..255] pass 0, [256..511] pass 1
         uint32_t *row_start = reinterpret_cast<uint32_t *>(ws + L.row_start);
@@ -1675,9 +1694,20 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
         // stable partition of the row items by tile row (canonical order kept within a row)
         const int rgrid = std::min((int)item_chunks, sort_grid(L.p_sort));
         const uint32_t *sorted_items = ival[0];
-        k_onesweep<8, kTileSortItems><<<rgrid, kSortThreads, 0, st>>>(ikey[0], nullptr, L.tiles_y > 256 ? ikey[1] : nullptr, ival[0],
-                                                       &ctr->n_items_part, epoch, &ctr->tile_ticket[0], 0, rbase, tstat,
-                                                       nullptr, nullptr);
+        // one pass when the rows fit its digit (6/7/8 bits: the digit width
+        // follows tiles_y, so the per-digit scans and look-backs cover only
+        // digits that can occur; C3/C4's 64 rows take 64 digits, not 256)
+        auto row_pass0 = [&](auto bits) {
+            k_onesweep<decltype(bits)::value, kTileSortItems><<<rgrid, kSortThreads, 0, st>>>(
+                ikey[0], nullptr, L.tiles_y > 256 ? ikey[1] : nullptr, ival[0], &ctr->n_items_part, epoch,
+                &ctr->tile_ticket[0], 0, rbase, tstat, nullptr, nullptr);
+        };
+#if FDGS_ROW_BITS_ADAPT
+        if (L.tiles_y <= 64) row_pass0(std::integral_constant<int, 6>{});
+        else if (L.tiles_y <= 128) row_pass0(std::integral_constant<int, 7>{});
+        else
+#endif
+        row_pass0(std::integral_constant<int, 8>{});
         if (L.tiles_y > 256) {
             k_onesweep<8, kTileSortItems><<<rgrid, kSortThreads, 0, st>>>(ikey[1], ival[0], nullptr, ival[1], &ctr->n_items_part, epoch,
                                                            &ctr->tile_ticket[1], 8, rbase + 256,
@@ -1741,6 +1771,11 @@ struct RenderGraphImpl {
     cudaGraphExec_t exec = nullptr;
     cudaGraphNode_t n_cull = nullptr, n_emit = nullptr, n_slice = nullptr;
     cudaKernelNodeParams p_cull{}, p_emit{}, p_slice{};
+    // stage events 0-2 (front-end start, after preprocess, after the depth
+    // sort) as event-record nodes, re-pointed per launch at the caller's events
+    cudaEvent_t ph[3] = {nullptr, nullptr, nullptr};  // the nodes' events when the launch passes none
+    cudaGraphNode_t n_ev[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t cur_ev[3] = {nullptr, nullptr, nullptr};
     RenderLayout L{};
     char *ws = nullptr;
 };
@@ -1753,9 +1788,12 @@ cudaError_t render_graph_build(RenderGraphImpl &g, const SceneDev &sc, const Cam
     // the caller's blend stream), so it keeps the stream-priority split
     cudaStream_t s1 = nullptr;
     cudaError_t e = cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking);
+    for (int k = 0; k < 3 && e == cudaSuccess; ++k) e = cudaEventCreate(&g.ph[k]);
+    for (int k = 0; k < 3; ++k) g.cur_ev[k] = g.ph[k];
+    cudaEvent_t evs[5] = {g.ph[0], g.ph[1], g.ph[2], nullptr, nullptr};
     if (e == cudaSuccess) e = cudaStreamBeginCapture(s1, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
-        cudaError_t le = launch_render(sc, nullptr, nullptr, cam, 0.0f, nullptr, nullptr, ws, L, nullptr, s1, nullptr,
+        cudaError_t le = launch_render(sc, nullptr, nullptr, cam, 0.0f, nullptr, nullptr, ws, L, nullptr, s1, evs,
                                        nullptr, nullptr, nullptr, nullptr, true);
         cudaError_t ee = cudaStreamEndCapture(s1, &g.graph);
         e = le != cudaSuccess ? le : ee;
@@ -1769,7 +1807,15 @@ cudaError_t render_graph_build(RenderGraphImpl &g, const SceneDev &sc, const Cam
         if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
         for (size_t k = 0; e == cudaSuccess && k < nn; ++k) {
             cudaGraphNodeType ty;
-            if ((e = cudaGraphNodeGetType(nodes[k], &ty)) != cudaSuccess || ty != cudaGraphNodeTypeKernel) continue;
+            if ((e = cudaGraphNodeGetType(nodes[k], &ty)) != cudaSuccess) break;
+            if (ty == cudaGraphNodeTypeEventRecord) {
+                cudaEvent_t x = nullptr;
+                if ((e = cudaGraphEventRecordNodeGetEvent(nodes[k], &x)) != cudaSuccess) break;
+                for (int j = 0; j < 3; ++j)
+                    if (x == g.ph[j]) g.n_ev[j] = nodes[k];
+                continue;
+            }
+            if (ty != cudaGraphNodeTypeKernel) continue;
             cudaKernelNodeParams p{};
             if ((e = cudaGraphKernelNodeGetParams(nodes[k], &p)) != cudaSuccess) break;
             cudaKernelNodeAttrValue pr{};
@@ -1779,7 +1825,8 @@ cudaError_t render_graph_build(RenderGraphImpl &g, const SceneDev &sc, const Cam
             else if (p.func == (void *)k_cull_emit) g.n_emit = nodes[k], g.p_emit = p;
             else if (p.func == (void *)k_slice) g.n_slice = nodes[k], g.p_slice = p;
         }
-        if (e == cudaSuccess && (!g.n_cull || !g.n_emit || !g.n_slice)) e = cudaErrorInvalidValue;
+        if (e == cudaSuccess && (!g.n_cull || !g.n_emit || !g.n_slice || !g.n_ev[0] || !g.n_ev[1] || !g.n_ev[2]))
+            e = cudaErrorInvalidValue;
     }
     // front-end nodes at the device's greatest priority, whatever the launching stream's
     if (e == cudaSuccess) e = cudaGraphInstantiateWithFlags(&g.exec, g.graph, cudaGraphInstantiateFlagUseNodePriority);
@@ -1789,7 +1836,8 @@ cudaError_t render_graph_build(RenderGraphImpl &g, const SceneDev &sc, const Cam
 
 cudaError_t render_graph_launch(RenderGraphImpl &g, const SceneDev &sc, const uint32_t *mask_l,
                                 const uint32_t *mask_r, const CamDev &cam, float t, float *out_rgb, float *out_T,
-                                cudaStream_t st, cudaStream_t blend_st, cudaEvent_t split_ev) {
+                                cudaStream_t st, cudaStream_t blend_st, cudaEvent_t split_ev,
+                                cudaEvent_t const *ev) {
     const RenderLayout &L = g.L;
     char *ws = g.ws;
     Counters *ctr = reinterpret_cast<Counters *>(ws + L.counters);
@@ -1829,6 +1877,11 @@ cudaError_t render_graph_launch(RenderGraphImpl &g, const SceneDev &sc, const ui
     p.kernelParams = a_slice;
     p.extra = nullptr;
     if (e == cudaSuccess) e = cudaGraphExecKernelNodeSetParams(g.exec, g.n_slice, &p);
+    for (int k = 0; k < 3 && e == cudaSuccess; ++k) {  // the stage events of this frame (or the placeholders)
+        cudaEvent_t want = ev ? ev[k] : g.ph[k];
+        if (want != g.cur_ev[k] && (e = cudaGraphExecEventRecordNodeSetEvent(g.exec, g.n_ev[k], want)) == cudaSuccess)
+            g.cur_ev[k] = want;
+    }
     if (e == cudaSuccess) e = cudaGraphLaunch(g.exec, st);
     if (e != cudaSuccess) return e;
     // the timed blend, launched directly (on the blend stream when given)
@@ -1838,13 +1891,19 @@ cudaError_t render_graph_launch(RenderGraphImpl &g, const SceneDev &sc, const ui
         if ((e = cudaStreamWaitEvent(blend_st, split_ev, 0)) != cudaSuccess) return e;
         bst = blend_st;
     }
+    if (ev && (e = cudaEventRecord(ev[3], bst)) != cudaSuccess) return e;
     launch_timed_blend(tstart, entries, rec0, rec1, rec2, cctr, L, cam, out_rgb, out_T, bst);
+    if (ev && (e = cudaEventRecord(ev[4], bst)) != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
 void render_graph_free(RenderGraphImpl &g) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
     if (g.graph) cudaGraphDestroy(g.graph);
+    for (auto &x : g.ph) {
+        if (x) cudaEventDestroy(x);
+        x = nullptr;
+    }
     g.exec = nullptr;
     g.graph = nullptr;
 }

@@ -458,6 +458,23 @@ def test_cuda_graph_frames_equal_launched_frames():
     torch.cuda.synchronize()
     for ref, o in zip(refs, outs):
         assert torch.equal(ref, o)
+    # stage events through the graph (event-record nodes re-pointed per frame),
+    # then a batch without events (the nodes fall back to their own events)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in frames]
+    outs = [pipe.renderers[0].new_output() for _ in frames]
+    pipe.render_many(frames, outs, stage_events=evs)
+    torch.cuda.synchronize()
+    for ref, o, ev in zip(refs, outs, evs):
+        assert torch.equal(ref, o)
+        dt = [ev[k].elapsed_time(ev[k + 1]) for k in range(4)]
+        assert all(x >= 0.0 for x in dt) and sum(dt) > 0.0, dt
+    stamp = [ev[0].elapsed_time(ev[4]) for ev in evs]
+    outs = [pipe.renderers[0].new_output() for _ in frames]
+    pipe.render_many(frames, outs)
+    torch.cuda.synchronize()
+    for ref, o in zip(refs, outs):
+        assert torch.equal(ref, o)
+    assert stamp == [ev[0].elapsed_time(ev[4]) for ev in evs]  # not re-recorded
 
 
 def test_aabb_redundant_flag_sound():

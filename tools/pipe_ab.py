@@ -111,7 +111,9 @@ def main():
         for _ in range(2):
             step(pipes[v], False)
     for r in range(a.rounds):
-        for v in a.variants:
+        p0 = ptr[0]
+        for v in a.variants:  # every variant renders the same frames in a round
+            ptr[0] = p0
             use_lib(libs[v])
             sync_now[0] = syncs[v]
             for _ in range(a.steps):
