@@ -206,10 +206,11 @@ fdgs_status fdgs_render_checked(const fdgs_scene *scene, const uint32_t *d_mask_
                                 void *stream);
 
 /* CUDA-graph form of fdgs_render (the same kernels and results): the frame's
- * the ~20 front-end launches are captured once per (workspace, layout) and
+ * 21 front-end launches are captured once per (workspace, layout) and
  * replayed with one graph launch per frame; only the arguments that change
- * between frames are updated (scene, masks, t, camera).  Front-end nodes
- * carry the device's greatest stream priority.  The blend (the timed
+ * between frames are updated (scene, masks, t, camera, stage events).
+ * Front-end nodes carry the device's greatest stream priority (cf. P:478:
+ * the FPS of the whole render call).  The blend (the timed
  * k_blend_wi, no work counters) is launched directly after the graph, on the
  * same stream or (fdgs_render_graph_launch_split) on a blend stream.
  *   create: `scene` fixes the layout (max(n, n_capacity)); d_ws / ws_bytes /

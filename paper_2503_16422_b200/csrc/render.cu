@@ -538,6 +538,10 @@ __device__ __forceinline__ TileRect tile_rect(uint2 r) {
 // of kScanNT Gaussians: the ny total, the band constants of the tile cover and
 // the per-tile-row item counts), k_count_scan over the partitions, then
 // k_bin_offsets (block scan + partition base).
+#ifndef FDGS_ITEM_ILP
+#define FDGS_ITEM_ILP 2
+#endif
+constexpr int kItemIlp = FDGS_ITEM_ILP;  // k_row_items / k_row_count: row items in flight per thread
 constexpr int kScanNT = 256;     // threads (= items) per scan partition
 constexpr int kItemTile = kScanNT;  // row items per chunk / partition
 __global__ void __launch_bounds__(kScanNT) k_bin_count(const uint2 *__restrict__ rects,
@@ -639,19 +643,44 @@ __global__ void __launch_bounds__(kScanNT) k_row_items(const uint2 *__restrict__
         if (ni > item_cap) c->status = FDGS_ERR_OVERFLOW;
     }
     if (ni > item_cap) return;  // more row items than the workspace holds
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ni; i += gridDim.x * blockDim.x) {
-        const uint32_t r = __ldg(item_v + i);  // owning Gaussian (canonical rank), from k_bin_offsets
-        const int ty = (int)__ldg(item_key + i);
-        const uint2 rc = __ldg(rects + r);
-        const int px0 = rc.x & 0xffff, px1 = rc.x >> 16, py0 = rc.y & 0xffff, py1 = rc.y >> 16;
-        const uint32_t v = __ldg(order + r);
-        const float4 a = __ldg(rec0 + v), b = __ldg(rec1 + v);
-        int txa, txb;
-        uint32_t pack = 0u;  // empty row: txb + 1 <= txa
-        if (band_tiles(bconst[r], a.x, a.y, a.z, a.w, b.x, px0, px1, py0, py1, ty, txa, txb))
-            pack = (uint32_t)txa | ((uint32_t)(txb + 1) << 16);
-        item_pack[i] = pack;
-        item_v[i] = v;  // the owner index is replaced by the record slot
+    // kItemIlp items per thread and iteration, their three levels of dependent
+    // loads (item -> Gaussian -> record) issued together: the kernel is bound
+    // by the latency of those gathers, not by the band arithmetic
+    constexpr int U = kItemIlp;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < ni; i0 += U * stride) {
+        uint32_t r[U], v[U];
+        int ty[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t i = i0 + u * stride < ni ? i0 + u * stride : i0;  // past the end: this thread's own first item again, not stored
+            r[u] = __ldg(item_v + i);  // owning Gaussian (canonical rank), from k_bin_offsets
+            ty[u] = (int)__ldg(item_key + i);
+        }
+        uint2 rc[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            rc[u] = __ldg(rects + r[u]);
+            v[u] = __ldg(order + r[u]);
+        }
+        float4 a[U], b[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            a[u] = __ldg(rec0 + v[u]);
+            b[u] = __ldg(rec1 + v[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t i = i0 + u * stride;
+            if (i >= ni) break;
+            const int px0 = rc[u].x & 0xffff, px1 = rc[u].x >> 16, py0 = rc[u].y & 0xffff, py1 = rc[u].y >> 16;
+            int txa, txb;
+            uint32_t pack = 0u;  // empty row: txb + 1 <= txa
+            if (band_tiles(bconst[r[u]], a[u].x, a[u].y, a[u].z, a[u].w, b[u].x, px0, px1, py0, py1, ty[u], txa, txb))
+                pack = (uint32_t)txa | ((uint32_t)(txb + 1) << 16);
+            item_pack[i] = pack;
+            item_v[i] = v[u];  // the owner index is replaced by the record slot
+        }
     }
 }
 
@@ -834,12 +863,20 @@ __global__ void __launch_bounds__(FDGS_ROWCNT_THREADS) k_row_count(const uint32_
     __syncthreads();
     uint32_t lo, hi;
     row_seg_range(row_start, ty, seg, lo, hi);
-    for (uint32_t r = lo + tid; r < hi; r += blockDim.x) {
-        const uint32_t pk = __ldg(item_pack + __ldg(sorted + r));
-        const int txa = (int)(pk & 0xffffu), txe = (int)(pk >> 16);
-        if (txe > txa) {
-            atomicAdd(&s_d[txa], 1);
-            atomicAdd(&s_d[txe], -1);
+    constexpr int U = kItemIlp;  // items in flight per thread (their two dependent loads issued together)
+    for (uint32_t r0 = lo + tid; r0 < hi; r0 += U * blockDim.x) {
+        uint32_t it[U], pk[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) it[u] = __ldg(sorted + min(r0 + u * blockDim.x, hi - 1));
+#pragma unroll
+        for (int u = 0; u < U; ++u) pk[u] = __ldg(item_pack + it[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int txa = (int)(pk[u] & 0xffffu), txe = (int)(pk[u] >> 16);
+            if (r0 + u * blockDim.x < hi && txe > txa) {
+                atomicAdd(&s_d[txa], 1);
+                atomicAdd(&s_d[txe], -1);
+            }
         }
     }
     __syncthreads();
