@@ -155,6 +155,11 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        after = not self.lines  # a timed region shorter than the sampling interval
+        if after:
+            t0 = time.perf_counter()
+            while not self.lines and time.perf_counter() - t0 < 2.0:
+                time.sleep(0.01)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -174,8 +179,11 @@ class ClockSampler:
             for nm, v in zip(names, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+               "reasons": sorted(reasons), "samples": len(sm)}
+        if after:
+            out["note"] = "timed region shorter than the 200 ms sampling interval: first sample after it"
+        return out
 
 
 # ----------------------------------------------------------------- helpers

@@ -379,18 +379,23 @@ class RenderPipeline:
     stream (fdgs_render_split), so the latency-bound front end of later frames
     is scheduled ahead of, and overlaps, the ALU-bound blends.
 
-    native=True: render_many submits the whole batch through
-    fdgs_pipeline_render -- one C call, frames issued in order on the calling
-    thread (threads > 1: in parallel by that many host threads, cheaper on the
-    host but slower on the device).  The default is the per-frame loop below:
-    its host cost is the same (the CUDA calls dominate, ~60 us per frame) and
-    it measured 1-2% faster on the device."""
+    graphs (default True unless native): each frame's front end is one
+    CUDA-graph launch (fdgs_render_graph_launch_timed) and its blend one
+    kernel launch -- ~0.02 ms of host time per frame at the device throughput
+    of stream launches; graphs=False launches the
+    front end's kernels one by one (~0.065 ms per frame).  native=True:
+    render_many submits the whole batch through fdgs_pipeline_render -- one C
+    call issuing stream launches in order on the calling thread (threads > 1:
+    in parallel by that many host threads, cheaper on the host but slower on
+    the device)."""
 
     def __init__(self, scene: Scene, width: int, height: int, depth: int = 4, max_entries: int | None = None,
-                 split: bool = True, copy_streams: int = 1, graphs: bool = False, native: bool | None = None,
+                 split: bool = True, copy_streams: int = 1, graphs: bool | None = None, native: bool | None = None,
                  threads: int = 1):
         self.renderers = [Renderer(scene, width, height, max_entries) for _ in range(depth)]
         self.native = False if native is None else bool(native)
+        if graphs is None:
+            graphs = not self.native
         if self.native and graphs:
             raise ValueError("the native batch submission launches streams, not graphs")
         self.threads = max(1, int(threads))

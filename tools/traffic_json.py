@@ -12,7 +12,7 @@ import sys
 from collections import defaultdict
 
 PER_FRAME = {"k_count_scan": 3, "k_onesweep": 5}   # launches per frame (tile grid <= 256 rows)
-FRAME_KERNELS = ("k_cull", "k_count_scan", "k_cull_emit", "k_slice", "k_vis_emit", "k_sort_hist", "k_onesweep",
+FRAME_KERNELS = ("k_zero", "k_cull", "k_count_scan", "k_cull_emit", "k_slice", "k_vis_emit", "k_sort_hist", "k_onesweep",
                  "k_bin_count", "k_bin_offsets", "k_row_items", "k_row_scan", "k_row_count", "k_tile_scan",
                  "k_row_scatter", "k_blend_wi")
 
