@@ -84,8 +84,8 @@ def parse():
     p.add_argument("--no-graphs", action="store_true",
                    help="launch the front end's kernels one by one instead of one CUDA-graph launch per frame")
     p.add_argument("--native-submit", action="store_true",
-                   help="submit each step's frames with one fdgs_pipeline_render call (stream launches, implies "
-                        "--no-graphs) instead of the per-frame loop")
+                   help="submit each step's frames with one fdgs_pipeline_render call instead of the per-frame "
+                        "loop")
     p.add_argument("--submit-threads", type=int, default=1,
                    help="host threads of fdgs_pipeline_render (1: frames issued in order; more cost device throughput)")
     p.add_argument("--copy-streams", type=int, default=1, help="e2e: D2H copy streams of the pipeline")
@@ -308,7 +308,7 @@ def run_ours(args):
     import paper_2503_16422_b200 as fd  # (the library itself loads on first use: not in --fake-render)
 
     fake = args.fake_render
-    graphs = not (args.no_graphs or args.native_submit)
+    graphs = not args.no_graphs
     rank, world, local = fdist.env_ranks()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
@@ -521,7 +521,9 @@ def run_ours(args):
                        "frames_per_step": F, "frames_per_rank": frames_rank, "partition": "frame f -> rank f mod N",
                        "l2": "flushed between steps (512 MiB write)", "parallelism": f"frames x{world}",
                        "streams_per_gpu": args.streams,
-                       "submission": ("native batch (fdgs_pipeline_render)" if args.native_submit else
+                       "submission": (("native batch (fdgs_pipeline_render)" +
+                                       (", front end as each slot's CUDA graph" if graphs else ""))
+                                      if args.native_submit else
                                       "per frame: one CUDA-graph launch of the front end + the blend launch"
                                       if graphs else "per frame: ~22 kernel launches"),
                        "stream_split": "front end high priority, blend low priority" if not args.no_split else "none",

@@ -268,17 +268,23 @@ fdgs_status fdgs_render_graph_destroy(fdgs_render_graph *graph);
  *   copy stream k mod n_copy after the blend; d_status (nullable, DEVICE 16
  *   bytes): the frame's {n_act, n_vis, n_entries, status} after the blend;
  *   done_event (nullable cudaEvent_t): recorded once the frame is complete.
+ *   fdgs_pipeline_slot.graph (nullable): a fdgs_render_graph created on the
+ *   slot's workspace; the slot's timed frames (d_stats NULL) then launch the
+ *   front end as that graph (fdgs_render_graph_launch_timed: one launch per
+ *   frame instead of ~21), frames with d_stats as stream launches.  The
+ *   caller keeps the graph alive while the pipeline uses it.
  *   fdgs_pipeline_render: ASYNC on `stream`: every slot and copy stream first
  *   waits for `stream`'s work, and `stream` waits for every frame and copy of
  *   the batch; stage_events (nullable): 5 caller-created events per job, as
  *   fdgs_render_timed.  Returns when every launch is issued.  One batch at a
  *   time per handle.
- * Errors: INVALID_ARG, those of fdgs_render_split, CUDA. */
+ * Errors: INVALID_ARG, those of fdgs_render_split / fdgs_render_graph_launch_timed, CUDA. */
 typedef struct {
     void *d_ws;
     size_t ws_bytes;
     int64_t max_entries;
     void *front_stream, *blend_stream;
+    fdgs_render_graph *graph;
 } fdgs_pipeline_slot;
 typedef struct {
     fdgs_scene scene;

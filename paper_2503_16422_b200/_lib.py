@@ -59,7 +59,7 @@ class FdgsDebugViews(C.Structure):
 
 class FdgsPipelineSlot(C.Structure):
     _fields_ = [("d_ws", C.c_void_p), ("ws_bytes", C.c_size_t), ("max_entries", C.c_int64),
-                ("front_stream", C.c_void_p), ("blend_stream", C.c_void_p)]
+                ("front_stream", C.c_void_p), ("blend_stream", C.c_void_p), ("graph", C.c_void_p)]
 
 
 class FdgsFrameJob(C.Structure):

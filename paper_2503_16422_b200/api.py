@@ -208,6 +208,16 @@ class Renderer:
         except Exception:
             pass
 
+    def _ensure_graph(self):
+        """The front-end graph of this workspace (captured on first use)."""
+        if not self._graph:
+            h = C.c_void_p()
+            base = self.scene  # the layout is the full scene's (working sets share it, n_capacity)
+            check(lib().fdgs_render_graph_create(C.byref(base.struct), self.width, self.height, _ptr(self.ws),
+                                                 self.ws_bytes, self.max_entries, C.byref(h)))
+            self._graph = h
+        return self._graph
+
     def render_graph(self, cam, t, mask_l=None, mask_r=None, out=None, out_T=None, stream=None, scene=None,
                      blend_stream=None, split_event=None, stage_events=None):
         """fdgs_render_graph_launch_timed: the front end as one CUDA-graph launch
@@ -221,12 +231,7 @@ class Renderer:
         sc = self._scene_for(scene, stream)
         ml, mr = self._masks(mask_l, mask_r, sc)
         cs = camera_struct(cam) if not isinstance(cam, FdgsCamera) else cam
-        if not self._graph:
-            h = C.c_void_p()
-            base = self.scene  # the layout is the full scene's (working sets share it, n_capacity)
-            check(lib().fdgs_render_graph_create(C.byref(base.struct), self.width, self.height, _ptr(self.ws),
-                                                 self.ws_bytes, self.max_entries, C.byref(h)))
-            self._graph = h
+        self._ensure_graph()
         evs = None
         if stage_events is not None:
             for e in stage_events:
@@ -379,15 +384,15 @@ class RenderPipeline:
     stream (fdgs_render_split), so the latency-bound front end of later frames
     is scheduled ahead of, and overlaps, the ALU-bound blends.
 
-    graphs (default True unless native): each frame's front end is one
-    CUDA-graph launch (fdgs_render_graph_launch_timed) and its blend one
-    kernel launch -- ~0.02 ms of host time per frame at the device throughput
-    of stream launches; graphs=False launches the
-    front end's kernels one by one (~0.065 ms per frame).  native=True:
-    render_many submits the whole batch through fdgs_pipeline_render -- one C
-    call issuing stream launches in order on the calling thread (threads > 1:
-    in parallel by that many host threads, cheaper on the host but slower on
-    the device)."""
+    graphs (default True): each frame's front end is one CUDA-graph launch
+    (fdgs_render_graph_launch_timed) and its blend one kernel launch -- ~0.02
+    ms of host time per frame at the device throughput of stream launches
+    (DESIGN.md "CUDA graphs"); graphs=False launches the front end's kernels
+    one by one (~0.065 ms per frame).  native=True: render_many submits the
+    whole batch through fdgs_pipeline_render -- one C call issuing the frames
+    in order on the calling thread (with graphs: each slot's graph;
+    threads > 1: in parallel by that many host threads, cheaper on the host
+    but slower on the device)."""
 
     def __init__(self, scene: Scene, width: int, height: int, depth: int = 4, max_entries: int | None = None,
                  split: bool = True, copy_streams: int = 1, graphs: bool | None = None, native: bool | None = None,
@@ -395,9 +400,7 @@ class RenderPipeline:
         self.renderers = [Renderer(scene, width, height, max_entries) for _ in range(depth)]
         self.native = False if native is None else bool(native)
         if graphs is None:
-            graphs = not self.native
-        if self.native and graphs:
-            raise ValueError("the native batch submission launches streams, not graphs")
+            graphs = True
         self.threads = max(1, int(threads))
         self._handle = None
         self._handle_key = None
@@ -434,13 +437,14 @@ class RenderPipeline:
 
     def _native_handle(self):
         """fdgs_pipeline over the current workspaces (re-created when one grew)."""
-        key = tuple((r.ws.data_ptr(), r.ws_bytes, r.max_entries) for r in self.renderers)
+        graphs = [r._ensure_graph().value if self.graphs else None for r in self.renderers]
+        key = tuple((r.ws.data_ptr(), r.ws_bytes, r.max_entries, g) for r, g in zip(self.renderers, graphs))
         if self._handle is None or key != self._handle_key:
             self._drop_handle()
             slots = (FdgsPipelineSlot * self.depth)()
             for i, r in enumerate(self.renderers):
                 slots[i] = FdgsPipelineSlot(r.ws.data_ptr(), r.ws_bytes, r.max_entries, self.front[i].cuda_stream,
-                                            self.blend[i].cuda_stream if self.split else None)
+                                            self.blend[i].cuda_stream if self.split else None, graphs[i])
             cps = (C.c_void_p * len(self.copies))(*[c.cuda_stream for c in self.copies])
             h = C.c_void_p()
             check(lib().fdgs_pipeline_create(slots, self.depth, cps, len(self.copies), self.threads, C.byref(h)))

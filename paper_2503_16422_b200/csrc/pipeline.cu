@@ -83,7 +83,12 @@ fdgs_status submit(fdgs_pipeline *p, int w, int nw) {
             if ((e = cudaStreamWaitEvent(front, p->done_ev[s], 0)) != cudaSuccess) return cuda_status(e, "wait");
         }
         void *const *evs = p->stage_events ? p->stage_events + 5 * (size_t)k : nullptr;
-        fdgs_status st = blend ? fdgs_render_split(&J.scene, J.d_mask_l, J.d_mask_r, &J.cam, J.t, J.d_out_rgb,
+        fdgs_status st =
+            S.graph != nullptr && J.d_stats == nullptr
+                ? fdgs_render_graph_launch_timed(S.graph, &J.scene, J.d_mask_l, J.d_mask_r, &J.cam, J.t, J.d_out_rgb,
+                                                 J.d_out_T, S.front_stream, S.blend_stream,
+                                                 blend ? (void *)p->split_ev[s] : nullptr, evs)
+            : blend ? fdgs_render_split(&J.scene, J.d_mask_l, J.d_mask_r, &J.cam, J.t, J.d_out_rgb,
                                                    J.d_out_T, S.d_ws, S.ws_bytes, S.max_entries, J.d_stats,
                                                    S.front_stream, S.blend_stream, (void *)p->split_ev[s], evs)
                                : fdgs_render_timed(&J.scene, J.d_mask_l, J.d_mask_r, &J.cam, J.t, J.d_out_rgb,

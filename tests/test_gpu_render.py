@@ -338,9 +338,10 @@ def test_render_pipeline_matches_sequential():
         frames.append((cams[fr % 4], float(times[fr]), masks[l], masks[r]))
     seq = fd.Renderer(sc, W, H)
     refs = [seq.render_checked(cam, t, ml, mr)[0] for (cam, t, ml, mr) in frames]
-    for split, native, threads in ((False, False, 1), (True, False, 1), (False, True, 1), (True, True, 3),
-                                   (True, True, 2)):
-        pipe = fd.RenderPipeline(sc, W, H, depth=3, split=split, native=native, threads=threads)
+    for split, native, threads, graphs in ((False, False, 1, True), (True, False, 1, True), (False, True, 1, True),
+                                           (True, True, 3, True), (True, True, 2, True), (True, False, 1, False),
+                                           (True, True, 1, False), (False, False, 1, False)):
+        pipe = fd.RenderPipeline(sc, W, H, depth=3, split=split, native=native, threads=threads, graphs=graphs)
         outs = [pipe.renderers[0].new_output() for _ in frames]
         pipe.render_many(frames, outs)
         pipe.render_many(frames[::-1], outs[::-1])   # reuse every workspace again

@@ -41,7 +41,8 @@ def use_lib(name):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("variants", nargs="+",
-                    help="py | native:T | graphs, optionally @depth (native:3@8), #lib variant (native:1#sleep200)")
+                    help="py | native:T | graphs | gnative:T (native with graphs), optionally @depth (native:3@8), "
+                         "#lib variant (native:1#sleep200)")
     ap.add_argument("--config", default="c3")
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--steps", type=int, default=6)
@@ -83,8 +84,9 @@ def main():
         name, _, rest = spec.partition("@")
         depth = int(rest or 6)
         kind, _, thr = name.partition(":")
-        pipes[v] = fd.RenderPipeline(sc, cams[0].width, cams[0].height, depth=depth, graphs=kind == "graphs",
-                                     native=kind == "native", threads=int(thr or 3))
+        pipes[v] = fd.RenderPipeline(sc, cams[0].width, cams[0].height, depth=depth,
+                                     graphs=kind in ("graphs", "gnative"), native=kind in ("native", "gnative"),
+                                     threads=int(thr or 3))
     outs = [pipes[a.variants[0]].renderers[0].new_output() for _ in range(a.frames)]
     res = {v: [] for v in a.variants}
     host = {v: [] for v in a.variants}
