@@ -1403,8 +1403,11 @@ cudaError_t launch_debug_strip_reach(char *ws, const RenderLayout &L, uint8_t *o
 #ifndef FDGS_WI_PAIR
 #define FDGS_WI_PAIR 1
 #endif
+#ifndef FDGS_WI_VOTE
+#define FDGS_WI_VOTE 1  // the paired stop test as a warp vote (a uniform branch: no reconvergence barrier per pair)
+#endif
 #ifndef FDGS_WI_PAIR_UNROLL
-#define FDGS_WI_PAIR_UNROLL 2
+#define FDGS_WI_PAIR_UNROLL 4
 #endif
 constexpr int kWiPairUnroll = FDGS_WI_PAIR_UNROLL;
 
@@ -1505,7 +1508,11 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
         blend1(s_list[warp][q].a, s_list[warp][q].t[rr], kAabb, w1);
         const float2 T1 = T;
         blend1(s_list[warp][q + 1].a, s_list[warp][q + 1].t[rr], kAabb, w2);
+#if FDGS_WI_VOTE
+        if (__builtin_expect(__any_sync(0xffffffffu, fminf(T.x, T.y) < kStopU), 0)) {  // warp-uniform branch
+#else
         if (__builtin_expect(fminf(T.x, T.y) < kStopU, 0)) {
+#endif
             const float4 a1 = s_list[warp][q].a, r1 = s_list[warp][q].t[rr];
             const float4 a2 = s_list[warp][q + 1].a, r2 = s_list[warp][q + 1].t[rr];
             auto undo = [&](float &cr, float &cg, float &cb, float &t, float &th, float t0, float t1, float x1,
