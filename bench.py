@@ -59,6 +59,8 @@ def apply_config(args):
     import fdgs_inputs as fi
     CONFIG = args.config
     cfg = fi.CONFIGS[CONFIG]
+    if args.streams is None:
+        args.streams = 8 if CONFIG == "c2" else 6
     N_CAMS = {"hemisphere50": 50, "arc20": 20, "c1": 1}[cfg["rig"]]
     N_FRAMES_T = cfg["frames"]
     INTERVAL = cfg["keyframe_interval"]
@@ -79,7 +81,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-stage-events", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
-    p.add_argument("--streams", type=int, default=6, help="frame-pipelining depth (workspaces/streams)")
+    p.add_argument("--streams", type=int, default=None,
+                   help="frame-pipelining depth (workspaces/streams); default 8 at c2 (800x800: shorter frames "
+                        "want more in flight, measured), else 6")
     p.add_argument("--no-split", action="store_true", help="blend on the front-end stream (no priority split)")
     p.add_argument("--no-graphs", action="store_true",
                    help="launch the front end's kernels one by one instead of one CUDA-graph launch per frame")
