@@ -87,6 +87,10 @@ def main():
         pipes[v] = fd.RenderPipeline(sc, cams[0].width, cams[0].height, depth=depth,
                                      graphs=kind in ("graphs", "gnative"), native=kind in ("native", "gnative"),
                                      threads=int(thr or 3))
+        if kind == "pyswap":  # experiment: blend streams high priority, front-end streams low
+            pp = pipes[v]
+            pp.front = [torch.cuda.Stream(priority=0) for _ in range(depth)]
+            pp.blend = [torch.cuda.Stream(priority=-1) for _ in range(depth)]
     outs = [pipes[a.variants[0]].renderers[0].new_output() for _ in range(a.frames)]
     res = {v: [] for v in a.variants}
     host = {v: [] for v in a.variants}
