@@ -348,7 +348,6 @@ fdgs_status fdgs_render_graph_create(const fdgs_scene *scene, int32_t width, int
     if (s != FDGS_OK) return s;
     if (width < 1 || height < 1 || width > 8192 || height > 8192) return fail(FDGS_ERR_INVALID_ARG, "image size");
     if (max_entries < 0 || max_entries > 0xffffffffll) return fail(FDGS_ERR_INVALID_ARG, "max_entries out of range");
-    if (scene->n < 1) return fail(FDGS_ERR_INVALID_ARG, "capture needs a non-empty scene");
     const RenderLayout L = render_layout(layout_n(*scene), width, height, max_entries);
     if (L.n_tiles > FDGS_MAX_TILES) return fail(FDGS_ERR_UNSUPPORTED, "tile grid %d > %d", L.n_tiles, FDGS_MAX_TILES);
     if (d_ws == nullptr || ws_bytes < L.total || (uintptr_t)d_ws % 256 != 0)

@@ -1869,7 +1869,9 @@ cudaError_t render_graph_build(RenderGraphImpl &g, const SceneDev &sc, const Cam
             else if (p.func == (void *)k_cull_emit) g.n_emit = nodes[k], g.p_emit = p;
             else if (p.func == (void *)k_slice) g.n_slice = nodes[k], g.p_slice = p;
         }
-        if (e == cudaSuccess && (!g.n_cull || !g.n_emit || !g.n_slice || !g.n_ev[0] || !g.n_ev[1] || !g.n_ev[2]))
+        // an empty layout (n = 0) captures no cull / slice nodes (launch_render skips them)
+        const bool cull_nodes = g.n_cull && g.n_emit && g.n_slice;
+        if (e == cudaSuccess && ((L.n > 0 && !cull_nodes) || !g.n_ev[0] || !g.n_ev[1] || !g.n_ev[2]))
             e = cudaErrorInvalidValue;
     }
     // front-end nodes at the device's greatest priority, whatever the launching stream's
@@ -1904,7 +1906,7 @@ cudaError_t render_graph_launch(RenderGraphImpl &g, const SceneDev &sc, const ui
     cudaKernelNodeParams p = g.p_cull;
     p.kernelParams = a_cull;
     p.extra = nullptr;
-    cudaError_t e = cudaGraphExecKernelNodeSetParams(g.exec, g.n_cull, &p);
+    cudaError_t e = g.n_cull ? cudaGraphExecKernelNodeSetParams(g.exec, g.n_cull, &p) : cudaSuccess;
     // k_cull_emit(bits, base, n, surv)
     const uint32_t *cbits_c = cbits, *ccnt_c = ccnt;
     int n = sc.n;
@@ -1912,7 +1914,7 @@ cudaError_t render_graph_launch(RenderGraphImpl &g, const SceneDev &sc, const ui
     p = g.p_emit;
     p.kernelParams = a_emit;
     p.extra = nullptr;
-    if (e == cudaSuccess) e = cudaGraphExecKernelNodeSetParams(g.exec, g.n_emit, &p);
+    if (e == cudaSuccess && g.n_emit) e = cudaGraphExecKernelNodeSetParams(g.exec, g.n_emit, &p);
     // k_slice(sc, cam, t, ctr, surv, rec0, rec1, rec2, depth, rect, vbits, vcnt)
     const uint32_t *surv_c = surv;
     void *a_slice[] = {(void *)&sc,   (void *)&cam,  (void *)&t,     (void *)&ctr,   (void *)&surv_c, (void *)&rec0,
@@ -1920,7 +1922,7 @@ cudaError_t render_graph_launch(RenderGraphImpl &g, const SceneDev &sc, const ui
     p = g.p_slice;
     p.kernelParams = a_slice;
     p.extra = nullptr;
-    if (e == cudaSuccess) e = cudaGraphExecKernelNodeSetParams(g.exec, g.n_slice, &p);
+    if (e == cudaSuccess && g.n_slice) e = cudaGraphExecKernelNodeSetParams(g.exec, g.n_slice, &p);
     for (int k = 0; k < 3 && e == cudaSuccess; ++k) {  // the stage events of this frame (or the placeholders)
         cudaEvent_t want = ev ? ev[k] : g.ph[k];
         if (want != g.cur_ev[k] && (e = cudaGraphExecEventRecordNodeSetEvent(g.exec, g.n_ev[k], want)) == cudaSuccess)

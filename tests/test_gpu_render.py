@@ -206,6 +206,16 @@ def test_empty_scene_and_all_zero_mask_give_background():
     img, T, stats, _ = _render(scene, cam, 0.5, zero)
     assert stats.n_act == 0 and stats.n_vis == 0
     assert np.all(img == np.array(cam.bg, np.float32)[:, None, None])
+    # the pipeline's front-end graphs (an empty layout captures no cull / slice
+    # nodes) and the native batch, both submission paths
+    sc = fd.Scene.from_arrays(empty)
+    for native in (False, True):
+        pipe = fd.RenderPipeline(sc, cam.width, cam.height, depth=2, native=native)
+        outs = [pipe.renderers[0].new_output() for _ in range(3)]
+        pipe.render_many([(cam, 0.5, None, None)] * 3, outs)
+        torch.cuda.synchronize()
+        for o in outs:
+            assert np.all(o.cpu().numpy() == np.array(cam.bg, np.float32)[:, None, None])
 
 
 @pytest.mark.parametrize("W,H", [(1, 1), (17, 33), (16, 16), (250, 7)])
