@@ -132,3 +132,8 @@ def test_bench_orchestration_two_ranks():
     # value = all frames / the slowest rank's total time
     tmax = max(fk["per_rank_total_ms"])
     assert abs(d["value"] - 2 * 39 / (tmax / 1e3)) <= 1e-4 * d["value"]  # (totals rounded to 0.1 us)
+    # per-step statistics over the max-over-ranks step times, outliers listed
+    st = d["step_stats"]
+    assert st["min_ms"] <= st["median_ms"] <= st["max_ms"] and isinstance(st["outliers"], list)
+    assert all(o["ms"] > 1.5 * st["median_ms"] for o in st["outliers"])
+    assert d["config"]["submission"].startswith("per frame: one CUDA-graph launch")
