@@ -793,7 +793,7 @@ template <bool kWrite>
 __device__ __forceinline__ void row_walk(uint32_t w0, uint32_t w1, int lane, const uint32_t *__restrict__ sorted,
                                          const uint32_t *__restrict__ item_pack,
                                          const uint32_t *__restrict__ item_v, uint32_t *cnt, const uint32_t *base,
-                                         uint32_t *__restrict__ entries) {
+                                         uint32_t *__restrict__ entries, uint8_t *s_own) {
     for (uint32_t r0 = w0; r0 < w1; r0 += 32) {
         const uint32_t r = r0 + lane;
         int c = 0, txa = 0;
@@ -814,13 +814,16 @@ __device__ __forceinline__ void row_walk(uint32_t w0, uint32_t w1, int lane, con
         const int total = __shfl_sync(0xffffffffu, incl, 31);
         for (int e0 = 0; e0 < total; e0 += 32) {
             const int e = e0 + lane;
-            int j = 0;  // owning item: smallest j with incl_j > e
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const int cand = __shfl_sync(0xffffffffu, incl, j + step - 1);
-                if (cand <= e) j += step;
-            }
-            j = min(j, 31);
+            // owning item of entry e: every item with entries in [e0, e0 + 32)
+            // marks the window slot where its run starts; the owner of slot
+            // e - e0 is the run starting at the highest mark <= it
+            const int ex = incl - c;
+            const bool owns = c > 0 && ex < e0 + 32 && incl > e0;
+            const int slot = max(ex, e0) - e0;
+            const uint32_t marks = __reduce_or_sync(0xffffffffu, owns ? 1u << slot : 0u);
+            if (owns) s_own[slot] = (uint8_t)lane;
+            __syncwarp();
+            const int j = s_own[31 - __clz(marks & ((2u << lane) - 1u))];
             const int exj = __shfl_sync(0xffffffffu, incl - c, j);
             const int jx = __shfl_sync(0xffffffffu, txa, j);
             const uint32_t vj = __shfl_sync(0xffffffffu, v, j);
@@ -959,7 +962,8 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_row_scatter(const uint32_t *
         }
     }
     __syncthreads();
-    row_walk<true>(w0, w1, lane, sorted, item_pack, item_v, my, s_base, entries);
+    __shared__ uint8_t s_own[kRowWarps][32];  // run-start owner per window slot (row_walk)
+    row_walk<true>(w0, w1, lane, sorted, item_pack, item_v, my, s_base, entries, s_own[warp]);
 }
 
 // ---------------------------------------------------------------- row 6
