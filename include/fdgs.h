@@ -9,9 +9,11 @@
  * Conventions for every entry point
  *   - All pointers named d_* / documented "device" are CUDA device pointers;
  *     "host" pointers are ordinary host memory.  The caller owns every buffer.
- *     The library never allocates or frees memory; scratch lives in a
+ *     The library never allocates or frees device memory; scratch lives in a
  *     caller-provided workspace whose size the *_workspace_bytes functions
- *     return (256-byte aligned base required).
+ *     return (256-byte aligned base required).  The two handle types
+ *     (fdgs_render_graph, fdgs_pipeline) own host objects, CUDA graphs and
+ *     events, released by their destroy calls.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *     All work is stream-ordered; functions documented "async" never
  *     synchronise the host.
@@ -36,7 +38,7 @@
 extern "C" {
 #endif
 
-#define FDGS_ABI_VERSION 1
+#define FDGS_ABI_VERSION 2  /* 2: fdgs_scene.d_n, fdgs_pipeline_slot.graph, the pipeline and timed-graph entries */
 #define FDGS_TILE 16            /* 16x16-pixel tiles (reading R7) */
 #define FDGS_MAX_TILES 16384    /* tile-grid limit of the binning kernel    */
 

@@ -81,6 +81,8 @@ class FdgsError(RuntimeError):
 
 _lock = threading.Lock()
 _lib = None
+ABI_VERSION = 2            # include/fdgs.h FDGS_ABI_VERSION this binding's structs follow
+CHECK_ABI = True           # tools/ loading older A/B variant libraries turn this off
 
 
 def lib():
@@ -136,6 +138,9 @@ def lib():
                 continue
             f.argtypes = args
             f.restype = res
+        if CHECK_ABI and L.fdgs_abi_version() != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH} has ABI version {L.fdgs_abi_version()}, the binding needs {ABI_VERSION}: "
+                              "rebuild it (python -m paper_2503_16422_b200.build)")
         _lib = L
         return L
 

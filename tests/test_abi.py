@@ -45,7 +45,8 @@ def test_library_is_sm100a(lib):
 
 
 def test_status_strings_and_version(lib):
-    assert lib.fdgs_abi_version() == 1
+    from paper_2503_16422_b200 import _lib as _lib_mod
+    assert lib.fdgs_abi_version() == 2 == _lib_mod.ABI_VERSION
     assert lib.fdgs_status_string(0) == b"ok"
     assert lib.fdgs_status_string(4) == b"tile-entry capacity exceeded"
 

@@ -33,8 +33,9 @@ def use_lib(name):
         _lib._lib = None
         if name:
             _lib.LIB_PATH = f"tools/variants/libfdgs_{name}.so"
+            _lib.CHECK_ABI = name != "r01"  # the round-1 library predates ABI version 2
         _LIBS[name] = _lib.lib()
-        _lib.LIB_PATH, _lib._lib = saved_path, saved
+        _lib.LIB_PATH, _lib._lib, _lib.CHECK_ABI = saved_path, saved, True
     _lib._lib = _LIBS[name]
 
 
