@@ -486,6 +486,18 @@ def test_cuda_graph_frames_equal_launched_frames():
     for ref, o in zip(refs, outs):
         assert torch.equal(ref, o)
     assert stamp == [ev[0].elapsed_time(ev[4]) for ev in evs]  # not re-recorded
+    # the native batch over the slots' graphs, with stage events
+    nat = fd.RenderPipeline(sc, 240, 180, depth=3, native=True, graphs=True)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in frames]
+    for row in evs:
+        for e in row:
+            e.record()
+    outs = [nat.renderers[0].new_output() for _ in frames]
+    nat.render_many(frames, outs, stage_events=evs)
+    torch.cuda.synchronize()
+    for ref, o, ev in zip(refs, outs, evs):
+        assert torch.equal(ref, o)
+        assert all(ev[k].elapsed_time(ev[k + 1]) >= 0.0 for k in range(4))
 
 
 def test_aabb_redundant_flag_sound():
