@@ -309,9 +309,6 @@ constexpr int kSortThreads = 256;
 #define FDGS_LB_WIN 8
 #endif
 constexpr int kLbWin = FDGS_LB_WIN;  // predecessors read per look-back round trip
-#ifndef FDGS_LB_SLEEP
-#define FDGS_LB_SLEEP 0
-#endif
 constexpr uint64_t kStA = 1ull << 30, kStP = 2ull << 30;
 
 __device__ __forceinline__ uint64_t ld_volatile64(const uint64_t *p) { return *(const volatile uint64_t *)p; }
@@ -442,11 +439,6 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint32_t *__res
                     }
                 }
                 q -= k;  // resume at the first unpublished predecessor
-#if FDGS_LB_SLEEP > 0
-                // no progress: back off instead of re-polling at full issue rate (the
-                // spinning warps would take issue slots from co-resident blend warps)
-                if (!found && k == 0) __nanosleep(FDGS_LB_SLEEP);
-#endif
             }
             st_volatile64(st, epoch | kStP | (excl + tot));
         }
@@ -1404,21 +1396,12 @@ cudaError_t launch_debug_strip_reach(char *ws, const RenderLayout &L, uint8_t *o
 #ifndef FDGS_WI_MINB
 #define FDGS_WI_MINB 8
 #endif
-#ifndef FDGS_WI_PAIR
-#define FDGS_WI_PAIR 1
-#endif
-#ifndef FDGS_WI_VOTE
-#define FDGS_WI_VOTE 1  // the paired stop test as a warp vote (a uniform branch: no reconvergence barrier per pair)
-#endif
 #ifndef FDGS_WI_PAIR_UNROLL
 #define FDGS_WI_PAIR_UNROLL 4
 #endif
 constexpr int kWiPairUnroll = FDGS_WI_PAIR_UNROLL;
 
 constexpr int kWiThreads = 128;
-#ifndef FDGS_WI_PREFETCH
-#define FDGS_WI_PREFETCH 1  // gather the next batch's records while this one is composited
-#endif
 __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uint32_t *__restrict__ tile_start,
                                                          const uint32_t *__restrict__ entries,
                                                          const float4 *__restrict__ rec0,
@@ -1482,7 +1465,7 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
             }
         }
     };
-    // Two records, one stop test (FDGS_WI_PAIR): U after both is checked; a
+    // Two records, one stop test: U after both is checked; a
     // pixel that fell below the threshold is rolled back to the record that
     // crossed it (U restored to before that record, the colour steps of the
     // crossing record and of any later one subtracted, colours reloaded from
@@ -1512,11 +1495,8 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
         blend1(s_list[warp][q].a, s_list[warp][q].t[rr], kAabb, w1);
         const float2 T1 = T;
         blend1(s_list[warp][q + 1].a, s_list[warp][q + 1].t[rr], kAabb, w2);
-#if FDGS_WI_VOTE
-        if (__builtin_expect(__any_sync(0xffffffffu, fminf(T.x, T.y) < kStopU), 0)) {  // warp-uniform branch
-#else
-        if (__builtin_expect(fminf(T.x, T.y) < kStopU, 0)) {
-#endif
+        // a warp vote: the branch is uniform (no reconvergence barrier per pair)
+        if (__builtin_expect(__any_sync(0xffffffffu, fminf(T.x, T.y) < kStopU), 0)) {
             const float4 a1 = s_list[warp][q].a, r1 = s_list[warp][q].t[rr];
             const float4 a2 = s_list[warp][q + 1].a, r2 = s_list[warp][q + 1].t[rr];
             auto undo = [&](float &cr, float &cg, float &cb, float &t, float &th, float t0, float t1, float x1,
@@ -1552,13 +1532,8 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
     };
     bool wdone = __all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf);
     float4 r0, r1, r2;
-#if FDGS_WI_PREFETCH
     if (start < end) fetch(start, r0, r1, r2);
-#endif
     for (uint32_t base = start; base < end && !wdone; base += 32) {
-#if !FDGS_WI_PREFETCH
-        fetch(base, r0, r1, r2);
-#endif
         const int n = (int)min(32u, end - base);
         // ---- stage this warp's list of the batch
         const bool redundant = (__float_as_uint(r1.w) & 0x80000000u) != 0u;
@@ -1577,24 +1552,17 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
             for (int r = 0; r < kWlRows; ++r) E.t[r] = make_float4(r2.z, __uint_as_float(mb), t1s[r], t4s[r]);
         }
         // ---- gather the next batch while this one is composited
-#if FDGS_WI_PREFETCH
         if (base + 32 < end) fetch(base + 32, r0, r1, r2);
-#endif
         __syncwarp();
         const int cnt = __popc(bal);
         if (masked) {
 #pragma unroll kWlUnroll
             for (int q = 0; q < cnt; ++q) step(q, std::true_type{});
         } else {
-#if FDGS_WI_PAIR
             int q = 0;
 #pragma unroll kWiPairUnroll
             for (; q + 1 < cnt; q += 2) step2(q, std::false_type{});
             if (q < cnt) step(q, std::false_type{});
-#else
-#pragma unroll kWlUnroll
-            for (int q = 0; q < cnt; ++q) step(q, std::false_type{});
-#endif
         }
         wdone = __all_sync(0xffffffffu, thr.x == kInf && thr.y == kInf);
     }
@@ -1635,15 +1603,9 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
 #define FDGS_ITEM_GRID 2
 #endif
 static_assert(FDGS_PGRID >= 1 && FDGS_PGRID_DIV >= 1 && FDGS_BIN_GRID >= 1 && FDGS_ITEM_GRID >= 1, "grid shapes");
-#ifndef FDGS_ZERO_KERNEL
-#define FDGS_ZERO_KERNEL 1
-#endif
 __global__ void __launch_bounds__(256) k_zero(uint4 *__restrict__ p, size_t n16) {
     for (size_t i = threadIdx.x; i < n16; i += 256) p[i] = make_uint4(0u, 0u, 0u, 0u);
 }
-#ifndef FDGS_ROW_BITS_ADAPT
-#define FDGS_ROW_BITS_ADAPT 1
-#endif
 static int sort_grid(int p_sort) { return std::max(1, FDGS_PGRID * p_sort / FDGS_PGRID_DIV); }
 
 static void launch_timed_blend(const uint32_t *tstart, const uint32_t *entries, const float4 *rec0,
@@ -1678,14 +1640,9 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     };
     if (ev && (e = rec(0)) != cudaSuccess) return e;
     {
-#if FDGS_ZERO_KERNEL
         // counters, digit bases, histograms: a kernel, not a memset (a memset
         // node in a captured graph adds a copy-engine hop to every frame)
         k_zero<<<1, 256, 0, st>>>(reinterpret_cast<uint4 *>(ws + L.counters), (L.zero_end - L.counters) / 16);
-#else
-        e = cudaMemsetAsync(ws + L.counters, 0, L.zero_end - L.counters, st);  // counters, look-back, histograms
-        if (e != cudaSuccess) return e;
-#endif
         if (sc.n > 0) {
             uint32_t *cbits = reinterpret_cast<uint32_t *>(ws + L.surv_bits);
             uint32_t *ccnt = reinterpret_cast<uint32_t *>(ws + L.cull_cnt);
@@ -1750,12 +1707,9 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
                 ikey[0], nullptr, L.tiles_y > 256 ? ikey[1] : nullptr, ival[0], &ctr->n_items_part, epoch,
                 &ctr->tile_ticket[0], 0, rbase, tstat, nullptr, nullptr);
         };
-#if FDGS_ROW_BITS_ADAPT
         if (L.tiles_y <= 64) row_pass0(std::integral_constant<int, 6>{});
         else if (L.tiles_y <= 128) row_pass0(std::integral_constant<int, 7>{});
-        else
-#endif
-        row_pass0(std::integral_constant<int, 8>{});
+        else row_pass0(std::integral_constant<int, 8>{});
         if (L.tiles_y > 256) {
             k_onesweep<8, kTileSortItems><<<rgrid, kSortThreads, 0, st>>>(ikey[1], ival[0], nullptr, ival[1], &ctr->n_items_part, epoch,
                                                            &ctr->tile_ticket[1], 8, rbase + 256,
