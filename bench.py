@@ -73,10 +73,11 @@ def apply_config(args):
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=100)  # 100 x 60 = the whole 6000-frame C3 sequence
+    p.add_argument("--steps", type=int, default=50)  # 50 x 120 = the whole 6000-frame C3 sequence
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--frames-per-step", type=int, default=60)
+    p.add_argument("--frames-per-step", type=int, default=120,
+                   help="frames per step (the pipeline drains at every step end; 60 measured 1.3%% lower)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-stage-events", action="store_true")
