@@ -1604,7 +1604,8 @@ __global__ void __launch_bounds__(kWiThreads, FDGS_WI_MINB) k_blend_wi(const uin
 #endif
 static_assert(FDGS_PGRID >= 1 && FDGS_PGRID_DIV >= 1 && FDGS_BIN_GRID >= 1 && FDGS_ITEM_GRID >= 1, "grid shapes");
 __global__ void __launch_bounds__(256) k_zero(uint4 *__restrict__ p, size_t n16) {
-    for (size_t i = threadIdx.x; i < n16; i += 256) p[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (size_t i = (size_t)blockIdx.x * 256 + threadIdx.x; i < n16; i += (size_t)gridDim.x * 256)
+        p[i] = make_uint4(0u, 0u, 0u, 0u);
 }
 static int sort_grid(int p_sort) { return std::max(1, FDGS_PGRID * p_sort / FDGS_PGRID_DIV); }
 
@@ -1642,7 +1643,11 @@ cudaError_t launch_render(const SceneDev &sc, const uint32_t *mask_l, const uint
     {
         // counters, digit bases, histograms: a kernel, not a memset (a memset
         // node in a captured graph adds a copy-engine hop to every frame)
-        k_zero<<<1, 256, 0, st>>>(reinterpret_cast<uint4 *>(ws + L.counters), (L.zero_end - L.counters) / 16);
+        {
+            const size_t n16 = (L.zero_end - L.counters) / 16;  // ~30 KB at C3; one block per 64 KB
+            k_zero<<<(int)std::min<size_t>(std::max<size_t>(1, n16 / 4096), 148), 256, 0, st>>>(
+                reinterpret_cast<uint4 *>(ws + L.counters), n16);
+        }
         if (sc.n > 0) {
             uint32_t *cbits = reinterpret_cast<uint32_t *>(ws + L.surv_bits);
             uint32_t *ccnt = reinterpret_cast<uint32_t *>(ws + L.cull_cnt);
