@@ -434,6 +434,11 @@ def test_pipeline_overflow_detected_and_re_rendered():
     assert (st[:, 3] == 0).all() and (st[:, 2] > 4096).any()
     for ref, o in zip(refs, outs):
         assert torch.equal(ref, o)
+    # the grown workspaces serve the graph path afterwards (graphs re-captured on them)
+    pipe.render_many(frames, outs := [pipe.renderers[0].new_output() for _ in frames])
+    torch.cuda.synchronize()
+    for ref, o in zip(refs, outs):
+        assert torch.equal(ref, o)
 
 
 def test_cuda_graph_frames_equal_launched_frames():
